@@ -1,0 +1,143 @@
+/*
+ * capt_b200 -- B200-native CAPT batched sphere-vs-point-cloud collision query.
+ *
+ * C-ABI boundary of libcapt_b200.so.  Plain pointers and sizes only; every
+ * entry point is stream-ordered on the caller's cudaStream_t (passed as
+ * void*, NULL = legacy default stream) unless CAPT_HOST_IO is set, in which
+ * case the call copies host buffers in/out and returns after the results are
+ * on the host.
+ *
+ * The reference (arXiv 2406.02807 companion package `captree`, pure
+ * Python/numpy) has no FFI; its boundary is the Python API.  Each entry point
+ * below names the reference function it replaces (file:line relative to
+ * /root/reference/pkg/src/captree).  INTEGRATION.md shows the ctypes binding
+ * the reference would add; paper_2406_02807_b200/ is that binding.
+ *
+ * Status codes (capt_last_error() returns the thread-local message):
+ *   CAPT_OK       0
+ *   CAPT_EINVAL   1  invalid argument            -> ValueError
+ *   CAPT_ERANGE   2  radius outside [r_min,r_max] -> ValueError (query.py:30-34)
+ *   CAPT_ECUDA    3  CUDA runtime/launch failure  -> RuntimeError
+ *   CAPT_ENOMEM   4  device allocation failed     -> MemoryError
+ */
+#ifndef CAPT_B200_H
+#define CAPT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CAPT_OK 0
+#define CAPT_EINVAL 1
+#define CAPT_ERANGE 2
+#define CAPT_ECUDA 3
+#define CAPT_ENOMEM 4
+
+/* capt_query / capt_leaf_indices flags */
+#define CAPT_PREFILTER 0x1u   /* use_aabb_prefilter (query.py:184-186)          */
+#define CAPT_CHECK_RADII 0x2u /* check_radii: report first out-of-band radius  */
+#define CAPT_STATS 0x4u       /* fill counters[0..3] (see capt_query)           */
+#define CAPT_INPUT_F64 0x8u   /* centers/radii are double (else float)          */
+#define CAPT_HOST_IO 0x10u    /* all array arguments are host memory; blocking  */
+#define CAPT_MODE_DIRECT 0x100u /* force the one-thread-per-sphere kernel      */
+#define CAPT_MODE_BINNED 0x200u /* force the leaf-binned kernels               */
+
+typedef struct capt_tree capt_tree;
+
+typedef struct {
+  int32_t k;              /* dimension (1..3)                                 */
+  int32_t depth;          /* log2(n_leaves) descent steps (tree.py:93)        */
+  int64_t n_leaves;       /* power of two (tree.py:150)                       */
+  int64_t n_points;       /* points in the source cloud                       */
+  int64_t total_stored;   /* sum of affordance-set sizes (BuildStats)         */
+  int64_t max_affordance; /* largest set                                      */
+  double r_min, r_max;    /* exactness band (BuildParams, tree.py:41-52)      */
+  int64_t device_bytes;   /* size of the device slab                          */
+  int32_t device;         /* CUDA ordinal holding the slab                    */
+  int32_t reserved;
+  int64_t n_ties;         /* split nodes with equal rank-(m/2-1)/(m/2) coords */
+} capt_tree_info;
+
+/* Thread-local message for the last non-OK status. */
+const char* capt_last_error(void);
+int capt_version(void);
+
+/* Capt.__init__ (tree.py:74-97) / load_capt (tree.py:291-320): upload a tree
+ * given in the reference layout (host arrays): tests (n-1) fp32 Eytzinger,
+ * aff_lo/aff_hi (n*k) fp32, offsets (n+1) int64 CSR, aff_values
+ * (offsets[n]*k) fp32, SoA within each set, representative first. */
+int capt_tree_create(int device, int k, int64_t n_leaves, int64_t n_points,
+                     double r_min, double r_max, const float* tests,
+                     const float* aff_lo, const float* aff_hi,
+                     const int64_t* offsets, const float* aff_values,
+                     capt_tree** out);
+
+/* construct(cloud, BuildParams(r_min, r_max), use_rmin_shortcut)
+ * (tree.py:139-241), on device.  points: (n_points, k) fp32, device memory
+ * unless flags has CAPT_HOST_IO.  Ties at a split go left by original index. */
+int capt_tree_build(int device, int k, const float* points, int64_t n_points,
+                    double r_min, double r_max, int use_rmin_shortcut,
+                    uint32_t flags, void* stream, capt_tree** out);
+
+int capt_tree_info_get(const capt_tree* tree, capt_tree_info* info);
+
+/* Copy the tree back in the reference layout (host buffers sized from
+ * capt_tree_info).  Rows 1.. of each set are in ascending original-index
+ * order for device-built trees, in upload order for uploaded trees. */
+int capt_tree_export(const capt_tree* tree, float* tests, float* aff_lo,
+                     float* aff_hi, int64_t* offsets, float* aff_values);
+
+void capt_tree_destroy(capt_tree* tree);
+
+/* Position-independent device slab (for replication across GPUs: NCCL
+ * broadcast the slab bytes, then capt_tree_from_slab on each rank). */
+int capt_tree_slab(const capt_tree* tree, const void** dev_ptr, int64_t* bytes);
+int capt_tree_from_slab(int device, const void* dev_slab, int64_t bytes,
+                        void* stream, capt_tree** out);
+
+/* collides_many (query.py:184-219) when lane_width == 1; otherwise
+ * collides_batch(tree, SphereBatch(...)).any_collision (query.py:126-167)
+ * for every consecutive group of lane_width (power of two <= 32) spheres.
+ *   centers: (n, k) float (or double with CAPT_INPUT_F64); radii: (n,)
+ *   lane_mask: optional (n,) bytes, 0 = masked lane (SphereBatch.mask)
+ *   out_bits: ceil((n/lane_width)/32) words; verdict g is bit g%32 of word g/32
+ *   counters (optional, 6 x uint64, written with CAPT_STATS):
+ *     [0] collisions (spheres, or groups when lane_width > 1)
+ *     [1] boundary spheres: some scanned point has |d^2 - r^2| < 1e-6 (fp64)
+ *     [2] points scanned, reference semantics (query.py:153-155): full set
+ *         sizes of AABB-passing spheres; for groups, lanes in order up to and
+ *         including the first colliding lane
+ *     [3] spheres resolved by the float64 fix-up path
+ *     [4] valid spheres rejected by the AABB prefilter (aabb_rejections)
+ *     [5] reserved (0)
+ *   first_bad (optional): index of the first out-of-band radius among valid
+ *     lanes, -1 if none (CAPT_CHECK_RADII).  With CAPT_HOST_IO a bad radius
+ *     makes the call return CAPT_ERANGE. */
+int capt_query(const capt_tree* tree, const void* centers, const void* radii,
+               int64_t n, int lane_width, const uint8_t* lane_mask,
+               uint32_t flags, uint32_t* out_bits, uint64_t* counters,
+               int64_t* first_bad, void* stream);
+
+/* leaf_indices (tree.py:266-273): out (n,) int64 leaf of every center. */
+int capt_leaf_indices(const capt_tree* tree, const void* centers, int64_t n,
+                      uint32_t flags, int64_t* out, void* stream);
+
+/* filter_cloud (morton.py:185-236), optional reach_filter pre-pass
+ * (morton.py:173-182).  points (n, k) fp32; out_points must hold n rows;
+ * *n_out receives the output count.  Host memory with CAPT_HOST_IO, else
+ * device memory (then *n_out is written by the call before it returns). */
+int capt_filter_cloud(int device, int k, const float* points, int64_t n,
+                      double r_filter, int has_reach, const double* base,
+                      double max_reach, uint32_t flags, float* out_points,
+                      int64_t* n_out, void* stream);
+
+/* Measurement helper for the roofline denominator: FFMA throughput of this
+ * device in TFLOP/s (CUDA-event timed dependent-chain FMA kernel). */
+int capt_measure_fp32_peak(int device, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CAPT_B200_H */

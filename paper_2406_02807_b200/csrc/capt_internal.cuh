@@ -1,0 +1,148 @@
+// Internal definitions shared by the libcapt_b200 translation units.
+//
+// Device tree layout (one position-independent slab per tree; DESIGN.md
+// "Data layout in HBM"):
+//   SlabHeader                      (copy of the host header, 256 B)
+//   T      float[n-1]               Eytzinger split values (tree.py:156)
+//   box    float4[2n]               leaf AABB of the affordance set: lo.xyz,_ / hi.xyz,_
+//   set    uint2[n]                 (start in float4 units, true set size m)
+//   offs   int64[n+1]               reference CSR offsets (tree.py:226-228)
+//   data   float4[...]              per set: xs[m4] ys[m4] zs[m4], m4 = roundup(m,4),
+//                                   padding rows +inf; unused dims (k<3) are 0
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/capt_b200.h"
+
+namespace capt {
+
+constexpr uint64_t kSlabMagic = 0x3030324254504143ull;  // "CAPTB200"
+constexpr int kSlabVersion = 1;
+constexpr int kMaxK = 3;
+
+struct SlabHeader {
+  uint64_t magic;
+  int32_t version;
+  int32_t k;
+  int32_t depth;
+  int32_t pad0;
+  int64_t n;          // leaves
+  int64_t n_points;   // source cloud size
+  int64_t total;      // sum of set sizes
+  int64_t max_aff;
+  int64_t n_ties;
+  double r_min, r_max;
+  int64_t off_T, off_box, off_set, off_offs, off_data;  // byte offsets in slab
+  int64_t data_f4;    // float4 count of the data section
+  int64_t bytes;      // slab size
+  int64_t reserved[10];
+};
+static_assert(sizeof(SlabHeader) <= 256, "header must fit its 256-B section");
+
+struct DevTree {
+  int k, depth;
+  int64_t n;
+  double r_min, r_max;
+  const float* T;
+  const float4* box;
+  const uint2* set;
+  const int64_t* offs;
+  const float4* data;
+};
+
+}  // namespace capt
+
+struct capt_tree {
+  capt::SlabHeader h;
+  int device;
+  char* slab;  // device pointer
+};
+
+namespace capt {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define CAPT_CUDA(call)                                  \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return capt::cuda_fail(_e, #call); \
+  } while (0)
+
+inline DevTree view(const capt_tree* t) {
+  DevTree d;
+  d.k = t->h.k;
+  d.depth = t->h.depth;
+  d.n = t->h.n;
+  d.r_min = t->h.r_min;
+  d.r_max = t->h.r_max;
+  d.T = reinterpret_cast<const float*>(t->slab + t->h.off_T);
+  d.box = reinterpret_cast<const float4*>(t->slab + t->h.off_box);
+  d.set = reinterpret_cast<const uint2*>(t->slab + t->h.off_set);
+  d.offs = reinterpret_cast<const int64_t*>(t->slab + t->h.off_offs);
+  d.data = reinterpret_cast<const float4*>(t->slab + t->h.off_data);
+  return d;
+}
+
+inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
+
+// Fill the header's section offsets for a tree of n leaves and data_f4
+// float4s of set data; returns the slab size.
+inline int64_t layout_slab(SlabHeader& h, int64_t data_f4) {
+  int64_t off = 256;
+  h.off_T = off;
+  off = align256(off + sizeof(float) * (h.n > 1 ? h.n - 1 : 1));
+  h.off_box = off;
+  off = align256(off + sizeof(float4) * 2 * h.n);
+  h.off_set = off;
+  off = align256(off + sizeof(uint2) * h.n);
+  h.off_offs = off;
+  off = align256(off + sizeof(int64_t) * (h.n + 1));
+  h.off_data = off;
+  off = align256(off + sizeof(float4) * (data_f4 > 0 ? data_f4 : 1));
+  h.data_f4 = data_f4;
+  h.bytes = off;
+  return off;
+}
+
+inline int depth_of(int64_t n) {
+  int d = 0;
+  while ((int64_t(1) << d) < n) ++d;
+  return d;
+}
+
+// Kernels shared between tree creation paths (capt_tree.cu).
+// Given per-leaf sizes m (device, uint2.y filled), fill start4 (uint2.x) by an
+// exclusive scan of 3*roundup(m,4)/4 and return the total float4 count.
+int assign_set_starts(uint2* set, int64_t n, int64_t* data_f4, int64_t* total,
+                      int64_t* max_aff, int64_t* d_offs, cudaStream_t s);
+
+int alloc_slab(capt_tree** out, int device, SlabHeader h);
+
+// scratch allocation helpers (stream-ordered allocator)
+template <class T>
+inline cudaError_t dmalloc(T** p, size_t count, cudaStream_t s) {
+  return cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(T) * (count ? count : 1), s);
+}
+
+inline int grid_for(int64_t work, int block, int max_blocks_per_sm = 8) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  int64_t need = (work + block - 1) / block;
+  int64_t cap = int64_t(sms) * max_blocks_per_sm;
+  if (need < 1) need = 1;
+  return int(need < cap ? need : cap);
+}
+
+}  // namespace capt

@@ -1,0 +1,366 @@
+// Batched sphere-vs-point-cloud collision query (the hot path).
+//
+// Replaces collides_many (query.py:184-219) and collides_batch(...).
+// any_collision (query.py:126-167).  Two kernel families:
+//   * direct  (this file): one thread per sphere -- branchless Eytzinger
+//     descent with the top 12 levels in shared memory (tree.py:266-273),
+//     fp32 leaf-AABB reject (query.py:202-208), float4 SoA scan of the
+//     affordance set (query.py:96-99), warp-ballot bit packing, and for
+//     lane_width > 1 a per-group __ballot_sync vote after every 4-point chunk
+//     (edge-validation early exit, query.py:152-160).
+//   * binned  (capt_binned.cu): for large batches, spheres are bucketed by
+//     leaf and every leaf's set is staged once in shared memory.
+//
+// Exactness.  The reference evaluates in float64 on fp32 data.  The descent
+// compares fp32 values, so an fp32 compare is identical.  Squared distances
+// are computed in fp32 with a proven relative error < 5u (u = 2^-24); any
+// comparison within a relative band TAU = 2^-19 of r^2 is re-evaluated with
+// the reference's exact float64 expression ((dx^2 + dy^2) + dz^2, no FMA,
+// __dadd_rn/__dmul_rn), so verdicts are bit-identical to the reference.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <type_traits>
+
+#include "capt_internal.cuh"
+#include "capt_query_common.cuh"
+
+namespace capt {
+
+constexpr int kBlock = 256;
+
+template <typename InT>
+struct SphereIn;
+
+template <>
+struct SphereIn<float> {
+  __device__ static void load(const void* c, const void* r, int64_t q, int k, double c64[3],
+                              double& r64) {
+    const float* cf = static_cast<const float*>(c);
+    c64[0] = c64[1] = c64[2] = 0.0;
+    for (int d = 0; d < k; ++d) c64[d] = double(__ldg(cf + q * k + d));
+    r64 = double(__ldg(static_cast<const float*>(r) + q));
+  }
+};
+template <>
+struct SphereIn<double> {
+  __device__ static void load(const void* c, const void* r, int64_t q, int k, double c64[3],
+                              double& r64) {
+    const double* cd = static_cast<const double*>(c);
+    c64[0] = c64[1] = c64[2] = 0.0;
+    for (int d = 0; d < k; ++d) c64[d] = __ldg(cd + q * k + d);
+    r64 = __ldg(static_cast<const double*>(r) + q);
+  }
+};
+
+// Sphere status in the direct kernel
+enum : int { ST_FALSE = 0, ST_TRUE = 1, ST_SCAN = 2, ST_SLOW = 3, ST_SKIP = 4 };
+
+template <typename InT, bool kStats>
+__global__ void __launch_bounds__(kBlock)
+    k_query_direct(DevTree t, const void* __restrict__ centers, const void* __restrict__ radii,
+                   int64_t n, int L, const uint8_t* __restrict__ lane_mask, uint32_t flags,
+                   uint32_t* __restrict__ out_bits, int64_t n_words,
+                   unsigned long long* __restrict__ counters,
+                   unsigned long long* __restrict__ first_bad) {
+  __shared__ float sT[kSmemNodes];
+  __shared__ uint32_t sWords[kBlock / 32];
+  const int n_smem = int(t.n - 1 < kSmemNodes ? t.n - 1 : kSmemNodes);
+  for (int i = threadIdx.x; i < n_smem; i += blockDim.x) sT[i] = t.T[i];
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const bool prefilter = flags & CAPT_PREFILTER;
+  const bool check = flags & CAPT_CHECK_RADII;
+  const uint32_t seg = (L >= 32) ? 0xffffffffu : ((1u << L) - 1u);
+  const uint32_t my_seg = seg << ((lane / L) * L);
+  const int64_t n_tiles = (n + kBlock - 1) / kBlock;
+
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t q = tile * kBlock + threadIdx.x;
+    bool valid = q < n;
+    if (valid && lane_mask) valid = lane_mask[q] != 0;
+    double c64[3] = {0.0, 0.0, 0.0}, r64 = 0.0;
+    if (valid) SphereIn<InT>::load(centers, radii, q, t.k, c64, r64);
+    if (valid && check && (r64 < t.r_min || r64 > t.r_max))
+      atomicMin(first_bad, static_cast<unsigned long long>(q));
+
+    int status = ST_FALSE;
+    int64_t leaf = 0;
+    uint2 set = make_uint2(0, 0);
+    float cx = 0.f, cy = 0.f, cz = 0.f, r2 = 0.f, loB = 0.f, hiB = 0.f;
+    bool passed = false;  // AABB passed (scanned)
+    bool leaf_ok = false; // reached the AABB test (finite centre)
+    if (valid) {
+      if constexpr (std::is_same<InT, float>::value) {
+        const float cf[3] = {float(c64[0]), float(c64[1]), float(c64[2])};
+        leaf = descend_t<float>(t, sT, n_smem, cf);
+      } else {
+        leaf = descend(t, sT, n_smem, c64);
+      }
+      status = classify(t, leaf, c64, r64, prefilter, cx, cy, cz, r2, loB, hiB);
+      passed = status == ST_SCAN || status == ST_SLOW;
+      leaf_ok = passed || prefilter;
+      if (passed) set = __ldg(t.set + leaf);
+    }
+
+    // ---- scan: warp-uniform loop over 4-point chunks ----
+    bool hit = false, amb = false, bnd_cand = false;
+    uint32_t pos = 0;
+    const float* base = reinterpret_cast<const float*>(t.data + set.x);
+    const uint32_t m4 = (set.y + 3u) & ~3u;
+    while (__any_sync(0xffffffffu, status == ST_SCAN)) {
+      if (status == ST_SCAN) {
+        const float4 px = __ldg(reinterpret_cast<const float4*>(base + pos));
+        const float4 py = __ldg(reinterpret_cast<const float4*>(base + m4 + pos));
+        const float4 pz = __ldg(reinterpret_cast<const float4*>(base + 2 * m4 + pos));
+        test4(px, py, pz, cx, cy, cz, r2, loB, hiB, hit, amb, bnd_cand, kStats);
+        pos += 4;
+        if (hit && !kStats) status = ST_TRUE;
+        else if (pos >= m4) status = hit ? ST_TRUE : (amb ? ST_SLOW : ST_FALSE);
+      }
+      if (!kStats && L > 1) {
+        const uint32_t done = __ballot_sync(0xffffffffu, status == ST_TRUE);
+        if ((done & my_seg) && status == ST_SCAN) status = ST_SKIP;
+      }
+    }
+    // ---- float64 fix-up (exact reference arithmetic) ----
+    if (!kStats && L > 1) {
+      const uint32_t done = __ballot_sync(0xffffffffu, status == ST_TRUE);
+      if ((done & my_seg) && status == ST_SLOW) status = ST_SKIP;
+    }
+    bool slow = false, boundary = false;
+    if (status == ST_SLOW || (kStats && bnd_cand)) {
+      slow = status == ST_SLOW;
+      bool b = false;
+      const bool h64 = scan_f64(t, set, c64, r64, kStats ? &b : nullptr);
+      status = h64 ? ST_TRUE : ST_FALSE;
+      boundary = b;
+    }
+    const bool verdict = status == ST_TRUE;
+
+    // ---- bit packing ----
+    const uint32_t bits = __ballot_sync(0xffffffffu, verdict);
+    uint32_t gbits = bits;
+    if (L > 1) {
+      gbits = 0;
+      for (int j = 0; j < 32 / L; ++j)
+        if ((bits >> (j * L)) & seg) gbits |= 1u << j;
+    }
+    if (L <= 8) {
+      if (threadIdx.x < kBlock / 32) sWords[threadIdx.x] = 0;
+      __syncthreads();
+      if (lane == 0) {
+        const int per = 32 / L;                   // group bits per warp
+        const int bitpos = warp * per;            // within the tile
+        atomicOr(&sWords[bitpos >> 5], gbits << (bitpos & 31));
+      }
+      __syncthreads();
+      const int words_per_tile = (kBlock / L) / 32;
+      if (threadIdx.x < words_per_tile) {
+        const int64_t w = tile * words_per_tile + threadIdx.x;
+        if (w < n_words) out_bits[w] = sWords[threadIdx.x];
+      }
+    } else if (lane == 0 && gbits) {
+      const int64_t g0 = (tile * kBlock + warp * 32) / L;
+      atomicOr(out_bits + (g0 >> 5), gbits << (g0 & 31));
+    }
+
+    // ---- counters (reference semantics) ----
+    if (kStats) {
+      unsigned long long c_hit, c_bnd = boundary, c_scan = 0, c_fix = slow;
+      unsigned long long c_rej = (valid && !passed && leaf_ok) ? 1ull : 0ull;
+      if (L == 1) {
+        c_hit = verdict;
+        c_scan = passed ? set.y : 0;
+      } else {
+        // lanes in order up to and including the first colliding lane
+        const uint32_t segbits = bits & my_seg;
+        const int first = segbits ? __ffs(segbits) - 1 : 32;
+        c_scan = (passed && lane <= first) ? set.y : 0;
+        c_hit = ((lane % L) == 0) && (segbits != 0);
+      }
+      c_hit = warp_sum(c_hit);
+      c_bnd = warp_sum(c_bnd);
+      c_scan = warp_sum(c_scan);
+      c_fix = warp_sum(c_fix);
+      c_rej = warp_sum(c_rej);
+      if (lane == 0) {
+        atomicAdd(counters + 4, c_rej);
+        atomicAdd(counters + 0, c_hit);
+        atomicAdd(counters + 1, c_bnd);
+        atomicAdd(counters + 2, c_scan);
+        atomicAdd(counters + 3, c_fix);
+      }
+    }
+  }
+}
+
+template <typename InT>
+__global__ void k_leaf_indices(DevTree t, const void* __restrict__ centers, int64_t n,
+                               int64_t* __restrict__ out) {
+  __shared__ float sT[kSmemNodes];
+  const int n_smem = int(t.n - 1 < kSmemNodes ? t.n - 1 : kSmemNodes);
+  for (int i = threadIdx.x; i < n_smem; i += blockDim.x) sT[i] = t.T[i];
+  __syncthreads();
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+       q += int64_t(gridDim.x) * blockDim.x) {
+    double c64[3], r64;
+    SphereIn<InT>::load(centers, centers, q, t.k, c64, r64);
+    out[q] = descend(t, sT, n_smem, c64);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+
+struct HostIO {
+  // device mirrors of host arguments (CAPT_HOST_IO)
+  void* centers = nullptr;
+  void* radii = nullptr;
+  uint8_t* mask = nullptr;
+  uint32_t* bits = nullptr;
+  unsigned long long* counters = nullptr;
+  unsigned long long* first_bad = nullptr;
+  cudaStream_t s = nullptr;
+  ~HostIO() {
+    if (centers) cudaFreeAsync(centers, s);
+    if (radii) cudaFreeAsync(radii, s);
+    if (mask) cudaFreeAsync(mask, s);
+    if (bits) cudaFreeAsync(bits, s);
+    if (counters) cudaFreeAsync(counters, s);
+    if (first_bad) cudaFreeAsync(first_bad, s);
+  }
+};
+
+int launch_direct(const DevTree& t, const void* centers, const void* radii, int64_t n, int L,
+                  const uint8_t* mask, uint32_t flags, uint32_t* bits, int64_t n_words,
+                  unsigned long long* counters, unsigned long long* first_bad, cudaStream_t s) {
+  const int64_t n_tiles = (n + kBlock - 1) / kBlock;
+  const int grid = grid_for(n_tiles * kBlock, kBlock, 8);
+  const bool f64 = flags & CAPT_INPUT_F64;
+  const bool stats = flags & CAPT_STATS;
+#define LAUNCH(T, S) \
+  k_query_direct<T, S><<<grid, kBlock, 0, s>>>(t, centers, radii, n, L, mask, flags, bits, n_words, counters, first_bad)
+  if (f64) {
+    if (stats) LAUNCH(double, true); else LAUNCH(double, false);
+  } else {
+    if (stats) LAUNCH(float, true); else LAUNCH(float, false);
+  }
+#undef LAUNCH
+  CAPT_CUDA(cudaGetLastError());
+  return CAPT_OK;
+}
+
+}  // namespace capt
+
+using namespace capt;
+
+extern "C" int capt_query(const capt_tree* tree, const void* centers, const void* radii,
+                          int64_t n, int L, const uint8_t* lane_mask, uint32_t flags,
+                          uint32_t* out_bits, uint64_t* counters, int64_t* first_bad,
+                          void* stream) {
+  if (!tree) return fail(CAPT_EINVAL, "NULL tree");
+  if (n < 0) return fail(CAPT_EINVAL, "negative sphere count");
+  if (L < 1 || L > 32 || (L & (L - 1))) return fail(CAPT_EINVAL, "lane width must be a power of two <= 32");
+  if (n % L) return fail(CAPT_EINVAL, "sphere count must be a multiple of the lane width");
+  if (n > 0 && (!centers || !radii || !out_bits)) return fail(CAPT_EINVAL, "NULL array argument");
+  if ((flags & CAPT_STATS) && !counters) return fail(CAPT_EINVAL, "CAPT_STATS needs counters");
+  CAPT_CUDA(cudaSetDevice(tree->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const DevTree t = view(tree);
+  const int64_t n_groups = n / L;
+  const int64_t n_words = (n_groups + 31) / 32;
+  const bool host = flags & CAPT_HOST_IO;
+  const size_t in_elem = (flags & CAPT_INPUT_F64) ? sizeof(double) : sizeof(float);
+
+  HostIO io;
+  io.s = s;
+  const void* d_c = centers;
+  const void* d_r = radii;
+  const uint8_t* d_m = lane_mask;
+  uint32_t* d_bits = out_bits;
+  unsigned long long* d_cnt = reinterpret_cast<unsigned long long*>(counters);
+  unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(first_bad);
+  if (host) {
+    CAPT_CUDA(cudaMallocAsync(&io.centers, in_elem * t.k * (n ? n : 1), s));
+    CAPT_CUDA(cudaMallocAsync(&io.radii, in_elem * (n ? n : 1), s));
+    CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&io.bits), 4 * (n_words ? n_words : 1), s));
+    CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&io.counters), 8 * 6, s));
+    CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&io.first_bad), 8, s));
+    if (n) {
+      CAPT_CUDA(cudaMemcpyAsync(io.centers, centers, in_elem * t.k * n, cudaMemcpyHostToDevice, s));
+      CAPT_CUDA(cudaMemcpyAsync(io.radii, radii, in_elem * n, cudaMemcpyHostToDevice, s));
+    }
+    if (lane_mask) {
+      CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&io.mask), n ? n : 1, s));
+      if (n) CAPT_CUDA(cudaMemcpyAsync(io.mask, lane_mask, n, cudaMemcpyHostToDevice, s));
+    }
+    d_c = io.centers;
+    d_r = io.radii;
+    d_m = io.mask;
+    d_bits = io.bits;
+    d_cnt = io.counters;
+    d_bad = io.first_bad;
+  }
+  unsigned long long* bad = d_bad;
+  if (bad) CAPT_CUDA(cudaMemsetAsync(bad, 0xff, 8, s));
+  if (d_cnt && (flags & CAPT_STATS)) CAPT_CUDA(cudaMemsetAsync(d_cnt, 0, 48, s));
+  if (L > 8 || n == 0) CAPT_CUDA(cudaMemsetAsync(d_bits, 0, 4 * (n_words ? n_words : 1), s));
+  if (n > 0) {
+    uint32_t fl = flags;
+    if (!bad) fl &= ~CAPT_CHECK_RADII;
+    int rc = launch_direct(t, d_c, d_r, n, L, d_m, fl, d_bits, n_words, d_cnt, bad, s);
+    if (rc) return rc;
+  }
+  if (host) {
+    if (n_words) CAPT_CUDA(cudaMemcpyAsync(out_bits, d_bits, 4 * n_words, cudaMemcpyDeviceToHost, s));
+    int64_t fb = -1;
+    CAPT_CUDA(cudaMemcpyAsync(&fb, d_bad, 8, cudaMemcpyDeviceToHost, s));
+    uint64_t cnt[6] = {0, 0, 0, 0, 0, 0};
+    if (flags & CAPT_STATS) CAPT_CUDA(cudaMemcpyAsync(cnt, d_cnt, 48, cudaMemcpyDeviceToHost, s));
+    CAPT_CUDA(cudaStreamSynchronize(s));
+    if (first_bad) *first_bad = fb;
+    if (counters && (flags & CAPT_STATS)) memcpy(counters, cnt, sizeof(cnt));
+    if ((flags & CAPT_CHECK_RADII) && fb >= 0) {
+      set_error("radius outside the tree's exactness band");
+      return CAPT_ERANGE;
+    }
+  }
+  return CAPT_OK;
+}
+
+extern "C" int capt_leaf_indices(const capt_tree* tree, const void* centers, int64_t n,
+                                 uint32_t flags, int64_t* out, void* stream) {
+  if (!tree) return fail(CAPT_EINVAL, "NULL tree");
+  if (n < 0) return fail(CAPT_EINVAL, "negative count");
+  if (n == 0) return CAPT_OK;
+  if (!centers || !out) return fail(CAPT_EINVAL, "NULL array argument");
+  CAPT_CUDA(cudaSetDevice(tree->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const DevTree t = view(tree);
+  const bool host = flags & CAPT_HOST_IO;
+  const size_t in_elem = (flags & CAPT_INPUT_F64) ? sizeof(double) : sizeof(float);
+  void* d_c = const_cast<void*>(centers);
+  int64_t* d_out = out;
+  if (host) {
+    CAPT_CUDA(cudaMallocAsync(&d_c, in_elem * t.k * n, s));
+    CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_out), 8 * n, s));
+    CAPT_CUDA(cudaMemcpyAsync(d_c, centers, in_elem * t.k * n, cudaMemcpyHostToDevice, s));
+  }
+  const int grid = grid_for(n, 256, 8);
+  if (flags & CAPT_INPUT_F64)
+    k_leaf_indices<double><<<grid, 256, 0, s>>>(t, d_c, n, d_out);
+  else
+    k_leaf_indices<float><<<grid, 256, 0, s>>>(t, d_c, n, d_out);
+  CAPT_CUDA(cudaGetLastError());
+  if (host) {
+    CAPT_CUDA(cudaMemcpyAsync(out, d_out, 8 * n, cudaMemcpyDeviceToHost, s));
+    CAPT_CUDA(cudaFreeAsync(d_c, s));
+    CAPT_CUDA(cudaFreeAsync(d_out, s));
+    CAPT_CUDA(cudaStreamSynchronize(s));
+  }
+  return CAPT_OK;
+}

@@ -1,0 +1,152 @@
+// Device helpers shared by the direct and binned query kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "capt_internal.cuh"
+
+namespace capt {
+
+// Top 12 levels of the Eytzinger split array live in shared memory (16 KB).
+constexpr int kSmemNodes = 4095;
+
+// Relative decision band: the fp32 distance has relative error < 5u
+// (u = 2^-24: one rounded difference per axis, one product, two rounded
+// fused adds), r^2 one more u; TAU = 2^-19 = 32u leaves a wide margin.
+constexpr float kTau = 0x1p-19f;
+constexpr float kR2Min = 0x1p-100f;  // outside [kR2Min, kR2Max] -> float64 path
+constexpr float kR2Max = 0x1p100f;
+
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// np.maximum: NaN-propagating
+__device__ __forceinline__ double np_max(double a, double b) {
+  if (a != a) return a;
+  if (b != b) return b;
+  return a >= b ? a : b;
+}
+
+// leaf_indices (tree.py:266-273): i = 2i + 1 + (x[step % k] > T[i]).
+// The reference compares fp32 values upcast to float64 -> identical to an
+// fp32 compare for fp32 inputs; float64 inputs compare in float64.
+template <typename C>
+__device__ __forceinline__ int64_t descend_t(const DevTree& t, const float* sT, int n_smem,
+                                             const C c[3]) {
+  int64_t i = 0;
+  int ax = 0;
+  for (int s = 0; s < t.depth; ++s) {
+    const float tv = (i < n_smem) ? sT[i] : __ldg(t.T + i);
+    i = 2 * i + 1 + (c[ax] > C(tv) ? 1 : 0);
+    ax = (ax + 1 == t.k) ? 0 : ax + 1;
+  }
+  return i - (t.n - 1);
+}
+
+__device__ __forceinline__ int64_t descend(const DevTree& t, const float* sT, int n_smem,
+                                           const double c64[3]) {
+  return descend_t<double>(t, sT, n_smem, c64);
+}
+
+// Exact reference AABB prefilter (query.py:202-208): fp64 copies of the fp32
+// box, res = max(max(lo - c, 0), c - hi), ((r0^2 + r1^2) + r2^2) <= r^2.
+__device__ __forceinline__ bool aabb_keep64(int k, const float4 lo, const float4 hi,
+                                            const double c[3], double R) {
+  const double l[3] = {lo.x, lo.y, lo.z};
+  const double h[3] = {hi.x, hi.y, hi.z};
+  double s = 0.0;
+  for (int d = 0; d < k; ++d) {
+    double r = np_max(__dsub_rn(l[d], c[d]), 0.0);
+    r = np_max(r, __dsub_rn(c[d], h[d]));
+    const double sq = __dmul_rn(r, r);
+    s = (d == 0) ? sq : __dadd_rn(s, sq);
+  }
+  return s <= R;
+}
+
+// Exact reference scan of one affordance set (query.py:96-99, 214-218).
+__device__ __noinline__ bool scan_f64(const DevTree& t, uint2 set, const double c[3],
+                                      double r64, bool* boundary) {
+  const float* base = reinterpret_cast<const float*>(t.data + set.x);
+  const uint32_t m4 = (set.y + 3u) & ~3u;
+  const double R = __dmul_rn(r64, r64);
+  bool hit = false;
+  for (uint32_t i = 0; i < set.y; ++i) {
+    double s = 0.0;
+    for (int d = 0; d < t.k; ++d) {
+      const double x = __dsub_rn(c[d], double(__ldg(base + d * m4 + i)));
+      const double sq = __dmul_rn(x, x);
+      s = (d == 0) ? sq : __dadd_rn(s, sq);
+    }
+    if (s <= R) {
+      hit = true;
+      if (!boundary) break;
+    }
+    if (boundary && fabs(s - R) < 1e-6) *boundary = true;
+  }
+  return hit;
+}
+
+// Shared per-sphere setup.  Returns ST_FALSE (0) when the verdict is false
+// (non-finite centre, AABB reject), ST_SCAN (2) for the fp32 scan, ST_SLOW (3)
+// for the exact float64 scan (radius outside the safe fp32 range, or a
+// float64 input that is not exactly representable in fp32).
+__device__ __forceinline__ int classify(const DevTree& t, int64_t leaf, const double c64[3],
+                                        double r64, bool prefilter, float& cx, float& cy,
+                                        float& cz, float& r2, float& loB, float& hiB) {
+  bool cfin = true;
+  for (int d = 0; d < t.k; ++d) cfin &= isfinite(c64[d]);
+  // +-inf / NaN centres give inf or NaN distances: never a collision unless
+  // r^2 itself overflows to inf (then the exact path decides)
+  if (!cfin && __dmul_rn(r64, r64) <= 1.7976931348623157e308) return 0;
+  const float cf0 = float(c64[0]), cf1 = float(c64[1]), cf2 = float(c64[2]);
+  const float rf = float(r64);
+  const bool exact = double(cf0) == c64[0] && double(cf1) == c64[1] && double(cf2) == c64[2] &&
+                     double(rf) == r64;
+  r2 = rf * rf;
+  const bool fast = cfin && exact && r2 >= kR2Min && r2 <= kR2Max;
+  cx = cf0;
+  cy = cf1;
+  cz = cf2;
+  loB = r2 * (1.0f - kTau);
+  hiB = r2 * (1.0f + kTau);
+  if (prefilter) {
+    const float4 lo = __ldg(t.box + 2 * leaf);
+    const float4 hi = __ldg(t.box + 2 * leaf + 1);
+    bool exact_check = !fast;
+    if (fast) {
+      const float rx = fmaxf(fmaxf(lo.x - cx, 0.f), cx - hi.x);
+      const float ry = fmaxf(fmaxf(lo.y - cy, 0.f), cy - hi.y);
+      const float rz = fmaxf(fmaxf(lo.z - cz, 0.f), cz - hi.z);
+      const float s = fmaf(rz, rz, fmaf(ry, ry, rx * rx));
+      if (s > hiB) return 0;
+      if (s >= loB) exact_check = true;
+    }
+    if (exact_check && !aabb_keep64(t.k, lo, hi, c64, __dmul_rn(r64, r64))) return 0;
+  }
+  return fast ? 2 : 3;
+}
+
+// fp32 test of 4 points (SoA float4 of x, y, z).
+__device__ __forceinline__ void test4(const float4 px, const float4 py, const float4 pz,
+                                      float cx, float cy, float cz, float r2, float loB,
+                                      float hiB, bool& hit, bool& amb, bool& bnd, bool stats) {
+  const float xs[4] = {px.x, px.y, px.z, px.w};
+  const float ys[4] = {py.x, py.y, py.z, py.w};
+  const float zs[4] = {pz.x, pz.y, pz.z, pz.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float dx = cx - xs[i], dy = cy - ys[i], dz = cz - zs[i];
+    const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+    hit |= d2 <= loB;
+    amb |= d2 < hiB;
+    if (stats)
+      bnd |= isfinite(d2) && fabsf(d2 - r2) <= 1.001e-6f + 0x1p-17f * fmaxf(d2, r2);
+  }
+}
+
+}  // namespace capt

@@ -1,0 +1,298 @@
+// Tree handles: error plumbing, upload from the reference layout
+// (Capt.__init__ tree.py:74-97), export back to it, slab replication.
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "capt_internal.cuh"
+
+namespace capt {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  char buf[512];
+  snprintf(buf, sizeof(buf), "CUDA error %d (%s) in %s", int(e), cudaGetErrorString(e), what);
+  g_last_error = buf;
+  cudaGetLastError();  // clear sticky-free errors
+  return e == cudaErrorMemoryAllocation ? CAPT_ENOMEM : CAPT_ECUDA;
+}
+
+int alloc_slab(capt_tree** out, int device, SlabHeader h) {
+  capt_tree* t = new capt_tree();
+  t->h = h;
+  t->device = device;
+  t->slab = nullptr;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&t->slab), size_t(h.bytes));
+  if (e != cudaSuccess) {
+    delete t;
+    return cuda_fail(e, "cudaMalloc(tree slab)");
+  }
+  *out = t;
+  return CAPT_OK;
+}
+
+// --------------------------------------------------------------------------
+// upload: reference layout -> padded device layout
+// --------------------------------------------------------------------------
+
+// One warp per leaf: copy the SoA coordinates of set j from the reference's
+// compact layout (values[off*k + d*m + i]) to the padded per-set layout,
+// +inf padding rows, zeros for unused dims.
+__global__ void k_pack_sets(int k, int64_t n, const int64_t* __restrict__ offs,
+                            const float* __restrict__ vals, const uint2* __restrict__ set,
+                            float4* __restrict__ data) {
+  int lane = threadIdx.x & 31;
+  int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t j = warp; j < n; j += nwarps) {
+    int64_t a = offs[j];
+    int64_t m = offs[j + 1] - a;
+    int64_t m4 = (m + 3) & ~int64_t(3);
+    float* dst = reinterpret_cast<float*>(data + set[j].x);
+    for (int d = 0; d < kMaxK; ++d) {
+      for (int64_t i = lane; i < m4; i += 32) {
+        float v;
+        if (d >= k) v = 0.f;
+        else if (i < m) v = vals[a * k + d * m + i];
+        else v = __int_as_float(0x7f800000);
+        dst[d * m4 + i] = v;
+      }
+    }
+  }
+}
+
+__global__ void k_pack_boxes(int k, int64_t n, const float* __restrict__ lo,
+                             const float* __restrict__ hi, float4* __restrict__ box) {
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+       j += int64_t(gridDim.x) * blockDim.x) {
+    float l[3] = {0.f, 0.f, 0.f}, h[3] = {0.f, 0.f, 0.f};
+    for (int d = 0; d < k; ++d) {
+      l[d] = lo[j * k + d];
+      h[d] = hi[j * k + d];
+    }
+    box[2 * j] = make_float4(l[0], l[1], l[2], 0.f);
+    box[2 * j + 1] = make_float4(h[0], h[1], h[2], 0.f);
+  }
+}
+
+// Inverse of k_pack_sets (export).
+__global__ void k_unpack_sets(int k, int64_t n, const int64_t* __restrict__ offs,
+                              const uint2* __restrict__ set, const float4* __restrict__ data,
+                              float* __restrict__ vals) {
+  int lane = threadIdx.x & 31;
+  int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t j = warp; j < n; j += nwarps) {
+    int64_t a = offs[j];
+    int64_t m = offs[j + 1] - a;
+    int64_t m4 = (m + 3) & ~int64_t(3);
+    const float* src = reinterpret_cast<const float*>(data + set[j].x);
+    for (int d = 0; d < k; ++d)
+      for (int64_t i = lane; i < m; i += 32) vals[a * k + d * m + i] = src[d * m4 + i];
+  }
+}
+
+__global__ void k_unpack_boxes(int k, int64_t n, const float4* __restrict__ box,
+                               float* __restrict__ lo, float* __restrict__ hi) {
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+       j += int64_t(gridDim.x) * blockDim.x) {
+    float4 l = box[2 * j], h = box[2 * j + 1];
+    float lv[3] = {l.x, l.y, l.z}, hv[3] = {h.x, h.y, h.z};
+    for (int d = 0; d < k; ++d) {
+      lo[j * k + d] = lv[d];
+      hi[j * k + d] = hv[d];
+    }
+  }
+}
+
+}  // namespace capt
+
+using namespace capt;
+
+extern "C" {
+
+const char* capt_last_error(void) { return g_last_error.c_str(); }
+
+int capt_version(void) { return 1; }
+
+int capt_tree_create(int device, int k, int64_t n, int64_t n_points, double r_min,
+                     double r_max, const float* tests, const float* aff_lo,
+                     const float* aff_hi, const int64_t* offsets, const float* aff_values,
+                     capt_tree** out) {
+  if (!out) return fail(CAPT_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (k < 1 || k > kMaxK) return fail(CAPT_EINVAL, "k must be 1..3 on the device path");
+  if (n < 1 || (n & (n - 1))) return fail(CAPT_EINVAL, "leaf count is not a power of two");
+  if (!aff_lo || !aff_hi || !offsets || (n > 1 && !tests))
+    return fail(CAPT_EINVAL, "missing tree array");
+  if (offsets[0] != 0) return fail(CAPT_EINVAL, "offsets[0] must be 0");
+  CAPT_CUDA(cudaSetDevice(device));
+  SlabHeader h;
+  memset(&h, 0, sizeof(h));
+  h.magic = kSlabMagic;
+  h.version = kSlabVersion;
+  h.k = k;
+  h.n = n;
+  h.depth = depth_of(n);
+  h.n_points = n_points;
+  h.r_min = r_min;
+  h.r_max = r_max;
+  std::vector<uint2> set(static_cast<size_t>(n));
+  int64_t f4 = 0, maxm = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    int64_t m = offsets[j + 1] - offsets[j];
+    if (m < 1) return fail(CAPT_EINVAL, "every affordance set holds at least its representative");
+    if (m > 0xffffffffll) return fail(CAPT_EINVAL, "affordance set too large");
+    int64_t m4 = (m + 3) & ~int64_t(3);
+    set[j] = make_uint2(unsigned(f4), unsigned(m));
+    f4 += 3 * m4 / 4;
+    if (f4 > 0xffffffffll) return fail(CAPT_EINVAL, "tree too large for 32-bit float4 offsets");
+    if (m > maxm) maxm = m;
+  }
+  h.total = offsets[n];
+  h.max_aff = maxm;
+  layout_slab(h, f4);
+  int rc = alloc_slab(out, device, h);
+  if (rc) return rc;
+  capt_tree* t = *out;
+  cudaStream_t s = 0;
+  float* d_vals = nullptr;
+  float* d_lo = nullptr;
+  float* d_hi = nullptr;
+  cudaError_t e = cudaSuccess;
+#define UPCHK(x)                                  \
+  do {                                            \
+    e = (x);                                      \
+    if (e != cudaSuccess) {                       \
+      cudaFree(d_vals); cudaFree(d_lo); cudaFree(d_hi); \
+      capt_tree_destroy(t); *out = nullptr;       \
+      return cuda_fail(e, #x);                    \
+    }                                             \
+  } while (0)
+  UPCHK(cudaMemcpy(t->slab, &h, sizeof(h), cudaMemcpyHostToDevice));
+  if (n > 1)
+    UPCHK(cudaMemcpy(t->slab + h.off_T, tests, sizeof(float) * (n - 1), cudaMemcpyHostToDevice));
+  UPCHK(cudaMemcpy(t->slab + h.off_set, set.data(), sizeof(uint2) * n, cudaMemcpyHostToDevice));
+  UPCHK(cudaMemcpy(t->slab + h.off_offs, offsets, sizeof(int64_t) * (n + 1),
+                   cudaMemcpyHostToDevice));
+  UPCHK(cudaMalloc(&d_vals, sizeof(float) * (h.total * k + 1)));
+  UPCHK(cudaMalloc(&d_lo, sizeof(float) * n * k));
+  UPCHK(cudaMalloc(&d_hi, sizeof(float) * n * k));
+  UPCHK(cudaMemcpy(d_vals, aff_values, sizeof(float) * h.total * k, cudaMemcpyHostToDevice));
+  UPCHK(cudaMemcpy(d_lo, aff_lo, sizeof(float) * n * k, cudaMemcpyHostToDevice));
+  UPCHK(cudaMemcpy(d_hi, aff_hi, sizeof(float) * n * k, cudaMemcpyHostToDevice));
+  DevTree v = view(t);
+  k_pack_sets<<<grid_for(n * 32, 256), 256, 0, s>>>(k, n, v.offs, d_vals, v.set,
+                                                    const_cast<float4*>(v.data));
+  k_pack_boxes<<<grid_for(n, 256), 256, 0, s>>>(k, n, d_lo, d_hi, const_cast<float4*>(v.box));
+  UPCHK(cudaGetLastError());
+  UPCHK(cudaDeviceSynchronize());
+  cudaFree(d_vals);
+  cudaFree(d_lo);
+  cudaFree(d_hi);
+#undef UPCHK
+  return CAPT_OK;
+}
+
+int capt_tree_info_get(const capt_tree* t, capt_tree_info* info) {
+  if (!t || !info) return fail(CAPT_EINVAL, "NULL argument");
+  memset(info, 0, sizeof(*info));
+  info->k = t->h.k;
+  info->depth = t->h.depth;
+  info->n_leaves = t->h.n;
+  info->n_points = t->h.n_points;
+  info->total_stored = t->h.total;
+  info->max_affordance = t->h.max_aff;
+  info->r_min = t->h.r_min;
+  info->r_max = t->h.r_max;
+  info->device_bytes = t->h.bytes;
+  info->device = t->device;
+  info->n_ties = t->h.n_ties;
+  return CAPT_OK;
+}
+
+int capt_tree_export(const capt_tree* t, float* tests, float* aff_lo, float* aff_hi,
+                     int64_t* offsets, float* aff_values) {
+  if (!t) return fail(CAPT_EINVAL, "NULL tree");
+  CAPT_CUDA(cudaSetDevice(t->device));
+  const SlabHeader& h = t->h;
+  DevTree v = view(t);
+  int k = h.k;
+  int64_t n = h.n;
+  if (tests && n > 1)
+    CAPT_CUDA(cudaMemcpy(tests, v.T, sizeof(float) * (n - 1), cudaMemcpyDeviceToHost));
+  if (offsets) CAPT_CUDA(cudaMemcpy(offsets, v.offs, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
+  if (aff_lo || aff_hi) {
+    float *d_lo = nullptr, *d_hi = nullptr;
+    CAPT_CUDA(cudaMalloc(&d_lo, sizeof(float) * n * k));
+    CAPT_CUDA(cudaMalloc(&d_hi, sizeof(float) * n * k));
+    k_unpack_boxes<<<grid_for(n, 256), 256>>>(k, n, v.box, d_lo, d_hi);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess && aff_lo) e = cudaMemcpy(aff_lo, d_lo, sizeof(float) * n * k, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && aff_hi) e = cudaMemcpy(aff_hi, d_hi, sizeof(float) * n * k, cudaMemcpyDeviceToHost);
+    cudaFree(d_lo);
+    cudaFree(d_hi);
+    if (e != cudaSuccess) return cuda_fail(e, "export boxes");
+  }
+  if (aff_values && h.total > 0) {
+    float* d_vals = nullptr;
+    CAPT_CUDA(cudaMalloc(&d_vals, sizeof(float) * h.total * k));
+    k_unpack_sets<<<grid_for(n * 32, 256), 256>>>(k, n, v.offs, v.set, v.data, d_vals);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess)
+      e = cudaMemcpy(aff_values, d_vals, sizeof(float) * h.total * k, cudaMemcpyDeviceToHost);
+    cudaFree(d_vals);
+    if (e != cudaSuccess) return cuda_fail(e, "export values");
+  }
+  return CAPT_OK;
+}
+
+void capt_tree_destroy(capt_tree* t) {
+  if (!t) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(t->device);
+  cudaFree(t->slab);
+  cudaSetDevice(cur);
+  delete t;
+}
+
+int capt_tree_slab(const capt_tree* t, const void** dev_ptr, int64_t* bytes) {
+  if (!t || !dev_ptr || !bytes) return fail(CAPT_EINVAL, "NULL argument");
+  *dev_ptr = t->slab;
+  *bytes = t->h.bytes;
+  return CAPT_OK;
+}
+
+int capt_tree_from_slab(int device, const void* dev_slab, int64_t bytes, void* stream,
+                        capt_tree** out) {
+  if (!out || !dev_slab) return fail(CAPT_EINVAL, "NULL argument");
+  *out = nullptr;
+  CAPT_CUDA(cudaSetDevice(device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SlabHeader h;
+  CAPT_CUDA(cudaMemcpyAsync(&h, dev_slab, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CAPT_CUDA(cudaStreamSynchronize(s));
+  if (h.magic != kSlabMagic || h.version != kSlabVersion || h.bytes != bytes)
+    return fail(CAPT_EINVAL, "not a capt_b200 tree slab");
+  int rc = alloc_slab(out, device, h);
+  if (rc) return rc;
+  cudaError_t e = cudaMemcpyAsync((*out)->slab, dev_slab, size_t(bytes), cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    capt_tree_destroy(*out);
+    *out = nullptr;
+    return cuda_fail(e, "copy slab");
+  }
+  return CAPT_OK;
+}
+
+}  // extern "C"
