@@ -1,11 +1,6 @@
 // Temporary: device construct / filter land in capt_build.cu / capt_filter.cu.
 #include "capt_internal.cuh"
 using namespace capt;
-extern "C" int capt_tree_build(int, int, const float*, int64_t, double, double, int, uint32_t,
-                               void*, capt_tree** out) {
-  if (out) *out = nullptr;
-  return fail(CAPT_EINVAL, "capt_tree_build not built yet");
-}
 extern "C" int capt_filter_cloud(int, int, const float*, int64_t, double, int, const double*,
                                  double, uint32_t, float*, int64_t*, void*) {
   return fail(CAPT_EINVAL, "capt_filter_cloud not built yet");

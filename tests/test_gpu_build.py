@@ -1,0 +1,107 @@
+"""Device construct (capt_tree_build) vs the reference's trees (golden
+fixtures) and the oracle: T, offsets and boxes bit-exact, affordance sets
+bit-exact in canonical per-leaf order."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_tree, load_golden
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2406_02807_b200")
+
+
+def assert_same_tree(dev, ref, canon=True):
+    assert dev.n == ref["n"] and dev.k == ref["k"]
+    assert np.array_equal(dev.tests, ref["tests"])
+    assert np.array_equal(dev.offsets, ref["offsets"])
+    assert np.array_equal(dev.aff_lo, ref["aff_lo"])
+    assert np.array_equal(dev.aff_hi, ref["aff_hi"])
+    if canon:
+        assert np.array_equal(O.canonical_values(dev), O.canonical_values(ref))
+
+
+def test_build_matches_reference_golden_trees():
+    z = load_golden("trees.npz")
+    for name in z["names"]:
+        ref = golden_tree(z, f"{name}/")
+        pts = z[f"{name}/points"]
+        sc = bool(z[f"{name}/shortcut"][0])
+        tree = P.construct(P.PointCloud(pts), P.BuildParams(ref["r_min"], ref["r_max"]),
+                           use_rmin_shortcut=sc)
+        # straddling ties make leaf membership argpartition-dependent (8c)
+        assert_same_tree(tree, ref, canon=(tree.n_ties == 0 or name.startswith("dup")))
+        # the oracle uses the same tie rule as the device build: always bit-exact
+        orc = O.construct(pts, ref["r_min"], ref["r_max"], sc)
+        assert_same_tree(tree, orc)
+        assert tree.n_ties == orc["ties"]
+
+
+def test_build_cfg0_golden():
+    from paper_2406_02807_b200 import workloads as W
+    z = load_golden("cfg0.npz")
+    tree = P.construct(P.PointCloud(W.cfg0_cloud()), P.BuildParams(0.01, 0.08))
+    assert_same_tree(tree, golden_tree(z, ""))
+    n = int(z["n_queries"][0])
+    c, r = W.cfg0_queries()
+    assert np.array_equal(P.collides_many(tree, c[:n], r[:n]),
+                          np.unpackbits(z["mask"])[:n].astype(bool))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 100, 1000, 4097])
+def test_build_small_and_padded(n):
+    rng = np.random.default_rng(n)
+    pts = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+    tree = P.construct(P.PointCloud(pts), P.BuildParams(0.01, 0.3))
+    assert_same_tree(tree, O.construct(pts, 0.01, 0.3))
+
+
+def test_build_k2_and_k1():
+    rng = np.random.default_rng(6)
+    for k in (1, 2):
+        pts = rng.uniform(0, 1, (300, k)).astype(np.float32)
+        tree = P.construct(P.PointCloud(pts), P.BuildParams(0.01, 0.08))
+        assert_same_tree(tree, O.construct(pts, 0.01, 0.08))
+        c = rng.uniform(-0.1, 1.1, (5000, k)).astype(np.float32)
+        r = rng.uniform(0.01, 0.08, 5000).astype(np.float32)
+        assert np.array_equal(P.collides_many(tree, c, r), O.brute_collides_many(pts, c, r))
+
+
+def test_build_cfg1_scene_vs_oracle_and_brute():
+    from paper_2406_02807_b200 import workloads as W
+    cloud = W.cfg1_cloud()
+    for sc in (True, False):
+        tree = P.construct(P.PointCloud(cloud), P.BuildParams(0.02, 0.08), use_rmin_shortcut=sc)
+        assert_same_tree(tree, O.construct(cloud, 0.02, 0.08, sc))
+    c, r = W.cfg1_queries(cloud, n_groups=1 << 14)
+    assert np.array_equal(P.collides_many(tree, c, r), O.brute_collides_many(cloud, c, r))
+
+
+def test_build_duplicates_and_ties():
+    rng = np.random.default_rng(11)
+    base = rng.uniform(0, 1, (200, 3)).astype(np.float32)
+    pts = np.concatenate([base, base, base[:50]])
+    grid = np.stack(np.meshgrid(*[np.linspace(0, 1, 8)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    for cloud in (pts, grid.astype(np.float32)):
+        tree = P.construct(P.PointCloud(cloud), P.BuildParams(0.01, 0.2))
+        assert_same_tree(tree, O.construct(cloud, 0.01, 0.2))
+        c = rng.uniform(-0.1, 1.1, (20000, 3))
+        r = rng.uniform(0.01, 0.2, 20000)
+        assert np.array_equal(P.collides_many(tree, c, r), O.brute_collides_many(cloud, c, r))
+
+
+def test_build_from_device_tensor():
+    import torch
+    rng = np.random.default_rng(12)
+    pts = rng.uniform(-1, 1, (5000, 3)).astype(np.float32)
+    tree = P.construct(torch.from_numpy(pts).cuda(), P.BuildParams(0.01, 0.08))
+    assert_same_tree(tree, O.construct(pts, 0.01, 0.08))
+
+
+def test_build_rejects_bad_input():
+    with pytest.raises(ValueError):
+        P.construct(P.PointCloud(np.empty((0, 3), np.float32)), P.BuildParams(0.01, 0.08))
+    with pytest.raises(ValueError):
+        P.BuildParams(0.0, 1.0)
