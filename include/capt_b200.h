@@ -133,6 +133,10 @@ int capt_filter_cloud(int device, int k, const float* points, int64_t n,
                       double max_reach, uint32_t flags, float* out_points,
                       int64_t* n_out, void* stream);
 
+/* Number of kernels this library has launched in the process so far
+ * (all devices/threads); used by bench.py to report gpu_launches. */
+int64_t capt_kernel_launches(void);
+
 /* Measurement helper for the roofline denominator: FFMA throughput of this
  * device in TFLOP/s (CUDA-event timed dependent-chain FMA kernel). */
 int capt_measure_fp32_peak(int device, double* tflops);

@@ -53,7 +53,7 @@ def lib():
     L.oracle_leaf_indices.argtypes = [C.c_int, i64, _f32p, _f64p, i64, _i64p]
     L.oracle_collides_many.argtypes = [C.c_int, i64, _f32p, _f32p, _f32p, _i64p,
                                        _f32p, _f64p, _f64p, i64, C.c_int, _u8p,
-                                       _i64p, C.c_int]
+                                       C.c_void_p, C.c_int]
     L.oracle_collides_groups.argtypes = [C.c_int, i64, _f32p, _f32p, _f32p, _i64p,
                                          _f32p, _f64p, _f64p, C.c_void_p, i64,
                                          C.c_int, C.c_int, _u8p, _i64p, C.c_int]
@@ -161,7 +161,8 @@ def collides_many(tree, centers, radii, use_aabb_prefilter: bool = True,
     out = np.empty(len(c), np.uint8)
     cnt = np.zeros(3, np.int64)
     lib().oracle_collides_many(*_tree_args(t), c.ravel(), r, len(c),
-                               int(bool(use_aabb_prefilter)), out, cnt, int(threads))
+                               int(bool(use_aabb_prefilter)), out,
+                               cnt.ctypes.data if return_counters else None, int(threads))
     res = out.astype(bool)
     return (res, tuple(int(x) for x in cnt)) if return_counters else res
 

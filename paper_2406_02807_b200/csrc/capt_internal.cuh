@@ -64,6 +64,9 @@ struct capt_tree {
 
 namespace capt {
 
+// ---------------------------------------------------------------- launches
+void note_launches(int64_t k);
+
 // ---------------------------------------------------------------- errors
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);

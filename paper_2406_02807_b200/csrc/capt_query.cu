@@ -251,6 +251,7 @@ int launch_direct(const DevTree& t, const void* centers, const void* radii, int6
   }
 #undef LAUNCH
   CAPT_CUDA(cudaGetLastError());
+  note_launches(1);
   return CAPT_OK;
 }
 

@@ -1,5 +1,6 @@
 // Tree handles: error plumbing, upload from the reference layout
 // (Capt.__init__ tree.py:74-97), export back to it, slab replication.
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -9,6 +10,9 @@
 namespace capt {
 
 static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+void note_launches(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 
@@ -122,6 +126,8 @@ extern "C" {
 const char* capt_last_error(void) { return g_last_error.c_str(); }
 
 int capt_version(void) { return 1; }
+
+int64_t capt_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int capt_tree_create(int device, int k, int64_t n, int64_t n_points, double r_min,
                      double r_max, const float* tests, const float* aff_lo,

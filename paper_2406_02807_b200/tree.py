@@ -189,6 +189,34 @@ class Capt:
     def device_bytes(self) -> int:
         return int(self._info.device_bytes)
 
+    # -- replication (multi-GPU) ---------------------------------------------
+    def slab_tensor(self):
+        """Zero-copy torch uint8 view of the position-independent device slab
+        (include/capt_b200.h capt_tree_slab) -- what NCCL broadcasts."""
+        import torch
+        p, b = C.c_void_p(), C.c_int64()
+        _lib.check(_lib.lib().capt_tree_slab(self._h, C.byref(p), C.byref(b)), "capt_tree_slab")
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (int(b.value),), "typestr": "|u1",
+                                        "data": (int(p.value), False), "version": 3}
+
+        t = torch.as_tensor(_View(), device=torch.device("cuda", self.device))
+        t._capt_owner = self  # keep the tree alive while the view exists
+        return t
+
+    @classmethod
+    def from_slab(cls, slab, device: int | None = None, stream=None) -> "Capt":
+        """Copy a slab (CUDA uint8 tensor) into a new tree on ``device``."""
+        dev = slab.device.index if device is None else int(device)
+        h = C.c_void_p()
+        _lib.check(_lib.lib().capt_tree_from_slab(dev, slab.data_ptr(), int(slab.numel()),
+                                                  None if stream is None else int(stream),
+                                                  C.byref(h)), "capt_tree_from_slab")
+        info = _lib.CaptTreeInfo()
+        _lib.check(_lib.lib().capt_tree_info_get(h, C.byref(info)))
+        return cls._from_handle(h, info.r_min, info.r_max)
+
     def __repr__(self) -> str:
         return (f"Capt(k={self.k}, n={self.n}, points={self.n_points}, "
                 f"r_min={self.r_min}, r_max={self.r_max}, device=cuda:{self.device})")
