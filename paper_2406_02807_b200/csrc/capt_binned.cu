@@ -1,0 +1,521 @@
+// Leaf-binned query pipeline (the large-batch hot path).
+//
+// The reference itself groups spheres by leaf and scans each affordance set
+// once as a dense (spheres x points) distance matrix (query.py:209-218).  On
+// B200 that becomes:
+//   K1 k_bin_count    per sphere: band check, descent, fp32 AABB reject
+//                     (float64 fix-up in the band), warp-aggregated per-leaf
+//                     histogram; spheres needing the exact path go to a list
+//   K2 (CUB scans)    per-leaf start offsets and tile counts
+//   K3 k_bin_scatter  recompute the leaf, scatter a float4 {c, r} record and
+//                     the sphere id into leaf order (warp-aggregated cursor)
+//   K4 k_make_tiles   (leaf, chunk of <= 1024 spheres) work items
+//   K5 k_binned_scan  persistent CTAs pull tiles from an atomic counter; the
+//                     leaf's set is staged once into shared memory in local
+//                     coordinates b = p - o with w = |b|^2, and each thread
+//                     holds 8 spheres as 4 packed fp32x2 pairs:
+//                         t = w - 2 a.b    (3 FFMA2 per 2 tests)
+//                         min = min3(min, t_j, t_j+1)   (FMNMX3)
+//                     a sphere collides iff min_t <= r^2 - |a|^2; a proven
+//                     error band (64u relative to |a|^2 + |b|^2 + r^2) sends
+//                     the rare ambiguous sphere to an exact float64 rescan
+//                     done cooperatively by the CTA
+//   K6 k_slow         exact float64 scan for the K1 list
+//   K7 k_pack         verdict bytes -> bit words, OR over each lane group
+#include <cub/cub.cuh>
+
+#include <cstring>
+#include <type_traits>
+
+#include "capt_binned.cuh"
+#include "capt_query_common.cuh"
+
+namespace capt {
+
+namespace {
+
+constexpr int kBT = 128;           // threads per binned CTA
+constexpr int kS = 8;              // spheres per thread (4 packed pairs)
+constexpr int kTS = kBT * kS;      // spheres per tile
+constexpr int kChunk = 1024;       // staged points per shared-memory chunk
+constexpr float kBand = 0x1p-18f;  // 64u
+
+template <typename InT>
+__device__ __forceinline__ void load_sphere(const void* c, const void* r, int64_t q, int k,
+                                            double c64[3], double& r64) {
+  c64[0] = c64[1] = c64[2] = 0.0;
+  if constexpr (std::is_same<InT, float>::value) {
+    const float* cf = static_cast<const float*>(c);
+    for (int d = 0; d < k; ++d) c64[d] = double(__ldg(cf + q * k + d));
+    r64 = double(__ldg(static_cast<const float*>(r) + q));
+  } else {
+    const double* cd = static_cast<const double*>(c);
+    for (int d = 0; d < k; ++d) c64[d] = __ldg(cd + q * k + d);
+    r64 = __ldg(static_cast<const double*>(r) + q);
+  }
+}
+
+struct SphereClass {
+  int status;  // 0 false, 2 scan, 3 slow
+  int64_t leaf;
+  float cx, cy, cz, rf;
+};
+
+template <typename InT>
+__device__ __forceinline__ SphereClass classify_sphere(const DevTree& t, const float* sT, int n_smem,
+                                                       const BinArgs& a, int64_t q, bool check) {
+  SphereClass sc;
+  sc.status = 0;
+  sc.leaf = 0;
+  bool valid = q < a.n;
+  if (valid && a.mask) valid = a.mask[q] != 0;
+  if (!valid) return sc;
+  double c64[3], r64;
+  load_sphere<InT>(a.centers, a.radii, q, t.k, c64, r64);
+  if (check && (r64 < t.r_min || r64 > t.r_max))
+    atomicMin(a.first_bad, static_cast<unsigned long long>(q));
+  if constexpr (std::is_same<InT, float>::value) {
+    const float cf[3] = {float(c64[0]), float(c64[1]), float(c64[2])};
+    sc.leaf = descend_t<float>(t, sT, n_smem, cf);
+  } else {
+    sc.leaf = descend(t, sT, n_smem, c64);
+  }
+  float r2, loB, hiB;
+  sc.status = classify(t, sc.leaf, c64, r64, a.flags & CAPT_PREFILTER, sc.cx, sc.cy, sc.cz, r2,
+                       loB, hiB);
+  sc.rf = float(r64);
+  return sc;
+}
+
+template <typename InT>
+__global__ void __launch_bounds__(256) k_bin_count(BinArgs a) {
+  __shared__ float sT[kSmemNodes];
+  const DevTree& t = a.t;
+  const int n_smem = int(t.n - 1 < kSmemNodes ? t.n - 1 : kSmemNodes);
+  for (int i = threadIdx.x; i < n_smem; i += blockDim.x) sT[i] = t.T[i];
+  __syncthreads();
+  const bool check = a.flags & CAPT_CHECK_RADII;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int64_t n_pad = (a.n + 31) & ~int64_t(31);
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n_pad; q += stride) {
+    const SphereClass sc = classify_sphere<InT>(t, sT, n_smem, a, q, check);
+    const bool scan = sc.status == 2;
+    const unsigned act = __ballot_sync(0xffffffffu, scan);
+    if (scan) {
+      const unsigned peers = __match_any_sync(act, unsigned(sc.leaf));
+      if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(a.counts + sc.leaf, __popc(peers));
+    }
+    if (sc.status == 3) {
+      const unsigned i = atomicAdd(a.slow_n, 1u);
+      a.slow[i] = make_int2(int(q), int(sc.leaf));
+    }
+  }
+}
+
+template <typename InT>
+__global__ void __launch_bounds__(256) k_bin_scatter(BinArgs a) {
+  __shared__ float sT[kSmemNodes];
+  const DevTree& t = a.t;
+  const int n_smem = int(t.n - 1 < kSmemNodes ? t.n - 1 : kSmemNodes);
+  for (int i = threadIdx.x; i < n_smem; i += blockDim.x) sT[i] = t.T[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int64_t n_pad = (a.n + 31) & ~int64_t(31);
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n_pad; q += stride) {
+    const SphereClass sc = classify_sphere<InT>(t, sT, n_smem, a, q, false);
+    const bool scan = sc.status == 2;
+    const unsigned act = __ballot_sync(0xffffffffu, scan);
+    if (scan) {
+      const unsigned peers = __match_any_sync(act, unsigned(sc.leaf));
+      const int leader = __ffs(peers) - 1;
+      unsigned base = 0;
+      if (lane == leader) base = atomicAdd(a.cursor + sc.leaf, __popc(peers));
+      base = __shfl_sync(peers, base, leader);
+      const unsigned rank = __popc(peers & ((1u << lane) - 1u));
+      const int64_t pos = int64_t(a.start[sc.leaf]) + base + rank;
+      a.rec[pos] = make_float4(sc.cx, sc.cy, sc.cz, sc.rf);
+      a.rid[pos] = int(q);
+    }
+  }
+}
+
+__global__ void k_tile_counts(int64_t n, const uint32_t* __restrict__ counts,
+                              uint32_t* __restrict__ tcount) {
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+       j += int64_t(gridDim.x) * blockDim.x)
+    tcount[j] = (counts[j] + kTS - 1) / kTS;
+}
+
+__global__ void k_make_tiles(int64_t n, const uint32_t* __restrict__ tcount,
+                             const uint32_t* __restrict__ tstart, int2* __restrict__ tiles,
+                             uint32_t* __restrict__ n_tiles) {
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+       j += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t c = tcount[j], s = tstart[j];
+    for (uint32_t i = 0; i < c; ++i) tiles[s + i] = make_int2(int(j), int(i));
+    if (j == n - 1) *n_tiles = s + c;
+  }
+}
+
+// ---- packed fp32x2 helpers (sm_100: FFMA2 / FMNMX3) ----
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void unpack2(unsigned long long v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+  float d;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t okey(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float okey_inv(uint32_t u) {
+  u = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+  return __uint_as_float(u);
+}
+
+struct __align__(16) SmemBinned {
+  ulonglong2 A[kChunk];  // {bx,bx}, {by,by}
+  ulonglong2 B[kChunk];  // {bz,bz}, {w,w}
+  uint32_t minkey[kTS];
+  float thr[kTS];
+  float band[kTS];
+  uint32_t hitmask[kTS / kS];
+  int amb[kTS];
+  int n_amb;
+  int tile;
+  int flag;
+};
+
+__global__ void __launch_bounds__(kBT) k_binned_scan(BinArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SmemBinned& S = *reinterpret_cast<SmemBinned*>(smem_raw);
+  const DevTree& t = a.t;
+  const int tid = threadIdx.x;
+  const float INF = __int_as_float(0x7f800000);
+  while (true) {
+    if (tid == 0) S.tile = int(atomicAdd(a.tile_ctr, 1u));
+    __syncthreads();
+    const int tile = S.tile;
+    if (tile >= int(*a.n_tiles)) break;
+    const int2 tl = a.tiles[tile];
+    const int64_t leaf = tl.x;
+    const int64_t s0 = int64_t(a.start[leaf]) + int64_t(tl.y) * kTS;
+    const int cnt = int(min(uint32_t(kTS), a.counts[leaf] - uint32_t(tl.y) * kTS));
+    const uint2 st = t.set[leaf];
+    const float4 org = t.org[leaf];
+    const uint32_t m = st.y;
+    const uint32_t m4 = (m + 3u) & ~3u;
+    const float* xs = reinterpret_cast<const float*>(t.data + st.x);
+
+    const int nslot = (cnt + kS - 1) / kS;
+    const int P = max(1, kBT / nslot);
+    const bool active = tid < nslot * P;
+    const int slot = tid % nslot;
+    const int ph = tid / nslot;
+
+    // this thread's spheres, in local coordinates relative to the set origin
+    unsigned long long Kx[kS / 2], Ky[kS / 2], Kz[kS / 2];
+    float thr[kS], band[kS], mn[kS];
+    bool real[kS];
+#pragma unroll
+    for (int i = 0; i < kS; i += 2) {
+      float kx[2], ky[2], kz[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int s = slot * kS + i + h;
+        real[i + h] = active && s < cnt;
+        if (real[i + h]) {
+          const float4 rc = a.rec[s0 + s];
+          const float ax = rc.x - org.x, ay = rc.y - org.y, az = rc.z - org.z;
+          const float aa = fmaf(az, az, fmaf(ay, ay, ax * ax));
+          const float r2 = rc.w * rc.w;
+          kx[h] = -2.f * ax;
+          ky[h] = -2.f * ay;
+          kz[h] = -2.f * az;
+          thr[i + h] = r2 - aa;
+          band[i + h] = kBand * (aa + org.w + r2);
+        } else {
+          kx[h] = ky[h] = kz[h] = 0.f;
+          thr[i + h] = -INF;
+          band[i + h] = 0.f;
+        }
+        mn[i + h] = INF;
+      }
+      Kx[i / 2] = pack2(kx[0], kx[1]);
+      Ky[i / 2] = pack2(ky[0], ky[1]);
+      Kz[i / 2] = pack2(kz[0], kz[1]);
+    }
+    for (int s = tid; s < kTS; s += kBT) S.minkey[s] = 0xffffffffu;
+    for (int s = tid; s < kTS / kS; s += kBT) S.hitmask[s] = 0;
+    if (active && ph == 0) {
+#pragma unroll
+      for (int i = 0; i < kS; ++i) {
+        const int s = slot * kS + i;
+        if (s < cnt) {
+          S.thr[s] = thr[i];
+          S.band[s] = band[i];
+        }
+      }
+    }
+    uint32_t my_real = 0;
+#pragma unroll
+    for (int i = 0; i < kS; ++i) my_real |= uint32_t(real[i]) << i;
+    bool done = !active || my_real == 0;
+
+    for (uint32_t c0 = 0; c0 < m; c0 += kChunk) {
+      const uint32_t len = min(uint32_t(kChunk), m - c0);
+      const uint32_t len2 = (len + 1u) & ~1u;
+      __syncthreads();  // previous chunk fully consumed
+      for (uint32_t i = tid; i < len2; i += kBT) {
+        const uint32_t g = c0 + i;
+        float bx = 0.f, by = 0.f, bz = 0.f, w = INF;
+        if (i < len) {
+          const float px = xs[g], py = xs[m4 + g], pz = xs[2 * m4 + g];
+          if (isfinite(px) && isfinite(py) && isfinite(pz)) {
+            bx = px - org.x;
+            by = py - org.y;
+            bz = pz - org.z;
+            w = fmaf(bz, bz, fmaf(by, by, bx * bx));
+          }
+        }
+        S.A[i] = make_ulonglong2(pack2(bx, bx), pack2(by, by));
+        S.B[i] = make_ulonglong2(pack2(bz, bz), pack2(w, w));
+      }
+      __syncthreads();
+      if (!done) {
+        const int npairs = int(len2 / 2);
+        int it = 0;
+        for (int u = ph; u < npairs; u += P) {
+          const ulonglong2 A0 = S.A[2 * u], B0 = S.B[2 * u];
+          const ulonglong2 A1 = S.A[2 * u + 1], B1 = S.B[2 * u + 1];
+#pragma unroll
+          for (int q = 0; q < kS / 2; ++q) {
+            unsigned long long t0 = ffma2(A0.x, Kx[q], B0.y);
+            t0 = ffma2(A0.y, Ky[q], t0);
+            t0 = ffma2(B0.x, Kz[q], t0);
+            unsigned long long t1 = ffma2(A1.x, Kx[q], B1.y);
+            t1 = ffma2(A1.y, Ky[q], t1);
+            t1 = ffma2(B1.x, Kz[q], t1);
+            float t0l, t0h, t1l, t1h;
+            unpack2(t0, t0l, t0h);
+            unpack2(t1, t1l, t1h);
+            mn[2 * q] = fmin3(mn[2 * q], t0l, t1l);
+            mn[2 * q + 1] = fmin3(mn[2 * q + 1], t0h, t1h);
+          }
+          if ((++it & 7) == 0) {
+            uint32_t h = 0;
+#pragma unroll
+            for (int i = 0; i < kS; ++i) h |= uint32_t(mn[i] <= thr[i] - band[i]) << i;
+            if (h) atomicOr(&S.hitmask[slot], h);
+            const uint32_t seen = *reinterpret_cast<volatile uint32_t*>(&S.hitmask[slot]);
+            if (((seen | h) & my_real) == my_real) break;
+          }
+        }
+        uint32_t h = 0;
+#pragma unroll
+        for (int i = 0; i < kS; ++i) h |= uint32_t(mn[i] <= thr[i] - band[i]) << i;
+        if (h) atomicOr(&S.hitmask[slot], h);
+        if (((S.hitmask[slot] | h) & my_real) == my_real) done = true;
+      }
+    }
+    // combine the phases' minima
+    if (active) {
+#pragma unroll
+      for (int i = 0; i < kS; ++i)
+        if (real[i]) atomicMin(&S.minkey[slot * kS + i], okey(mn[i]));
+    }
+    if (tid == 0) S.n_amb = 0;
+    __syncthreads();
+    for (int s = tid; s < cnt; s += kBT) {
+      const bool hit_flag = (S.hitmask[s / kS] >> (s % kS)) & 1u;
+      const float mv = okey_inv(S.minkey[s]);
+      const float th = S.thr[s], bd = S.band[s];
+      if (hit_flag || mv <= th - bd) {
+        a.verdict[a.rid[s0 + s]] = 1;
+      } else if (!(mv > th + bd)) {
+        S.amb[atomicAdd(&S.n_amb, 1)] = s;
+      }
+    }
+    __syncthreads();
+    // exact float64 rescan of ambiguous spheres (query.py:96-99 arithmetic)
+    const int n_amb = S.n_amb;
+    for (int i = 0; i < n_amb; ++i) {
+      const int s = S.amb[i];
+      const float4 rc = a.rec[s0 + s];
+      const double c[3] = {rc.x, rc.y, rc.z};
+      const double R = __dmul_rn(double(rc.w), double(rc.w));
+      if (tid == 0) S.flag = 0;
+      __syncthreads();
+      bool hit = false;
+      for (uint32_t j = tid; j < m; j += kBT) {
+        double sum = 0.0;
+        for (int d = 0; d < t.k; ++d) {
+          const double x = __dsub_rn(c[d], double(xs[d * m4 + j]));
+          const double sq = __dmul_rn(x, x);
+          sum = d == 0 ? sq : __dadd_rn(sum, sq);
+        }
+        hit |= sum <= R;
+      }
+      if (hit) S.flag = 1;
+      __syncthreads();
+      if (tid == 0) {
+        if (S.flag) a.verdict[a.rid[s0 + s]] = 1;
+        atomicAdd(a.n_refined, 1u);
+      }
+      __syncthreads();
+    }
+  }
+}
+
+template <typename InT>
+__global__ void k_slow(BinArgs a) {
+  const unsigned n = *a.slow_n;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int2 e = a.slow[i];
+    double c64[3], r64;
+    load_sphere<InT>(a.centers, a.radii, e.x, a.t.k, c64, r64);
+    if (scan_f64(a.t, a.t.set[e.y], c64, r64, nullptr)) a.verdict[e.x] = 1;
+  }
+}
+
+__global__ void k_pack(int64_t n_groups, int L, const uint8_t* __restrict__ v,
+                       uint32_t* __restrict__ bits, int64_t n_words) {
+  for (int64_t w = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < n_words;
+       w += int64_t(gridDim.x) * blockDim.x) {
+    uint32_t word = 0;
+    const int64_t g0 = w * 32;
+    const int ng = int(min(int64_t(32), n_groups - g0));
+    if (L == 8) {
+      const uint64_t* v8 = reinterpret_cast<const uint64_t*>(v);
+      for (int g = 0; g < ng; ++g) word |= uint32_t(v8[g0 + g] != 0) << g;
+    } else if (L == 1) {
+      for (int g = 0; g < ng; ++g) word |= uint32_t(v[g0 + g] != 0) << g;
+    } else {
+      for (int g = 0; g < ng; ++g) {
+        uint32_t any = 0;
+        for (int l = 0; l < L; ++l) any |= v[(g0 + g) * L + l];
+        word |= uint32_t(any != 0) << g;
+      }
+    }
+    bits[w] = word;
+  }
+}
+
+struct Arena {
+  cudaStream_t s;
+  void* ptrs[24];
+  int np = 0;
+  template <class T>
+  T* get(size_t count) {
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, (count ? count : 1) * sizeof(T), s) != cudaSuccess) return nullptr;
+    ptrs[np++] = p;
+    return static_cast<T*>(p);
+  }
+  ~Arena() {
+    for (int i = 0; i < np; ++i) cudaFreeAsync(ptrs[i], s);
+  }
+};
+
+}  // namespace
+
+bool binned_preferred(const DevTree& t, int64_t n, uint32_t flags) {
+  if (flags & CAPT_STATS) return false;
+  if (flags & CAPT_MODE_DIRECT) return false;
+  if (n >= (int64_t(1) << 31)) return false;
+  if (flags & CAPT_MODE_BINNED) return true;
+  return n >= (int64_t(1) << 18) && n >= 16 * t.n;
+}
+
+int launch_binned(const DevTree& t, const void* centers, const void* radii, int64_t n, int L,
+                  const uint8_t* mask, uint32_t flags, uint32_t* bits, int64_t n_words,
+                  unsigned long long* first_bad, cudaStream_t s) {
+  static bool smem_set = false;
+  if (!smem_set) {
+    CAPT_CUDA(cudaFuncSetAttribute(k_binned_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(sizeof(SmemBinned))));
+    smem_set = true;
+  }
+  Arena A;
+  A.s = s;
+  BinArgs a;
+  memset(&a, 0, sizeof(a));
+  a.t = t;
+  a.centers = centers;
+  a.radii = radii;
+  a.n = n;
+  a.L = L;
+  a.mask = mask;
+  a.flags = flags;
+  a.first_bad = first_bad;
+  const int64_t nl = t.n;
+  uint32_t* ctr = A.get<uint32_t>(4);  // slow_n, n_tiles, tile_ctr, n_refined
+  a.counts = A.get<uint32_t>(nl);
+  a.cursor = A.get<uint32_t>(nl);
+  a.start = A.get<uint32_t>(nl);
+  uint32_t* tcount = A.get<uint32_t>(nl);
+  uint32_t* tstart = A.get<uint32_t>(nl);
+  a.tiles = A.get<int2>(nl + n / kTS + 1);
+  a.rec = A.get<float4>(n);
+  a.rid = A.get<int>(n);
+  a.verdict = A.get<uint8_t>(n + 8);
+  a.slow = A.get<int2>(n);
+  if (!ctr || !a.counts || !a.cursor || !a.start || !tcount || !tstart || !a.tiles || !a.rec ||
+      !a.rid || !a.verdict || !a.slow)
+    return fail(CAPT_ENOMEM, "binned scratch allocation");
+  a.slow_n = ctr;
+  a.n_tiles = ctr + 1;
+  a.tile_ctr = ctr + 2;
+  a.n_refined = ctr + 3;
+  CAPT_CUDA(cudaMemsetAsync(ctr, 0, 16, s));
+  CAPT_CUDA(cudaMemsetAsync(a.counts, 0, 4 * nl, s));
+  CAPT_CUDA(cudaMemsetAsync(a.cursor, 0, 4 * nl, s));
+  CAPT_CUDA(cudaMemsetAsync(a.verdict, 0, n + 8, s));
+  const bool f64 = flags & CAPT_INPUT_F64;
+  const int G = grid_for(n, 256, 8);
+  if (f64) k_bin_count<double><<<G, 256, 0, s>>>(a);
+  else k_bin_count<float><<<G, 256, 0, s>>>(a);
+  // per-leaf starts and tiles
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, a.counts, a.start, nl, s);
+  void* tmp = A.get<char>(tb);
+  if (!tmp) return fail(CAPT_ENOMEM, "binned scratch allocation");
+  CAPT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, a.counts, a.start, nl, s));
+  const int Gl = grid_for(nl, 256, 8);
+  k_tile_counts<<<Gl, 256, 0, s>>>(nl, a.counts, tcount);
+  CAPT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, tcount, tstart, nl, s));
+  k_make_tiles<<<Gl, 256, 0, s>>>(nl, tcount, tstart, a.tiles, a.n_tiles);
+  if (f64) k_bin_scatter<double><<<G, 256, 0, s>>>(a);
+  else k_bin_scatter<float><<<G, 256, 0, s>>>(a);
+  static int sms = 0, occ = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_binned_scan, kBT, sizeof(SmemBinned));
+    if (occ < 1) occ = 1;
+  }
+  k_binned_scan<<<sms * occ, kBT, sizeof(SmemBinned), s>>>(a);
+  if (f64) k_slow<double><<<sms, 128, 0, s>>>(a);
+  else k_slow<float><<<sms, 128, 0, s>>>(a);
+  k_pack<<<grid_for(n_words, 256, 8), 256, 0, s>>>(n / L, L, a.verdict, bits, n_words);
+  CAPT_CUDA(cudaGetLastError());
+  note_launches(9);  // count, 2 scans, tile counts, tiles, scatter, scan, slow, pack
+  return CAPT_OK;
+}
+
+}  // namespace capt

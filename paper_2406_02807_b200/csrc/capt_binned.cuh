@@ -1,0 +1,37 @@
+// Leaf-binned query pipeline (capt_binned.cu) -- shared declarations.
+#pragma once
+
+#include "capt_internal.cuh"
+
+namespace capt {
+
+struct BinArgs {
+  DevTree t;
+  const void* centers;
+  const void* radii;
+  int64_t n;
+  int L;
+  const uint8_t* mask;
+  uint32_t flags;
+  uint32_t* counts;   // per leaf: AABB-passing spheres
+  uint32_t* cursor;   // per leaf: scatter cursor
+  uint32_t* start;    // per leaf: first binned slot
+  int2* tiles;        // (leaf, chunk)
+  float4* rec;        // binned {cx, cy, cz, r}
+  int* rid;           // binned sphere ids
+  uint8_t* verdict;   // per sphere
+  int2* slow;         // (sphere, leaf) for the exact float64 path
+  uint32_t* slow_n;
+  uint32_t* n_tiles;
+  uint32_t* tile_ctr;
+  uint32_t* n_refined;
+  unsigned long long* first_bad;
+};
+
+bool binned_preferred(const DevTree& t, int64_t n, uint32_t flags);
+
+int launch_binned(const DevTree& t, const void* centers, const void* radii, int64_t n, int L,
+                  const uint8_t* mask, uint32_t flags, uint32_t* bits, int64_t n_words,
+                  unsigned long long* first_bad, cudaStream_t s);
+
+}  // namespace capt

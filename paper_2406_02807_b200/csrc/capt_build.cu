@@ -474,6 +474,7 @@ extern "C" int capt_tree_build(int device, int k, const float* points, int64_t n
     k_fill<<<grid_for(n, 128, 16), 128, 0, s>>>(v, dv.set, const_cast<float4*>(dv.data),
                                                 const_cast<float4*>(dv.box));
     e = cudaGetLastError();
+    if (e == cudaSuccess && compute_origins(dv, s)) e = cudaErrorLaunchFailure;
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) {

@@ -9,6 +9,9 @@
 //   offs   int64[n+1]               reference CSR offsets (tree.py:226-228)
 //   data   float4[...]              per set: xs[m4] ys[m4] zs[m4], m4 = roundup(m,4),
 //                                   padding rows +inf; unused dims (k<3) are 0
+//   org    float4[n]                binned-scan origin of each set: centre of the
+//                                   finite points' box (xyz) and the largest
+//                                   fp32 |p - o|^2 over the set (w)
 #pragma once
 
 #include <cuda_runtime.h>
@@ -21,7 +24,7 @@
 namespace capt {
 
 constexpr uint64_t kSlabMagic = 0x3030324254504143ull;  // "CAPTB200"
-constexpr int kSlabVersion = 1;
+constexpr int kSlabVersion = 2;
 constexpr int kMaxK = 3;
 
 struct SlabHeader {
@@ -39,7 +42,8 @@ struct SlabHeader {
   int64_t off_T, off_box, off_set, off_offs, off_data;  // byte offsets in slab
   int64_t data_f4;    // float4 count of the data section
   int64_t bytes;      // slab size
-  int64_t reserved[10];
+  int64_t off_org;    // byte offset of the org section
+  int64_t reserved[9];
 };
 static_assert(sizeof(SlabHeader) <= 256, "header must fit its 256-B section");
 
@@ -52,6 +56,7 @@ struct DevTree {
   const uint2* set;
   const int64_t* offs;
   const float4* data;
+  const float4* org;
 };
 
 }  // namespace capt
@@ -66,6 +71,10 @@ namespace capt {
 
 // ---------------------------------------------------------------- launches
 void note_launches(int64_t k);
+
+// Keep stream-ordered scratch allocations cached in the device's default
+// memory pool (no release at synchronisation points).
+void ensure_pool(int device);
 
 // ---------------------------------------------------------------- errors
 void set_error(const std::string& msg);
@@ -90,6 +99,7 @@ inline DevTree view(const capt_tree* t) {
   d.set = reinterpret_cast<const uint2*>(t->slab + t->h.off_set);
   d.offs = reinterpret_cast<const int64_t*>(t->slab + t->h.off_offs);
   d.data = reinterpret_cast<const float4*>(t->slab + t->h.off_data);
+  d.org = reinterpret_cast<const float4*>(t->slab + t->h.off_org);
   return d;
 }
 
@@ -107,6 +117,8 @@ inline int64_t layout_slab(SlabHeader& h, int64_t data_f4) {
   off = align256(off + sizeof(uint2) * h.n);
   h.off_offs = off;
   off = align256(off + sizeof(int64_t) * (h.n + 1));
+  h.off_org = off;
+  off = align256(off + sizeof(float4) * h.n);
   h.off_data = off;
   off = align256(off + sizeof(float4) * (data_f4 > 0 ? data_f4 : 1));
   h.data_f4 = data_f4;
@@ -120,11 +132,8 @@ inline int depth_of(int64_t n) {
   return d;
 }
 
-// Kernels shared between tree creation paths (capt_tree.cu).
-// Given per-leaf sizes m (device, uint2.y filled), fill start4 (uint2.x) by an
-// exclusive scan of 3*roundup(m,4)/4 and return the total float4 count.
-int assign_set_starts(uint2* set, int64_t n, int64_t* data_f4, int64_t* total,
-                      int64_t* max_aff, int64_t* d_offs, cudaStream_t s);
+// Fill the org section (binned-scan origins) of a slab whose data is final.
+int compute_origins(const DevTree& t, cudaStream_t s);
 
 int alloc_slab(capt_tree** out, int device, SlabHeader h);
 

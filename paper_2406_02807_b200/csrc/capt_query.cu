@@ -22,6 +22,7 @@
 #include <cstring>
 #include <type_traits>
 
+#include "capt_binned.cuh"
 #include "capt_internal.cuh"
 #include "capt_query_common.cuh"
 
@@ -270,6 +271,7 @@ extern "C" int capt_query(const capt_tree* tree, const void* centers, const void
   if (n > 0 && (!centers || !radii || !out_bits)) return fail(CAPT_EINVAL, "NULL array argument");
   if ((flags & CAPT_STATS) && !counters) return fail(CAPT_EINVAL, "CAPT_STATS needs counters");
   CAPT_CUDA(cudaSetDevice(tree->device));
+  ensure_pool(tree->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const DevTree t = view(tree);
   const int64_t n_groups = n / L;
@@ -313,7 +315,9 @@ extern "C" int capt_query(const capt_tree* tree, const void* centers, const void
   if (n > 0) {
     uint32_t fl = flags;
     if (!bad) fl &= ~CAPT_CHECK_RADII;
-    int rc = launch_direct(t, d_c, d_r, n, L, d_m, fl, d_bits, n_words, d_cnt, bad, s);
+    int rc = binned_preferred(t, n, fl)
+                 ? launch_binned(t, d_c, d_r, n, L, d_m, fl, d_bits, n_words, bad, s)
+                 : launch_direct(t, d_c, d_r, n, L, d_m, fl, d_bits, n_words, d_cnt, bad, s);
     if (rc) return rc;
   }
   if (host) {

@@ -69,7 +69,7 @@ __device__ __forceinline__ bool aabb_keep64(int k, const float4 lo, const float4
 }
 
 // Exact reference scan of one affordance set (query.py:96-99, 214-218).
-__device__ __noinline__ bool scan_f64(const DevTree& t, uint2 set, const double c[3],
+static __device__ __noinline__ bool scan_f64(const DevTree& t, uint2 set, const double c[3],
                                       double r64, bool* boundary) {
   const float* base = reinterpret_cast<const float*>(t.data + set.x);
   const uint32_t m4 = (set.y + 3u) & ~3u;

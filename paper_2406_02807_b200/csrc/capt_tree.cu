@@ -14,6 +14,17 @@ static std::atomic<int64_t> g_launches{0};
 
 void note_launches(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
+void ensure_pool(int device) {
+  static std::atomic<uint64_t> done{0};
+  if (device < 0 || device >= 64 || (done.load() >> device) & 1ull) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done.fetch_or(1ull << device);
+}
+
 void set_error(const std::string& msg) { g_last_error = msg; }
 
 int fail(int code, const std::string& msg) {
@@ -117,6 +128,52 @@ __global__ void k_unpack_boxes(int k, int64_t n, const float4* __restrict__ box,
   }
 }
 
+// One warp per leaf: centre of the finite points' box and the largest fp32
+// |fl(p - o)|^2, evaluated exactly as the binned scan stages the set.
+__global__ void k_origins(DevTree t) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t j = warp; j < t.n; j += nwarps) {
+    const uint2 st = t.set[j];
+    const uint32_t m4 = (st.y + 3u) & ~3u;
+    const float* base = reinterpret_cast<const float*>(t.data + st.x);
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (uint32_t i = lane; i < st.y; i += 32) {
+      const float p[3] = {base[i], base[m4 + i], base[2 * m4 + i]};
+      if (!isfinite(p[0]) || !isfinite(p[1]) || !isfinite(p[2])) continue;
+      for (int d = 0; d < 3; ++d) {
+        lo[d] = fminf(lo[d], p[d]);
+        hi[d] = fmaxf(hi[d], p[d]);
+      }
+    }
+    float o[3];
+    for (int d = 0; d < 3; ++d) {
+      for (int s = 16; s > 0; s >>= 1) {
+        lo[d] = fminf(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], s));
+        hi[d] = fmaxf(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], s));
+      }
+      o[d] = lo[d] <= hi[d] ? 0.5f * lo[d] + 0.5f * hi[d] : 0.f;
+    }
+    float bb = 0.f;
+    for (uint32_t i = lane; i < st.y; i += 32) {
+      const float p[3] = {base[i], base[m4 + i], base[2 * m4 + i]};
+      if (!isfinite(p[0]) || !isfinite(p[1]) || !isfinite(p[2])) continue;
+      const float bx = p[0] - o[0], by = p[1] - o[1], bz = p[2] - o[2];
+      bb = fmaxf(bb, fmaf(bz, bz, fmaf(by, by, bx * bx)));
+    }
+    for (int s = 16; s > 0; s >>= 1) bb = fmaxf(bb, __shfl_xor_sync(0xffffffffu, bb, s));
+    if (lane == 0) const_cast<float4*>(t.org)[j] = make_float4(o[0], o[1], o[2], bb);
+  }
+}
+
+int compute_origins(const DevTree& t, cudaStream_t s) {
+  k_origins<<<grid_for(t.n * 32, 256), 256, 0, s>>>(t);
+  CAPT_CUDA(cudaGetLastError());
+  note_launches(1);
+  return CAPT_OK;
+}
+
 }  // namespace capt
 
 using namespace capt;
@@ -200,6 +257,12 @@ int capt_tree_create(int device, int k, int64_t n, int64_t n_points, double r_mi
                                                     const_cast<float4*>(v.data));
   k_pack_boxes<<<grid_for(n, 256), 256, 0, s>>>(k, n, d_lo, d_hi, const_cast<float4*>(v.box));
   UPCHK(cudaGetLastError());
+  if (compute_origins(v, s)) {
+    cudaFree(d_vals); cudaFree(d_lo); cudaFree(d_hi);
+    capt_tree_destroy(t);
+    *out = nullptr;
+    return CAPT_ECUDA;
+  }
   UPCHK(cudaDeviceSynchronize());
   cudaFree(d_vals);
   cudaFree(d_lo);

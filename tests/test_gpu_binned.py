@@ -1,0 +1,128 @@
+"""Parity of the leaf-binned query pipeline (capt_binned.cu) with the oracle.
+
+Every case forces CAPT_MODE_BINNED and, where useful, compares against the
+direct kernel as well (both must equal the oracle bit for bit)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_tree, load_golden
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2406_02807_b200")
+from paper_2406_02807_b200 import _lib  # noqa: E402
+from paper_2406_02807_b200 import workloads as W  # noqa: E402
+from paper_2406_02807_b200.query import _host_inputs, _host_query  # noqa: E402
+
+BINNED, DIRECT = _lib.MODE_BINNED, _lib.MODE_DIRECT
+
+
+def upload(t):
+    return P.Capt(t["k"], t["n_points"], t["r_min"], t["r_max"], t["tests"], t["aff_lo"],
+                  t["aff_hi"], t["offsets"], t["aff_values"])
+
+
+def q(tree, c, r, L=1, mask=None, prefilter=True, mode=BINNED):
+    cc, rr, f64 = _host_inputs(tree, c, r)
+    bits, _, bad = _host_query(tree, cc, rr, f64, L, mask, prefilter, False, mode=mode)
+    return bits
+
+
+def test_binned_golden_masks():
+    z = load_golden("queries.npz")
+    for name in z["names"]:
+        pts = z[f"{name}/points"]
+        rmin, rmax = z[f"{name}/band"]
+        tree = upload(O.construct(pts, rmin, rmax))
+        c, r = z[f"{name}/centers"], z[f"{name}/radii"]
+        n = len(r)
+        exp = np.unpackbits(z[f"{name}/mask"])[:n].astype(bool)
+        assert np.array_equal(q(tree, c, r), exp), name
+        nopre = np.unpackbits(z[f"{name}/mask_nopre"])[:n].astype(bool)
+        assert np.array_equal(q(tree, c, r, prefilter=False), nopre), name
+        lane = np.unpackbits(z[f"{name}/lane_mask"])[:n].astype(bool)
+        gb = np.unpackbits(z[f"{name}/group8"])[: n // 8].astype(bool)
+        assert np.array_equal(q(tree, c, r, 8, lane.astype(np.uint8)), gb), name
+
+
+def test_binned_cfg0_golden():
+    z = load_golden("cfg0.npz")
+    tree = upload(golden_tree(z, ""))
+    n = int(z["n_queries"][0])
+    c, r = W.cfg0_queries()
+    assert np.array_equal(q(tree, c[:n], r[:n]), np.unpackbits(z["mask"])[:n].astype(bool))
+    # full config-0 batch: binned == direct == oracle
+    exp = O.collides_many(golden_tree(z, ""), c, r)
+    assert np.array_equal(q(tree, c, r), exp)
+    assert np.array_equal(q(tree, c, r, mode=DIRECT), exp)
+
+
+@pytest.mark.parametrize("L", [1, 2, 8, 32])
+def test_binned_cfg1_groups(L):
+    cloud = W.cfg1_cloud()
+    t = O.construct(cloud, 0.02, 0.08)
+    tree = upload(t)
+    c, r = W.cfg1_queries(cloud, n_groups=1 << 16)
+    per = O.collides_many(t, c, r)
+    exp = per.reshape(-1, L).any(1)
+    assert np.array_equal(q(tree, c, r, L), exp)
+    if L == 8:
+        assert np.array_equal(q(tree, c, r, 8, mode=DIRECT), exp)
+        assert np.array_equal(O.collides_groups(t, c, r, 8), exp)
+
+
+def test_binned_dense_gaussians_multichunk():
+    # dense mixture: affordance sets larger than one 1024-point shared-memory chunk
+    cloud = W.cfg3_cloud(n=32768, n_comp=8, seed=5)
+    t = O.construct(cloud, 0.01, 0.1)
+    assert np.diff(t["offsets"]).max() > 1024
+    tree = upload(t)
+    c, r = W.cfg3_queries(1 << 19, seed=7)
+    exp = O.collides_many(t, c, r)
+    assert np.array_equal(q(tree, c, r), exp)
+
+
+def test_binned_f64_and_nonfinite():
+    rng = np.random.default_rng(17)
+    pts = rng.uniform(0, 1, (3000, 3)).astype(np.float32)
+    t = O.construct(pts, 0.01, 0.08)
+    tree = upload(t)
+    c = rng.uniform(-0.1, 1.1, (300000, 3))
+    r = rng.uniform(0.01, 0.08, 300000)
+    c[:1000] = c[:1000].astype(np.float32)  # some fp32-exact rows
+    r[:1000] = r[:1000].astype(np.float32)
+    c[5, 0] = np.nan
+    c[6, 1] = np.inf
+    r[7] = np.nan
+    exp = O.collides_many(t, c, r)
+    assert np.array_equal(q(tree, c, r), exp)
+
+
+def test_binned_tangency_heavy():
+    # spheres exactly tangent (in float64) to cloud points: exercises the
+    # ambiguous-band rescan inside the binned kernel
+    rng = np.random.default_rng(23)
+    pts = rng.uniform(0, 1, (4096, 3)).astype(np.float32)
+    t = O.construct(pts, 0.01, 0.08)
+    tree = upload(t)
+    n = 1 << 18
+    idx = rng.integers(0, len(pts), n)
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    r = W.clamp_radii(rng.uniform(0.01, 0.08, n).astype(np.float32), 0.01, 0.08)
+    c = (pts[idx].astype(np.float64) + d * r[:, None].astype(np.float64)).astype(np.float32)
+    exp = O.collides_many(t, c, r)
+    got = q(tree, c, r)
+    assert np.array_equal(got, exp)
+    assert np.array_equal(got, O.brute_collides_many(pts, c, r))
+
+
+def test_binned_device_built_tree_and_auto_mode():
+    cloud = W.cfg1_cloud()
+    tree = P.construct(P.PointCloud(cloud), P.BuildParams(0.02, 0.08))
+    c, r = W.cfg1_queries(cloud, n_groups=1 << 15, seed=3)
+    exp = O.brute_collides_many(cloud, c, r)
+    assert np.array_equal(P.collides_many(tree, c, r), exp)  # auto -> binned here
+    assert np.array_equal(q(tree, c, r, mode=DIRECT), exp)
