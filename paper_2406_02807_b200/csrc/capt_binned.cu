@@ -37,7 +37,7 @@ namespace {
 constexpr int kBT = 128;           // threads per binned CTA
 constexpr int kS = 8;              // spheres per thread (4 packed pairs)
 constexpr int kTS = kBT * kS;      // spheres per tile
-constexpr int kChunk = 1024;       // staged points per shared-memory chunk
+constexpr int kChunk = 768;        // staged points per shared-memory chunk
 constexpr float kBand = 0x1p-18f;  // 64u
 
 template <typename InT>
@@ -87,6 +87,68 @@ __device__ __forceinline__ SphereClass classify_sphere(const DevTree& t, const f
   return sc;
 }
 
+// fp32 inputs: branch-light classification without any float64 work on the
+// common path.  Band check against the fp32 images of the double band edges
+// (r < r_min in double <=> r < smallest float >= r_min).  Returns 0 (false),
+// 2 (binned fp32 scan) or 3 (exact float64 scan; AABB already decided).
+__device__ __forceinline__ int classify_f32(const DevTree& t, const float* sT, int n_smem,
+                                            const BinArgs& a, int64_t q, bool check, int& leaf) {
+  const float* cf = static_cast<const float*>(a.centers);
+  float c[3] = {0.f, 0.f, 0.f};
+  for (int d = 0; d < t.k; ++d) c[d] = __ldg(cf + q * t.k + d);
+  const float r = __ldg(static_cast<const float*>(a.radii) + q);
+  if (check && (r < a.rlo_f || r > a.rhi_f))
+    atomicMin(a.first_bad, static_cast<unsigned long long>(q));
+  int i = 0;
+  if (t.k == 3) {
+    // levels 0..11 (node ids < 4095) come from shared memory, 3 axes per step
+    const float c0 = c[0], c1 = c[1], c2 = c[2];
+    const int dsm = t.depth < 12 ? t.depth : 12;
+    int s = 0;
+    for (; s + 3 <= dsm; s += 3) {
+      i = 2 * i + 1 + (c0 > sT[i] ? 1 : 0);
+      i = 2 * i + 1 + (c1 > sT[i] ? 1 : 0);
+      i = 2 * i + 1 + (c2 > sT[i] ? 1 : 0);
+    }
+    for (; s < t.depth; ++s) {
+      const int ax = s % 3;
+      const float cv = ax == 0 ? c0 : (ax == 1 ? c1 : c2);
+      const float tv = s < dsm ? sT[i] : __ldg(t.T + i);
+      i = 2 * i + 1 + (cv > tv ? 1 : 0);
+    }
+  } else {
+    int ax = 0;
+    for (int s = 0; s < t.depth; ++s) {
+      const float tv = (i < n_smem) ? sT[i] : __ldg(t.T + i);
+      const float cv = ax == 0 ? c[0] : (ax == 1 ? c[1] : c[2]);
+      i = 2 * i + 1 + (cv > tv ? 1 : 0);
+      ax = (ax + 1 == t.k) ? 0 : ax + 1;
+    }
+  }
+  leaf = i - int(t.n - 1);
+  const bool cfin = isfinite(c[0]) && isfinite(c[1]) && isfinite(c[2]);
+  const float r2 = r * r;
+  const bool fast = cfin && r2 >= kR2Min && r2 <= kR2Max;
+  if (!fast && !cfin && isfinite(r)) return 0;  // finite r^2 in float64: never collides
+  const bool prefilter = a.flags & CAPT_PREFILTER;
+  if (!prefilter) return fast ? 2 : 3;
+  const float4 lo = __ldg(t.box + 2 * leaf);
+  const float4 hi = __ldg(t.box + 2 * leaf + 1);
+  if (fast) {
+    const float rx = fmaxf(fmaxf(lo.x - c[0], 0.f), c[0] - hi.x);
+    const float ry = fmaxf(fmaxf(lo.y - c[1], 0.f), c[1] - hi.y);
+    const float rz = fmaxf(fmaxf(lo.z - c[2], 0.f), c[2] - hi.z);
+    const float s = fmaf(rz, rz, fmaf(ry, ry, rx * rx));
+    if (s > r2 * (1.0f + kTau)) return 0;
+    if (s < r2 * (1.0f - kTau)) return 2;
+  }
+  const double c64[3] = {c[0], c[1], c[2]};
+  const double r64 = r;
+  if (!aabb_keep64(t.k, lo, hi, c64, __dmul_rn(r64, r64))) return 0;
+  return fast ? 2 : 3;
+}
+
+// K1: classify, per-leaf histogram (warp-aggregated), exact-path list
 template <typename InT>
 __global__ void __launch_bounds__(256) k_bin_count(BinArgs a) {
   __shared__ float sT[kSmemNodes];
@@ -98,43 +160,62 @@ __global__ void __launch_bounds__(256) k_bin_count(BinArgs a) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   const int64_t n_pad = (a.n + 31) & ~int64_t(31);
   for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n_pad; q += stride) {
-    const SphereClass sc = classify_sphere<InT>(t, sT, n_smem, a, q, check);
-    const bool scan = sc.status == 2;
+    int status = 0, leaf = -1;
+    bool valid = q < a.n;
+    if (valid && a.mask) valid = a.mask[q] != 0;
+    if (valid) {
+      if constexpr (std::is_same<InT, float>::value) {
+        status = classify_f32(t, sT, n_smem, a, q, check, leaf);
+      } else {
+        const SphereClass sc = classify_sphere<InT>(t, sT, n_smem, a, q, check);
+        status = sc.status;
+        leaf = int(sc.leaf);
+      }
+    }
+    const bool scan = status == 2;
+    if (q < a.n) a.leafid[q] = scan ? leaf : -1;
     const unsigned act = __ballot_sync(0xffffffffu, scan);
     if (scan) {
-      const unsigned peers = __match_any_sync(act, unsigned(sc.leaf));
-      if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(a.counts + sc.leaf, __popc(peers));
+      const unsigned peers = __match_any_sync(act, unsigned(leaf));
+      if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(a.counts + leaf, __popc(peers));
     }
-    if (sc.status == 3) {
+    if (status == 3) {
       const unsigned i = atomicAdd(a.slow_n, 1u);
-      a.slow[i] = make_int2(int(q), int(sc.leaf));
+      a.slow[i] = make_int2(int(q), leaf);
     }
   }
 }
 
+// K3: scatter {c, r} records of binned spheres into leaf order
 template <typename InT>
 __global__ void __launch_bounds__(256) k_bin_scatter(BinArgs a) {
-  __shared__ float sT[kSmemNodes];
-  const DevTree& t = a.t;
-  const int n_smem = int(t.n - 1 < kSmemNodes ? t.n - 1 : kSmemNodes);
-  for (int i = threadIdx.x; i < n_smem; i += blockDim.x) sT[i] = t.T[i];
-  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   const int64_t n_pad = (a.n + 31) & ~int64_t(31);
+  const int k = a.t.k;
   for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n_pad; q += stride) {
-    const SphereClass sc = classify_sphere<InT>(t, sT, n_smem, a, q, false);
-    const bool scan = sc.status == 2;
+    const int leaf = q < a.n ? a.leafid[q] : -1;
+    const bool scan = leaf >= 0;
     const unsigned act = __ballot_sync(0xffffffffu, scan);
     if (scan) {
-      const unsigned peers = __match_any_sync(act, unsigned(sc.leaf));
+      float c[3] = {0.f, 0.f, 0.f}, r;
+      if constexpr (std::is_same<InT, float>::value) {
+        const float* cf = static_cast<const float*>(a.centers);
+        for (int d = 0; d < k; ++d) c[d] = __ldg(cf + q * k + d);
+        r = __ldg(static_cast<const float*>(a.radii) + q);
+      } else {  // binned float64 inputs are exact fp32 values
+        const double* cd = static_cast<const double*>(a.centers);
+        for (int d = 0; d < k; ++d) c[d] = float(__ldg(cd + q * k + d));
+        r = float(__ldg(static_cast<const double*>(a.radii) + q));
+      }
+      const unsigned peers = __match_any_sync(act, unsigned(leaf));
       const int leader = __ffs(peers) - 1;
       unsigned base = 0;
-      if (lane == leader) base = atomicAdd(a.cursor + sc.leaf, __popc(peers));
+      if (lane == leader) base = atomicAdd(a.cursor + leaf, __popc(peers));
       base = __shfl_sync(peers, base, leader);
       const unsigned rank = __popc(peers & ((1u << lane) - 1u));
-      const int64_t pos = int64_t(a.start[sc.leaf]) + base + rank;
-      a.rec[pos] = make_float4(sc.cx, sc.cy, sc.cz, sc.rf);
+      const int64_t pos = int64_t(a.start[leaf]) + base + rank;
+      a.rec[pos] = make_float4(c[0], c[1], c[2], r);
       a.rid[pos] = int(q);
     }
   }
@@ -190,9 +271,7 @@ __device__ __forceinline__ float okey_inv(uint32_t u) {
 struct __align__(16) SmemBinned {
   ulonglong2 A[kChunk];  // {bx,bx}, {by,by}
   ulonglong2 B[kChunk];  // {bz,bz}, {w,w}
-  uint32_t minkey[kTS];
-  float thr[kTS];
-  float band[kTS];
+  uint32_t minkey[kTS];  // per sphere: combined min over phases (P > 1)
   uint32_t hitmask[kTS / kS];
   int amb[kTS];
   int n_amb;
@@ -200,14 +279,19 @@ struct __align__(16) SmemBinned {
   int flag;
 };
 
-__global__ void __launch_bounds__(kBT) k_binned_scan(BinArgs a) {
+__global__ void __launch_bounds__(kBT, 5) k_binned_scan(BinArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SmemBinned& S = *reinterpret_cast<SmemBinned*>(smem_raw);
+  ulonglong2* const sA = S.A;
+  ulonglong2* const sB = S.B;
   const DevTree& t = a.t;
   const int tid = threadIdx.x;
   const float INF = __int_as_float(0x7f800000);
   while (true) {
-    if (tid == 0) S.tile = int(atomicAdd(a.tile_ctr, 1u));
+    if (tid == 0) {
+      S.tile = int(atomicAdd(a.tile_ctr, 1u));
+      S.n_amb = 0;
+    }
     __syncthreads();
     const int tile = S.tile;
     if (tile >= int(*a.n_tiles)) break;
@@ -226,20 +310,24 @@ __global__ void __launch_bounds__(kBT) k_binned_scan(BinArgs a) {
     const bool active = tid < nslot * P;
     const int slot = tid % nslot;
     const int ph = tid / nslot;
+    const bool owner = active && ph == 0;
 
     // this thread's spheres, in local coordinates relative to the set origin
     unsigned long long Kx[kS / 2], Ky[kS / 2], Kz[kS / 2];
     float thr[kS], band[kS], mn[kS];
-    bool real[kS];
+    int rid[kS];
+    uint32_t my_real = 0;
 #pragma unroll
     for (int i = 0; i < kS; i += 2) {
       float kx[2], ky[2], kz[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int s = slot * kS + i + h;
-        real[i + h] = active && s < cnt;
-        if (real[i + h]) {
+        rid[i + h] = -1;
+        if (active && s < cnt) {
+          my_real |= 1u << (i + h);
           const float4 rc = a.rec[s0 + s];
+          if (owner) rid[i + h] = a.rid[s0 + s];
           const float ax = rc.x - org.x, ay = rc.y - org.y, az = rc.z - org.z;
           const float aa = fmaf(az, az, fmaf(ay, ay, ax * ax));
           const float r2 = rc.w * rc.w;
@@ -259,27 +347,15 @@ __global__ void __launch_bounds__(kBT) k_binned_scan(BinArgs a) {
       Ky[i / 2] = pack2(ky[0], ky[1]);
       Kz[i / 2] = pack2(kz[0], kz[1]);
     }
-    for (int s = tid; s < kTS; s += kBT) S.minkey[s] = 0xffffffffu;
-    for (int s = tid; s < kTS / kS; s += kBT) S.hitmask[s] = 0;
-    if (active && ph == 0) {
-#pragma unroll
-      for (int i = 0; i < kS; ++i) {
-        const int s = slot * kS + i;
-        if (s < cnt) {
-          S.thr[s] = thr[i];
-          S.band[s] = band[i];
-        }
-      }
-    }
-    uint32_t my_real = 0;
-#pragma unroll
-    for (int i = 0; i < kS; ++i) my_real |= uint32_t(real[i]) << i;
-    bool done = !active || my_real == 0;
+    if (P > 1)
+      for (int s = tid; s < nslot * kS; s += kBT) S.minkey[s] = 0xffffffffu;
+    for (int s = tid; s < nslot; s += kBT) S.hitmask[s] = 0;
+    bool done = my_real == 0;
 
     for (uint32_t c0 = 0; c0 < m; c0 += kChunk) {
       const uint32_t len = min(uint32_t(kChunk), m - c0);
       const uint32_t len2 = (len + 1u) & ~1u;
-      __syncthreads();  // previous chunk fully consumed
+      __syncthreads();  // previous chunk fully consumed, inits visible
       for (uint32_t i = tid; i < len2; i += kBT) {
         const uint32_t g = c0 + i;
         float bx = 0.f, by = 0.f, bz = 0.f, w = INF;
@@ -292,16 +368,20 @@ __global__ void __launch_bounds__(kBT) k_binned_scan(BinArgs a) {
             w = fmaf(bz, bz, fmaf(by, by, bx * bx));
           }
         }
-        S.A[i] = make_ulonglong2(pack2(bx, bx), pack2(by, by));
-        S.B[i] = make_ulonglong2(pack2(bz, bz), pack2(w, w));
+        sA[i] = make_ulonglong2(pack2(bx, bx), pack2(by, by));
+        sB[i] = make_ulonglong2(pack2(bz, bz), pack2(w, w));
       }
       __syncthreads();
       if (!done) {
         const int npairs = int(len2 / 2);
+        const ulonglong2* pa = sA + 2 * ph;
+        const ulonglong2* pb = sB + 2 * ph;
+        const int step = 2 * P;
         int it = 0;
-        for (int u = ph; u < npairs; u += P) {
-          const ulonglong2 A0 = S.A[2 * u], B0 = S.B[2 * u];
-          const ulonglong2 A1 = S.A[2 * u + 1], B1 = S.B[2 * u + 1];
+#pragma unroll 2
+        for (int u = ph; u < npairs; u += P, pa += step, pb += step) {
+          const ulonglong2 A0 = pa[0], B0 = pb[0];
+          const ulonglong2 A1 = pa[1], B1 = pb[1];
 #pragma unroll
           for (int q = 0; q < kS / 2; ++q) {
             unsigned long long t0 = ffma2(A0.x, Kx[q], B0.y);
@@ -316,38 +396,44 @@ __global__ void __launch_bounds__(kBT) k_binned_scan(BinArgs a) {
             mn[2 * q] = fmin3(mn[2 * q], t0l, t1l);
             mn[2 * q + 1] = fmin3(mn[2 * q + 1], t0h, t1h);
           }
-          if ((++it & 7) == 0) {
+          if ((++it & 15) == 0) {
             uint32_t h = 0;
 #pragma unroll
             for (int i = 0; i < kS; ++i) h |= uint32_t(mn[i] <= thr[i] - band[i]) << i;
-            if (h) atomicOr(&S.hitmask[slot], h);
-            const uint32_t seen = *reinterpret_cast<volatile uint32_t*>(&S.hitmask[slot]);
-            if (((seen | h) & my_real) == my_real) break;
+            if (P > 1) {
+              if (h) atomicOr(&S.hitmask[slot], h);
+              h |= *reinterpret_cast<volatile uint32_t*>(&S.hitmask[slot]);
+            }
+            if ((h & my_real) == my_real) break;
           }
         }
         uint32_t h = 0;
 #pragma unroll
         for (int i = 0; i < kS; ++i) h |= uint32_t(mn[i] <= thr[i] - band[i]) << i;
         if (h) atomicOr(&S.hitmask[slot], h);
-        if (((S.hitmask[slot] | h) & my_real) == my_real) done = true;
+        if (P > 1) h |= *reinterpret_cast<volatile uint32_t*>(&S.hitmask[slot]);
+        if ((h & my_real) == my_real) done = true;
       }
     }
     // combine the phases' minima
-    if (active) {
+    if (P > 1 && active) {
 #pragma unroll
       for (int i = 0; i < kS; ++i)
-        if (real[i]) atomicMin(&S.minkey[slot * kS + i], okey(mn[i]));
+        if ((my_real >> i) & 1u) atomicMin(&S.minkey[slot * kS + i], okey(mn[i]));
     }
-    if (tid == 0) S.n_amb = 0;
     __syncthreads();
-    for (int s = tid; s < cnt; s += kBT) {
-      const bool hit_flag = (S.hitmask[s / kS] >> (s % kS)) & 1u;
-      const float mv = okey_inv(S.minkey[s]);
-      const float th = S.thr[s], bd = S.band[s];
-      if (hit_flag || mv <= th - bd) {
-        a.verdict[a.rid[s0 + s]] = 1;
-      } else if (!(mv > th + bd)) {
-        S.amb[atomicAdd(&S.n_amb, 1)] = s;
+    // decision by each slot's owner thread
+    if (owner) {
+      const uint32_t hm = S.hitmask[slot];
+#pragma unroll
+      for (int i = 0; i < kS; ++i) {
+        if (!((my_real >> i) & 1u)) continue;
+        const float mv = P > 1 ? okey_inv(S.minkey[slot * kS + i]) : mn[i];
+        if (((hm >> i) & 1u) || mv <= thr[i] - band[i]) {
+          a.verdict[rid[i]] = 1;
+        } else if (!(mv > thr[i] + band[i])) {
+          S.amb[atomicAdd(&S.n_amb, 1)] = slot * kS + i;
+        }
       }
     }
     __syncthreads();
@@ -474,9 +560,17 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.rid = A.get<int>(n);
   a.verdict = A.get<uint8_t>(n + 8);
   a.slow = A.get<int2>(n);
+  a.leafid = A.get<int>(n);
   if (!ctr || !a.counts || !a.cursor || !a.start || !tcount || !tstart || !a.tiles || !a.rec ||
-      !a.rid || !a.verdict || !a.slow)
+      !a.rid || !a.verdict || !a.slow || !a.leafid)
     return fail(CAPT_ENOMEM, "binned scratch allocation");
+  {
+    float lo = float(t.r_min), hi = float(t.r_max);
+    if (double(lo) < t.r_min) lo = nextafterf(lo, INFINITY);
+    if (double(hi) > t.r_max) hi = nextafterf(hi, -INFINITY);
+    a.rlo_f = lo;
+    a.rhi_f = hi;
+  }
   a.slow_n = ctr;
   a.n_tiles = ctr + 1;
   a.tile_ctr = ctr + 2;

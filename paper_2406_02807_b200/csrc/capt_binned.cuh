@@ -26,6 +26,8 @@ struct BinArgs {
   uint32_t* tile_ctr;
   uint32_t* n_refined;
   unsigned long long* first_bad;
+  int* leafid;        // per sphere: leaf if binned, else -1
+  float rlo_f, rhi_f; // fp32 images of the double band edges
 };
 
 bool binned_preferred(const DevTree& t, int64_t n, uint32_t flags);
