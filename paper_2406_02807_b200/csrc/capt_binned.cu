@@ -8,7 +8,7 @@
 //                     histogram; spheres needing the exact path go to a list
 //   K2 (CUB scans)    per-leaf start offsets and tile counts
 //   K3 k_bin_scatter  recompute the leaf, scatter a float4 {c, r} record and
-//                     the sphere id into leaf order (warp-aggregated cursor)
+//                     the sphere id into leaf order (slot = start + K1 ticket)
 //   K4 k_make_tiles   (leaf, chunk of <= 1024 spheres) work items
 //   K5 k_binned_scan  persistent CTAs pull tiles from an atomic counter; the
 //                     leaf's set is staged once into shared memory in local
@@ -148,6 +148,28 @@ __device__ __forceinline__ int classify_f32(const DevTree& t, const float* sT, i
   return fast ? 2 : 3;
 }
 
+// Warp-collective: per-leaf histogram with a ticket (rank within the leaf)
+// per binned sphere (warp-aggregated atomics), exact-path list.
+__device__ __forceinline__ void record_bin(const BinArgs& a, int64_t q, int status, int leaf) {
+  const bool scan = status == 2;
+  const unsigned act = __ballot_sync(0xffffffffu, scan);
+  int ticket = 0;
+  if (scan) {
+    const int lane = threadIdx.x & 31;
+    const unsigned peers = __match_any_sync(act, unsigned(leaf));
+    const int leader = __ffs(peers) - 1;
+    unsigned b = 0;
+    if (lane == leader) b = atomicAdd(a.counts + leaf, __popc(peers));
+    b = __shfl_sync(peers, b, leader);
+    ticket = int(b + __popc(peers & ((1u << lane) - 1u)));
+  }
+  if (q < a.n) a.slot[q] = make_int2(scan ? leaf : -1, ticket);
+  if (status == 3) {
+    const unsigned i = atomicAdd(a.slow_n, 1u);
+    a.slow[i] = make_int2(int(q), leaf);
+  }
+}
+
 // K1: classify, per-leaf histogram (warp-aggregated), exact-path list
 template <typename InT>
 __global__ void __launch_bounds__(256) k_bin_count(BinArgs a) {
@@ -172,49 +194,139 @@ __global__ void __launch_bounds__(256) k_bin_count(BinArgs a) {
         leaf = int(sc.leaf);
       }
     }
-    const bool scan = status == 2;
-    if (q < a.n) a.leafid[q] = scan ? leaf : -1;
-    const unsigned act = __ballot_sync(0xffffffffu, scan);
-    if (scan) {
-      const unsigned peers = __match_any_sync(act, unsigned(leaf));
-      if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(a.counts + leaf, __popc(peers));
+    record_bin(a, q, status, leaf);
+  }
+}
+
+// K1 specialised for k = 3, fp32 input: V spheres per thread in flight
+// (independent descents interleave), the top 13 levels of T in shared memory.
+constexpr int kSmemNodes3 = 8191;
+template <int V>
+__global__ void __launch_bounds__(256) k_bin_count3(BinArgs a) {
+  __shared__ float sT[kSmemNodes3];
+  const DevTree& t = a.t;
+  const int n_smem = int(t.n - 1 < kSmemNodes3 ? t.n - 1 : kSmemNodes3);
+  for (int i = threadIdx.x; i < n_smem; i += blockDim.x) sT[i] = t.T[i];
+  __syncthreads();
+  const bool check = a.flags & CAPT_CHECK_RADII;
+  const bool prefilter = a.flags & CAPT_PREFILTER;
+  const float* cf = static_cast<const float*>(a.centers);
+  const float* rf = static_cast<const float*>(a.radii);
+  const int dsm = t.depth < 13 ? t.depth : 13;
+  const int nl1 = int(t.n - 1);
+  const int64_t n_pad = (a.n + 31) & ~int64_t(31);
+  const int64_t per_iter = int64_t(gridDim.x) * blockDim.x * V;
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x * V; base < n_pad; base += per_iter) {
+    float cx[V], cy[V], cz[V], r[V];
+    bool valid[V];
+    int i[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int64_t q = base + int64_t(v) * blockDim.x + threadIdx.x;
+      valid[v] = q < a.n;
+      if (valid[v] && a.mask) valid[v] = a.mask[q] != 0;
+      cx[v] = cy[v] = cz[v] = r[v] = 0.f;
+      if (valid[v]) {
+        cx[v] = __ldg(cf + 3 * q);
+        cy[v] = __ldg(cf + 3 * q + 1);
+        cz[v] = __ldg(cf + 3 * q + 2);
+        r[v] = __ldg(rf + q);
+        if (check && (r[v] < a.rlo_f || r[v] > a.rhi_f))
+          atomicMin(a.first_bad, static_cast<unsigned long long>(q));
+      }
+      i[v] = 0;
     }
-    if (status == 3) {
-      const unsigned i = atomicAdd(a.slow_n, 1u);
-      a.slow[i] = make_int2(int(q), leaf);
+    int s = 0;
+    for (; s + 3 <= dsm; s += 3) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        int j = i[v];
+        j = 2 * j + 1 + (cx[v] > sT[j] ? 1 : 0);
+        j = 2 * j + 1 + (cy[v] > sT[j] ? 1 : 0);
+        j = 2 * j + 1 + (cz[v] > sT[j] ? 1 : 0);
+        i[v] = j;
+      }
+    }
+    for (; s < t.depth; ++s) {
+      const int ax = s % 3;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const float c = ax == 0 ? cx[v] : (ax == 1 ? cy[v] : cz[v]);
+        const float tv = s < dsm ? sT[i[v]] : __ldg(t.T + i[v]);
+        i[v] = 2 * i[v] + 1 + (c > tv ? 1 : 0);
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int64_t q = base + int64_t(v) * blockDim.x + threadIdx.x;
+      const int leaf = i[v] - nl1;
+      int status = 0;
+      if (valid[v]) {
+        const bool cfin = isfinite(cx[v]) && isfinite(cy[v]) && isfinite(cz[v]);
+        const float r2 = r[v] * r[v];
+        const bool fast = cfin && r2 >= kR2Min && r2 <= kR2Max;
+        // non-finite centre with a finite radius never collides (float64 r^2 is finite)
+        status = fast ? 2 : ((!cfin && isfinite(r[v])) ? 0 : 3);
+        {
+          if (status && prefilter) {
+            const float4 lo = __ldg(t.box + 2 * leaf);
+            const float4 hi = __ldg(t.box + 2 * leaf + 1);
+            bool exact = !fast;
+            if (fast) {
+              const float rx = fmaxf(fmaxf(lo.x - cx[v], 0.f), cx[v] - hi.x);
+              const float ry = fmaxf(fmaxf(lo.y - cy[v], 0.f), cy[v] - hi.y);
+              const float rz = fmaxf(fmaxf(lo.z - cz[v], 0.f), cz[v] - hi.z);
+              const float ss = fmaf(rz, rz, fmaf(ry, ry, rx * rx));
+              if (ss > r2 * (1.0f + kTau)) status = 0;
+              else if (!(ss < r2 * (1.0f - kTau))) exact = true;
+            }
+            if (status && exact) {
+              const double c64[3] = {cx[v], cy[v], cz[v]};
+              const double r64 = r[v];
+              if (!aabb_keep64(3, lo, hi, c64, __dmul_rn(r64, r64))) status = 0;
+            }
+          }
+        }
+      }
+      record_bin(a, q, status, leaf);
     }
   }
 }
 
-// K3: scatter {c, r} records of binned spheres into leaf order
-template <typename InT>
+// K3: scatter {c, r} records of binned spheres into leaf order (no atomics:
+// the slot is start[leaf] + the ticket drawn in K1)
+template <typename InT, int V>
 __global__ void __launch_bounds__(256) k_bin_scatter(BinArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  const int64_t n_pad = (a.n + 31) & ~int64_t(31);
   const int k = a.t.k;
-  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n_pad; q += stride) {
-    const int leaf = q < a.n ? a.leafid[q] : -1;
-    const bool scan = leaf >= 0;
-    const unsigned act = __ballot_sync(0xffffffffu, scan);
-    if (scan) {
+  const int64_t per_iter = int64_t(gridDim.x) * blockDim.x * V;
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x * V; base < a.n; base += per_iter) {
+    int2 sl[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int64_t q = base + int64_t(v) * blockDim.x + threadIdx.x;
+      sl[v] = q < a.n ? a.slot[q] : make_int2(-1, 0);
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      if (sl[v].x < 0) continue;
+      const int64_t q = base + int64_t(v) * blockDim.x + threadIdx.x;
       float c[3] = {0.f, 0.f, 0.f}, r;
       if constexpr (std::is_same<InT, float>::value) {
         const float* cf = static_cast<const float*>(a.centers);
-        for (int d = 0; d < k; ++d) c[d] = __ldg(cf + q * k + d);
+        if (k == 3) {
+          c[0] = __ldg(cf + 3 * q);
+          c[1] = __ldg(cf + 3 * q + 1);
+          c[2] = __ldg(cf + 3 * q + 2);
+        } else {
+          for (int d = 0; d < k; ++d) c[d] = __ldg(cf + q * k + d);
+        }
         r = __ldg(static_cast<const float*>(a.radii) + q);
       } else {  // binned float64 inputs are exact fp32 values
         const double* cd = static_cast<const double*>(a.centers);
         for (int d = 0; d < k; ++d) c[d] = float(__ldg(cd + q * k + d));
         r = float(__ldg(static_cast<const double*>(a.radii) + q));
       }
-      const unsigned peers = __match_any_sync(act, unsigned(leaf));
-      const int leader = __ffs(peers) - 1;
-      unsigned base = 0;
-      if (lane == leader) base = atomicAdd(a.cursor + leaf, __popc(peers));
-      base = __shfl_sync(peers, base, leader);
-      const unsigned rank = __popc(peers & ((1u << lane) - 1u));
-      const int64_t pos = int64_t(a.start[leaf]) + base + rank;
+      const int64_t pos = int64_t(__ldg(a.start + sl[v].x)) + sl[v].y;
       a.rec[pos] = make_float4(c[0], c[1], c[2], r);
       a.rid[pos] = int(q);
     }
@@ -551,7 +663,6 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   const int64_t nl = t.n;
   uint32_t* ctr = A.get<uint32_t>(4);  // slow_n, n_tiles, tile_ctr, n_refined
   a.counts = A.get<uint32_t>(nl);
-  a.cursor = A.get<uint32_t>(nl);
   a.start = A.get<uint32_t>(nl);
   uint32_t* tcount = A.get<uint32_t>(nl);
   uint32_t* tstart = A.get<uint32_t>(nl);
@@ -560,9 +671,9 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.rid = A.get<int>(n);
   a.verdict = A.get<uint8_t>(n + 8);
   a.slow = A.get<int2>(n);
-  a.leafid = A.get<int>(n);
-  if (!ctr || !a.counts || !a.cursor || !a.start || !tcount || !tstart || !a.tiles || !a.rec ||
-      !a.rid || !a.verdict || !a.slow || !a.leafid)
+  a.slot = A.get<int2>(n);
+  if (!ctr || !a.counts || !a.start || !tcount || !tstart || !a.tiles || !a.rec || !a.rid ||
+      !a.verdict || !a.slow || !a.slot)
     return fail(CAPT_ENOMEM, "binned scratch allocation");
   {
     float lo = float(t.r_min), hi = float(t.r_max);
@@ -577,11 +688,13 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.n_refined = ctr + 3;
   CAPT_CUDA(cudaMemsetAsync(ctr, 0, 16, s));
   CAPT_CUDA(cudaMemsetAsync(a.counts, 0, 4 * nl, s));
-  CAPT_CUDA(cudaMemsetAsync(a.cursor, 0, 4 * nl, s));
   CAPT_CUDA(cudaMemsetAsync(a.verdict, 0, n + 8, s));
   const bool f64 = flags & CAPT_INPUT_F64;
   const int G = grid_for(n, 256, 8);
+  constexpr int V = 4;
+  const int G4 = grid_for((n + V - 1) / V, 256, 8);
   if (f64) k_bin_count<double><<<G, 256, 0, s>>>(a);
+  else if (t.k == 3) k_bin_count3<V><<<G4, 256, 0, s>>>(a);
   else k_bin_count<float><<<G, 256, 0, s>>>(a);
   // per-leaf starts and tiles
   size_t tb = 0;
@@ -593,8 +706,8 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   k_tile_counts<<<Gl, 256, 0, s>>>(nl, a.counts, tcount);
   CAPT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, tcount, tstart, nl, s));
   k_make_tiles<<<Gl, 256, 0, s>>>(nl, tcount, tstart, a.tiles, a.n_tiles);
-  if (f64) k_bin_scatter<double><<<G, 256, 0, s>>>(a);
-  else k_bin_scatter<float><<<G, 256, 0, s>>>(a);
+  if (f64) k_bin_scatter<double, V><<<G4, 256, 0, s>>>(a);
+  else k_bin_scatter<float, V><<<G4, 256, 0, s>>>(a);
   static int sms = 0, occ = 0;
   if (!sms) {
     int dev = 0;

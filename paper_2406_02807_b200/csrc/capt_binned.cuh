@@ -14,7 +14,6 @@ struct BinArgs {
   const uint8_t* mask;
   uint32_t flags;
   uint32_t* counts;   // per leaf: AABB-passing spheres
-  uint32_t* cursor;   // per leaf: scatter cursor
   uint32_t* start;    // per leaf: first binned slot
   int2* tiles;        // (leaf, chunk)
   float4* rec;        // binned {cx, cy, cz, r}
@@ -26,7 +25,7 @@ struct BinArgs {
   uint32_t* tile_ctr;
   uint32_t* n_refined;
   unsigned long long* first_bad;
-  int* leafid;        // per sphere: leaf if binned, else -1
+  int2* slot;         // per sphere: (leaf, rank within leaf) if binned, else (-1, 0)
   float rlo_f, rhi_f; // fp32 images of the double band edges
 };
 
