@@ -299,17 +299,23 @@ template <typename InT, int V>
 __global__ void __launch_bounds__(256) k_bin_scatter(BinArgs a) {
   const int k = a.t.k;
   const int64_t per_iter = int64_t(gridDim.x) * blockDim.x * V;
+  // every load of the V spheres is issued before any store (memory-level
+  // parallelism: this kernel is latency-bound otherwise)
   for (int64_t base = int64_t(blockIdx.x) * blockDim.x * V; base < a.n; base += per_iter) {
     int2 sl[V];
+    int64_t qv[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      const int64_t q = base + int64_t(v) * blockDim.x + threadIdx.x;
-      sl[v] = q < a.n ? a.slot[q] : make_int2(-1, 0);
+      qv[v] = base + int64_t(v) * blockDim.x + threadIdx.x;
+      sl[v] = qv[v] < a.n ? __ldcs(a.slot + qv[v]) : make_int2(-1, 0);
     }
+    uint32_t st[V];
+    float4 rc[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      if (sl[v].x < 0) continue;
-      const int64_t q = base + int64_t(v) * blockDim.x + threadIdx.x;
+      const bool on = sl[v].x >= 0;
+      const int64_t q = on ? qv[v] : 0;
+      st[v] = __ldg(a.start + (on ? sl[v].x : 0));
       float c[3] = {0.f, 0.f, 0.f}, r;
       if constexpr (std::is_same<InT, float>::value) {
         const float* cf = static_cast<const float*>(a.centers);
@@ -326,9 +332,15 @@ __global__ void __launch_bounds__(256) k_bin_scatter(BinArgs a) {
         for (int d = 0; d < k; ++d) c[d] = float(__ldg(cd + q * k + d));
         r = float(__ldg(static_cast<const double*>(a.radii) + q));
       }
-      const int64_t pos = int64_t(__ldg(a.start + sl[v].x)) + sl[v].y;
-      a.rec[pos] = make_float4(c[0], c[1], c[2], r);
-      a.rid[pos] = int(q);
+      rc[v] = make_float4(c[0], c[1], c[2], r);
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      if (sl[v].x >= 0) {
+        const int64_t pos = int64_t(st[v]) + sl[v].y;
+        a.rec[pos] = rc[v];
+        a.rid[pos] = int(qv[v]);
+      }
     }
   }
 }
@@ -383,13 +395,158 @@ __device__ __forceinline__ float okey_inv(uint32_t u) {
 struct __align__(16) SmemBinned {
   ulonglong2 A[kChunk];  // {bx,bx}, {by,by}
   ulonglong2 B[kChunk];  // {bz,bz}, {w,w}
-  uint32_t minkey[kTS];  // per sphere: combined min over phases (P > 1)
+  uint32_t minkey[kTS];  // per sphere: running min over phases / passes
   uint32_t hitmask[kTS / kS];
-  int amb[kTS];
-  int n_amb;
+  int list[kTS];         // spheres still unresolved after the probe pass
+  int n_list;
   int tile;
-  int flag;
 };
+
+// Eight spheres of one thread in local coordinates of the set origin o:
+// t = |b|^2 - 2 a.b compared with thr = r^2 - |a|^2 (a = c - o, b = p - o).
+struct Spheres8 {
+  unsigned long long Kx[kS / 2], Ky[kS / 2], Kz[kS / 2];
+  float thr[kS], band[kS], mn[kS];
+  int sidx[kS];
+  uint32_t real;
+};
+
+// list == nullptr: tile-local spheres slot*kS + i; else list[slot*kS + i].
+// init_min: start from the min recorded in S.minkey (second pass).
+__device__ __forceinline__ void load_spheres(Spheres8& sp, const BinArgs& a, int64_t s0,
+                                             const float4 org, const int* list, int count,
+                                             int slot, bool active, const uint32_t* minkey) {
+  const float INF = __int_as_float(0x7f800000);
+  sp.real = 0;
+#pragma unroll
+  for (int i = 0; i < kS; i += 2) {
+    float kx[2], ky[2], kz[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = slot * kS + i + h;
+      sp.sidx[i + h] = -1;
+      sp.mn[i + h] = INF;
+      if (active && e < count) {
+        const int sl = list ? list[e] : e;
+        sp.sidx[i + h] = sl;
+        sp.real |= 1u << (i + h);
+        const float4 rc = a.rec[s0 + sl];
+        const float ax = rc.x - org.x, ay = rc.y - org.y, az = rc.z - org.z;
+        const float aa = fmaf(az, az, fmaf(ay, ay, ax * ax));
+        const float r2 = rc.w * rc.w;
+        kx[h] = -2.f * ax;
+        ky[h] = -2.f * ay;
+        kz[h] = -2.f * az;
+        sp.thr[i + h] = r2 - aa;
+        sp.band[i + h] = kBand * (aa + org.w + r2);
+        if (minkey) sp.mn[i + h] = okey_inv(minkey[sl]);
+      } else {
+        kx[h] = ky[h] = kz[h] = 0.f;
+        sp.thr[i + h] = -INF;
+        sp.band[i + h] = 0.f;
+      }
+    }
+    sp.Kx[i / 2] = pack2(kx[0], kx[1]);
+    sp.Ky[i / 2] = pack2(ky[0], ky[1]);
+    sp.Kz[i / 2] = pack2(kz[0], kz[1]);
+  }
+}
+
+__device__ __forceinline__ uint32_t definite_hits(const Spheres8& sp) {
+  uint32_t h = 0;
+#pragma unroll
+  for (int i = 0; i < kS; ++i) h |= uint32_t(sp.mn[i] <= sp.thr[i] - sp.band[i]) << i;
+  return h & sp.real;
+}
+
+// One point pair (2u, 2u+1) against the thread's 8 spheres: 12 FFMA2 + 8 FMNMX3.
+__device__ __forceinline__ void test_pair(Spheres8& sp, const ulonglong2* sA, const ulonglong2* sB,
+                                          int u) {
+  const ulonglong2 A0 = sA[2 * u], B0 = sB[2 * u];
+  const ulonglong2 A1 = sA[2 * u + 1], B1 = sB[2 * u + 1];
+#pragma unroll
+  for (int q = 0; q < kS / 2; ++q) {
+    unsigned long long t0 = ffma2(A0.x, sp.Kx[q], B0.y);
+    t0 = ffma2(A0.y, sp.Ky[q], t0);
+    t0 = ffma2(B0.x, sp.Kz[q], t0);
+    unsigned long long t1 = ffma2(A1.x, sp.Kx[q], B1.y);
+    t1 = ffma2(A1.y, sp.Ky[q], t1);
+    t1 = ffma2(B1.x, sp.Kz[q], t1);
+    float t0l, t0h, t1l, t1h;
+    unpack2(t0, t0l, t0h);
+    unpack2(t1, t1l, t1h);
+    sp.mn[2 * q] = fmin3(sp.mn[2 * q], t0l, t1l);
+    sp.mn[2 * q + 1] = fmin3(sp.mn[2 * q + 1], t0h, t1h);
+  }
+}
+
+// Pairs u = 4g + o for o in [OB, OE), g = ph, ph + P, ...  Stops early once
+// every sphere of the slot is a definite hit (hitmask shared by the phases).
+template <int OB, int OE>
+__device__ __forceinline__ void scan_pairs(Spheres8& sp, const ulonglong2* sA,
+                                           const ulonglong2* sB, int npairs, int ph, int P,
+                                           uint32_t* hitmask) {
+  const int ngroups = (npairs + 3) / 4;
+  int it = 0;
+  for (int g = ph; g < ngroups; g += P) {
+#pragma unroll
+    for (int o = OB; o < OE; ++o) {
+      const int u = 4 * g + o;
+      if (u < npairs) test_pair(sp, sA, sB, u);
+    }
+    if ((++it & 7) == 0) {
+      uint32_t h = definite_hits(sp);
+      if (P > 1) {
+        if (h) atomicOr(hitmask, h);
+        h |= *reinterpret_cast<volatile uint32_t*>(hitmask);
+      }
+      if ((h & sp.real) == sp.real) break;
+    }
+  }
+  const uint32_t h = definite_hits(sp);
+  if (h) atomicOr(hitmask, h);
+}
+
+__device__ __forceinline__ void stage_points(ulonglong2* sA, ulonglong2* sB, const float* xs,
+                                             uint32_t m4, uint32_t c0, uint32_t len,
+                                             uint32_t len2, const float4 org) {
+  const float INF = __int_as_float(0x7f800000);
+  for (uint32_t i = threadIdx.x; i < len2; i += kBT) {
+    const uint32_t g = c0 + i;
+    float bx = 0.f, by = 0.f, bz = 0.f, w = INF;
+    if (i < len) {
+      const float px = xs[g], py = xs[m4 + g], pz = xs[2 * m4 + g];
+      if (isfinite(px) && isfinite(py) && isfinite(pz)) {
+        bx = px - org.x;
+        by = py - org.y;
+        bz = pz - org.z;
+        w = fmaf(bz, bz, fmaf(by, by, bx * bx));
+      }
+    }
+    sA[i] = make_ulonglong2(pack2(bx, bx), pack2(by, by));
+    sB[i] = make_ulonglong2(pack2(bz, bz), pack2(w, w));
+  }
+}
+
+// Final decision for a slot's spheres: definite hit -> verdict byte, definite
+// miss -> nothing, inside the error band -> exact float64 path (k_slow).
+__device__ __forceinline__ void decide(const Spheres8& sp, const BinArgs& a, int64_t s0,
+                                       int64_t leaf, uint32_t hm, const uint32_t* minkey,
+                                       bool combined) {
+#pragma unroll
+  for (int i = 0; i < kS; ++i) {
+    if (!((sp.real >> i) & 1u)) continue;
+    const float mv = combined ? okey_inv(minkey[sp.sidx[i]]) : sp.mn[i];
+    const int q = a.rid[s0 + sp.sidx[i]];
+    if (((hm >> i) & 1u) || mv <= sp.thr[i] - sp.band[i]) {
+      a.verdict[q] = 1;
+    } else if (!(mv > sp.thr[i] + sp.band[i])) {
+      const unsigned j = atomicAdd(a.slow_n, 1u);
+      a.slow[j] = make_int2(q, int(leaf));
+      atomicAdd(a.n_refined, 1u);
+    }
+  }
+}
 
 __global__ void __launch_bounds__(kBT, 5) k_binned_scan(BinArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -398,11 +555,10 @@ __global__ void __launch_bounds__(kBT, 5) k_binned_scan(BinArgs a) {
   ulonglong2* const sB = S.B;
   const DevTree& t = a.t;
   const int tid = threadIdx.x;
-  const float INF = __int_as_float(0x7f800000);
   while (true) {
     if (tid == 0) {
       S.tile = int(atomicAdd(a.tile_ctr, 1u));
-      S.n_amb = 0;
+      S.n_list = 0;
     }
     __syncthreads();
     const int tile = S.tile;
@@ -417,165 +573,90 @@ __global__ void __launch_bounds__(kBT, 5) k_binned_scan(BinArgs a) {
     const uint32_t m4 = (m + 3u) & ~3u;
     const float* xs = reinterpret_cast<const float*>(t.data + st.x);
 
-    const int nslot = (cnt + kS - 1) / kS;
-    const int P = max(1, kBT / nslot);
-    const bool active = tid < nslot * P;
-    const int slot = tid % nslot;
-    const int ph = tid / nslot;
-    const bool owner = active && ph == 0;
+    int nslot = (cnt + kS - 1) / kS;
+    int P = max(1, kBT / nslot);
+    bool active = tid < nslot * P;
+    int slot = tid % nslot;
+    int ph = tid / nslot;
+    Spheres8 sp;
+    load_spheres(sp, a, s0, org, nullptr, cnt, slot, active, nullptr);
+    for (int e = tid; e < nslot * kS; e += kBT) S.minkey[e] = 0xffffffffu;
+    for (int e = tid; e < nslot; e += kBT) S.hitmask[e] = 0;
 
-    // this thread's spheres, in local coordinates relative to the set origin
-    unsigned long long Kx[kS / 2], Ky[kS / 2], Kz[kS / 2];
-    float thr[kS], band[kS], mn[kS];
-    int rid[kS];
-    uint32_t my_real = 0;
+    if (m <= kChunk) {
+      // ---- probe pass over every 4th point pair, then repack the spheres
+      //      that are still unresolved and scan the remaining pairs ----
+      const uint32_t len2 = (m + 1u) & ~1u;
+      stage_points(sA, sB, xs, m4, 0, m, len2, org);
+      __syncthreads();
+      const int npairs = int(len2 / 2);
+      if (sp.real) scan_pairs<0, 1>(sp, sA, sB, npairs, ph, P, &S.hitmask[slot]);
+      if (P > 1 && active) {
 #pragma unroll
-    for (int i = 0; i < kS; i += 2) {
-      float kx[2], ky[2], kz[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int s = slot * kS + i + h;
-        rid[i + h] = -1;
-        if (active && s < cnt) {
-          my_real |= 1u << (i + h);
-          const float4 rc = a.rec[s0 + s];
-          if (owner) rid[i + h] = a.rid[s0 + s];
-          const float ax = rc.x - org.x, ay = rc.y - org.y, az = rc.z - org.z;
-          const float aa = fmaf(az, az, fmaf(ay, ay, ax * ax));
-          const float r2 = rc.w * rc.w;
-          kx[h] = -2.f * ax;
-          ky[h] = -2.f * ay;
-          kz[h] = -2.f * az;
-          thr[i + h] = r2 - aa;
-          band[i + h] = kBand * (aa + org.w + r2);
-        } else {
-          kx[h] = ky[h] = kz[h] = 0.f;
-          thr[i + h] = -INF;
-          band[i + h] = 0.f;
-        }
-        mn[i + h] = INF;
+        for (int i = 0; i < kS; ++i)
+          if ((sp.real >> i) & 1u) atomicMin(&S.minkey[sp.sidx[i]], okey(sp.mn[i]));
       }
-      Kx[i / 2] = pack2(kx[0], kx[1]);
-      Ky[i / 2] = pack2(ky[0], ky[1]);
-      Kz[i / 2] = pack2(kz[0], kz[1]);
-    }
-    if (P > 1)
-      for (int s = tid; s < nslot * kS; s += kBT) S.minkey[s] = 0xffffffffu;
-    for (int s = tid; s < nslot; s += kBT) S.hitmask[s] = 0;
-    bool done = my_real == 0;
-
-    for (uint32_t c0 = 0; c0 < m; c0 += kChunk) {
-      const uint32_t len = min(uint32_t(kChunk), m - c0);
-      const uint32_t len2 = (len + 1u) & ~1u;
-      __syncthreads();  // previous chunk fully consumed, inits visible
-      for (uint32_t i = tid; i < len2; i += kBT) {
-        const uint32_t g = c0 + i;
-        float bx = 0.f, by = 0.f, bz = 0.f, w = INF;
-        if (i < len) {
-          const float px = xs[g], py = xs[m4 + g], pz = xs[2 * m4 + g];
-          if (isfinite(px) && isfinite(py) && isfinite(pz)) {
-            bx = px - org.x;
-            by = py - org.y;
-            bz = pz - org.z;
-            w = fmaf(bz, bz, fmaf(by, by, bx * bx));
+      __syncthreads();
+      if (active && ph == 0) {
+        const uint32_t hm = S.hitmask[slot];
+#pragma unroll
+        for (int i = 0; i < kS; ++i) {
+          if (!((sp.real >> i) & 1u)) continue;
+          const float mv = P > 1 ? okey_inv(S.minkey[sp.sidx[i]]) : sp.mn[i];
+          if (((hm >> i) & 1u) || mv <= sp.thr[i] - sp.band[i]) {
+            a.verdict[a.rid[s0 + sp.sidx[i]]] = 1;
+          } else {
+            S.minkey[sp.sidx[i]] = okey(mv);
+            S.list[atomicAdd(&S.n_list, 1)] = sp.sidx[i];
           }
         }
-        sA[i] = make_ulonglong2(pack2(bx, bx), pack2(by, by));
-        sB[i] = make_ulonglong2(pack2(bz, bz), pack2(w, w));
       }
       __syncthreads();
-      if (!done) {
-        const int npairs = int(len2 / 2);
-        const ulonglong2* pa = sA + 2 * ph;
-        const ulonglong2* pb = sB + 2 * ph;
-        const int step = 2 * P;
-        int it = 0;
-#pragma unroll 2
-        for (int u = ph; u < npairs; u += P, pa += step, pb += step) {
-          const ulonglong2 A0 = pa[0], B0 = pb[0];
-          const ulonglong2 A1 = pa[1], B1 = pb[1];
+      const int nu = S.n_list;
+      if (nu > 0) {
+        nslot = (nu + kS - 1) / kS;
+        P = max(1, kBT / nslot);
+        active = tid < nslot * P;
+        slot = tid % nslot;
+        ph = tid / nslot;
+        load_spheres(sp, a, s0, org, S.list, nu, slot, active, S.minkey);
+        __syncthreads();  // everyone has read the probe minima
+        for (int e = tid; e < nslot; e += kBT) S.hitmask[e] = 0;
+        __syncthreads();
+        if (sp.real) scan_pairs<1, 4>(sp, sA, sB, npairs, ph, P, &S.hitmask[slot]);
+        if (P > 1 && active) {
 #pragma unroll
-          for (int q = 0; q < kS / 2; ++q) {
-            unsigned long long t0 = ffma2(A0.x, Kx[q], B0.y);
-            t0 = ffma2(A0.y, Ky[q], t0);
-            t0 = ffma2(B0.x, Kz[q], t0);
-            unsigned long long t1 = ffma2(A1.x, Kx[q], B1.y);
-            t1 = ffma2(A1.y, Ky[q], t1);
-            t1 = ffma2(B1.x, Kz[q], t1);
-            float t0l, t0h, t1l, t1h;
-            unpack2(t0, t0l, t0h);
-            unpack2(t1, t1l, t1h);
-            mn[2 * q] = fmin3(mn[2 * q], t0l, t1l);
-            mn[2 * q + 1] = fmin3(mn[2 * q + 1], t0h, t1h);
-          }
-          if ((++it & 15) == 0) {
-            uint32_t h = 0;
-#pragma unroll
-            for (int i = 0; i < kS; ++i) h |= uint32_t(mn[i] <= thr[i] - band[i]) << i;
-            if (P > 1) {
-              if (h) atomicOr(&S.hitmask[slot], h);
-              h |= *reinterpret_cast<volatile uint32_t*>(&S.hitmask[slot]);
-            }
-            if ((h & my_real) == my_real) break;
-          }
+          for (int i = 0; i < kS; ++i)
+            if ((sp.real >> i) & 1u) atomicMin(&S.minkey[sp.sidx[i]], okey(sp.mn[i]));
         }
-        uint32_t h = 0;
-#pragma unroll
-        for (int i = 0; i < kS; ++i) h |= uint32_t(mn[i] <= thr[i] - band[i]) << i;
-        if (h) atomicOr(&S.hitmask[slot], h);
-        if (P > 1) h |= *reinterpret_cast<volatile uint32_t*>(&S.hitmask[slot]);
-        if ((h & my_real) == my_real) done = true;
+        __syncthreads();
+        if (active && ph == 0) decide(sp, a, s0, leaf, S.hitmask[slot], S.minkey, P > 1);
       }
-    }
-    // combine the phases' minima
-    if (P > 1 && active) {
-#pragma unroll
-      for (int i = 0; i < kS; ++i)
-        if ((my_real >> i) & 1u) atomicMin(&S.minkey[slot * kS + i], okey(mn[i]));
-    }
-    __syncthreads();
-    // decision by each slot's owner thread
-    if (owner) {
-      const uint32_t hm = S.hitmask[slot];
-#pragma unroll
-      for (int i = 0; i < kS; ++i) {
-        if (!((my_real >> i) & 1u)) continue;
-        const float mv = P > 1 ? okey_inv(S.minkey[slot * kS + i]) : mn[i];
-        if (((hm >> i) & 1u) || mv <= thr[i] - band[i]) {
-          a.verdict[rid[i]] = 1;
-        } else if (!(mv > thr[i] + band[i])) {
-          S.amb[atomicAdd(&S.n_amb, 1)] = slot * kS + i;
+    } else {
+      // ---- large sets: stream the set through shared memory in chunks ----
+      bool done = sp.real == 0;
+      for (uint32_t c0 = 0; c0 < m; c0 += kChunk) {
+        const uint32_t len = min(uint32_t(kChunk), m - c0);
+        const uint32_t len2 = (len + 1u) & ~1u;
+        __syncthreads();  // previous chunk consumed
+        stage_points(sA, sB, xs, m4, c0, len, len2, org);
+        __syncthreads();
+        if (!done) {
+          scan_pairs<0, 4>(sp, sA, sB, int(len2 / 2), ph, P, &S.hitmask[slot]);
+          uint32_t h = definite_hits(sp);
+          if (P > 1) h |= *reinterpret_cast<volatile uint32_t*>(&S.hitmask[slot]);
+          done = (h & sp.real) == sp.real;
         }
       }
-    }
-    __syncthreads();
-    // exact float64 rescan of ambiguous spheres (query.py:96-99 arithmetic)
-    const int n_amb = S.n_amb;
-    for (int i = 0; i < n_amb; ++i) {
-      const int s = S.amb[i];
-      const float4 rc = a.rec[s0 + s];
-      const double c[3] = {rc.x, rc.y, rc.z};
-      const double R = __dmul_rn(double(rc.w), double(rc.w));
-      if (tid == 0) S.flag = 0;
-      __syncthreads();
-      bool hit = false;
-      for (uint32_t j = tid; j < m; j += kBT) {
-        double sum = 0.0;
-        for (int d = 0; d < t.k; ++d) {
-          const double x = __dsub_rn(c[d], double(xs[d * m4 + j]));
-          const double sq = __dmul_rn(x, x);
-          sum = d == 0 ? sq : __dadd_rn(sum, sq);
-        }
-        hit |= sum <= R;
-      }
-      if (hit) S.flag = 1;
-      __syncthreads();
-      if (tid == 0) {
-        if (S.flag) a.verdict[a.rid[s0 + s]] = 1;
-        atomicAdd(a.n_refined, 1u);
+      if (P > 1 && active) {
+#pragma unroll
+        for (int i = 0; i < kS; ++i)
+          if ((sp.real >> i) & 1u) atomicMin(&S.minkey[sp.sidx[i]], okey(sp.mn[i]));
       }
       __syncthreads();
+      if (active && ph == 0) decide(sp, a, s0, leaf, S.hitmask[slot], S.minkey, P > 1);
     }
+    __syncthreads();  // tile state (list, minkey, smem points) free for the next tile
   }
 }
 
@@ -706,8 +787,10 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   k_tile_counts<<<Gl, 256, 0, s>>>(nl, a.counts, tcount);
   CAPT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, tcount, tstart, nl, s));
   k_make_tiles<<<Gl, 256, 0, s>>>(nl, tcount, tstart, a.tiles, a.n_tiles);
-  if (f64) k_bin_scatter<double, V><<<G4, 256, 0, s>>>(a);
-  else k_bin_scatter<float, V><<<G4, 256, 0, s>>>(a);
+  constexpr int VS = 8;
+  const int G8 = grid_for((n + VS - 1) / VS, 256, 8);
+  if (f64) k_bin_scatter<double, VS><<<G8, 256, 0, s>>>(a);
+  else k_bin_scatter<float, VS><<<G8, 256, 0, s>>>(a);
   static int sms = 0, occ = 0;
   if (!sms) {
     int dev = 0;
