@@ -24,6 +24,8 @@
 //   K7 k_pack         verdict bytes -> bit words, OR over each lane group
 #include <cub/cub.cuh>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 
@@ -613,6 +615,7 @@ __global__ void __launch_bounds__(kBT, 5) k_binned_scan(BinArgs a) {
       }
       __syncthreads();
       const int nu = S.n_list;
+      if (tid == 0) atomicAdd(a.n_pass_b, unsigned(nu));
       if (nu > 0) {
         nslot = (nu + kS - 1) / kS;
         P = max(1, kBT / nslot);
@@ -660,14 +663,34 @@ __global__ void __launch_bounds__(kBT, 5) k_binned_scan(BinArgs a) {
   }
 }
 
+// Exact float64 path, one warp per queued sphere: lanes split the set,
+// query.py:96-99 arithmetic (fp64, no FMA), ballot OR.
 template <typename InT>
 __global__ void k_slow(BinArgs a) {
   const unsigned n = *a.slow_n;
-  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
+  const DevTree& t = a.t;
+  for (unsigned i = warp; i < n; i += nwarps) {
     const int2 e = a.slow[i];
     double c64[3], r64;
-    load_sphere<InT>(a.centers, a.radii, e.x, a.t.k, c64, r64);
-    if (scan_f64(a.t, a.t.set[e.y], c64, r64, nullptr)) a.verdict[e.x] = 1;
+    load_sphere<InT>(a.centers, a.radii, e.x, t.k, c64, r64);
+    const uint2 st = t.set[e.y];
+    const float* base = reinterpret_cast<const float*>(t.data + st.x);
+    const uint32_t m4 = (st.y + 3u) & ~3u;
+    const double R = __dmul_rn(r64, r64);
+    bool hit = false;
+    for (uint32_t j = lane; j < st.y && !hit; j += 32) {
+      double sum = 0.0;
+      for (int d = 0; d < t.k; ++d) {
+        const double x = __dsub_rn(c64[d], double(base[d * m4 + j]));
+        const double sq = __dmul_rn(x, x);
+        sum = d == 0 ? sq : __dadd_rn(sum, sq);
+      }
+      hit = sum <= R;
+    }
+    if (__any_sync(0xffffffffu, hit) && lane == 0) a.verdict[e.x] = 1;
   }
 }
 
@@ -742,7 +765,7 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.flags = flags;
   a.first_bad = first_bad;
   const int64_t nl = t.n;
-  uint32_t* ctr = A.get<uint32_t>(4);  // slow_n, n_tiles, tile_ctr, n_refined
+  uint32_t* ctr = A.get<uint32_t>(8);  // slow_n, n_tiles, tile_ctr, n_refined, n_pass_b
   a.counts = A.get<uint32_t>(nl);
   a.start = A.get<uint32_t>(nl);
   uint32_t* tcount = A.get<uint32_t>(nl);
@@ -767,7 +790,8 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.n_tiles = ctr + 1;
   a.tile_ctr = ctr + 2;
   a.n_refined = ctr + 3;
-  CAPT_CUDA(cudaMemsetAsync(ctr, 0, 16, s));
+  CAPT_CUDA(cudaMemsetAsync(ctr, 0, 32, s));
+  a.n_pass_b = ctr + 4;
   CAPT_CUDA(cudaMemsetAsync(a.counts, 0, 4 * nl, s));
   CAPT_CUDA(cudaMemsetAsync(a.verdict, 0, n + 8, s));
   const bool f64 = flags & CAPT_INPUT_F64;
@@ -805,6 +829,14 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   k_pack<<<grid_for(n_words, 256, 8), 256, 0, s>>>(n / L, L, a.verdict, bits, n_words);
   CAPT_CUDA(cudaGetLastError());
   note_launches(9);  // count, 2 scans, tile counts, tiles, scatter, scan, slow, pack
+  static const bool debug = getenv("CAPT_DEBUG") != nullptr;
+  if (debug) {
+    uint32_t h[8];
+    CAPT_CUDA(cudaMemcpyAsync(h, ctr, 32, cudaMemcpyDeviceToHost, s));
+    CAPT_CUDA(cudaStreamSynchronize(s));
+    fprintf(stderr, "[capt binned] n=%lld exact_queue=%u tiles=%u refined=%u pass_b=%u\n",
+            (long long)n, h[0], h[1], h[3], h[4]);
+  }
   return CAPT_OK;
 }
 

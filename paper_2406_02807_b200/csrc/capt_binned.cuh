@@ -24,6 +24,7 @@ struct BinArgs {
   uint32_t* n_tiles;
   uint32_t* tile_ctr;
   uint32_t* n_refined;
+  uint32_t* n_pass_b;   // spheres left unresolved by the probe pass (debug)
   unsigned long long* first_bad;
   int2* slot;         // per sphere: (leaf, rank within leaf) if binned, else (-1, 0)
   float rlo_f, rhi_f; // fp32 images of the double band edges
