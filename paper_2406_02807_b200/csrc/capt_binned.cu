@@ -172,6 +172,35 @@ __device__ __forceinline__ void record_bin(const BinArgs& a, int64_t q, int stat
   }
 }
 
+// Warp-collective representative probe before binning.  Row 0 of a leaf's
+// set is the point that owns the leaf's cell -- the cell the sphere centre
+// lies in -- so it is the likeliest hit.  A definite fp32 hit (same error band
+// as the scan) resolves the sphere; with lane groups (query.py:152-160 early
+// exit) it resolves the whole group, whose other spheres are then never
+// binned.  Returns the status to bin with.
+__device__ __forceinline__ int rep_probe(const BinArgs& a, int64_t q, int status, int leaf,
+                                         float cx, float cy, float cz, float r) {
+  bool hit = false;
+  if (status == 2) {
+    const DevTree& t = a.t;
+    const uint2 st = __ldg(t.set + leaf);
+    const uint32_t m4 = (st.y + 3u) & ~3u;
+    const float* base = reinterpret_cast<const float*>(t.data + st.x);
+    const float dx = cx - __ldg(base), dy = cy - __ldg(base + m4), dz = cz - __ldg(base + 2 * m4);
+    const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+    hit = d2 <= (r * r) * (1.0f - kTau);
+  }
+  if (hit) a.verdict[q] = 1;
+  bool resolved = hit;
+  if (a.L > 1) {
+    const unsigned hb = __ballot_sync(0xffffffffu, hit);
+    const int lane = threadIdx.x & 31;
+    const unsigned seg = a.L >= 32 ? 0xffffffffu : ((1u << a.L) - 1u) << ((lane / a.L) * a.L);
+    resolved = (hb & seg) != 0;
+  }
+  return resolved ? 0 : status;
+}
+
 // K1: classify, per-leaf histogram (warp-aggregated), exact-path list
 template <typename InT>
 __global__ void __launch_bounds__(256) k_bin_count(BinArgs a) {
@@ -196,6 +225,18 @@ __global__ void __launch_bounds__(256) k_bin_count(BinArgs a) {
         leaf = int(sc.leaf);
       }
     }
+    float c[3] = {0.f, 0.f, 0.f}, r = 0.f;
+    if (status == 2) {  // binned spheres are exact fp32 values
+      for (int d = 0; d < t.k; ++d) {
+        if constexpr (std::is_same<InT, float>::value)
+          c[d] = static_cast<const float*>(a.centers)[q * t.k + d];
+        else
+          c[d] = float(static_cast<const double*>(a.centers)[q * t.k + d]);
+      }
+      if constexpr (std::is_same<InT, float>::value) r = static_cast<const float*>(a.radii)[q];
+      else r = float(static_cast<const double*>(a.radii)[q]);
+    }
+    status = rep_probe(a, q, status, leaf, c[0], c[1], c[2], r);
     record_bin(a, q, status, leaf);
   }
 }
@@ -290,6 +331,7 @@ __global__ void __launch_bounds__(256) k_bin_count3(BinArgs a) {
           }
         }
       }
+      status = rep_probe(a, q, status, leaf, cx[v], cy[v], cz[v], r[v]);
       record_bin(a, q, status, leaf);
     }
   }
