@@ -279,24 +279,29 @@ __global__ void __launch_bounds__(256) k_bin_count3(BinArgs a) {
       }
       i[v] = 0;
     }
-    int s = 0;
-    for (; s + 3 <= dsm; s += 3) {
+    if (t.grid) {
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        int j = i[v];
-        j = 2 * j + 1 + (cx[v] > sT[j] ? 1 : 0);
-        j = 2 * j + 1 + (cy[v] > sT[j] ? 1 : 0);
-        j = 2 * j + 1 + (cz[v] > sT[j] ? 1 : 0);
-        i[v] = j;
+      for (int v = 0; v < V; ++v) i[v] = nl1 + descend3_grid(t, sT, n_smem, cx[v], cy[v], cz[v]);
+    } else {
+      int s = 0;
+      for (; s + 3 <= dsm; s += 3) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          int j = i[v];
+          j = 2 * j + 1 + (cx[v] > sT[j] ? 1 : 0);
+          j = 2 * j + 1 + (cy[v] > sT[j] ? 1 : 0);
+          j = 2 * j + 1 + (cz[v] > sT[j] ? 1 : 0);
+          i[v] = j;
+        }
       }
-    }
-    for (; s < t.depth; ++s) {
-      const int ax = s % 3;
+      for (; s < t.depth; ++s) {
+        const int ax = s % 3;
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const float c = ax == 0 ? cx[v] : (ax == 1 ? cy[v] : cz[v]);
-        const float tv = s < dsm ? sT[i[v]] : __ldg(t.T + i[v]);
-        i[v] = 2 * i[v] + 1 + (c > tv ? 1 : 0);
+        for (int v = 0; v < V; ++v) {
+          const float c = ax == 0 ? cx[v] : (ax == 1 ? cy[v] : cz[v]);
+          const float tv = s < dsm ? sT[i[v]] : __ldg(t.T + i[v]);
+          i[v] = 2 * i[v] + 1 + (c > tv ? 1 : 0);
+        }
       }
     }
 #pragma unroll

@@ -126,3 +126,22 @@ def test_binned_device_built_tree_and_auto_mode():
     exp = O.brute_collides_many(cloud, c, r)
     assert np.array_equal(P.collides_many(tree, c, r), exp)  # auto -> binned here
     assert np.array_equal(q(tree, c, r, mode=DIRECT), exp)
+
+
+def test_binned_split_walls_and_grid_cells():
+    # lattice cloud: many split values shared by queries that sit exactly on
+    # split walls (x == T goes left) and on descent-grid cell boundaries
+    ax = np.linspace(-1, 1, 24, dtype=np.float32)
+    pts = np.stack(np.meshgrid(ax, ax, ax, indexing="ij"), -1).reshape(-1, 3)
+    t = O.construct(pts, 0.01, 0.12)
+    tree = upload(t)
+    rng = np.random.default_rng(9)
+    n = 1 << 18
+    c = pts[rng.integers(0, len(pts), n)].copy()
+    jitter = rng.integers(0, 3, (n, 3)).astype(np.float32) * np.float32(ax[1] - ax[0]) / 2
+    c = (c + jitter).astype(np.float32)
+    r = W.clamp_radii(rng.uniform(0.01, 0.12, n).astype(np.float32), 0.01, 0.12)
+    assert np.array_equal(P.leaf_indices(tree, c), O.leaf_indices(t, c))
+    exp = O.collides_many(t, c, r)
+    assert np.array_equal(q(tree, c, r), exp)
+    assert np.array_equal(q(tree, c, r, mode=DIRECT), exp)
