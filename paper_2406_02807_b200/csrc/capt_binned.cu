@@ -279,56 +279,24 @@ __global__ void __launch_bounds__(256) k_bin_count3(BinArgs a) {
       }
       i[v] = 0;
     }
-    if (t.grid) {
-      // grid start nodes for all V spheres first (independent loads in
-      // flight), then the remaining levels in lockstep
-      int ax[V];
-      const int g = t.grid_g;
-      const float G = float(g);
+    int s = 0;
+    for (; s + 3 <= dsm; s += 3) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        const float fx = (cx[v] - t.glo[0]) * t.ginv[0];
-        const float fy = (cy[v] - t.glo[1]) * t.ginv[1];
-        const float fz = (cz[v] - t.glo[2]) * t.ginv[2];
-        const bool in = fx >= 0.f && fx < G && fy >= 0.f && fy < G && fz >= 0.f && fz < G;
-        i[v] = in ? __ldg(t.grid + (int(fx) * g + int(fy)) * g + int(fz)) : 0;
+        int j = i[v];
+        j = 2 * j + 1 + (cx[v] > sT[j] ? 1 : 0);
+        j = 2 * j + 1 + (cy[v] > sT[j] ? 1 : 0);
+        j = 2 * j + 1 + (cz[v] > sT[j] ? 1 : 0);
+        i[v] = j;
       }
+    }
+    for (; s < t.depth; ++s) {
+      const int ax = s % 3;
 #pragma unroll
-      for (int v = 0; v < V; ++v) ax[v] = (31 - __clz(i[v] + 1)) % 3;
-      bool more = true;
-      while (more) {
-        more = false;
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          if (i[v] < nl1) {
-            const float tv = i[v] < n_smem ? sT[i[v]] : __ldg(t.T + i[v]);
-            const float c = ax[v] == 0 ? cx[v] : (ax[v] == 1 ? cy[v] : cz[v]);
-            i[v] = 2 * i[v] + 1 + (c > tv ? 1 : 0);
-            ax[v] = ax[v] == 2 ? 0 : ax[v] + 1;
-            more |= i[v] < nl1;
-          }
-        }
-      }
-    } else {
-      int s = 0;
-      for (; s + 3 <= dsm; s += 3) {
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          int j = i[v];
-          j = 2 * j + 1 + (cx[v] > sT[j] ? 1 : 0);
-          j = 2 * j + 1 + (cy[v] > sT[j] ? 1 : 0);
-          j = 2 * j + 1 + (cz[v] > sT[j] ? 1 : 0);
-          i[v] = j;
-        }
-      }
-      for (; s < t.depth; ++s) {
-        const int ax = s % 3;
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          const float c = ax == 0 ? cx[v] : (ax == 1 ? cy[v] : cz[v]);
-          const float tv = s < dsm ? sT[i[v]] : __ldg(t.T + i[v]);
-          i[v] = 2 * i[v] + 1 + (c > tv ? 1 : 0);
-        }
+      for (int v = 0; v < V; ++v) {
+        const float c = ax == 0 ? cx[v] : (ax == 1 ? cy[v] : cz[v]);
+        const float tv = s < dsm ? sT[i[v]] : __ldg(t.T + i[v]);
+        i[v] = 2 * i[v] + 1 + (c > tv ? 1 : 0);
       }
     }
 #pragma unroll

@@ -475,7 +475,6 @@ extern "C" int capt_tree_build(int device, int k, const float* points, int64_t n
                                                 const_cast<float4*>(dv.box));
     e = cudaGetLastError();
     if (e == cudaSuccess && compute_origins(dv, s)) e = cudaErrorLaunchFailure;
-    if (e == cudaSuccess && compute_grid(t, s)) e = cudaErrorLaunchFailure;
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) {

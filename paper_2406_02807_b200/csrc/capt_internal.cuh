@@ -24,7 +24,7 @@
 namespace capt {
 
 constexpr uint64_t kSlabMagic = 0x3030324254504143ull;  // "CAPTB200"
-constexpr int kSlabVersion = 3;
+constexpr int kSlabVersion = 2;
 constexpr int kMaxK = 3;
 
 struct SlabHeader {
@@ -43,12 +43,7 @@ struct SlabHeader {
   int64_t data_f4;    // float4 count of the data section
   int64_t bytes;      // slab size
   int64_t off_org;    // byte offset of the org section
-  int64_t off_grid;   // byte offset of the descent-start grid (k = 3)
-  int32_t grid_g;     // cells per axis (0: no grid)
-  float grid_lo[3];   // grid origin
-  float grid_inv[3];  // cells per unit length per axis
-  int32_t pad1;
-  int64_t reserved[4];
+  int64_t reserved[9];
 };
 static_assert(sizeof(SlabHeader) <= 256, "header must fit its 256-B section");
 
@@ -62,9 +57,6 @@ struct DevTree {
   const int64_t* offs;
   const float4* data;
   const float4* org;
-  const int* grid;    // G^3 start nodes for the descent (nullptr: start at the root)
-  int grid_g;
-  float glo[3], ginv[3];
 };
 
 }  // namespace capt
@@ -108,22 +100,7 @@ inline DevTree view(const capt_tree* t) {
   d.offs = reinterpret_cast<const int64_t*>(t->slab + t->h.off_offs);
   d.data = reinterpret_cast<const float4*>(t->slab + t->h.off_data);
   d.org = reinterpret_cast<const float4*>(t->slab + t->h.off_org);
-  d.grid_g = t->h.grid_g;
-  d.grid = t->h.grid_g ? reinterpret_cast<const int*>(t->slab + t->h.off_grid) : nullptr;
-  for (int i = 0; i < 3; ++i) {
-    d.glo[i] = t->h.grid_lo[i];
-    d.ginv[i] = t->h.grid_inv[i];
-  }
   return d;
-}
-
-// Descent-start grid size for a tree of n leaves (k = 3): ~16 cells per leaf,
-// 16..128 cells per axis (at most 8 MB).
-inline int grid_cells_per_axis(int k, int64_t n) {
-  if (k != 3 || n < 64) return 0;
-  int g = 16;
-  while (g < 128 && int64_t(g) * g * g < 16 * n) g *= 2;
-  return g;
 }
 
 inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
@@ -142,9 +119,6 @@ inline int64_t layout_slab(SlabHeader& h, int64_t data_f4) {
   off = align256(off + sizeof(int64_t) * (h.n + 1));
   h.off_org = off;
   off = align256(off + sizeof(float4) * h.n);
-  h.grid_g = grid_cells_per_axis(h.k, h.n);
-  h.off_grid = off;
-  off = align256(off + sizeof(int) * int64_t(h.grid_g) * h.grid_g * h.grid_g);
   h.off_data = off;
   off = align256(off + sizeof(float4) * (data_f4 > 0 ? data_f4 : 1));
   h.data_f4 = data_f4;
@@ -158,10 +132,8 @@ inline int depth_of(int64_t n) {
   return d;
 }
 
-// Fill the org section (binned-scan origins) of a slab whose data is final,
-// then the descent-start grid (updates the host header and its device copy).
+// Fill the org section (binned-scan origins) of a slab whose data is final.
 int compute_origins(const DevTree& t, cudaStream_t s);
-int compute_grid(capt_tree* t, cudaStream_t s);
 
 int alloc_slab(capt_tree** out, int device, SlabHeader h);
 

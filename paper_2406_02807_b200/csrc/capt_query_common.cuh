@@ -52,34 +52,6 @@ __device__ __forceinline__ int64_t descend(const DevTree& t, const float* sT, in
   return descend_t<double>(t, sT, n_smem, c64);
 }
 
-// k = 3 fp32 descent that starts from the grid cell's precomputed node: every
-// point of the (slightly expanded) cell box takes the same path down to that
-// node (capt_tree.cu k_grid), so the remaining levels give exactly the leaf of
-// tree.py:266-273.  Centres outside the grid (or NaN) start at the root.
-__device__ __forceinline__ int descend3_grid(const DevTree& t, const float* sT, int n_smem,
-                                             float cx, float cy, float cz) {
-  int i = 0, ax = 0;
-  if (t.grid) {
-    const float G = float(t.grid_g);
-    const float fx = (cx - t.glo[0]) * t.ginv[0];
-    const float fy = (cy - t.glo[1]) * t.ginv[1];
-    const float fz = (cz - t.glo[2]) * t.ginv[2];
-    if (fx >= 0.f && fx < G && fy >= 0.f && fy < G && fz >= 0.f && fz < G) {
-      const int g = t.grid_g;
-      i = __ldg(t.grid + (int(fx) * g + int(fy)) * g + int(fz));
-      ax = (31 - __clz(i + 1)) % 3;
-    }
-  }
-  const int inner = int(t.n - 1);
-  while (i < inner) {
-    const float tv = i < n_smem ? sT[i] : __ldg(t.T + i);
-    const float c = ax == 0 ? cx : (ax == 1 ? cy : cz);
-    i = 2 * i + 1 + (c > tv ? 1 : 0);
-    ax = ax == 2 ? 0 : ax + 1;
-  }
-  return i - inner;
-}
-
 // Exact reference AABB prefilter (query.py:202-208): fp64 copies of the fp32
 // box, res = max(max(lo - c, 0), c - hi), ((r0^2 + r1^2) + r2^2) <= r^2.
 __device__ __forceinline__ bool aabb_keep64(int k, const float4 lo, const float4 hi,

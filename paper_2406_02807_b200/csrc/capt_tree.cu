@@ -167,97 +167,6 @@ __global__ void k_origins(DevTree t) {
   }
 }
 
-__device__ __forceinline__ uint32_t grid_key(float f) {
-  const uint32_t u = __float_as_uint(f);
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-
-// bounding box of all finite stored points (= the cloud) from the leaf boxes
-__global__ void k_finite_bounds(DevTree t, uint32_t* __restrict__ mnmx) {
-  uint32_t mn[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, mx[3] = {0, 0, 0};
-  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < t.n;
-       j += int64_t(gridDim.x) * blockDim.x) {
-    const float4 lo = t.box[2 * j], hi = t.box[2 * j + 1];
-    const float l[3] = {lo.x, lo.y, lo.z}, h[3] = {hi.x, hi.y, hi.z};
-    for (int d = 0; d < 3; ++d) {
-      if (isfinite(l[d])) mn[d] = min(mn[d], grid_key(l[d]));
-      if (isfinite(h[d])) mx[d] = max(mx[d], grid_key(h[d]));
-    }
-  }
-  for (int d = 0; d < 3; ++d) {
-    atomicMin(mnmx + d, mn[d]);
-    atomicMax(mnmx + 3 + d, mx[d]);
-  }
-}
-
-// Start node of every grid cell: descend with the cell box expanded by 1e-3
-// cells per side while the whole box falls on one side of each split
-// (x <= T goes left, x > T goes right: tree.py:266-273).
-__global__ void k_grid(DevTree t, int* __restrict__ grid) {
-  const int g = t.grid_g;
-  const int64_t cells = int64_t(g) * g * g;
-  const int inner = int(t.n - 1);
-  for (int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < cells;
-       c += int64_t(gridDim.x) * blockDim.x) {
-    const int ix[3] = {int(c / (int64_t(g) * g)), int((c / g) % g), int(c % g)};
-    double lo[3], hi[3];
-    for (int d = 0; d < 3; ++d) {
-      const double h = 1.0 / double(t.ginv[d]);
-      lo[d] = double(t.glo[d]) + (ix[d] - 1e-3) * h;
-      hi[d] = double(t.glo[d]) + (ix[d] + 1 + 1e-3) * h;
-    }
-    int i = 0, ax = 0;
-    while (i < inner) {
-      const double tv = double(t.T[i]);
-      if (hi[ax] <= tv) i = 2 * i + 1;
-      else if (lo[ax] > tv) i = 2 * i + 2;
-      else break;
-      ax = ax == 2 ? 0 : ax + 1;
-    }
-    grid[c] = i;
-  }
-}
-
-int compute_grid(capt_tree* tree, cudaStream_t s) {
-  SlabHeader& h = tree->h;
-  if (!h.grid_g) return CAPT_OK;
-  DevTree t = view(tree);
-  uint32_t* d_mnmx = nullptr;
-  CAPT_CUDA(cudaMallocAsync(&d_mnmx, 24, s));
-  const uint32_t init[6] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0, 0, 0};
-  CAPT_CUDA(cudaMemcpyAsync(d_mnmx, init, 24, cudaMemcpyHostToDevice, s));
-  k_finite_bounds<<<grid_for(t.n, 256), 256, 0, s>>>(t, d_mnmx);
-  uint32_t mnmx[6];
-  CAPT_CUDA(cudaMemcpyAsync(mnmx, d_mnmx, 24, cudaMemcpyDeviceToHost, s));
-  CAPT_CUDA(cudaStreamSynchronize(s));
-  cudaFreeAsync(d_mnmx, s);
-  auto inv_key = [](uint32_t u) {
-    u = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
-    float f;
-    memcpy(&f, &u, 4);
-    return f;
-  };
-  for (int d = 0; d < 3; ++d) {
-    if (mnmx[d] == 0xffffffffu) {  // no finite point at all
-      h.grid_g = 0;
-      break;
-    }
-    const float lo = inv_key(mnmx[d]), hi = inv_key(mnmx[3 + d]);
-    const float span = hi - lo;
-    const float pad = span > 0.f ? span * 1e-4f : (fabsf(lo) + 1.f) * 1e-4f;
-    h.grid_lo[d] = lo - pad;
-    h.grid_inv[d] = float(h.grid_g) / (span + 2.f * pad);
-  }
-  CAPT_CUDA(cudaMemcpyAsync(tree->slab, &h, sizeof(h), cudaMemcpyHostToDevice, s));
-  if (!h.grid_g) return CAPT_OK;
-  t = view(tree);
-  k_grid<<<grid_for(int64_t(h.grid_g) * h.grid_g * h.grid_g, 256), 256, 0, s>>>(
-      t, const_cast<int*>(t.grid));
-  CAPT_CUDA(cudaGetLastError());
-  note_launches(2);
-  return CAPT_OK;
-}
-
 int compute_origins(const DevTree& t, cudaStream_t s) {
   k_origins<<<grid_for(t.n * 32, 256), 256, 0, s>>>(t);
   CAPT_CUDA(cudaGetLastError());
@@ -348,7 +257,7 @@ int capt_tree_create(int device, int k, int64_t n, int64_t n_points, double r_mi
                                                     const_cast<float4*>(v.data));
   k_pack_boxes<<<grid_for(n, 256), 256, 0, s>>>(k, n, d_lo, d_hi, const_cast<float4*>(v.box));
   UPCHK(cudaGetLastError());
-  if (compute_origins(v, s) || compute_grid(t, s)) {
+  if (compute_origins(v, s)) {
     cudaFree(d_vals); cudaFree(d_lo); cudaFree(d_hi);
     capt_tree_destroy(t);
     *out = nullptr;
