@@ -256,6 +256,124 @@ int launch_direct(const DevTree& t, const void* centers, const void* radii, int6
   return CAPT_OK;
 }
 
+// One query over device buffers on stream s (direct or binned pipeline).
+int query_device(const DevTree& t, const void* d_c, const void* d_r, int64_t n, int L,
+                 const uint8_t* d_m, uint32_t flags, uint32_t* d_bits,
+                 unsigned long long* d_cnt, unsigned long long* d_bad, cudaStream_t s) {
+  const int64_t n_words = (n / L + 31) / 32;
+  if (d_bad) CAPT_CUDA(cudaMemsetAsync(d_bad, 0xff, 8, s));
+  if (d_cnt && (flags & CAPT_STATS)) CAPT_CUDA(cudaMemsetAsync(d_cnt, 0, 48, s));
+  if (L > 8 || n == 0) CAPT_CUDA(cudaMemsetAsync(d_bits, 0, 4 * (n_words ? n_words : 1), s));
+  if (n == 0) return CAPT_OK;
+  uint32_t fl = flags;
+  if (!d_bad) fl &= ~CAPT_CHECK_RADII;
+  return binned_preferred(t, n, fl)
+             ? launch_binned(t, d_c, d_r, n, L, d_m, fl, d_bits, n_words, d_bad, s)
+             : launch_direct(t, d_c, d_r, n, L, d_m, fl, d_bits, n_words, d_cnt, d_bad, s);
+}
+
+// Host-buffer queries larger than one chunk: a two-stream pipeline so the
+// host->device copy of chunk i+1 overlaps the kernels of chunk i (and the
+// verdict copy-back of chunk i-1).  Chunks are multiples of 32 lane groups,
+// so every chunk owns whole verdict words.
+struct PipeState {
+  cudaStream_t w[2] = {nullptr, nullptr};
+  cudaEvent_t start = nullptr, done[2] = {nullptr, nullptr};
+  unsigned long long* pinned = nullptr;  // per chunk: first_bad + 6 counters
+  static constexpr int kMaxChunks = 1024;
+};
+
+static PipeState* pipe_state(int device) {
+  static PipeState states[64];
+  static bool init[64] = {false};
+  if (device < 0 || device >= 64) return nullptr;
+  PipeState& p = states[device];
+  if (!init[device]) {
+    for (int i = 0; i < 2; ++i) {
+      cudaStreamCreateWithFlags(&p.w[i], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&p.done[i], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&p.start, cudaEventDisableTiming);
+    cudaHostAlloc(reinterpret_cast<void**>(&p.pinned),
+                  sizeof(unsigned long long) * 7 * PipeState::kMaxChunks, cudaHostAllocDefault);
+    init[device] = true;
+  }
+  return p.pinned ? &p : nullptr;
+}
+
+int query_host_pipelined(const capt_tree* tree, const DevTree& t, const void* centers,
+                         const void* radii, int64_t n, int L, const uint8_t* lane_mask,
+                         uint32_t flags, uint32_t* out_bits, uint64_t* counters,
+                         int64_t* first_bad, cudaStream_t s, int64_t chunk) {
+  PipeState* p = pipe_state(tree->device);
+  if (!p) return fail(CAPT_ECUDA, "pipeline streams unavailable");
+  const size_t in_elem = (flags & CAPT_INPUT_F64) ? sizeof(double) : sizeof(float);
+  const int64_t n_chunks = (n + chunk - 1) / chunk;
+  if (n_chunks > PipeState::kMaxChunks) return fail(CAPT_EINVAL, "batch too large for the pipeline");
+  struct Buf {
+    void* c = nullptr;
+    void* r = nullptr;
+    uint8_t* m = nullptr;
+    uint32_t* bits = nullptr;
+    unsigned long long* aux = nullptr;  // first_bad + 6 counters
+  } buf[2];
+  CAPT_CUDA(cudaEventRecord(p->start, s));
+  for (int i = 0; i < 2; ++i) {
+    cudaStream_t w = p->w[i];
+    CAPT_CUDA(cudaStreamWaitEvent(w, p->start, 0));
+    CAPT_CUDA(cudaMallocAsync(&buf[i].c, in_elem * t.k * chunk, w));
+    CAPT_CUDA(cudaMallocAsync(&buf[i].r, in_elem * chunk, w));
+    if (lane_mask) CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf[i].m), chunk, w));
+    CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf[i].bits), 4 * (chunk / L / 32 + 1), w));
+    CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf[i].aux), 8 * 7, w));
+  }
+  int rc = CAPT_OK;
+  for (int64_t ci = 0; ci < n_chunks && rc == CAPT_OK; ++ci) {
+    const int b = int(ci & 1);
+    cudaStream_t w = p->w[b];
+    const int64_t base = ci * chunk;
+    const int64_t len = n - base < chunk ? n - base : chunk;
+    const char* hc = static_cast<const char*>(centers) + in_elem * t.k * base;
+    const char* hr = static_cast<const char*>(radii) + in_elem * base;
+    CAPT_CUDA(cudaMemcpyAsync(buf[b].c, hc, in_elem * t.k * len, cudaMemcpyHostToDevice, w));
+    CAPT_CUDA(cudaMemcpyAsync(buf[b].r, hr, in_elem * len, cudaMemcpyHostToDevice, w));
+    if (lane_mask)
+      CAPT_CUDA(cudaMemcpyAsync(buf[b].m, lane_mask + base, len, cudaMemcpyHostToDevice, w));
+    rc = query_device(t, buf[b].c, buf[b].r, len, L, lane_mask ? buf[b].m : nullptr, flags,
+                      buf[b].bits, buf[b].aux + 1, buf[b].aux, w);
+    if (rc) break;
+    const int64_t words = (len / L + 31) / 32;
+    CAPT_CUDA(cudaMemcpyAsync(out_bits + base / L / 32, buf[b].bits, 4 * words,
+                              cudaMemcpyDeviceToHost, w));
+    CAPT_CUDA(cudaMemcpyAsync(p->pinned + 7 * ci, buf[b].aux, 8 * 7, cudaMemcpyDeviceToHost, w));
+  }
+  for (int i = 0; i < 2; ++i) {
+    cudaFreeAsync(buf[i].c, p->w[i]);
+    cudaFreeAsync(buf[i].r, p->w[i]);
+    if (buf[i].m) cudaFreeAsync(buf[i].m, p->w[i]);
+    cudaFreeAsync(buf[i].bits, p->w[i]);
+    cudaFreeAsync(buf[i].aux, p->w[i]);
+    CAPT_CUDA(cudaEventRecord(p->done[i], p->w[i]));
+    CAPT_CUDA(cudaStreamWaitEvent(s, p->done[i], 0));
+  }
+  CAPT_CUDA(cudaStreamSynchronize(s));
+  if (rc) return rc;
+  int64_t fb = -1;
+  uint64_t cnt[6] = {0, 0, 0, 0, 0, 0};
+  for (int64_t ci = 0; ci < n_chunks; ++ci) {
+    const unsigned long long* a = p->pinned + 7 * ci;
+    if (fb < 0 && a[0] != ~0ull) fb = ci * chunk + int64_t(a[0]);
+    for (int j = 0; j < 6; ++j) cnt[j] += a[1 + j];
+  }
+  if (first_bad) *first_bad = fb;
+  if (counters && (flags & CAPT_STATS)) memcpy(counters, cnt, sizeof(cnt));
+  if ((flags & CAPT_CHECK_RADII) && fb >= 0) {
+    set_error("radius outside the tree's exactness band");
+    return CAPT_ERANGE;
+  }
+  return CAPT_OK;
+}
+
 }  // namespace capt
 
 using namespace capt;
@@ -278,6 +396,13 @@ extern "C" int capt_query(const capt_tree* tree, const void* centers, const void
   const int64_t n_words = (n_groups + 31) / 32;
   const bool host = flags & CAPT_HOST_IO;
   const size_t in_elem = (flags & CAPT_INPUT_F64) ? sizeof(double) : sizeof(float);
+
+  // group-sequential counters (STATS with lane groups) are additive per chunk
+  const int64_t chunk = int64_t(1) << 22;  // spheres per pipeline chunk (multiple of 32 * L)
+  if (host && n > chunk) {
+    return query_host_pipelined(tree, t, centers, radii, n, L, lane_mask, flags, out_bits,
+                                counters, first_bad, s, chunk);
+  }
 
   HostIO io;
   io.s = s;
@@ -308,16 +433,8 @@ extern "C" int capt_query(const capt_tree* tree, const void* centers, const void
     d_cnt = io.counters;
     d_bad = io.first_bad;
   }
-  unsigned long long* bad = d_bad;
-  if (bad) CAPT_CUDA(cudaMemsetAsync(bad, 0xff, 8, s));
-  if (d_cnt && (flags & CAPT_STATS)) CAPT_CUDA(cudaMemsetAsync(d_cnt, 0, 48, s));
-  if (L > 8 || n == 0) CAPT_CUDA(cudaMemsetAsync(d_bits, 0, 4 * (n_words ? n_words : 1), s));
-  if (n > 0) {
-    uint32_t fl = flags;
-    if (!bad) fl &= ~CAPT_CHECK_RADII;
-    int rc = binned_preferred(t, n, fl)
-                 ? launch_binned(t, d_c, d_r, n, L, d_m, fl, d_bits, n_words, bad, s)
-                 : launch_direct(t, d_c, d_r, n, L, d_m, fl, d_bits, n_words, d_cnt, bad, s);
+  {
+    const int rc = query_device(t, d_c, d_r, n, L, d_m, flags, d_bits, d_cnt, d_bad, s);
     if (rc) return rc;
   }
   if (host) {

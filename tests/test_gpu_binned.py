@@ -145,3 +145,25 @@ def test_binned_split_walls_and_grid_cells():
     exp = O.collides_many(t, c, r)
     assert np.array_equal(q(tree, c, r), exp)
     assert np.array_equal(q(tree, c, r, mode=DIRECT), exp)
+
+
+def test_host_pipeline_chunks_counters_and_bad_radius():
+    # host buffers larger than one pipeline chunk (4M spheres): two-stream
+    # chunked path; verdict words, counters and the first bad index must all
+    # match the single-shot device path / the oracle
+    cloud = W.cfg1_cloud()
+    t = O.construct(cloud, 0.02, 0.08)
+    tree = upload(t)
+    c, r = W.cfg1_queries(cloud, n_groups=(1 << 20) + 96, seed=77)  # 8.4M spheres, 3 chunks
+    exp = O.collides_groups(t, c, r, 8)
+    bits, cnt, _ = _host_query(tree, c, r, 0, 8, None, True, True, stats=True)
+    assert np.array_equal(bits, exp)
+    e_hits, e_rej, e_scanned = O.collides_groups(t, c, r, 8, return_counters=True)[1]
+    assert int(cnt[0]) == e_hits and int(cnt[4]) == e_rej and int(cnt[2]) == e_scanned
+    bits2, _, _ = _host_query(tree, c, r, 0, 8, None, True, True)
+    assert np.array_equal(bits2, exp)
+    r_bad = r.copy()
+    r_bad[5_000_001] = 0.5
+    r_bad[7_000_000] = 0.001
+    with pytest.raises(ValueError, match="radius 0.5 outside"):
+        P.collides_many(tree, c, r_bad)
