@@ -1,0 +1,79 @@
+"""Turn gpurun ncu outputs into the committed profile summaries.
+
+    python profiles/summarize.py launches <launches.csv> <out.md>
+    python profiles/summarize.py full <report.ncu-rep> <out.json>
+
+``launches``: per-kernel device time from an
+``ncu --metrics gpu__time_duration.sum --clock-control none`` launch list
+(cold-cache, serialised: compare shares, not absolutes).
+``full``: headline metrics of every kernel in an ``ncu --set full`` report
+(duration, DRAM bytes, throughputs, IPC, occupancy, FP32/FMA pipe use).
+"""
+
+from __future__ import annotations
+
+import collections
+import csv
+import json
+import subprocess
+import sys
+
+
+def launches(path: str, out: str) -> None:
+    rows = list(csv.reader(open(path)))
+    hdr, data = None, []
+    for r in rows:
+        if "Kernel Name" in r:
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            data.append(dict(zip(hdr, r)))
+    agg = collections.OrderedDict()
+    for d in data:
+        name = d["Kernel Name"].split("(")[0].replace("capt::", "").replace("<unnamed>::", "")
+        agg.setdefault(name, []).append(float(d["Metric Value"]) / 1e3)
+    lines = [f"# Kernel launch list: {path.split('/')[-1]}", "",
+             "| kernel | launches | mean us | total us |", "|---|---:|---:|---:|"]
+    for k, v in agg.items():
+        lines.append(f"| `{k}` | {len(v)} | {sum(v) / len(v):.1f} | {sum(v):.1f} |")
+    open(out, "w").write("\n".join(lines) + "\n")
+
+
+WANT = {
+    "gpu__time_duration.sum": "duration_ns",
+    "dram__bytes_read.sum": "dram_read",
+    "dram__bytes_write.sum": "dram_write",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct_of_peak",
+    "lts__t_sector_hit_rate.pct": "l2_hit_rate_pct",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput_pct",
+    "sm__inst_executed.avg.per_cycle_active": "ipc_active",
+    "sm__warps_active.avg.pct_of_peak_sustained_active": "achieved_occupancy_pct",
+    "launch__registers_per_thread": "registers",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "fma_pipe_pct",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active": "fma_inst_pct",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active": "alu_pipe_pct",
+    "smsp__inst_executed.sum": "warp_instructions",
+}
+
+
+def full(path: str, out: str) -> None:
+    txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(txt.splitlines()))
+    hdr, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        u = dict(zip(hdr, units))
+        item = {"kernel": d.get("Kernel Name", "")[:120]}
+        for k, name in WANT.items():
+            if k in d:
+                item[name] = d[k]
+                if u.get(k):
+                    item[name + "_unit"] = u[k]
+        res.append(item)
+    json.dump(res, open(out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
