@@ -241,8 +241,10 @@ __global__ void __launch_bounds__(256) k_bin_count(BinArgs a) {
   }
 }
 
-// K1 specialised for k = 3, fp32 input: V spheres per thread in flight
-// (independent descents interleave), the top 13 levels of T in shared memory.
+// K1 specialised for k = 3, fp32 input (the hot path): V spheres per thread
+// in flight, 32-bit indexing, the top 13 levels of T in shared memory walked
+// with byte offsets (child = 2*off + 4 + 4*(x > T): 4 instructions per level),
+// one plain atomic per binned sphere for its ticket.
 constexpr int kSmemNodes3 = 8191;
 template <int V>
 __global__ void __launch_bounds__(256) k_bin_count3(BinArgs a) {
@@ -253,41 +255,43 @@ __global__ void __launch_bounds__(256) k_bin_count3(BinArgs a) {
   __syncthreads();
   const bool check = a.flags & CAPT_CHECK_RADII;
   const bool prefilter = a.flags & CAPT_PREFILTER;
-  const float* cf = static_cast<const float*>(a.centers);
-  const float* rf = static_cast<const float*>(a.radii);
+  const float* __restrict__ cf = static_cast<const float*>(a.centers);
+  const float* __restrict__ rf = static_cast<const float*>(a.radii);
+  const unsigned char* sb = reinterpret_cast<const unsigned char*>(sT);
   const int dsm = t.depth < 13 ? t.depth : 13;
   const int nl1 = int(t.n - 1);
-  const int64_t n_pad = (a.n + 31) & ~int64_t(31);
-  const int64_t per_iter = int64_t(gridDim.x) * blockDim.x * V;
-  for (int64_t base = int64_t(blockIdx.x) * blockDim.x * V; base < n_pad; base += per_iter) {
+  const int n = int(a.n);
+  const int n_pad = (n + 31) & ~31;
+  const int lane = threadIdx.x & 31;
+  const unsigned seg = a.L >= 32 ? 0xffffffffu : ((1u << a.L) - 1u) << ((lane / a.L) * a.L);
+  const float band_lo = 1.0f - kTau, band_hi = 1.0f + kTau;
+  for (int base = blockIdx.x * blockDim.x * V; base < n_pad; base += gridDim.x * blockDim.x * V) {
     float cx[V], cy[V], cz[V], r[V];
     bool valid[V];
-    int i[V];
+    unsigned off[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      const int64_t q = base + int64_t(v) * blockDim.x + threadIdx.x;
-      valid[v] = q < a.n;
-      if (valid[v] && a.mask) valid[v] = a.mask[q] != 0;
-      cx[v] = cy[v] = cz[v] = r[v] = 0.f;
-      if (valid[v]) {
-        cx[v] = __ldg(cf + 3 * q);
-        cy[v] = __ldg(cf + 3 * q + 1);
-        cz[v] = __ldg(cf + 3 * q + 2);
-        r[v] = __ldg(rf + q);
-        if (check && (r[v] < a.rlo_f || r[v] > a.rhi_f))
-          atomicMin(a.first_bad, static_cast<unsigned long long>(q));
-      }
-      i[v] = 0;
+      const int q = base + v * blockDim.x + threadIdx.x;
+      valid[v] = q < n;
+      if (a.mask && valid[v]) valid[v] = a.mask[q] != 0;
+      const int qq = valid[v] ? q : 0;
+      cx[v] = __ldg(cf + 3 * qq);
+      cy[v] = __ldg(cf + 3 * qq + 1);
+      cz[v] = __ldg(cf + 3 * qq + 2);
+      r[v] = __ldg(rf + qq);
+      if (check && valid[v] && (r[v] < a.rlo_f || r[v] > a.rhi_f))
+        atomicMin(a.first_bad, static_cast<unsigned long long>(q));
+      off[v] = 0;
     }
     int s = 0;
     for (; s + 3 <= dsm; s += 3) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        int j = i[v];
-        j = 2 * j + 1 + (cx[v] > sT[j] ? 1 : 0);
-        j = 2 * j + 1 + (cy[v] > sT[j] ? 1 : 0);
-        j = 2 * j + 1 + (cz[v] > sT[j] ? 1 : 0);
-        i[v] = j;
+        unsigned o = off[v];
+        o = 2 * o + (cx[v] > *reinterpret_cast<const float*>(sb + o) ? 8u : 4u);
+        o = 2 * o + (cy[v] > *reinterpret_cast<const float*>(sb + o) ? 8u : 4u);
+        o = 2 * o + (cz[v] > *reinterpret_cast<const float*>(sb + o) ? 8u : 4u);
+        off[v] = o;
       }
     }
     for (; s < t.depth; ++s) {
@@ -295,44 +299,62 @@ __global__ void __launch_bounds__(256) k_bin_count3(BinArgs a) {
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const float c = ax == 0 ? cx[v] : (ax == 1 ? cy[v] : cz[v]);
-        const float tv = s < dsm ? sT[i[v]] : __ldg(t.T + i[v]);
-        i[v] = 2 * i[v] + 1 + (c > tv ? 1 : 0);
+        const float tv = s < dsm ? *reinterpret_cast<const float*>(sb + off[v])
+                                 : __ldg(t.T + (off[v] >> 2));
+        off[v] = 2 * off[v] + (c > tv ? 8u : 4u);
       }
     }
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      const int64_t q = base + int64_t(v) * blockDim.x + threadIdx.x;
-      const int leaf = i[v] - nl1;
+      const int q = base + v * blockDim.x + threadIdx.x;
+      const int leaf = int(off[v] >> 2) - nl1;
       int status = 0;
+      const float r2 = r[v] * r[v];
       if (valid[v]) {
         const bool cfin = isfinite(cx[v]) && isfinite(cy[v]) && isfinite(cz[v]);
-        const float r2 = r[v] * r[v];
         const bool fast = cfin && r2 >= kR2Min && r2 <= kR2Max;
         // non-finite centre with a finite radius never collides (float64 r^2 is finite)
         status = fast ? 2 : ((!cfin && isfinite(r[v])) ? 0 : 3);
-        {
-          if (status && prefilter) {
-            const float4 lo = __ldg(t.box + 2 * leaf);
-            const float4 hi = __ldg(t.box + 2 * leaf + 1);
-            bool exact = !fast;
-            if (fast) {
-              const float rx = fmaxf(fmaxf(lo.x - cx[v], 0.f), cx[v] - hi.x);
-              const float ry = fmaxf(fmaxf(lo.y - cy[v], 0.f), cy[v] - hi.y);
-              const float rz = fmaxf(fmaxf(lo.z - cz[v], 0.f), cz[v] - hi.z);
-              const float ss = fmaf(rz, rz, fmaf(ry, ry, rx * rx));
-              if (ss > r2 * (1.0f + kTau)) status = 0;
-              else if (!(ss < r2 * (1.0f - kTau))) exact = true;
-            }
-            if (status && exact) {
-              const double c64[3] = {cx[v], cy[v], cz[v]};
-              const double r64 = r[v];
-              if (!aabb_keep64(3, lo, hi, c64, __dmul_rn(r64, r64))) status = 0;
-            }
+        if (status && prefilter) {
+          const float4 lo = __ldg(t.box + 2 * leaf);
+          const float4 hi = __ldg(t.box + 2 * leaf + 1);
+          bool exact = !fast;
+          if (fast) {
+            const float rx = fmaxf(fmaxf(lo.x - cx[v], 0.f), cx[v] - hi.x);
+            const float ry = fmaxf(fmaxf(lo.y - cy[v], 0.f), cy[v] - hi.y);
+            const float rz = fmaxf(fmaxf(lo.z - cz[v], 0.f), cz[v] - hi.z);
+            const float ss = fmaf(rz, rz, fmaf(ry, ry, rx * rx));
+            if (ss > r2 * band_hi) status = 0;
+            else if (!(ss < r2 * band_lo)) exact = true;
+          }
+          if (status && exact) {
+            const double c64[3] = {cx[v], cy[v], cz[v]};
+            const double r64 = r[v];
+            if (!aabb_keep64(3, lo, hi, c64, __dmul_rn(r64, r64))) status = 0;
           }
         }
       }
-      status = rep_probe(a, q, status, leaf, cx[v], cy[v], cz[v], r[v]);
-      record_bin(a, q, status, leaf);
+      // representative probe (see rep_probe)
+      bool hit = false;
+      if (status == 2) {
+        const uint2 st = __ldg(t.set + leaf);
+        const unsigned m4 = (st.y + 3u) & ~3u;
+        const float* pb = reinterpret_cast<const float*>(t.data + st.x);
+        const float dx = cx[v] - __ldg(pb), dy = cy[v] - __ldg(pb + m4),
+                    dz = cz[v] - __ldg(pb + 2 * m4);
+        hit = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) <= r2 * band_lo;
+      }
+      if (hit) a.verdict[q] = 1;
+      bool resolved = hit;
+      if (a.L > 1) resolved = (__ballot_sync(0xffffffffu, hit) & seg) != 0;
+      if (resolved) status = 0;
+      int ticket = 0;
+      if (status == 2) ticket = int(atomicAdd(a.counts + leaf, 1u));
+      if (q < n) a.slot[q] = make_int2(status == 2 ? leaf : -1, ticket);
+      if (status == 3) {
+        const unsigned j = atomicAdd(a.slow_n, 1u);
+        a.slow[j] = make_int2(q, leaf);
+      }
     }
   }
 }
