@@ -348,13 +348,7 @@ __global__ void __launch_bounds__(256) k_bin_count3(BinArgs a) {
       bool resolved = hit;
       if (a.L > 1) resolved = (__ballot_sync(0xffffffffu, hit) & seg) != 0;
       if (resolved) status = 0;
-      int ticket = 0;
-      if (status == 2) ticket = int(atomicAdd(a.counts + leaf, 1u));
-      if (q < n) a.slot[q] = make_int2(status == 2 ? leaf : -1, ticket);
-      if (status == 3) {
-        const unsigned j = atomicAdd(a.slow_n, 1u);
-        a.slow[j] = make_int2(q, leaf);
-      }
+      record_bin(a, q, status, leaf);
     }
   }
 }
