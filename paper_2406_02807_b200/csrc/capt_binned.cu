@@ -165,7 +165,7 @@ __device__ __forceinline__ void record_bin(const BinArgs& a, int64_t q, int stat
     b = __shfl_sync(peers, b, leader);
     ticket = int(b + __popc(peers & ((1u << lane) - 1u)));
   }
-  if (q < a.n) a.slot[q] = make_int2(scan ? leaf : -1, ticket);
+  if (q < a.n) __stcs(a.slot + q, make_int2(scan ? leaf : -1, ticket));
   if (status == 3) {
     const unsigned i = atomicAdd(a.slow_n, 1u);
     a.slow[i] = make_int2(int(q), leaf);
@@ -265,20 +265,41 @@ __global__ void __launch_bounds__(256) k_bin_count3(BinArgs a) {
   const int lane = threadIdx.x & 31;
   const unsigned seg = a.L >= 32 ? 0xffffffffu : ((1u << a.L) - 1u) << ((lane / a.L) * a.L);
   const float band_lo = 1.0f - kTau, band_hi = 1.0f + kTau;
-  for (int base = blockIdx.x * blockDim.x * V; base < n_pad; base += gridDim.x * blockDim.x * V) {
+  const int stride = gridDim.x * blockDim.x * V;
+  // streaming (evict-first) input loads, software-pipelined one iteration
+  // ahead: the DRAM latency of iteration i+1 hides behind iteration i
+  float nx[V], ny[V], nz[V], nr[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const int q = blockIdx.x * blockDim.x * V + v * blockDim.x + threadIdx.x;
+    const int qq = q < n ? q : 0;
+    nx[v] = __ldcs(cf + 3 * qq);
+    ny[v] = __ldcs(cf + 3 * qq + 1);
+    nz[v] = __ldcs(cf + 3 * qq + 2);
+    nr[v] = __ldcs(rf + qq);
+  }
+  for (int base = blockIdx.x * blockDim.x * V; base < n_pad; base += stride) {
     float cx[V], cy[V], cz[V], r[V];
     bool valid[V];
     unsigned off[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
+      cx[v] = nx[v];
+      cy[v] = ny[v];
+      cz[v] = nz[v];
+      r[v] = nr[v];
+      const int qn = base + stride + v * blockDim.x + threadIdx.x;
+      const int qq = qn < n ? qn : 0;
+      nx[v] = __ldcs(cf + 3 * qq);
+      ny[v] = __ldcs(cf + 3 * qq + 1);
+      nz[v] = __ldcs(cf + 3 * qq + 2);
+      nr[v] = __ldcs(rf + qq);
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
       const int q = base + v * blockDim.x + threadIdx.x;
       valid[v] = q < n;
       if (a.mask && valid[v]) valid[v] = a.mask[q] != 0;
-      const int qq = valid[v] ? q : 0;
-      cx[v] = __ldg(cf + 3 * qq);
-      cy[v] = __ldg(cf + 3 * qq + 1);
-      cz[v] = __ldg(cf + 3 * qq + 2);
-      r[v] = __ldg(rf + qq);
       if (check && valid[v] && (r[v] < a.rlo_f || r[v] > a.rhi_f))
         atomicMin(a.first_bad, static_cast<unsigned long long>(q));
       off[v] = 0;
@@ -380,13 +401,13 @@ __global__ void __launch_bounds__(256) k_bin_scatter(BinArgs a) {
       if constexpr (std::is_same<InT, float>::value) {
         const float* cf = static_cast<const float*>(a.centers);
         if (k == 3) {
-          c[0] = __ldg(cf + 3 * q);
-          c[1] = __ldg(cf + 3 * q + 1);
-          c[2] = __ldg(cf + 3 * q + 2);
+          c[0] = __ldcs(cf + 3 * q);
+          c[1] = __ldcs(cf + 3 * q + 1);
+          c[2] = __ldcs(cf + 3 * q + 2);
         } else {
-          for (int d = 0; d < k; ++d) c[d] = __ldg(cf + q * k + d);
+          for (int d = 0; d < k; ++d) c[d] = __ldcs(cf + q * k + d);
         }
-        r = __ldg(static_cast<const float*>(a.radii) + q);
+        r = __ldcs(static_cast<const float*>(a.radii) + q);
       } else {  // binned float64 inputs are exact fp32 values
         const double* cd = static_cast<const double*>(a.centers);
         for (int d = 0; d < k; ++d) c[d] = float(__ldg(cd + q * k + d));
