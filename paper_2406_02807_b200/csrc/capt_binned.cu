@@ -150,22 +150,17 @@ __device__ __forceinline__ int classify_f32(const DevTree& t, const float* sT, i
   return fast ? 2 : 3;
 }
 
-// Warp-collective: per-leaf histogram with a ticket (rank within the leaf)
-// per binned sphere (warp-aggregated atomics), exact-path list.
+// Warp-collective: per-leaf histogram (warp-aggregated, fire-and-forget
+// atomics), per-sphere leaf id for K3, exact-path list.
 __device__ __forceinline__ void record_bin(const BinArgs& a, int64_t q, int status, int leaf) {
   const bool scan = status == 2;
   const unsigned act = __ballot_sync(0xffffffffu, scan);
-  int ticket = 0;
   if (scan) {
     const int lane = threadIdx.x & 31;
     const unsigned peers = __match_any_sync(act, unsigned(leaf));
-    const int leader = __ffs(peers) - 1;
-    unsigned b = 0;
-    if (lane == leader) b = atomicAdd(a.counts + leaf, __popc(peers));
-    b = __shfl_sync(peers, b, leader);
-    ticket = int(b + __popc(peers & ((1u << lane) - 1u)));
+    if (lane == __ffs(peers) - 1) atomicAdd(a.counts + leaf, __popc(peers));
   }
-  if (q < a.n) __stcs(a.slot + q, make_int2(scan ? leaf : -1, ticket));
+  if (q < a.n) __stcs(a.leafid + q, scan ? leaf : -1);
   if (status == 3) {
     const unsigned i = atomicAdd(a.slow_n, 1u);
     a.slow[i] = make_int2(int(q), leaf);
@@ -325,51 +320,71 @@ __global__ void __launch_bounds__(256) k_bin_count3(BinArgs a) {
         off[v] = 2 * off[v] + (c > tv ? 8u : 4u);
       }
     }
+    // per-sphere classification; no warp-synchronous intrinsic in this loop,
+    // so the box / set / representative loads of the V spheres can overlap
+    int leaf[V], status[V];
+    bool hit[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      const int q = base + v * blockDim.x + threadIdx.x;
-      const int leaf = int(off[v] >> 2) - nl1;
-      int status = 0;
+      leaf[v] = int(off[v] >> 2) - nl1;
+      status[v] = 0;
+      hit[v] = false;
       const float r2 = r[v] * r[v];
       if (valid[v]) {
         const bool cfin = isfinite(cx[v]) && isfinite(cy[v]) && isfinite(cz[v]);
         const bool fast = cfin && r2 >= kR2Min && r2 <= kR2Max;
         // non-finite centre with a finite radius never collides (float64 r^2 is finite)
-        status = fast ? 2 : ((!cfin && isfinite(r[v])) ? 0 : 3);
-        if (status && prefilter) {
-          const float4 lo = __ldg(t.box + 2 * leaf);
-          const float4 hi = __ldg(t.box + 2 * leaf + 1);
+        status[v] = fast ? 2 : ((!cfin && isfinite(r[v])) ? 0 : 3);
+        if (status[v] && prefilter) {
+          const float4 lo = __ldg(t.box + 2 * leaf[v]);
+          const float4 hi = __ldg(t.box + 2 * leaf[v] + 1);
           bool exact = !fast;
           if (fast) {
             const float rx = fmaxf(fmaxf(lo.x - cx[v], 0.f), cx[v] - hi.x);
             const float ry = fmaxf(fmaxf(lo.y - cy[v], 0.f), cy[v] - hi.y);
             const float rz = fmaxf(fmaxf(lo.z - cz[v], 0.f), cz[v] - hi.z);
             const float ss = fmaf(rz, rz, fmaf(ry, ry, rx * rx));
-            if (ss > r2 * band_hi) status = 0;
+            if (ss > r2 * band_hi) status[v] = 0;
             else if (!(ss < r2 * band_lo)) exact = true;
           }
-          if (status && exact) {
+          if (status[v] && exact) {
             const double c64[3] = {cx[v], cy[v], cz[v]};
             const double r64 = r[v];
-            if (!aabb_keep64(3, lo, hi, c64, __dmul_rn(r64, r64))) status = 0;
+            if (!aabb_keep64(3, lo, hi, c64, __dmul_rn(r64, r64))) status[v] = 0;
           }
         }
       }
-      // representative probe (see rep_probe)
-      bool hit = false;
-      if (status == 2) {
-        const uint2 st = __ldg(t.set + leaf);
-        const unsigned m4 = (st.y + 3u) & ~3u;
-        const float* pb = reinterpret_cast<const float*>(t.data + st.x);
-        const float dx = cx[v] - __ldg(pb), dy = cy[v] - __ldg(pb + m4),
-                    dz = cz[v] - __ldg(pb + 2 * m4);
-        hit = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) <= r2 * band_lo;
+      // representative probe (see rep_probe); the rep section is loaded
+      // alongside the box, not through the set
+      if (status[v] == 2) {
+        const float4 rp = __ldg(t.rep + leaf[v]);
+        const float dx = cx[v] - rp.x, dy = cy[v] - rp.y, dz = cz[v] - rp.z;
+        hit[v] = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) <= r2 * band_lo;
       }
-      if (hit) a.verdict[q] = 1;
-      bool resolved = hit;
-      if (a.L > 1) resolved = (__ballot_sync(0xffffffffu, hit) & seg) != 0;
-      if (resolved) status = 0;
-      record_bin(a, q, status, leaf);
+      if (hit[v]) a.verdict[base + v * blockDim.x + threadIdx.x] = 1;
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      bool resolved = hit[v];
+      if (a.L > 1) resolved = (__ballot_sync(0xffffffffu, hit[v]) & seg) != 0;
+      if (resolved) status[v] = 0;
+    }
+    // per-leaf counts only (fire-and-forget reductions, nothing waits on
+    // them); the rank inside the leaf is drawn by K3
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int q = base + v * blockDim.x + threadIdx.x;
+      const bool scan = status[v] == 2;
+      const unsigned act = __ballot_sync(0xffffffffu, scan);
+      if (scan) {
+        const unsigned peers = __match_any_sync(act, unsigned(leaf[v]));
+        if (lane == __ffs(peers) - 1) atomicAdd(a.counts + leaf[v], __popc(peers));
+      }
+      if (q < n) __stcs(a.leafid + q, scan ? leaf[v] : -1);
+      if (status[v] == 3) {
+        const unsigned j = atomicAdd(a.slow_n, 1u);
+        a.slow[j] = make_int2(q, leaf[v]);
+      }
     }
   }
 }
@@ -382,21 +397,41 @@ __global__ void __launch_bounds__(256) k_bin_scatter(BinArgs a) {
   const int64_t per_iter = int64_t(gridDim.x) * blockDim.x * V;
   // every load of the V spheres is issued before any store (memory-level
   // parallelism: this kernel is latency-bound otherwise)
+  const int lane = threadIdx.x & 31;
   for (int64_t base = int64_t(blockIdx.x) * blockDim.x * V; base < a.n; base += per_iter) {
-    int2 sl[V];
+    int leaf[V];
     int64_t qv[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       qv[v] = base + int64_t(v) * blockDim.x + threadIdx.x;
-      sl[v] = qv[v] < a.n ? __ldcs(a.slot + qv[v]) : make_int2(-1, 0);
+      leaf[v] = qv[v] < a.n ? __ldcs(a.leafid + qv[v]) : -1;
+    }
+    // rank inside the leaf: warp-aggregated cursor atomics, all V issued
+    // before any result is consumed
+    unsigned peers[V], tk[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const unsigned act = __ballot_sync(0xffffffffu, leaf[v] >= 0);
+      peers[v] = 0;
+      tk[v] = 0;
+      if (leaf[v] >= 0) {
+        peers[v] = __match_any_sync(act, unsigned(leaf[v]));
+        if (lane == __ffs(peers[v]) - 1) tk[v] = atomicAdd(a.cursor + leaf[v], __popc(peers[v]));
+      }
     }
     uint32_t st[V];
     float4 rc[V];
+    int2 sl[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      const bool on = sl[v].x >= 0;
+      const bool on = leaf[v] >= 0;
+      sl[v] = make_int2(leaf[v], 0);
+      if (on) {
+        const unsigned b = __shfl_sync(peers[v], tk[v], __ffs(peers[v]) - 1);
+        sl[v].y = int(b + __popc(peers[v] & ((1u << lane) - 1u)));
+      }
       const int64_t q = on ? qv[v] : 0;
-      st[v] = __ldg(a.start + (on ? sl[v].x : 0));
+      st[v] = __ldg(a.start + (on ? leaf[v] : 0));
       float c[3] = {0.f, 0.f, 0.f}, r;
       if constexpr (std::is_same<InT, float>::value) {
         const float* cf = static_cast<const float*>(a.centers);
@@ -854,9 +889,10 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.rid = A.get<int>(n);
   a.verdict = A.get<uint8_t>(n + 8);
   a.slow = A.get<int2>(n);
-  a.slot = A.get<int2>(n);
+  a.leafid = A.get<int>(n);
+  a.cursor = A.get<uint32_t>(nl);
   if (!ctr || !a.counts || !a.start || !tcount || !tstart || !a.tiles || !a.rec || !a.rid ||
-      !a.verdict || !a.slow || !a.slot)
+      !a.verdict || !a.slow || !a.leafid || !a.cursor)
     return fail(CAPT_ENOMEM, "binned scratch allocation");
   {
     float lo = float(t.r_min), hi = float(t.r_max);
@@ -872,6 +908,7 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   CAPT_CUDA(cudaMemsetAsync(ctr, 0, 32, s));
   a.n_pass_b = ctr + 4;
   CAPT_CUDA(cudaMemsetAsync(a.counts, 0, 4 * nl, s));
+  CAPT_CUDA(cudaMemsetAsync(a.cursor, 0, 4 * nl, s));
   CAPT_CUDA(cudaMemsetAsync(a.verdict, 0, n + 8, s));
   const bool f64 = flags & CAPT_INPUT_F64;
   const int G = grid_for(n, 256, 8);
@@ -890,7 +927,7 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   k_tile_counts<<<Gl, 256, 0, s>>>(nl, a.counts, tcount);
   CAPT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, tcount, tstart, nl, s));
   k_make_tiles<<<Gl, 256, 0, s>>>(nl, tcount, tstart, a.tiles, a.n_tiles);
-  constexpr int VS = 8;
+  constexpr int VS = 4;
   const int G8 = grid_for((n + VS - 1) / VS, 256, 8);
   if (f64) k_bin_scatter<double, VS><<<G8, 256, 0, s>>>(a);
   else k_bin_scatter<float, VS><<<G8, 256, 0, s>>>(a);

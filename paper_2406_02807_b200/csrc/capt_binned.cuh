@@ -26,7 +26,8 @@ struct BinArgs {
   uint32_t* n_refined;
   uint32_t* n_pass_b;   // spheres left unresolved by the probe pass (debug)
   unsigned long long* first_bad;
-  int2* slot;         // per sphere: (leaf, rank within leaf) if binned, else (-1, 0)
+  int* leafid;        // per sphere: leaf if binned, else -1
+  uint32_t* cursor;   // per leaf: scatter cursor (K3)
   float rlo_f, rhi_f; // fp32 images of the double band edges
 };
 

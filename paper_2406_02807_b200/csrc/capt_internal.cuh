@@ -12,6 +12,7 @@
 //   org    float4[n]                binned-scan origin of each set: centre of the
 //                                   finite points' box (xyz) and the largest
 //                                   fp32 |p - o|^2 over the set (w)
+//   rep    float4[n]                row 0 of each set (xyz), loaded beside the box
 #pragma once
 
 #include <cuda_runtime.h>
@@ -24,7 +25,7 @@
 namespace capt {
 
 constexpr uint64_t kSlabMagic = 0x3030324254504143ull;  // "CAPTB200"
-constexpr int kSlabVersion = 2;
+constexpr int kSlabVersion = 3;
 constexpr int kMaxK = 3;
 
 struct SlabHeader {
@@ -43,7 +44,8 @@ struct SlabHeader {
   int64_t data_f4;    // float4 count of the data section
   int64_t bytes;      // slab size
   int64_t off_org;    // byte offset of the org section
-  int64_t reserved[9];
+  int64_t off_rep;    // byte offset of the rep section
+  int64_t reserved[8];
 };
 static_assert(sizeof(SlabHeader) <= 256, "header must fit its 256-B section");
 
@@ -57,6 +59,7 @@ struct DevTree {
   const int64_t* offs;
   const float4* data;
   const float4* org;
+  const float4* rep;  // row 0 of every set (the point owning the cell), +inf for padding
 };
 
 }  // namespace capt
@@ -100,6 +103,7 @@ inline DevTree view(const capt_tree* t) {
   d.offs = reinterpret_cast<const int64_t*>(t->slab + t->h.off_offs);
   d.data = reinterpret_cast<const float4*>(t->slab + t->h.off_data);
   d.org = reinterpret_cast<const float4*>(t->slab + t->h.off_org);
+  d.rep = reinterpret_cast<const float4*>(t->slab + t->h.off_rep);
   return d;
 }
 
@@ -118,6 +122,8 @@ inline int64_t layout_slab(SlabHeader& h, int64_t data_f4) {
   h.off_offs = off;
   off = align256(off + sizeof(int64_t) * (h.n + 1));
   h.off_org = off;
+  off = align256(off + sizeof(float4) * h.n);
+  h.off_rep = off;
   off = align256(off + sizeof(float4) * h.n);
   h.off_data = off;
   off = align256(off + sizeof(float4) * (data_f4 > 0 ? data_f4 : 1));

@@ -163,7 +163,10 @@ __global__ void k_origins(DevTree t) {
       bb = fmaxf(bb, fmaf(bz, bz, fmaf(by, by, bx * bx)));
     }
     for (int s = 16; s > 0; s >>= 1) bb = fmaxf(bb, __shfl_xor_sync(0xffffffffu, bb, s));
-    if (lane == 0) const_cast<float4*>(t.org)[j] = make_float4(o[0], o[1], o[2], bb);
+    if (lane == 0) {
+      const_cast<float4*>(t.org)[j] = make_float4(o[0], o[1], o[2], bb);
+      const_cast<float4*>(t.rep)[j] = make_float4(base[0], base[m4], base[2 * m4], 0.f);
+    }
   }
 }
 
