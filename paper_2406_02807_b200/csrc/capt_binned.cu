@@ -927,7 +927,7 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   k_tile_counts<<<Gl, 256, 0, s>>>(nl, a.counts, tcount);
   CAPT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, tcount, tstart, nl, s));
   k_make_tiles<<<Gl, 256, 0, s>>>(nl, tcount, tstart, a.tiles, a.n_tiles);
-  constexpr int VS = 4;
+  constexpr int VS = 8;
   const int G8 = grid_for((n + VS - 1) / VS, 256, 8);
   if (f64) k_bin_scatter<double, VS><<<G8, 256, 0, s>>>(a);
   else k_bin_scatter<float, VS><<<G8, 256, 0, s>>>(a);
@@ -947,11 +947,14 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   note_launches(9);  // count, 2 scans, tile counts, tiles, scatter, scan, slow, pack
   static const bool debug = getenv("CAPT_DEBUG") != nullptr;
   if (debug) {
-    uint32_t h[8];
+    uint32_t h[8], last[2];
     CAPT_CUDA(cudaMemcpyAsync(h, ctr, 32, cudaMemcpyDeviceToHost, s));
+    CAPT_CUDA(cudaMemcpyAsync(last, a.start + nl - 1, 4, cudaMemcpyDeviceToHost, s));
+    CAPT_CUDA(cudaMemcpyAsync(last + 1, a.counts + nl - 1, 4, cudaMemcpyDeviceToHost, s));
     CAPT_CUDA(cudaStreamSynchronize(s));
-    fprintf(stderr, "[capt binned] n=%lld exact_queue=%u tiles=%u refined=%u pass_b=%u\n",
-            (long long)n, h[0], h[1], h[3], h[4]);
+    fprintf(stderr,
+            "[capt binned] n=%lld binned=%u exact_queue=%u tiles=%u refined=%u pass_b=%u\n",
+            (long long)n, last[0] + last[1], h[0], h[1], h[3], h[4]);
   }
   return CAPT_OK;
 }
