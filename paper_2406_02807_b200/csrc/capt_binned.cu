@@ -41,6 +41,11 @@ constexpr int kS = 8;              // spheres per thread (4 packed pairs)
 constexpr int kTS = kBT * kS;      // spheres per tile
 constexpr int kChunk = 768;        // staged points per shared-memory chunk
 constexpr float kBand = 0x1p-18f;  // 64u
+// Probe pass + repack inside K5 (every 4th point pair first).  Off: since K1
+// resolves representative hits (and their groups) before binning, the binned
+// spheres are mostly misses and the probe resolved only ~14% of them on
+// config 1 -- less than its overhead.
+constexpr bool kProbePass = false;
 
 template <typename InT>
 __device__ __forceinline__ void load_sphere(const void* c, const void* r, int64_t q, int k,
@@ -699,7 +704,7 @@ __global__ void __launch_bounds__(kBT, 5) k_binned_scan(BinArgs a) {
     for (int e = tid; e < nslot * kS; e += kBT) S.minkey[e] = 0xffffffffu;
     for (int e = tid; e < nslot; e += kBT) S.hitmask[e] = 0;
 
-    if (m <= kChunk) {
+    if (kProbePass && m <= kChunk) {
       // ---- probe pass over every 4th point pair, then repack the spheres
       //      that are still unresolved and scan the remaining pairs ----
       const uint32_t len2 = (m + 1u) & ~1u;
