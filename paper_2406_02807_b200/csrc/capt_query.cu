@@ -277,10 +277,8 @@ int query_device(const DevTree& t, const void* d_c, const void* d_r, int64_t n, 
 // verdict copy-back of chunk i-1).  Chunks are multiples of 32 lane groups,
 // so every chunk owns whole verdict words.
 struct PipeState {
-  cudaStream_t w[2] = {nullptr, nullptr};    // host-buffer pipeline
-  cudaStream_t dw[2] = {nullptr, nullptr};   // device-resident chunk overlap
+  cudaStream_t w[2] = {nullptr, nullptr};
   cudaEvent_t start = nullptr, done[2] = {nullptr, nullptr};
-  cudaEvent_t dstart = nullptr, ddone[2] = {nullptr, nullptr};
   unsigned long long* pinned = nullptr;  // per chunk: first_bad + 6 counters
   static constexpr int kMaxChunks = 1024;
 };
@@ -293,71 +291,14 @@ static PipeState* pipe_state(int device) {
   if (!init[device]) {
     for (int i = 0; i < 2; ++i) {
       cudaStreamCreateWithFlags(&p.w[i], cudaStreamNonBlocking);
-      cudaStreamCreateWithFlags(&p.dw[i], cudaStreamNonBlocking);
       cudaEventCreateWithFlags(&p.done[i], cudaEventDisableTiming);
-      cudaEventCreateWithFlags(&p.ddone[i], cudaEventDisableTiming);
     }
     cudaEventCreateWithFlags(&p.start, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&p.dstart, cudaEventDisableTiming);
     cudaHostAlloc(reinterpret_cast<void**>(&p.pinned),
                   sizeof(unsigned long long) * 7 * PipeState::kMaxChunks, cudaHostAllocDefault);
     init[device] = true;
   }
   return p.pinned ? &p : nullptr;
-}
-
-__global__ void k_combine_bad(const unsigned long long* __restrict__ slots, int n_chunks,
-                              int64_t chunk, unsigned long long* __restrict__ out) {
-  unsigned long long best = ~0ull;
-  for (int i = 0; i < n_chunks; ++i)
-    if (slots[i] != ~0ull) {
-      const unsigned long long v = static_cast<unsigned long long>(i) * chunk + slots[i];
-      best = v < best ? v : best;
-    }
-  *out = best;
-}
-
-// Device-resident binned queries on large batches: chunks alternate between
-// two streams so the latency-bound kernels of neighbouring chunks (classify,
-// scatter, scan) overlap on the SMs.  Returns CAPT_OK and sets *handled when
-// it took the batch.
-int query_device_overlapped(int device, const DevTree& t, const void* d_c, const void* d_r,
-                            int64_t n, int L, const uint8_t* d_m, uint32_t flags,
-                            uint32_t* d_bits, unsigned long long* d_bad, cudaStream_t s,
-                            bool* handled) {
-  constexpr int64_t kChunkSpheres = int64_t(1) << 23;  // multiple of 32 * L
-  *handled = false;
-  if (n <= kChunkSpheres || (flags & CAPT_STATS) || !binned_preferred(t, n, flags)) return CAPT_OK;
-  const int64_t n_chunks = (n + kChunkSpheres - 1) / kChunkSpheres;
-  PipeState* p = pipe_state(device);
-  if (!p || n_chunks > PipeState::kMaxChunks) return CAPT_OK;
-  *handled = true;
-  const size_t in_elem = (flags & CAPT_INPUT_F64) ? sizeof(double) : sizeof(float);
-  unsigned long long* slots = nullptr;
-  if (d_bad) CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&slots), 8 * n_chunks, s));
-  CAPT_CUDA(cudaEventRecord(p->dstart, s));
-  for (int i = 0; i < 2; ++i) CAPT_CUDA(cudaStreamWaitEvent(p->dw[i], p->dstart, 0));
-  for (int64_t ci = 0; ci < n_chunks; ++ci) {
-    cudaStream_t w = p->dw[ci & 1];
-    const int64_t base = ci * kChunkSpheres;
-    const int64_t len = n - base < kChunkSpheres ? n - base : kChunkSpheres;
-    const int rc = query_device(t, static_cast<const char*>(d_c) + in_elem * t.k * base,
-                                static_cast<const char*>(d_r) + in_elem * base, len, L,
-                                d_m ? d_m + base : nullptr, flags, d_bits + base / L / 32,
-                                nullptr, slots ? slots + ci : nullptr, w);
-    if (rc) return rc;
-  }
-  for (int i = 0; i < 2; ++i) {
-    CAPT_CUDA(cudaEventRecord(p->ddone[i], p->dw[i]));
-    CAPT_CUDA(cudaStreamWaitEvent(s, p->ddone[i], 0));
-  }
-  if (slots) {
-    k_combine_bad<<<1, 1, 0, s>>>(slots, int(n_chunks), kChunkSpheres, d_bad);
-    CAPT_CUDA(cudaGetLastError());
-    note_launches(1);
-    CAPT_CUDA(cudaFreeAsync(slots, s));
-  }
-  return CAPT_OK;
 }
 
 int query_host_pipelined(const capt_tree* tree, const DevTree& t, const void* centers,
@@ -493,16 +434,7 @@ extern "C" int capt_query(const capt_tree* tree, const void* centers, const void
     d_bad = io.first_bad;
   }
   {
-    bool handled = false;
-    int rc = CAPT_OK;
-    if (!host) {
-      uint32_t fl = flags;
-      if (!d_bad) fl &= ~CAPT_CHECK_RADII;
-      rc = query_device_overlapped(tree->device, t, d_c, d_r, n, L, d_m, fl, d_bits, d_bad, s,
-                                   &handled);
-    }
-    if (rc == CAPT_OK && !handled)
-      rc = query_device(t, d_c, d_r, n, L, d_m, flags, d_bits, d_cnt, d_bad, s);
+    const int rc = query_device(t, d_c, d_r, n, L, d_m, flags, d_bits, d_cnt, d_bad, s);
     if (rc) return rc;
   }
   if (host) {

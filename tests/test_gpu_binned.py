@@ -167,24 +167,3 @@ def test_host_pipeline_chunks_counters_and_bad_radius():
     r_bad[7_000_000] = 0.001
     with pytest.raises(ValueError, match="radius 0.5 outside"):
         P.collides_many(tree, c, r_bad)
-
-
-def test_device_overlapped_chunks_and_bad_radius():
-    # device-resident batch > 8M spheres: chunks alternate between two
-    # streams; bits and the combined first-bad index must be exact
-    import torch
-    cloud = W.cfg1_cloud()
-    t = O.construct(cloud, 0.02, 0.08)
-    tree = upload(t)
-    c, r = W.cfg1_queries(cloud, n_groups=(5 << 19) + 64, seed=78)  # ~21M spheres, 3 chunks
-    exp = O.collides_groups(t, c, r, 8)
-    cd, rd = torch.from_numpy(c).cuda(), torch.from_numpy(r).cuda()
-    bad = torch.full((1,), -1, dtype=torch.int64, device="cuda")
-    words = P.query_bits(tree, cd, rd, 8, first_bad=bad)
-    got = np.unpackbits(words.cpu().numpy().view(np.uint8), bitorder="little")[: len(exp)]
-    assert np.array_equal(got.astype(bool), exp)
-    assert int(bad.item()) == -1
-    rd[(1 << 23) + 12345] = 0.5
-    rd[(2 << 23) + 7] = 0.001
-    P.query_bits(tree, cd, rd, 8, first_bad=bad)
-    assert int(bad.item()) == (1 << 23) + 12345
