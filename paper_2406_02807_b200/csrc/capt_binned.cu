@@ -3,12 +3,16 @@
 // The reference itself groups spheres by leaf and scans each affordance set
 // once as a dense (spheres x points) distance matrix (query.py:209-218).  On
 // B200 that becomes:
-//   K1 k_bin_count    per sphere: band check, descent, fp32 AABB reject
-//                     (float64 fix-up in the band), warp-aggregated per-leaf
-//                     histogram; spheres needing the exact path go to a list
+//   K1 k_bin_count3   per sphere: band check, descent (top 13 levels in smem),
+//                     fp32 AABB reject (float64 fix-up in the band), the
+//                     representative probe (a definite hit resolves the sphere
+//                     and its whole lane group), warp-aggregated per-leaf
+//                     counts; spheres needing the exact path go to a queue
+//                     (k_bin_count: generic k / float64 inputs)
 //   K2 (CUB scans)    per-leaf start offsets and tile counts
-//   K3 k_bin_scatter  recompute the leaf, scatter a float4 {c, r} record and
-//                     the sphere id into leaf order (slot = start + K1 ticket)
+//   K3 k_bin_scatter  rank inside the leaf (warp-aggregated cursor atomics),
+//                     scatter a float4 {c, r} record + the sphere id to
+//                     start[leaf] + rank
 //   K4 k_make_tiles   (leaf, chunk of <= 1024 spheres) work items
 //   K5 k_binned_scan  persistent CTAs pull tiles from an atomic counter; the
 //                     leaf's set is staged once into shared memory in local
@@ -18,9 +22,8 @@
 //                         min = min3(min, t_j, t_j+1)   (FMNMX3)
 //                     a sphere collides iff min_t <= r^2 - |a|^2; a proven
 //                     error band (64u relative to |a|^2 + |b|^2 + r^2) sends
-//                     the rare ambiguous sphere to an exact float64 rescan
-//                     done cooperatively by the CTA
-//   K6 k_slow         exact float64 scan for the K1 list
+//                     the rare ambiguous sphere to the exact queue
+//   K6 k_slow         exact float64 scan of the queue, one warp per sphere
 //   K7 k_pack         verdict bytes -> bit words, OR over each lane group
 #include <cub/cub.cuh>
 
@@ -41,11 +44,6 @@ constexpr int kS = 8;              // spheres per thread (4 packed pairs)
 constexpr int kTS = kBT * kS;      // spheres per tile
 constexpr int kChunk = 768;        // staged points per shared-memory chunk
 constexpr float kBand = 0x1p-18f;  // 64u
-// Probe pass + repack inside K5 (every 4th point pair first).  Off: since K1
-// resolves representative hits (and their groups) before binning, the binned
-// spheres are mostly misses and the probe resolved only ~14% of them on
-// config 1 -- less than its overhead.
-constexpr bool kProbePass = false;
 
 template <typename InT>
 __device__ __forceinline__ void load_sphere(const void* c, const void* r, int64_t q, int k,
@@ -182,11 +180,8 @@ __device__ __forceinline__ int rep_probe(const BinArgs& a, int64_t q, int status
                                          float cx, float cy, float cz, float r) {
   bool hit = false;
   if (status == 2) {
-    const DevTree& t = a.t;
-    const uint2 st = __ldg(t.set + leaf);
-    const uint32_t m4 = (st.y + 3u) & ~3u;
-    const float* base = reinterpret_cast<const float*>(t.data + st.x);
-    const float dx = cx - __ldg(base), dy = cy - __ldg(base + m4), dz = cz - __ldg(base + 2 * m4);
+    const float4 rp = __ldg(a.t.rep + leaf);
+    const float dx = cx - rp.x, dy = cy - rp.y, dz = cz - rp.z;
     const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
     hit = d2 <= (r * r) * (1.0f - kTau);
   }
@@ -516,10 +511,8 @@ __device__ __forceinline__ float okey_inv(uint32_t u) {
 struct __align__(16) SmemBinned {
   ulonglong2 A[kChunk];  // {bx,bx}, {by,by}
   ulonglong2 B[kChunk];  // {bz,bz}, {w,w}
-  uint32_t minkey[kTS];  // per sphere: running min over phases / passes
+  uint32_t minkey[kTS];  // per sphere: min over the phases (orderable key)
   uint32_t hitmask[kTS / kS];
-  int list[kTS];         // spheres still unresolved after the probe pass
-  int n_list;
   int tile;
 };
 
@@ -532,11 +525,10 @@ struct Spheres8 {
   uint32_t real;
 };
 
-// list == nullptr: tile-local spheres slot*kS + i; else list[slot*kS + i].
-// init_min: start from the min recorded in S.minkey (second pass).
+// The tile-local spheres slot*kS .. slot*kS + kS-1 (those < count).
 __device__ __forceinline__ void load_spheres(Spheres8& sp, const BinArgs& a, int64_t s0,
-                                             const float4 org, const int* list, int count,
-                                             int slot, bool active, const uint32_t* minkey) {
+                                             const float4 org, int count, int slot,
+                                             bool active) {
   const float INF = __int_as_float(0x7f800000);
   sp.real = 0;
 #pragma unroll
@@ -548,10 +540,9 @@ __device__ __forceinline__ void load_spheres(Spheres8& sp, const BinArgs& a, int
       sp.sidx[i + h] = -1;
       sp.mn[i + h] = INF;
       if (active && e < count) {
-        const int sl = list ? list[e] : e;
-        sp.sidx[i + h] = sl;
+        sp.sidx[i + h] = e;
         sp.real |= 1u << (i + h);
-        const float4 rc = a.rec[s0 + sl];
+        const float4 rc = a.rec[s0 + e];
         const float ax = rc.x - org.x, ay = rc.y - org.y, az = rc.z - org.z;
         const float aa = fmaf(az, az, fmaf(ay, ay, ax * ax));
         const float r2 = rc.w * rc.w;
@@ -560,7 +551,6 @@ __device__ __forceinline__ void load_spheres(Spheres8& sp, const BinArgs& a, int
         kz[h] = -2.f * az;
         sp.thr[i + h] = r2 - aa;
         sp.band[i + h] = kBand * (aa + org.w + r2);
-        if (minkey) sp.mn[i + h] = okey_inv(minkey[sl]);
       } else {
         kx[h] = ky[h] = kz[h] = 0.f;
         sp.thr[i + h] = -INF;
@@ -601,9 +591,8 @@ __device__ __forceinline__ void test_pair(Spheres8& sp, const ulonglong2* sA, co
   }
 }
 
-// Pairs u = 4g + o for o in [OB, OE), g = ph, ph + P, ...  Stops early once
-// every sphere of the slot is a definite hit (hitmask shared by the phases).
-template <int OB, int OE>
+// Pairs u = 4g .. 4g+3 for g = ph, ph + P, ...  Stops early once every
+// sphere of the slot is a definite hit (hitmask shared by the phases).
 __device__ __forceinline__ void scan_pairs(Spheres8& sp, const ulonglong2* sA,
                                            const ulonglong2* sB, int npairs, int ph, int P,
                                            uint32_t* hitmask) {
@@ -611,7 +600,7 @@ __device__ __forceinline__ void scan_pairs(Spheres8& sp, const ulonglong2* sA,
   int it = 0;
   for (int g = ph; g < ngroups; g += P) {
 #pragma unroll
-    for (int o = OB; o < OE; ++o) {
+    for (int o = 0; o < 4; ++o) {
       const int u = 4 * g + o;
       if (u < npairs) test_pair(sp, sA, sB, u);
     }
@@ -677,10 +666,7 @@ __global__ void __launch_bounds__(kBT, 5) k_binned_scan(BinArgs a) {
   const DevTree& t = a.t;
   const int tid = threadIdx.x;
   while (true) {
-    if (tid == 0) {
-      S.tile = int(atomicAdd(a.tile_ctr, 1u));
-      S.n_list = 0;
-    }
+    if (tid == 0) S.tile = int(atomicAdd(a.tile_ctr, 1u));
     __syncthreads();
     const int tile = S.tile;
     if (tile >= int(*a.n_tiles)) break;
@@ -694,91 +680,41 @@ __global__ void __launch_bounds__(kBT, 5) k_binned_scan(BinArgs a) {
     const uint32_t m4 = (m + 3u) & ~3u;
     const float* xs = reinterpret_cast<const float*>(t.data + st.x);
 
-    int nslot = (cnt + kS - 1) / kS;
-    int P = max(1, kBT / nslot);
-    bool active = tid < nslot * P;
-    int slot = tid % nslot;
-    int ph = tid / nslot;
+    // thread -> (sphere slot of kS spheres, phase over the point pairs)
+    const int nslot = (cnt + kS - 1) / kS;
+    const int P = max(1, kBT / nslot);
+    const bool active = tid < nslot * P;
+    const int slot = tid % nslot;
+    const int ph = tid / nslot;
     Spheres8 sp;
-    load_spheres(sp, a, s0, org, nullptr, cnt, slot, active, nullptr);
+    load_spheres(sp, a, s0, org, cnt, slot, active);
     for (int e = tid; e < nslot * kS; e += kBT) S.minkey[e] = 0xffffffffu;
     for (int e = tid; e < nslot; e += kBT) S.hitmask[e] = 0;
 
-    if (kProbePass && m <= kChunk) {
-      // ---- probe pass over every 4th point pair, then repack the spheres
-      //      that are still unresolved and scan the remaining pairs ----
-      const uint32_t len2 = (m + 1u) & ~1u;
-      stage_points(sA, sB, xs, m4, 0, m, len2, org);
+    // stream the set through shared memory in chunks of kChunk points
+    bool done = sp.real == 0;
+    for (uint32_t c0 = 0; c0 < m; c0 += kChunk) {
+      const uint32_t len = min(uint32_t(kChunk), m - c0);
+      const uint32_t len2 = (len + 1u) & ~1u;
+      __syncthreads();  // previous chunk consumed, inits visible
+      stage_points(sA, sB, xs, m4, c0, len, len2, org);
       __syncthreads();
-      const int npairs = int(len2 / 2);
-      if (sp.real) scan_pairs<0, 1>(sp, sA, sB, npairs, ph, P, &S.hitmask[slot]);
-      if (P > 1 && active) {
-#pragma unroll
-        for (int i = 0; i < kS; ++i)
-          if ((sp.real >> i) & 1u) atomicMin(&S.minkey[sp.sidx[i]], okey(sp.mn[i]));
+      if (!done) {
+        scan_pairs(sp, sA, sB, int(len2 / 2), ph, P, &S.hitmask[slot]);
+        uint32_t h = definite_hits(sp);
+        if (P > 1) h |= *reinterpret_cast<volatile uint32_t*>(&S.hitmask[slot]);
+        done = (h & sp.real) == sp.real;
       }
-      __syncthreads();
-      if (active && ph == 0) {
-        const uint32_t hm = S.hitmask[slot];
-#pragma unroll
-        for (int i = 0; i < kS; ++i) {
-          if (!((sp.real >> i) & 1u)) continue;
-          const float mv = P > 1 ? okey_inv(S.minkey[sp.sidx[i]]) : sp.mn[i];
-          if (((hm >> i) & 1u) || mv <= sp.thr[i] - sp.band[i]) {
-            a.verdict[a.rid[s0 + sp.sidx[i]]] = 1;
-          } else {
-            S.minkey[sp.sidx[i]] = okey(mv);
-            S.list[atomicAdd(&S.n_list, 1)] = sp.sidx[i];
-          }
-        }
-      }
-      __syncthreads();
-      const int nu = S.n_list;
-      if (tid == 0) atomicAdd(a.n_pass_b, unsigned(nu));
-      if (nu > 0) {
-        nslot = (nu + kS - 1) / kS;
-        P = max(1, kBT / nslot);
-        active = tid < nslot * P;
-        slot = tid % nslot;
-        ph = tid / nslot;
-        load_spheres(sp, a, s0, org, S.list, nu, slot, active, S.minkey);
-        __syncthreads();  // everyone has read the probe minima
-        for (int e = tid; e < nslot; e += kBT) S.hitmask[e] = 0;
-        __syncthreads();
-        if (sp.real) scan_pairs<1, 4>(sp, sA, sB, npairs, ph, P, &S.hitmask[slot]);
-        if (P > 1 && active) {
-#pragma unroll
-          for (int i = 0; i < kS; ++i)
-            if ((sp.real >> i) & 1u) atomicMin(&S.minkey[sp.sidx[i]], okey(sp.mn[i]));
-        }
-        __syncthreads();
-        if (active && ph == 0) decide(sp, a, s0, leaf, S.hitmask[slot], S.minkey, P > 1);
-      }
-    } else {
-      // ---- large sets: stream the set through shared memory in chunks ----
-      bool done = sp.real == 0;
-      for (uint32_t c0 = 0; c0 < m; c0 += kChunk) {
-        const uint32_t len = min(uint32_t(kChunk), m - c0);
-        const uint32_t len2 = (len + 1u) & ~1u;
-        __syncthreads();  // previous chunk consumed
-        stage_points(sA, sB, xs, m4, c0, len, len2, org);
-        __syncthreads();
-        if (!done) {
-          scan_pairs<0, 4>(sp, sA, sB, int(len2 / 2), ph, P, &S.hitmask[slot]);
-          uint32_t h = definite_hits(sp);
-          if (P > 1) h |= *reinterpret_cast<volatile uint32_t*>(&S.hitmask[slot]);
-          done = (h & sp.real) == sp.real;
-        }
-      }
-      if (P > 1 && active) {
-#pragma unroll
-        for (int i = 0; i < kS; ++i)
-          if ((sp.real >> i) & 1u) atomicMin(&S.minkey[sp.sidx[i]], okey(sp.mn[i]));
-      }
-      __syncthreads();
-      if (active && ph == 0) decide(sp, a, s0, leaf, S.hitmask[slot], S.minkey, P > 1);
     }
-    __syncthreads();  // tile state (list, minkey, smem points) free for the next tile
+    // combine the phases' minima, then each slot's owner decides
+    if (P > 1 && active) {
+#pragma unroll
+      for (int i = 0; i < kS; ++i)
+        if ((sp.real >> i) & 1u) atomicMin(&S.minkey[sp.sidx[i]], okey(sp.mn[i]));
+    }
+    __syncthreads();
+    if (active && ph == 0) decide(sp, a, s0, leaf, S.hitmask[slot], S.minkey, P > 1);
+    __syncthreads();  // tile state (minkey, hitmask, smem points) free for the next tile
   }
 }
 
@@ -884,7 +820,7 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.flags = flags;
   a.first_bad = first_bad;
   const int64_t nl = t.n;
-  uint32_t* ctr = A.get<uint32_t>(8);  // slow_n, n_tiles, tile_ctr, n_refined, n_pass_b
+  uint32_t* ctr = A.get<uint32_t>(4);  // slow_n, n_tiles, tile_ctr, n_refined
   a.counts = A.get<uint32_t>(nl);
   a.start = A.get<uint32_t>(nl);
   uint32_t* tcount = A.get<uint32_t>(nl);
@@ -910,8 +846,7 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.n_tiles = ctr + 1;
   a.tile_ctr = ctr + 2;
   a.n_refined = ctr + 3;
-  CAPT_CUDA(cudaMemsetAsync(ctr, 0, 32, s));
-  a.n_pass_b = ctr + 4;
+  CAPT_CUDA(cudaMemsetAsync(ctr, 0, 16, s));
   CAPT_CUDA(cudaMemsetAsync(a.counts, 0, 4 * nl, s));
   CAPT_CUDA(cudaMemsetAsync(a.cursor, 0, 4 * nl, s));
   CAPT_CUDA(cudaMemsetAsync(a.verdict, 0, n + 8, s));
@@ -952,14 +887,13 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   note_launches(9);  // count, 2 scans, tile counts, tiles, scatter, scan, slow, pack
   static const bool debug = getenv("CAPT_DEBUG") != nullptr;
   if (debug) {
-    uint32_t h[8], last[2];
-    CAPT_CUDA(cudaMemcpyAsync(h, ctr, 32, cudaMemcpyDeviceToHost, s));
+    uint32_t h[4], last[2];
+    CAPT_CUDA(cudaMemcpyAsync(h, ctr, 16, cudaMemcpyDeviceToHost, s));
     CAPT_CUDA(cudaMemcpyAsync(last, a.start + nl - 1, 4, cudaMemcpyDeviceToHost, s));
     CAPT_CUDA(cudaMemcpyAsync(last + 1, a.counts + nl - 1, 4, cudaMemcpyDeviceToHost, s));
     CAPT_CUDA(cudaStreamSynchronize(s));
-    fprintf(stderr,
-            "[capt binned] n=%lld binned=%u exact_queue=%u tiles=%u refined=%u pass_b=%u\n",
-            (long long)n, last[0] + last[1], h[0], h[1], h[3], h[4]);
+    fprintf(stderr, "[capt binned] n=%lld binned=%u exact_queue=%u tiles=%u refined=%u\n",
+            (long long)n, last[0] + last[1], h[0], h[1], h[3]);
   }
   return CAPT_OK;
 }

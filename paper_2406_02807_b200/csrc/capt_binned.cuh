@@ -24,7 +24,6 @@ struct BinArgs {
   uint32_t* n_tiles;
   uint32_t* tile_ctr;
   uint32_t* n_refined;
-  uint32_t* n_pass_b;   // spheres left unresolved by the probe pass (debug)
   unsigned long long* first_bad;
   int* leafid;        // per sphere: leaf if binned, else -1
   uint32_t* cursor;   // per leaf: scatter cursor (K3)
