@@ -42,7 +42,7 @@ namespace {
 constexpr int kBT = 128;           // threads per binned CTA
 constexpr int kS = 8;              // spheres per thread (4 packed pairs)
 constexpr int kTS = kBT * kS;      // spheres per tile
-constexpr int kChunk = 768;        // staged points per shared-memory chunk
+constexpr int kChunk = 512;        // staged points per shared-memory chunk
 constexpr float kBand = 0x1p-18f;  // 64u
 
 template <typename InT>
@@ -512,35 +512,40 @@ struct __align__(16) SmemBinned {
   ulonglong2 A[kChunk];  // {bx,bx}, {by,by}
   ulonglong2 B[kChunk];  // {bz,bz}, {w,w}
   uint32_t minkey[kTS];  // per sphere: min over the phases (orderable key)
+  float lim_lo[kTS];     // per sphere: thr - band (min <= it: definite hit)
+  float lim_hi[kTS];     // per sphere: thr + band (min > it: definite miss)
   uint32_t hitmask[kTS / kS];
   int tile;
 };
 
 // Eight spheres of one thread in local coordinates of the set origin o:
 // t = |b|^2 - 2 a.b compared with thr = r^2 - |a|^2 (a = c - o, b = p - o).
+// Only the packed -2a and the running minima live in registers; the decision
+// limits sit in shared memory (read every 8 point groups and at the end).
 struct Spheres8 {
   unsigned long long Kx[kS / 2], Ky[kS / 2], Kz[kS / 2];
-  float thr[kS], band[kS], mn[kS];
-  int sidx[kS];
-  uint32_t real;
+  float mn[kS];
+  int base;        // tile-local index of sphere 0 of this slot
+  uint32_t real;   // bit i: sphere base + i exists
 };
 
-// The tile-local spheres slot*kS .. slot*kS + kS-1 (those < count).
-__device__ __forceinline__ void load_spheres(Spheres8& sp, const BinArgs& a, int64_t s0,
-                                             const float4 org, int count, int slot,
-                                             bool active) {
+// The tile-local spheres slot*kS .. slot*kS + kS-1 (those < count); the
+// slot's owner (phase 0) writes their decision limits.
+__device__ __forceinline__ void load_spheres(Spheres8& sp, SmemBinned& S, const BinArgs& a,
+                                             int64_t s0, const float4 org, int count, int slot,
+                                             bool active, bool owner) {
   const float INF = __int_as_float(0x7f800000);
   sp.real = 0;
+  sp.base = slot * kS;
 #pragma unroll
   for (int i = 0; i < kS; i += 2) {
     float kx[2], ky[2], kz[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int e = slot * kS + i + h;
-      sp.sidx[i + h] = -1;
+      const int e = sp.base + i + h;
       sp.mn[i + h] = INF;
+      kx[h] = ky[h] = kz[h] = 0.f;
       if (active && e < count) {
-        sp.sidx[i + h] = e;
         sp.real |= 1u << (i + h);
         const float4 rc = a.rec[s0 + e];
         const float ax = rc.x - org.x, ay = rc.y - org.y, az = rc.z - org.z;
@@ -549,12 +554,11 @@ __device__ __forceinline__ void load_spheres(Spheres8& sp, const BinArgs& a, int
         kx[h] = -2.f * ax;
         ky[h] = -2.f * ay;
         kz[h] = -2.f * az;
-        sp.thr[i + h] = r2 - aa;
-        sp.band[i + h] = kBand * (aa + org.w + r2);
-      } else {
-        kx[h] = ky[h] = kz[h] = 0.f;
-        sp.thr[i + h] = -INF;
-        sp.band[i + h] = 0.f;
+        if (owner) {
+          const float thr = r2 - aa, band = kBand * (aa + org.w + r2);
+          S.lim_lo[e] = thr - band;
+          S.lim_hi[e] = thr + band;
+        }
       }
     }
     sp.Kx[i / 2] = pack2(kx[0], kx[1]);
@@ -563,11 +567,12 @@ __device__ __forceinline__ void load_spheres(Spheres8& sp, const BinArgs& a, int
   }
 }
 
-__device__ __forceinline__ uint32_t definite_hits(const Spheres8& sp) {
+__device__ __forceinline__ uint32_t definite_hits(const Spheres8& sp, const float* lim_lo) {
   uint32_t h = 0;
 #pragma unroll
-  for (int i = 0; i < kS; ++i) h |= uint32_t(sp.mn[i] <= sp.thr[i] - sp.band[i]) << i;
-  return h & sp.real;
+  for (int i = 0; i < kS; ++i)
+    if ((sp.real >> i) & 1u) h |= uint32_t(sp.mn[i] <= lim_lo[sp.base + i]) << i;
+  return h;
 }
 
 // One point pair (2u, 2u+1) against the thread's 8 spheres: 12 FFMA2 + 8 FMNMX3.
@@ -595,7 +600,7 @@ __device__ __forceinline__ void test_pair(Spheres8& sp, const ulonglong2* sA, co
 // sphere of the slot is a definite hit (hitmask shared by the phases).
 __device__ __forceinline__ void scan_pairs(Spheres8& sp, const ulonglong2* sA,
                                            const ulonglong2* sB, int npairs, int ph, int P,
-                                           uint32_t* hitmask) {
+                                           uint32_t* hitmask, const float* lim_lo) {
   const int ngroups = (npairs + 3) / 4;
   int it = 0;
   for (int g = ph; g < ngroups; g += P) {
@@ -605,7 +610,7 @@ __device__ __forceinline__ void scan_pairs(Spheres8& sp, const ulonglong2* sA,
       if (u < npairs) test_pair(sp, sA, sB, u);
     }
     if ((++it & 7) == 0) {
-      uint32_t h = definite_hits(sp);
+      uint32_t h = definite_hits(sp, lim_lo);
       if (P > 1) {
         if (h) atomicOr(hitmask, h);
         h |= *reinterpret_cast<volatile uint32_t*>(hitmask);
@@ -613,7 +618,7 @@ __device__ __forceinline__ void scan_pairs(Spheres8& sp, const ulonglong2* sA,
       if ((h & sp.real) == sp.real) break;
     }
   }
-  const uint32_t h = definite_hits(sp);
+  const uint32_t h = definite_hits(sp, lim_lo);
   if (h) atomicOr(hitmask, h);
 }
 
@@ -640,17 +645,17 @@ __device__ __forceinline__ void stage_points(ulonglong2* sA, ulonglong2* sB, con
 
 // Final decision for a slot's spheres: definite hit -> verdict byte, definite
 // miss -> nothing, inside the error band -> exact float64 path (k_slow).
-__device__ __forceinline__ void decide(const Spheres8& sp, const BinArgs& a, int64_t s0,
-                                       int64_t leaf, uint32_t hm, const uint32_t* minkey,
-                                       bool combined) {
+__device__ __forceinline__ void decide(const Spheres8& sp, const SmemBinned& S, const BinArgs& a,
+                                       int64_t s0, int64_t leaf, uint32_t hm, bool combined) {
 #pragma unroll
   for (int i = 0; i < kS; ++i) {
     if (!((sp.real >> i) & 1u)) continue;
-    const float mv = combined ? okey_inv(minkey[sp.sidx[i]]) : sp.mn[i];
-    const int q = a.rid[s0 + sp.sidx[i]];
-    if (((hm >> i) & 1u) || mv <= sp.thr[i] - sp.band[i]) {
+    const int e = sp.base + i;
+    const float mv = combined ? okey_inv(S.minkey[e]) : sp.mn[i];
+    const int q = a.rid[s0 + e];
+    if (((hm >> i) & 1u) || mv <= S.lim_lo[e]) {
       a.verdict[q] = 1;
-    } else if (!(mv > sp.thr[i] + sp.band[i])) {
+    } else if (!(mv > S.lim_hi[e])) {
       const unsigned j = atomicAdd(a.slow_n, 1u);
       a.slow[j] = make_int2(q, int(leaf));
       atomicAdd(a.n_refined, 1u);
@@ -658,7 +663,7 @@ __device__ __forceinline__ void decide(const Spheres8& sp, const BinArgs& a, int
   }
 }
 
-__global__ void __launch_bounds__(kBT, 5) k_binned_scan(BinArgs a) {
+__global__ void __launch_bounds__(kBT, 7) k_binned_scan(BinArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SmemBinned& S = *reinterpret_cast<SmemBinned*>(smem_raw);
   ulonglong2* const sA = S.A;
@@ -687,7 +692,7 @@ __global__ void __launch_bounds__(kBT, 5) k_binned_scan(BinArgs a) {
     const int slot = tid % nslot;
     const int ph = tid / nslot;
     Spheres8 sp;
-    load_spheres(sp, a, s0, org, cnt, slot, active);
+    load_spheres(sp, S, a, s0, org, cnt, slot, active, active && ph == 0);
     for (int e = tid; e < nslot * kS; e += kBT) S.minkey[e] = 0xffffffffu;
     for (int e = tid; e < nslot; e += kBT) S.hitmask[e] = 0;
 
@@ -696,12 +701,12 @@ __global__ void __launch_bounds__(kBT, 5) k_binned_scan(BinArgs a) {
     for (uint32_t c0 = 0; c0 < m; c0 += kChunk) {
       const uint32_t len = min(uint32_t(kChunk), m - c0);
       const uint32_t len2 = (len + 1u) & ~1u;
-      __syncthreads();  // previous chunk consumed, inits visible
+      __syncthreads();  // previous chunk consumed, inits and limits visible
       stage_points(sA, sB, xs, m4, c0, len, len2, org);
       __syncthreads();
       if (!done) {
-        scan_pairs(sp, sA, sB, int(len2 / 2), ph, P, &S.hitmask[slot]);
-        uint32_t h = definite_hits(sp);
+        scan_pairs(sp, sA, sB, int(len2 / 2), ph, P, &S.hitmask[slot], S.lim_lo);
+        uint32_t h = definite_hits(sp, S.lim_lo);
         if (P > 1) h |= *reinterpret_cast<volatile uint32_t*>(&S.hitmask[slot]);
         done = (h & sp.real) == sp.real;
       }
@@ -710,10 +715,10 @@ __global__ void __launch_bounds__(kBT, 5) k_binned_scan(BinArgs a) {
     if (P > 1 && active) {
 #pragma unroll
       for (int i = 0; i < kS; ++i)
-        if ((sp.real >> i) & 1u) atomicMin(&S.minkey[sp.sidx[i]], okey(sp.mn[i]));
+        if ((sp.real >> i) & 1u) atomicMin(&S.minkey[sp.base + i], okey(sp.mn[i]));
     }
     __syncthreads();
-    if (active && ph == 0) decide(sp, a, s0, leaf, S.hitmask[slot], S.minkey, P > 1);
+    if (active && ph == 0) decide(sp, S, a, s0, leaf, S.hitmask[slot], P > 1);
     __syncthreads();  // tile state (minkey, hitmask, smem points) free for the next tile
   }
 }
