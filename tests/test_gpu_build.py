@@ -105,3 +105,61 @@ def test_build_rejects_bad_input():
         P.construct(P.PointCloud(np.empty((0, 3), np.float32)), P.BuildParams(0.01, 0.08))
     with pytest.raises(ValueError):
         P.BuildParams(0.0, 1.0)
+
+
+def _leaf_cells(tests, n, k, leaves):
+    """Cell walls of the given leaves replayed from T (conftest.py:11-31 pattern)."""
+    depth = int(n).bit_length() - 1
+    lo = np.full((n, k), -np.inf)
+    hi = np.full((n, k), np.inf)
+    for j in leaves:
+        node = 0
+        for L in range(depth):
+            a = L % k
+            right = (j >> (depth - 1 - L)) & 1
+            t = float(tests[node])
+            if right:
+                lo[j, a] = t
+            else:
+                hi[j, a] = t
+            node = 2 * node + 1 + right
+    return lo, hi
+
+
+def test_build_cfg3_full_scale_properties():
+    """Config 3 at full size (262,144 points, ~475 M stored points): the
+    per-leaf affordance sets of sampled leaves equal the brute-force
+    definition {rep} U {p : dist^2(p, cell) <= r_max^2} (tree.py:164-218),
+    boxes are the sets' min/max, and sampled query verdicts equal brute force."""
+    from paper_2406_02807_b200 import workloads as W
+    cloud = W.cfg3_cloud()
+    tree = P.construct(P.PointCloud(cloud), P.BuildParams(0.01, 0.1))
+    assert tree.n == 262144
+    st = tree.stats()
+    assert st.total_stored == int(tree.offsets[-1]) and st.max_affordance > 1000
+    rng = np.random.default_rng(0)
+    leaves = rng.choice(tree.n, 64, replace=False)
+    lo, hi = _leaf_cells(tree.tests, tree.n, 3, leaves)
+    pts = cloud.astype(np.float64)
+    for j in leaves:
+        aset = tree.affordance_set(int(j)).astype(np.float64)
+        res = np.maximum(np.maximum(lo[j] - pts, 0.0), pts - hi[j])
+        d2 = (res[:, 0] ** 2 + res[:, 1] ** 2) + res[:, 2] ** 2
+        rep = aset[0]
+        corner = np.maximum(np.abs(rep - lo[j]), np.abs(rep - hi[j]))
+        if ((corner[0] ** 2 + corner[1] ** 2) + corner[2] ** 2) <= 0.01 ** 2:
+            assert len(aset) == 1
+            continue
+        want = pts[d2 <= 0.1 ** 2]
+        got = aset[1:]
+        # the rep itself is the only member not counted among the afforded
+        # points of *other* leaves; compare as multisets with the rep removed once
+        w = sorted(map(tuple, want))
+        w.remove(tuple(rep))
+        assert sorted(map(tuple, got)) == w, int(j)
+        assert np.array_equal(tree.aff_lo[j], aset.min(0).astype(np.float32))
+        assert np.array_equal(tree.aff_hi[j], aset.max(0).astype(np.float32))
+    c, r = W.cfg3_queries(1 << 22, seed=103)
+    got = P.collides_many(tree, c, r)
+    sample = rng.choice(len(r), 20000, replace=False)
+    assert np.array_equal(got[sample], O.brute_collides_many(cloud, c[sample], r[sample]))
