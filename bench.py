@@ -54,6 +54,10 @@ def parse():
     ap.add_argument("--mode", default="auto", choices=["auto", "direct", "binned"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", action="store_true",
+                    help="config-4 batch-size x collision-rate sweep (one JSON object)")
+    ap.add_argument("--sweep-max-exp", type=int, default=13,
+                    help="largest batch is 4^this spheres (14 -> 268M, needs ~4.3 GB)")
     return ap.parse_args()
 
 
@@ -196,6 +200,8 @@ def main():
 
     if args.impl == "reference":
         return main_reference(args, rank, world)
+    if args.sweep:
+        return main_sweep(args)
 
     import torch
     import torch.distributed as dist
@@ -356,6 +362,58 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def main_sweep(args):
+    """Config 4 (BASELINE.json configs[4]): batch size (4^5 .. 4^14 spheres) x
+    collision rate (0, 10, 50, 90, 100 %) on the config-1 cloud, per-sphere
+    verdicts.  Each rate's spheres come from a 4M-sphere labelled pool
+    (colliding / rejection-sampled free centres, workloads.cfg4_queries) tiled
+    to the batch size; the pool's verdicts are checked against its labels.
+    Prints one JSON object with the grid."""
+    import torch
+    import paper_2406_02807_b200 as P
+    from paper_2406_02807_b200 import _lib
+
+    dev = torch.device("cuda", 0)
+    cloud = W.cfg1_cloud()
+    tree = P.construct(P.PointCloud(cloud), P.BuildParams(0.02, 0.08), device=0)
+    pool_n = 1 << 22
+    max_exp = args.sweep_max_exp
+    rows = []
+    for rate in (0.0, 0.1, 0.5, 0.9, 1.0):
+        c, r, label = W.cfg4_queries(cloud, pool_n, rate, seed=104)
+        cd, rd = torch.from_numpy(c).to(dev), torch.from_numpy(r).to(dev)
+        words = P.query_bits(tree, cd, rd, 1, check_radii=False)
+        got = np.unpackbits(words.cpu().numpy().view(np.uint8), bitorder="little")[:pool_n]
+        label_ok = bool(np.array_equal(got.astype(bool), label))
+        for e in range(5, max_exp + 1):
+            n = 4 ** e
+            reps = -(-n // pool_n)
+            cN = cd.repeat(reps, 1)[:n].contiguous() if reps > 1 else cd[:n].contiguous()
+            rN = rd.repeat(reps)[:n].contiguous() if reps > 1 else rd[:n].contiguous()
+            out = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
+            stream = torch.cuda.current_stream(dev)
+            for _ in range(3):
+                P.query_bits(tree, cN, rN, 1, out=out, check_radii=False,
+                             stream=stream.cuda_stream)
+            steps = max(3, min(200, int(2e8 // n)))
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(steps):
+                P.query_bits(tree, cN, rN, 1, out=out, check_radii=False,
+                             stream=stream.cuda_stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / steps
+            mode = "binned" if n >= (1 << 18) and n >= 16 * tree.n else "direct"
+            rows.append({"rate": rate, "n": n, "ms": ms, "queries_per_s": n / (ms * 1e-3),
+                         "mode": mode, "labels_match": label_ok})
+            del cN, rN, out
+    print(json.dumps({"sweep": "cfg4 batch size x collision rate", "n_gpus": 1,
+                      "tree_leaves": tree.n, "pool": pool_n, "rows": rows}))
 
 
 def main_reference(args, rank, world):
