@@ -408,9 +408,32 @@ def main_sweep(args):
             e1.record(stream)
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / steps
+            # the same query captured once in a CUDA graph and replayed: device
+            # latency without the per-call Python/ctypes dispatch
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                P.query_bits(tree, cN, rN, 1, out=out, check_radii=False,
+                             stream=side.cuda_stream)
+                with torch.cuda.graph(g, stream=side):
+                    P.query_bits(tree, cN, rN, 1, out=out, check_radii=False,
+                                 stream=side.cuda_stream)
+            stream.wait_stream(side)
+            for _ in range(3):
+                g.replay()
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(steps):
+                g.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms_graph = e0.elapsed_time(e1) / steps
             mode = "binned" if n >= (1 << 18) and n >= 16 * tree.n else "direct"
             rows.append({"rate": rate, "n": n, "ms": ms, "queries_per_s": n / (ms * 1e-3),
+                         "ms_graph": ms_graph, "queries_per_s_graph": n / (ms_graph * 1e-3),
                          "mode": mode, "labels_match": label_ok})
+            del g
             del cN, rN, out
     print(json.dumps({"sweep": "cfg4 batch size x collision rate", "n_gpus": 1,
                       "tree_leaves": tree.n, "pool": pool_n, "rows": rows}))
