@@ -41,8 +41,10 @@ extern "C" {
 #define CAPT_STATS 0x4u       /* fill counters[0..3] (see capt_query)           */
 #define CAPT_INPUT_F64 0x8u   /* centers/radii are double (else float)          */
 #define CAPT_HOST_IO 0x10u    /* all array arguments are host memory; blocking  */
-#define CAPT_MODE_DIRECT 0x100u /* force the one-thread-per-sphere kernel      */
+#define CAPT_MODE_DIRECT 0x100u /* force the unbinned (warp-per-sphere) kernel */
 #define CAPT_MODE_BINNED 0x200u /* force the leaf-binned kernels               */
+#define CAPT_MODE_THREAD 0x400u /* force the one-thread-per-sphere kernel
+                                   (always used with CAPT_STATS)               */
 
 typedef struct capt_tree capt_tree;
 

@@ -13,6 +13,8 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libcapt_b200.so")
+# experiments only: load a variant built with build_ext --out (never rebuilt)
+VARIANT = os.environ.get("CAPT_LIB_VARIANT")
 
 CAPT_OK, CAPT_EINVAL, CAPT_ERANGE, CAPT_ECUDA, CAPT_ENOMEM = range(5)
 PREFILTER = 0x1
@@ -22,6 +24,7 @@ INPUT_F64 = 0x8
 HOST_IO = 0x10
 MODE_DIRECT = 0x100
 MODE_BINNED = 0x200
+MODE_THREAD = 0x400
 
 
 class CaptTreeInfo(C.Structure):
@@ -48,7 +51,7 @@ def lib():
         except Exception as exc:  # noqa: BLE001 - surface the real cause below
             if not os.path.exists(LIB_PATH):
                 raise RuntimeError(f"libcapt_b200.so is not built and building failed: {exc}")
-    L = C.CDLL(LIB_PATH)
+    L = C.CDLL(os.path.join(HERE, VARIANT) if VARIANT else LIB_PATH)
     vp, i64, i32, u32, dbl = C.c_void_p, C.c_int64, C.c_int, C.c_uint32, C.c_double
     L.capt_last_error.restype = C.c_char_p
     L.capt_version.restype = C.c_int

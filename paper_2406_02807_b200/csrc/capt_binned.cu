@@ -51,11 +51,15 @@ __device__ __forceinline__ void load_sphere(const void* c, const void* r, int64_
   c64[0] = c64[1] = c64[2] = 0.0;
   if constexpr (std::is_same<InT, float>::value) {
     const float* cf = static_cast<const float*>(c);
-    for (int d = 0; d < k; ++d) c64[d] = double(__ldg(cf + q * k + d));
+#pragma unroll
+    for (int d = 0; d < kMaxK; ++d)
+      if (d < k) c64[d] = double(__ldg(cf + q * k + d));
     r64 = double(__ldg(static_cast<const float*>(r) + q));
   } else {
     const double* cd = static_cast<const double*>(c);
-    for (int d = 0; d < k; ++d) c64[d] = __ldg(cd + q * k + d);
+#pragma unroll
+    for (int d = 0; d < kMaxK; ++d)
+      if (d < k) c64[d] = __ldg(cd + q * k + d);
     r64 = __ldg(static_cast<const double*>(r) + q);
   }
 }
@@ -663,7 +667,10 @@ __device__ __forceinline__ void decide(const Spheres8& sp, const SmemBinned& S, 
   }
 }
 
-__global__ void __launch_bounds__(kBT, 7) k_binned_scan(BinArgs a) {
+#ifndef CAPT_K5_MINB
+#define CAPT_K5_MINB 6
+#endif
+__global__ void __launch_bounds__(kBT, CAPT_K5_MINB) k_binned_scan(BinArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SmemBinned& S = *reinterpret_cast<SmemBinned*>(smem_raw);
   ulonglong2* const sA = S.A;
@@ -743,7 +750,9 @@ __global__ void k_slow(BinArgs a) {
     bool hit = false;
     for (uint32_t j = lane; j < st.y && !hit; j += 32) {
       double sum = 0.0;
-      for (int d = 0; d < t.k; ++d) {
+#pragma unroll
+      for (int d = 0; d < kMaxK; ++d) {
+        if (d >= t.k) break;
         const double x = __dsub_rn(c64[d], double(base[d * m4 + j]));
         const double sq = __dmul_rn(x, x);
         sum = d == 0 ? sq : __dadd_rn(sum, sq);
@@ -797,7 +806,7 @@ struct Arena {
 
 bool binned_preferred(const DevTree& t, int64_t n, uint32_t flags) {
   if (flags & CAPT_STATS) return false;
-  if (flags & CAPT_MODE_DIRECT) return false;
+  if (flags & (CAPT_MODE_DIRECT | CAPT_MODE_THREAD)) return false;
   if (n >= (int64_t(1) << 31)) return false;
   if (flags & CAPT_MODE_BINNED) return true;
   return n >= (int64_t(1) << 18) && n >= 16 * t.n;

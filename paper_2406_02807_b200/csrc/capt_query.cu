@@ -1,8 +1,11 @@
 // Batched sphere-vs-point-cloud collision query (the hot path).
 //
 // Replaces collides_many (query.py:184-219) and collides_batch(...).
-// any_collision (query.py:126-167).  Two kernel families:
-//   * direct  (this file): one thread per sphere -- branchless Eytzinger
+// any_collision (query.py:126-167).  Three kernels:
+//   * warp    (this file, k_query_warp): one warp per sphere / lane group,
+//     the latency path for batches too small to bin (see below).
+//   * thread  (this file, k_query_direct, also the CAPT_STATS counter
+//     kernel): one thread per sphere -- branchless Eytzinger
 //     descent with the top 12 levels in shared memory (tree.py:266-273),
 //     fp32 leaf-AABB reject (query.py:202-208), float4 SoA scan of the
 //     affordance set (query.py:96-99), warp-ballot bit packing, and for
@@ -39,7 +42,9 @@ struct SphereIn<float> {
                               double& r64) {
     const float* cf = static_cast<const float*>(c);
     c64[0] = c64[1] = c64[2] = 0.0;
-    for (int d = 0; d < k; ++d) c64[d] = double(__ldg(cf + q * k + d));
+#pragma unroll
+    for (int d = 0; d < kMaxK; ++d)
+      if (d < k) c64[d] = double(__ldg(cf + q * k + d));
     r64 = double(__ldg(static_cast<const float*>(r) + q));
   }
 };
@@ -49,7 +54,9 @@ struct SphereIn<double> {
                               double& r64) {
     const double* cd = static_cast<const double*>(c);
     c64[0] = c64[1] = c64[2] = 0.0;
-    for (int d = 0; d < k; ++d) c64[d] = __ldg(cd + q * k + d);
+#pragma unroll
+    for (int d = 0; d < kMaxK; ++d)
+      if (d < k) c64[d] = __ldg(cd + q * k + d);
     r64 = __ldg(static_cast<const double*>(r) + q);
   }
 };
@@ -198,6 +205,140 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-per-sphere kernel (latency path for batches too small to bin).
+//
+// One warp owns one lane group (L spheres, scanned in lane order with the
+// reference's early exit, query.py:152-160).  For each sphere the 32 lanes
+//   * descend 5 Eytzinger levels per round: lane j loads node j of the
+//     31-node subtree under the current node, the path is then walked with
+//     shuffles -- one L1/L2 round trip per 5 levels instead of per level;
+//   * scan the affordance set cooperatively, 128 points per iteration
+//     (coalesced SoA loads), with a warp vote after every iteration;
+//   * re-run the exact float64 scan cooperatively for band/slow spheres.
+// ---------------------------------------------------------------------------
+template <typename C>
+__device__ __forceinline__ int64_t warp_descend(const DevTree& t, const C c[3], int lane) {
+  int64_t i = 0;
+  int ax = 0;
+  for (int s = 0; s < t.depth;) {
+    const int lv = min(5, t.depth - s);
+    const int nodes = (1 << lv) - 1;
+    float tv = 0.f;
+    if (lane < nodes) {
+      const int lvl = 31 - __clz(lane + 1);
+      const int64_t g = ((i + 1) << lvl) - 1 + (lane + 1 - (1 << lvl));
+      tv = __ldg(t.T + g);
+    }
+    int j = 0;
+    for (int r = 0; r < lv; ++r) {
+      const float v = __shfl_sync(0xffffffffu, tv, j);
+      j = 2 * j + 1 + (pick3(c, ax) > C(v) ? 1 : 0);
+      ax = (ax + 1 == t.k) ? 0 : ax + 1;
+    }
+    i = ((i + 1) << lv) - 1 + (j + 1 - (1 << lv));
+    s += lv;
+  }
+  return i - (t.n - 1);
+}
+
+// fp32 cooperative scan: 0 = no point within the band, 1 = definite hit,
+// 2 = some point inside the error band (decide exactly).
+__device__ __forceinline__ int warp_scan_f32(const DevTree& t, uint2 set, float cx, float cy,
+                                             float cz, float loB, float hiB, int lane) {
+  const float* xs = reinterpret_cast<const float*>(t.data + set.x);
+  const uint32_t m4 = (set.y + 3u) & ~3u;
+  bool amb = false;
+  for (uint32_t p0 = 0; p0 < set.y; p0 += 128) {
+    float x[4], y[4], z[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t p = p0 + j * 32 + lane;
+      x[j] = y[j] = z[j] = __int_as_float(0x7f800000);
+      if (p < m4) {
+        x[j] = __ldg(xs + p);
+        y[j] = __ldg(xs + m4 + p);
+        z[j] = __ldg(xs + 2 * m4 + p);
+      }
+    }
+    bool hit = false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float dx = cx - x[j], dy = cy - y[j], dz = cz - z[j];
+      const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+      hit |= d2 <= loB;
+      amb |= d2 < hiB;
+    }
+    if (__any_sync(0xffffffffu, hit)) return 1;
+  }
+  return __any_sync(0xffffffffu, amb) ? 2 : 0;
+}
+
+// Exact reference scan (query.py:96-99), one point per lane per step.
+__device__ __forceinline__ bool warp_scan_f64(const DevTree& t, uint2 set, const double c[3],
+                                              double r64, int lane) {
+  const float* base = reinterpret_cast<const float*>(t.data + set.x);
+  const uint32_t m4 = (set.y + 3u) & ~3u;
+  const double R = __dmul_rn(r64, r64);
+  for (uint32_t p0 = 0; p0 < set.y; p0 += 32) {
+    const uint32_t p = p0 + lane;
+    bool hit = false;
+    if (p < set.y) {
+      double s = 0.0;
+#pragma unroll
+      for (int d = 0; d < kMaxK; ++d) {
+        if (d >= t.k) break;
+        const double x = __dsub_rn(c[d], double(__ldg(base + d * m4 + p)));
+        const double sq = __dmul_rn(x, x);
+        s = (d == 0) ? sq : __dadd_rn(s, sq);
+      }
+      hit = s <= R;
+    }
+    if (__any_sync(0xffffffffu, hit)) return true;
+  }
+  return false;
+}
+
+template <typename InT>
+__global__ void __launch_bounds__(kBlock)
+    k_query_warp(DevTree t, const void* __restrict__ centers, const void* __restrict__ radii,
+                 int64_t n, int L, const uint8_t* __restrict__ lane_mask, uint32_t flags,
+                 uint32_t* __restrict__ out_bits, unsigned long long* __restrict__ first_bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const bool prefilter = flags & CAPT_PREFILTER;
+  const bool check = flags & CAPT_CHECK_RADII;
+  const int64_t n_groups = n / L;
+  for (int64_t g = warp; g < n_groups; g += nwarps) {
+    bool verdict = false;
+    for (int l = 0; l < L; ++l) {
+      const int64_t q = g * L + l;
+      if (lane_mask && !lane_mask[q]) continue;
+      double c64[3], r64;
+      SphereIn<InT>::load(centers, radii, q, t.k, c64, r64);
+      if (check && lane == 0 && (r64 < t.r_min || r64 > t.r_max))
+        atomicMin(first_bad, static_cast<unsigned long long>(q));
+      if (verdict) continue;  // radii of later lanes are still checked
+      int64_t leaf;
+      if constexpr (std::is_same<InT, float>::value) {
+        const float cf[3] = {float(c64[0]), float(c64[1]), float(c64[2])};
+        leaf = warp_descend<float>(t, cf, lane);
+      } else {
+        leaf = warp_descend<double>(t, c64, lane);
+      }
+      const uint2 set = __ldg(t.set + leaf);
+      float cx, cy, cz, r2, loB, hiB;
+      const int status = classify(t, leaf, c64, r64, prefilter, cx, cy, cz, r2, loB, hiB);
+      if (status == ST_FALSE) continue;
+      int v = 2;
+      if (status == ST_SCAN) v = warp_scan_f32(t, set, cx, cy, cz, loB, hiB, lane);
+      verdict = (v == 1) || (v == 2 && warp_scan_f64(t, set, c64, r64, lane));
+    }
+    if (verdict && lane == 0) atomicOr(out_bits + (g >> 5), 1u << (g & 31));
+  }
+}
+
 template <typename InT>
 __global__ void k_leaf_indices(DevTree t, const void* __restrict__ centers, int64_t n,
                                int64_t* __restrict__ out) {
@@ -239,10 +380,21 @@ struct HostIO {
 int launch_direct(const DevTree& t, const void* centers, const void* radii, int64_t n, int L,
                   const uint8_t* mask, uint32_t flags, uint32_t* bits, int64_t n_words,
                   unsigned long long* counters, unsigned long long* first_bad, cudaStream_t s) {
-  const int64_t n_tiles = (n + kBlock - 1) / kBlock;
-  const int grid = grid_for(n_tiles * kBlock, kBlock, 8);
   const bool f64 = flags & CAPT_INPUT_F64;
   const bool stats = flags & CAPT_STATS;
+  if (!stats && !(flags & CAPT_MODE_THREAD)) {
+    if (L <= 8) CAPT_CUDA(cudaMemsetAsync(bits, 0, 4 * (n_words ? n_words : 1), s));
+    const int grid = grid_for((n / L) * 32, kBlock, 8);
+    if (f64)
+      k_query_warp<double><<<grid, kBlock, 0, s>>>(t, centers, radii, n, L, mask, flags, bits, first_bad);
+    else
+      k_query_warp<float><<<grid, kBlock, 0, s>>>(t, centers, radii, n, L, mask, flags, bits, first_bad);
+    CAPT_CUDA(cudaGetLastError());
+    note_launches(1);
+    return CAPT_OK;
+  }
+  const int64_t n_tiles = (n + kBlock - 1) / kBlock;
+  const int grid = grid_for(n_tiles * kBlock, kBlock, 8);
 #define LAUNCH(T, S) \
   k_query_direct<T, S><<<grid, kBlock, 0, s>>>(t, centers, radii, n, L, mask, flags, bits, n_words, counters, first_bad)
   if (f64) {

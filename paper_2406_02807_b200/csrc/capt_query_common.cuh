@@ -18,6 +18,12 @@ constexpr float kTau = 0x1p-19f;
 constexpr float kR2Min = 0x1p-100f;  // outside [kR2Min, kR2Max] -> float64 path
 constexpr float kR2Max = 0x1p100f;
 
+// c[ax] without dynamic indexing (keeps the centre in registers)
+template <typename C>
+__device__ __forceinline__ C pick3(const C c[3], int ax) {
+  return ax == 0 ? c[0] : (ax == 1 ? c[1] : c[2]);
+}
+
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -41,7 +47,7 @@ __device__ __forceinline__ int64_t descend_t(const DevTree& t, const float* sT, 
   int ax = 0;
   for (int s = 0; s < t.depth; ++s) {
     const float tv = (i < n_smem) ? sT[i] : __ldg(t.T + i);
-    i = 2 * i + 1 + (c[ax] > C(tv) ? 1 : 0);
+    i = 2 * i + 1 + (pick3(c, ax) > C(tv) ? 1 : 0);
     ax = (ax + 1 == t.k) ? 0 : ax + 1;
   }
   return i - (t.n - 1);
@@ -59,7 +65,9 @@ __device__ __forceinline__ bool aabb_keep64(int k, const float4 lo, const float4
   const double l[3] = {lo.x, lo.y, lo.z};
   const double h[3] = {hi.x, hi.y, hi.z};
   double s = 0.0;
-  for (int d = 0; d < k; ++d) {
+#pragma unroll
+  for (int d = 0; d < kMaxK; ++d) {
+    if (d >= k) break;
     double r = np_max(__dsub_rn(l[d], c[d]), 0.0);
     r = np_max(r, __dsub_rn(c[d], h[d]));
     const double sq = __dmul_rn(r, r);
@@ -77,7 +85,9 @@ static __device__ __noinline__ bool scan_f64(const DevTree& t, uint2 set, const 
   bool hit = false;
   for (uint32_t i = 0; i < set.y; ++i) {
     double s = 0.0;
-    for (int d = 0; d < t.k; ++d) {
+#pragma unroll
+    for (int d = 0; d < kMaxK; ++d) {
+      if (d >= t.k) break;
       const double x = __dsub_rn(c[d], double(__ldg(base + d * m4 + i)));
       const double sq = __dmul_rn(x, x);
       s = (d == 0) ? sq : __dadd_rn(s, sq);
@@ -99,7 +109,8 @@ __device__ __forceinline__ int classify(const DevTree& t, int64_t leaf, const do
                                         double r64, bool prefilter, float& cx, float& cy,
                                         float& cz, float& r2, float& loB, float& hiB) {
   bool cfin = true;
-  for (int d = 0; d < t.k; ++d) cfin &= isfinite(c64[d]);
+#pragma unroll
+  for (int d = 0; d < kMaxK; ++d) cfin &= d >= t.k || isfinite(c64[d]);
   // +-inf / NaN centres give inf or NaN distances: never a collision unless
   // r^2 itself overflows to inf (then the exact path decides)
   if (!cfin && __dmul_rn(r64, r64) <= 1.7976931348623157e308) return 0;

@@ -242,3 +242,39 @@ def test_infinite_radius_with_infinite_centre():
     for pre in (True, False):
         got = P.collides_many(tree, c, r, use_aabb_prefilter=pre, check_radii=False)
         assert np.array_equal(got, O.collides_many(t, c, r, use_aabb_prefilter=pre)), pre
+
+
+@pytest.mark.parametrize("mode", ["thread", "warp"])
+def test_unbinned_kernels(mode):
+    """Both unbinned kernels (one thread per sphere / one warp per sphere),
+    forced through the C-ABI flags, against the oracle: float and float64
+    inputs, non-finite and extreme values, every lane width, lane masks."""
+    from paper_2406_02807_b200 import _lib
+    from paper_2406_02807_b200 import workloads as W
+    from paper_2406_02807_b200.query import _host_query
+    flag = _lib.MODE_THREAD if mode == "thread" else _lib.MODE_DIRECT
+    cloud = W.cfg1_cloud()
+    t = O.construct(cloud, 0.02, 0.08)
+    tree = upload(t)
+    c, r = W.cfg1_queries(cloud, n_groups=1 << 12)
+    exp = O.collides_many(t, c, r)
+    for L in (1, 2, 8, 32):
+        gb, _, _ = _host_query(tree, c, r, 0, L, None, True, True, mode=flag)
+        assert np.array_equal(gb, exp.reshape(-1, L).any(1)), L
+    rng = np.random.default_rng(5)
+    m = rng.uniform(size=len(r)) < 0.7
+    gb, _, _ = _host_query(tree, c, r, 0, 8, m, True, True, mode=flag)
+    assert np.array_equal(gb, (exp & m).reshape(-1, 8).any(1))
+    c64 = c.astype(np.float64) + rng.normal(0, 1e-9, c.shape)
+    r64 = r.astype(np.float64)
+    gb, _, _ = _host_query(tree, c64, r64, _lib.INPUT_F64, 1, None, True, True, mode=flag)
+    assert np.array_equal(gb, O.collides_many(t, c64, r64))
+    # non-finite / extreme spheres, with and without the AABB prefilter
+    c2 = rng.uniform(-0.8, 0.8, (256, 3))
+    c2[:, 2] = rng.uniform(0, 0.3, 256)
+    r2 = rng.uniform(0.02, 0.08, 256)
+    c2[0, 0], c2[1, 1], c2[2, 2], c2[3] = np.nan, np.inf, -np.inf, 1e30
+    r2[4], r2[5], r2[6], r2[7], r2[8] = np.nan, 0.0, 1e30, -0.05, np.inf
+    for pre in (True, False):
+        gb, _, _ = _host_query(tree, c2, r2, _lib.INPUT_F64, 1, None, pre, False, mode=flag)
+        assert np.array_equal(gb, O.collides_many(t, c2, r2, use_aabb_prefilter=pre)), pre
