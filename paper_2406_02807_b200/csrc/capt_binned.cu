@@ -10,9 +10,9 @@
 //                     counts; spheres needing the exact path go to a queue
 //                     (k_bin_count: generic k / float64 inputs)
 //   K2 (CUB scans)    per-leaf start offsets and tile counts
-//   K3 k_bin_scatter  rank inside the leaf (warp-aggregated cursor atomics),
-//                     scatter a float4 {c, r} record + the sphere id to
-//                     start[leaf] + rank
+//   K3 k_bin_scatter  over K1's compact list of binned spheres: rank inside
+//                     the leaf (warp-aggregated cursor atomics), scatter the
+//                     float4 {c, r} record + the sphere id to start[leaf] + rank
 //   K4 k_make_tiles   (leaf, chunk of <= 1024 spheres) work items
 //   K5 k_binned_scan  persistent CTAs pull tiles from an atomic counter; the
 //                     leaf's set is staged once into shared memory in local
@@ -158,16 +158,25 @@ __device__ __forceinline__ int classify_f32(const DevTree& t, const float* sT, i
 }
 
 // Warp-collective: per-leaf histogram (warp-aggregated, fire-and-forget
-// atomics), per-sphere leaf id for K3, exact-path list.
-__device__ __forceinline__ void record_bin(const BinArgs& a, int64_t q, int status, int leaf) {
+// atomics), compact list entry for K3 (one list atomic per warp), exact-path
+// list.
+__device__ __forceinline__ void record_bin(const BinArgs& a, int64_t q, int status, int leaf,
+                                           float4 rc) {
   const bool scan = status == 2;
   const unsigned act = __ballot_sync(0xffffffffu, scan);
+  const int lane = threadIdx.x & 31;
+  unsigned lbase = 0;
+  if (act && lane == 0) lbase = atomicAdd(a.list_n, __popc(act));
   if (scan) {
-    const int lane = threadIdx.x & 31;
     const unsigned peers = __match_any_sync(act, unsigned(leaf));
     if (lane == __ffs(peers) - 1) atomicAdd(a.counts + leaf, __popc(peers));
   }
-  if (q < a.n) __stcs(a.leafid + q, scan ? leaf : -1);
+  lbase = __shfl_sync(0xffffffffu, lbase, 0);
+  if (scan) {
+    const unsigned j = lbase + __popc(act & ((1u << lane) - 1u));
+    a.lrec[j] = rc;
+    a.lmeta[j] = make_int2(int(q), leaf);
+  }
   if (status == 3) {
     const unsigned i = atomicAdd(a.slow_n, 1u);
     a.slow[i] = make_int2(int(q), leaf);
@@ -236,7 +245,7 @@ __global__ void __launch_bounds__(256) k_bin_count(BinArgs a) {
       else r = float(static_cast<const double*>(a.radii)[q]);
     }
     status = rep_probe(a, q, status, leaf, c[0], c[1], c[2], r);
-    record_bin(a, q, status, leaf);
+    record_bin(a, q, status, leaf, make_float4(c[0], c[1], c[2], r));
   }
 }
 
@@ -245,8 +254,11 @@ __global__ void __launch_bounds__(256) k_bin_count(BinArgs a) {
 // with byte offsets (child = 2*off + 4 + 4*(x > T): 4 instructions per level),
 // one plain atomic per binned sphere for its ticket.
 constexpr int kSmemNodes3 = 8191;
+#ifndef CAPT_K1_MINB
+#define CAPT_K1_MINB 4
+#endif
 template <int V>
-__global__ void __launch_bounds__(256) k_bin_count3(BinArgs a) {
+__global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
   __shared__ float sT[kSmemNodes3];
   const DevTree& t = a.t;
   const int n_smem = int(t.n - 1 < kSmemNodes3 ? t.n - 1 : kSmemNodes3);
@@ -373,93 +385,100 @@ __global__ void __launch_bounds__(256) k_bin_count3(BinArgs a) {
       if (a.L > 1) resolved = (__ballot_sync(0xffffffffu, hit[v]) & seg) != 0;
       if (resolved) status[v] = 0;
     }
-    // per-leaf counts only (fire-and-forget reductions, nothing waits on
-    // them); the rank inside the leaf is drawn by K3
+    // binned spheres go to the compact list (one returning atomic per warp,
+    // issued before the per-leaf counts so its latency overlaps them); the
+    // counts are fire-and-forget reductions; the rank inside the leaf is
+    // drawn by K3
+    unsigned act[V], tot = 0;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      act[v] = __ballot_sync(0xffffffffu, status[v] == 2);
+      tot += __popc(act[v]);
+    }
+    unsigned lbase = 0;
+    if (tot && lane == 0) lbase = atomicAdd(a.list_n, tot);
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int q = base + v * blockDim.x + threadIdx.x;
-      const bool scan = status[v] == 2;
-      const unsigned act = __ballot_sync(0xffffffffu, scan);
-      if (scan) {
-        const unsigned peers = __match_any_sync(act, unsigned(leaf[v]));
+      if (status[v] == 2) {
+        const unsigned peers = __match_any_sync(act[v], unsigned(leaf[v]));
         if (lane == __ffs(peers) - 1) atomicAdd(a.counts + leaf[v], __popc(peers));
       }
-      if (q < n) __stcs(a.leafid + q, scan ? leaf[v] : -1);
       if (status[v] == 3) {
         const unsigned j = atomicAdd(a.slow_n, 1u);
         a.slow[j] = make_int2(q, leaf[v]);
       }
     }
+    if (tot) {
+      unsigned j = __shfl_sync(0xffffffffu, lbase, 0);
+      const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        if (status[v] == 2) {
+          const unsigned p = j + __popc(act[v] & lt);
+          __stcs(a.lrec + p, make_float4(cx[v], cy[v], cz[v], r[v]));
+          __stcs(a.lmeta + p, make_int2(base + v * int(blockDim.x) + int(threadIdx.x), leaf[v]));
+        }
+        j += __popc(act[v]);
+      }
+    }
   }
 }
 
-// K3: scatter {c, r} records of binned spheres into leaf order (no atomics:
-// the slot is start[leaf] + the ticket drawn in K1)
-template <typename InT, int V>
+// K3: scatter the compact list into leaf order: rank inside the leaf from
+// warp-aggregated cursor atomics (all V issued before any result is used),
+// slot = start[leaf] + rank.  Persistent grid over the device-side count.
+#ifndef CAPT_K3_EXP
+#define CAPT_K3_EXP 0
+#endif
+template <int V>
 __global__ void __launch_bounds__(256) k_bin_scatter(BinArgs a) {
-  const int k = a.t.k;
-  const int64_t per_iter = int64_t(gridDim.x) * blockDim.x * V;
-  // every load of the V spheres is issued before any store (memory-level
-  // parallelism: this kernel is latency-bound otherwise)
+  const uint32_t n = *a.list_n;
   const int lane = threadIdx.x & 31;
-  for (int64_t base = int64_t(blockIdx.x) * blockDim.x * V; base < a.n; base += per_iter) {
-    int leaf[V];
-    int64_t qv[V];
+  const uint32_t per_iter = gridDim.x * blockDim.x * V;
+  for (uint32_t base = blockIdx.x * blockDim.x * V; base < n; base += per_iter) {
+    int2 meta[V];
+    float4 rc[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      qv[v] = base + int64_t(v) * blockDim.x + threadIdx.x;
-      leaf[v] = qv[v] < a.n ? __ldcs(a.leafid + qv[v]) : -1;
+      const uint32_t i = base + v * blockDim.x + threadIdx.x;
+      meta[v] = make_int2(-1, -1);
+      if (i < n) {
+        meta[v] = __ldcs(a.lmeta + i);
+        rc[v] = __ldcs(a.lrec + i);
+      }
     }
-    // rank inside the leaf: warp-aggregated cursor atomics, all V issued
-    // before any result is consumed
     unsigned peers[V], tk[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      const unsigned act = __ballot_sync(0xffffffffu, leaf[v] >= 0);
+      const unsigned act = __ballot_sync(0xffffffffu, meta[v].y >= 0);
       peers[v] = 0;
       tk[v] = 0;
-      if (leaf[v] >= 0) {
-        peers[v] = __match_any_sync(act, unsigned(leaf[v]));
-        if (lane == __ffs(peers[v]) - 1) tk[v] = atomicAdd(a.cursor + leaf[v], __popc(peers[v]));
+      if (meta[v].y >= 0) {
+        peers[v] = __match_any_sync(act, unsigned(meta[v].y));
+#if CAPT_K3_EXP == 1 || CAPT_K3_EXP == 3
+        if (lane == __ffs(peers[v]) - 1) tk[v] = 0;
+#else
+        if (lane == __ffs(peers[v]) - 1) tk[v] = atomicAdd(a.cursor + meta[v].y, __popc(peers[v]));
+#endif
       }
     }
     uint32_t st[V];
-    float4 rc[V];
-    int2 sl[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) st[v] = meta[v].y >= 0 ? __ldg(a.start + meta[v].y) : 0u;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      const bool on = leaf[v] >= 0;
-      sl[v] = make_int2(leaf[v], 0);
-      if (on) {
+      if (meta[v].y >= 0) {
         const unsigned b = __shfl_sync(peers[v], tk[v], __ffs(peers[v]) - 1);
-        sl[v].y = int(b + __popc(peers[v] & ((1u << lane) - 1u)));
-      }
-      const int64_t q = on ? qv[v] : 0;
-      st[v] = __ldg(a.start + (on ? leaf[v] : 0));
-      float c[3] = {0.f, 0.f, 0.f}, r;
-      if constexpr (std::is_same<InT, float>::value) {
-        const float* cf = static_cast<const float*>(a.centers);
-        if (k == 3) {
-          c[0] = __ldcs(cf + 3 * q);
-          c[1] = __ldcs(cf + 3 * q + 1);
-          c[2] = __ldcs(cf + 3 * q + 2);
-        } else {
-          for (int d = 0; d < k; ++d) c[d] = __ldcs(cf + q * k + d);
-        }
-        r = __ldcs(static_cast<const float*>(a.radii) + q);
-      } else {  // binned float64 inputs are exact fp32 values
-        const double* cd = static_cast<const double*>(a.centers);
-        for (int d = 0; d < k; ++d) c[d] = float(__ldg(cd + q * k + d));
-        r = float(__ldg(static_cast<const double*>(a.radii) + q));
-      }
-      rc[v] = make_float4(c[0], c[1], c[2], r);
-    }
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      if (sl[v].x >= 0) {
-        const int64_t pos = int64_t(st[v]) + sl[v].y;
+#if CAPT_K3_EXP == 1 || CAPT_K3_EXP == 2
+        const uint32_t pos = base + v * blockDim.x + threadIdx.x + (b & st[v] & 1u);
+#elif CAPT_K3_EXP == 3
+        const uint32_t pos = ((base + v * blockDim.x + threadIdx.x) * 2654435761u) % n + (b & st[v] & 1u) * 0;
+#else
+        const uint32_t pos = st[v] + b + __popc(peers[v] & ((1u << lane) - 1u));
+#endif
         a.rec[pos] = rc[v];
-        a.rid[pos] = int(qv[v]);
+        a.rid[pos] = meta[v].x;
       }
     }
   }
@@ -804,6 +823,45 @@ struct Arena {
 
 }  // namespace
 
+// CAPT_STAGE_TIMING=1: CUDA events between the pipeline stages (in-loop
+// times, unlike a serialised profiler pass), summed over calls and printed at
+// exit.  Diagnostics only; adds a synchronisation per call.
+struct StageTimer {
+  static constexpr int kStages = 6;
+  bool on = getenv("CAPT_STAGE_TIMING") != nullptr;
+  cudaEvent_t ev[kStages + 1] = {};
+  double sum[kStages] = {};
+  long calls = 0;
+  StageTimer() {
+    if (on)
+      for (auto& e : ev) cudaEventCreate(&e);
+  }
+  ~StageTimer() {
+    if (!on || !calls) return;
+    static const char* names[kStages] = {"memsets", "K1 count", "K2 scans+tiles", "K3 scatter",
+                                         "K5 scan", "K6+K7 slow+pack"};
+    double tot = 0;
+    for (double v : sum) tot += v;
+    fprintf(stderr, "[capt stages] %ld calls, mean us per call:", calls);
+    for (int i = 0; i < kStages; ++i) fprintf(stderr, " %s=%.1f", names[i], 1e3 * sum[i] / calls);
+    fprintf(stderr, " total=%.1f\n", 1e3 * tot / calls);
+  }
+  void mark(int i, cudaStream_t s) {
+    if (on) cudaEventRecord(ev[i], s);
+  }
+  void finish(cudaStream_t s) {
+    if (!on) return;
+    cudaEventSynchronize(ev[kStages]);
+    for (int i = 0; i < kStages; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+      sum[i] += ms;
+    }
+    ++calls;
+  }
+};
+static StageTimer g_stage_timer;
+
 bool binned_preferred(const DevTree& t, int64_t n, uint32_t flags) {
   if (flags & CAPT_STATS) return false;
   if (flags & (CAPT_MODE_DIRECT | CAPT_MODE_THREAD)) return false;
@@ -834,7 +892,7 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.flags = flags;
   a.first_bad = first_bad;
   const int64_t nl = t.n;
-  uint32_t* ctr = A.get<uint32_t>(4);  // slow_n, n_tiles, tile_ctr, n_refined
+  uint32_t* ctr = A.get<uint32_t>(5);  // slow_n, n_tiles, tile_ctr, n_refined, list_n
   a.counts = A.get<uint32_t>(nl);
   a.start = A.get<uint32_t>(nl);
   uint32_t* tcount = A.get<uint32_t>(nl);
@@ -844,10 +902,11 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.rid = A.get<int>(n);
   a.verdict = A.get<uint8_t>(n + 8);
   a.slow = A.get<int2>(n);
-  a.leafid = A.get<int>(n);
+  a.lrec = A.get<float4>(n);
+  a.lmeta = A.get<int2>(n);
   a.cursor = A.get<uint32_t>(nl);
   if (!ctr || !a.counts || !a.start || !tcount || !tstart || !a.tiles || !a.rec || !a.rid ||
-      !a.verdict || !a.slow || !a.leafid || !a.cursor)
+      !a.verdict || !a.slow || !a.lrec || !a.lmeta || !a.cursor)
     return fail(CAPT_ENOMEM, "binned scratch allocation");
   {
     float lo = float(t.r_min), hi = float(t.r_max);
@@ -860,7 +919,10 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.n_tiles = ctr + 1;
   a.tile_ctr = ctr + 2;
   a.n_refined = ctr + 3;
-  CAPT_CUDA(cudaMemsetAsync(ctr, 0, 16, s));
+  a.list_n = ctr + 4;
+  StageTimer& tm = g_stage_timer;
+  tm.mark(0, s);
+  CAPT_CUDA(cudaMemsetAsync(ctr, 0, 20, s));
   CAPT_CUDA(cudaMemsetAsync(a.counts, 0, 4 * nl, s));
   CAPT_CUDA(cudaMemsetAsync(a.cursor, 0, 4 * nl, s));
   CAPT_CUDA(cudaMemsetAsync(a.verdict, 0, n + 8, s));
@@ -868,9 +930,11 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   const int G = grid_for(n, 256, 8);
   constexpr int V = 4;
   const int G4 = grid_for((n + V - 1) / V, 256, 8);
+  tm.mark(1, s);
   if (f64) k_bin_count<double><<<G, 256, 0, s>>>(a);
   else if (t.k == 3) k_bin_count3<V><<<G4, 256, 0, s>>>(a);
   else k_bin_count<float><<<G, 256, 0, s>>>(a);
+  tm.mark(2, s);
   // per-leaf starts and tiles
   size_t tb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, a.counts, a.start, nl, s);
@@ -881,10 +945,9 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   k_tile_counts<<<Gl, 256, 0, s>>>(nl, a.counts, tcount);
   CAPT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, tcount, tstart, nl, s));
   k_make_tiles<<<Gl, 256, 0, s>>>(nl, tcount, tstart, a.tiles, a.n_tiles);
-  constexpr int VS = 8;
-  const int G8 = grid_for((n + VS - 1) / VS, 256, 8);
-  if (f64) k_bin_scatter<double, VS><<<G8, 256, 0, s>>>(a);
-  else k_bin_scatter<float, VS><<<G8, 256, 0, s>>>(a);
+  tm.mark(3, s);
+  constexpr int VS = 4;
+  k_bin_scatter<VS><<<grid_for((n + VS - 1) / VS, 256, 8), 256, 0, s>>>(a);
   static int sms = 0, occ = 0;
   if (!sms) {
     int dev = 0;
@@ -893,10 +956,14 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_binned_scan, kBT, sizeof(SmemBinned));
     if (occ < 1) occ = 1;
   }
+  tm.mark(4, s);
   k_binned_scan<<<sms * occ, kBT, sizeof(SmemBinned), s>>>(a);
+  tm.mark(5, s);
   if (f64) k_slow<double><<<sms, 128, 0, s>>>(a);
   else k_slow<float><<<sms, 128, 0, s>>>(a);
   k_pack<<<grid_for(n_words, 256, 8), 256, 0, s>>>(n / L, L, a.verdict, bits, n_words);
+  tm.mark(6, s);
+  tm.finish(s);
   CAPT_CUDA(cudaGetLastError());
   note_launches(9);  // count, 2 scans, tile counts, tiles, scatter, scan, slow, pack
   static const bool debug = getenv("CAPT_DEBUG") != nullptr;

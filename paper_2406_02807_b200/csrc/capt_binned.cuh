@@ -25,7 +25,9 @@ struct BinArgs {
   uint32_t* tile_ctr;
   uint32_t* n_refined;
   unsigned long long* first_bad;
-  int* leafid;        // per sphere: leaf if binned, else -1
+  float4* lrec;       // compact list of binned spheres (K1 -> K3): {c, r}
+  int2* lmeta;        //   ... and (sphere id, leaf)
+  uint32_t* list_n;   //   ... length
   uint32_t* cursor;   // per leaf: scatter cursor (K3)
   float rlo_f, rhi_f; // fp32 images of the double band edges
 };

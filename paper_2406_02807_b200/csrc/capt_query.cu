@@ -425,9 +425,11 @@ int query_device(const DevTree& t, const void* d_c, const void* d_r, int64_t n, 
 }
 
 // Host-buffer queries larger than one chunk: a two-stream pipeline so the
-// host->device copy of chunk i+1 overlaps the kernels of chunk i (and the
-// verdict copy-back of chunk i-1).  Chunks are multiples of 32 lane groups,
-// so every chunk owns whole verdict words.
+// host->device copy of chunk i+1 overlaps the kernels of chunk i.  Chunks are
+// multiples of 32 lane groups, so every chunk owns whole verdict words; they
+// are written into one device array copied back once at the end (a
+// per-chunk copy into pageable user memory would block the host thread and
+// serialise the pipeline).
 struct PipeState {
   cudaStream_t w[2] = {nullptr, nullptr};
   cudaEvent_t start = nullptr, done[2] = {nullptr, nullptr};
@@ -466,9 +468,11 @@ int query_host_pipelined(const capt_tree* tree, const DevTree& t, const void* ce
     void* c = nullptr;
     void* r = nullptr;
     uint8_t* m = nullptr;
-    uint32_t* bits = nullptr;
     unsigned long long* aux = nullptr;  // first_bad + 6 counters
   } buf[2];
+  const int64_t words_total = (n / L + 31) / 32;
+  uint32_t* d_bits = nullptr;
+  CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_bits), 4 * words_total, s));
   CAPT_CUDA(cudaEventRecord(p->start, s));
   for (int i = 0; i < 2; ++i) {
     cudaStream_t w = p->w[i];
@@ -476,7 +480,6 @@ int query_host_pipelined(const capt_tree* tree, const DevTree& t, const void* ce
     CAPT_CUDA(cudaMallocAsync(&buf[i].c, in_elem * t.k * chunk, w));
     CAPT_CUDA(cudaMallocAsync(&buf[i].r, in_elem * chunk, w));
     if (lane_mask) CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf[i].m), chunk, w));
-    CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf[i].bits), 4 * (chunk / L / 32 + 1), w));
     CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf[i].aux), 8 * 7, w));
   }
   int rc = CAPT_OK;
@@ -492,22 +495,21 @@ int query_host_pipelined(const capt_tree* tree, const DevTree& t, const void* ce
     if (lane_mask)
       CAPT_CUDA(cudaMemcpyAsync(buf[b].m, lane_mask + base, len, cudaMemcpyHostToDevice, w));
     rc = query_device(t, buf[b].c, buf[b].r, len, L, lane_mask ? buf[b].m : nullptr, flags,
-                      buf[b].bits, buf[b].aux + 1, buf[b].aux, w);
+                      d_bits + base / L / 32, buf[b].aux + 1, buf[b].aux, w);
     if (rc) break;
-    const int64_t words = (len / L + 31) / 32;
-    CAPT_CUDA(cudaMemcpyAsync(out_bits + base / L / 32, buf[b].bits, 4 * words,
-                              cudaMemcpyDeviceToHost, w));
     CAPT_CUDA(cudaMemcpyAsync(p->pinned + 7 * ci, buf[b].aux, 8 * 7, cudaMemcpyDeviceToHost, w));
   }
   for (int i = 0; i < 2; ++i) {
     cudaFreeAsync(buf[i].c, p->w[i]);
     cudaFreeAsync(buf[i].r, p->w[i]);
     if (buf[i].m) cudaFreeAsync(buf[i].m, p->w[i]);
-    cudaFreeAsync(buf[i].bits, p->w[i]);
     cudaFreeAsync(buf[i].aux, p->w[i]);
     CAPT_CUDA(cudaEventRecord(p->done[i], p->w[i]));
     CAPT_CUDA(cudaStreamWaitEvent(s, p->done[i], 0));
   }
+  if (rc == CAPT_OK)
+    CAPT_CUDA(cudaMemcpyAsync(out_bits, d_bits, 4 * words_total, cudaMemcpyDeviceToHost, s));
+  cudaFreeAsync(d_bits, s);
   CAPT_CUDA(cudaStreamSynchronize(s));
   if (rc) return rc;
   int64_t fb = -1;

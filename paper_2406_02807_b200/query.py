@@ -131,7 +131,7 @@ def _host_query(tree: Capt, c, r, f64: int, lane_width: int = 1, lane_mask=None,
     if rc == _lib.CAPT_ERANGE:
         return None, None, int(bad.value)
     _lib.check(rc, "capt_query")
-    bits = np.unpackbits(words.view(np.uint8), bitorder="little")[:ng].astype(bool)
+    bits = np.unpackbits(words.view(np.uint8), bitorder="little")[:ng].view(bool)
     return bits, (cnt if stats else None), int(bad.value)
 
 
