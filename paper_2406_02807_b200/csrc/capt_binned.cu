@@ -10,9 +10,10 @@
 //                     counts; spheres needing the exact path go to a queue
 //                     (k_bin_count: generic k / float64 inputs)
 //   K2 (CUB scans)    per-leaf start offsets and tile counts
-//   K3 k_bin_scatter  over K1's compact list of binned spheres: rank inside
-//                     the leaf (warp-aggregated cursor atomics), scatter the
-//                     float4 {c, r} record + the sphere id to start[leaf] + rank
+//   K3 k_part_bucket, k_part_leaf: group K1's compact list of binned spheres
+//                     by leaf in two shared-memory-ranked passes (bucket of
+//                     leaves, then leaf) into a permutation; K5 gathers the
+//                     float4 {c, r} records through it
 //   K4 k_make_tiles   (leaf, chunk of <= 1024 spheres) work items
 //   K5 k_binned_scan  persistent CTAs pull tiles from an atomic counter; the
 //                     leaf's set is staged once into shared memory in local
@@ -27,6 +28,7 @@
 //   K7 k_pack         verdict bytes -> bit words, OR over each lane group
 #include <cub/cub.cuh>
 
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -425,62 +427,111 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
   }
 }
 
-// K3: scatter the compact list into leaf order: rank inside the leaf from
-// warp-aggregated cursor atomics (all V issued before any result is used),
-// slot = start[leaf] + rank.  Persistent grid over the device-side count.
-#ifndef CAPT_K3_EXP
-#define CAPT_K3_EXP 0
-#endif
-template <int V>
-__global__ void __launch_bounds__(256) k_bin_scatter(BinArgs a) {
+// K3: group K1's compact list by leaf in two coalescing passes instead of
+// one random scatter with a returning atomic per sphere (both of which are
+// L2-transaction bound at this size).  Only 8-byte (leaf, list index) pairs
+// move; K5 gathers each tile's records through the permutation.
+//   K3a k_part_bucket: a CTA takes 4096 list entries, ranks them per leaf
+//       bucket (<= 256 buckets of 2^bshift consecutive leaves) with shared
+//       memory atomics, reserves each bucket's run with ONE global atomic and
+//       writes (leaf, list index) pairs -- runs of ~16 pairs per bucket.
+//       Bucket b's region starts at start[b << bshift] (the leaf scan).
+//   K3b k_part_leaf: a CTA takes 4096 bucket-ordered pairs (their leaves span
+//       one or a few buckets), ranks them per leaf in shared memory, reserves
+//       per leaf with one global atomic, and writes perm[start[leaf] + rank]
+//       (writes stay inside the buckets' regions).
+constexpr int kBuckets = 256;
+constexpr int kPartItems = 4096;  // entries per CTA pass
+constexpr int kPartPer = kPartItems / 256;
+constexpr int kLeafSpan = 2048;  // K3b shared-memory leaf counters
+
+__global__ void __launch_bounds__(256) k_part_bucket(BinArgs a) {
+  __shared__ uint32_t hist[kBuckets];
+  __shared__ uint32_t gbase[kBuckets];
   const uint32_t n = *a.list_n;
-  const int lane = threadIdx.x & 31;
-  const uint32_t per_iter = gridDim.x * blockDim.x * V;
-  for (uint32_t base = blockIdx.x * blockDim.x * V; base < n; base += per_iter) {
-    int2 meta[V];
-    float4 rc[V];
+  const int tid = threadIdx.x;
+  for (uint32_t c0 = blockIdx.x * kPartItems; c0 < n; c0 += gridDim.x * kPartItems) {
+    hist[tid] = 0;
+    __syncthreads();
+    int leaf[kPartPer];
+    uint32_t rank[kPartPer];
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const uint32_t i = base + v * blockDim.x + threadIdx.x;
-      meta[v] = make_int2(-1, -1);
-      if (i < n) {
-        meta[v] = __ldcs(a.lmeta + i);
-        rc[v] = __ldcs(a.lrec + i);
+    for (int i = 0; i < kPartPer; ++i) {
+      const uint32_t j = c0 + i * 256 + tid;
+      leaf[i] = j < n ? __ldcs(&a.lmeta[j].y) : -1;
+    }
+#pragma unroll
+    for (int i = 0; i < kPartPer; ++i)
+      if (leaf[i] >= 0) rank[i] = atomicAdd(&hist[leaf[i] >> a.bshift], 1u);
+    __syncthreads();
+    const uint32_t hc = hist[tid];
+    if (hc) gbase[tid] = a.start[tid << a.bshift] + atomicAdd(a.bcursor + tid, hc);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kPartPer; ++i) {
+      if (leaf[i] >= 0) {
+        const uint32_t j = c0 + i * 256 + tid;
+        a.part[gbase[leaf[i] >> a.bshift] + rank[i]] = make_int2(leaf[i], int(j));
       }
     }
-    unsigned peers[V], tk[V];
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_part_leaf(BinArgs a) {
+  __shared__ uint32_t cnt[kLeafSpan];
+  __shared__ int lmin_s, lmax_s;
+  const uint32_t n = *a.list_n;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  for (uint32_t c0 = blockIdx.x * kPartItems; c0 < n; c0 += gridDim.x * kPartItems) {
+    int2 it[kPartPer];  // (leaf, list index)
+    int lo = INT_MAX, hi = -1;
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const unsigned act = __ballot_sync(0xffffffffu, meta[v].y >= 0);
-      peers[v] = 0;
-      tk[v] = 0;
-      if (meta[v].y >= 0) {
-        peers[v] = __match_any_sync(act, unsigned(meta[v].y));
-#if CAPT_K3_EXP == 1 || CAPT_K3_EXP == 3
-        if (lane == __ffs(peers[v]) - 1) tk[v] = 0;
-#else
-        if (lane == __ffs(peers[v]) - 1) tk[v] = atomicAdd(a.cursor + meta[v].y, __popc(peers[v]));
-#endif
+    for (int i = 0; i < kPartPer; ++i) {
+      const uint32_t j = c0 + i * 256 + tid;
+      it[i] = j < n ? __ldcs(a.part + j) : make_int2(-1, -1);
+      if (it[i].x >= 0) {
+        lo = min(lo, it[i].x);
+        hi = max(hi, it[i].x);
       }
     }
-    uint32_t st[V];
-#pragma unroll
-    for (int v = 0; v < V; ++v) st[v] = meta[v].y >= 0 ? __ldg(a.start + meta[v].y) : 0u;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      if (meta[v].y >= 0) {
-        const unsigned b = __shfl_sync(peers[v], tk[v], __ffs(peers[v]) - 1);
-#if CAPT_K3_EXP == 1 || CAPT_K3_EXP == 2
-        const uint32_t pos = base + v * blockDim.x + threadIdx.x + (b & st[v] & 1u);
-#elif CAPT_K3_EXP == 3
-        const uint32_t pos = ((base + v * blockDim.x + threadIdx.x) * 2654435761u) % n + (b & st[v] & 1u) * 0;
-#else
-        const uint32_t pos = st[v] + b + __popc(peers[v] & ((1u << lane) - 1u));
-#endif
-        a.rec[pos] = rc[v];
-        a.rid[pos] = meta[v].x;
-      }
+    if (tid == 0) {
+      lmin_s = INT_MAX;
+      lmax_s = -1;
     }
+    for (int i = tid; i < kLeafSpan; i += 256) cnt[i] = 0;
+    __syncthreads();
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if (lane == 0) {
+      atomicMin(&lmin_s, lo);
+      atomicMax(&lmax_s, hi);
+    }
+    __syncthreads();
+    const int lmin = lmin_s;
+    const bool local = lmax_s - lmin < kLeafSpan;
+    uint32_t rank[kPartPer];
+    if (local) {
+#pragma unroll
+      for (int i = 0; i < kPartPer; ++i)
+        if (it[i].x >= 0) rank[i] = atomicAdd(&cnt[it[i].x - lmin], 1u);
+      __syncthreads();
+      for (int i = tid; i < kLeafSpan; i += 256) {
+        const uint32_t c = cnt[i];
+        if (c) cnt[i] = a.start[lmin + i] + atomicAdd(a.cursor + lmin + i, c);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < kPartPer; ++i) {
+      const int2 e = it[i];
+      if (e.x < 0) continue;
+      const uint32_t pos = local ? cnt[e.x - lmin] + rank[i]
+                                 : a.start[e.x] + atomicAdd(a.cursor + e.x, 1u);
+      a.perm[pos] = uint32_t(e.y);
+    }
+    __syncthreads();
   }
 }
 
@@ -570,7 +621,7 @@ __device__ __forceinline__ void load_spheres(Spheres8& sp, SmemBinned& S, const 
       kx[h] = ky[h] = kz[h] = 0.f;
       if (active && e < count) {
         sp.real |= 1u << (i + h);
-        const float4 rc = a.rec[s0 + e];
+        const float4 rc = a.lrec[a.perm[s0 + e]];
         const float ax = rc.x - org.x, ay = rc.y - org.y, az = rc.z - org.z;
         const float aa = fmaf(az, az, fmaf(ay, ay, ax * ax));
         const float r2 = rc.w * rc.w;
@@ -675,7 +726,7 @@ __device__ __forceinline__ void decide(const Spheres8& sp, const SmemBinned& S, 
     if (!((sp.real >> i) & 1u)) continue;
     const int e = sp.base + i;
     const float mv = combined ? okey_inv(S.minkey[e]) : sp.mn[i];
-    const int q = a.rid[s0 + e];
+    const int q = a.lmeta[a.perm[s0 + e]].x;
     if (((hm >> i) & 1u) || mv <= S.lim_lo[e]) {
       a.verdict[q] = 1;
     } else if (!(mv > S.lim_hi[e])) {
@@ -827,7 +878,7 @@ struct Arena {
 // times, unlike a serialised profiler pass), summed over calls and printed at
 // exit.  Diagnostics only; adds a synchronisation per call.
 struct StageTimer {
-  static constexpr int kStages = 6;
+  static constexpr int kStages = 7;
   bool on = getenv("CAPT_STAGE_TIMING") != nullptr;
   cudaEvent_t ev[kStages + 1] = {};
   double sum[kStages] = {};
@@ -838,7 +889,7 @@ struct StageTimer {
   }
   ~StageTimer() {
     if (!on || !calls) return;
-    static const char* names[kStages] = {"memsets", "K1 count", "K2 scans+tiles", "K3 scatter",
+    static const char* names[kStages] = {"memsets", "K1 count", "K2 scans+tiles", "K3a bucket", "K3b leaf",
                                          "K5 scan", "K6+K7 slow+pack"};
     double tot = 0;
     for (double v : sum) tot += v;
@@ -898,14 +949,17 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   uint32_t* tcount = A.get<uint32_t>(nl);
   uint32_t* tstart = A.get<uint32_t>(nl);
   a.tiles = A.get<int2>(nl + n / kTS + 1);
-  a.rec = A.get<float4>(n);
-  a.rid = A.get<int>(n);
+  a.perm = A.get<uint32_t>(n);
   a.verdict = A.get<uint8_t>(n + 8);
   a.slow = A.get<int2>(n);
   a.lrec = A.get<float4>(n);
   a.lmeta = A.get<int2>(n);
   a.cursor = A.get<uint32_t>(nl);
-  if (!ctr || !a.counts || !a.start || !tcount || !tstart || !a.tiles || !a.rec || !a.rid ||
+  a.part = A.get<int2>(n);
+  a.bcursor = A.get<uint32_t>(kBuckets);
+  a.bshift = 0;
+  while ((nl >> a.bshift) > kBuckets) ++a.bshift;
+  if (!a.part || !a.bcursor || !ctr || !a.counts || !a.start || !tcount || !tstart || !a.tiles || !a.perm ||
       !a.verdict || !a.slow || !a.lrec || !a.lmeta || !a.cursor)
     return fail(CAPT_ENOMEM, "binned scratch allocation");
   {
@@ -925,6 +979,7 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   CAPT_CUDA(cudaMemsetAsync(ctr, 0, 20, s));
   CAPT_CUDA(cudaMemsetAsync(a.counts, 0, 4 * nl, s));
   CAPT_CUDA(cudaMemsetAsync(a.cursor, 0, 4 * nl, s));
+  CAPT_CUDA(cudaMemsetAsync(a.bcursor, 0, 4 * kBuckets, s));
   CAPT_CUDA(cudaMemsetAsync(a.verdict, 0, n + 8, s));
   const bool f64 = flags & CAPT_INPUT_F64;
   const int G = grid_for(n, 256, 8);
@@ -946,8 +1001,12 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   CAPT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, tcount, tstart, nl, s));
   k_make_tiles<<<Gl, 256, 0, s>>>(nl, tcount, tstart, a.tiles, a.n_tiles);
   tm.mark(3, s);
-  constexpr int VS = 4;
-  k_bin_scatter<VS><<<grid_for((n + VS - 1) / VS, 256, 8), 256, 0, s>>>(a);
+  {
+    const int Gp = grid_for((n + kPartItems - 1) / kPartItems * 256, 256, 4);
+    k_part_bucket<<<Gp, 256, 0, s>>>(a);
+    tm.mark(4, s);
+    k_part_leaf<<<Gp, 256, 0, s>>>(a);
+  }
   static int sms = 0, occ = 0;
   if (!sms) {
     int dev = 0;
@@ -956,16 +1015,16 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_binned_scan, kBT, sizeof(SmemBinned));
     if (occ < 1) occ = 1;
   }
-  tm.mark(4, s);
-  k_binned_scan<<<sms * occ, kBT, sizeof(SmemBinned), s>>>(a);
   tm.mark(5, s);
+  k_binned_scan<<<sms * occ, kBT, sizeof(SmemBinned), s>>>(a);
+  tm.mark(6, s);
   if (f64) k_slow<double><<<sms, 128, 0, s>>>(a);
   else k_slow<float><<<sms, 128, 0, s>>>(a);
   k_pack<<<grid_for(n_words, 256, 8), 256, 0, s>>>(n / L, L, a.verdict, bits, n_words);
-  tm.mark(6, s);
+  tm.mark(7, s);
   tm.finish(s);
   CAPT_CUDA(cudaGetLastError());
-  note_launches(9);  // count, 2 scans, tile counts, tiles, scatter, scan, slow, pack
+  note_launches(10);  // count, 2 scans, tile counts, tiles, 2 partition passes, scan, slow, pack
   static const bool debug = getenv("CAPT_DEBUG") != nullptr;
   if (debug) {
     uint32_t h[4], last[2];

@@ -16,8 +16,6 @@ struct BinArgs {
   uint32_t* counts;   // per leaf: AABB-passing spheres
   uint32_t* start;    // per leaf: first binned slot
   int2* tiles;        // (leaf, chunk)
-  float4* rec;        // binned {cx, cy, cz, r}
-  int* rid;           // binned sphere ids
   uint8_t* verdict;   // per sphere
   int2* slow;         // (sphere, leaf) for the exact float64 path
   uint32_t* slow_n;
@@ -28,7 +26,11 @@ struct BinArgs {
   float4* lrec;       // compact list of binned spheres (K1 -> K3): {c, r}
   int2* lmeta;        //   ... and (sphere id, leaf)
   uint32_t* list_n;   //   ... length
-  uint32_t* cursor;   // per leaf: scatter cursor (K3)
+  uint32_t* cursor;   // per leaf: scatter cursor (K3b)
+  int2* part;         // K3a output: (leaf, list index), grouped by leaf bucket
+  uint32_t* perm;     // K3b output: list index of binned slot i (leaf order)
+  uint32_t* bcursor;  // per leaf bucket: K3a cursor
+  int bshift;         // leaf bucket = leaf >> bshift (<= kBuckets buckets)
   float rlo_f, rhi_f; // fp32 images of the double band edges
 };
 
