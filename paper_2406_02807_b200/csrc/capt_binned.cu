@@ -535,20 +535,24 @@ __global__ void __launch_bounds__(256) k_part_leaf(BinArgs a) {
   }
 }
 
+// Tiles are laid out leaf by leaf in the tree's order section (descending
+// set size), so the persistent K5 CTAs draw the costliest tiles first and the
+// tail of the launch is made of small ones.
 __global__ void k_tile_counts(int64_t n, const uint32_t* __restrict__ counts,
-                              uint32_t* __restrict__ tcount) {
+                              const int* __restrict__ order, uint32_t* __restrict__ tcount) {
   for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
        j += int64_t(gridDim.x) * blockDim.x)
-    tcount[j] = (counts[j] + kTS - 1) / kTS;
+    tcount[j] = (counts[order[j]] + kTS - 1) / kTS;
 }
 
 __global__ void k_make_tiles(int64_t n, const uint32_t* __restrict__ tcount,
-                             const uint32_t* __restrict__ tstart, int2* __restrict__ tiles,
-                             uint32_t* __restrict__ n_tiles) {
+                             const uint32_t* __restrict__ tstart, const int* __restrict__ order,
+                             int2* __restrict__ tiles, uint32_t* __restrict__ n_tiles) {
   for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
        j += int64_t(gridDim.x) * blockDim.x) {
     const uint32_t c = tcount[j], s = tstart[j];
-    for (uint32_t i = 0; i < c; ++i) tiles[s + i] = make_int2(int(j), int(i));
+    const int leaf = order[j];
+    for (uint32_t i = 0; i < c; ++i) tiles[s + i] = make_int2(leaf, int(i));
     if (j == n - 1) *n_tiles = s + c;
   }
 }
@@ -670,19 +674,18 @@ __device__ __forceinline__ void test_pair(Spheres8& sp, const ulonglong2* sA, co
   }
 }
 
-// Pairs u = 4g .. 4g+3 for g = ph, ph + P, ...  Stops early once every
-// sphere of the slot is a definite hit (hitmask shared by the phases).
+// Pairs u = 4g .. 4g+3 for g = ph, ph + P, ...  (chunks are padded to a
+// multiple of 8 points with w = +inf rows, so groups are always full).  Stops
+// early once every sphere of the slot is a definite hit (hitmask shared by
+// the phases).
 __device__ __forceinline__ void scan_pairs(Spheres8& sp, const ulonglong2* sA,
                                            const ulonglong2* sB, int npairs, int ph, int P,
                                            uint32_t* hitmask, const float* lim_lo) {
-  const int ngroups = (npairs + 3) / 4;
+  const int ngroups = npairs / 4;
   int it = 0;
   for (int g = ph; g < ngroups; g += P) {
 #pragma unroll
-    for (int o = 0; o < 4; ++o) {
-      const int u = 4 * g + o;
-      if (u < npairs) test_pair(sp, sA, sB, u);
-    }
+    for (int o = 0; o < 4; ++o) test_pair(sp, sA, sB, 4 * g + o);
     if ((++it & 7) == 0) {
       uint32_t h = definite_hits(sp, lim_lo);
       if (P > 1) {
@@ -696,21 +699,40 @@ __device__ __forceinline__ void scan_pairs(Spheres8& sp, const ulonglong2* sA,
   if (h) atomicOr(hitmask, h);
 }
 
-__device__ __forceinline__ void stage_points(ulonglong2* sA, ulonglong2* sB, const float* xs,
-                                             uint32_t m4, uint32_t c0, uint32_t len,
-                                             uint32_t len2, const float4 org) {
+// Chunk staging, split so the loads of a tile's first chunk can be issued
+// before the sphere gathers and stored after them.  Rows i >= len (up to the
+// padded length) and non-finite rows become w = +inf: never a hit.
+constexpr int kStageU = kChunk / kBT;  // rows per thread per chunk
+struct StagedRows {
+  float x[kStageU], y[kStageU], z[kStageU];
+};
+__device__ __forceinline__ void stage_load(StagedRows& r, const float* xs, uint32_t m4,
+                                           uint32_t c0, uint32_t len) {
   const float INF = __int_as_float(0x7f800000);
-  for (uint32_t i = threadIdx.x; i < len2; i += kBT) {
-    const uint32_t g = c0 + i;
-    float bx = 0.f, by = 0.f, bz = 0.f, w = INF;
+#pragma unroll
+  for (int u = 0; u < kStageU; ++u) {
+    const uint32_t i = threadIdx.x + u * kBT;
+    r.x[u] = r.y[u] = r.z[u] = INF;
     if (i < len) {
-      const float px = xs[g], py = xs[m4 + g], pz = xs[2 * m4 + g];
-      if (isfinite(px) && isfinite(py) && isfinite(pz)) {
-        bx = px - org.x;
-        by = py - org.y;
-        bz = pz - org.z;
-        w = fmaf(bz, bz, fmaf(by, by, bx * bx));
-      }
+      r.x[u] = __ldg(xs + c0 + i);
+      r.y[u] = __ldg(xs + m4 + c0 + i);
+      r.z[u] = __ldg(xs + 2 * m4 + c0 + i);
+    }
+  }
+}
+__device__ __forceinline__ void stage_store(const StagedRows& r, ulonglong2* sA, ulonglong2* sB,
+                                            uint32_t len8, const float4 org) {
+  const float INF = __int_as_float(0x7f800000);
+#pragma unroll
+  for (int u = 0; u < kStageU; ++u) {
+    const uint32_t i = threadIdx.x + u * kBT;
+    if (i >= len8) break;
+    float bx = 0.f, by = 0.f, bz = 0.f, w = INF;
+    if (isfinite(r.x[u]) && isfinite(r.y[u]) && isfinite(r.z[u])) {
+      bx = r.x[u] - org.x;
+      by = r.y[u] - org.y;
+      bz = r.z[u] - org.z;
+      w = fmaf(bz, bz, fmaf(by, by, bx * bx));
     }
     sA[i] = make_ulonglong2(pack2(bx, bx), pack2(by, by));
     sB[i] = make_ulonglong2(pack2(bz, bz), pack2(w, w));
@@ -768,21 +790,29 @@ __global__ void __launch_bounds__(kBT, CAPT_K5_MINB) k_binned_scan(BinArgs a) {
     const bool active = tid < nslot * P;
     const int slot = tid % nslot;
     const int ph = tid / nslot;
+    // the first chunk's rows are loaded before the sphere gathers so that
+    // both latencies overlap; the previous tile's final barrier freed sA/sB
+    StagedRows rows;
+    stage_load(rows, xs, m4, 0, min(uint32_t(kChunk), m));
     Spheres8 sp;
     load_spheres(sp, S, a, s0, org, cnt, slot, active, active && ph == 0);
     for (int e = tid; e < nslot * kS; e += kBT) S.minkey[e] = 0xffffffffu;
     for (int e = tid; e < nslot; e += kBT) S.hitmask[e] = 0;
+    stage_store(rows, sA, sB, (min(uint32_t(kChunk), m) + 7u) & ~7u, org);
 
     // stream the set through shared memory in chunks of kChunk points
     bool done = sp.real == 0;
     for (uint32_t c0 = 0; c0 < m; c0 += kChunk) {
       const uint32_t len = min(uint32_t(kChunk), m - c0);
-      const uint32_t len2 = (len + 1u) & ~1u;
-      __syncthreads();  // previous chunk consumed, inits and limits visible
-      stage_points(sA, sB, xs, m4, c0, len, len2, org);
-      __syncthreads();
+      const uint32_t len8 = (len + 7u) & ~7u;
+      if (c0) {
+        __syncthreads();  // previous chunk consumed
+        stage_load(rows, xs, m4, c0, len);
+        stage_store(rows, sA, sB, len8, org);
+      }
+      __syncthreads();  // chunk staged; inits and limits visible
       if (!done) {
-        scan_pairs(sp, sA, sB, int(len2 / 2), ph, P, &S.hitmask[slot], S.lim_lo);
+        scan_pairs(sp, sA, sB, int(len8 / 2), ph, P, &S.hitmask[slot], S.lim_lo);
         uint32_t h = definite_hits(sp, S.lim_lo);
         if (P > 1) h |= *reinterpret_cast<volatile uint32_t*>(&S.hitmask[slot]);
         done = (h & sp.real) == sp.real;
@@ -997,9 +1027,9 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   if (!tmp) return fail(CAPT_ENOMEM, "binned scratch allocation");
   CAPT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, a.counts, a.start, nl, s));
   const int Gl = grid_for(nl, 256, 8);
-  k_tile_counts<<<Gl, 256, 0, s>>>(nl, a.counts, tcount);
+  k_tile_counts<<<Gl, 256, 0, s>>>(nl, a.counts, t.order, tcount);
   CAPT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, tcount, tstart, nl, s));
-  k_make_tiles<<<Gl, 256, 0, s>>>(nl, tcount, tstart, a.tiles, a.n_tiles);
+  k_make_tiles<<<Gl, 256, 0, s>>>(nl, tcount, tstart, t.order, a.tiles, a.n_tiles);
   tm.mark(3, s);
   {
     const int Gp = grid_for((n + kPartItems - 1) / kPartItems * 256, 256, 4);

@@ -13,6 +13,8 @@
 //                                   finite points' box (xyz) and the largest
 //                                   fp32 |p - o|^2 over the set (w)
 //   rep    float4[n]                row 0 of each set (xyz), loaded beside the box
+//   order  int32[n]                 leaves by descending set size (binned K5 takes
+//                                   the costliest tiles first: shorter tail)
 #pragma once
 
 #include <cuda_runtime.h>
@@ -25,7 +27,7 @@
 namespace capt {
 
 constexpr uint64_t kSlabMagic = 0x3030324254504143ull;  // "CAPTB200"
-constexpr int kSlabVersion = 3;
+constexpr int kSlabVersion = 4;
 constexpr int kMaxK = 3;
 
 struct SlabHeader {
@@ -45,7 +47,8 @@ struct SlabHeader {
   int64_t bytes;      // slab size
   int64_t off_org;    // byte offset of the org section
   int64_t off_rep;    // byte offset of the rep section
-  int64_t reserved[8];
+  int64_t off_order;  // byte offset of the order section
+  int64_t reserved[7];
 };
 static_assert(sizeof(SlabHeader) <= 256, "header must fit its 256-B section");
 
@@ -60,6 +63,7 @@ struct DevTree {
   const float4* data;
   const float4* org;
   const float4* rep;  // row 0 of every set (the point owning the cell), +inf for padding
+  const int* order;   // leaves by descending set size
 };
 
 }  // namespace capt
@@ -104,6 +108,7 @@ inline DevTree view(const capt_tree* t) {
   d.data = reinterpret_cast<const float4*>(t->slab + t->h.off_data);
   d.org = reinterpret_cast<const float4*>(t->slab + t->h.off_org);
   d.rep = reinterpret_cast<const float4*>(t->slab + t->h.off_rep);
+  d.order = reinterpret_cast<const int*>(t->slab + t->h.off_order);
   return d;
 }
 
@@ -125,6 +130,8 @@ inline int64_t layout_slab(SlabHeader& h, int64_t data_f4) {
   off = align256(off + sizeof(float4) * h.n);
   h.off_rep = off;
   off = align256(off + sizeof(float4) * h.n);
+  h.off_order = off;
+  off = align256(off + sizeof(int) * h.n);
   h.off_data = off;
   off = align256(off + sizeof(float4) * (data_f4 > 0 ? data_f4 : 1));
   h.data_f4 = data_f4;
@@ -138,7 +145,7 @@ inline int depth_of(int64_t n) {
   return d;
 }
 
-// Fill the org section (binned-scan origins) of a slab whose data is final.
+// Fill the org, rep and order sections of a slab whose data is final.
 int compute_origins(const DevTree& t, cudaStream_t s);
 
 int alloc_slab(capt_tree** out, int device, SlabHeader h);

@@ -1,5 +1,7 @@
 // Tree handles: error plumbing, upload from the reference layout
 // (Capt.__init__ tree.py:74-97), export back to it, slab replication.
+#include <cub/cub.cuh>
+
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -170,10 +172,38 @@ __global__ void k_origins(DevTree t) {
   }
 }
 
+__global__ void k_order_keys(DevTree t, uint32_t* keys, int* ids) {
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < t.n;
+       j += int64_t(gridDim.x) * blockDim.x) {
+    keys[j] = t.set[j].y;
+    ids[j] = int(j);
+  }
+}
+
 int compute_origins(const DevTree& t, cudaStream_t s) {
   k_origins<<<grid_for(t.n * 32, 256), 256, 0, s>>>(t);
   CAPT_CUDA(cudaGetLastError());
-  note_launches(1);
+  // leaves by descending set size (stable: equal sizes keep leaf order)
+  uint32_t *keys = nullptr, *keys_out = nullptr;
+  int* ids = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  const int n = int(t.n);
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, keys, keys_out, ids,
+                                            const_cast<int*>(t.order), n, 0, 32, s);
+  CAPT_CUDA(cudaMallocAsync(&keys, 4 * size_t(n), s));
+  CAPT_CUDA(cudaMallocAsync(&keys_out, 4 * size_t(n), s));
+  CAPT_CUDA(cudaMallocAsync(&ids, 4 * size_t(n), s));
+  CAPT_CUDA(cudaMallocAsync(&tmp, tb ? tb : 1, s));
+  k_order_keys<<<grid_for(t.n, 256), 256, 0, s>>>(t, keys, ids);
+  CAPT_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, tb, keys, keys_out, ids,
+                                                      const_cast<int*>(t.order), n, 0, 32, s));
+  cudaFreeAsync(keys, s);
+  cudaFreeAsync(keys_out, s);
+  cudaFreeAsync(ids, s);
+  cudaFreeAsync(tmp, s);
+  CAPT_CUDA(cudaGetLastError());
+  note_launches(3);
   return CAPT_OK;
 }
 
