@@ -187,7 +187,15 @@ def cpu_reference_rate(tree_ref, c, r, lane_width, target_s=10.0, max_spheres=No
     rate = n / max(dt, 1e-9)
     n = int(min(len(r), max_spheres or len(r), rate * target_s))
     n, dt = run(max(n, lane_width))
-    return n / dt, n, dt, threads
+    # the whole batch finishes in well under target_s: repeat passes over it
+    passes = 1
+    if dt < 0.5 * target_s and max_spheres is None:
+        passes = max(1, int(target_s / max(dt, 1e-9)))
+        t0 = time.perf_counter()
+        for _ in range(passes):
+            run(n)
+        dt = time.perf_counter() - t0
+    return n * passes / dt, n, dt, threads, passes
 
 
 # --------------------------------------------------------------------------
@@ -334,10 +342,11 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import oracle as O
         ref_tree = O.tree_from(tree)
-        rate, ns, dt, th = cpu_reference_rate(ref_tree, c_np, r_np, L, target_s=10.0)
+        rate, ns, dt, th, passes = cpu_reference_rate(ref_tree, c_np, r_np, L, target_s=10.0)
         cpu_base = {"value": rate, "unit": UNIT, "cores": th, "kind": "port",
-                    "sample": f"first {ns} spheres ({ns // L} groups) of rank 0's batch, "
-                              f"{dt:.1f} s, oracle/capt_oracle.c OpenMP x{th} on {cpu_model()}"}
+                    "sample": f"{passes} pass(es) over the first {ns} spheres ({ns // L} groups) "
+                              f"of rank 0's batch, {dt:.1f} s, oracle/capt_oracle.c OpenMP "
+                              f"x{th} on {cpu_model()}"}
 
     if rank == 0:
         line = {
@@ -447,7 +456,7 @@ def main_reference(args, rank, world):
     tree = O.construct(cloud, r_min, r_max)
     threads = cpu_threads()
     # size one step to ~2 s of CPU work
-    rate, _, _, _ = cpu_reference_rate(tree, c, r, L, target_s=0.5)
+    rate = cpu_reference_rate(tree, c, r, L, target_s=0.5, max_spheres=len(r))[0]
     per_step = int(max(L, min(len(r), rate * 2.0)))
     per_step -= per_step % L
     cc, rr = c[:per_step].astype(np.float64), r[:per_step].astype(np.float64)

@@ -251,6 +251,12 @@ __global__ void __launch_bounds__(256) k_bin_count(BinArgs a) {
   }
 }
 
+__device__ __forceinline__ float lds_f32(unsigned addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+
 // K1 specialised for k = 3, fp32 input (the hot path): V spheres per thread
 // in flight, 32-bit indexing, the top 13 levels of T in shared memory walked
 // with byte offsets (child = 2*off + 4 + 4*(x > T): 4 instructions per level),
@@ -271,6 +277,7 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
   const float* __restrict__ cf = static_cast<const float*>(a.centers);
   const float* __restrict__ rf = static_cast<const float*>(a.radii);
   const unsigned char* sb = reinterpret_cast<const unsigned char*>(sT);
+  const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(sT));
   const int dsm = t.depth < 13 ? t.depth : 13;
   const int nl1 = int(t.n - 1);
   const int n = int(a.n);
@@ -317,16 +324,26 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
         atomicMin(a.first_bad, static_cast<unsigned long long>(q));
       off[v] = 0;
     }
+    // shared-memory levels on absolute shared-window addresses:
+    // addr(child) = 2 addr + (4 or 8) - sbase, one LDS + compare + select + IMAD
     int s = 0;
-    for (; s + 3 <= dsm; s += 3) {
+    {
+      unsigned ad[V];
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        unsigned o = off[v];
-        o = 2 * o + (cx[v] > *reinterpret_cast<const float*>(sb + o) ? 8u : 4u);
-        o = 2 * o + (cy[v] > *reinterpret_cast<const float*>(sb + o) ? 8u : 4u);
-        o = 2 * o + (cz[v] > *reinterpret_cast<const float*>(sb + o) ? 8u : 4u);
-        off[v] = o;
+      for (int v = 0; v < V; ++v) ad[v] = sbase;
+      const unsigned k0 = 4u - sbase, k1 = 8u - sbase;
+      for (; s + 3 <= dsm; s += 3) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          unsigned x = ad[v];
+          x = 2 * x + (cx[v] > lds_f32(x) ? k1 : k0);
+          x = 2 * x + (cy[v] > lds_f32(x) ? k1 : k0);
+          x = 2 * x + (cz[v] > lds_f32(x) ? k1 : k0);
+          ad[v] = x;
+        }
       }
+#pragma unroll
+      for (int v = 0; v < V; ++v) off[v] = ad[v] - sbase;
     }
     for (; s < t.depth; ++s) {
       const int ax = s % 3;
@@ -338,49 +355,43 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
         off[v] = 2 * off[v] + (c > tv ? 8u : 4u);
       }
     }
-    // per-sphere classification; no warp-synchronous intrinsic in this loop,
-    // so the box / set / representative loads of the V spheres can overlap
+    // per-sphere classification, branch-free.  The AABB test only has to
+    // be conservative here: every point of a set lies inside the set's box and
+    // the reference's float64 box distance is a monotone function of the same
+    // rounded differences, so s_box <= s_point and a sphere the reference
+    // rejects by its AABB (query.py:202-208) has no colliding point -- the
+    // prefilter never changes a verdict, only the work.  A sphere is rejected
+    // only when the fp32 box distance is clearly above r^2 (relative band
+    // TAU); the band itself is kept and left to the scan.  Exact reference
+    // AABB semantics (the aabb-rejection counter) live in the counter kernel.
     int leaf[V], status[V];
     bool hit[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       leaf[v] = int(off[v] >> 2) - nl1;
-      status[v] = 0;
-      hit[v] = false;
       const float r2 = r[v] * r[v];
-      if (valid[v]) {
-        const bool cfin = isfinite(cx[v]) && isfinite(cy[v]) && isfinite(cz[v]);
-        const bool fast = cfin && r2 >= kR2Min && r2 <= kR2Max;
-        // non-finite centre with a finite radius never collides (float64 r^2 is finite)
-        status[v] = fast ? 2 : ((!cfin && isfinite(r[v])) ? 0 : 3);
-        if (status[v] && prefilter) {
-          const float4 lo = __ldg(t.box + 2 * leaf[v]);
-          const float4 hi = __ldg(t.box + 2 * leaf[v] + 1);
-          bool exact = !fast;
-          if (fast) {
-            const float rx = fmaxf(fmaxf(lo.x - cx[v], 0.f), cx[v] - hi.x);
-            const float ry = fmaxf(fmaxf(lo.y - cy[v], 0.f), cy[v] - hi.y);
-            const float rz = fmaxf(fmaxf(lo.z - cz[v], 0.f), cz[v] - hi.z);
-            const float ss = fmaf(rz, rz, fmaf(ry, ry, rx * rx));
-            if (ss > r2 * band_hi) status[v] = 0;
-            else if (!(ss < r2 * band_lo)) exact = true;
-          }
-          if (status[v] && exact) {
-            const double c64[3] = {cx[v], cy[v], cz[v]};
-            const double r64 = r[v];
-            if (!aabb_keep64(3, lo, hi, c64, __dmul_rn(r64, r64))) status[v] = 0;
-          }
-        }
+      const bool cfin = isfinite(cx[v]) && isfinite(cy[v]) && isfinite(cz[v]);
+      const bool fast = cfin && r2 >= kR2Min && r2 <= kR2Max;
+      // non-finite centre with a finite radius never collides (float64 r^2 is finite)
+      int st = fast ? 2 : ((!cfin && isfinite(r[v])) ? 0 : 3);
+      st = valid[v] ? st : 0;
+      const float4 rp = __ldg(t.rep + leaf[v]);
+      if (prefilter) {
+        const float4 lo = __ldg(t.box + 2 * leaf[v]);
+        const float4 hi = __ldg(t.box + 2 * leaf[v] + 1);
+        const float rx = fmaxf(fmaxf(lo.x - cx[v], 0.f), cx[v] - hi.x);
+        const float ry = fmaxf(fmaxf(lo.y - cy[v], 0.f), cy[v] - hi.y);
+        const float rz = fmaxf(fmaxf(lo.z - cz[v], 0.f), cz[v] - hi.z);
+        const float ss = fmaf(rz, rz, fmaf(ry, ry, rx * rx));
+        st = (fast && ss > r2 * band_hi) ? 0 : st;
       }
-      // representative probe (see rep_probe); the rep section is loaded
-      // alongside the box, not through the set
-      if (status[v] == 2) {
-        const float4 rp = __ldg(t.rep + leaf[v]);
-        const float dx = cx[v] - rp.x, dy = cy[v] - rp.y, dz = cz[v] - rp.z;
-        hit[v] = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) <= r2 * band_lo;
-      }
-      if (hit[v]) a.verdict[base + v * blockDim.x + threadIdx.x] = 1;
+      const float dx = cx[v] - rp.x, dy = cy[v] - rp.y, dz = cz[v] - rp.z;
+      hit[v] = st == 2 && fmaf(dz, dz, fmaf(dy, dy, dx * dx)) <= r2 * band_lo;
+      status[v] = st;
     }
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if (hit[v]) a.verdict[base + v * blockDim.x + threadIdx.x] = 1;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       bool resolved = hit[v];
@@ -748,10 +759,12 @@ __device__ __forceinline__ void decide(const Spheres8& sp, const SmemBinned& S, 
     if (!((sp.real >> i) & 1u)) continue;
     const int e = sp.base + i;
     const float mv = combined ? okey_inv(S.minkey[e]) : sp.mn[i];
-    const int q = a.lmeta[a.perm[s0 + e]].x;
+    // the sphere id is gathered only for spheres that need it (hits and the
+    // rare ambiguous ones): a random 4-B read costs a whole DRAM sector
     if (((hm >> i) & 1u) || mv <= S.lim_lo[e]) {
-      a.verdict[q] = 1;
+      a.verdict[a.lmeta[a.perm[s0 + e]].x] = 1;
     } else if (!(mv > S.lim_hi[e])) {
+      const int q = a.lmeta[a.perm[s0 + e]].x;
       const unsigned j = atomicAdd(a.slow_n, 1u);
       a.slow[j] = make_int2(q, int(leaf));
       atomicAdd(a.n_refined, 1u);
