@@ -167,3 +167,36 @@ def test_host_pipeline_chunks_counters_and_bad_radius():
     r_bad[7_000_000] = 0.001
     with pytest.raises(ValueError, match="radius 0.5 outside"):
         P.collides_many(tree, c, r_bad)
+
+
+def test_binned_aabb_boundary_spheres():
+    """Spheres whose centre lies exactly r (and one ulp either side) outside a
+    leaf's affordance box: the binned path's conservative fp32 AABB filter
+    must give the reference verdict (the reference's own float64 AABB test is
+    never the deciding factor, but these are the cases that stress it)."""
+    rng = np.random.default_rng(77)
+    pts = rng.uniform(0, 1, (3000, 3)).astype(np.float32)
+    t = O.construct(pts, 0.01, 0.08)
+    tree = upload(t)
+    lo, hi = t["aff_lo"].reshape(-1, 3), t["aff_hi"].reshape(-1, 3)
+    leaves = rng.integers(0, len(lo), 4000)
+    ok = np.isfinite(lo).all(1) & np.isfinite(hi).all(1)  # empty sets have +inf boxes
+    leaves = leaves[ok[leaves]]
+    r = rng.uniform(0.01, 0.08, len(leaves)).astype(np.float32)
+    ax = rng.integers(0, 3, len(leaves))
+    c = rng.uniform(lo[leaves], hi[leaves]).astype(np.float32)
+    side = rng.integers(0, 2, len(leaves)).astype(bool)
+    idx = np.arange(len(leaves))
+    c[idx, ax] = np.where(side, hi[leaves, ax] + r, lo[leaves, ax] - r)
+    cs = [c]
+    for d in (-1, 1):  # one ulp inward / outward
+        c2 = c.copy()
+        c2[idx, ax] = np.nextafter(c[idx, ax], c[idx, ax] + d * np.float32(1.0))
+        cs.append(c2)
+    c = np.concatenate(cs)
+    r = np.concatenate([r] * 3)
+    exp = O.collides_many(t, c, r)
+    assert np.array_equal(q(tree, c, r), exp)
+    assert np.array_equal(q(tree, c, r, mode=DIRECT), exp)
+    n8 = len(r) // 8 * 8
+    assert np.array_equal(q(tree, c[:n8], r[:n8], 8), exp[:n8].reshape(-1, 8).any(1))
