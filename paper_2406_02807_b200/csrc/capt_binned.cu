@@ -9,12 +9,12 @@
 //                     and its whole lane group), warp-aggregated per-leaf
 //                     counts; spheres needing the exact path go to a queue
 //                     (k_bin_count: generic k / float64 inputs)
-//   K2 (CUB scans)    per-leaf start offsets and tile counts
+//   K2 k_scan_tiles   per-leaf start offsets and first-tile indices, one CTA;
+//                     K3a writes the (leaf, chunk of <= 1024 spheres) tiles
 //   K3 k_part_bucket, k_part_leaf: group K1's compact list of binned spheres
 //                     by leaf in two shared-memory-ranked passes (bucket of
 //                     leaves, then leaf) into a permutation; K5 gathers the
 //                     float4 {c, r} records through it
-//   K4 k_make_tiles   (leaf, chunk of <= 1024 spheres) work items
 //   K5 k_binned_scan  persistent CTAs pull tiles from an atomic counter; the
 //                     leaf's set is staged once into shared memory in local
 //                     coordinates b = p - o with w = |b|^2, and each thread
@@ -200,7 +200,7 @@ __device__ __forceinline__ int rep_probe(const BinArgs& a, int64_t q, int status
     const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
     hit = d2 <= (r * r) * (1.0f - kTau);
   }
-  if (hit) a.verdict[q] = 1;
+  if (q < a.n) a.verdict[q] = hit ? 1 : 0;  // every byte written: no memset
   bool resolved = hit;
   if (a.L > 1) {
     const unsigned hb = __ballot_sync(0xffffffffu, hit);
@@ -390,8 +390,10 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
       status[v] = st;
     }
 #pragma unroll
-    for (int v = 0; v < V; ++v)
-      if (hit[v]) a.verdict[base + v * blockDim.x + threadIdx.x] = 1;
+    for (int v = 0; v < V; ++v) {
+      const int q = base + v * blockDim.x + threadIdx.x;
+      if (q < n) a.verdict[q] = hit[v] ? 1 : 0;  // every byte written: no memset
+    }
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       bool resolved = hit[v];
@@ -461,6 +463,14 @@ __global__ void __launch_bounds__(256) k_part_bucket(BinArgs a) {
   __shared__ uint32_t gbase[kBuckets];
   const uint32_t n = *a.list_n;
   const int tid = threadIdx.x;
+  // the K5 tile list: (leaf, chunk) for every chunk of <= kTS spheres, leaf
+  // by leaf in the tree's order (K2 gave each leaf its first tile index)
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + tid; j < a.t.n;
+       j += int64_t(gridDim.x) * blockDim.x) {
+    const int leaf = a.t.order[j];
+    const uint32_t nt = (a.counts[leaf] + kTS - 1) / kTS, t0 = a.tstart[j];
+    for (uint32_t k = 0; k < nt; ++k) a.tiles[t0 + k] = make_int2(leaf, int(k));
+  }
   for (uint32_t c0 = blockIdx.x * kPartItems; c0 < n; c0 += gridDim.x * kPartItems) {
     hist[tid] = 0;
     __syncthreads();
@@ -546,26 +556,76 @@ __global__ void __launch_bounds__(256) k_part_leaf(BinArgs a) {
   }
 }
 
-// Tiles are laid out leaf by leaf in the tree's order section (descending
-// set size), so the persistent K5 CTAs draw the costliest tiles first and the
-// tail of the launch is made of small ones.
-__global__ void k_tile_counts(int64_t n, const uint32_t* __restrict__ counts,
-                              const int* __restrict__ order, uint32_t* __restrict__ tcount) {
-  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
-       j += int64_t(gridDim.x) * blockDim.x)
-    tcount[j] = (counts[order[j]] + kTS - 1) / kTS;
-}
-
-__global__ void k_make_tiles(int64_t n, const uint32_t* __restrict__ tcount,
-                             const uint32_t* __restrict__ tstart, const int* __restrict__ order,
-                             int2* __restrict__ tiles, uint32_t* __restrict__ n_tiles) {
-  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
-       j += int64_t(gridDim.x) * blockDim.x) {
-    const uint32_t c = tcount[j], s = tstart[j];
-    const int leaf = order[j];
-    for (uint32_t i = 0; i < c; ++i) tiles[s + i] = make_int2(leaf, int(i));
-    if (j == n - 1) *n_tiles = s + c;
+// K2: one CTA turns the per-leaf counts into per-leaf start offsets (leaf
+// order; K3's buckets are leaf ranges) and per-leaf first-tile indices in
+// tile order (the tile list itself is written by K3a's CTAs).  Tiles are laid
+// out leaf by leaf in the tree's order section (descending set size), so the
+// persistent K5 CTAs draw the costliest tiles first and the tail of the
+// launch is made of small ones.  One launch instead of two device-wide scans
+// (this stage is pure latency at every batch size).
+constexpr int kScanT = 512;
+constexpr int kScanI = 16;  // leaves per thread per pass
+__global__ void __launch_bounds__(kScanT) k_scan_tiles(BinArgs a) {
+  using Load = cub::BlockLoad<uint32_t, kScanT, kScanI, cub::BLOCK_LOAD_TRANSPOSE>;
+  using Store = cub::BlockStore<uint32_t, kScanT, kScanI, cub::BLOCK_STORE_TRANSPOSE>;
+  using Scan = cub::BlockScan<uint32_t, kScanT>;
+  __shared__ union {
+    typename Load::TempStorage load;
+    typename Store::TempStorage store;
+    typename Scan::TempStorage scan;
+  } tmp;
+  __shared__ uint32_t carry[2];
+  const int nl = int(a.t.n);
+  const int tid = threadIdx.x;
+  if (tid == 0) carry[0] = carry[1] = 0;
+  for (int p0 = 0; p0 < nl; p0 += kScanT * kScanI) {
+    const int valid = min(kScanT * kScanI, nl - p0);
+    uint32_t c[kScanI], ord[kScanI], tc[kScanI];
+    __syncthreads();  // carry visible; temp storage free
+    Load(tmp.load).Load(a.counts + p0, c, valid, 0u);
+    __syncthreads();
+    Load(tmp.load).Load(reinterpret_cast<const uint32_t*>(a.t.order) + p0, ord, valid, 0u);
+#pragma unroll
+    for (int i = 0; i < kScanI; ++i)  // blocked: leaves p0 + tid*kScanI + i
+      tc[i] = (tid * kScanI + i < valid) ? (a.counts[ord[i]] + kTS - 1) / kTS : 0u;
+    uint32_t cs = 0, ts = 0;
+#pragma unroll
+    for (int i = 0; i < kScanI; ++i) {
+      cs += c[i];
+      ts += tc[i];
+    }
+    const uint32_t c0 = carry[0], t0 = carry[1];
+    uint32_t cpre, tpre, ctot, ttot;
+    __syncthreads();
+    Scan(tmp.scan).ExclusiveSum(cs, cpre, ctot);
+    __syncthreads();
+    Scan(tmp.scan).ExclusiveSum(ts, tpre, ttot);
+    cpre += c0;
+    tpre += t0;
+    uint32_t st[kScanI];
+#pragma unroll
+    for (int i = 0; i < kScanI; ++i) {
+      st[i] = cpre;
+      cpre += c[i];
+    }
+    __syncthreads();
+    Store(tmp.store).Store(a.start + p0, st, valid);
+    uint32_t tst[kScanI];
+#pragma unroll
+    for (int i = 0; i < kScanI; ++i) {
+      tst[i] = tpre;
+      tpre += tc[i];
+    }
+    __syncthreads();
+    Store(tmp.store).Store(a.tstart + p0, tst, valid);
+    __syncthreads();
+    if (tid == 0) {
+      carry[0] = c0 + ctot;
+      carry[1] = t0 + ttot;
+    }
   }
+  __syncthreads();
+  if (tid == 0) *a.n_tiles = carry[1];
 }
 
 // ---- packed fp32x2 helpers (sm_100: FFMA2 / FMNMX3) ----
@@ -861,41 +921,61 @@ __global__ void k_slow(BinArgs a) {
     const uint32_t m4 = (st.y + 3u) & ~3u;
     const double R = __dmul_rn(r64, r64);
     bool hit = false;
-    for (uint32_t j = lane; j < st.y && !hit; j += 32) {
-      double sum = 0.0;
+    // 4 rows per lane per step: the loads of 128 points are in flight at once
+    for (uint32_t j0 = 0; j0 < st.y && !__any_sync(0xffffffffu, hit); j0 += 128) {
+      float p[4][kMaxK];
 #pragma unroll
-      for (int d = 0; d < kMaxK; ++d) {
-        if (d >= t.k) break;
-        const double x = __dsub_rn(c64[d], double(base[d * m4 + j]));
-        const double sq = __dmul_rn(x, x);
-        sum = d == 0 ? sq : __dadd_rn(sum, sq);
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t j = j0 + u * 32 + lane;
+#pragma unroll
+        for (int d = 0; d < kMaxK; ++d)
+          p[u][d] = (j < st.y && d < t.k) ? __ldg(base + d * m4 + j) : 0.f;
       }
-      hit = sum <= R;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (j0 + u * 32 + lane >= st.y) continue;
+        double sum = 0.0;
+#pragma unroll
+        for (int d = 0; d < kMaxK; ++d) {
+          if (d >= t.k) break;
+          const double x = __dsub_rn(c64[d], double(p[u][d]));
+          const double sq = __dmul_rn(x, x);
+          sum = d == 0 ? sq : __dadd_rn(sum, sq);
+        }
+        hit |= sum <= R;
+      }
     }
     if (__any_sync(0xffffffffu, hit) && lane == 0) a.verdict[e.x] = 1;
   }
 }
 
+// One thread per lane group: its L verdict bytes in one vector load (L <= 8:
+// 1/2/4/8 bytes; larger L: several 8-byte loads), coalesced across the warp;
+// the warp ballot is the verdict word.  The verdict array is padded to a
+// multiple of 8 bytes past n.
 __global__ void k_pack(int64_t n_groups, int L, const uint8_t* __restrict__ v,
                        uint32_t* __restrict__ bits, int64_t n_words) {
-  for (int64_t w = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < n_words;
-       w += int64_t(gridDim.x) * blockDim.x) {
-    uint32_t word = 0;
-    const int64_t g0 = w * 32;
-    const int ng = int(min(int64_t(32), n_groups - g0));
-    if (L == 8) {
-      const uint64_t* v8 = reinterpret_cast<const uint64_t*>(v);
-      for (int g = 0; g < ng; ++g) word |= uint32_t(v8[g0 + g] != 0) << g;
-    } else if (L == 1) {
-      for (int g = 0; g < ng; ++g) word |= uint32_t(v[g0 + g] != 0) << g;
-    } else {
-      for (int g = 0; g < ng; ++g) {
-        uint32_t any = 0;
-        for (int l = 0; l < L; ++l) any |= v[(g0 + g) * L + l];
-        word |= uint32_t(any != 0) << g;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int64_t n_thr = n_words * 32;
+  for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < n_thr; g += stride) {
+    bool any = false;
+    if (g < n_groups) {
+      const uint8_t* p = v + g * L;
+      switch (L) {
+        case 1: any = p[0] != 0; break;
+        case 2: any = *reinterpret_cast<const uint16_t*>(p) != 0; break;
+        case 4: any = *reinterpret_cast<const uint32_t*>(p) != 0; break;
+        case 8: any = *reinterpret_cast<const uint64_t*>(p) != 0; break;
+        default: {
+          const uint64_t* q = reinterpret_cast<const uint64_t*>(p);
+          uint64_t acc = 0;
+          for (int k = 0; k < L / 8; ++k) acc |= q[k];
+          any = acc != 0;
+        }
       }
     }
-    bits[w] = word;
+    const uint32_t word = __ballot_sync(0xffffffffu, any);
+    if ((threadIdx.x & 31) == 0) bits[g >> 5] = word;
   }
 }
 
@@ -986,23 +1066,25 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.flags = flags;
   a.first_bad = first_bad;
   const int64_t nl = t.n;
-  uint32_t* ctr = A.get<uint32_t>(5);  // slow_n, n_tiles, tile_ctr, n_refined, list_n
-  a.counts = A.get<uint32_t>(nl);
+  // everything that must start at zero, in one block (one memset):
+  // counters (slow_n, n_tiles, tile_ctr, n_refined, list_n) | counts | cursor | bcursor
+  const int64_t zero_words = 8 + 2 * nl + kBuckets;
+  uint32_t* ctr = A.get<uint32_t>(zero_words);
+  a.counts = ctr ? ctr + 8 : nullptr;
+  a.cursor = ctr ? ctr + 8 + nl : nullptr;
+  a.bcursor = ctr ? ctr + 8 + 2 * nl : nullptr;
   a.start = A.get<uint32_t>(nl);
-  uint32_t* tcount = A.get<uint32_t>(nl);
-  uint32_t* tstart = A.get<uint32_t>(nl);
+  a.tstart = A.get<uint32_t>(nl);
   a.tiles = A.get<int2>(nl + n / kTS + 1);
   a.perm = A.get<uint32_t>(n);
   a.verdict = A.get<uint8_t>(n + 8);
   a.slow = A.get<int2>(n);
   a.lrec = A.get<float4>(n);
   a.lmeta = A.get<int2>(n);
-  a.cursor = A.get<uint32_t>(nl);
   a.part = A.get<int2>(n);
-  a.bcursor = A.get<uint32_t>(kBuckets);
   a.bshift = 0;
   while ((nl >> a.bshift) > kBuckets) ++a.bshift;
-  if (!a.part || !a.bcursor || !ctr || !a.counts || !a.start || !tcount || !tstart || !a.tiles || !a.perm ||
+  if (!a.part || !a.bcursor || !ctr || !a.counts || !a.start || !a.tstart || !a.tiles || !a.perm ||
       !a.verdict || !a.slow || !a.lrec || !a.lmeta || !a.cursor)
     return fail(CAPT_ENOMEM, "binned scratch allocation");
   {
@@ -1019,11 +1101,8 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.list_n = ctr + 4;
   StageTimer& tm = g_stage_timer;
   tm.mark(0, s);
-  CAPT_CUDA(cudaMemsetAsync(ctr, 0, 20, s));
-  CAPT_CUDA(cudaMemsetAsync(a.counts, 0, 4 * nl, s));
-  CAPT_CUDA(cudaMemsetAsync(a.cursor, 0, 4 * nl, s));
-  CAPT_CUDA(cudaMemsetAsync(a.bcursor, 0, 4 * kBuckets, s));
-  CAPT_CUDA(cudaMemsetAsync(a.verdict, 0, n + 8, s));
+  // (verdict bytes need no clearing: K1 writes one for every sphere)
+  CAPT_CUDA(cudaMemsetAsync(ctr, 0, 4 * zero_words, s));
   const bool f64 = flags & CAPT_INPUT_F64;
   const int G = grid_for(n, 256, 8);
   constexpr int V = 4;
@@ -1034,15 +1113,7 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   else k_bin_count<float><<<G, 256, 0, s>>>(a);
   tm.mark(2, s);
   // per-leaf starts and tiles
-  size_t tb = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tb, a.counts, a.start, nl, s);
-  void* tmp = A.get<char>(tb);
-  if (!tmp) return fail(CAPT_ENOMEM, "binned scratch allocation");
-  CAPT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, a.counts, a.start, nl, s));
-  const int Gl = grid_for(nl, 256, 8);
-  k_tile_counts<<<Gl, 256, 0, s>>>(nl, a.counts, t.order, tcount);
-  CAPT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, tcount, tstart, nl, s));
-  k_make_tiles<<<Gl, 256, 0, s>>>(nl, tcount, tstart, t.order, a.tiles, a.n_tiles);
+  k_scan_tiles<<<1, kScanT, 0, s>>>(a);
   tm.mark(3, s);
   {
     const int Gp = grid_for((n + kPartItems - 1) / kPartItems * 256, 256, 4);
@@ -1063,11 +1134,11 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   tm.mark(6, s);
   if (f64) k_slow<double><<<sms, 128, 0, s>>>(a);
   else k_slow<float><<<sms, 128, 0, s>>>(a);
-  k_pack<<<grid_for(n_words, 256, 8), 256, 0, s>>>(n / L, L, a.verdict, bits, n_words);
+  k_pack<<<grid_for(n_words * 32, 256, 8), 256, 0, s>>>(n / L, L, a.verdict, bits, n_words);
   tm.mark(7, s);
   tm.finish(s);
   CAPT_CUDA(cudaGetLastError());
-  note_launches(10);  // count, 2 scans, tile counts, tiles, 2 partition passes, scan, slow, pack
+  note_launches(7);  // count, scan+tiles, 2 partition passes, scan, slow, pack
   static const bool debug = getenv("CAPT_DEBUG") != nullptr;
   if (debug) {
     uint32_t h[4], last[2];

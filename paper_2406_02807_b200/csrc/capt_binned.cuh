@@ -15,6 +15,7 @@ struct BinArgs {
   uint32_t flags;
   uint32_t* counts;   // per leaf: AABB-passing spheres
   uint32_t* start;    // per leaf: first binned slot
+  uint32_t* tstart;   // per order index: first tile
   int2* tiles;        // (leaf, chunk)
   uint8_t* verdict;   // per sphere
   int2* slow;         // (sphere, leaf) for the exact float64 path
