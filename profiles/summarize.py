@@ -2,6 +2,7 @@
 
     python profiles/summarize.py launches <launches.csv> <out.md>
     python profiles/summarize.py full <report.ncu-rep> <out.json>
+    python profiles/summarize.py sweep <sweep.json> <out.md>
 
 ``launches``: per-kernel device time from an
 ``ncu --metrics gpu__time_duration.sum --clock-control none`` launch list
@@ -75,5 +76,27 @@ def full(path: str, out: str) -> None:
     json.dump(res, open(out, "w"), indent=1)
 
 
+def sweep(path: str, out: str) -> None:
+    """bench.py --sweep JSON line -> markdown table (G sphere queries/s per
+    call | with CUDA-graph replay, path taken, label check)."""
+    d = json.loads(open(path).read().strip().splitlines()[-1])
+    rows = d["rows"]
+    rates = sorted({r["rate"] for r in rows})
+    ns = sorted({r["n"] for r in rows})
+    lines = [f"# {d['sweep']} (1x B200, tree {d['tree_leaves']} leaves)", "",
+             "G sphere queries/s: per call | CUDA-graph replay; path d = unbinned "
+             "(warp kernel), b = binned; ! = label mismatch", "",
+             "| spheres | " + " | ".join(f"rate {x}" for x in rates) + " |",
+             "|---:|" + "---:|" * len(rates)]
+    for n in ns:
+        cells = []
+        for x in rates:
+            r = [q for q in rows if q["n"] == n and q["rate"] == x][0]
+            cells.append(f"{r['queries_per_s'] / 1e9:.2f} \\| {r['queries_per_s_graph'] / 1e9:.2f} "
+                         f"{r['mode'][0]}{'' if r['labels_match'] else ' !'}")
+        lines.append(f"| {n:,} | " + " | ".join(cells) + " |")
+    open(out, "w").write("\n".join(lines) + "\n")
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"launches": launches, "full": full, "sweep": sweep}[sys.argv[1]](sys.argv[2], sys.argv[3])
