@@ -24,7 +24,8 @@
 //                     a sphere collides iff min_t <= r^2 - |a|^2; a proven
 //                     error band (64u relative to |a|^2 + |b|^2 + r^2) sends
 //                     the rare ambiguous sphere to the exact queue
-//   K6 k_slow         exact float64 scan of the queue, one warp per sphere
+//   K6 k_slow         K5's hits (by list index) -> sphere verdicts; exact
+//                     float64 scan of the queue, one warp per sphere
 //   K7 k_pack         verdict bytes -> bit words, OR over each lane group
 #include <cub/cub.cuh>
 
@@ -178,6 +179,7 @@ __device__ __forceinline__ void record_bin(const BinArgs& a, int64_t q, int stat
     const unsigned j = lbase + __popc(act & ((1u << lane) - 1u));
     a.lrec[j] = rc;
     a.lmeta[j] = make_int2(int(q), leaf);
+    a.lhit[j] = 0;
   }
   if (status == 3) {
     const unsigned i = atomicAdd(a.slow_n, 1u);
@@ -432,6 +434,7 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
         if (status[v] == 2) {
           const unsigned p = j + __popc(act[v] & lt);
           __stcs(a.lrec + p, make_float4(cx[v], cy[v], cz[v], r[v]));
+          a.lhit[p] = 0;
           __stcs(a.lmeta + p, make_int2(base + v * int(blockDim.x) + int(threadIdx.x), leaf[v]));
         }
         j += __popc(act[v]);
@@ -468,8 +471,23 @@ __global__ void __launch_bounds__(256) k_part_bucket(BinArgs a) {
   for (int64_t j = int64_t(blockIdx.x) * blockDim.x + tid; j < a.t.n;
        j += int64_t(gridDim.x) * blockDim.x) {
     const int leaf = a.t.order[j];
-    const uint32_t nt = (a.counts[leaf] + kTS - 1) / kTS, t0 = a.tstart[j];
-    for (uint32_t k = 0; k < nt; ++k) a.tiles[t0 + k] = make_int2(leaf, int(k));
+    const uint32_t total = a.counts[leaf];
+    const uint32_t nt = (total + kTS - 1) / kTS, t0 = a.tstart[j];
+    if (nt) {
+      TileMeta tm;
+      tm.leaf = leaf;
+      const uint2 st = a.t.set[leaf];
+      tm.setx = st.x;
+      tm.m = st.y;
+      tm.pad[0] = tm.pad[1] = tm.pad[2] = 0;
+      tm.org = a.t.org[leaf];
+      const uint32_t s0 = a.start[leaf];
+      for (uint32_t k = 0; k < nt; ++k) {
+        tm.s0 = s0 + k * kTS;
+        tm.cnt = int(min(uint32_t(kTS), total - k * kTS));
+        a.tiles[t0 + k] = tm;
+      }
+    }
   }
   for (uint32_t c0 = blockIdx.x * kPartItems; c0 < n; c0 += gridDim.x * kPartItems) {
     hist[tid] = 0;
@@ -819,10 +837,10 @@ __device__ __forceinline__ void decide(const Spheres8& sp, const SmemBinned& S, 
     if (!((sp.real >> i) & 1u)) continue;
     const int e = sp.base + i;
     const float mv = combined ? okey_inv(S.minkey[e]) : sp.mn[i];
-    // the sphere id is gathered only for spheres that need it (hits and the
-    // rare ambiguous ones): a random 4-B read costs a whole DRAM sector
+    // hits are flagged by list index (the slot's permutation entry); the
+    // sphere id is gathered only for the rare ambiguous spheres
     if (((hm >> i) & 1u) || mv <= S.lim_lo[e]) {
-      a.verdict[a.lmeta[a.perm[s0 + e]].x] = 1;
+      a.lhit[a.perm[s0 + e]] = 1;  // mapped back to the sphere by K6
     } else if (!(mv > S.lim_hi[e])) {
       const int q = a.lmeta[a.perm[s0 + e]].x;
       const unsigned j = atomicAdd(a.slow_n, 1u);
@@ -847,12 +865,12 @@ __global__ void __launch_bounds__(kBT, CAPT_K5_MINB) k_binned_scan(BinArgs a) {
     __syncthreads();
     const int tile = S.tile;
     if (tile >= int(*a.n_tiles)) break;
-    const int2 tl = a.tiles[tile];
-    const int64_t leaf = tl.x;
-    const int64_t s0 = int64_t(a.start[leaf]) + int64_t(tl.y) * kTS;
-    const int cnt = int(min(uint32_t(kTS), a.counts[leaf] - uint32_t(tl.y) * kTS));
-    const uint2 st = t.set[leaf];
-    const float4 org = t.org[leaf];
+    const TileMeta tm = a.tiles[tile];
+    const int64_t leaf = tm.leaf;
+    const int64_t s0 = tm.s0;
+    const int cnt = tm.cnt;
+    const uint2 st = make_uint2(tm.setx, tm.m);
+    const float4 org = tm.org;
     const uint32_t m = st.y;
     const uint32_t m4 = (m + 3u) & ~3u;
     const float* xs = reinterpret_cast<const float*>(t.data + st.x);
@@ -907,6 +925,27 @@ __global__ void __launch_bounds__(kBT, CAPT_K5_MINB) k_binned_scan(BinArgs a) {
 // query.py:96-99 arithmetic (fp64, no FMA), ballot OR.
 template <typename InT>
 __global__ void k_slow(BinArgs a) {
+  // K5's hits, flagged by list index -> the spheres' verdict bytes
+  {
+    const uint32_t nl = *a.list_n;
+    // 8 entries per thread, strided by the grid so that every load coalesces
+    constexpr int kU = 8;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t j0 = blockIdx.x * blockDim.x + threadIdx.x; j0 < nl; j0 += kU * stride) {
+      uint8_t f[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t j = j0 + u * stride;
+        f[u] = j < nl ? __ldcs(a.lhit + j) : 0;
+      }
+      int q[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) q[u] = f[u] ? __ldcs(&a.lmeta[j0 + u * stride].x) : -1;
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (q[u] >= 0) a.verdict[q[u]] = 1;
+    }
+  }
   const unsigned n = *a.slow_n;
   const int lane = threadIdx.x & 31;
   const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1075,17 +1114,18 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.bcursor = ctr ? ctr + 8 + 2 * nl : nullptr;
   a.start = A.get<uint32_t>(nl);
   a.tstart = A.get<uint32_t>(nl);
-  a.tiles = A.get<int2>(nl + n / kTS + 1);
+  a.tiles = A.get<TileMeta>(nl + n / kTS + 1);
   a.perm = A.get<uint32_t>(n);
   a.verdict = A.get<uint8_t>(n + 8);
   a.slow = A.get<int2>(n);
   a.lrec = A.get<float4>(n);
   a.lmeta = A.get<int2>(n);
+  a.lhit = A.get<uint8_t>(n);
   a.part = A.get<int2>(n);
   a.bshift = 0;
   while ((nl >> a.bshift) > kBuckets) ++a.bshift;
   if (!a.part || !a.bcursor || !ctr || !a.counts || !a.start || !a.tstart || !a.tiles || !a.perm ||
-      !a.verdict || !a.slow || !a.lrec || !a.lmeta || !a.cursor)
+      !a.verdict || !a.slow || !a.lrec || !a.lmeta || !a.lhit || !a.cursor)
     return fail(CAPT_ENOMEM, "binned scratch allocation");
   {
     float lo = float(t.r_min), hi = float(t.r_max);
@@ -1132,8 +1172,8 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   tm.mark(5, s);
   k_binned_scan<<<sms * occ, kBT, sizeof(SmemBinned), s>>>(a);
   tm.mark(6, s);
-  if (f64) k_slow<double><<<sms, 128, 0, s>>>(a);
-  else k_slow<float><<<sms, 128, 0, s>>>(a);
+  if (f64) k_slow<double><<<sms * 8, 128, 0, s>>>(a);
+  else k_slow<float><<<sms * 8, 128, 0, s>>>(a);
   k_pack<<<grid_for(n_words * 32, 256, 8), 256, 0, s>>>(n / L, L, a.verdict, bits, n_words);
   tm.mark(7, s);
   tm.finish(s);

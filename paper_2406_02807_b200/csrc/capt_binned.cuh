@@ -5,6 +5,18 @@
 
 namespace capt {
 
+// One K5 work item: up to 1024 binned spheres of one leaf, with everything
+// K5 needs to start it (one 48-B load instead of a chain of dependent ones).
+struct __align__(16) TileMeta {
+  int leaf;
+  uint32_t s0;    // first binned slot
+  int cnt;        // spheres in the tile
+  uint32_t setx;  // set start (float4 units)
+  uint32_t m;     // set size
+  uint32_t pad[3];
+  float4 org;     // binned-scan origin of the set
+};
+
 struct BinArgs {
   DevTree t;
   const void* centers;
@@ -16,7 +28,7 @@ struct BinArgs {
   uint32_t* counts;   // per leaf: AABB-passing spheres
   uint32_t* start;    // per leaf: first binned slot
   uint32_t* tstart;   // per order index: first tile
-  int2* tiles;        // (leaf, chunk)
+  TileMeta* tiles;
   uint8_t* verdict;   // per sphere
   int2* slow;         // (sphere, leaf) for the exact float64 path
   uint32_t* slow_n;
@@ -26,6 +38,7 @@ struct BinArgs {
   unsigned long long* first_bad;
   float4* lrec;       // compact list of binned spheres (K1 -> K3): {c, r}
   int2* lmeta;        //   ... and (sphere id, leaf)
+  uint8_t* lhit;      //   ... and K5's hit flag (mapped back to spheres by K6)
   uint32_t* list_n;   //   ... length
   uint32_t* cursor;   // per leaf: scatter cursor (K3b)
   int2* part;         // K3a output: (leaf, list index), grouped by leaf bucket
