@@ -860,11 +860,16 @@ __global__ void __launch_bounds__(kBT, CAPT_K5_MINB) k_binned_scan(BinArgs a) {
   ulonglong2* const sB = S.B;
   const DevTree& t = a.t;
   const int tid = threadIdx.x;
+  const int n_tiles = int(*a.n_tiles);
+  if (tid == 0) S.tile = int(atomicAdd(a.tile_ctr, 1u));
+  __syncthreads();
   while (true) {
-    if (tid == 0) S.tile = int(atomicAdd(a.tile_ctr, 1u));
-    __syncthreads();
     const int tile = S.tile;
-    if (tile >= int(*a.n_tiles)) break;
+    if (tile >= n_tiles) break;
+    // the next tile is drawn now (by warp 1, off warp 0's path); its index is
+    // published after the tile's decision barrier
+    int next = 0;
+    if (tid == 32) next = int(atomicAdd(a.tile_ctr, 1u));
     const TileMeta tm = a.tiles[tile];
     const int64_t leaf = tm.leaf;
     const int64_t s0 = tm.s0;
@@ -916,6 +921,7 @@ __global__ void __launch_bounds__(kBT, CAPT_K5_MINB) k_binned_scan(BinArgs a) {
         if ((sp.real >> i) & 1u) atomicMin(&S.minkey[sp.base + i], okey(sp.mn[i]));
     }
     __syncthreads();
+    if (tid == 32) S.tile = next;  // every thread has read S.tile by now
     if (active && ph == 0) decide(sp, S, a, s0, leaf, S.hitmask[slot], P > 1);
     __syncthreads();  // tile state (minkey, hitmask, smem points) free for the next tile
   }
