@@ -28,6 +28,7 @@
 //                     float64 scan of the queue, one warp per sphere
 //   K7 k_pack         verdict bytes -> bit words, OR over each lane group
 #include <cub/cub.cuh>
+#include <cuda_fp16.h>
 
 #include <climits>
 #include <cstdio>
@@ -253,6 +254,17 @@ __global__ void __launch_bounds__(256) k_bin_count(BinArgs a) {
   }
 }
 
+__device__ __forceinline__ void ld_v8(const float* p, float (&v)[8]) {
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+        "=f"(v[7])
+      : "l"(p));
+}
+__device__ __forceinline__ float2 h2f2(float bits) {
+  const unsigned u = __float_as_uint(bits);
+  return __half22float2(*reinterpret_cast<const __half2*>(&u));
+}
+
 __device__ __forceinline__ float lds_f32(unsigned addr) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
@@ -357,7 +369,8 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
         off[v] = 2 * off[v] + (c > tv ? 8u : 4u);
       }
     }
-    // per-sphere classification, branch-free.  The AABB test only has to
+    // per-sphere classification, branch-free.  The AABB test (on the probe
+    // record's outward-rounded fp16 box) only has to
     // be conservative here: every point of a set lies inside the set's box and
     // the reference's float64 box distance is a monotone function of the same
     // rounded differences, so s_box <= s_point and a sphere the reference
@@ -377,13 +390,15 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
       // non-finite centre with a finite radius never collides (float64 r^2 is finite)
       int st = fast ? 2 : ((!cfin && isfinite(r[v])) ? 0 : 3);
       st = valid[v] ? st : 0;
-      const float4 rp = __ldg(t.rep + leaf[v]);
+      // one 32-B load: representative + outward-rounded fp16 box
+      float pr[8];
+      ld_v8(t.probe + 8 * leaf[v], pr);
+      const float4 rp = make_float4(pr[0], pr[1], pr[2], 0.f);
       if (prefilter) {
-        const float4 lo = __ldg(t.box + 2 * leaf[v]);
-        const float4 hi = __ldg(t.box + 2 * leaf[v] + 1);
-        const float rx = fmaxf(fmaxf(lo.x - cx[v], 0.f), cx[v] - hi.x);
-        const float ry = fmaxf(fmaxf(lo.y - cy[v], 0.f), cy[v] - hi.y);
-        const float rz = fmaxf(fmaxf(lo.z - cz[v], 0.f), cz[v] - hi.z);
+        const float2 l01 = h2f2(pr[3]), l2h0 = h2f2(pr[4]), h12 = h2f2(pr[5]);
+        const float rx = fmaxf(fmaxf(l01.x - cx[v], 0.f), cx[v] - l2h0.y);
+        const float ry = fmaxf(fmaxf(l01.y - cy[v], 0.f), cy[v] - h12.x);
+        const float rz = fmaxf(fmaxf(l2h0.x - cz[v], 0.f), cz[v] - h12.y);
         const float ss = fmaf(rz, rz, fmaf(ry, ry, rx * rx));
         st = (fast && ss > r2 * band_hi) ? 0 : st;
       }

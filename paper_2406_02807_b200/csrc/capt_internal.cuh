@@ -15,6 +15,10 @@
 //   rep    float4[n]                row 0 of each set (xyz), loaded beside the box
 //   order  int32[n]                 leaves by descending set size (binned K5 takes
 //                                   the costliest tiles first: shorter tail)
+//   probe  float[8][n]              the binned classifier's per-leaf record, one
+//                                   32-B load: representative xyz (fp32) and the
+//                                   leaf box as outward-rounded fp16 (lo.xyz rounded
+//                                   down, hi.xyz up -- a conservative box)
 #pragma once
 
 #include <cuda_runtime.h>
@@ -27,7 +31,7 @@
 namespace capt {
 
 constexpr uint64_t kSlabMagic = 0x3030324254504143ull;  // "CAPTB200"
-constexpr int kSlabVersion = 4;
+constexpr int kSlabVersion = 5;
 constexpr int kMaxK = 3;
 
 struct SlabHeader {
@@ -48,7 +52,8 @@ struct SlabHeader {
   int64_t off_org;    // byte offset of the org section
   int64_t off_rep;    // byte offset of the rep section
   int64_t off_order;  // byte offset of the order section
-  int64_t reserved[7];
+  int64_t off_probe;  // byte offset of the probe section
+  int64_t reserved[6];
 };
 static_assert(sizeof(SlabHeader) <= 256, "header must fit its 256-B section");
 
@@ -64,6 +69,7 @@ struct DevTree {
   const float4* org;
   const float4* rep;  // row 0 of every set (the point owning the cell), +inf for padding
   const int* order;   // leaves by descending set size
+  const float* probe; // 8 floats per leaf: rep xyz, fp16 box (conservative), 2 spare
 };
 
 }  // namespace capt
@@ -109,6 +115,7 @@ inline DevTree view(const capt_tree* t) {
   d.org = reinterpret_cast<const float4*>(t->slab + t->h.off_org);
   d.rep = reinterpret_cast<const float4*>(t->slab + t->h.off_rep);
   d.order = reinterpret_cast<const int*>(t->slab + t->h.off_order);
+  d.probe = reinterpret_cast<const float*>(t->slab + t->h.off_probe);
   return d;
 }
 
@@ -132,6 +139,8 @@ inline int64_t layout_slab(SlabHeader& h, int64_t data_f4) {
   off = align256(off + sizeof(float4) * h.n);
   h.off_order = off;
   off = align256(off + sizeof(int) * h.n);
+  h.off_probe = off;
+  off = align256(off + 32 * h.n);
   h.off_data = off;
   off = align256(off + sizeof(float4) * (data_f4 > 0 ? data_f4 : 1));
   h.data_f4 = data_f4;
@@ -145,7 +154,7 @@ inline int depth_of(int64_t n) {
   return d;
 }
 
-// Fill the org, rep and order sections of a slab whose data is final.
+// Fill the org, rep, order and probe sections of a slab whose data is final.
 int compute_origins(const DevTree& t, cudaStream_t s);
 
 int alloc_slab(capt_tree** out, int device, SlabHeader h);

@@ -1,6 +1,7 @@
 // Tree handles: error plumbing, upload from the reference layout
 // (Capt.__init__ tree.py:74-97), export back to it, slab replication.
 #include <cub/cub.cuh>
+#include <cuda_fp16.h>
 
 #include <atomic>
 #include <cstdio>
@@ -167,7 +168,16 @@ __global__ void k_origins(DevTree t) {
     for (int s = 16; s > 0; s >>= 1) bb = fmaxf(bb, __shfl_xor_sync(0xffffffffu, bb, s));
     if (lane == 0) {
       const_cast<float4*>(t.org)[j] = make_float4(o[0], o[1], o[2], bb);
-      const_cast<float4*>(t.rep)[j] = make_float4(base[0], base[m4], base[2 * m4], 0.f);
+      const float4 rp = make_float4(base[0], base[m4], base[2 * m4], 0.f);
+      const_cast<float4*>(t.rep)[j] = rp;
+      const float4 lo = t.box[2 * j], hi = t.box[2 * j + 1];
+      const __half2 h0 = __halves2half2(__float2half_rd(lo.x), __float2half_rd(lo.y));
+      const __half2 h1 = __halves2half2(__float2half_rd(lo.z), __float2half_ru(hi.x));
+      const __half2 h2 = __halves2half2(__float2half_ru(hi.y), __float2half_ru(hi.z));
+      float4* pr = reinterpret_cast<float4*>(const_cast<float*>(t.probe) + 8 * j);
+      pr[0] = make_float4(rp.x, rp.y, rp.z, __uint_as_float(*reinterpret_cast<const unsigned*>(&h0)));
+      pr[1] = make_float4(__uint_as_float(*reinterpret_cast<const unsigned*>(&h1)),
+                          __uint_as_float(*reinterpret_cast<const unsigned*>(&h2)), 0.f, 0.f);
     }
   }
 }
