@@ -328,11 +328,19 @@ __global__ void __launch_bounds__(kBlock)
         leaf = warp_descend<double>(t, c64, lane);
       }
       const uint2 set = __ldg(t.set + leaf);
+      const float4 rp = __ldg(t.rep + leaf);
       float cx, cy, cz, r2, loB, hiB;
       const int status = classify(t, leaf, c64, r64, prefilter, cx, cy, cz, r2, loB, hiB);
       if (status == ST_FALSE) continue;
       int v = 2;
-      if (status == ST_SCAN) v = warp_scan_f32(t, set, cx, cy, cz, loB, hiB, lane);
+      if (status == ST_SCAN) {
+        // representative probe: row 0 of the set owns the cell holding the
+        // centre; a definite fp32 hit (same band as the scan) ends the sphere
+        const float dx = cx - rp.x, dy = cy - rp.y, dz = cz - rp.z;
+        v = fmaf(dz, dz, fmaf(dy, dy, dx * dx)) <= loB
+                ? 1
+                : warp_scan_f32(t, set, cx, cy, cz, loB, hiB, lane);
+      }
       verdict = (v == 1) || (v == 2 && warp_scan_f64(t, set, c64, r64, lane));
     }
     if (verdict && lane == 0) atomicOr(out_bits + (g >> 5), 1u << (g & 31));
