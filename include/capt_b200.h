@@ -143,6 +143,10 @@ int64_t capt_kernel_launches(void);
  * device in TFLOP/s (CUDA-event timed dependent-chain FMA kernel). */
 int capt_measure_fp32_peak(int device, double* tflops);
 
+/* Diagnostic: one 128x256x16 tf32 tcgen05 product through the library's
+ * tensor-core operand layout; *max_rel_err = worst |D - ref| / sum|a_k b_k|. */
+int capt_tc_selftest(int device, double* max_rel_err);
+
 #ifdef __cplusplus
 }
 #endif
