@@ -38,6 +38,7 @@
 
 #include "capt_binned.cuh"
 #include "capt_query_common.cuh"
+#include "capt_tc.cuh"
 
 namespace capt {
 
@@ -46,6 +47,13 @@ namespace {
 constexpr int kBT = 128;           // threads per binned CTA
 constexpr int kS = 8;              // spheres per thread (4 packed pairs)
 constexpr int kTS = kBT * kS;      // spheres per tile
+#ifndef CAPT_TC_TS
+#define CAPT_TC_TS 128
+#endif
+#ifndef CAPT_TC_NC
+#define CAPT_TC_NC 64
+#endif
+constexpr int kTsTc = CAPT_TC_TS;  // spheres per tile, tensor-core K5
 constexpr int kChunk = 512;        // staged points per shared-memory chunk
 constexpr float kBand = 0x1p-18f;  // 64u
 
@@ -481,25 +489,31 @@ __global__ void __launch_bounds__(256) k_part_bucket(BinArgs a) {
   __shared__ uint32_t gbase[kBuckets];
   const uint32_t n = *a.list_n;
   const int tid = threadIdx.x;
-  // the K5 tile list: (leaf, chunk) for every chunk of <= kTS spheres, leaf
-  // by leaf in the tree's order (K2 gave each leaf its first tile index)
-  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + tid; j < a.t.n;
-       j += int64_t(gridDim.x) * blockDim.x) {
-    const int leaf = a.t.order[j];
-    const uint32_t total = a.counts[leaf];
-    const uint32_t nt = (total + kTS - 1) / kTS, t0 = a.tstart[j];
-    if (nt) {
-      TileMeta tm;
-      tm.leaf = leaf;
+  // the K5 tile list: every chunk of <= ts spheres of a leaf, leaf by leaf in
+  // the tree's order (K2 gave each leaf its first tile index); one warp per
+  // leaf, its lanes write the leaf's tiles
+  {
+    const int lane = tid & 31;
+    const int64_t wg = (int64_t(blockIdx.x) * blockDim.x + tid) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t j = wg; j < a.t.n; j += nw) {
+      const int leaf = a.t.order[j];
+      const uint32_t total = a.counts[leaf];
+      const uint32_t ts = a.ts;
+      const uint32_t nt = (total + ts - 1) / ts;
+      if (!nt) continue;
+      const uint32_t t0 = a.tstart[j], s0 = a.start[leaf];
       const uint2 st = a.t.set[leaf];
-      tm.setx = st.x;
-      tm.m = st.y;
-      tm.pad[0] = tm.pad[1] = tm.pad[2] = 0;
-      tm.org = a.t.org[leaf];
-      const uint32_t s0 = a.start[leaf];
-      for (uint32_t k = 0; k < nt; ++k) {
-        tm.s0 = s0 + k * kTS;
-        tm.cnt = int(min(uint32_t(kTS), total - k * kTS));
+      const float4 org = a.t.org[leaf];
+      for (uint32_t k = lane; k < nt; k += 32) {
+        TileMeta tm;
+        tm.leaf = leaf;
+        tm.setx = st.x;
+        tm.m = st.y;
+        tm.pad[0] = tm.pad[1] = tm.pad[2] = 0;
+        tm.org = org;
+        tm.s0 = s0 + k * ts;
+        tm.cnt = int(min(ts, total - k * ts));
         a.tiles[t0 + k] = tm;
       }
     }
@@ -620,7 +634,7 @@ __global__ void __launch_bounds__(kScanT) k_scan_tiles(BinArgs a) {
     Load(tmp.load).Load(reinterpret_cast<const uint32_t*>(a.t.order) + p0, ord, valid, 0u);
 #pragma unroll
     for (int i = 0; i < kScanI; ++i)  // blocked: leaves p0 + tid*kScanI + i
-      tc[i] = (tid * kScanI + i < valid) ? (a.counts[ord[i]] + kTS - 1) / kTS : 0u;
+      tc[i] = (tid * kScanI + i < valid) ? (a.counts[ord[i]] + a.ts - 1) / a.ts : 0u;
     uint32_t cs = 0, ts = 0;
 #pragma unroll
     for (int i = 0; i < kScanI; ++i) {
@@ -942,6 +956,207 @@ __global__ void __launch_bounds__(kBT, CAPT_K5_MINB) k_binned_scan(BinArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// K5 on the tensor cores (tcgen05, kind::tf32).  For a tile of <= 512 spheres
+// of one leaf and a chunk of <= 128 points of its set:
+//     D[s][p] = w_p + (-2 a_s) . b_p     (a = c - o, b = p - o, w = |b|^2)
+// as ONE 128 x N x 16 product per 128-sphere block, with every fp32 operand
+// split into tf32 hi + lo parts (K = 16: Kh.bh + Kl.bh + Kh.bl + wh + wl;
+// the dropped Kl.bl and the truncations are < 3 * 2^-20 |K||b|, tf32 products
+// are exact, accumulation is fp32).  The accumulator lives in TMEM; each warp
+// reads its 32 spheres' rows (tcgen05.ld) and keeps the running minimum.  A
+// sphere collides iff min_p D <= r^2 - |a|^2; the decision band is
+// kBandTc (|a|^2 + max|b|^2 + r^2), 16x the FFMA kernel's, so definite
+// verdicts stay provably the reference's and the rest go to the exact queue.
+// CTA: 128 threads; thread i owns row i of every 128-sphere block.
+// ---------------------------------------------------------------------------
+constexpr int kTcNc = CAPT_TC_NC;        // points per chunk
+constexpr int kTcMb = kTsTc / 128;        // 128-sphere blocks per tile
+constexpr float kBandTc = 0x1p-14f;
+constexpr int kTcCols = kTcMb * kTcNc;    // TMEM columns: every block of a chunk at once
+
+struct __align__(1024) SmemTc {
+  unsigned char A[kTsTc * 64];   // sphere rows, K-major canonical layout
+  unsigned char B[kTcNc * 64];   // point rows
+  uint64_t mbar;
+  uint32_t tmem;
+  int tile;
+};
+
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+
+// one operand row: 16 tf32 values at row r of a K-major tile
+__device__ __forceinline__ void put_row(unsigned char* base, int r, const float (&v)[16]) {
+#pragma unroll
+  for (int k = 0; k < 16; k += 4)
+    *reinterpret_cast<float4*>(base + tc::kmaj_off(r, k)) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+}
+
+__global__ void __launch_bounds__(128) k_binned_scan_tc(BinArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  SmemTc& S = *reinterpret_cast<SmemTc*>(smem_raw);
+  const DevTree& t = a.t;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int n_tiles = int(*a.n_tiles);
+  if (tid == 0) {
+    tc::mbar_init(&S.mbar, 1);
+    S.tile = int(atomicAdd(a.tile_ctr, 1u));
+  }
+  if (warp == 0) tc::tmem_alloc<kTcCols>(&S.tmem);
+  tc::fence_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = S.tmem;
+  const uint32_t taddr = tmem + (uint32_t(32 * warp) << 16);
+  uint32_t phase = 0;
+  const float INF = __int_as_float(0x7f800000);
+  while (true) {
+    const int tile = S.tile;
+    if (tile >= n_tiles) break;
+    int next = 0;
+    if (tid == 32) next = int(atomicAdd(a.tile_ctr, 1u));
+    const TileMeta tm = a.tiles[tile];
+    const int cnt = tm.cnt;
+    const float4 org = tm.org;
+    const uint32_t m = tm.m, m4 = (m + 3u) & ~3u;
+    const float* xs = reinterpret_cast<const float*>(t.data + tm.setx);
+    const int nb = (cnt + 127) >> 7;  // sphere blocks in this tile
+    // this thread's spheres: rows tid of blocks 0..nb-1
+    float lim_lo[kTcMb], lim_hi[kTcMb], mn[kTcMb];
+#pragma unroll
+    for (int b = 0; b < kTcMb; ++b) {
+      const int e = b * 128 + tid;
+      mn[b] = INF;
+      lim_lo[b] = -INF;  // padding rows: never a hit, never ambiguous
+      lim_hi[b] = -INF;
+      if (b >= nb) continue;
+      float row[16];
+      if (e < cnt) {
+        const float4 rc = a.lrec[a.perm[tm.s0 + e]];
+        const float ax = rc.x - org.x, ay = rc.y - org.y, az = rc.z - org.z;
+        const float aa = fmaf(az, az, fmaf(ay, ay, ax * ax));
+        const float r2 = rc.w * rc.w;
+        const float thr = r2 - aa, band = kBandTc * (aa + org.w + r2);
+        lim_lo[b] = thr - band;
+        lim_hi[b] = thr + band;
+        const float K[3] = {-2.f * ax, -2.f * ay, -2.f * az};
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const float h = tf32_hi(K[d]);
+          row[d] = h;
+          row[3 + d] = tf32_hi(K[d] - h);
+          row[6 + d] = h;
+        }
+        row[9] = 1.f;
+        row[10] = 1.f;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 11; ++k) row[k] = 0.f;
+      }
+#pragma unroll
+      for (int k = 11; k < 16; ++k) row[k] = 0.f;
+      put_row(S.A, e, row);
+    }
+    bool done = false;
+    for (uint32_t c0 = 0; c0 < m && !done; c0 += kTcNc) {
+      const uint32_t len = min(uint32_t(kTcNc), m - c0);
+      const uint32_t nc = (len + 31u) & ~31u;  // MMA N (multiple of 16) = whole TMEM loads
+      // stage the chunk's point rows (w = +inf for padding / non-finite rows)
+      for (uint32_t i = tid; i < nc; i += 128) {
+        float px = INF, py = INF, pz = INF;
+        if (i < len) {
+          px = __ldg(xs + c0 + i);
+          py = __ldg(xs + m4 + c0 + i);
+          pz = __ldg(xs + 2 * m4 + c0 + i);
+        }
+        float row[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) row[k] = 0.f;
+        if (isfinite(px) && isfinite(py) && isfinite(pz)) {
+          const float bv[3] = {px - org.x, py - org.y, pz - org.z};
+          const float w = fmaf(bv[2], bv[2], fmaf(bv[1], bv[1], bv[0] * bv[0]));
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            const float h = tf32_hi(bv[d]);
+            row[d] = h;
+            row[3 + d] = h;
+            row[6 + d] = tf32_hi(bv[d] - h);
+          }
+          const float wh = tf32_hi(w);
+          row[9] = wh;
+          row[10] = tf32_hi(w - wh);
+        } else {
+          row[9] = INF;
+        }
+        put_row(S.B, int(i), row);
+      }
+      tc::fence_async_smem();
+      __syncthreads();
+      // every block's product for this chunk in one batch, one commit
+      if (tid == 0) {
+        tc::fence_after_sync();
+        const uint32_t idesc = tc::idesc_tf32(128, int(nc));
+        const uint32_t sb = tc::smem_u32(S.B);
+        for (int b = 0; b < nb; ++b) {
+          const uint32_t sa = tc::smem_u32(S.A) + uint32_t(b) * 16u * tc::kRowBlockBytes;
+          const uint32_t d = tmem + uint32_t(b * kTcNc);
+          tc::mma_tf32(d, tc::make_desc(sa), tc::make_desc(sb), idesc, 0u);
+          tc::mma_tf32(d, tc::make_desc(sa + 2 * tc::kCoreBytes), tc::make_desc(sb + 2 * tc::kCoreBytes),
+                       idesc, 1u);
+        }
+        tc::commit(&S.mbar);
+      }
+      tc::mbar_wait(&S.mbar, phase);
+      phase ^= 1u;
+      tc::fence_after_sync();
+#pragma unroll
+      for (int b = 0; b < kTcMb; ++b) {
+        if (b >= nb) break;
+        float bm = INF;
+        for (uint32_t c = 0; c < nc; c += 32) {
+          uint32_t v[32];
+          tc::tmem_ld32(taddr + uint32_t(b * kTcNc) + c, v);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; j += 2)
+            bm = fmin3(bm, __uint_as_float(v[j]), __uint_as_float(v[j + 1]));
+        }
+        mn[b] = fminf(mn[b], bm);
+      }
+      tc::fence_before_sync();
+      bool mine = true;
+#pragma unroll
+      for (int b = 0; b < kTcMb; ++b)
+        if (b < nb && b * 128 + tid < cnt) mine &= mn[b] <= lim_lo[b];
+      done = __syncthreads_and(mine);
+    }
+    // decisions (thread-owned spheres)
+#pragma unroll
+    for (int b = 0; b < kTcMb; ++b) {
+      const int e = b * 128 + tid;
+      if (b >= nb || e >= cnt) continue;
+      if (mn[b] <= lim_lo[b]) {
+        a.lhit[a.perm[tm.s0 + e]] = 1;
+      } else if (!(mn[b] > lim_hi[b])) {
+        const int q = a.lmeta[a.perm[tm.s0 + e]].x;
+        const unsigned j = atomicAdd(a.slow_n, 1u);
+        a.slow[j] = make_int2(q, tm.leaf);
+        atomicAdd(a.n_refined, 1u);
+      }
+    }
+    if (tid == 32) S.tile = next;
+    __syncthreads();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (warp == 0) tc::tmem_free<kTcCols>(tmem);
+}
+
 // Exact float64 path, one warp per queued sphere: lanes split the set,
 // query.py:96-99 arithmetic (fp64, no FMA), ballot OR.
 template <typename InT>
@@ -1135,7 +1350,13 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.bcursor = ctr ? ctr + 8 + 2 * nl : nullptr;
   a.start = A.get<uint32_t>(nl);
   a.tstart = A.get<uint32_t>(nl);
-  a.tiles = A.get<TileMeta>(nl + n / kTS + 1);
+  // K5 on the tensor cores unless CAPT_K5_TC=0 (the FFMA kernel)
+  static const bool use_tc = [] {
+    const char* e = getenv("CAPT_K5_TC");
+    return !(e && e[0] == '0');
+  }();
+  a.ts = use_tc ? uint32_t(kTsTc) : uint32_t(kTS);
+  a.tiles = A.get<TileMeta>(nl + n / a.ts + 1);
   a.perm = A.get<uint32_t>(n);
   a.verdict = A.get<uint8_t>(n + 8);
   a.slow = A.get<int2>(n);
@@ -1191,7 +1412,20 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
     if (occ < 1) occ = 1;
   }
   tm.mark(5, s);
-  k_binned_scan<<<sms * occ, kBT, sizeof(SmemBinned), s>>>(a);
+  if (use_tc) {
+    static int occ_tc = 0;
+    if (!occ_tc) {
+      CAPT_CUDA(cudaFuncSetAttribute(k_binned_scan_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(SmemTc))));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tc, k_binned_scan_tc, 128, sizeof(SmemTc));
+      if (getenv("CAPT_DEBUG")) fprintf(stderr, "[capt tc] occupancy %d smem %d\n", occ_tc, int(sizeof(SmemTc)));
+      occ_tc = 512 / kTcCols;  // TMEM columns per SM
+      if (occ_tc > 8) occ_tc = 8;
+    }
+    k_binned_scan_tc<<<sms * occ_tc, 128, sizeof(SmemTc), s>>>(a);
+  } else {
+    k_binned_scan<<<sms * occ, kBT, sizeof(SmemBinned), s>>>(a);
+  }
   tm.mark(6, s);
   if (f64) k_slow<double><<<sms * 8, 128, 0, s>>>(a);
   else k_slow<float><<<sms * 8, 128, 0, s>>>(a);

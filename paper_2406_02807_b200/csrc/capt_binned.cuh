@@ -46,6 +46,7 @@ struct BinArgs {
   uint32_t* bcursor;  // per leaf bucket: K3a cursor
   int bshift;         // leaf bucket = leaf >> bshift (<= kBuckets buckets)
   float rlo_f, rhi_f; // fp32 images of the double band edges
+  uint32_t ts;        // spheres per K5 tile (kernel dependent)
 };
 
 bool binned_preferred(const DevTree& t, int64_t n, uint32_t flags);
