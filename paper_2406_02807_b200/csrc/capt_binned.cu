@@ -1025,6 +1025,16 @@ __global__ void __launch_bounds__(128) k_binned_scan_tc(BinArgs a) {
     const uint32_t m = tm.m, m4 = (m + 3u) & ~3u;
     const float* xs = reinterpret_cast<const float*>(t.data + tm.setx);
     const int nb = (cnt + 127) >> 7;  // sphere blocks in this tile
+    // thread i < kTcNc stages row i of every chunk; the next chunk's point is
+    // loaded while the current chunk's product runs (one chunk ahead), the
+    // first one beside the sphere gathers
+    static_assert(kTcNc <= 128, "one staged row per thread");
+    float qx = INF, qy = INF, qz = INF;
+    if (tid < kTcNc && uint32_t(tid) < m) {
+      qx = __ldg(xs + tid);
+      qy = __ldg(xs + m4 + tid);
+      qz = __ldg(xs + 2 * m4 + tid);
+    }
     // this thread's spheres: rows tid of blocks 0..nb-1
     float lim_lo[kTcMb], lim_hi[kTcMb], mn[kTcMb];
 #pragma unroll
@@ -1066,13 +1076,9 @@ __global__ void __launch_bounds__(128) k_binned_scan_tc(BinArgs a) {
       const uint32_t len = min(uint32_t(kTcNc), m - c0);
       const uint32_t nc = (len + 31u) & ~31u;  // MMA N (multiple of 16) = whole TMEM loads
       // stage the chunk's point rows (w = +inf for padding / non-finite rows)
-      for (uint32_t i = tid; i < nc; i += 128) {
-        float px = INF, py = INF, pz = INF;
-        if (i < len) {
-          px = __ldg(xs + c0 + i);
-          py = __ldg(xs + m4 + c0 + i);
-          pz = __ldg(xs + 2 * m4 + c0 + i);
-        }
+      if (uint32_t(tid) < nc) {
+        const uint32_t i = tid;
+        const float px = qx, py = qy, pz = qz;
         float row[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) row[k] = 0.f;
@@ -1096,6 +1102,15 @@ __global__ void __launch_bounds__(128) k_binned_scan_tc(BinArgs a) {
       }
       tc::fence_async_smem();
       __syncthreads();
+      {
+        const uint32_t j = c0 + kTcNc + tid;  // next chunk's row for this thread
+        qx = qy = qz = INF;
+        if (tid < kTcNc && j < m) {
+          qx = __ldg(xs + j);
+          qy = __ldg(xs + m4 + j);
+          qz = __ldg(xs + 2 * m4 + j);
+        }
+      }
       // every block's product for this chunk in one batch, one commit
       if (tid == 0) {
         tc::fence_after_sync();
