@@ -316,27 +316,52 @@ def main():
     roof["streamed_bytes_per_step"] = bytes_step
     roof["roofline_ms"] = max(t_hbm, t_fp32) * 1e3
 
-    # e2e: public API with pinned host buffers, H2D + kernel + D2H in the region
+    # e2e: the C-ABI call a plugin makes (capt_query with CAPT_HOST_IO) on
+    # pinned host buffers -- H2D of the spheres, the kernels and the D2H of
+    # the verdict words all inside the region; the Python API (which also
+    # unpacks the words to a bool array on the host) is reported beside it
     e2e = None
     if args.e2e_steps > 0:
+        import ctypes as C
+        from paper_2406_02807_b200 import _lib
+        from paper_2406_02807_b200.query import _host_query
         c_pin = torch.from_numpy(c_np).pin_memory().numpy()
         r_pin = torch.from_numpy(r_np).pin_memory().numpy()
-        from paper_2406_02807_b200.query import _host_query
-        _host_query(tree, c_pin, r_pin, 0, L, None, True, True, mode=mode)  # warm-up
+        n_words = (n // L + 31) // 32
+        w_pin = torch.zeros(n_words, dtype=torch.int32).pin_memory().numpy().view(np.uint32)
+        bad = C.c_int64(-1)
+        flags = _lib.HOST_IO | _lib.PREFILTER | _lib.CHECK_RADII | mode
+        lib = _lib.lib()
+
+        def abi_call():
+            _lib.check(lib.capt_query(tree.handle, c_pin.ctypes.data, r_pin.ctypes.data, n, L,
+                                      None, flags, w_pin.ctypes.data, None, C.byref(bad), None),
+                       "capt_query")
+
+        abi_call()  # warm-up
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            bits, _, fb = _host_query(tree, c_pin, r_pin, 0, L, None, True, True, mode=mode)
+            abi_call()
         dt = time.perf_counter() - t0
-        t_e = torch.tensor([dt], dtype=torch.float64, device=dev)
+        hits_e2e = int(np.unpackbits(w_pin.view(np.uint8)).sum())
+        _host_query(tree, c_pin, r_pin, 0, L, None, True, True, mode=mode)  # warm-up
+        t1 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            bits, _, fb = _host_query(tree, c_pin, r_pin, 0, L, None, True, True, mode=mode)
+        dt_py = time.perf_counter() - t1
+        t_e = torch.tensor([dt, dt_py], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
-        dt = float(t_e.item())
-        assert int(bits.sum()) == hits_ref
+        dt, dt_py = float(t_e[0].item()), float(t_e[1].item())
+        assert hits_e2e == hits_ref and int(bits.sum()) == hits_ref
         e2e = {"value": world * n * args.e2e_steps / dt, "unit": UNIT,
                "h2d_bytes_per_step": int(c_pin.nbytes + r_pin.nbytes),
-               "d2h_bytes_per_step": int(words.numel() * 4)}
+               "d2h_bytes_per_step": int(n_words * 4),
+               "api": "capt_query(CAPT_HOST_IO) C-ABI, pinned host buffers, verdict words out",
+               "python_api_value": world * n * args.e2e_steps / dt_py,
+               "python_api": "query._host_query: the same call + unpack to a bool array"}
 
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
