@@ -342,9 +342,19 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
       const int q = base + v * blockDim.x + threadIdx.x;
       valid[v] = q < n;
       if (a.mask && valid[v]) valid[v] = a.mask[q] != 0;
-      if (check && valid[v] && (r[v] < a.rlo_f || r[v] > a.rhi_f))
-        atomicMin(a.first_bad, static_cast<unsigned long long>(q));
       off[v] = 0;
+    }
+    if (check) {  // out-of-band radii are rare: one warp vote, then the atomics
+      bool bad = false;
+#pragma unroll
+      for (int v = 0; v < V; ++v) bad |= valid[v] && (r[v] < a.rlo_f || r[v] > a.rhi_f);
+      if (__any_sync(0xffffffffu, bad)) {
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+          if (valid[v] && (r[v] < a.rlo_f || r[v] > a.rhi_f))
+            atomicMin(a.first_bad,
+                      static_cast<unsigned long long>(base + v * blockDim.x + threadIdx.x));
+      }
     }
     // shared-memory levels on absolute shared-window addresses:
     // addr(child) = 2 addr + (4 or 8) - sbase, one LDS + compare + select + IMAD
@@ -367,14 +377,24 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
 #pragma unroll
       for (int v = 0; v < V; ++v) off[v] = ad[v] - sbase;
     }
+    // the remaining (< 3) shared levels, then the global ones; the axis is
+    // uniform per level, selected without branches
+#pragma unroll 1
+    for (; s < dsm; ++s) {
+      const int ax = s % 3;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const float c = ax == 0 ? cx[v] : (ax == 1 ? cy[v] : cz[v]);
+        off[v] = 2 * off[v] + (c > lds_f32(sbase + off[v]) ? 8u : 4u);
+      }
+    }
+#pragma unroll 1
     for (; s < t.depth; ++s) {
       const int ax = s % 3;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const float c = ax == 0 ? cx[v] : (ax == 1 ? cy[v] : cz[v]);
-        const float tv = s < dsm ? *reinterpret_cast<const float*>(sb + off[v])
-                                 : __ldg(t.T + (off[v] >> 2));
-        off[v] = 2 * off[v] + (c > tv ? 8u : 4u);
+        off[v] = 2 * off[v] + (c > __ldg(t.T + (off[v] >> 2)) ? 8u : 4u);
       }
     }
     // per-sphere classification, branch-free.  The AABB test (on the probe
