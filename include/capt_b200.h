@@ -45,6 +45,8 @@ extern "C" {
 #define CAPT_MODE_BINNED 0x200u /* force the leaf-binned kernels               */
 #define CAPT_MODE_THREAD 0x400u /* force the one-thread-per-sphere kernel
                                    (always used with CAPT_STATS)               */
+#define CAPT_K5_FFMA 0x800u     /* binned scan on the CUDA cores (FFMA2) instead
+                                   of the tensor cores (tcgen05 tf32)          */
 
 typedef struct capt_tree capt_tree;
 

@@ -25,6 +25,7 @@ HOST_IO = 0x10
 MODE_DIRECT = 0x100
 MODE_BINNED = 0x200
 MODE_THREAD = 0x400
+K5_FFMA = 0x800
 
 
 class CaptTreeInfo(C.Structure):

@@ -1385,11 +1385,13 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.bcursor = ctr ? ctr + 8 + 2 * nl : nullptr;
   a.start = A.get<uint32_t>(nl);
   a.tstart = A.get<uint32_t>(nl);
-  // K5 on the tensor cores unless CAPT_K5_TC=0 (the FFMA kernel)
-  static const bool use_tc = [] {
+  // K5 on the tensor cores unless CAPT_K5_FFMA (or CAPT_K5_TC=0 in the
+  // environment) selects the CUDA-core kernel
+  static const bool env_ffma = [] {
     const char* e = getenv("CAPT_K5_TC");
-    return !(e && e[0] == '0');
+    return e && e[0] == '0';
   }();
+  const bool use_tc = !(env_ffma || (flags & CAPT_K5_FFMA));
   a.ts = use_tc ? uint32_t(kTsTc) : uint32_t(kTS);
   a.tiles = A.get<TileMeta>(nl + n / a.ts + 1);
   a.perm = A.get<uint32_t>(n);

@@ -17,6 +17,9 @@ from paper_2406_02807_b200 import workloads as W  # noqa: E402
 from paper_2406_02807_b200.query import _host_inputs, _host_query  # noqa: E402
 
 BINNED, DIRECT = _lib.MODE_BINNED, _lib.MODE_DIRECT
+# the binned scan runs on the tensor cores by default; K5_FFMA selects the
+# CUDA-core kernel -- both must give the reference's verdicts
+K5 = {"tc": BINNED, "ffma": BINNED | _lib.K5_FFMA}
 
 
 def upload(t):
@@ -30,7 +33,8 @@ def q(tree, c, r, L=1, mask=None, prefilter=True, mode=BINNED):
     return bits
 
 
-def test_binned_golden_masks():
+@pytest.mark.parametrize("k5", ["tc", "ffma"])
+def test_binned_golden_masks(k5):
     z = load_golden("queries.npz")
     for name in z["names"]:
         pts = z[f"{name}/points"]
@@ -39,12 +43,12 @@ def test_binned_golden_masks():
         c, r = z[f"{name}/centers"], z[f"{name}/radii"]
         n = len(r)
         exp = np.unpackbits(z[f"{name}/mask"])[:n].astype(bool)
-        assert np.array_equal(q(tree, c, r), exp), name
+        assert np.array_equal(q(tree, c, r, mode=K5[k5]), exp), name
         nopre = np.unpackbits(z[f"{name}/mask_nopre"])[:n].astype(bool)
-        assert np.array_equal(q(tree, c, r, prefilter=False), nopre), name
+        assert np.array_equal(q(tree, c, r, prefilter=False, mode=K5[k5]), nopre), name
         lane = np.unpackbits(z[f"{name}/lane_mask"])[:n].astype(bool)
         gb = np.unpackbits(z[f"{name}/group8"])[: n // 8].astype(bool)
-        assert np.array_equal(q(tree, c, r, 8, lane.astype(np.uint8)), gb), name
+        assert np.array_equal(q(tree, c, r, 8, lane.astype(np.uint8), mode=K5[k5]), gb), name
 
 
 def test_binned_cfg0_golden():
@@ -73,7 +77,8 @@ def test_binned_cfg1_groups(L):
         assert np.array_equal(O.collides_groups(t, c, r, 8), exp)
 
 
-def test_binned_dense_gaussians_multichunk():
+@pytest.mark.parametrize("k5", ["tc", "ffma"])
+def test_binned_dense_gaussians_multichunk(k5):
     # dense mixture: affordance sets larger than one 1024-point shared-memory chunk
     cloud = W.cfg3_cloud(n=32768, n_comp=8, seed=5)
     t = O.construct(cloud, 0.01, 0.1)
@@ -81,7 +86,7 @@ def test_binned_dense_gaussians_multichunk():
     tree = upload(t)
     c, r = W.cfg3_queries(1 << 19, seed=7)
     exp = O.collides_many(t, c, r)
-    assert np.array_equal(q(tree, c, r), exp)
+    assert np.array_equal(q(tree, c, r, mode=K5[k5]), exp)
 
 
 def test_binned_f64_and_nonfinite():
@@ -100,7 +105,8 @@ def test_binned_f64_and_nonfinite():
     assert np.array_equal(q(tree, c, r), exp)
 
 
-def test_binned_tangency_heavy():
+@pytest.mark.parametrize("k5", ["tc", "ffma"])
+def test_binned_tangency_heavy(k5):
     # spheres exactly tangent (in float64) to cloud points: exercises the
     # ambiguous-band rescan inside the binned kernel
     rng = np.random.default_rng(23)
@@ -114,7 +120,7 @@ def test_binned_tangency_heavy():
     r = W.clamp_radii(rng.uniform(0.01, 0.08, n).astype(np.float32), 0.01, 0.08)
     c = (pts[idx].astype(np.float64) + d * r[:, None].astype(np.float64)).astype(np.float32)
     exp = O.collides_many(t, c, r)
-    got = q(tree, c, r)
+    got = q(tree, c, r, mode=K5[k5])
     assert np.array_equal(got, exp)
     assert np.array_equal(got, O.brute_collides_many(pts, c, r))
 
@@ -169,7 +175,8 @@ def test_host_pipeline_chunks_counters_and_bad_radius():
         P.collides_many(tree, c, r_bad)
 
 
-def test_binned_aabb_boundary_spheres():
+@pytest.mark.parametrize("k5", ["tc", "ffma"])
+def test_binned_aabb_boundary_spheres(k5):
     """Spheres whose centre lies exactly r (and one ulp either side) outside a
     leaf's affordance box: the binned path's conservative fp32 AABB filter
     must give the reference verdict (the reference's own float64 AABB test is
@@ -196,7 +203,8 @@ def test_binned_aabb_boundary_spheres():
     c = np.concatenate(cs)
     r = np.concatenate([r] * 3)
     exp = O.collides_many(t, c, r)
-    assert np.array_equal(q(tree, c, r), exp)
+    assert np.array_equal(q(tree, c, r, mode=K5[k5]), exp)
     assert np.array_equal(q(tree, c, r, mode=DIRECT), exp)
     n8 = len(r) // 8 * 8
-    assert np.array_equal(q(tree, c[:n8], r[:n8], 8), exp[:n8].reshape(-1, 8).any(1))
+    assert np.array_equal(q(tree, c[:n8], r[:n8], 8, mode=K5[k5]),
+                          exp[:n8].reshape(-1, 8).any(1))
