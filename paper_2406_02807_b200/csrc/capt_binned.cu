@@ -630,6 +630,18 @@ __global__ void __launch_bounds__(256) k_part_leaf(BinArgs a) {
 // persistent K5 CTAs draw the costliest tiles first and the tail of the
 // launch is made of small ones.  One launch instead of two device-wide scans
 // (this stage is pure latency at every batch size).
+// large trees (more leaves than a few single-CTA passes cover): device-wide
+// scans instead
+__global__ void k_tile_counts(BinArgs a, uint32_t* __restrict__ tc) {
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < a.t.n;
+       j += int64_t(gridDim.x) * blockDim.x)
+    tc[j] = (a.counts[a.t.order[j]] + a.ts - 1) / a.ts;
+}
+__global__ void k_tile_total(BinArgs a, const uint32_t* __restrict__ tc) {
+  *a.n_tiles = a.tstart[a.t.n - 1] + tc[a.t.n - 1];
+}
+constexpr int64_t kScanSingleMax = 32768;  // leaves handled by the one-CTA K2
+
 constexpr int kScanT = 512;
 constexpr int kScanI = 16;  // leaves per thread per pass
 __global__ void __launch_bounds__(kScanT) k_scan_tiles(BinArgs a) {
@@ -1432,7 +1444,20 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   else k_bin_count<float><<<G, 256, 0, s>>>(a);
   tm.mark(2, s);
   // per-leaf starts and tiles
-  k_scan_tiles<<<1, kScanT, 0, s>>>(a);
+  if (nl <= kScanSingleMax) {
+    k_scan_tiles<<<1, kScanT, 0, s>>>(a);
+  } else {
+    uint32_t* tc = A.get<uint32_t>(nl);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, a.counts, a.start, nl, s);
+    void* tmp = A.get<char>(tb);
+    if (!tc || !tmp) return fail(CAPT_ENOMEM, "binned scratch allocation");
+    CAPT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, a.counts, a.start, nl, s));
+    k_tile_counts<<<grid_for(nl, 256, 8), 256, 0, s>>>(a, tc);
+    CAPT_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, tc, a.tstart, nl, s));
+    k_tile_total<<<1, 1, 0, s>>>(a, tc);
+    note_launches(6);
+  }
   tm.mark(3, s);
   {
     const int Gp = grid_for((n + kPartItems - 1) / kPartItems * 256, 256, 4);

@@ -208,3 +208,18 @@ def test_binned_aabb_boundary_spheres(k5):
     n8 = len(r) // 8 * 8
     assert np.array_equal(q(tree, c[:n8], r[:n8], 8, mode=K5[k5]),
                           exp[:n8].reshape(-1, 8).any(1))
+
+
+def test_binned_many_leaves_device_scans():
+    # > 32768 leaves: per-leaf starts and tile indices come from device-wide
+    # scans instead of the one-CTA pass
+    rng = np.random.default_rng(41)
+    pts = rng.uniform(0, 1, (40000, 3)).astype(np.float32)
+    t = O.construct(pts, 0.005, 0.03)
+    assert t["n"] > 32768
+    tree = upload(t)
+    c = rng.uniform(0, 1, (1 << 20, 3)).astype(np.float32)
+    r = rng.uniform(0.005, 0.03, 1 << 20).astype(np.float32)
+    exp = O.collides_many(t, c, r)
+    for k5 in ("tc", "ffma"):
+        assert np.array_equal(q(tree, c, r, mode=K5[k5]), exp), k5
