@@ -60,6 +60,7 @@ static_assert(sizeof(SlabHeader) <= 256, "header must fit its 256-B section");
 struct DevTree {
   int k, depth;
   int64_t n;
+  int64_t total;  // sum of set sizes
   double r_min, r_max;
   const float* T;
   const float4* box;
@@ -105,6 +106,7 @@ inline DevTree view(const capt_tree* t) {
   d.k = t->h.k;
   d.depth = t->h.depth;
   d.n = t->h.n;
+  d.total = t->h.total;
   d.r_min = t->h.r_min;
   d.r_max = t->h.r_max;
   d.T = reinterpret_cast<const float*>(t->slab + t->h.off_T);
