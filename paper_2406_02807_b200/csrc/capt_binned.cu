@@ -1241,6 +1241,43 @@ __global__ void k_slow(BinArgs a) {
     const uint2 st = t.set[e.y];
     const float* base = reinterpret_cast<const float*>(t.data + st.x);
     const uint32_t m4 = (st.y + 3u) & ~3u;
+    // fp32 first pass in the direct form (relative error < 5u, band TAU as in
+    // the direct kernels): most spheres the binned scan left ambiguous (its
+    // band is wider) are decided here; the rest take the float64 pass
+    {
+      const float cf[3] = {float(c64[0]), float(c64[1]), float(c64[2])};
+      const float rf = float(r64), r2 = rf * rf;
+      const bool fast = double(cf[0]) == c64[0] && double(cf[1]) == c64[1] &&
+                        double(cf[2]) == c64[2] && double(rf) == r64 && isfinite(cf[0]) &&
+                        isfinite(cf[1]) && isfinite(cf[2]) && r2 >= kR2Min && r2 <= kR2Max;
+      if (fast && t.k == 3) {
+        const float loB = r2 * (1.0f - kTau), hiB = r2 * (1.0f + kTau);
+        bool h32 = false, amb = false;
+        for (uint32_t j0 = 0; j0 < st.y && !__any_sync(0xffffffffu, h32); j0 += 128) {
+          float px[4], py[4], pz[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t j = j0 + u * 32 + lane;
+            const bool in = j < m4;
+            px[u] = in ? __ldg(base + j) : __int_as_float(0x7f800000);
+            py[u] = in ? __ldg(base + m4 + j) : 0.f;
+            pz[u] = in ? __ldg(base + 2 * m4 + j) : 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float dx = cf[0] - px[u], dy = cf[1] - py[u], dz = cf[2] - pz[u];
+            const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+            h32 |= d2 <= loB;
+            amb |= d2 < hiB;
+          }
+        }
+        if (__any_sync(0xffffffffu, h32)) {
+          if (lane == 0) a.verdict[e.x] = 1;
+          continue;
+        }
+        if (!__any_sync(0xffffffffu, amb)) continue;  // definite miss
+      }
+    }
     const double R = __dmul_rn(r64, r64);
     bool hit = false;
     // 4 rows per lane per step: the loads of 128 points are in flight at once
