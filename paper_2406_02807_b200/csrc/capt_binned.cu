@@ -47,6 +47,9 @@ namespace {
 constexpr int kBT = 128;           // threads per binned CTA
 constexpr int kS = 8;              // spheres per thread (4 packed pairs)
 constexpr int kTS = kBT * kS;      // spheres per tile
+// Compile-time tunables (build_ext --out ... -D NAME=VALUE builds a variant).
+// Measured on config 1 (K5 us): TS 128/NC 64 265; 128/128 404 (4 CTAs/SM);
+// 256/128 577; 512/64 ~1100; 128/32 371.
 #ifndef CAPT_TC_TS
 #define CAPT_TC_TS 128
 #endif
@@ -284,6 +287,7 @@ __device__ __forceinline__ float lds_f32(unsigned addr) {
 // with byte offsets (child = 2*off + 4 + 4*(x > T): 4 instructions per level),
 // one plain atomic per binned sphere for its ticket.
 constexpr int kSmemNodes3 = 8191;
+// K1 min CTAs per SM (caps registers at 64): 4 beats 1 (70 regs) by ~10%
 #ifndef CAPT_K1_MINB
 #define CAPT_K1_MINB 4
 #endif
@@ -911,6 +915,7 @@ __device__ __forceinline__ void decide(const Spheres8& sp, const SmemBinned& S, 
   }
 }
 
+// FFMA K5 min CTAs per SM: 6 (85 regs) beats 7 (spills) and 5
 #ifndef CAPT_K5_MINB
 #define CAPT_K5_MINB 6
 #endif
