@@ -11,6 +11,8 @@ from .geom import Aabb, Sphere
 from .morton import FilterConfig, axis_bits, filter_cloud, reach_filter
 from .query import (DEFAULT_LANE_WIDTH, QueryOutcome, SphereBatch, collides, collides_any,
                     collides_batch, collides_many, collides_unchecked, query_bits)
+from .trace import (ParseError, QueryTraceRecord, VerificationError, capt_verdicts, query_phase,
+                    read_trace, verify_trace, write_trace)
 from .tree import (BuildParams, BuildStats, Capt, construct, leaf_index, leaf_index_counted,
                    leaf_indices, load_capt, save_capt)
 
@@ -23,4 +25,6 @@ __all__ = [
     "leaf_indices", "save_capt", "load_capt",
     "SphereBatch", "QueryOutcome", "collides", "collides_unchecked", "collides_batch",
     "collides_any", "collides_many", "query_bits", "DEFAULT_LANE_WIDTH",
+    "QueryTraceRecord", "ParseError", "VerificationError", "read_trace", "write_trace",
+    "capt_verdicts", "verify_trace", "query_phase",
 ]

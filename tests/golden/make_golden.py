@@ -225,6 +225,36 @@ def make_cfg0_slice():
     print("cfg0.npz")
 
 
+
+def make_trace():
+    """A mixed trace from the reference's own generator (synth.gen_queries),
+    written by its writer, and the reference's replay verdicts
+    (bench.capt_verdicts) on the tree over the same cloud."""
+    from captree.bench import capt_verdicts
+    from captree.io import read_trace, write_trace
+    from captree.synth import gen_queries
+    rng = np.random.default_rng(77)
+    pts = rng.uniform(-1, 1, (3000, 3)).astype(np.float32)
+    cloud = PointCloud(pts)
+    params = BuildParams(0.02, 0.08)
+    tree = construct(cloud, params)
+    out = {"points": pts, "band": np.array([0.02, 0.08])}
+    for name, batch in (("b8", 8), ("b5", 5), ("b40", 40)):
+        recs = gen_queries(cloud, params, 2000, workload="mixed", batch_size=batch, seed=batch)
+        path = os.path.join("/tmp", f"capt_trace_{name}.csv")
+        write_trace(recs, path)
+        with open(path, "rb") as f:
+            out[f"{name}/csv"] = np.frombuffer(f.read(), np.uint8)
+        back = read_trace(path)
+        out[f"{name}/verdicts"] = capt_verdicts(tree, back)
+        out[f"{name}/nopre"] = capt_verdicts(tree, back, use_aabb_prefilter=False)
+        out[f"{name}/batch_ids"] = np.array([r.batch_id for r in back], np.int64)
+        out[f"{name}/sizes"] = np.array([len(r) for r in back], np.int64)
+        out[f"{name}/expected"] = np.array([-1 if r.expected is None else int(r.expected)
+                                            for r in back], np.int64)
+        os.remove(path)
+    np.savez_compressed(os.path.join(HERE, "trace.npz"), **out)
+
 if __name__ == "__main__":
     print("reference", captree.__version__, "numpy", np.__version__)
     make_hand_cases()
@@ -232,3 +262,4 @@ if __name__ == "__main__":
     make_queries()
     make_filters()
     make_cfg0_slice()
+    make_trace()
