@@ -137,6 +137,13 @@ int capt_filter_cloud(int device, int k, const float* points, int64_t n,
                       double max_reach, uint32_t flags, float* out_points,
                       int64_t* n_out, void* stream);
 
+/* dispersion_stats (oracle.py:141-158): out (n,) float64 distance from every
+ * point to its nearest OTHER point (duplicates: 0), the value a float64
+ * k-d tree query with k=2 returns.  points (n, k) fp32; host buffers with
+ * CAPT_HOST_IO, else device memory.  n >= 2. */
+int capt_nn_distances(int device, int k, const float* points, int64_t n,
+                      uint32_t flags, double* out, void* stream);
+
 /* Number of kernels this library has launched in the process so far
  * (all devices/threads); used by bench.py to report gpu_launches. */
 int64_t capt_kernel_launches(void);

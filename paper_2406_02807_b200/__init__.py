@@ -7,6 +7,7 @@ kernels behind the C-ABI in include/capt_b200.h.
 """
 
 from .cloud import PointCloud
+from .dispersion import DispersionStats, dispersion_stats, nn_distances, safe_filter_radius
 from .geom import Aabb, Sphere
 from .morton import FilterConfig, axis_bits, filter_cloud, reach_filter
 from .query import (DEFAULT_LANE_WIDTH, QueryOutcome, SphereBatch, collides, collides_any,
@@ -27,4 +28,5 @@ __all__ = [
     "collides_any", "collides_many", "query_bits", "DEFAULT_LANE_WIDTH",
     "QueryTraceRecord", "ParseError", "VerificationError", "read_trace", "write_trace",
     "capt_verdicts", "verify_trace", "query_phase",
+    "DispersionStats", "dispersion_stats", "nn_distances", "safe_filter_radius",
 ]

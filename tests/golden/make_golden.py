@@ -255,6 +255,31 @@ def make_trace():
         os.remove(path)
     np.savez_compressed(os.path.join(HERE, "trace.npz"), **out)
 
+
+def make_dispersion():
+    """dispersion_stats (oracle.py:141-158) on assorted clouds, plus the
+    per-point values of the float64 cKDTree query it is built on."""
+    from scipy import __version__ as scipy_version
+    from scipy.spatial import cKDTree
+    from captree.oracle import dispersion_stats
+    rng = np.random.default_rng(91)
+    clouds = {
+        "uniform": rng.uniform(-1, 1, (5000, 3)).astype(np.float32),
+        "dups": np.repeat(rng.uniform(0, 1, (700, 3)).astype(np.float32), 3, axis=0),
+        "k2": rng.normal(0, 0.1, (3000, 2)).astype(np.float32),
+        "cfg1": W.cfg1_cloud(),
+        "tiny": np.array([[0, 0, 0], [1, 0, 0]], np.float32),
+    }
+    out = {"scipy": np.frombuffer(scipy_version.encode(), np.uint8)}
+    for name, pts in clouds.items():
+        st = dispersion_stats(PointCloud(pts))
+        p64 = pts.astype(np.float64)
+        nn = cKDTree(p64).query(p64, k=2)[0][:, 1]
+        out[f"{name}/points"] = pts
+        out[f"{name}/stats"] = np.array([st.mean, st.median, st.p95, st.count], np.float64)
+        out[f"{name}/nn"] = nn
+    np.savez_compressed(os.path.join(HERE, "dispersion.npz"), **out)
+
 if __name__ == "__main__":
     print("reference", captree.__version__, "numpy", np.__version__)
     make_hand_cases()
@@ -263,3 +288,4 @@ if __name__ == "__main__":
     make_filters()
     make_cfg0_slice()
     make_trace()
+    make_dispersion()
