@@ -49,7 +49,9 @@ constexpr int kS = 8;              // spheres per thread (4 packed pairs)
 constexpr int kTS = kBT * kS;      // spheres per tile
 // Compile-time tunables (build_ext --out ... -D NAME=VALUE builds a variant).
 // Measured on config 1 (K5 us): TS 128/NC 64 265; 128/128 404 (4 CTAs/SM);
-// 256/128 577; 512/64 ~1100; 128/32 371.
+// 256/128 577; 512/64 ~1100; 128/32 371; 256/64 with 256 threads 286
+// (config 3: 4384 vs 5659); a two-accumulator ping-pong over chunks was
+// slower at both configs (fewer CTAs/SM).
 #ifndef CAPT_TC_TS
 #define CAPT_TC_TS 128
 #endif
@@ -1031,7 +1033,8 @@ __device__ __forceinline__ void put_row(unsigned char* base, int r, const float 
     *reinterpret_cast<float4*>(base + tc::kmaj_off(r, k)) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
 }
 
-__global__ void __launch_bounds__(128) k_binned_scan_tc(BinArgs a) {
+constexpr int kTcThreads = 128 * kTcMb;  // one sphere row per thread
+__global__ void __launch_bounds__(kTcThreads) k_binned_scan_tc(BinArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   SmemTc& S = *reinterpret_cast<SmemTc*>(smem_raw);
   const DevTree& t = a.t;
@@ -1048,7 +1051,10 @@ __global__ void __launch_bounds__(128) k_binned_scan_tc(BinArgs a) {
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = S.tmem;
-  const uint32_t taddr = tmem + (uint32_t(32 * warp) << 16);
+  // thread -> (128-sphere block tb, row): a warp reads the TMEM lanes of its
+  // quadrant (warp % 4) in its block's columns
+  const int tb = tid >> 7, row_id = tid & 127;
+  const uint32_t taddr = tmem + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(tb * kTcNc);
   uint32_t phase = 0;
   const float INF = __int_as_float(0x7f800000);
   while (true) {
@@ -1065,22 +1071,17 @@ __global__ void __launch_bounds__(128) k_binned_scan_tc(BinArgs a) {
     // thread i < kTcNc stages row i of every chunk; the next chunk's point is
     // loaded while the current chunk's product runs (one chunk ahead), the
     // first one beside the sphere gathers
-    static_assert(kTcNc <= 128, "one staged row per thread");
+    static_assert(kTcNc <= kTcThreads, "one staged row per thread");
     float qx = INF, qy = INF, qz = INF;
     if (tid < kTcNc && uint32_t(tid) < m) {
       qx = __ldg(xs + tid);
       qy = __ldg(xs + m4 + tid);
       qz = __ldg(xs + 2 * m4 + tid);
     }
-    // this thread's spheres: rows tid of blocks 0..nb-1
-    float lim_lo[kTcMb], lim_hi[kTcMb], mn[kTcMb];
-#pragma unroll
-    for (int b = 0; b < kTcMb; ++b) {
-      const int e = b * 128 + tid;
-      mn[b] = INF;
-      lim_lo[b] = -INF;  // padding rows: never a hit, never ambiguous
-      lim_hi[b] = -INF;
-      if (b >= nb) continue;
+    // this thread's sphere: row row_id of block tb
+    const int e = tb * 128 + row_id;
+    float mn = INF, lim_lo = -INF, lim_hi = -INF;  // padding rows: never decided
+    if (tb < nb) {
       float row[16];
       if (e < cnt) {
         const float4 rc = a.lrec[a.perm[tm.s0 + e]];
@@ -1088,8 +1089,8 @@ __global__ void __launch_bounds__(128) k_binned_scan_tc(BinArgs a) {
         const float aa = fmaf(az, az, fmaf(ay, ay, ax * ax));
         const float r2 = rc.w * rc.w;
         const float thr = r2 - aa, band = kBandTc * (aa + org.w + r2);
-        lim_lo[b] = thr - band;
-        lim_hi[b] = thr + band;
+        lim_lo = thr - band;
+        lim_hi = thr + band;
         const float K[3] = {-2.f * ax, -2.f * ay, -2.f * az};
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
@@ -1165,35 +1166,26 @@ __global__ void __launch_bounds__(128) k_binned_scan_tc(BinArgs a) {
       tc::mbar_wait(&S.mbar, phase);
       phase ^= 1u;
       tc::fence_after_sync();
-#pragma unroll
-      for (int b = 0; b < kTcMb; ++b) {
-        if (b >= nb) break;
+      if (tb < nb) {  // warp-uniform (tb is per warp)
         float bm = INF;
         for (uint32_t c = 0; c < nc; c += 32) {
           uint32_t v[32];
-          tc::tmem_ld32(taddr + uint32_t(b * kTcNc) + c, v);
+          tc::tmem_ld32(taddr + c, v);
           tc::tmem_wait_ld();
 #pragma unroll
           for (int j = 0; j < 32; j += 2)
             bm = fmin3(bm, __uint_as_float(v[j]), __uint_as_float(v[j + 1]));
         }
-        mn[b] = fminf(mn[b], bm);
+        mn = fminf(mn, bm);
       }
       tc::fence_before_sync();
-      bool mine = true;
-#pragma unroll
-      for (int b = 0; b < kTcMb; ++b)
-        if (b < nb && b * 128 + tid < cnt) mine &= mn[b] <= lim_lo[b];
-      done = __syncthreads_and(mine);
+      done = __syncthreads_and(tb >= nb || e >= cnt || mn <= lim_lo);
     }
-    // decisions (thread-owned spheres)
-#pragma unroll
-    for (int b = 0; b < kTcMb; ++b) {
-      const int e = b * 128 + tid;
-      if (b >= nb || e >= cnt) continue;
-      if (mn[b] <= lim_lo[b]) {
+    // decision (thread-owned sphere)
+    if (tb < nb && e < cnt) {
+      if (mn <= lim_lo) {
         a.lhit[a.perm[tm.s0 + e]] = 1;
-      } else if (!(mn[b] > lim_hi[b])) {
+      } else if (!(mn > lim_hi)) {
         const int q = a.lmeta[a.perm[tm.s0 + e]].x;
         const unsigned j = atomicAdd(a.slow_n, 1u);
         a.slow[j] = make_int2(q, tm.leaf);
@@ -1521,12 +1513,12 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
     if (!occ_tc) {
       CAPT_CUDA(cudaFuncSetAttribute(k_binned_scan_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(sizeof(SmemTc))));
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tc, k_binned_scan_tc, 128, sizeof(SmemTc));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tc, k_binned_scan_tc, kTcThreads, sizeof(SmemTc));
       if (getenv("CAPT_DEBUG")) fprintf(stderr, "[capt tc] occupancy %d smem %d\n", occ_tc, int(sizeof(SmemTc)));
       occ_tc = 512 / kTcCols;  // TMEM columns per SM
       if (occ_tc > 8) occ_tc = 8;
     }
-    k_binned_scan_tc<<<sms * occ_tc, 128, sizeof(SmemTc), s>>>(a);
+    k_binned_scan_tc<<<sms * occ_tc, kTcThreads, sizeof(SmemTc), s>>>(a);
   } else {
     k_binned_scan<<<sms * occ, kBT, sizeof(SmemBinned), s>>>(a);
   }
