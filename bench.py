@@ -414,6 +414,8 @@ def main_sweep(args):
     tree = P.construct(P.PointCloud(cloud), P.BuildParams(0.02, 0.08), device=0)
     pool_n = 1 << 22
     max_exp = args.sweep_max_exp
+    from paper_2406_02807_b200 import _lib
+    mflag = {"auto": 0, "direct": _lib.MODE_DIRECT, "binned": _lib.MODE_BINNED}[args.mode]
     rows = []
     for rate in (0.0, 0.1, 0.5, 0.9, 1.0):
         c, r, label = W.cfg4_queries(cloud, pool_n, rate, seed=104)
@@ -430,7 +432,7 @@ def main_sweep(args):
             stream = torch.cuda.current_stream(dev)
             for _ in range(3):
                 P.query_bits(tree, cN, rN, 1, out=out, check_radii=False,
-                             stream=stream.cuda_stream)
+                             stream=stream.cuda_stream, mode=mflag)
             steps = max(3, min(200, int(2e8 // n)))
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -438,7 +440,7 @@ def main_sweep(args):
             e0.record(stream)
             for _ in range(steps):
                 P.query_bits(tree, cN, rN, 1, out=out, check_radii=False,
-                             stream=stream.cuda_stream)
+                             stream=stream.cuda_stream, mode=mflag)
             e1.record(stream)
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / steps
@@ -449,10 +451,10 @@ def main_sweep(args):
             side.wait_stream(stream)
             with torch.cuda.stream(side):
                 P.query_bits(tree, cN, rN, 1, out=out, check_radii=False,
-                             stream=side.cuda_stream)
+                             stream=side.cuda_stream, mode=mflag)
                 with torch.cuda.graph(g, stream=side):
                     P.query_bits(tree, cN, rN, 1, out=out, check_radii=False,
-                                 stream=side.cuda_stream)
+                                 stream=side.cuda_stream, mode=mflag)
             stream.wait_stream(side)
             for _ in range(3):
                 g.replay()
@@ -463,7 +465,10 @@ def main_sweep(args):
             e1.record(stream)
             torch.cuda.synchronize()
             ms_graph = e0.elapsed_time(e1) / steps
-            mode = "binned" if n >= (1 << 18) and n >= 16 * tree.n else "direct"
+            if args.mode != "auto":
+                mode = args.mode
+            else:
+                mode = "binned" if n >= (1 << 20) and n >= 64 * tree.n else "direct"
             rows.append({"rate": rate, "n": n, "ms": ms, "queries_per_s": n / (ms * 1e-3),
                          "ms_graph": ms_graph, "queries_per_s_graph": n / (ms_graph * 1e-3),
                          "mode": mode, "labels_match": label_ok})

@@ -41,12 +41,15 @@ extern "C" {
 #define CAPT_STATS 0x4u       /* fill counters[0..3] (see capt_query)           */
 #define CAPT_INPUT_F64 0x8u   /* centers/radii are double (else float)          */
 #define CAPT_HOST_IO 0x10u    /* all array arguments are host memory; blocking  */
-#define CAPT_MODE_DIRECT 0x100u /* force the unbinned (warp-per-sphere) kernel */
+#define CAPT_MODE_DIRECT 0x100u /* force the unbinned path (the hybrid kernel
+                                   for fp32 k=3 input, else warp-per-sphere) */
 #define CAPT_MODE_BINNED 0x200u /* force the leaf-binned kernels               */
 #define CAPT_MODE_THREAD 0x400u /* force the one-thread-per-sphere kernel
                                    (always used with CAPT_STATS)               */
 #define CAPT_K5_FFMA 0x800u     /* binned scan on the CUDA cores (FFMA2) instead
                                    of the tensor cores (tcgen05 tf32)          */
+#define CAPT_MODE_WARP 0x1000u  /* unbinned: the warp-per-sphere kernel instead
+                                   of the hybrid (thread classify + warp scan) */
 
 typedef struct capt_tree capt_tree;
 

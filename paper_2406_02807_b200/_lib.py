@@ -26,6 +26,7 @@ MODE_DIRECT = 0x100
 MODE_BINNED = 0x200
 MODE_THREAD = 0x400
 K5_FFMA = 0x800
+MODE_WARP = 0x1000
 
 
 class CaptTreeInfo(C.Structure):

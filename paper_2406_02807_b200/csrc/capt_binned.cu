@@ -267,23 +267,6 @@ __global__ void __launch_bounds__(256) k_bin_count(BinArgs a) {
   }
 }
 
-__device__ __forceinline__ void ld_v8(const float* p, float (&v)[8]) {
-  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
-        "=f"(v[7])
-      : "l"(p));
-}
-__device__ __forceinline__ float2 h2f2(float bits) {
-  const unsigned u = __float_as_uint(bits);
-  return __half22float2(*reinterpret_cast<const __half2*>(&u));
-}
-
-__device__ __forceinline__ float lds_f32(unsigned addr) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
-  return v;
-}
-
 // K1 specialised for k = 3, fp32 input (the hot path): V spheres per thread
 // in flight, 32-bit indexing, the top 13 levels of T in shared memory walked
 // with byte offsets (child = 2*off + 4 + 4*(x > T): 4 instructions per level),
@@ -1397,7 +1380,9 @@ bool binned_preferred(const DevTree& t, int64_t n, uint32_t flags) {
   if (flags & (CAPT_MODE_DIRECT | CAPT_MODE_THREAD)) return false;
   if (n >= (int64_t(1) << 31)) return false;
   if (flags & CAPT_MODE_BINNED) return true;
-  return n >= (int64_t(1) << 18) && n >= 16 * t.n;
+  // measured (config-4 sweep): the hybrid unbinned kernel wins up to ~1 M
+  // spheres (5.7 vs 2.8 G q/s at 256 K, a tie at 1 M, 13 vs 26 at 4 M)
+  return n >= (int64_t(1) << 20) && n >= 64 * t.n;
 }
 
 int launch_binned(const DevTree& t, const void* centers, const void* radii, int64_t n, int L,

@@ -347,6 +347,146 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Hybrid unbinned kernel (fp32 inputs, k = 3): the classifier of the binned
+// pipeline's K1, one sphere per thread -- 13 shared-memory levels, one
+// 256-bit probe record load, conservative AABB reject, representative probe,
+// group resolution by ballot -- then the warp scans the sets of its still
+// unresolved spheres one after the other, cooperatively (warp_scan_f32 /
+// warp_scan_f64).  Every sphere's descent runs in parallel; only the rare
+// unresolved ones pay a serial scan.
+// ---------------------------------------------------------------------------
+constexpr int kHybSmem = 8191;  // top 13 levels
+constexpr int64_t kHybridMin = int64_t(1) << 15;
+__global__ void __launch_bounds__(kBlock) k_query_hybrid(
+    DevTree t, const float* __restrict__ centers, const float* __restrict__ radii, int64_t n,
+    int L, const uint8_t* __restrict__ lane_mask, uint32_t flags, uint32_t* __restrict__ out_bits,
+    unsigned long long* __restrict__ first_bad, float rlo_f, float rhi_f) {
+  __shared__ float sT[kHybSmem];
+  const int n_smem = int(t.n - 1 < kHybSmem ? t.n - 1 : kHybSmem);
+  for (int i = threadIdx.x; i < n_smem; i += blockDim.x) sT[i] = t.T[i];
+  __syncthreads();
+  const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(sT));
+  const int dsm = t.depth < 13 ? t.depth : 13;
+  const int lane = threadIdx.x & 31;
+  const bool prefilter = flags & CAPT_PREFILTER;
+  const bool check = flags & CAPT_CHECK_RADII;
+  const unsigned seg = L >= 32 ? 0xffffffffu : ((1u << L) - 1u) << ((lane / L) * L);
+  const float band_lo = 1.0f - kTau, band_hi = 1.0f + kTau;
+  const float INF = __int_as_float(0x7f800000);
+  const int64_t n_pad = (n + 31) & ~int64_t(31);
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q - lane < n_pad;
+       q += int64_t(gridDim.x) * blockDim.x) {
+    bool valid = q < n;
+    if (valid && lane_mask) valid = lane_mask[q] != 0;
+    float cx = 0.f, cy = 0.f, cz = 0.f, r = 0.f;
+    if (valid) {
+      cx = __ldg(centers + 3 * q);
+      cy = __ldg(centers + 3 * q + 1);
+      cz = __ldg(centers + 3 * q + 2);
+      r = __ldg(radii + q);
+    }
+    if (check && valid && (r < rlo_f || r > rhi_f))
+      atomicMin(first_bad, static_cast<unsigned long long>(q));
+    // descent: 13 shared levels on absolute addresses, the rest from T
+    unsigned ad = sbase;
+    int s = 0;
+    {
+      const unsigned k0 = 4u - sbase, k1 = 8u - sbase;
+      for (; s + 3 <= dsm; s += 3) {
+        ad = 2 * ad + (cx > lds_f32(ad) ? k1 : k0);
+        ad = 2 * ad + (cy > lds_f32(ad) ? k1 : k0);
+        ad = 2 * ad + (cz > lds_f32(ad) ? k1 : k0);
+      }
+    }
+    unsigned off = ad - sbase;
+    for (; s < dsm; ++s) {
+      const int ax = s % 3;
+      const float c = ax == 0 ? cx : (ax == 1 ? cy : cz);
+      off = 2 * off + (c > lds_f32(sbase + off) ? 8u : 4u);
+    }
+    for (; s < t.depth; ++s) {
+      const int ax = s % 3;
+      const float c = ax == 0 ? cx : (ax == 1 ? cy : cz);
+      off = 2 * off + (c > __ldg(t.T + (off >> 2)) ? 8u : 4u);
+    }
+    const int64_t leaf = int64_t(off >> 2) - (t.n - 1);
+    // classification (see k_bin_count3: conservative AABB, probe)
+    const float r2 = r * r;
+    const bool cfin = isfinite(cx) && isfinite(cy) && isfinite(cz);
+    const bool fast = cfin && r2 >= kR2Min && r2 <= kR2Max;
+    int st = fast ? 2 : ((!cfin && isfinite(r)) ? 0 : 3);
+    st = valid ? st : 0;
+    float pr[8];
+    ld_v8(t.probe + 8 * leaf, pr);
+    if (prefilter) {
+      const float2 l01 = h2f2(pr[3]), l2h0 = h2f2(pr[4]), h12 = h2f2(pr[5]);
+      const float rx = fmaxf(fmaxf(l01.x - cx, 0.f), cx - l2h0.y);
+      const float ry = fmaxf(fmaxf(l01.y - cy, 0.f), cy - h12.x);
+      const float rz = fmaxf(fmaxf(l2h0.x - cz, 0.f), cz - h12.y);
+      const float ss = fmaf(rz, rz, fmaf(ry, ry, rx * rx));
+      st = (fast && ss > r2 * band_hi) ? 0 : st;
+    }
+    const float dx = cx - pr[0], dy = cy - pr[1], dz = cz - pr[2];
+    bool verdict = st == 2 && fmaf(dz, dz, fmaf(dy, dy, dx * dx)) <= r2 * band_lo;
+    // unresolved spheres of unresolved groups: cooperative scans
+    unsigned done_groups = __ballot_sync(0xffffffffu, verdict);
+    unsigned todo = __ballot_sync(0xffffffffu, (st == 2 || st == 3) && !verdict);
+    const unsigned leaf_lo = unsigned(leaf);
+    while (true) {
+      // drop lanes whose group already has a hit
+      if (L > 1) {
+        unsigned resolved = 0;
+        for (int g0 = 0; g0 < 32; g0 += L) {
+          const unsigned m = (L >= 32 ? 0xffffffffu : ((1u << L) - 1u)) << g0;
+          if (done_groups & m) resolved |= m;
+        }
+        todo &= ~resolved;
+      }
+      if (!todo) break;
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const float sx = __shfl_sync(0xffffffffu, cx, src);
+      const float sy = __shfl_sync(0xffffffffu, cy, src);
+      const float sz = __shfl_sync(0xffffffffu, cz, src);
+      const float sr = __shfl_sync(0xffffffffu, r, src);
+      const int sst = __shfl_sync(0xffffffffu, st, src);
+      const unsigned sleaf = __shfl_sync(0xffffffffu, leaf_lo, src);
+      const uint2 set = __ldg(t.set + sleaf);
+      int v = 2;
+      if (sst == 2) {
+        const float sr2 = sr * sr;
+        v = warp_scan_f32(t, set, sx, sy, sz, sr2 * band_lo, sr2 * band_hi, lane);
+      }
+      bool hit = v == 1;
+      if (v == 2) {
+        const double c64[3] = {sx, sy, sz};
+        hit = warp_scan_f64(t, set, c64, double(sr), lane);
+      }
+      if (hit) {
+        if (lane == src) verdict = true;
+        done_groups |= 1u << src;
+      }
+    }
+    // bit packing: one bit per lane group (atomicOr into cleared words)
+    const unsigned bits = __ballot_sync(0xffffffffu, verdict);
+    if (lane == 0 && bits) {
+      const int64_t wbase = q - lane;  // first sphere of this warp
+      if (L == 1) {
+        atomicOr(out_bits + (wbase >> 5), bits);
+      } else {
+        uint32_t gb = 0;
+        for (int j = 0; j < 32 / L; ++j)
+          if ((bits >> (j * L)) & (L >= 32 ? 0xffffffffu : ((1u << L) - 1u))) gb |= 1u << j;
+        const int64_t g0 = wbase / L;
+        atomicOr(out_bits + (g0 >> 5), gb << (g0 & 31));
+      }
+    }
+    (void)seg;
+  }
+}
+
 template <typename InT>
 __global__ void k_leaf_indices(DevTree t, const void* __restrict__ centers, int64_t n,
                                int64_t* __restrict__ out) {
@@ -390,6 +530,22 @@ int launch_direct(const DevTree& t, const void* centers, const void* radii, int6
                   unsigned long long* counters, unsigned long long* first_bad, cudaStream_t s) {
   const bool f64 = flags & CAPT_INPUT_F64;
   const bool stats = flags & CAPT_STATS;
+  // hybrid for batches with enough warps to hide its serial per-warp scans
+  // (measured crossover with the warp kernel between 16 K and 64 K spheres)
+  const bool hybrid_ok = !f64 && t.k == 3 && !(flags & CAPT_MODE_WARP) &&
+                         (n >= kHybridMin || (flags & CAPT_MODE_DIRECT));
+  if (!stats && !(flags & CAPT_MODE_THREAD) && hybrid_ok) {
+    if (L <= 8) CAPT_CUDA(cudaMemsetAsync(bits, 0, 4 * (n_words ? n_words : 1), s));
+    float lo = float(t.r_min), hi = float(t.r_max);
+    if (double(lo) < t.r_min) lo = nextafterf(lo, INFINITY);
+    if (double(hi) > t.r_max) hi = nextafterf(hi, -INFINITY);
+    k_query_hybrid<<<grid_for(n, kBlock, 4), kBlock, 0, s>>>(
+        t, static_cast<const float*>(centers), static_cast<const float*>(radii), n, L, mask, flags,
+        bits, first_bad, lo, hi);
+    CAPT_CUDA(cudaGetLastError());
+    note_launches(1);
+    return CAPT_OK;
+  }
   if (!stats && !(flags & CAPT_MODE_THREAD)) {
     if (L <= 8) CAPT_CUDA(cudaMemsetAsync(bits, 0, 4 * (n_words ? n_words : 1), s));
     const int grid = grid_for((n / L) * 32, kBlock, 8);

@@ -1,12 +1,32 @@
 // Device helpers shared by the direct and binned query kernels.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "capt_internal.cuh"
 
 namespace capt {
+
+// one 256-bit load (sm_100): a leaf's probe record
+__device__ __forceinline__ void ld_v8(const float* p, float (&v)[8]) {
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+        "=f"(v[7])
+      : "l"(p));
+}
+// two fp16 values packed in a float's bits -> float2
+__device__ __forceinline__ float2 h2f2(float bits) {
+  const unsigned u = __float_as_uint(bits);
+  return __half22float2(*reinterpret_cast<const __half2*>(&u));
+}
+// shared-memory load at an absolute shared-window address
+__device__ __forceinline__ float lds_f32(unsigned addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
 
 // Top 12 levels of the Eytzinger split array live in shared memory (16 KB).
 constexpr int kSmemNodes = 4095;

@@ -130,8 +130,11 @@ def test_binned_device_built_tree_and_auto_mode():
     tree = P.construct(P.PointCloud(cloud), P.BuildParams(0.02, 0.08))
     c, r = W.cfg1_queries(cloud, n_groups=1 << 15, seed=3)
     exp = O.brute_collides_many(cloud, c, r)
-    assert np.array_equal(P.collides_many(tree, c, r), exp)  # auto -> binned here
+    assert np.array_equal(P.collides_many(tree, c, r), exp)  # auto -> hybrid here
     assert np.array_equal(q(tree, c, r, mode=DIRECT), exp)
+    assert np.array_equal(q(tree, c, r), exp)  # forced binned
+    c2, r2 = W.cfg1_queries(cloud, n_groups=1 << 18, seed=4)  # 2 M spheres: auto -> binned
+    assert np.array_equal(P.collides_many(tree, c2, r2), O.collides_many(O.tree_from(tree), c2, r2))
 
 
 def test_binned_split_walls_and_grid_cells():

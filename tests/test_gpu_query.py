@@ -244,15 +244,17 @@ def test_infinite_radius_with_infinite_centre():
         assert np.array_equal(got, O.collides_many(t, c, r, use_aabb_prefilter=pre)), pre
 
 
-@pytest.mark.parametrize("mode", ["thread", "warp"])
+@pytest.mark.parametrize("mode", ["thread", "warp", "hybrid"])
 def test_unbinned_kernels(mode):
-    """Both unbinned kernels (one thread per sphere / one warp per sphere),
+    """The unbinned kernels (one thread per sphere / one warp per sphere /
+    thread classification + warp scans),
     forced through the C-ABI flags, against the oracle: float and float64
     inputs, non-finite and extreme values, every lane width, lane masks."""
     from paper_2406_02807_b200 import _lib
     from paper_2406_02807_b200 import workloads as W
     from paper_2406_02807_b200.query import _host_query
-    flag = _lib.MODE_THREAD if mode == "thread" else _lib.MODE_DIRECT
+    flag = {"thread": _lib.MODE_THREAD, "warp": _lib.MODE_DIRECT | _lib.MODE_WARP,
+            "hybrid": _lib.MODE_DIRECT}[mode]
     cloud = W.cfg1_cloud()
     t = O.construct(cloud, 0.02, 0.08)
     tree = upload(t)
