@@ -468,7 +468,7 @@ def main_sweep(args):
             if args.mode != "auto":
                 mode = args.mode
             else:
-                mode = "binned" if n >= (1 << 20) and n >= 64 * tree.n else "direct"
+                mode = "binned" if n >= (1 << 20) else "direct"
             rows.append({"rate": rate, "n": n, "ms": ms, "queries_per_s": n / (ms * 1e-3),
                          "ms_graph": ms_graph, "queries_per_s_graph": n / (ms_graph * 1e-3),
                          "mode": mode, "labels_match": label_ok})

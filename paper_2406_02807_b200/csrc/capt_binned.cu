@@ -1380,9 +1380,11 @@ bool binned_preferred(const DevTree& t, int64_t n, uint32_t flags) {
   if (flags & (CAPT_MODE_DIRECT | CAPT_MODE_THREAD)) return false;
   if (n >= (int64_t(1) << 31)) return false;
   if (flags & CAPT_MODE_BINNED) return true;
-  // measured (config-4 sweep): the hybrid unbinned kernel wins up to ~1 M
-  // spheres (5.7 vs 2.8 G q/s at 256 K, a tie at 1 M, 13 vs 26 at 4 M)
-  return n >= (int64_t(1) << 20) && n >= 64 * t.n;
+  // measured: the hybrid unbinned kernel wins below ~1 M spheres (config-4
+  // sweep: 5.7 vs 2.8 G q/s at 256 K, a tie at 1 M, 13 vs 26 at 4 M); with
+  // large sets (config 3, mean 1.8 k points) the binned pipeline already wins
+  // 2x at 1 M spheres, whatever the leaf count
+  return n >= (int64_t(1) << 20);
 }
 
 int launch_binned(const DevTree& t, const void* centers, const void* radii, int64_t n, int L,
