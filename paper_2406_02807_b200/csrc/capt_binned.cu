@@ -268,9 +268,11 @@ __global__ void __launch_bounds__(256) k_bin_count(BinArgs a) {
 }
 
 // K1 specialised for k = 3, fp32 input (the hot path): V spheres per thread
-// in flight, 32-bit indexing, the top 13 levels of T in shared memory walked
-// with byte offsets (child = 2*off + 4 + 4*(x > T): 4 instructions per level),
-// one plain atomic per binned sphere for its ticket.
+// in flight (one sphere per lane: the inputs stay coalesced -- a thread-per-
+// group variant sharing the descent prefix of an 8-sphere group was measured
+// 2x slower), 32-bit indexing, the top 13 levels of T in shared memory walked
+// on absolute shared addresses (LDS, FSETP, SEL, IADD3 per level), one
+// 256-bit probe record per sphere, one list atomic per warp.
 constexpr int kSmemNodes3 = 8191;
 // K1 min CTAs per SM (caps registers at 64): 4 beats 1 (70 regs) by ~10%
 #ifndef CAPT_K1_MINB
