@@ -168,6 +168,24 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def profiled_traffic(config):
+    """DRAM bytes (read + write) per query launch from the committed ncu
+    --set full capture of this bench command (profiles/r01_cfg<k>_ncu_full.json,
+    summed over the captured kernels), or (None, reason)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                        f"r01_cfg{config}_ncu_full.json")
+    if not os.path.exists(path):
+        return None, "no ncu capture committed for this config"
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    total, names = 0.0, []
+    for k in json.load(open(path)):
+        for f in ("dram_read", "dram_write"):
+            total += float(k[f]) * scale.get(k.get(f + "_unit", "byte"), 1)
+        names.append(k["kernel"].split("(")[0].split("::")[-1])
+    return total, (f"{os.path.relpath(path, os.path.dirname(path) + '/..')}: dram read+write of "
+                   f"{', '.join(names)} (one launch each)")
+
+
 def cpu_reference_rate(tree_ref, c, r, lane_width, target_s=10.0, max_spheres=None):
     """Spheres/s of the oracle port on a bounded sample sized for ~target_s."""
     from oracle import oracle as O
@@ -309,7 +327,7 @@ def main():
         roof = {"bound": "hbm", "achieved": bytes_step / (kernel_ms * 1e-3) / 1e9,
                 "peak": hbm_peak, "unit": "GB/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+    roof["traffic"], roof["traffic_source"] = profiled_traffic(args.config)
     roof["peak_source"] = ("FP32: FFMA microbenchmark measured live (capt_measure_fp32_peak); "
                            "HBM: MEASURED_PEAKS.json hbm_gbs")
     roof["counted_tests_per_step"] = tests
