@@ -1459,7 +1459,10 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   CAPT_CUDA(cudaMemsetAsync(ctr, 0, 4 * zero_words, s));
   const bool f64 = flags & CAPT_INPUT_F64;
   const int G = grid_for(n, 256, 8);
-  constexpr int V = 4;
+#ifndef CAPT_K1_V  // spheres in flight per K1 thread: 4 (339 us) beats 2 (442) and 6 (482)
+#define CAPT_K1_V 4
+#endif
+  constexpr int V = CAPT_K1_V;
   const int G4 = grid_for((n + V - 1) / V, 256, 8);
   tm.mark(1, s);
   if (f64) k_bin_count<double><<<G, 256, 0, s>>>(a);
