@@ -273,14 +273,19 @@ __global__ void __launch_bounds__(256) k_bin_count(BinArgs a) {
 // 2x slower), 32-bit indexing, the top 13 levels of T in shared memory walked
 // on absolute shared addresses (LDS, FSETP, SEL, IADD3 per level), one
 // 256-bit probe record per sphere, one list atomic per warp.
-constexpr int kSmemNodes3 = 8191;
+// split levels K1 keeps in shared memory: 13 (32 KB, 4 CTAs/SM; 339 us)
+// beats 14 (64 KB, 3 CTAs/SM; 370-401 us) on config 1
+#ifndef CAPT_K1_SMEM_LEVELS
+#define CAPT_K1_SMEM_LEVELS 13
+#endif
+constexpr int kSmemNodes3 = (1 << CAPT_K1_SMEM_LEVELS) - 1;
 // K1 min CTAs per SM (caps registers at 64): 4 beats 1 (70 regs) by ~10%
 #ifndef CAPT_K1_MINB
 #define CAPT_K1_MINB 4
 #endif
 template <int V>
 __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
-  __shared__ float sT[kSmemNodes3];
+  extern __shared__ __align__(16) float sT[];  // kSmemNodes3 floats (dynamic: may exceed 48 KB)
   const DevTree& t = a.t;
   const int n_smem = int(t.n - 1 < kSmemNodes3 ? t.n - 1 : kSmemNodes3);
   for (int i = threadIdx.x; i < n_smem; i += blockDim.x) sT[i] = t.T[i];
@@ -291,7 +296,7 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
   const float* __restrict__ rf = static_cast<const float*>(a.radii);
   const unsigned char* sb = reinterpret_cast<const unsigned char*>(sT);
   const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(sT));
-  const int dsm = t.depth < 13 ? t.depth : 13;
+  const int dsm = t.depth < CAPT_K1_SMEM_LEVELS ? t.depth : CAPT_K1_SMEM_LEVELS;
   const int nl1 = int(t.n - 1);
   const int n = int(a.n);
   const int n_pad = (n + 31) & ~31;
@@ -1466,7 +1471,15 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   const int G4 = grid_for((n + V - 1) / V, 256, 8);
   tm.mark(1, s);
   if (f64) k_bin_count<double><<<G, 256, 0, s>>>(a);
-  else if (t.k == 3) k_bin_count3<V><<<G4, 256, 0, s>>>(a);
+  else if (t.k == 3) {
+    static bool k1_attr = false;
+    if (!k1_attr) {
+      CAPT_CUDA(cudaFuncSetAttribute(k_bin_count3<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(float) * kSmemNodes3)));
+      k1_attr = true;
+    }
+    k_bin_count3<V><<<G4, 256, sizeof(float) * kSmemNodes3, s>>>(a);
+  }
   else k_bin_count<float><<<G, 256, 0, s>>>(a);
   tm.mark(2, s);
   // per-leaf starts and tiles
