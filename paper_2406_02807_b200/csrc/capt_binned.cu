@@ -62,6 +62,16 @@ constexpr int kTsTc = CAPT_TC_TS;  // spheres per tile, tensor-core K5
 constexpr int kChunk = 512;        // staged points per shared-memory chunk
 constexpr float kBand = 0x1p-18f;  // 64u
 
+// Programmatic dependent launch: each stage after K1 is launched with
+// programmatic stream serialisation, so its CTAs are scheduled while the
+// previous stage drains; it waits (griddepcontrol.wait) before reading the
+// previous stage's output.  Every stage signals its dependents once its CTAs
+// are past their last write.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 template <typename InT>
 __device__ __forceinline__ void load_sphere(const void* c, const void* r, int64_t q, int k,
                                             double c64[3], double& r64) {
@@ -480,6 +490,7 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
       }
     }
   }
+  pdl_trigger();
 }
 
 // K3: group K1's compact list by leaf in two coalescing passes instead of
@@ -503,6 +514,7 @@ constexpr int kLeafSpan = 2048;  // K3b shared-memory leaf counters
 __global__ void __launch_bounds__(256) k_part_bucket(BinArgs a) {
   __shared__ uint32_t hist[kBuckets];
   __shared__ uint32_t gbase[kBuckets];
+  pdl_wait();
   const uint32_t n = *a.list_n;
   const int tid = threadIdx.x;
   // the K5 tile list: every chunk of <= ts spheres of a leaf, leaf by leaf in
@@ -560,11 +572,13 @@ __global__ void __launch_bounds__(256) k_part_bucket(BinArgs a) {
     }
     __syncthreads();
   }
+  pdl_trigger();
 }
 
 __global__ void __launch_bounds__(256) k_part_leaf(BinArgs a) {
   __shared__ uint32_t cnt[kLeafSpan];
   __shared__ int lmin_s, lmax_s;
+  pdl_wait();
   const uint32_t n = *a.list_n;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -617,6 +631,7 @@ __global__ void __launch_bounds__(256) k_part_leaf(BinArgs a) {
     }
     __syncthreads();
   }
+  pdl_trigger();
 }
 
 // K2: one CTA turns the per-leaf counts into per-leaf start offsets (leaf
@@ -641,6 +656,7 @@ constexpr int64_t kScanSingleMax = 32768;  // leaves handled by the one-CTA K2
 constexpr int kScanT = 512;
 constexpr int kScanI = 16;  // leaves per thread per pass
 __global__ void __launch_bounds__(kScanT) k_scan_tiles(BinArgs a) {
+  pdl_wait();
   using Load = cub::BlockLoad<uint32_t, kScanT, kScanI, cub::BLOCK_LOAD_TRANSPOSE>;
   using Store = cub::BlockStore<uint32_t, kScanT, kScanI, cub::BLOCK_STORE_TRANSPOSE>;
   using Scan = cub::BlockScan<uint32_t, kScanT>;
@@ -701,6 +717,7 @@ __global__ void __launch_bounds__(kScanT) k_scan_tiles(BinArgs a) {
   }
   __syncthreads();
   if (tid == 0) *a.n_tiles = carry[1];
+  pdl_trigger();
 }
 
 // ---- packed fp32x2 helpers (sm_100: FFMA2 / FMNMX3) ----
@@ -1030,12 +1047,13 @@ __global__ void __launch_bounds__(kTcThreads) k_binned_scan_tc(BinArgs a) {
   const DevTree& t = a.t;
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
-  const int n_tiles = int(*a.n_tiles);
-  if (tid == 0) {
-    tc::mbar_init(&S.mbar, 1);
-    S.tile = int(atomicAdd(a.tile_ctr, 1u));
-  }
+  if (tid == 0) tc::mbar_init(&S.mbar, 1);
   if (warp == 0) tc::tmem_alloc<kTcCols>(&S.tmem);
+  // (TMEM and the barrier are set up while K3 drains; tiles, records and the
+  // permutation come from K2/K3)
+  pdl_wait();
+  const int n_tiles = int(*a.n_tiles);
+  if (tid == 0) S.tile = int(atomicAdd(a.tile_ctr, 1u));
   tc::fence_async_smem();
   tc::fence_before_sync();
   __syncthreads();
@@ -1189,12 +1207,14 @@ __global__ void __launch_bounds__(kTcThreads) k_binned_scan_tc(BinArgs a) {
   __syncthreads();
   tc::fence_after_sync();
   if (warp == 0) tc::tmem_free<kTcCols>(tmem);
+  pdl_trigger();
 }
 
 // Exact float64 path, one warp per queued sphere: lanes split the set,
 // query.py:96-99 arithmetic (fp64, no FMA), ballot OR.
 template <typename InT>
 __global__ void k_slow(BinArgs a) {
+  pdl_wait();
   // K5's hits, flagged by list index -> the spheres' verdict bytes
   {
     const uint32_t nl = *a.list_n;
@@ -1293,6 +1313,7 @@ __global__ void k_slow(BinArgs a) {
     }
     if (__any_sync(0xffffffffu, hit) && lane == 0) a.verdict[e.x] = 1;
   }
+  pdl_trigger();
 }
 
 // One thread per lane group: its L verdict bytes in one vector load (L <= 8:
@@ -1301,6 +1322,7 @@ __global__ void k_slow(BinArgs a) {
 // multiple of 8 bytes past n.
 __global__ void k_pack(int64_t n_groups, int L, const uint8_t* __restrict__ v,
                        uint32_t* __restrict__ bits, int64_t n_words) {
+  pdl_wait();
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   const int64_t n_thr = n_words * 32;
   for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < n_thr; g += stride) {
@@ -1342,6 +1364,23 @@ struct Arena {
 };
 
 }  // namespace
+
+// launch with programmatic stream serialisation (see pdl_wait)
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem,
+                              cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 // CAPT_STAGE_TIMING=1: CUDA events between the pipeline stages (in-loop
 // times, unlike a serialised profiler pass), summed over calls and printed at
@@ -1484,7 +1523,7 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   tm.mark(2, s);
   // per-leaf starts and tiles
   if (nl <= kScanSingleMax) {
-    k_scan_tiles<<<1, kScanT, 0, s>>>(a);
+    CAPT_CUDA(launch_pdl(k_scan_tiles, 1, kScanT, 0, s, a));
   } else {
     uint32_t* tc = A.get<uint32_t>(nl);
     size_t tb = 0;
@@ -1500,9 +1539,9 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   tm.mark(3, s);
   {
     const int Gp = grid_for((n + kPartItems - 1) / kPartItems * 256, 256, 4);
-    k_part_bucket<<<Gp, 256, 0, s>>>(a);
+    CAPT_CUDA(launch_pdl(k_part_bucket, Gp, 256, 0, s, a));
     tm.mark(4, s);
-    k_part_leaf<<<Gp, 256, 0, s>>>(a);
+    CAPT_CUDA(launch_pdl(k_part_leaf, Gp, 256, 0, s, a));
   }
   static int sms = 0, occ = 0;
   if (!sms) {
@@ -1523,14 +1562,15 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
       occ_tc = 512 / kTcCols;  // TMEM columns per SM
       if (occ_tc > 8) occ_tc = 8;
     }
-    k_binned_scan_tc<<<sms * occ_tc, kTcThreads, sizeof(SmemTc), s>>>(a);
+    CAPT_CUDA(launch_pdl(k_binned_scan_tc, sms * occ_tc, kTcThreads, sizeof(SmemTc), s, a));
   } else {
     k_binned_scan<<<sms * occ, kBT, sizeof(SmemBinned), s>>>(a);
   }
   tm.mark(6, s);
-  if (f64) k_slow<double><<<sms * 8, 128, 0, s>>>(a);
-  else k_slow<float><<<sms * 8, 128, 0, s>>>(a);
-  k_pack<<<grid_for(n_words * 32, 256, 8), 256, 0, s>>>(n / L, L, a.verdict, bits, n_words);
+  if (f64) CAPT_CUDA(launch_pdl(k_slow<double>, sms * 8, 128, 0, s, a));
+  else CAPT_CUDA(launch_pdl(k_slow<float>, sms * 8, 128, 0, s, a));
+  CAPT_CUDA(launch_pdl(k_pack, grid_for(n_words * 32, 256, 8), 256, 0, s, n / L, L,
+                       static_cast<const uint8_t*>(a.verdict), bits, n_words));
   tm.mark(7, s);
   tm.finish(s);
   CAPT_CUDA(cudaGetLastError());
