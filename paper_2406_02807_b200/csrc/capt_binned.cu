@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
   const int n_smem = int(t.n - 1 < kSmemNodes3 ? t.n - 1 : kSmemNodes3);
   for (int i = threadIdx.x; i < n_smem; i += blockDim.x) sT[i] = t.T[i];
   __syncthreads();
+  pdl_wait();  // the counters are cleared by k_zero (T staging overlaps it)
   const bool check = a.flags & CAPT_CHECK_RADII;
   const bool prefilter = a.flags & CAPT_PREFILTER;
   const float* __restrict__ cf = static_cast<const float*>(a.centers);
@@ -1365,6 +1366,13 @@ struct Arena {
 
 }  // namespace
 
+__global__ void k_zero(uint32_t* __restrict__ p, int64_t n) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = 0u;
+  pdl_trigger();
+}
+
 // launch with programmatic stream serialisation (see pdl_wait)
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem,
@@ -1500,7 +1508,7 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   StageTimer& tm = g_stage_timer;
   tm.mark(0, s);
   // (verdict bytes need no clearing: K1 writes one for every sphere)
-  CAPT_CUDA(cudaMemsetAsync(ctr, 0, 4 * zero_words, s));
+  k_zero<<<grid_for(zero_words, 256, 4), 256, 0, s>>>(ctr, zero_words);
   const bool f64 = flags & CAPT_INPUT_F64;
   const int G = grid_for(n, 256, 8);
 #ifndef CAPT_K1_V  // spheres in flight per K1 thread: 4 (339 us) beats 2 (442) and 6 (482)
@@ -1517,7 +1525,7 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
                                      int(sizeof(float) * kSmemNodes3)));
       k1_attr = true;
     }
-    k_bin_count3<V><<<G4, 256, sizeof(float) * kSmemNodes3, s>>>(a);
+    CAPT_CUDA(launch_pdl(k_bin_count3<V>, G4, 256, sizeof(float) * kSmemNodes3, s, a));
   }
   else k_bin_count<float><<<G, 256, 0, s>>>(a);
   tm.mark(2, s);
@@ -1574,7 +1582,7 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   tm.mark(7, s);
   tm.finish(s);
   CAPT_CUDA(cudaGetLastError());
-  note_launches(7);  // count, scan+tiles, 2 partition passes, scan, slow, pack
+  note_launches(8);  // zero, count, scan+tiles, 2 partition passes, scan, slow, pack
   static const bool debug = getenv("CAPT_DEBUG") != nullptr;
   if (debug) {
     uint32_t h[4], last[2];
