@@ -657,59 +657,71 @@ constexpr int64_t kScanSingleMax = 32768;  // leaves handled by the one-CTA K2
 constexpr int kScanT = 512;
 constexpr int kScanI = 16;  // leaves per thread per pass
 __global__ void __launch_bounds__(kScanT) k_scan_tiles(BinArgs a) {
-  pdl_wait();
-  using Load = cub::BlockLoad<uint32_t, kScanT, kScanI, cub::BLOCK_LOAD_TRANSPOSE>;
-  using Store = cub::BlockStore<uint32_t, kScanT, kScanI, cub::BLOCK_STORE_TRANSPOSE>;
   using Scan = cub::BlockScan<uint32_t, kScanT>;
-  __shared__ union {
-    typename Load::TempStorage load;
-    typename Store::TempStorage store;
-    typename Scan::TempStorage scan;
-  } tmp;
+  __shared__ typename Scan::TempStorage tmp;
   __shared__ uint32_t carry[2];
+  pdl_wait();
   const int nl = int(a.t.n);
   const int tid = threadIdx.x;
   if (tid == 0) carry[0] = carry[1] = 0;
   for (int p0 = 0; p0 < nl; p0 += kScanT * kScanI) {
-    const int valid = min(kScanT * kScanI, nl - p0);
+    // blocked arrangement, direct 128-bit loads: leaves p0 + 16 tid + i
+    const int b0 = p0 + kScanI * tid;
+    const int nv = max(0, min(kScanI, nl - b0));
     uint32_t c[kScanI], ord[kScanI], tc[kScanI];
-    __syncthreads();  // carry visible; temp storage free
-    Load(tmp.load).Load(a.counts + p0, c, valid, 0u);
-    __syncthreads();
-    Load(tmp.load).Load(reinterpret_cast<const uint32_t*>(a.t.order) + p0, ord, valid, 0u);
+    if (nv == kScanI) {
 #pragma unroll
-    for (int i = 0; i < kScanI; ++i)  // blocked: leaves p0 + tid*kScanI + i
-      tc[i] = (tid * kScanI + i < valid) ? (a.counts[ord[i]] + a.ts - 1) / a.ts : 0u;
+      for (int k = 0; k < kScanI / 4; ++k) {
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(a.counts + b0) + k);
+        const uint4 y = __ldg(reinterpret_cast<const uint4*>(a.t.order + b0) + k);
+        c[4 * k] = x.x; c[4 * k + 1] = x.y; c[4 * k + 2] = x.z; c[4 * k + 3] = x.w;
+        ord[4 * k] = y.x; ord[4 * k + 1] = y.y; ord[4 * k + 2] = y.z; ord[4 * k + 3] = y.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < kScanI; ++i) {
+        c[i] = i < nv ? a.counts[b0 + i] : 0u;
+        ord[i] = i < nv ? uint32_t(a.t.order[b0 + i]) : 0u;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kScanI; ++i) tc[i] = i < nv ? (a.counts[ord[i]] + a.ts - 1) / a.ts : 0u;
     uint32_t cs = 0, ts = 0;
 #pragma unroll
     for (int i = 0; i < kScanI; ++i) {
       cs += c[i];
       ts += tc[i];
     }
+    __syncthreads();  // carry visible; scan storage free
     const uint32_t c0 = carry[0], t0 = carry[1];
     uint32_t cpre, tpre, ctot, ttot;
+    Scan(tmp).ExclusiveSum(cs, cpre, ctot);
     __syncthreads();
-    Scan(tmp.scan).ExclusiveSum(cs, cpre, ctot);
-    __syncthreads();
-    Scan(tmp.scan).ExclusiveSum(ts, tpre, ttot);
+    Scan(tmp).ExclusiveSum(ts, tpre, ttot);
     cpre += c0;
     tpre += t0;
-    uint32_t st[kScanI];
 #pragma unroll
-    for (int i = 0; i < kScanI; ++i) {
-      st[i] = cpre;
-      cpre += c[i];
+    for (int i = 0; i < kScanI; ++i) {  // c[] / tc[] become the exclusive prefixes
+      const uint32_t cv = c[i], tv = tc[i];
+      c[i] = cpre;
+      tc[i] = tpre;
+      cpre += cv;
+      tpre += tv;
     }
-    __syncthreads();
-    Store(tmp.store).Store(a.start + p0, st, valid);
-    uint32_t tst[kScanI];
+    if (nv == kScanI) {
 #pragma unroll
-    for (int i = 0; i < kScanI; ++i) {
-      tst[i] = tpre;
-      tpre += tc[i];
+      for (int k = 0; k < kScanI / 4; ++k) {
+        reinterpret_cast<uint4*>(a.start + b0)[k] =
+            make_uint4(c[4 * k], c[4 * k + 1], c[4 * k + 2], c[4 * k + 3]);
+        reinterpret_cast<uint4*>(a.tstart + b0)[k] =
+            make_uint4(tc[4 * k], tc[4 * k + 1], tc[4 * k + 2], tc[4 * k + 3]);
+      }
+    } else {
+      for (int i = 0; i < nv; ++i) {
+        a.start[b0 + i] = c[i];
+        a.tstart[b0 + i] = tc[i];
+      }
     }
-    __syncthreads();
-    Store(tmp.store).Store(a.tstart + p0, tst, valid);
     __syncthreads();
     if (tid == 0) {
       carry[0] = c0 + ctot;
