@@ -50,6 +50,12 @@ extern "C" {
                                    of the tensor cores (tcgen05 tf32)          */
 #define CAPT_MODE_WARP 0x1000u  /* unbinned: the warp-per-sphere kernel instead
                                    of the hybrid (thread classify + warp scan) */
+#define CAPT_MODE_FIELD 0x2000u /* force the clearance-field pipeline (the
+                                   default for fp32 k=3 queries without
+                                   CAPT_STATS); EINVAL if the tree has none.
+                                   With CAPT_MODE_BINNED / CAPT_MODE_DIRECT:
+                                   the undecided spheres go through the
+                                   binned pipeline / the warp list kernel  */
 
 typedef struct capt_tree capt_tree;
 
@@ -146,6 +152,23 @@ int capt_filter_cloud(int device, int k, const float* points, int64_t n,
  * CAPT_HOST_IO, else device memory.  n >= 2. */
 int capt_nn_distances(int device, int k, const float* points, int64_t n,
                       uint32_t flags, double* out, void* stream);
+
+/* Clearance field of a k = 3 tree (derived data, built on the device with
+ * the tree): a uniform grid of nx*ny*nz cells of edge h from lo; cell
+ * (ix,iy,iz) is record (iz*ny + iy)*nx + ix = {witness x, y, z, nn} with
+ * centre x0 = fmaf(ix + 0.5f, h, lo[0]) (likewise y, z), witness = the
+ * cloud point nearest x0 (+inf if none within rcap) and nn <= the distance
+ * from x0 to every cloud point (nn <= rcap).  box_lo/box_hi: the cloud's box.
+ * cells: NULL, or a host buffer of 4 * n_cells floats.  Returns CAPT_EINVAL
+ * for trees without a field. */
+typedef struct {
+  int32_t nx, ny, nz, reserved;
+  int64_t n_cells;
+  float lo[3], h;
+  float box_lo[3], box_hi[3];
+  float rcap, pad;
+} capt_field_info;
+int capt_tree_field(const capt_tree* tree, capt_field_info* info, float* cells);
 
 /* Number of kernels this library has launched in the process so far
  * (all devices/threads); used by bench.py to report gpu_launches. */

@@ -27,6 +27,7 @@ MODE_BINNED = 0x200
 MODE_THREAD = 0x400
 K5_FFMA = 0x800
 MODE_WARP = 0x1000
+MODE_FIELD = 0x2000
 
 
 class CaptTreeInfo(C.Structure):
@@ -35,6 +36,13 @@ class CaptTreeInfo(C.Structure):
                 ("max_affordance", C.c_int64), ("r_min", C.c_double),
                 ("r_max", C.c_double), ("device_bytes", C.c_int64),
                 ("device", C.c_int32), ("reserved", C.c_int32), ("n_ties", C.c_int64)]
+
+
+class CaptFieldInfo(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32),
+                ("reserved", C.c_int32), ("n_cells", C.c_int64), ("lo", C.c_float * 3),
+                ("h", C.c_float), ("box_lo", C.c_float * 3), ("box_hi", C.c_float * 3),
+                ("rcap", C.c_float), ("pad", C.c_float)]
 
 
 _lib = None
@@ -72,12 +80,13 @@ def lib():
     L.capt_measure_fp32_peak.argtypes = [i32, C.POINTER(dbl)]
     L.capt_tc_selftest.argtypes = [i32, C.POINTER(dbl)]
     L.capt_nn_distances.argtypes = [i32, i32, vp, i64, u32, vp, vp]
+    L.capt_tree_field.argtypes = [vp, C.POINTER(CaptFieldInfo), vp]
     L.capt_kernel_launches.restype = C.c_int64
     L.capt_kernel_launches.argtypes = []
     for name in ("capt_tree_create", "capt_tree_build", "capt_tree_info_get",
                  "capt_tree_export", "capt_tree_slab", "capt_tree_from_slab", "capt_query",
                  "capt_leaf_indices", "capt_filter_cloud", "capt_measure_fp32_peak",
-                 "capt_tc_selftest", "capt_nn_distances"):
+                 "capt_tc_selftest", "capt_nn_distances", "capt_tree_field"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -127,4 +136,5 @@ EXPORTED_SYMBOLS = (
     "capt_tree_info_get", "capt_tree_export", "capt_tree_destroy", "capt_tree_slab",
     "capt_tree_from_slab", "capt_query", "capt_leaf_indices", "capt_filter_cloud",
     "capt_measure_fp32_peak", "capt_kernel_launches", "capt_tc_selftest", "capt_nn_distances",
+    "capt_tree_field",
 )

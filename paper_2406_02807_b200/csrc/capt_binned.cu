@@ -293,7 +293,10 @@ constexpr int kSmemNodes3 = (1 << CAPT_K1_SMEM_LEVELS) - 1;
 #ifndef CAPT_K1_MINB
 #define CAPT_K1_MINB 4
 #endif
-template <int V>
+// kList: the spheres are the clearance field's list (capt_field.cu) --
+// sphere ids a.qlist[0 .. *a.qlist_n), already masked and band-checked,
+// resolved one by one (a.L == 1; the caller ORs lane groups).
+template <int V, bool kList>
 __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
   extern __shared__ __align__(16) float sT[];  // kSmemNodes3 floats (dynamic: may exceed 48 KB)
   const DevTree& t = a.t;
@@ -305,11 +308,10 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
   const bool prefilter = a.flags & CAPT_PREFILTER;
   const float* __restrict__ cf = static_cast<const float*>(a.centers);
   const float* __restrict__ rf = static_cast<const float*>(a.radii);
-  const unsigned char* sb = reinterpret_cast<const unsigned char*>(sT);
   const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(sT));
   const int dsm = t.depth < CAPT_K1_SMEM_LEVELS ? t.depth : CAPT_K1_SMEM_LEVELS;
   const int nl1 = int(t.n - 1);
-  const int n = int(a.n);
+  const int n = kList ? int(*a.qlist_n) : int(a.n);
   const int n_pad = (n + 31) & ~31;
   const int lane = threadIdx.x & 31;
   const unsigned seg = a.L >= 32 ? 0xffffffffu : ((1u << a.L) - 1u) << ((lane / a.L) * a.L);
@@ -318,10 +320,12 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
   // streaming (evict-first) input loads, software-pipelined one iteration
   // ahead: the DRAM latency of iteration i+1 hides behind iteration i
   float nx[V], ny[V], nz[V], nr[V];
+  int nsid[V];  // sphere ids (the list entries in list mode)
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const int q = blockIdx.x * blockDim.x * V + v * blockDim.x + threadIdx.x;
-    const int qq = q < n ? q : 0;
+    const int qq = q < n ? (kList ? int(__ldcs(a.qlist + q)) : q) : 0;
+    nsid[v] = qq;
     nx[v] = __ldcs(cf + 3 * qq);
     ny[v] = __ldcs(cf + 3 * qq + 1);
     nz[v] = __ldcs(cf + 3 * qq + 2);
@@ -329,6 +333,7 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
   }
   for (int base = blockIdx.x * blockDim.x * V; base < n_pad; base += stride) {
     float cx[V], cy[V], cz[V], r[V];
+    int sid[V];
     bool valid[V];
     unsigned off[V];
 #pragma unroll
@@ -337,8 +342,10 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
       cy[v] = ny[v];
       cz[v] = nz[v];
       r[v] = nr[v];
+      sid[v] = nsid[v];
       const int qn = base + stride + v * blockDim.x + threadIdx.x;
-      const int qq = qn < n ? qn : 0;
+      const int qq = qn < n ? (kList ? int(__ldcs(a.qlist + qn)) : qn) : 0;
+      nsid[v] = qq;
       nx[v] = __ldcs(cf + 3 * qq);
       ny[v] = __ldcs(cf + 3 * qq + 1);
       nz[v] = __ldcs(cf + 3 * qq + 2);
@@ -348,10 +355,10 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
     for (int v = 0; v < V; ++v) {
       const int q = base + v * blockDim.x + threadIdx.x;
       valid[v] = q < n;
-      if (a.mask && valid[v]) valid[v] = a.mask[q] != 0;
+      if (!kList && a.mask && valid[v]) valid[v] = a.mask[q] != 0;
       off[v] = 0;
     }
-    if (check) {  // out-of-band radii are rare: one warp vote, then the atomics
+    if (!kList && check) {  // out-of-band radii are rare: one warp vote, then the atomics
       bool bad = false;
 #pragma unroll
       for (int v = 0; v < V; ++v) bad |= valid[v] && (r[v] < a.rlo_f || r[v] > a.rhi_f);
@@ -444,7 +451,7 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int q = base + v * blockDim.x + threadIdx.x;
-      if (q < n) a.verdict[q] = hit[v] ? 1 : 0;  // every byte written: no memset
+      if (q < n) a.verdict[sid[v]] = hit[v] ? 1 : 0;  // every byte written: no memset
     }
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -466,7 +473,7 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
     if (tot && lane == 0) lbase = atomicAdd(a.list_n, tot);
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      const int q = base + v * blockDim.x + threadIdx.x;
+      const int q = sid[v];
       if (status[v] == 2) {
         const unsigned peers = __match_any_sync(act[v], unsigned(leaf[v]));
         if (lane == __ffs(peers) - 1) atomicAdd(a.counts + leaf[v], __popc(peers));
@@ -485,7 +492,7 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
           const unsigned p = j + __popc(act[v] & lt);
           __stcs(a.lrec + p, make_float4(cx[v], cy[v], cz[v], r[v]));
           a.lhit[p] = 0;
-          __stcs(a.lmeta + p, make_int2(base + v * int(blockDim.x) + int(threadIdx.x), leaf[v]));
+          __stcs(a.lmeta + p, make_int2(sid[v], leaf[v]));
         }
         j += __popc(act[v]);
       }
@@ -1360,6 +1367,21 @@ __global__ void k_pack(int64_t n_groups, int L, const uint8_t* __restrict__ v,
   }
 }
 
+// list mode: the listed spheres' verdict bytes -> OR into the verdict words
+// (bit q, or bit q / L for lane groups)
+__global__ void k_list_bits(const uint32_t* __restrict__ qlist, const uint32_t* __restrict__ qlist_n,
+                            const uint8_t* __restrict__ v, int L, uint32_t* __restrict__ bits) {
+  pdl_wait();
+  const uint32_t nq = *qlist_n;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nq; j += gridDim.x * blockDim.x) {
+    const uint32_t q = qlist[j];
+    if (v[q]) {
+      const uint32_t b = L == 1 ? q : q / uint32_t(L);
+      atomicOr(bits + (b >> 5), 1u << (b & 31));
+    }
+  }
+}
+
 struct Arena {
   cudaStream_t s;
   void* ptrs[24];
@@ -1455,7 +1477,15 @@ bool binned_preferred(const DevTree& t, int64_t n, uint32_t flags) {
 
 int launch_binned(const DevTree& t, const void* centers, const void* radii, int64_t n, int L,
                   const uint8_t* mask, uint32_t flags, uint32_t* bits, int64_t n_words,
-                  unsigned long long* first_bad, cudaStream_t s) {
+                  unsigned long long* first_bad, cudaStream_t s, const uint32_t* qlist,
+                  const uint32_t* qlist_n) {
+  const bool list_mode = qlist != nullptr;
+  const int L_out = L;
+  if (list_mode) {
+    L = 1;
+    mask = nullptr;
+    flags &= ~uint32_t(CAPT_CHECK_RADII);
+  }
   static bool smem_set = false;
   if (!smem_set) {
     CAPT_CUDA(cudaFuncSetAttribute(k_binned_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1474,6 +1504,8 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.mask = mask;
   a.flags = flags;
   a.first_bad = first_bad;
+  a.qlist = qlist;
+  a.qlist_n = qlist_n;
   const int64_t nl = t.n;
   // everything that must start at zero, in one block (one memset):
   // counters (slow_n, n_tiles, tile_ctr, n_refined, list_n) | counts | cursor | bcursor
@@ -1533,11 +1565,16 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   else if (t.k == 3) {
     static bool k1_attr = false;
     if (!k1_attr) {
-      CAPT_CUDA(cudaFuncSetAttribute(k_bin_count3<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CAPT_CUDA(cudaFuncSetAttribute(k_bin_count3<V, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(float) * kSmemNodes3)));
+      CAPT_CUDA(cudaFuncSetAttribute(k_bin_count3<V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(sizeof(float) * kSmemNodes3)));
       k1_attr = true;
     }
-    CAPT_CUDA(launch_pdl(k_bin_count3<V>, G4, 256, sizeof(float) * kSmemNodes3, s, a));
+    if (list_mode)
+      CAPT_CUDA(launch_pdl(k_bin_count3<V, true>, G4, 256, sizeof(float) * kSmemNodes3, s, a));
+    else
+      CAPT_CUDA(launch_pdl(k_bin_count3<V, false>, G4, 256, sizeof(float) * kSmemNodes3, s, a));
   }
   else k_bin_count<float><<<G, 256, 0, s>>>(a);
   tm.mark(2, s);
@@ -1589,8 +1626,12 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   tm.mark(6, s);
   if (f64) CAPT_CUDA(launch_pdl(k_slow<double>, sms * 8, 128, 0, s, a));
   else CAPT_CUDA(launch_pdl(k_slow<float>, sms * 8, 128, 0, s, a));
-  CAPT_CUDA(launch_pdl(k_pack, grid_for(n_words * 32, 256, 8), 256, 0, s, n / L, L,
-                       static_cast<const uint8_t*>(a.verdict), bits, n_words));
+  if (list_mode)
+    CAPT_CUDA(launch_pdl(k_list_bits, grid_for(n, 256, 4), 256, 0, s, qlist, qlist_n,
+                         static_cast<const uint8_t*>(a.verdict), L_out, bits));
+  else
+    CAPT_CUDA(launch_pdl(k_pack, grid_for(n_words * 32, 256, 8), 256, 0, s, n / L, L,
+                         static_cast<const uint8_t*>(a.verdict), bits, n_words));
   tm.mark(7, s);
   tm.finish(s);
   CAPT_CUDA(cudaGetLastError());

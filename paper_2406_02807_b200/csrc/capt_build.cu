@@ -482,5 +482,10 @@ extern "C" int capt_tree_build(int device, int k, const float* points, int64_t n
     *out = nullptr;
     return cuda_fail(e, "tree build");
   }
-  return CAPT_OK;
+  rc = build_field(t, s);
+  if (rc) {
+    capt_tree_destroy(t);
+    *out = nullptr;
+  }
+  return rc;
 }

@@ -57,6 +57,19 @@ struct SlabHeader {
 };
 static_assert(sizeof(SlabHeader) <= 256, "header must fit its 256-B section");
 
+// Clearance field geometry (capt_field.cu): a uniform grid of nx*ny*nz cells
+// of edge h starting at lo; cell centre x0(i) = fma(i + 0.5, h, lo) per axis.
+// blo/bhi = the cloud's box (finite representatives); rcap caps the stored
+// lower bounds.  field == nullptr: no field (k < 3, or not built).
+struct FieldGeom {
+  int nx, ny, nz, m;   // cells per axis; bucket edge in cells (build only)
+  float lo[3];
+  float h, inv_h;
+  float blo[3], bhi[3];
+  float rcap;
+  int64_t cells;
+};
+
 struct DevTree {
   int k, depth;
   int64_t n;
@@ -71,6 +84,8 @@ struct DevTree {
   const float4* rep;  // row 0 of every set (the point owning the cell), +inf for padding
   const int* order;   // leaves by descending set size
   const float* probe; // 8 floats per leaf: rep xyz, fp16 box (conservative), 2 spare
+  const float4* field;  // clearance field: per cell witness xyz + lower bound (or nullptr)
+  FieldGeom fg;
 };
 
 }  // namespace capt
@@ -79,6 +94,8 @@ struct capt_tree {
   capt::SlabHeader h;
   int device;
   char* slab;  // device pointer
+  float4* field = nullptr;  // derived per device from the slab (capt_field.cu)
+  capt::FieldGeom fg{};
 };
 
 namespace capt {
@@ -118,6 +135,8 @@ inline DevTree view(const capt_tree* t) {
   d.rep = reinterpret_cast<const float4*>(t->slab + t->h.off_rep);
   d.order = reinterpret_cast<const int*>(t->slab + t->h.off_order);
   d.probe = reinterpret_cast<const float*>(t->slab + t->h.off_probe);
+  d.field = t->field;
+  d.fg = t->fg;
   return d;
 }
 
@@ -160,6 +179,16 @@ inline int depth_of(int64_t n) {
 int compute_origins(const DevTree& t, cudaStream_t s);
 
 int alloc_slab(capt_tree** out, int device, SlabHeader h);
+
+// Build the clearance field of a tree whose rep section is final (k = 3 only;
+// other trees keep field == nullptr).  Synchronises stream s.
+int build_field(capt_tree* t, cudaStream_t s);
+
+// The clearance-field query pipeline (fp32, k = 3, no CAPT_STATS / mode flags).
+bool field_eligible(const DevTree& t, int64_t n, uint32_t flags);
+int launch_field(const DevTree& t, const void* centers, const void* radii, int64_t n, int L,
+                 const uint8_t* mask, uint32_t flags, uint32_t* bits, int64_t n_words,
+                 unsigned long long* first_bad, cudaStream_t s);
 
 // scratch allocation helpers (stream-ordered allocator)
 template <class T>

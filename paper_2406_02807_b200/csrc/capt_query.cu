@@ -242,63 +242,6 @@ __device__ __forceinline__ int64_t warp_descend(const DevTree& t, const C c[3], 
   return i - (t.n - 1);
 }
 
-// fp32 cooperative scan: 0 = no point within the band, 1 = definite hit,
-// 2 = some point inside the error band (decide exactly).
-__device__ __forceinline__ int warp_scan_f32(const DevTree& t, uint2 set, float cx, float cy,
-                                             float cz, float loB, float hiB, int lane) {
-  const float* xs = reinterpret_cast<const float*>(t.data + set.x);
-  const uint32_t m4 = (set.y + 3u) & ~3u;
-  bool amb = false;
-  for (uint32_t p0 = 0; p0 < set.y; p0 += 128) {
-    float x[4], y[4], z[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t p = p0 + j * 32 + lane;
-      x[j] = y[j] = z[j] = __int_as_float(0x7f800000);
-      if (p < m4) {
-        x[j] = __ldg(xs + p);
-        y[j] = __ldg(xs + m4 + p);
-        z[j] = __ldg(xs + 2 * m4 + p);
-      }
-    }
-    bool hit = false;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float dx = cx - x[j], dy = cy - y[j], dz = cz - z[j];
-      const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      hit |= d2 <= loB;
-      amb |= d2 < hiB;
-    }
-    if (__any_sync(0xffffffffu, hit)) return 1;
-  }
-  return __any_sync(0xffffffffu, amb) ? 2 : 0;
-}
-
-// Exact reference scan (query.py:96-99), one point per lane per step.
-__device__ __forceinline__ bool warp_scan_f64(const DevTree& t, uint2 set, const double c[3],
-                                              double r64, int lane) {
-  const float* base = reinterpret_cast<const float*>(t.data + set.x);
-  const uint32_t m4 = (set.y + 3u) & ~3u;
-  const double R = __dmul_rn(r64, r64);
-  for (uint32_t p0 = 0; p0 < set.y; p0 += 32) {
-    const uint32_t p = p0 + lane;
-    bool hit = false;
-    if (p < set.y) {
-      double s = 0.0;
-#pragma unroll
-      for (int d = 0; d < kMaxK; ++d) {
-        if (d >= t.k) break;
-        const double x = __dsub_rn(c[d], double(__ldg(base + d * m4 + p)));
-        const double sq = __dmul_rn(x, x);
-        s = (d == 0) ? sq : __dadd_rn(s, sq);
-      }
-      hit = s <= R;
-    }
-    if (__any_sync(0xffffffffu, hit)) return true;
-  }
-  return false;
-}
-
 template <typename InT>
 __global__ void __launch_bounds__(kBlock)
     k_query_warp(DevTree t, const void* __restrict__ centers, const void* __restrict__ radii,
@@ -583,6 +526,10 @@ int query_device(const DevTree& t, const void* d_c, const void* d_r, int64_t n, 
   if (n == 0) return CAPT_OK;
   uint32_t fl = flags;
   if (!d_bad) fl &= ~CAPT_CHECK_RADII;
+  if (field_eligible(t, n, fl))
+    return launch_field(t, d_c, d_r, n, L, d_m, fl, d_bits, n_words, d_bad, s);
+  if (fl & CAPT_MODE_FIELD)
+    return fail(CAPT_EINVAL, "clearance-field pipeline unavailable for this tree/input");
   return binned_preferred(t, n, fl)
              ? launch_binned(t, d_c, d_r, n, L, d_m, fl, d_bits, n_words, d_bad, s)
              : launch_direct(t, d_c, d_r, n, L, d_m, fl, d_bits, n_words, d_cnt, d_bad, s);

@@ -311,7 +311,12 @@ int capt_tree_create(int device, int k, int64_t n, int64_t n_points, double r_mi
   cudaFree(d_lo);
   cudaFree(d_hi);
 #undef UPCHK
-  return CAPT_OK;
+  rc = build_field(t, s);
+  if (rc) {
+    capt_tree_destroy(t);
+    *out = nullptr;
+  }
+  return rc;
 }
 
 int capt_tree_info_get(const capt_tree* t, capt_tree_info* info) {
@@ -373,6 +378,7 @@ void capt_tree_destroy(capt_tree* t) {
   cudaGetDevice(&cur);
   cudaSetDevice(t->device);
   cudaFree(t->slab);
+  if (t->field) cudaFree(t->field);
   cudaSetDevice(cur);
   delete t;
 }
@@ -404,7 +410,12 @@ int capt_tree_from_slab(int device, const void* dev_slab, int64_t bytes, void* s
     *out = nullptr;
     return cuda_fail(e, "copy slab");
   }
-  return CAPT_OK;
+  rc = build_field(*out, s);
+  if (rc) {
+    capt_tree_destroy(*out);
+    *out = nullptr;
+  }
+  return rc;
 }
 
 }  // extern "C"

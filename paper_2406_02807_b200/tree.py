@@ -189,6 +189,25 @@ class Capt:
     def device_bytes(self) -> int:
         return int(self._info.device_bytes)
 
+    def clearance_field(self, cells: bool = False):
+        """The tree's clearance field (include/capt_b200.h capt_tree_field):
+        a dict of its geometry, plus the (nz, ny, nx, 4) float32 records
+        {witness xyz, nn} when ``cells``; None for trees without one (k < 3)."""
+        info = _lib.CaptFieldInfo()
+        L = _lib.lib()
+        if L.capt_tree_field(self._h, C.byref(info), None) != _lib.CAPT_OK:
+            return None
+        out = dict(shape=(info.nz, info.ny, info.nx), n_cells=int(info.n_cells),
+                   lo=np.array(info.lo[:], np.float32), h=np.float32(info.h),
+                   box_lo=np.array(info.box_lo[:], np.float32),
+                   box_hi=np.array(info.box_hi[:], np.float32), rcap=np.float32(info.rcap))
+        if cells:
+            buf = np.empty((info.nz, info.ny, info.nx, 4), np.float32)
+            _lib.check(L.capt_tree_field(self._h, C.byref(info), buf.ctypes.data),
+                       "capt_tree_field")
+            out["cells"] = buf
+        return out
+
     # -- replication (multi-GPU) ---------------------------------------------
     def slab_tensor(self):
         """Zero-copy torch uint8 view of the position-independent device slab

@@ -1,0 +1,234 @@
+"""The clearance-field query pipeline (csrc/capt_field.cu) against the oracle.
+
+The field resolves most in-band spheres from a per-cell witness point and a
+certified nearest-point lower bound; everything else goes through the tree
+path.  Every case forces CAPT_MODE_FIELD and must equal the oracle's
+collides_many / group bits (query.py:184-219, 126-167) bit for bit; the field
+records themselves are checked against float64 nearest-neighbour distances."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_tree, load_golden
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2406_02807_b200")
+from paper_2406_02807_b200 import _lib  # noqa: E402
+from paper_2406_02807_b200 import workloads as W  # noqa: E402
+from paper_2406_02807_b200.query import _host_inputs, _host_query  # noqa: E402
+
+FIELD = _lib.MODE_FIELD
+# the undecided spheres go through the warp list kernel or the binned pipeline
+LIST = {"warp": FIELD | _lib.MODE_DIRECT, "binned": FIELD | _lib.MODE_BINNED}
+
+
+def upload(t):
+    return P.Capt(t["k"], t["n_points"], t["r_min"], t["r_max"], t["tests"], t["aff_lo"],
+                  t["aff_hi"], t["offsets"], t["aff_values"])
+
+
+def q(tree, c, r, L=1, mask=None, prefilter=True, check=False, mode=FIELD):
+    cc, rr, f64 = _host_inputs(tree, c, r)
+    bits, _, bad = _host_query(tree, cc, rr, f64, L, mask, prefilter, check, mode=mode)
+    return bits if not check else (bits, bad)
+
+
+def centres(f):
+    nz, ny, nx = f["shape"]
+    lo, h = f["lo"].astype(np.float64), np.float64(f["h"])
+    # fma((i + 0.5), h, lo) rounded once to fp32: the product is exact in fp64
+    ax = [np.float32((np.arange(n, dtype=np.float64) + 0.5) * h + lo[d])
+          for d, n in enumerate((nx, ny, nz))]
+    return ax
+
+
+def check_field(tree, cloud, sample=200000, seed=0):
+    from scipy.spatial import cKDTree
+    f = tree.clearance_field(cells=True)
+    assert f is not None
+    cells = f["cells"].reshape(-1, 4)
+    nz, ny, nx = f["shape"]
+    assert f["n_cells"] == nx * ny * nz <= int((1 << 21) * 1.05)
+    pts = np.unique(cloud.astype(np.float32), axis=0).astype(np.float64)
+    assert np.array_equal(f["box_lo"], cloud.min(0)) and np.array_equal(f["box_hi"], cloud.max(0))
+    ax = centres(f)
+    rng = np.random.default_rng(seed)
+    idx = np.arange(len(cells)) if len(cells) <= sample else rng.choice(len(cells), sample, False)
+    iz, rem = np.divmod(idx, ny * nx)
+    iy, ix = np.divmod(rem, nx)
+    x0 = np.stack([ax[0][ix], ax[1][iy], ax[2][iz]], 1).astype(np.float64)
+    nn, _ = cKDTree(pts).query(x0)
+    rec = cells[idx].astype(np.float64)
+    rcap = np.float64(f["rcap"])
+    # certified lower bound (one fp32 ulp of slack for the centre's double rounding here)
+    slack = 2.0 * np.spacing(np.abs(x0).max(1).astype(np.float32)).astype(np.float64)
+    assert np.all(rec[:, 3] <= nn + slack)
+    assert np.all(rec[:, 3] <= rcap)
+    # and tight where a witness exists: the witness is a cloud point at distance nn
+    has = np.isfinite(rec[:, 0])
+    assert np.all(rec[~has, 3] == np.float32(rcap))
+    assert np.all(nn[~has] > rcap * (1 - 1e-6))
+    near = nn < rcap * (1 - 1e-6)
+    assert np.all(has[near])
+    # (beyond rcap the witness is only the nearest point of the 27 buckets)
+    dw = np.linalg.norm(x0[near] - rec[near, :3], axis=1)
+    assert np.allclose(dw, nn[near], rtol=1e-5, atol=1e-7)
+    assert np.allclose(rec[near, 3], nn[near], rtol=1e-5, atol=1e-7)
+    wset = {tuple(p) for p in cloud.astype(np.float32)[:, :3].tolist()}
+    assert all(tuple(w) in wset for w in rec[has][:2000, :3].astype(np.float32).tolist())
+    return f
+
+
+def test_field_records_uploaded_and_built_trees():
+    z = load_golden("cfg0.npz")
+    t = golden_tree(z, "")
+    tree = upload(t)
+    check_field(tree, W.cfg0_cloud())
+    cloud = W.cfg1_cloud()
+    tree1 = P.construct(P.PointCloud(cloud), P.BuildParams(0.02, 0.08))
+    f = check_field(tree1, cloud)
+    assert f["h"] < 0.02  # about 2 M cells over the tabletop box
+    # replicated trees rebuild the same field from the slab
+    pytest.importorskip("torch")
+    t2 = P.Capt.from_slab(tree1.slab_tensor())
+    f2 = t2.clearance_field(cells=True)
+    assert np.array_equal(f2["cells"], tree1.clearance_field(cells=True)["cells"])
+
+
+@pytest.mark.parametrize("lp", ["warp", "binned"])
+def test_field_golden_masks_and_groups(lp):
+    z = load_golden("queries.npz")
+    for name in z["names"]:
+        pts = z[f"{name}/points"]
+        rmin, rmax = z[f"{name}/band"]
+        t = O.construct(pts, rmin, rmax)
+        if t["k"] != 3:
+            continue
+        tree = upload(t)
+        c, r = z[f"{name}/centers"], z[f"{name}/radii"]
+        n = len(r)
+        exp = np.unpackbits(z[f"{name}/mask"])[:n].astype(bool)
+        assert np.array_equal(q(tree, c, r, mode=LIST[lp]), exp), name
+        nopre = np.unpackbits(z[f"{name}/mask_nopre"])[:n].astype(bool)
+        assert np.array_equal(q(tree, c, r, prefilter=False, mode=LIST[lp]), nopre), name
+        lane = np.unpackbits(z[f"{name}/lane_mask"])[:n].astype(bool)
+        gb = np.unpackbits(z[f"{name}/group8"])[: n // 8].astype(bool)
+        assert np.array_equal(q(tree, c, r, 8, lane.astype(np.uint8), mode=LIST[lp]), gb), name
+
+
+def test_field_cfg0_golden_and_full_batch():
+    z = load_golden("cfg0.npz")
+    t = golden_tree(z, "")
+    tree = upload(t)
+    n = int(z["n_queries"][0])
+    c, r = W.cfg0_queries()
+    assert np.array_equal(q(tree, c[:n], r[:n]), np.unpackbits(z["mask"])[:n].astype(bool))
+    assert np.array_equal(q(tree, c, r), O.collides_many(t, c, r))
+    # the default (auto) path is the field pipeline for fp32 input
+    assert np.array_equal(P.collides_many(tree, c, r), O.collides_many(t, c, r))
+
+
+@pytest.mark.parametrize("lp", ["warp", "binned"])
+@pytest.mark.parametrize("L", [1, 2, 8, 32])
+def test_field_tabletop_groups_and_lane_masks(L, lp):
+    cloud = W.cfg1_cloud()
+    tree = P.construct(P.PointCloud(cloud), P.BuildParams(0.02, 0.08))
+    t = O.tree_from(tree)
+    c, r = W.cfg1_queries(cloud, n_groups=1 << 16, seed=11)
+    rng = np.random.default_rng(L)
+    mask = (rng.uniform(size=len(r)) > 0.2).astype(np.uint8)
+    exp = O.collides_groups(t, c, r, L, mask.astype(bool))
+    assert np.array_equal(q(tree, c, r, L, mask, mode=LIST[lp]), exp)
+    if L == 1:
+        assert np.array_equal(q(tree, c, r, mode=LIST[lp]), O.brute_collides_many(cloud, c, r))
+
+
+@pytest.mark.parametrize("lp", ["warp", "binned"])
+def test_field_tangent_spheres(lp):
+    # radius = the float32 image of the exact nearest-point distance, and one
+    # ulp either side: every sphere sits on the certificates' decision edge
+    from scipy.spatial import cKDTree
+    rng = np.random.default_rng(23)
+    pts = rng.uniform(0, 1, (4096, 3)).astype(np.float32)
+    t = O.construct(pts, 0.01, 0.08)
+    tree = upload(t)
+    n = 1 << 17
+    idx = rng.integers(0, len(pts), n)
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    r0 = rng.uniform(0.011, 0.079, n)
+    c = (pts[idx].astype(np.float64) + d * r0[:, None]).astype(np.float32)
+    nn, _ = cKDTree(pts.astype(np.float64)).query(c.astype(np.float64))
+    r = np.float32(nn)
+    for rr in (r, np.nextafter(r, np.float32(0)), np.nextafter(r, np.float32(1))):
+        rr = W.clamp_radii(rr.astype(np.float32), 0.01, 0.08)
+        exp = O.collides_many(t, c, rr)
+        got = q(tree, c, rr, mode=LIST[lp])
+        assert np.array_equal(got, exp)
+        assert np.array_equal(got, O.brute_collides_many(pts, c, rr))
+
+
+@pytest.mark.parametrize("lp", ["warp", "binned"])
+def test_field_edge_inputs(lp):
+    # out-of-band radii with check_radii=False (the reference's own semantics,
+    # not the brute-force ones), NaN radii, non-finite centres, centres far
+    # outside the cloud's box, a batch that is not a multiple of 32
+    rng = np.random.default_rng(31)
+    pts = rng.uniform(-1, 1, (5000, 3)).astype(np.float32)
+    t = O.construct(pts, 0.02, 0.08)
+    tree = upload(t)
+    n = 200003
+    c = rng.uniform(-1.3, 1.3, (n, 3)).astype(np.float32)
+    r = rng.uniform(0.0, 0.2, n).astype(np.float32)  # many outside [0.02, 0.08]
+    c[::997, 0] = np.nan
+    c[5::991, 2] = np.inf
+    c[7::983] = np.float32(1e30)
+    r[11::977] = np.nan
+    r[13::971] = np.inf
+    exp = O.collides_many(t, c, r)
+    assert np.array_equal(q(tree, c, r, mode=LIST[lp]), exp)
+    assert np.array_equal(q(tree, c, r, prefilter=False, mode=LIST[lp]), O.collides_many(t, c, r, False))
+    # check_radii: the first out-of-band index is reported (NaN is not flagged)
+    bits, bad = q(tree, c, r, check=True, mode=LIST[lp])
+    inb = (r.astype(np.float64) >= 0.02) & (r.astype(np.float64) <= 0.08)
+    flagged = ~inb & ~np.isnan(r)
+    assert bad == int(np.argmax(flagged))
+
+
+@pytest.mark.parametrize("lp", ["warp", "binned"])
+def test_field_dense_gaussians(lp):
+    cloud = W.cfg3_cloud(n=32768, n_comp=8, seed=5)
+    t = O.construct(cloud, 0.01, 0.1)
+    tree = upload(t)
+    check_field(tree, cloud, sample=50000)
+    c, r = W.cfg3_queries(1 << 19, seed=7)
+    assert np.array_equal(q(tree, c, r, mode=LIST[lp]), O.collides_many(t, c, r))
+
+
+@pytest.mark.parametrize("lp", ["warp", "binned"])
+def test_field_degenerate_clouds(lp):
+    # one point; a flat plane (zero z extent); duplicates; a line
+    rng = np.random.default_rng(3)
+    clouds = [np.array([[0.25, -0.5, 1.0]], np.float32),
+              np.c_[rng.uniform(-1, 1, (3000, 2)), np.zeros(3000)].astype(np.float32),
+              np.repeat(rng.uniform(0, 1, (500, 3)), 3, axis=0).astype(np.float32),
+              np.c_[np.linspace(0, 1, 2000), np.zeros(2000), np.zeros(2000)].astype(np.float32)]
+    for i, cloud in enumerate(clouds):
+        t = O.construct(cloud, 0.01, 0.05)
+        tree = upload(t)
+        check_field(tree, cloud, sample=20000)
+        lo, hi = cloud.min(0) - 0.1, cloud.max(0) + 0.1
+        c = rng.uniform(lo, hi, (100000, 3)).astype(np.float32)
+        r = W.clamp_radii(rng.uniform(0.01, 0.05, 100000).astype(np.float32), 0.01, 0.05)
+        assert np.array_equal(q(tree, c, r, mode=LIST[lp]), O.collides_many(t, c, r)), i
+        assert np.array_equal(q(tree, c, r, 8, mode=LIST[lp]), O.collides_groups(t, c, r, 8)), i
+
+
+def test_field_forced_mode_rejects_f64():
+    z = load_golden("cfg0.npz")
+    tree = upload(golden_tree(z, ""))
+    c, r = W.cfg0_queries(1024)
+    with pytest.raises(ValueError, match="clearance-field"):
+        q(tree, c.astype(np.float64) + 1e-12, r.astype(np.float64))
