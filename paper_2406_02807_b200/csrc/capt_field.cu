@@ -37,6 +37,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -71,6 +72,19 @@ __device__ __forceinline__ int cell_of(float c, float lo, float inv, int n) {
 // cell centre; the build and the query evaluate the same expression
 __device__ __forceinline__ float centre_of(int i, float h, float lo) {
   return __fmaf_rn(__fadd_rn(__int2float_rn(i), 0.5f), h, lo);
+}
+// field records stay in L2 while the sphere stream passes through it
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ float4 ldg_keep(const float4* p, uint64_t pol) {
+  float4 v;
+  asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p), "l"(pol));
+  return v;
 }
 __device__ __forceinline__ float d2_fma(float dx, float dy, float dz) {
   return fmaf(dz, dz, fmaf(dy, dy, dx * dx));
@@ -224,154 +238,223 @@ struct FieldArgs {
   float rlo_f, rhi_f;  // fp32 images of the double band edges
 };
 
-// K0: per sphere (V in flight per thread, inputs prefetched one iteration
-// ahead with evict-first loads):
-//   status 1 = hit, 0 = free / masked, 2 = the tree path decides.
-// In-band fp32 spheres with a finite centre are tested against
-//   (a) the cloud box: fp32 gap^2 > r^2 (1 + TAU) -> free (every point lies
-//       in the box; fp32 gap^2 has relative error < 5u);
-//   (b) the cell's witness: fp32 |c - w|^2 <= r^2 (1 - TAU) -> hit;
-//   (c) the cell's bound: nn > fl(fl(r + e) (1 + 2^-20)), e = sqrtf(fp32
-//       |c - x0|^2) -> free.  e overestimates nothing by more than 3.6u
-//       relative, the sum and product lose <= 2u, so nn > (r + |c - x0|)
-//       (1 + 10u) and dist(c, cloud) >= nn - |c - x0| > r (1 + 10u): every
-//       float64 d^2 of the reference is > r*r.
-// Lane groups (L | 32) resolve on any definite hit (query.py:152-160); the
-// verdict bits are written directly (L = 1: one word per warp; L > 1: OR
-// into cleared words); unresolved spheres of unresolved groups are appended
-// to the list with one atomic per warp.
-template <int V>
+// K0.  A warp takes chunks of 128 consecutive spheres; lane l owns spheres
+// 4l .. 4l+3 of the chunk, so a chunk is three 128-bit centre loads and one
+// 128-bit radius load per lane (the next chunk is loaded while this one is
+// decided).  For an in-band sphere (r in [r_min, r_max] in double; NaN is
+// not) the verdict is certified without the tree (see the file comment):
+//   * outside the grid: the raw cell index leaves [0, n) on some axis, so the
+//     centre is more than r_max + h from the cloud's box -> free (this also
+//     takes +-inf centres: the float64 distances are infinite, no collision);
+//   * hit: fp32 |c - w|^2 <= r^2 (1 - TAU) for the cell's witness w;
+//   * free: with e2 = fp32 |c - x0|^2 and A = fma(-r, 1 + 2^-20, nn):
+//     A > 0 and A*A > e2 (1 + 2^-20).  fp32 e2 >= |c - x0|^2 (1 - 5u) and the
+//     products lose <= 3u, so nn - r (1 + 16u) > |c - x0| (1 + 3u) and
+//     dist(c, cloud) >= nn - |c - x0| > r (1 + 16u): every float64 d^2 of the
+//     reference exceeds r*r.
+// Everything else (NaN centres, out-of-band radii with check_radii=False,
+// spheres near |dist - r| ~ h) is undecided.  Lane groups (L | 32) resolve on
+// any definite hit (query.py:152-160); verdict bits are written directly
+// (L <= 4: whole words; L >= 8: OR into cleared words); the undecided
+// spheres of unresolved groups are appended to the list in sphere order (a
+// group's spheres stay contiguous) with one atomic per warp and chunk.
+constexpr float kK1 = 1.0f + 0x1p-20f;
+
+struct Chunk {
+  float4 p0, p1, p2, pr;  // xyz of 4 consecutive spheres in 3 float4, their radii
+};
+
+template <bool kVec>
+__device__ __forceinline__ Chunk load_chunk(const float* __restrict__ cf,
+                                            const float* __restrict__ rf, int c, int lane, int n) {
+  Chunk k;
+  const int q0 = (c << 7) + 4 * lane;
+  if (kVec && (c << 7) + 128 <= n) {
+    const float4* c4 = reinterpret_cast<const float4*>(cf + 3 * size_t(q0));
+    k.p0 = __ldcs(c4);
+    k.p1 = __ldcs(c4 + 1);
+    k.p2 = __ldcs(c4 + 2);
+    k.pr = __ldcs(reinterpret_cast<const float4*>(rf + q0));
+  } else {
+    float t[12], u[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int q = q0 + v < n ? q0 + v : 0;
+      t[3 * v] = __ldcs(cf + 3 * size_t(q));
+      t[3 * v + 1] = __ldcs(cf + 3 * size_t(q) + 1);
+      t[3 * v + 2] = __ldcs(cf + 3 * size_t(q) + 2);
+      u[v] = __ldcs(rf + q);
+    }
+    k.p0 = make_float4(t[0], t[1], t[2], t[3]);
+    k.p1 = make_float4(t[4], t[5], t[6], t[7]);
+    k.p2 = make_float4(t[8], t[9], t[10], t[11]);
+    k.pr = make_float4(u[0], u[1], u[2], u[3]);
+  }
+  return k;
+}
+
+// Decide one chunk (see above): writes its bits and list entries.  LT: the
+// lane width when known at compile time (0: a.L at run time).
+template <bool kMask, int LT>
+__device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeom& g,
+                                              const Chunk& k, int ch, int lane, bool check,
+                                              uint64_t pol) {
+  const float x[4] = {k.p0.x, k.p0.w, k.p1.z, k.p2.y};
+  const float y[4] = {k.p0.y, k.p1.x, k.p1.w, k.p2.z};
+  const float z[4] = {k.p0.z, k.p1.y, k.p2.x, k.p2.w};
+  const float r[4] = {k.pr.x, k.pr.y, k.pr.z, k.pr.w};
+  const int n = a.n;
+  const int q0 = (ch << 7) + 4 * lane;
+  const unsigned nxu = unsigned(g.nx), nyu = unsigned(g.ny), nzu = unsigned(g.nz);
+  // phase 1: validity, band, cells; all four record loads in flight
+  bool valid[4], inband[4], look[4];
+  unsigned ix[4], iy[4], iz[4];
+  float4 rec[4];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    valid[v] = q0 + v < n;
+    if (kMask) valid[v] = valid[v] && a.mask[valid[v] ? q0 + v : 0] != 0;
+    inband[v] = r[v] >= a.rlo_f && r[v] <= a.rhi_f;
+    const int fx = __float2int_rd(__fmul_rn(__fsub_rn(x[v], g.lo[0]), g.inv_h));
+    const int fy = __float2int_rd(__fmul_rn(__fsub_rn(y[v], g.lo[1]), g.inv_h));
+    const int fz = __float2int_rd(__fmul_rn(__fsub_rn(z[v], g.lo[2]), g.inv_h));
+    const bool in = unsigned(fx) < nxu && unsigned(fy) < nyu && unsigned(fz) < nzu;
+    ix[v] = min(unsigned(fx), nxu - 1);
+    iy[v] = min(unsigned(fy), nyu - 1);
+    iz[v] = min(unsigned(fz), nzu - 1);
+    look[v] = valid[v] && inband[v] && in;
+    rec[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (look[v]) rec[v] = ldg_keep(a.t.field + ((iz[v] * nyu + iy[v]) * nxu + ix[v]), pol);
+  }
+  // phase 2: the certificates
+  unsigned hitb = 0, undb = 0, badb = 0;
+  const float band_lo = 1.0f - kTau;
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const float ex = x[v] - centre_of(int(ix[v]), g.h, g.lo[0]);
+    const float ey = y[v] - centre_of(int(iy[v]), g.h, g.lo[1]);
+    const float ez = z[v] - centre_of(int(iz[v]), g.h, g.lo[2]);
+    const float e2 = d2_fma(ex, ey, ez);
+    const float r2 = r[v] * r[v];
+    const bool hit = d2_fma(x[v] - rec[v].x, y[v] - rec[v].y, z[v] - rec[v].z) <= r2 * band_lo;
+    const float A = fmaf(-r[v], kK1, rec[v].w);
+    const bool free = A > 0.f && A * A > e2 * kK1;
+    hitb |= unsigned(look[v] && hit) << v;
+    // decided: in-band and (outside the grid, or certified); with check_radii
+    // an out-of-band (non-NaN) radius only reports first_bad
+    const bool bad = valid[v] && (r[v] < a.rlo_f || r[v] > a.rhi_f);
+    badb |= unsigned(bad) << v;
+    const bool decided = inband[v] && (!look[v] || hit || free);
+    undb |= unsigned(valid[v] && !decided && !(check && bad)) << v;
+  }
+  if (check && __any_sync(0xffffffffu, badb != 0)) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+      if ((badb >> v) & 1u) atomicMin(a.first_bad, static_cast<unsigned long long>(q0 + v));
+  }
+  const int L = LT ? LT : a.L;
+  // lane groups: a group with a hit is resolved
+  unsigned resb;  // spheres of this lane whose group has a hit
+  if (L == 1) {
+    resb = hitb;
+  } else if (L == 2) {
+    const unsigned p = (hitb | (hitb >> 1)) & 5u;
+    resb = p | (p << 1);
+  } else if (L == 4) {
+    resb = hitb ? 15u : 0u;
+  } else {
+    bool any = hitb != 0;
+    for (int o = 1; o < L / 4; o <<= 1) any |= __shfl_xor_sync(0xffffffffu, any, o);
+    resb = any ? 15u : 0u;
+  }
+  // verdict bits
+  if (L == 1) {
+    unsigned w = hitb << (4 * (lane & 7));
+    w |= __shfl_xor_sync(0xffffffffu, w, 1);
+    w |= __shfl_xor_sync(0xffffffffu, w, 2);
+    w |= __shfl_xor_sync(0xffffffffu, w, 4);
+    const int word = (ch << 2) + (lane >> 3);
+    if ((lane & 7) == 0 && (word << 5) < n) a.bits[word] = w;
+  } else if (L == 2) {
+    unsigned w = ((resb & 1u) | ((resb >> 1) & 2u)) << (2 * (lane & 15));
+    w |= __shfl_xor_sync(0xffffffffu, w, 1);
+    w |= __shfl_xor_sync(0xffffffffu, w, 2);
+    w |= __shfl_xor_sync(0xffffffffu, w, 4);
+    w |= __shfl_xor_sync(0xffffffffu, w, 8);
+    const int word = (ch << 1) + (lane >> 4);
+    if ((lane & 15) == 0 && (word << 6) < n) a.bits[word] = w;
+  } else if (L == 4) {
+    const unsigned w = __ballot_sync(0xffffffffu, resb != 0);
+    if (lane == 0) a.bits[ch] = w;
+  } else {
+    // one bit per L/4 lanes: keep every (L/4)-th ballot bit, compress
+    const int st = L >> 2;
+    const unsigned w = __ballot_sync(0xffffffffu, resb != 0 && (lane & (st - 1)) == 0);
+    unsigned outw = 0;
+    for (int j = 0; j < 32 / st; ++j) outw |= ((w >> (j * st)) & 1u) << j;
+    const int g0 = (ch << 7) / L;  // first group of the chunk
+    if (lane == 0 && outw) atomicOr(a.bits + (g0 >> 5), outw << (g0 & 31));
+  }
+  // the list, in sphere order
+  const unsigned lst = undb & ~resb;
+  const unsigned has = __ballot_sync(0xffffffffu, lst != 0);
+  if (has) {
+    const int cnt = __popc(lst);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(a.list_n, unsigned(tot));
+    base = __shfl_sync(0xffffffffu, base, 0) + unsigned(incl - cnt);
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+      if ((lst >> v) & 1u) a.list[base + __popc(lst & ((1u << v) - 1u))] = uint32_t(q0 + v);
+  }
+}
+
+// persistent warps over 128-sphere chunks, two chunks per round (ping-pong
+// registers: the next chunk's loads are in flight while one is decided)
+template <bool kVec, bool kMask, int LT>
 __global__ void __launch_bounds__(256) k_resolve(FieldArgs a) {
   const FieldGeom g = a.t.fg;
-  const float4* __restrict__ field = a.t.field;
-  const float* __restrict__ cf = a.c;
-  const float* __restrict__ rf = a.r;
   const bool check = a.flags & CAPT_CHECK_RADII;
   const int n = a.n;
-  const int n_pad = (n + 31) & ~31;
   const int lane = threadIdx.x & 31;
-  const int L = a.L;
-  const unsigned seg = L >= 32 ? 0xffffffffu : ((1u << L) - 1u) << ((lane / L) * L);
-  const float band_lo = 1.0f - kTau, band_hi = 1.0f + kTau;
-  const int stride = gridDim.x * blockDim.x * V;
-  float nx[V], ny[V], nz[V], nr[V];
-#pragma unroll
-  for (int v = 0; v < V; ++v) {
-    const int q = blockIdx.x * blockDim.x * V + v * blockDim.x + threadIdx.x;
-    const int qq = q < n ? q : 0;
-    nx[v] = __ldcs(cf + 3 * qq);
-    ny[v] = __ldcs(cf + 3 * qq + 1);
-    nz[v] = __ldcs(cf + 3 * qq + 2);
-    nr[v] = __ldcs(rf + qq);
-  }
-  for (int base = blockIdx.x * blockDim.x * V; base < n_pad; base += stride) {
-    float cx[V], cy[V], cz[V], r[V];
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      cx[v] = nx[v];
-      cy[v] = ny[v];
-      cz[v] = nz[v];
-      r[v] = nr[v];
-      const int qn = base + stride + v * blockDim.x + threadIdx.x;
-      const int qq = qn < n ? qn : 0;
-      nx[v] = __ldcs(cf + 3 * qq);
-      ny[v] = __ldcs(cf + 3 * qq + 1);
-      nz[v] = __ldcs(cf + 3 * qq + 2);
-      nr[v] = __ldcs(rf + qq);
-    }
-    int st[V];
-    bool bad_any = false;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const int q = base + v * blockDim.x + threadIdx.x;
-      bool valid = q < n;
-      if (a.mask && valid) valid = a.mask[q] != 0;
-      const bool inband = r[v] >= a.rlo_f && r[v] <= a.rhi_f;  // false for NaN
-      // the reference's band check (query.py:194-197) does not flag NaN
-      const bool bad = check && valid && (r[v] < a.rlo_f || r[v] > a.rhi_f);
-      bad_any |= bad;
-      const float r2 = r[v] * r[v];
-      const bool cfin = isfinite(cx[v]) && isfinite(cy[v]) && isfinite(cz[v]);
-      const bool elig = valid && inband && cfin && r2 >= kR2Min && r2 <= kR2Max;
-      // (a) the cloud box
-      const float gx = fmaxf(fmaxf(g.blo[0] - cx[v], 0.f), cx[v] - g.bhi[0]);
-      const float gy = fmaxf(fmaxf(g.blo[1] - cy[v], 0.f), cy[v] - g.bhi[1]);
-      const float gz = fmaxf(fmaxf(g.blo[2] - cz[v], 0.f), cz[v] - g.bhi[2]);
-      const bool boxfree = d2_fma(gx, gy, gz) > r2 * band_hi;
-      int s = (!valid || bad) ? 0 : 2;
-      if (elig && !boxfree) {
-        const int ix = cell_of(cx[v], g.lo[0], g.inv_h, g.nx);
-        const int iy = cell_of(cy[v], g.lo[1], g.inv_h, g.ny);
-        const int iz = cell_of(cz[v], g.lo[2], g.inv_h, g.nz);
-        const float4 rec = __ldg(field + (iz * g.ny + iy) * g.nx + ix);
-        // (b) the witness
-        const bool hit = d2_fma(cx[v] - rec.x, cy[v] - rec.y, cz[v] - rec.z) <= r2 * band_lo;
-        // (c) the Lipschitz bound from the cell centre
-        const float ex = cx[v] - centre_of(ix, g.h, g.lo[0]);
-        const float ey = cy[v] - centre_of(iy, g.h, g.lo[1]);
-        const float ez = cz[v] - centre_of(iz, g.h, g.lo[2]);
-        const float e = sqrtf(d2_fma(ex, ey, ez));
-        const bool free = rec.w > __fmul_rn(__fadd_rn(r[v], e), kFreeMargin);
-        s = hit ? 1 : (free ? 0 : 2);
-      } else if (elig) {
-        s = 0;
-      }
-      st[v] = s;
-    }
-    if (check && __any_sync(0xffffffffu, bad_any)) {
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const int q = base + v * blockDim.x + threadIdx.x;
-        bool valid = q < n;
-        if (a.mask && valid) valid = a.mask[q] != 0;
-        if (valid && (r[v] < a.rlo_f || r[v] > a.rhi_f))
-          atomicMin(a.first_bad, static_cast<unsigned long long>(q));
-      }
-    }
-    // verdict bits and lane-group resolution
-    unsigned act[V], tot = 0;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const unsigned hm = __ballot_sync(0xffffffffu, st[v] == 1);
-      const int qw = base + v * blockDim.x + (threadIdx.x & ~31);  // first sphere of the warp
-      if (L == 1) {
-        if (lane == 0 && qw < n) a.bits[qw >> 5] = hm;
-      } else {
-        unsigned gb = 0;
-        const unsigned gmask = L >= 32 ? 0xffffffffu : (1u << L) - 1u;
-        for (int j = 0; j < 32 / L; ++j)
-          if ((hm >> (j * L)) & gmask) gb |= 1u << j;
-        const int g0 = qw / L;
-        if (lane == 0 && gb) atomicOr(a.bits + (g0 >> 5), gb << (g0 & 31));
-      }
-      const bool resolved = (hm & seg) != 0;
-      act[v] = __ballot_sync(0xffffffffu, st[v] == 2 && !resolved);
-      tot += __popc(act[v]);
-    }
-    if (tot) {
-      unsigned j = 0;
-      if (lane == 0) j = atomicAdd(a.list_n, tot);
-      j = __shfl_sync(0xffffffffu, j, 0);
-      const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        if ((act[v] >> lane) & 1u)
-          a.list[j + __popc(act[v] & lt)] = uint32_t(base + v * blockDim.x + threadIdx.x);
-        j += __popc(act[v]);
-      }
-    }
+  const int nchunks = (n + 127) >> 7;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  int ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (ch >= nchunks) return;
+  const uint64_t pol = l2_keep_policy();
+  Chunk A = load_chunk<kVec>(a.c, a.r, ch, lane, n), B;
+  while (true) {
+    const int c1 = ch + nwarps;
+    if (c1 < nchunks) B = load_chunk<kVec>(a.c, a.r, c1, lane, n);
+    resolve_chunk<kMask, LT>(a, g, A, ch, lane, check, pol);
+    if (c1 >= nchunks) break;
+    const int c2 = c1 + nwarps;
+    if (c2 < nchunks) A = load_chunk<kVec>(a.c, a.r, c2, lane, n);
+    resolve_chunk<kMask, LT>(a, g, B, c1, lane, check, pol);
+    if (c2 >= nchunks) break;
+    ch = c2;
   }
 }
 
 // The tree path over the list (the reference's semantics for every sphere it
-// holds): per thread descent (top levels from shared memory), the leaf's
-// probe record (conservative AABB reject, representative probe), then each
-// warp scans the sets of its unresolved spheres one after the other,
-// cooperatively (fp32 with the float64 re-scan of the band).  A list entry's
-// lane group is recovered with __match_any_sync on q / L (K0 appends a
-// group's spheres contiguously); a hit resolves the group's other entries.
+// holds).  The list is short but its spheres are the hard ones, so the kernel
+// is built for short dependent-load chains: a warp takes 8 entries; lanes 0-7
+// descend (top levels from shared memory), load the leaf's probe record
+// (conservative AABB reject, representative probe); then 4 lanes per entry
+// scan its set, 64 points per step (12 128-bit loads in flight per lane),
+// fp32 with the float64 re-scan of the band.  (One entry per lane with a
+// serial warp scan, or a per-thread scan, measured ~73 us for config 1's 85 K
+// entries: the warp waits on its longest chain.)
 constexpr int kListSmemLevels = 11;
 constexpr int kListSmem = (1 << kListSmemLevels) - 1;
+constexpr int kLE = 8;  // list entries per warp
 
 __global__ void __launch_bounds__(256) k_resolve_list(FieldArgs a) {
   __shared__ float sT[kListSmem];
@@ -381,14 +464,15 @@ __global__ void __launch_bounds__(256) k_resolve_list(FieldArgs a) {
   __syncthreads();
   const uint32_t n_list = *a.list_n;
   const int lane = threadIdx.x & 31;
+  const int slot = lane >> 2, sl = lane & 3;
   const int L = a.L;
   const bool prefilter = a.flags & CAPT_PREFILTER;
   const float band_lo = 1.0f - kTau, band_hi = 1.0f + kTau;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t j0 = warp * 32; j0 < n_list; j0 += nwarps * 32) {
+  for (uint32_t j0 = warp * kLE; j0 < n_list; j0 += nwarps * kLE) {
     const uint32_t j = j0 + lane;
-    const bool active = j < n_list;
+    const bool active = lane < kLE && j < n_list;
     const uint32_t q = active ? a.list[j] : 0u;
     float cx = 0.f, cy = 0.f, cz = 0.f, r = 0.f;
     if (active) {
@@ -399,58 +483,93 @@ __global__ void __launch_bounds__(256) k_resolve_list(FieldArgs a) {
     }
     const uint32_t gid = active ? q / uint32_t(L) : 0xffffffffu - lane;
     const unsigned gm = L > 1 ? __match_any_sync(0xffffffffu, gid) : (1u << lane);
-    // descent (tree.py:266-273)
-    int i = 0, s = 0;
-    for (; s < t.depth; ++s) {
-      const int ax = s % 3;
-      const float cv = ax == 0 ? cx : (ax == 1 ? cy : cz);
-      const float tv = i < n_smem ? sT[i] : __ldg(t.T + i);
-      i = 2 * i + 1 + (cv > tv ? 1 : 0);
+    int st = 0, leaf = 0;
+    bool verdict = false;
+    float r2 = 0.f;
+    if (active) {
+      // descent (tree.py:266-273)
+      int i = 0;
+      for (int s = 0; s < t.depth; ++s) {
+        const int ax = s % 3;
+        const float cv = ax == 0 ? cx : (ax == 1 ? cy : cz);
+        const float tv = i < n_smem ? sT[i] : __ldg(t.T + i);
+        i = 2 * i + 1 + (cv > tv ? 1 : 0);
+      }
+      leaf = i - int(t.n - 1);
+      // classification (as k_bin_count3 / k_query_hybrid)
+      r2 = r * r;
+      const bool cfin = isfinite(cx) && isfinite(cy) && isfinite(cz);
+      const bool fast = cfin && r2 >= kR2Min && r2 <= kR2Max;
+      st = fast ? 2 : ((!cfin && isfinite(r)) ? 0 : 3);
+      float pr[8];
+      ld_v8(t.probe + 8 * leaf, pr);
+      if (prefilter) {
+        const float2 l01 = h2f2(pr[3]), l2h0 = h2f2(pr[4]), h12 = h2f2(pr[5]);
+        const float rx = fmaxf(fmaxf(l01.x - cx, 0.f), cx - l2h0.y);
+        const float ry = fmaxf(fmaxf(l01.y - cy, 0.f), cy - h12.x);
+        const float rz = fmaxf(fmaxf(l2h0.x - cz, 0.f), cz - h12.y);
+        st = (fast && d2_fma(rx, ry, rz) > r2 * band_hi) ? 0 : st;
+      }
+      verdict = st == 2 && d2_fma(cx - pr[0], cy - pr[1], cz - pr[2]) <= r2 * band_lo;
     }
-    const int leaf = i - int(t.n - 1);
-    // classification (as k_bin_count3 / k_query_hybrid)
-    const float r2 = r * r;
-    const bool cfin = isfinite(cx) && isfinite(cy) && isfinite(cz);
-    const bool fast = cfin && r2 >= kR2Min && r2 <= kR2Max;
-    int st = fast ? 2 : ((!cfin && isfinite(r)) ? 0 : 3);
-    st = active ? st : 0;
-    float pr[8];
-    ld_v8(t.probe + 8 * leaf, pr);
-    if (prefilter) {
-      const float2 l01 = h2f2(pr[3]), l2h0 = h2f2(pr[4]), h12 = h2f2(pr[5]);
-      const float rx = fmaxf(fmaxf(l01.x - cx, 0.f), cx - l2h0.y);
-      const float ry = fmaxf(fmaxf(l01.y - cy, 0.f), cy - h12.x);
-      const float rz = fmaxf(fmaxf(l2h0.x - cz, 0.f), cz - h12.y);
-      st = (fast && d2_fma(rx, ry, rz) > r2 * band_hi) ? 0 : st;
-    }
-    bool verdict = st == 2 && d2_fma(cx - pr[0], cy - pr[1], cz - pr[2]) <= r2 * band_lo;
     const unsigned hitm = __ballot_sync(0xffffffffu, verdict);
-    unsigned todo = __ballot_sync(0xffffffffu, (st == 2 || st == 3) && !verdict);
-    todo &= ~__ballot_sync(0xffffffffu, (hitm & gm) != 0);
-    while (todo) {
-      const int src = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const float sx = __shfl_sync(0xffffffffu, cx, src);
-      const float sy = __shfl_sync(0xffffffffu, cy, src);
-      const float sz = __shfl_sync(0xffffffffu, cz, src);
-      const float sr = __shfl_sync(0xffffffffu, r, src);
-      const int sst = __shfl_sync(0xffffffffu, st, src);
-      const int sleaf = __shfl_sync(0xffffffffu, leaf, src);
-      const unsigned sgm = __shfl_sync(0xffffffffu, gm, src);
-      const uint2 set = __ldg(t.set + sleaf);
-      int v = 2;
-      if (sst == 2) {
-        const float sr2 = sr * sr;
-        v = warp_scan_f32(t, set, sx, sy, sz, sr2 * band_lo, sr2 * band_hi, lane);
+    const bool scan = (st == 2 || st == 3) && !verdict && (hitm & gm) == 0;
+    uint2 set = make_uint2(0u, 0u);
+    if (scan) set = __ldg(t.set + leaf);
+    // the scan: slot k (lanes 4k .. 4k+3) takes entry k's set
+    const float sx = __shfl_sync(0xffffffffu, cx, slot);
+    const float sy = __shfl_sync(0xffffffffu, cy, slot);
+    const float sz = __shfl_sync(0xffffffffu, cz, slot);
+    const float sr2 = __shfl_sync(0xffffffffu, r2, slot);
+    const bool sf = __shfl_sync(0xffffffffu, scan && st == 2, slot);
+    const uint32_t sset = __shfl_sync(0xffffffffu, set.x, slot);
+    const uint32_t sy_m = __shfl_sync(0xffffffffu, set.y, slot);
+    const uint32_t sm = sf ? sy_m : 0u;
+    const uint32_t m4 = (sm + 3u) & ~3u;
+    const float* base = reinterpret_cast<const float*>(t.data + sset);
+    const float loB = sr2 * band_lo, hiB = sr2 * band_hi;
+    uint32_t mmax = m4;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
+    bool hit = false, amb = false;
+    for (uint32_t p0 = 0; p0 < mmax; p0 += 64) {
+      if (!hit) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t p = p0 + 16 * u + 4 * sl;
+          if (p < m4) {
+            const float4 px = __ldg(reinterpret_cast<const float4*>(base + p));
+            const float4 py = __ldg(reinterpret_cast<const float4*>(base + m4 + p));
+            const float4 pz = __ldg(reinterpret_cast<const float4*>(base + 2 * m4 + p));
+            const float xs[4] = {px.x, px.y, px.z, px.w}, ys[4] = {py.x, py.y, py.z, py.w},
+                        zs[4] = {pz.x, pz.y, pz.z, pz.w};
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              const float d2 = d2_fma(sx - xs[w], sy - ys[w], sz - zs[w]);
+              hit |= d2 <= loB;
+              amb |= d2 < hiB;
+            }
+          }
+        }
       }
-      bool hit = v == 1;
-      if (v == 2) {
-        const double c64[3] = {sx, sy, sz};
-        hit = warp_scan_f64(t, set, c64, double(sr), lane);
-      }
-      if (hit) {
-        if (lane == src) verdict = true;
-        todo &= ~sgm;
+      // a slot stops at its first hit (its 4 lanes agree after the vote)
+      const unsigned hb = __ballot_sync(0xffffffffu, hit);
+      hit = (hb >> (4 * slot)) & 15u;
+      const unsigned live = __ballot_sync(0xffffffffu, !hit && p0 + 64 < m4);
+      if (!live) break;
+    }
+    const unsigned hb = __ballot_sync(0xffffffffu, hit);
+    const unsigned ab = __ballot_sync(0xffffffffu, amb);
+    if (scan) {
+      if (st == 2) {
+        verdict = (hb >> (4 * lane)) & 15u;
+        if (!verdict && ((ab >> (4 * lane)) & 15u)) {
+          const double c64[3] = {cx, cy, cz};
+          verdict = scan_f64(t, set, c64, double(r), nullptr);
+        }
+      } else {  // st == 3: the exact path only
+        const double c64[3] = {cx, cy, cz};
+        verdict = scan_f64(t, set, c64, double(r), nullptr);
       }
     }
     // one OR per hit sphere (L = 1) or per group (first hitting lane)
@@ -587,6 +706,8 @@ int build_field(capt_tree* tree, cudaStream_t s) {
 bool field_eligible(const DevTree& t, int64_t n, uint32_t flags) {
   if (!t.field || t.k != 3 || (flags & (CAPT_INPUT_F64 | CAPT_STATS))) return false;
   if (n >= (int64_t(1) << 31) - (int64_t(1) << 24)) return false;
+  // fp32 r^2 of every in-band radius must stay normal and finite
+  if (!(t.r_min >= 0x1p-50) || !(t.r_max <= 0x1p50)) return false;
   if (flags & CAPT_MODE_FIELD) return true;  // (+ MODE_BINNED / MODE_DIRECT: the list path)
   return !(flags & (CAPT_MODE_DIRECT | CAPT_MODE_BINNED | CAPT_MODE_THREAD | CAPT_MODE_WARP));
 }
@@ -612,9 +733,16 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   CAPT_CUDA(dmalloc(&a.list_n, 1, s));
   CAPT_CUDA(dmalloc(&a.list, n, s));
   CAPT_CUDA(cudaMemsetAsync(a.list_n, 0, 4, s));
-  if (L > 1) CAPT_CUDA(cudaMemsetAsync(bits, 0, 4 * (n_words ? n_words : 1), s));
-  constexpr int V = 4;
-  k_resolve<V><<<grid_for((n + V - 1) / V, 256, 8), 256, 0, s>>>(a);
+  if (L >= 8) CAPT_CUDA(cudaMemsetAsync(bits, 0, 4 * (n_words ? n_words : 1), s));
+  const bool vec = (reinterpret_cast<uintptr_t>(centers) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(radii) & 15) == 0;
+  const int grid = grid_for(((n + 127) / 128) * 32, 256, 8);
+  // specialised for unmasked fp32 batches of single spheres and 8-sphere
+  // groups (configs 0-4); everything else takes the generic instantiation
+  if (vec && !mask && L == 1) k_resolve<true, false, 1><<<grid, 256, 0, s>>>(a);
+  else if (vec && !mask && L == 8) k_resolve<true, false, 8><<<grid, 256, 0, s>>>(a);
+  else if (mask) k_resolve<false, true, 0><<<grid, 256, 0, s>>>(a);
+  else k_resolve<false, false, 0><<<grid, 256, 0, s>>>(a);
   CAPT_CUDA(cudaGetLastError());
   note_launches(1);
   // the list: one warp-cooperative kernel, or -- for large batches over large
@@ -635,9 +763,17 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
     rc = launch_binned(t, centers, radii, n, L, nullptr, flags, bits, n_words, first_bad, s,
                        a.list, a.list_n);
   } else {
-    k_resolve_list<<<grid_for(int64_t(1) << 30, 256, 4), 256, 0, s>>>(a);
+    k_resolve_list<<<grid_for(int64_t(1) << 30, 256, 8), 256, 0, s>>>(a);
     CAPT_CUDA(cudaGetLastError());
     note_launches(1);
+  }
+  static const bool debug = getenv("CAPT_DEBUG") != nullptr;
+  if (debug) {
+    uint32_t nl = 0;
+    CAPT_CUDA(cudaMemcpyAsync(&nl, a.list_n, 4, cudaMemcpyDeviceToHost, s));
+    CAPT_CUDA(cudaStreamSynchronize(s));
+    fprintf(stderr, "[capt field] n=%lld L=%d undecided=%u (%.3f%%) list=%s\n", (long long)n, L, nl,
+            100.0 * nl / double(n ? n : 1), binned ? "binned" : "thread");
   }
   cudaFreeAsync(a.list, s);
   cudaFreeAsync(a.list_n, s);
