@@ -70,8 +70,8 @@ __device__ __forceinline__ int cell_of(float c, float lo, float inv, int n) {
   return min(max(i, 0), n - 1);
 }
 // cell centre; the build and the query evaluate the same expression
-__device__ __forceinline__ float centre_of(int i, float h, float lo) {
-  return __fmaf_rn(__fadd_rn(__int2float_rn(i), 0.5f), h, lo);
+__device__ __forceinline__ float centre_of(int i, float h, float c0) {
+  return __fmaf_rn(__int2float_rn(i), h, c0);
 }
 // field records stay in L2 while the sphere stream passes through it
 __device__ __forceinline__ uint64_t l2_keep_policy() {
@@ -175,9 +175,9 @@ __global__ void __launch_bounds__(256, 1) k_field_nn(FieldGeom g, BucketGrid b,
     for (int k = 0; k < kCellsPerThread; ++k) {
       const int j = pass + k * 256 + threadIdx.x;
       const int lx = j % cx, ly = (j / cx) % cy, lz = j / (cx * cy);
-      px[k] = centre_of(x0 + lx, g.h, g.lo[0]);
-      py[k] = centre_of(y0 + ly, g.h, g.lo[1]);
-      pz[k] = centre_of(z0 + lz, g.h, g.lo[2]);
+      px[k] = centre_of(x0 + lx, g.h, g.c0[0]);
+      py[k] = centre_of(y0 + ly, g.h, g.c0[1]);
+      pz[k] = centre_of(z0 + lz, g.h, g.c0[2]);
       best[k] = INF;
       bi[k] = -1;
     }
@@ -294,8 +294,9 @@ __device__ __forceinline__ Chunk load_chunk(const float* __restrict__ cf,
 }
 
 // Decide one chunk (see above): writes its bits and list entries.  LT: the
-// lane width when known at compile time (0: a.L at run time).
-template <bool kMask, int LT>
+// lane width when known at compile time (0: a.L at run time); kFull: a whole
+// unmasked chunk (no per-sphere validity test).
+template <bool kMask, int LT, bool kFull>
 __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeom& g,
                                               const Chunk& k, int ch, int lane, bool check,
                                               uint64_t pol) {
@@ -308,32 +309,32 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
   const unsigned nxu = unsigned(g.nx), nyu = unsigned(g.ny), nzu = unsigned(g.nz);
   // phase 1: validity, band, cells; all four record loads in flight
   bool valid[4], inband[4], look[4];
-  unsigned ix[4], iy[4], iz[4];
+  int ix[4], iy[4], iz[4];
   float4 rec[4];
 #pragma unroll
   for (int v = 0; v < 4; ++v) {
-    valid[v] = q0 + v < n;
+    valid[v] = kFull || q0 + v < n;
     if (kMask) valid[v] = valid[v] && a.mask[valid[v] ? q0 + v : 0] != 0;
     inband[v] = r[v] >= a.rlo_f && r[v] <= a.rhi_f;
-    const int fx = __float2int_rd(__fmul_rn(__fsub_rn(x[v], g.lo[0]), g.inv_h));
-    const int fy = __float2int_rd(__fmul_rn(__fsub_rn(y[v], g.lo[1]), g.inv_h));
-    const int fz = __float2int_rd(__fmul_rn(__fsub_rn(z[v], g.lo[2]), g.inv_h));
-    const bool in = unsigned(fx) < nxu && unsigned(fy) < nyu && unsigned(fz) < nzu;
-    ix[v] = min(unsigned(fx), nxu - 1);
-    iy[v] = min(unsigned(fy), nyu - 1);
-    iz[v] = min(unsigned(fz), nzu - 1);
+    ix[v] = __float2int_rd(__fmul_rn(__fsub_rn(x[v], g.lo[0]), g.inv_h));
+    iy[v] = __float2int_rd(__fmul_rn(__fsub_rn(y[v], g.lo[1]), g.inv_h));
+    iz[v] = __float2int_rd(__fmul_rn(__fsub_rn(z[v], g.lo[2]), g.inv_h));
+    // (the index is used only inside the grid: no clamp)
+    const bool in = unsigned(ix[v]) < nxu && unsigned(iy[v]) < nyu && unsigned(iz[v]) < nzu;
     look[v] = valid[v] && inband[v] && in;
     rec[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (look[v]) rec[v] = ldg_keep(a.t.field + ((iz[v] * nyu + iy[v]) * nxu + ix[v]), pol);
+    if (look[v])
+      rec[v] = ldg_keep(a.t.field + ((unsigned(iz[v]) * nyu + unsigned(iy[v])) * nxu + unsigned(ix[v])),
+                        pol);
   }
   // phase 2: the certificates
   unsigned hitb = 0, undb = 0, badb = 0;
   const float band_lo = 1.0f - kTau;
 #pragma unroll
   for (int v = 0; v < 4; ++v) {
-    const float ex = x[v] - centre_of(int(ix[v]), g.h, g.lo[0]);
-    const float ey = y[v] - centre_of(int(iy[v]), g.h, g.lo[1]);
-    const float ez = z[v] - centre_of(int(iz[v]), g.h, g.lo[2]);
+    const float ex = x[v] - centre_of(ix[v], g.h, g.c0[0]);
+    const float ey = y[v] - centre_of(iy[v], g.h, g.c0[1]);
+    const float ez = z[v] - centre_of(iz[v], g.h, g.c0[2]);
     const float e2 = d2_fma(ex, ey, ez);
     const float r2 = r[v] * r[v];
     const bool hit = d2_fma(x[v] - rec[v].x, y[v] - rec[v].y, z[v] - rec[v].z) <= r2 * band_lo;
@@ -342,10 +343,10 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
     hitb |= unsigned(look[v] && hit) << v;
     // decided: in-band and (outside the grid, or certified); with check_radii
     // an out-of-band (non-NaN) radius only reports first_bad
-    const bool bad = valid[v] && (r[v] < a.rlo_f || r[v] > a.rhi_f);
+    const bool bad = check && valid[v] && (r[v] < a.rlo_f || r[v] > a.rhi_f);
     badb |= unsigned(bad) << v;
     const bool decided = inband[v] && (!look[v] || hit || free);
-    undb |= unsigned(valid[v] && !decided && !(check && bad)) << v;
+    undb |= unsigned(valid[v] && !decided && !bad) << v;
   }
   if (check && __any_sync(0xffffffffu, badb != 0)) {
 #pragma unroll
@@ -416,30 +417,43 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
   }
 }
 
-// persistent warps over 128-sphere chunks, two chunks per round (ping-pong
-// registers: the next chunk's loads are in flight while one is decided)
+// K0 CTAs per SM the register allocation must allow: config 1, 0.250 ms at 3
+// (78 registers) vs 0.254 at 4 (64, spills) and 0.302 unbounded
+#ifndef CAPT_K0_MINB
+#define CAPT_K0_MINB 3
+#endif
+
+// persistent warps over the whole 128-sphere chunks, two per round (ping-pong
+// registers: the next chunk's loads are in flight while one is decided); the
+// last, partial chunk (scalar loads, per-sphere validity) after the loop
 template <bool kVec, bool kMask, int LT>
-__global__ void __launch_bounds__(256) k_resolve(FieldArgs a) {
+__global__ void __launch_bounds__(256, CAPT_K0_MINB) k_resolve(FieldArgs a) {
   const FieldGeom g = a.t.fg;
   const bool check = a.flags & CAPT_CHECK_RADII;
   const int n = a.n;
   const int lane = threadIdx.x & 31;
-  const int nchunks = (n + 127) >> 7;
+  const int nfull = n >> 7;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  int ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (ch >= nchunks) return;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t pol = l2_keep_policy();
-  Chunk A = load_chunk<kVec>(a.c, a.r, ch, lane, n), B;
-  while (true) {
-    const int c1 = ch + nwarps;
-    if (c1 < nchunks) B = load_chunk<kVec>(a.c, a.r, c1, lane, n);
-    resolve_chunk<kMask, LT>(a, g, A, ch, lane, check, pol);
-    if (c1 >= nchunks) break;
-    const int c2 = c1 + nwarps;
-    if (c2 < nchunks) A = load_chunk<kVec>(a.c, a.r, c2, lane, n);
-    resolve_chunk<kMask, LT>(a, g, B, c1, lane, check, pol);
-    if (c2 >= nchunks) break;
-    ch = c2;
+  int ch = w0;
+  if (ch < nfull) {
+    Chunk A = load_chunk<kVec>(a.c, a.r, ch, lane, n), B;
+    while (true) {
+      const int c1 = ch + nwarps;
+      if (c1 < nfull) B = load_chunk<kVec>(a.c, a.r, c1, lane, n);
+      resolve_chunk<kMask, LT, !kMask>(a, g, A, ch, lane, check, pol);
+      if (c1 >= nfull) break;
+      const int c2 = c1 + nwarps;
+      if (c2 < nfull) A = load_chunk<kVec>(a.c, a.r, c2, lane, n);
+      resolve_chunk<kMask, LT, !kMask>(a, g, B, c1, lane, check, pol);
+      if (c2 >= nfull) break;
+      ch = c2;
+    }
+  }
+  if ((n & 127) && w0 == nfull % nwarps) {
+    const Chunk T = load_chunk<false>(a.c, a.r, nfull, lane, n);
+    resolve_chunk<kMask, LT, false>(a, g, T, nfull, lane, check, pol);
   }
 }
 
@@ -638,7 +652,10 @@ int build_field(capt_tree* tree, cudaStream_t s) {
   g.h = float(h);
   h = double(g.h);
   g.inv_h = float(1.0 / h);
-  for (int d = 0; d < 3; ++d) g.lo[d] = float(double(g.blo[d]) - (rmax + h));
+  for (int d = 0; d < 3; ++d) {
+    g.lo[d] = float(double(g.blo[d]) - (rmax + h));
+    g.c0[d] = float(double(g.lo[d]) + 0.5 * h);
+  }
   g.nx = int(dims[0]);
   g.ny = int(dims[1]);
   g.nz = int(dims[2]);
@@ -797,6 +814,7 @@ extern "C" int capt_tree_field(const capt_tree* tree, capt_field_info* info, flo
   info->rcap = g.rcap;
   for (int d = 0; d < 3; ++d) {
     info->lo[d] = g.lo[d];
+    info->c0[d] = g.c0[d];
     info->box_lo[d] = g.blo[d];
     info->box_hi[d] = g.bhi[d];
   }

@@ -58,12 +58,13 @@ struct SlabHeader {
 static_assert(sizeof(SlabHeader) <= 256, "header must fit its 256-B section");
 
 // Clearance field geometry (capt_field.cu): a uniform grid of nx*ny*nz cells
-// of edge h starting at lo; cell centre x0(i) = fma(i + 0.5, h, lo) per axis.
+// of edge h starting at lo; cell centre x0(i) = fma(i, h, c0) per axis.
 // blo/bhi = the cloud's box (finite representatives); rcap caps the stored
 // lower bounds.  field == nullptr: no field (k < 3, or not built).
 struct FieldGeom {
   int nx, ny, nz, m;   // cells per axis; bucket edge in cells (build only)
-  float lo[3];
+  float lo[3];         // grid origin: cell i spans lo + [i, i+1) h (cell_of)
+  float c0[3];         // centre of cell 0: x0(i) = fma(i, h, c0) exactly, build and query
   float h, inv_h;
   float blo[3], bhi[3];
   float rcap;

@@ -199,6 +199,7 @@ class Capt:
             return None
         out = dict(shape=(info.nz, info.ny, info.nx), n_cells=int(info.n_cells),
                    lo=np.array(info.lo[:], np.float32), h=np.float32(info.h),
+                   c0=np.array(info.c0[:], np.float32),
                    box_lo=np.array(info.box_lo[:], np.float32),
                    box_hi=np.array(info.box_hi[:], np.float32), rcap=np.float32(info.rcap))
         if cells:

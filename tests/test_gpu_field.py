@@ -37,9 +37,9 @@ def q(tree, c, r, L=1, mask=None, prefilter=True, check=False, mode=FIELD):
 
 def centres(f):
     nz, ny, nx = f["shape"]
-    lo, h = f["lo"].astype(np.float64), np.float64(f["h"])
-    # fma((i + 0.5), h, lo) rounded once to fp32: the product is exact in fp64
-    ax = [np.float32((np.arange(n, dtype=np.float64) + 0.5) * h + lo[d])
+    c0, h = f["c0"].astype(np.float64), np.float64(f["h"])
+    # fma(i, h, c0) rounded to fp32 (the product is exact in fp64)
+    ax = [np.float32(np.arange(n, dtype=np.float64) * h + c0[d])
           for d, n in enumerate((nx, ny, nz))]
     return ax
 
