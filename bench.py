@@ -168,20 +168,24 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def profiled_traffic(config):
-    """DRAM bytes (read + write) per query launch from the committed ncu
-    --set full capture of this bench command (profiles/r01_cfg<k>_ncu_full.json,
-    summed over the captured kernels), or (None, reason)."""
+def profiled_traffic(config, name="ncu_full", only=None):
+    """DRAM bytes (read + write) per launch from the committed ncu --set full
+    capture of this bench command (profiles/r01_cfg<k>_<name>.json, summed
+    over the captured kernels whose name contains ``only``), or (None, why)."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                        f"r01_cfg{config}_ncu_full.json")
+                        f"r01_cfg{config}_{name}.json")
     if not os.path.exists(path):
         return None, "no ncu capture committed for this config"
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     total, names = 0.0, []
     for k in json.load(open(path)):
+        if only and only not in k["kernel"]:
+            continue
         for f in ("dram_read", "dram_write"):
             total += float(k[f]) * scale.get(k.get(f + "_unit", "byte"), 1)
         names.append(k["kernel"].split("(")[0].split("::")[-1])
+    if not names:
+        return None, f"no {only} launch in {os.path.basename(path)}"
     return total, (f"{os.path.relpath(path, os.path.dirname(path) + '/..')}: dram read+write of "
                    f"{', '.join(names)} (one launch each)")
 
@@ -285,6 +289,8 @@ def main():
     launches0 = _lib.lib().capt_kernel_launches()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    import ctypes
+    _lib.lib().capt_stage_timing(1)  # events around K0 / the list stage, on `stream`
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
@@ -292,6 +298,10 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
     launches = _lib.lib().capt_kernel_launches() - launches0
+    st_ms = (ctypes.c_double * 3)()
+    st_calls = ctypes.c_int64(0)
+    _lib.check(_lib.lib().capt_stage_times(st_ms, ctypes.byref(st_calls)))
+    _lib.lib().capt_stage_timing(0)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -307,8 +317,13 @@ def main():
 
     value = world * n * args.steps / (ms_max * 1e-3)
 
-    # roofline: max(streamed bytes / HBM peak, 8 flop x counted tests / FP32 peak)
-    import ctypes
+    # roofline.  The survey's definition is the slower of the
+    # streamed bytes at HBM peak and 8 flop x the reference's counted distance
+    # tests at FP32 peak, against the step time.  The product resolves most
+    # spheres without any distance test (clearance field), so its dominant
+    # kernel K0 is bound by the sphere stream: the primary roofline is K0's
+    # algorithmic bytes (16 B/sphere in, the verdict words out) over its
+    # event-timed duration against HBM peak.
     peak_fp32 = ctypes.c_double(0.0)
     _lib.check(_lib.lib().capt_measure_fp32_peak(local, ctypes.byref(peak_fp32)))
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
@@ -319,20 +334,39 @@ def main():
     flops_step = FLOP_PER_TEST * tests
     t_hbm = bytes_step / (hbm_peak * 1e9)
     t_fp32 = flops_step / (peak_fp32.value * 1e12)
-    kernel_ms = ms / args.steps  # the query kernel is the whole step in direct mode
-    if t_fp32 >= t_hbm:
-        roof = {"bound": "fp32", "achieved": flops_step / (kernel_ms * 1e-3) / 1e12,
-                "peak": peak_fp32.value, "unit": "TFLOP/s"}
-    else:
-        roof = {"bound": "hbm", "achieved": bytes_step / (kernel_ms * 1e-3) / 1e9,
-                "peak": hbm_peak, "unit": "GB/s"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"], roof["traffic_source"] = profiled_traffic(args.config)
-    roof["peak_source"] = ("FP32: FFMA microbenchmark measured live (capt_measure_fp32_peak); "
-                           "HBM: MEASURED_PEAKS.json hbm_gbs")
-    roof["counted_tests_per_step"] = tests
-    roof["streamed_bytes_per_step"] = bytes_step
-    roof["roofline_ms"] = max(t_hbm, t_fp32) * 1e3
+    survey = {"definition": "max(streamed bytes / HBM peak, 8 flop x counted tests / FP32 peak) "
+                            "over the whole step (SURVEY 8d)",
+              "roofline_ms": max(t_hbm, t_fp32) * 1e3,
+              "frac": max(t_hbm, t_fp32) * 1e3 / ms_per_step,
+              "bound": "fp32" if t_fp32 >= t_hbm else "hbm",
+              "achieved_tflops": flops_step / (ms_per_step * 1e-3) / 1e12,
+              "fp32_peak_tflops": peak_fp32.value,
+              "counted_tests_per_step": tests, "streamed_bytes_per_step": bytes_step}
+    calls = int(st_calls.value)
+    if calls == args.steps:
+        k0_ms, list_ms = st_ms[0] / calls, st_ms[1] / calls
+        roof = {"bound": "hbm", "kernel": "k_resolve (K0: clearance-field resolve)",
+                "achieved": bytes_step / (k0_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["traffic"], roof["traffic_source"] = profiled_traffic(args.config, "field_ncu_full",
+                                                                   "k_resolve<")
+        roof["algorithmic_bytes_per_launch"] = bytes_step
+        roof["kernel_ms"] = k0_ms
+        roof["stage_ms"] = {"k0_resolve": k0_ms, "list": list_ms}
+        roof["k0_share_of_step"] = k0_ms / ms_per_step
+    else:  # tree-only pipelines (forced modes): the whole step against the survey roofline
+        kernel_ms = ms_per_step
+        if t_fp32 >= t_hbm:
+            roof = {"bound": "fp32", "achieved": flops_step / (kernel_ms * 1e-3) / 1e12,
+                    "peak": peak_fp32.value, "unit": "TFLOP/s"}
+        else:
+            roof = {"bound": "hbm", "achieved": bytes_step / (kernel_ms * 1e-3) / 1e9,
+                    "peak": hbm_peak, "unit": "GB/s"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["traffic"], roof["traffic_source"] = profiled_traffic(args.config)
+    roof["peak_source"] = ("HBM: MEASURED_PEAKS.json hbm_gbs; FP32: FFMA microbenchmark measured "
+                           "live (capt_measure_fp32_peak)")
+    roof["survey_roofline"] = survey
 
     # e2e: the C-ABI call a plugin makes (capt_query with CAPT_HOST_IO) on
     # pinned host buffers -- H2D of the spheres, the kernels and the D2H of

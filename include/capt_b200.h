@@ -171,6 +171,15 @@ typedef struct {
 } capt_field_info;
 int capt_tree_field(const capt_tree* tree, capt_field_info* info, float* cells);
 
+/* Stage timing of the clearance-field pipeline (measurement helper for
+ * bench.py's roofline): while enabled, every field-pipeline capt_query
+ * records CUDA events on its stream around the resolve kernel (K0) and the
+ * list stage.  capt_stage_times waits for them and returns the summed
+ * milliseconds ms[0] = K0, ms[1] = list stage, ms[2] = both, with the number
+ * of calls, then clears the record.  Enabling also clears it. */
+int capt_stage_timing(int enable);
+int capt_stage_times(double* ms, int64_t* calls);
+
 /* Number of kernels this library has launched in the process so far
  * (all devices/threads); used by bench.py to report gpu_launches. */
 int64_t capt_kernel_launches(void);

@@ -42,6 +42,7 @@
 #include <cstring>
 
 #include "capt_binned.cuh"
+#include "capt_tc.cuh"
 #include "capt_internal.cuh"
 #include "capt_query_common.cuh"
 
@@ -264,12 +265,13 @@ struct Chunk {
   float4 p0, p1, p2, pr;  // xyz of 4 consecutive spheres in 3 float4, their radii
 };
 
-template <bool kVec>
+// kFull: the chunk is known to be whole (no bounds test)
+template <bool kVec, bool kFull = false>
 __device__ __forceinline__ Chunk load_chunk(const float* __restrict__ cf,
                                             const float* __restrict__ rf, int c, int lane, int n) {
   Chunk k;
   const int q0 = (c << 7) + 4 * lane;
-  if (kVec && (c << 7) + 128 <= n) {
+  if (kVec && (kFull || (c << 7) + 128 <= n)) {
     const float4* c4 = reinterpret_cast<const float4*>(cf + 3 * size_t(q0));
     k.p0 = __ldcs(c4);
     k.p1 = __ldcs(c4 + 1);
@@ -307,12 +309,12 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
   const int n = a.n;
   const int q0 = (ch << 7) + 4 * lane;
   const unsigned nxu = unsigned(g.nx), nyu = unsigned(g.ny), nzu = unsigned(g.nz);
-  // phase 1: validity, band, cells; all four record loads in flight
+  // phase 1: validity, band, cell, record load of sphere v (skip: its lane
+  // group already has a hit -- no record is fetched)
   bool valid[4], inband[4], look[4];
   int ix[4], iy[4], iz[4];
   float4 rec[4];
-#pragma unroll
-  for (int v = 0; v < 4; ++v) {
+  auto cell = [&](int v, bool skip) {
     valid[v] = kFull || q0 + v < n;
     if (kMask) valid[v] = valid[v] && a.mask[valid[v] ? q0 + v : 0] != 0;
     inband[v] = r[v] >= a.rlo_f && r[v] <= a.rhi_f;
@@ -321,17 +323,20 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
     iz[v] = __float2int_rd(__fmul_rn(__fsub_rn(z[v], g.lo[2]), g.inv_h));
     // (the index is used only inside the grid: no clamp)
     const bool in = unsigned(ix[v]) < nxu && unsigned(iy[v]) < nyu && unsigned(iz[v]) < nzu;
-    look[v] = valid[v] && inband[v] && in;
+    look[v] = valid[v] && inband[v] && in && !skip;
     rec[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+#ifndef CAPT_K0_NOFIELD
     if (look[v])
       rec[v] = ldg_keep(a.t.field + ((unsigned(iz[v]) * nyu + unsigned(iy[v])) * nxu + unsigned(ix[v])),
                         pol);
-  }
-  // phase 2: the certificates
+#else  // timing experiment only (wrong verdicts): no record loads
+    rec[v] = make_float4(float(ix[v]), float(iy[v]), float(iz[v]), 1e30f);
+#endif
+  };
+  // phase 2: the certificates of sphere v
   unsigned hitb = 0, undb = 0, badb = 0;
   const float band_lo = 1.0f - kTau;
-#pragma unroll
-  for (int v = 0; v < 4; ++v) {
+  auto cert = [&](int v) {
     const float ex = x[v] - centre_of(ix[v], g.h, g.c0[0]);
     const float ey = y[v] - centre_of(iy[v], g.h, g.c0[1]);
     const float ez = z[v] - centre_of(iz[v], g.h, g.c0[2]);
@@ -341,12 +346,29 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
     const float A = fmaf(-r[v], kK1, rec[v].w);
     const bool free = A > 0.f && A * A > e2 * kK1;
     hitb |= unsigned(look[v] && hit) << v;
-    // decided: in-band and (outside the grid, or certified); with check_radii
-    // an out-of-band (non-NaN) radius only reports first_bad
+    // decided: in-band and (outside the grid / skipped, or certified); with
+    // check_radii an out-of-band (non-NaN) radius only reports first_bad
     const bool bad = check && valid[v] && (r[v] < a.rlo_f || r[v] > a.rhi_f);
     badb |= unsigned(bad) << v;
     const bool decided = inband[v] && (!look[v] || hit || free);
     undb |= unsigned(valid[v] && !decided && !bad) << v;
+  };
+  if (LT == 8) {
+    // 8-sphere groups span lanes (2j, 2j+1): the first sphere of each lane
+    // goes first; a group with a hit fetches no more records (query.py:152-160
+    // early exit, applied to the L2 traffic -- K0 is bound by it)
+    cell(0, false);
+    cert(0);
+    const bool any0 = __shfl_xor_sync(0xffffffffu, hitb, 1) | hitb;
+#pragma unroll
+    for (int v = 1; v < 4; ++v) cell(v, any0);
+#pragma unroll
+    for (int v = 1; v < 4; ++v) cert(v);
+  } else {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) cell(v, false);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) cert(v);
   }
   if (check && __any_sync(0xffffffffu, badb != 0)) {
 #pragma unroll
@@ -438,14 +460,14 @@ __global__ void __launch_bounds__(256, CAPT_K0_MINB) k_resolve(FieldArgs a) {
   const uint64_t pol = l2_keep_policy();
   int ch = w0;
   if (ch < nfull) {
-    Chunk A = load_chunk<kVec>(a.c, a.r, ch, lane, n), B;
+    Chunk A = load_chunk<kVec, true>(a.c, a.r, ch, lane, n), B;
     while (true) {
       const int c1 = ch + nwarps;
-      if (c1 < nfull) B = load_chunk<kVec>(a.c, a.r, c1, lane, n);
+      if (c1 < nfull) B = load_chunk<kVec, true>(a.c, a.r, c1, lane, n);
       resolve_chunk<kMask, LT, !kMask>(a, g, A, ch, lane, check, pol);
       if (c1 >= nfull) break;
       const int c2 = c1 + nwarps;
-      if (c2 < nfull) A = load_chunk<kVec>(a.c, a.r, c2, lane, n);
+      if (c2 < nfull) A = load_chunk<kVec, true>(a.c, a.r, c2, lane, n);
       resolve_chunk<kMask, LT, !kMask>(a, g, B, c1, lane, check, pol);
       if (c2 >= nfull) break;
       ch = c2;
@@ -454,6 +476,94 @@ __global__ void __launch_bounds__(256, CAPT_K0_MINB) k_resolve(FieldArgs a) {
   if ((n & 127) && w0 == nfull % nwarps) {
     const Chunk T = load_chunk<false>(a.c, a.r, nfull, lane, n);
     resolve_chunk<kMask, LT, false>(a, g, T, nfull, lane, check, pol);
+  }
+}
+
+// K0 with TMA bulk copies (the default for unmasked, 16-B aligned batches).
+// Persistent CTAs of 8 warps take tiles of 1024 spheres; one thread streams
+// each tile's centres (12 KB) and radii (4 KB) into a ring of kStages
+// shared-memory stages with cp.async.bulk (completion on the stage's
+// mbarrier, L2 evict-first), so the sphere stream stays in flight without
+// holding registers; warp w decides chunk w of the tile from shared memory
+// (resolve_chunk), the stage is refilled once every warp is past it.  The
+// spheres after the last whole tile take the register path.
+constexpr int kTileSpheres = 1024;
+constexpr int kStages = 3;
+constexpr uint32_t kTileC = kTileSpheres * 12, kTileR = kTileSpheres * 4;
+constexpr size_t kTmaSmem = size_t(kStages) * (kTileC + kTileR) + 64;
+
+__device__ __forceinline__ uint64_t l2_stream_policy() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(mbar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(tc::smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(tc::smem_u32(mbar)), "l"(pol)
+      : "memory");
+}
+
+template <int LT>
+__global__ void __launch_bounds__(256, 4) k_resolve_tma(FieldArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* const sc = reinterpret_cast<float*>(smem);
+  float* const sr = reinterpret_cast<float*>(smem + kStages * kTileC);
+  uint64_t* const full = reinterpret_cast<uint64_t*>(smem + kStages * (kTileC + kTileR));
+  const FieldGeom g = a.t.fg;
+  const bool check = a.flags & CAPT_CHECK_RADII;
+  const int n = a.n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ntiles = n / kTileSpheres;
+  const uint64_t keep = l2_keep_policy();
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kStages; ++st) tc::mbar_init(&full[st], 1);
+    tc::fence_async_smem();
+  }
+  __syncthreads();
+  auto issue = [&](int tile, int st) {
+    const uint64_t pol = l2_stream_policy();
+    mbar_expect_tx(&full[st], kTileC + kTileR);
+    bulk_g2s(sc + st * (kTileC / 4), a.c + size_t(tile) * kTileSpheres * 3, kTileC, &full[st], pol);
+    bulk_g2s(sr + st * (kTileR / 4), a.r + size_t(tile) * kTileSpheres, kTileR, &full[st], pol);
+  };
+  if (threadIdx.x == 0)
+    for (int st = 0; st < kStages; ++st) {
+      const int tile = blockIdx.x + st * gridDim.x;
+      if (tile < ntiles) issue(tile, st);
+    }
+  int it = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int st = it % kStages;
+    tc::mbar_wait(&full[st], uint32_t((it / kStages) & 1));
+    const float4* c4 = reinterpret_cast<const float4*>(sc + st * (kTileC / 4) + warp * 384) + 3 * lane;
+    Chunk k;
+    k.p0 = c4[0];
+    k.p1 = c4[1];
+    k.p2 = c4[2];
+    k.pr = reinterpret_cast<const float4*>(sr + st * (kTileR / 4) + warp * 128)[lane];
+    resolve_chunk<false, LT, true>(a, g, k, tile * (kTileSpheres / 128) + warp, lane, check, keep);
+    __syncthreads();  // every warp is past stage st
+    if (threadIdx.x == 0) {
+      const int next = tile + kStages * gridDim.x;
+      if (next < ntiles) issue(next, st);
+    }
+  }
+  // the spheres after the last whole tile: register path, one chunk per warp
+  const int nchunks = (n + 127) >> 7;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int ch = ntiles * (kTileSpheres / 128) + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+       ch < nchunks; ch += nwarps) {
+    const Chunk k = load_chunk<true>(a.c, a.r, ch, lane, n);
+    if ((ch << 7) + 128 <= n) resolve_chunk<false, LT, true>(a, g, k, ch, lane, check, keep);
+    else resolve_chunk<false, LT, false>(a, g, k, ch, lane, check, keep);
   }
 }
 
@@ -729,6 +839,21 @@ bool field_eligible(const DevTree& t, int64_t n, uint32_t flags) {
   return !(flags & (CAPT_MODE_DIRECT | CAPT_MODE_BINNED | CAPT_MODE_THREAD | CAPT_MODE_WARP));
 }
 
+// Stage timing (capt_stage_timing / capt_stage_times): CUDA events on the
+// launching stream around K0 and the list stage of every field-pipeline call,
+// read back and summed on request (no synchronisation inside the calls).
+struct StageEvents {
+  static constexpr int kMax = 2048;
+  bool on = false;
+  int n = 0;
+  cudaEvent_t ev[kMax][3] = {};
+  void record(int call, int k, cudaStream_t s) {
+    if (!ev[call][k]) cudaEventCreate(&ev[call][k]);
+    cudaEventRecord(ev[call][k], s);
+  }
+};
+static StageEvents g_stage;
+
 int launch_field(const DevTree& t, const void* centers, const void* radii, int64_t n, int L,
                  const uint8_t* mask, uint32_t flags, uint32_t* bits, int64_t n_words,
                  unsigned long long* first_bad, cudaStream_t s) {
@@ -751,17 +876,32 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   CAPT_CUDA(dmalloc(&a.list, n, s));
   CAPT_CUDA(cudaMemsetAsync(a.list_n, 0, 4, s));
   if (L >= 8) CAPT_CUDA(cudaMemsetAsync(bits, 0, 4 * (n_words ? n_words : 1), s));
+  const int tcall = (g_stage.on && g_stage.n < StageEvents::kMax) ? g_stage.n++ : -1;
+  if (tcall >= 0) g_stage.record(tcall, 0, s);
   const bool vec = (reinterpret_cast<uintptr_t>(centers) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(radii) & 15) == 0;
   const int grid = grid_for(((n + 127) / 128) * 32, 256, 8);
-  // specialised for unmasked fp32 batches of single spheres and 8-sphere
-  // groups (configs 0-4); everything else takes the generic instantiation
-  if (vec && !mask && L == 1) k_resolve<true, false, 1><<<grid, 256, 0, s>>>(a);
+  // unmasked 16-B aligned batches: the TMA-fed kernel (specialised for single
+  // spheres and 8-sphere groups, configs 0-4); everything else the register path
+  static const bool use_tma = getenv("CAPT_K0_TMA") != nullptr;
+  if (vec && !mask && use_tma && n >= kTileSpheres) {
+    static bool attr = false;
+    if (!attr) {
+      for (auto f : {k_resolve_tma<1>, k_resolve_tma<8>, k_resolve_tma<0>})
+        CAPT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTmaSmem)));
+      attr = true;
+    }
+    const int gt = grid_for(((n + kTileSpheres - 1) / kTileSpheres) * 256, 256, 4);
+    if (L == 1) k_resolve_tma<1><<<gt, 256, kTmaSmem, s>>>(a);
+    else if (L == 8) k_resolve_tma<8><<<gt, 256, kTmaSmem, s>>>(a);
+    else k_resolve_tma<0><<<gt, 256, kTmaSmem, s>>>(a);
+  } else if (vec && !mask && L == 1) k_resolve<true, false, 1><<<grid, 256, 0, s>>>(a);
   else if (vec && !mask && L == 8) k_resolve<true, false, 8><<<grid, 256, 0, s>>>(a);
   else if (mask) k_resolve<false, true, 0><<<grid, 256, 0, s>>>(a);
   else k_resolve<false, false, 0><<<grid, 256, 0, s>>>(a);
   CAPT_CUDA(cudaGetLastError());
   note_launches(1);
+  if (tcall >= 0) g_stage.record(tcall, 1, s);
   // the list: one warp-cooperative kernel, or -- for large batches over large
   // affordance sets, where the tensor-core binned scan amortises each set
   // over up to 128 spheres -- the leaf-binned pipeline in list mode
@@ -784,6 +924,7 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
     CAPT_CUDA(cudaGetLastError());
     note_launches(1);
   }
+  if (tcall >= 0) g_stage.record(tcall, 2, s);
   static const bool debug = getenv("CAPT_DEBUG") != nullptr;
   if (debug) {
     uint32_t nl = 0;
@@ -823,5 +964,28 @@ extern "C" int capt_tree_field(const capt_tree* tree, capt_field_info* info, flo
     CAPT_CUDA(cudaMemcpy(cells, tree->field, sizeof(float4) * size_t(g.cells),
                          cudaMemcpyDeviceToHost));
   }
+  return CAPT_OK;
+}
+
+extern "C" int capt_stage_timing(int enable) {
+  g_stage.on = enable != 0;
+  g_stage.n = 0;
+  return CAPT_OK;
+}
+
+extern "C" int capt_stage_times(double* ms, int64_t* calls) {
+  if (!ms || !calls) return fail(CAPT_EINVAL, "NULL argument");
+  ms[0] = ms[1] = ms[2] = 0.0;
+  for (int i = 0; i < g_stage.n; ++i) {
+    CAPT_CUDA(cudaEventSynchronize(g_stage.ev[i][2]));
+    float a = 0.f, b = 0.f;
+    CAPT_CUDA(cudaEventElapsedTime(&a, g_stage.ev[i][0], g_stage.ev[i][1]));
+    CAPT_CUDA(cudaEventElapsedTime(&b, g_stage.ev[i][1], g_stage.ev[i][2]));
+    ms[0] += a;
+    ms[1] += b;
+    ms[2] += a + b;
+  }
+  *calls = g_stage.n;
+  g_stage.n = 0;
   return CAPT_OK;
 }
