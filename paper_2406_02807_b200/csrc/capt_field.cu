@@ -570,22 +570,16 @@ __global__ void __launch_bounds__(256, 4) k_resolve_tma(FieldArgs a) {
 // The tree path over the list (the reference's semantics for every sphere it
 // holds).  The list is short but its spheres are the hard ones, so the kernel
 // is built for short dependent-load chains: a warp takes 8 entries; lanes 0-7
-// descend (top levels from shared memory), load the leaf's probe record
+// descend (T through L1), load the leaf's probe record
 // (conservative AABB reject, representative probe); then 4 lanes per entry
 // scan its set, 64 points per step (12 128-bit loads in flight per lane),
 // fp32 with the float64 re-scan of the band.  (One entry per lane with a
 // serial warp scan, or a per-thread scan, measured ~73 us for config 1's 85 K
 // entries: the warp waits on its longest chain.)
-constexpr int kListSmemLevels = 11;
-constexpr int kListSmem = (1 << kListSmemLevels) - 1;
 constexpr int kLE = 8;  // list entries per warp
 
 __global__ void __launch_bounds__(256) k_resolve_list(FieldArgs a) {
-  __shared__ float sT[kListSmem];
   const DevTree& t = a.t;
-  const int n_smem = int(t.n - 1 < kListSmem ? t.n - 1 : kListSmem);
-  for (int i = threadIdx.x; i < n_smem; i += blockDim.x) sT[i] = t.T[i];
-  __syncthreads();
   const uint32_t n_list = *a.list_n;
   const int lane = threadIdx.x & 31;
   const int slot = lane >> 2, sl = lane & 3;
@@ -613,11 +607,10 @@ __global__ void __launch_bounds__(256) k_resolve_list(FieldArgs a) {
     if (active) {
       // descent (tree.py:266-273)
       int i = 0;
-      for (int s = 0; s < t.depth; ++s) {
+      for (int s = 0; s < t.depth; ++s) {  // (the top levels stay in L1)
         const int ax = s % 3;
         const float cv = ax == 0 ? cx : (ax == 1 ? cy : cz);
-        const float tv = i < n_smem ? sT[i] : __ldg(t.T + i);
-        i = 2 * i + 1 + (cv > tv ? 1 : 0);
+        i = 2 * i + 1 + (cv > __ldg(t.T + i) ? 1 : 0);
       }
       leaf = i - int(t.n - 1);
       // classification (as k_bin_count3 / k_query_hybrid)
@@ -640,54 +633,89 @@ __global__ void __launch_bounds__(256) k_resolve_list(FieldArgs a) {
     const bool scan = (st == 2 || st == 3) && !verdict && (hitm & gm) == 0;
     uint2 set = make_uint2(0u, 0u);
     if (scan) set = __ldg(t.set + leaf);
-    // the scan: slot k (lanes 4k .. 4k+3) takes entry k's set
-    const float sx = __shfl_sync(0xffffffffu, cx, slot);
-    const float sy = __shfl_sync(0xffffffffu, cy, slot);
-    const float sz = __shfl_sync(0xffffffffu, cz, slot);
-    const float sr2 = __shfl_sync(0xffffffffu, r2, slot);
-    const bool sf = __shfl_sync(0xffffffffu, scan && st == 2, slot);
-    const uint32_t sset = __shfl_sync(0xffffffffu, set.x, slot);
-    const uint32_t sy_m = __shfl_sync(0xffffffffu, set.y, slot);
-    const uint32_t sm = sf ? sy_m : 0u;
-    const uint32_t m4 = (sm + 3u) & ~3u;
-    const float* base = reinterpret_cast<const float*>(t.data + sset);
-    const float loB = sr2 * band_lo, hiB = sr2 * band_hi;
-    uint32_t mmax = m4;
+    // the scan, load-balanced over the warp: entry e's set is split into
+    // items of 64 points; in each step slot k (lanes 4k .. 4k+3, 16 points
+    // per lane) takes item 8 step + k of the concatenated item list, so the
+    // warp takes ceil(sum items / 8) steps instead of the longest set's
+    const bool scan32 = scan && st == 2;
+    const uint32_t m4e = scan32 ? ((set.y + 3u) & ~3u) : 0u;   // lanes 0-7: entry lane
+    const uint32_t items = (m4e + 63u) >> 6;
+    uint32_t incl = items;  // inclusive prefix over lanes 0-7
 #pragma unroll
-    for (int o = 4; o < 32; o <<= 1) mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
-    bool hit = false, amb = false;
-    for (uint32_t p0 = 0; p0 < mmax; p0 += 64) {
-      if (!hit) {
+    for (int o = 1; o < 8; o <<= 1) {
+      const uint32_t tv = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += tv;
+    }
+    uint32_t pre[kLE];  // inclusive prefix of every entry (uniform)
+#pragma unroll
+    for (int e = 0; e < kLE; ++e) pre[e] = __shfl_sync(0xffffffffu, incl, e);
+    const uint32_t total = pre[kLE - 1];
+    const float loB0 = r2 * band_lo, hiB0 = r2 * band_hi;
+    bool hit_e = false, amb_e = false;  // lanes 0-7: their entry's result
+    for (uint32_t s0 = 0; s0 < total; s0 += kLE) {
+      const uint32_t item = s0 + slot;
+      int e = 0;
+#pragma unroll
+      for (int k = 0; k < kLE - 1; ++k) e += item >= pre[k] ? 1 : 0;
+      const uint32_t first = e ? pre[e - 1] : 0u;
+      // entry e's data (shuffles are warp-wide; lanes past the end read entry 7)
+      const float sx = __shfl_sync(0xffffffffu, cx, e);
+      const float sy = __shfl_sync(0xffffffffu, cy, e);
+      const float sz = __shfl_sync(0xffffffffu, cz, e);
+      const float loB = __shfl_sync(0xffffffffu, loB0, e);
+      const float hiB = __shfl_sync(0xffffffffu, hiB0, e);
+      const uint32_t sset = __shfl_sync(0xffffffffu, set.x, e);
+      const uint32_t m4 = __shfl_sync(0xffffffffu, m4e, e);
+      const bool done = __shfl_sync(0xffffffffu, hit_e, e);  // entry already hit: skip
+      const bool live = item < total && !done;
+      const float* base = reinterpret_cast<const float*>(t.data + sset);
+      const uint32_t p0 = (item - first) * 64u;
+      bool hit = false, amb = false;
+      if (live) {
+        // all 12 loads in flight: rows past the set are clamped to row 0 and
+        // masked out of the result
+        float4 px[4], py[4], pz[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const uint32_t p = p0 + 16 * u + 4 * sl;
-          if (p < m4) {
-            const float4 px = __ldg(reinterpret_cast<const float4*>(base + p));
-            const float4 py = __ldg(reinterpret_cast<const float4*>(base + m4 + p));
-            const float4 pz = __ldg(reinterpret_cast<const float4*>(base + 2 * m4 + p));
-            const float xs[4] = {px.x, px.y, px.z, px.w}, ys[4] = {py.x, py.y, py.z, py.w},
-                        zs[4] = {pz.x, pz.y, pz.z, pz.w};
+          const uint32_t pc = p < m4 ? p : 0u;
+          px[u] = __ldg(reinterpret_cast<const float4*>(base + pc));
+          py[u] = __ldg(reinterpret_cast<const float4*>(base + m4 + pc));
+          pz[u] = __ldg(reinterpret_cast<const float4*>(base + 2 * m4 + pc));
+        }
 #pragma unroll
-            for (int w = 0; w < 4; ++w) {
-              const float d2 = d2_fma(sx - xs[w], sy - ys[w], sz - zs[w]);
-              hit |= d2 <= loB;
-              amb |= d2 < hiB;
-            }
+        for (int u = 0; u < 4; ++u) {
+          const bool in = p0 + 16 * u + 4 * sl < m4;
+          const float xs[4] = {px[u].x, px[u].y, px[u].z, px[u].w},
+                      ys[4] = {py[u].x, py[u].y, py[u].z, py[u].w},
+                      zs[4] = {pz[u].x, pz[u].y, pz[u].z, pz[u].w};
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const float d2 = d2_fma(sx - xs[w], sy - ys[w], sz - zs[w]);
+            hit |= in && d2 <= loB;
+            amb |= in && d2 < hiB;
           }
         }
       }
-      // a slot stops at its first hit (its 4 lanes agree after the vote)
+      // fold the step's results into the owning entries (lanes 0-7)
       const unsigned hb = __ballot_sync(0xffffffffu, hit);
-      hit = (hb >> (4 * slot)) & 15u;
-      const unsigned live = __ballot_sync(0xffffffffu, !hit && p0 + 64 < m4);
-      if (!live) break;
+      const unsigned ab = __ballot_sync(0xffffffffu, amb);
+#pragma unroll
+      for (int k = 0; k < kLE; ++k) {
+        const uint32_t ik = s0 + k;
+        int ek = 0;
+#pragma unroll
+        for (int j = 0; j < kLE - 1; ++j) ek += ik >= pre[j] ? 1 : 0;
+        if (ek == lane && ik < total) {
+          hit_e |= ((hb >> (4 * k)) & 15u) != 0;
+          amb_e |= ((ab >> (4 * k)) & 15u) != 0;
+        }
+      }
     }
-    const unsigned hb = __ballot_sync(0xffffffffu, hit);
-    const unsigned ab = __ballot_sync(0xffffffffu, amb);
     if (scan) {
       if (st == 2) {
-        verdict = (hb >> (4 * lane)) & 15u;
-        if (!verdict && ((ab >> (4 * lane)) & 15u)) {
+        verdict = hit_e;
+        if (!verdict && amb_e) {
           const double c64[3] = {cx, cy, cz};
           verdict = scan_f64(t, set, c64, double(r), nullptr);
         }
