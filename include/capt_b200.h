@@ -155,18 +155,21 @@ int capt_nn_distances(int device, int k, const float* points, int64_t n,
 
 /* Clearance field of a k = 3 tree (derived data, built on the device with
  * the tree): a uniform grid of nx*ny*nz cells of edge h from lo; cell
- * (ix,iy,iz) is record (iz*ny + iy)*nx + ix = {witness x, y, z, nn} with
- * centre x0 = fmaf((float)ix, h, c0[0]) (likewise y, z), witness = the
- * cloud point nearest x0 (+inf if none within rcap) and nn <= the distance
- * from x0 to every cloud point (nn <= rcap).  box_lo/box_hi: the cloud's box.
- * cells: NULL, or a host buffer of 4 * n_cells floats.  Returns CAPT_EINVAL
+ * (ix,iy,iz) is the 32-byte record (iz*ny + iy)*nx + ix = {witness x, y, z,
+ * nn, 8 x fp16 octant bounds} with centre x0 = fmaf((float)ix, h, c0[0])
+ * (likewise y, z).  witness = the cloud point nearest x0 (+inf if none within
+ * rcap); nn <= the distance from x0 to every cloud point (nn <= rcap); the
+ * fp16 bound o (bits 0/1/2 = x/y/z at or above x0) is <= the distance from
+ * every point of the octant box [x0, x0 + oct_half] / [x0 - oct_half, x0]
+ * (per axis) to every cloud point.  box_lo/box_hi: the cloud's box.
+ * cells: NULL, or a host buffer of 8 * n_cells floats.  Returns CAPT_EINVAL
  * for trees without a field. */
 typedef struct {
   int32_t nx, ny, nz, reserved;
   int64_t n_cells;
   float lo[3], h;
   float box_lo[3], box_hi[3];
-  float rcap, pad;
+  float rcap, oct_half;
   float c0[3], pad2;
 } capt_field_info;
 int capt_tree_field(const capt_tree* tree, capt_field_info* info, float* cells);

@@ -42,7 +42,7 @@ class CaptFieldInfo(C.Structure):
     _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32),
                 ("reserved", C.c_int32), ("n_cells", C.c_int64), ("lo", C.c_float * 3),
                 ("h", C.c_float), ("box_lo", C.c_float * 3), ("box_hi", C.c_float * 3),
-                ("rcap", C.c_float), ("pad", C.c_float), ("c0", C.c_float * 3),
+                ("rcap", C.c_float), ("oct_half", C.c_float), ("c0", C.c_float * 3),
                 ("pad2", C.c_float)]
 
 

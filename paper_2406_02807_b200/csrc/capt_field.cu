@@ -33,6 +33,7 @@
 //                       lane-group resolution, bit words, compact list)
 //           k_resolve_list (the tree path over the list)
 #include <cub/cub.cuh>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <climits>
@@ -40,6 +41,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "capt_binned.cuh"
 #include "capt_tc.cuh"
@@ -86,6 +88,12 @@ __device__ __forceinline__ float4 ldg_keep(const float4* p, uint64_t pol) {
       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
       : "l"(p), "l"(pol));
   return v;
+}
+// fp16 octant bound o of a cell (octant array: 8 halves per cell)
+__device__ __forceinline__ float oct_bound(const float4* oct, unsigned cell, unsigned o) {
+  const unsigned short hb =
+      __ldg(reinterpret_cast<const unsigned short*>(oct) + 8 * size_t(cell) + o);
+  return __half2float(__ushort_as_half(hb));
 }
 __device__ __forceinline__ float d2_fma(float dx, float dy, float dz) {
   return fmaf(dz, dz, fmaf(dy, dy, dx * dx));
@@ -169,8 +177,10 @@ __global__ void __launch_bounds__(256, 1) k_field_nn(FieldGeom g, BucketGrid b,
   const int cx = min(g.m, g.nx - x0), cy = min(g.m, g.ny - y0), cz = min(g.m, g.nz - z0);
   const int ncells = cx * cy * cz;
   const float INF = __int_as_float(0x7f800000);
+  const float hh = g.oct_half;
   for (int pass = 0; pass < ncells; pass += 256 * kCellsPerThread) {
     float px[kCellsPerThread], py[kCellsPerThread], pz[kCellsPerThread], best[kCellsPerThread];
+    float ob[kCellsPerThread][8];  // squared distance from each octant box
     int bi[kCellsPerThread];
 #pragma unroll
     for (int k = 0; k < kCellsPerThread; ++k) {
@@ -181,6 +191,8 @@ __global__ void __launch_bounds__(256, 1) k_field_nn(FieldGeom g, BucketGrid b,
       pz[k] = centre_of(z0 + lz, g.h, g.c0[2]);
       best[k] = INF;
       bi[k] = -1;
+#pragma unroll
+      for (int o = 0; o < 8; ++o) ob[k][o] = INF;
     }
     for (int nz = max(bz - 1, 0); nz <= min(bz + 1, b.nbz - 1); ++nz)
       for (int ny = max(by - 1, 0); ny <= min(by + 1, b.nby - 1); ++ny)
@@ -196,10 +208,23 @@ __global__ void __launch_bounds__(256, 1) k_field_nn(FieldGeom g, BucketGrid b,
               const float4 p = sp[i];
 #pragma unroll
               for (int k = 0; k < kCellsPerThread; ++k) {
-                const float d2 = d2_fma(px[k] - p.x, py[k] - p.y, pz[k] - p.z);
+                const float ax = p.x - px[k], ay = p.y - py[k], az = p.z - pz[k];
+                const float d2 = d2_fma(ax, ay, az);
                 if (d2 < best[k]) {
                   best[k] = d2;
                   bi[k] = int(c0) + i;
+                }
+                // gap from the octant box [x0, x0 + hh] (bit 1) / [x0 - hh, x0] (bit 0)
+                const float gx1 = fmaxf(fmaxf(-ax, ax - hh), 0.f), gx0 = fmaxf(fmaxf(ax, -ax - hh), 0.f);
+                const float gy1 = fmaxf(fmaxf(-ay, ay - hh), 0.f), gy0 = fmaxf(fmaxf(ay, -ay - hh), 0.f);
+                const float gz1 = fmaxf(fmaxf(-az, az - hh), 0.f), gz0 = fmaxf(fmaxf(az, -az - hh), 0.f);
+                const float xy[4] = {fmaf(gy0, gy0, gx0 * gx0), fmaf(gy0, gy0, gx1 * gx1),
+                                     fmaf(gy1, gy1, gx0 * gx0), fmaf(gy1, gy1, gx1 * gx1)};
+                const float zz0 = gz0 * gz0, zz1 = gz1 * gz1;
+#pragma unroll
+                for (int o = 0; o < 4; ++o) {
+                  ob[k][o] = fminf(ob[k][o], xy[o] + zz0);
+                  ob[k][o + 4] = fminf(ob[k][o + 4], xy[o] + zz1);
                 }
               }
             }
@@ -210,13 +235,27 @@ __global__ void __launch_bounds__(256, 1) k_field_nn(FieldGeom g, BucketGrid b,
       const int j = pass + k * 256 + threadIdx.x;
       // fp32 |x0 - p|^2 has relative error < 5u, sqrtf one more u:
       // sqrtf(d2) (1 - 2^-19) (rounded) < the real distance
-      const int b = bi[k] >= 0 ? bi[k] : 0;
+      const int bsel = bi[k] >= 0 ? bi[k] : 0;
       const float nn = fminf(g.rcap, __fmul_rn(sqrtf(best[k]), kNNShrink));
+      // octant bounds: the same relative margin and an absolute one for the
+      // rounded gaps, capped where the candidate search ends, fp16 rounded down
+      unsigned short hb[8];
+#pragma unroll
+      for (int o = 0; o < 8; ++o) {
+        float lb = fmaf(sqrtf(ob[k][o]), kNNShrink, -g.oct_abs);
+        lb = fminf(fmaxf(lb, 0.f), g.oct_cap);
+        hb[o] = __half_as_ushort(__float2half_rd(lb));
+      }
       if (j < ncells) {
         const int lx = j % cx, ly = (j / cx) % cy, lz = j / (cx * cy);
         const int64_t cell = (int64_t(z0 + lz) * g.ny + (y0 + ly)) * g.nx + (x0 + lx);
-        const float4 w = bi[k] >= 0 ? pts[b] : make_float4(INF, INF, INF, 0.f);
+        const float4 w = bi[k] >= 0 ? pts[bsel] : make_float4(INF, INF, INF, 0.f);
         field[cell] = make_float4(w.x, w.y, w.z, nn);
+        field[g.cells + cell] = make_float4(
+            __uint_as_float(unsigned(hb[0]) | (unsigned(hb[1]) << 16)),
+            __uint_as_float(unsigned(hb[2]) | (unsigned(hb[3]) << 16)),
+            __uint_as_float(unsigned(hb[4]) | (unsigned(hb[5]) << 16)),
+            __uint_as_float(unsigned(hb[6]) | (unsigned(hb[7]) << 16)));
       }
     }
   }
@@ -325,13 +364,9 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
     const bool in = unsigned(ix[v]) < nxu && unsigned(iy[v]) < nyu && unsigned(iz[v]) < nzu;
     look[v] = valid[v] && inband[v] && in && !skip;
     rec[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-#ifndef CAPT_K0_NOFIELD
     if (look[v])
       rec[v] = ldg_keep(a.t.field + ((unsigned(iz[v]) * nyu + unsigned(iy[v])) * nxu + unsigned(ix[v])),
                         pol);
-#else  // timing experiment only (wrong verdicts): no record loads
-    rec[v] = make_float4(float(ix[v]), float(iy[v]), float(iz[v]), 1e30f);
-#endif
   };
   // phase 2: the certificates of sphere v
   unsigned hitb = 0, undb = 0, badb = 0;
@@ -343,7 +378,7 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
     const float e2 = d2_fma(ex, ey, ez);
     const float r2 = r[v] * r[v];
     const bool hit = d2_fma(x[v] - rec[v].x, y[v] - rec[v].y, z[v] - rec[v].z) <= r2 * band_lo;
-    const float A = fmaf(-r[v], kK1, rec[v].w);
+    const float A = rec[v].w - r[v] * kK1;  // (fl(r k) >= r (1 + 15u))
     const bool free = A > 0.f && A * A > e2 * kK1;
     hitb |= unsigned(look[v] && hit) << v;
     // decided: in-band and (outside the grid / skipped, or certified); with
@@ -567,6 +602,51 @@ __global__ void __launch_bounds__(256, 4) k_resolve_tma(FieldArgs a) {
   }
 }
 
+// List filter: the octant certificate.  Each cell also stores, per octant
+// (bit d set: the centre is at or above x0 on axis d -- an exact sign test),
+// an fp16 lower bound of the distance from the octant's box to the cloud
+// (rounded down at build, the box grown by the cell-index rounding); an
+// undecided in-band sphere whose bound exceeds fl(r (1 + 2^-20)) is free.
+// Survivors are compacted in order within each warp (one atomic per warp).
+// One 2-byte load per listed sphere instead of an octant record for every
+// sphere in K0 (32-byte records there cost more than the shorter list saves).
+__global__ void __launch_bounds__(256) k_list_octant(FieldArgs a, uint32_t* __restrict__ out,
+                                                     uint32_t* __restrict__ out_n) {
+  const FieldGeom g = a.t.fg;
+  const float4* oct = a.t.field + g.cells;
+  const uint32_t n_list = *a.list_n;
+  const int lane = threadIdx.x & 31;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t j0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; j0 < n_list; j0 += stride) {
+    const uint32_t j = j0 + lane;
+    const bool act = j < n_list;
+    const uint32_t q = act ? a.list[j] : 0u;
+    bool keep = act;
+    if (act) {
+      const float x = __ldg(a.c + 3 * size_t(q)), y = __ldg(a.c + 3 * size_t(q) + 1),
+                  z = __ldg(a.c + 3 * size_t(q) + 2), r = __ldg(a.r + q);
+      const int ix = __float2int_rd(__fmul_rn(__fsub_rn(x, g.lo[0]), g.inv_h));
+      const int iy = __float2int_rd(__fmul_rn(__fsub_rn(y, g.lo[1]), g.inv_h));
+      const int iz = __float2int_rd(__fmul_rn(__fsub_rn(z, g.lo[2]), g.inv_h));
+      const bool in = unsigned(ix) < unsigned(g.nx) && unsigned(iy) < unsigned(g.ny) &&
+                      unsigned(iz) < unsigned(g.nz);
+      if (in && r >= a.rlo_f && r <= a.rhi_f) {
+        const unsigned o = (x - centre_of(ix, g.h, g.c0[0]) >= 0.f ? 1u : 0u) |
+                           (y - centre_of(iy, g.h, g.c0[1]) >= 0.f ? 2u : 0u) |
+                           (z - centre_of(iz, g.h, g.c0[2]) >= 0.f ? 4u : 0u);
+        const unsigned cell = (unsigned(iz) * unsigned(g.ny) + unsigned(iy)) * unsigned(g.nx) +
+                              unsigned(ix);
+        keep = !(oct_bound(oct, cell, o) > r * kK1);
+      }
+    }
+    const unsigned km = __ballot_sync(0xffffffffu, keep);
+    unsigned base = 0;
+    if (lane == 0 && km) base = atomicAdd(out_n, unsigned(__popc(km)));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (keep) out[base + __popc(km & ((1u << lane) - 1u))] = q;
+  }
+}
+
 // The tree path over the list (the reference's semantics for every sphere it
 // holds).  The list is short but its spheres are the hard ones, so the kernel
 // is built for short dependent-load chains: a warp takes 8 entries; lanes 0-7
@@ -712,17 +792,22 @@ __global__ void __launch_bounds__(256) k_resolve_list(FieldArgs a) {
         }
       }
     }
-    if (scan) {
-      if (st == 2) {
-        verdict = hit_e;
-        if (!verdict && amb_e) {
-          const double c64[3] = {cx, cy, cz};
-          verdict = scan_f64(t, set, c64, double(r), nullptr);
-        }
-      } else {  // st == 3: the exact path only
-        const double c64[3] = {cx, cy, cz};
-        verdict = scan_f64(t, set, c64, double(r), nullptr);
-      }
+    if (scan && st == 2) verdict = hit_e;
+    // float64 re-scans (fp32 band hits; st == 3: the exact path only), one
+    // entry at a time by the whole warp (a per-thread scan of a 600-point set
+    // is a chain of dependent loads that outlasts the rest of the kernel)
+    unsigned exact = __ballot_sync(0xffffffffu, scan && !verdict && (st == 3 || amb_e));
+    while (exact) {
+      const int src = __ffs(exact) - 1;
+      exact &= exact - 1;
+      const double c64[3] = {__shfl_sync(0xffffffffu, double(cx), src),
+                             __shfl_sync(0xffffffffu, double(cy), src),
+                             __shfl_sync(0xffffffffu, double(cz), src)};
+      const double r64 = __shfl_sync(0xffffffffu, double(r), src);
+      const uint2 sset = make_uint2(__shfl_sync(0xffffffffu, set.x, src),
+                                    __shfl_sync(0xffffffffu, set.y, src));
+      const bool h64 = warp_scan_f64(t, sset, c64, r64, lane);
+      if (lane == src) verdict = h64;
     }
     // one OR per hit sphere (L = 1) or per group (first hitting lane)
     const unsigned vm = __ballot_sync(0xffffffffu, verdict);
@@ -804,6 +889,24 @@ int build_field(capt_tree* tree, cudaStream_t s) {
   // even when its computed cell index is off by one
   g.rcap = float(rmax + h);
   g.m = int(std::ceil(double(g.rcap) / h)) + 2;
+  // octant boxes: a centre assigned to a cell lies within h/2 + delta of its
+  // x0 per axis (delta covers the rounding of the cell index and of x0);
+  // half-edge hh = h/2 + delta rounded up; absolute slack for the rounded
+  // gaps; bounds capped at rcap - sqrt(3) hh (points beyond the candidate
+  // search are farther than that from every octant point)
+  {
+    double maxabs = 0.0;
+    int64_t maxdim = std::max<int64_t>(dims[0], std::max<int64_t>(dims[1], dims[2]));
+    for (int d = 0; d < 3; ++d)
+      maxabs = std::max(maxabs, std::max(std::fabs(double(g.lo[d])),
+                                         std::fabs(double(g.lo[d]) + dims[d] * h)));
+    const double u = std::ldexp(1.0, -24);
+    const double delta = h * std::ldexp(1.0, -12) + 8 * u * (double(maxdim) * h + maxabs);
+    g.oct_half = std::nextafter(float(0.5 * h + delta), INFINITY);
+    g.oct_abs = float(16 * u * (maxabs + double(g.rcap) + h));
+    g.oct_cap = std::max(0.0f, float(double(g.rcap) - std::sqrt(3.0) * double(g.oct_half)) *
+                                   (1.0f - 0x1p-20f));
+  }
   BucketGrid b;
   b.nbx = (g.nx + g.m - 1) / g.m;
   b.nby = (g.ny + g.m - 1) / g.m;
@@ -835,7 +938,7 @@ int build_field(capt_tree* tree, cudaStream_t s) {
   CAPT_CUDA(cudaStreamSynchronize(s));
   k_bucket_points<<<grid_for(n_fin, 256, 8), 256, 0, s>>>(t.rep, ids_out, n_fin, pts);
   float4* field = nullptr;
-  cudaError_t e = cudaMalloc(&field, sizeof(float4) * size_t(g.cells));
+  cudaError_t e = cudaMalloc(&field, 2 * sizeof(float4) * size_t(g.cells));
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(clearance field)");
   k_field_nn<<<int(b.nb), 256, 0, s>>>(g, b, bstart, pts, field);
   e = cudaGetLastError();
@@ -930,6 +1033,15 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   CAPT_CUDA(cudaGetLastError());
   note_launches(1);
   if (tcall >= 0) g_stage.record(tcall, 1, s);
+  // octant filter: a.list -> list2 (the list stage reads list2)
+  FieldArgs a2 = a;
+  CAPT_CUDA(dmalloc(&a2.list_n, 1, s));
+  CAPT_CUDA(dmalloc(&a2.list, n, s));
+  CAPT_CUDA(cudaMemsetAsync(a2.list_n, 0, 4, s));
+  // (a short list: few CTAs, one 32-entry warp step each -- launch cost dominates)
+  k_list_octant<<<grid_for(int64_t(n) / 64 + 1, 256, 2), 256, 0, s>>>(a, a2.list, a2.list_n);
+  CAPT_CUDA(cudaGetLastError());
+  note_launches(1);
   // the list: one warp-cooperative kernel, or -- for large batches over large
   // affordance sets, where the tensor-core binned scan amortises each set
   // over up to 128 spheres -- the leaf-binned pipeline in list mode
@@ -946,23 +1058,27 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   int rc = CAPT_OK;
   if (binned) {
     rc = launch_binned(t, centers, radii, n, L, nullptr, flags, bits, n_words, first_bad, s,
-                       a.list, a.list_n);
+                       a2.list, a2.list_n);
   } else {
-    k_resolve_list<<<grid_for(int64_t(1) << 30, 256, 8), 256, 0, s>>>(a);
+    k_resolve_list<<<grid_for(int64_t(1) << 30, 256, 8), 256, 0, s>>>(a2);
     CAPT_CUDA(cudaGetLastError());
     note_launches(1);
   }
   if (tcall >= 0) g_stage.record(tcall, 2, s);
   static const bool debug = getenv("CAPT_DEBUG") != nullptr;
   if (debug) {
-    uint32_t nl = 0;
+    uint32_t nl = 0, nl2 = 0;
     CAPT_CUDA(cudaMemcpyAsync(&nl, a.list_n, 4, cudaMemcpyDeviceToHost, s));
+    CAPT_CUDA(cudaMemcpyAsync(&nl2, a2.list_n, 4, cudaMemcpyDeviceToHost, s));
     CAPT_CUDA(cudaStreamSynchronize(s));
-    fprintf(stderr, "[capt field] n=%lld L=%d undecided=%u (%.3f%%) list=%s\n", (long long)n, L, nl,
-            100.0 * nl / double(n ? n : 1), binned ? "binned" : "thread");
+    fprintf(stderr, "[capt field] n=%lld L=%d undecided=%u (%.3f%%) after octants=%u (%.3f%%) list=%s\n",
+            (long long)n, L, nl, 100.0 * nl / double(n ? n : 1), nl2, 100.0 * nl2 / double(n ? n : 1),
+            binned ? "binned" : "thread");
   }
   cudaFreeAsync(a.list, s);
   cudaFreeAsync(a.list_n, s);
+  cudaFreeAsync(a2.list, s);
+  cudaFreeAsync(a2.list_n, s);
   return rc;
 }
 
@@ -981,16 +1097,23 @@ extern "C" int capt_tree_field(const capt_tree* tree, capt_field_info* info, flo
   info->n_cells = g.cells;
   info->h = g.h;
   info->rcap = g.rcap;
+  info->oct_half = g.oct_half;
   for (int d = 0; d < 3; ++d) {
     info->lo[d] = g.lo[d];
     info->c0[d] = g.c0[d];
     info->box_lo[d] = g.blo[d];
     info->box_hi[d] = g.bhi[d];
   }
-  if (cells) {
+  if (cells) {  // device: all witness records, then all octant records; out: interleaved
     CAPT_CUDA(cudaSetDevice(tree->device));
-    CAPT_CUDA(cudaMemcpy(cells, tree->field, sizeof(float4) * size_t(g.cells),
+    std::vector<float4> tmp(2 * size_t(g.cells));
+    CAPT_CUDA(cudaMemcpy(tmp.data(), tree->field, 2 * sizeof(float4) * size_t(g.cells),
                          cudaMemcpyDeviceToHost));
+    float4* out = reinterpret_cast<float4*>(cells);
+    for (int64_t i = 0; i < g.cells; ++i) {
+      out[2 * i] = tmp[i];
+      out[2 * i + 1] = tmp[g.cells + i];
+    }
   }
   return CAPT_OK;
 }

@@ -68,6 +68,7 @@ struct FieldGeom {
   float h, inv_h;
   float blo[3], bhi[3];
   float rcap;
+  float oct_half, oct_abs, oct_cap;  // octant boxes (half-edge), bound slack and cap
   int64_t cells;
 };
 

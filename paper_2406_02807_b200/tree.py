@@ -191,8 +191,9 @@ class Capt:
 
     def clearance_field(self, cells: bool = False):
         """The tree's clearance field (include/capt_b200.h capt_tree_field):
-        a dict of its geometry, plus the (nz, ny, nx, 4) float32 records
-        {witness xyz, nn} when ``cells``; None for trees without one (k < 3)."""
+        a dict of its geometry, plus the (nz, ny, nx, 8) float32 records
+        {witness xyz, nn, 8 fp16 octant bounds in 4 words} when ``cells``;
+        None for trees without one (k < 3)."""
         info = _lib.CaptFieldInfo()
         L = _lib.lib()
         if L.capt_tree_field(self._h, C.byref(info), None) != _lib.CAPT_OK:
@@ -201,9 +202,10 @@ class Capt:
                    lo=np.array(info.lo[:], np.float32), h=np.float32(info.h),
                    c0=np.array(info.c0[:], np.float32),
                    box_lo=np.array(info.box_lo[:], np.float32),
-                   box_hi=np.array(info.box_hi[:], np.float32), rcap=np.float32(info.rcap))
+                   box_hi=np.array(info.box_hi[:], np.float32), rcap=np.float32(info.rcap),
+                   oct_half=np.float32(info.oct_half))
         if cells:
-            buf = np.empty((info.nz, info.ny, info.nx, 4), np.float32)
+            buf = np.empty((info.nz, info.ny, info.nx, 8), np.float32)
             _lib.check(L.capt_tree_field(self._h, C.byref(info), buf.ctypes.data),
                        "capt_tree_field")
             out["cells"] = buf

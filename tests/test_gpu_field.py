@@ -48,7 +48,7 @@ def check_field(tree, cloud, sample=200000, seed=0):
     from scipy.spatial import cKDTree
     f = tree.clearance_field(cells=True)
     assert f is not None
-    cells = f["cells"].reshape(-1, 4)
+    cells = f["cells"].reshape(-1, 8)
     nz, ny, nx = f["shape"]
     assert f["n_cells"] == nx * ny * nz <= int((1 << 21) * 1.05)
     pts = np.unique(cloud.astype(np.float32), axis=0).astype(np.float64)
@@ -78,6 +78,18 @@ def check_field(tree, cloud, sample=200000, seed=0):
     assert np.allclose(rec[near, 3], nn[near], rtol=1e-5, atol=1e-7)
     wset = {tuple(p) for p in cloud.astype(np.float32)[:, :3].tolist()}
     assert all(tuple(w) in wset for w in rec[has][:2000, :3].astype(np.float32).tolist())
+    # octant bounds: below the distance from random points of the octant box
+    # (and from its corners) to the cloud, and not vacuous where nn is small
+    octs = cells[idx, 4:].copy().view(np.float16).astype(np.float64)  # (m, 8)
+    hh = np.float64(f["oct_half"])
+    o = rng.integers(0, 8, len(idx))
+    bits = np.stack([(o >> d) & 1 for d in range(3)], 1).astype(np.float64)
+    for u in (rng.uniform(0, 1, (len(idx), 3)), np.ones((len(idx), 3)), np.zeros((len(idx), 3))):
+        qpt = x0 + np.where(bits == 1, u, -u) * hh
+        dq, _ = cKDTree(pts).query(qpt)
+        assert np.all(octs[np.arange(len(idx)), o] <= dq + 1e-9)
+    lb = octs[np.arange(len(idx)), o]
+    assert np.mean(lb[near] > 0) > 0.5
     return f
 
 
