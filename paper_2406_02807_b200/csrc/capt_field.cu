@@ -610,10 +610,25 @@ __global__ void __launch_bounds__(256, 4) k_resolve_tma(FieldArgs a) {
 // Survivors are compacted in order within each warp (one atomic per warp).
 // One 2-byte load per listed sphere instead of an octant record for every
 // sphere in K0 (32-byte records there cost more than the shorter list saves).
+__device__ __forceinline__ bool octant_free(const FieldArgs& a, const FieldGeom& g, float x,
+                                            float y, float z, float r) {
+  const int ix = __float2int_rd(__fmul_rn(__fsub_rn(x, g.lo[0]), g.inv_h));
+  const int iy = __float2int_rd(__fmul_rn(__fsub_rn(y, g.lo[1]), g.inv_h));
+  const int iz = __float2int_rd(__fmul_rn(__fsub_rn(z, g.lo[2]), g.inv_h));
+  const bool in = unsigned(ix) < unsigned(g.nx) && unsigned(iy) < unsigned(g.ny) &&
+                  unsigned(iz) < unsigned(g.nz);
+  if (!in || !(r >= a.rlo_f && r <= a.rhi_f)) return false;
+  const unsigned o = (x - centre_of(ix, g.h, g.c0[0]) >= 0.f ? 1u : 0u) |
+                     (y - centre_of(iy, g.h, g.c0[1]) >= 0.f ? 2u : 0u) |
+                     (z - centre_of(iz, g.h, g.c0[2]) >= 0.f ? 4u : 0u);
+  const unsigned cell =
+      (unsigned(iz) * unsigned(g.ny) + unsigned(iy)) * unsigned(g.nx) + unsigned(ix);
+  return oct_bound(a.t.field + g.cells, cell, o) > r * kK1;
+}
+
 __global__ void __launch_bounds__(256) k_list_octant(FieldArgs a, uint32_t* __restrict__ out,
                                                      uint32_t* __restrict__ out_n) {
   const FieldGeom g = a.t.fg;
-  const float4* oct = a.t.field + g.cells;
   const uint32_t n_list = *a.list_n;
   const int lane = threadIdx.x & 31;
   const uint32_t stride = gridDim.x * blockDim.x;
@@ -625,19 +640,7 @@ __global__ void __launch_bounds__(256) k_list_octant(FieldArgs a, uint32_t* __re
     if (act) {
       const float x = __ldg(a.c + 3 * size_t(q)), y = __ldg(a.c + 3 * size_t(q) + 1),
                   z = __ldg(a.c + 3 * size_t(q) + 2), r = __ldg(a.r + q);
-      const int ix = __float2int_rd(__fmul_rn(__fsub_rn(x, g.lo[0]), g.inv_h));
-      const int iy = __float2int_rd(__fmul_rn(__fsub_rn(y, g.lo[1]), g.inv_h));
-      const int iz = __float2int_rd(__fmul_rn(__fsub_rn(z, g.lo[2]), g.inv_h));
-      const bool in = unsigned(ix) < unsigned(g.nx) && unsigned(iy) < unsigned(g.ny) &&
-                      unsigned(iz) < unsigned(g.nz);
-      if (in && r >= a.rlo_f && r <= a.rhi_f) {
-        const unsigned o = (x - centre_of(ix, g.h, g.c0[0]) >= 0.f ? 1u : 0u) |
-                           (y - centre_of(iy, g.h, g.c0[1]) >= 0.f ? 2u : 0u) |
-                           (z - centre_of(iz, g.h, g.c0[2]) >= 0.f ? 4u : 0u);
-        const unsigned cell = (unsigned(iz) * unsigned(g.ny) + unsigned(iy)) * unsigned(g.nx) +
-                              unsigned(ix);
-        keep = !(oct_bound(oct, cell, o) > r * kK1);
-      }
+      keep = !octant_free(a, g, x, y, z, r);
     }
     const unsigned km = __ballot_sync(0xffffffffu, keep);
     unsigned base = 0;
@@ -658,6 +661,7 @@ __global__ void __launch_bounds__(256) k_list_octant(FieldArgs a, uint32_t* __re
 // entries: the warp waits on its longest chain.)
 constexpr int kLE = 8;  // list entries per warp
 
+template <bool kOct>
 __global__ void __launch_bounds__(256) k_resolve_list(FieldArgs a) {
   const DevTree& t = a.t;
   const uint32_t n_list = *a.list_n;
@@ -684,7 +688,9 @@ __global__ void __launch_bounds__(256) k_resolve_list(FieldArgs a) {
     int st = 0, leaf = 0;
     bool verdict = false;
     float r2 = 0.f;
-    if (active) {
+    // the octant certificate first (k_list_octant when the list is filtered)
+    const bool sure_free = kOct && active && octant_free(a, a.t.fg, cx, cy, cz, r);
+    if (active && !sure_free) {
       // descent (tree.py:266-273)
       int i = 0;
       for (int s = 0; s < t.depth; ++s) {  // (the top levels stay in L1)
@@ -1033,15 +1039,6 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   CAPT_CUDA(cudaGetLastError());
   note_launches(1);
   if (tcall >= 0) g_stage.record(tcall, 1, s);
-  // octant filter: a.list -> list2 (the list stage reads list2)
-  FieldArgs a2 = a;
-  CAPT_CUDA(dmalloc(&a2.list_n, 1, s));
-  CAPT_CUDA(dmalloc(&a2.list, n, s));
-  CAPT_CUDA(cudaMemsetAsync(a2.list_n, 0, 4, s));
-  // (a short list: few CTAs, one 32-entry warp step each -- launch cost dominates)
-  k_list_octant<<<grid_for(int64_t(n) / 64 + 1, 256, 2), 256, 0, s>>>(a, a2.list, a2.list_n);
-  CAPT_CUDA(cudaGetLastError());
-  note_launches(1);
   // the list: one warp-cooperative kernel, or -- for large batches over large
   // affordance sets, where the tensor-core binned scan amortises each set
   // over up to 128 spheres -- the leaf-binned pipeline in list mode
@@ -1056,11 +1053,20 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   }
   flags &= ~uint32_t(CAPT_MODE_BINNED | CAPT_MODE_DIRECT | CAPT_MODE_FIELD);
   int rc = CAPT_OK;
+  FieldArgs a2 = a;  // the filtered list (binned path)
   if (binned) {
+    // octant filter first: the binned pipeline's cost follows its list
+    CAPT_CUDA(dmalloc(&a2.list_n, 1, s));
+    CAPT_CUDA(dmalloc(&a2.list, n, s));
+    CAPT_CUDA(cudaMemsetAsync(a2.list_n, 0, 4, s));
+    k_list_octant<<<grid_for(int64_t(n) / 64 + 1, 256, 2), 256, 0, s>>>(a, a2.list, a2.list_n);
+    CAPT_CUDA(cudaGetLastError());
+    note_launches(1);
     rc = launch_binned(t, centers, radii, n, L, nullptr, flags, bits, n_words, first_bad, s,
                        a2.list, a2.list_n);
   } else {
-    k_resolve_list<<<grid_for(int64_t(1) << 30, 256, 8), 256, 0, s>>>(a2);
+    // grid for the worst case (every sphere listed): 8 entries per warp
+    k_resolve_list<true><<<grid_for(int64_t(n) * 4 + 32, 256, 8), 256, 0, s>>>(a);
     CAPT_CUDA(cudaGetLastError());
     note_launches(1);
   }
@@ -1069,7 +1075,7 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   if (debug) {
     uint32_t nl = 0, nl2 = 0;
     CAPT_CUDA(cudaMemcpyAsync(&nl, a.list_n, 4, cudaMemcpyDeviceToHost, s));
-    CAPT_CUDA(cudaMemcpyAsync(&nl2, a2.list_n, 4, cudaMemcpyDeviceToHost, s));
+    if (binned) CAPT_CUDA(cudaMemcpyAsync(&nl2, a2.list_n, 4, cudaMemcpyDeviceToHost, s));
     CAPT_CUDA(cudaStreamSynchronize(s));
     fprintf(stderr, "[capt field] n=%lld L=%d undecided=%u (%.3f%%) after octants=%u (%.3f%%) list=%s\n",
             (long long)n, L, nl, 100.0 * nl / double(n ? n : 1), nl2, 100.0 * nl2 / double(n ? n : 1),
@@ -1077,8 +1083,10 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   }
   cudaFreeAsync(a.list, s);
   cudaFreeAsync(a.list_n, s);
-  cudaFreeAsync(a2.list, s);
-  cudaFreeAsync(a2.list_n, s);
+  if (binned) {
+    cudaFreeAsync(a2.list, s);
+    cudaFreeAsync(a2.list_n, s);
+  }
   return rc;
 }
 

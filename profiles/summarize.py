@@ -84,8 +84,8 @@ def sweep(path: str, out: str) -> None:
     rates = sorted({r["rate"] for r in rows})
     ns = sorted({r["n"] for r in rows})
     lines = [f"# {d['sweep']} (1x B200, tree {d['tree_leaves']} leaves)", "",
-             "G sphere queries/s: per call | CUDA-graph replay; path d = unbinned "
-             "(warp kernel), b = binned; ! = label mismatch", "",
+             "G sphere queries/s: per call | CUDA-graph replay; path f = clearance field "
+             "(default), d = unbinned tree kernels, b = binned; ! = label mismatch", "",
              "| spheres | " + " | ".join(f"rate {x}" for x in rates) + " |",
              "|---:|" + "---:|" * len(rates)]
     for n in ns:
