@@ -290,7 +290,6 @@ def main():
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     import ctypes
-    _lib.lib().capt_stage_timing(1)  # events around K0 / the list stage, on `stream`
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
@@ -298,6 +297,14 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
     launches = _lib.lib().capt_kernel_launches() - launches0
+    # the per-stage split (K0 / list stage) from CUDA events that capt_query
+    # records around its kernels on `stream`, over a second run of the same
+    # K steps (the events sit between the kernels and would cost the timed
+    # steps their programmatic-launch overlap, ~9 us per config-1 step)
+    _lib.lib().capt_stage_timing(1)
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
     st_ms = (ctypes.c_double * 3)()
     st_calls = ctypes.c_int64(0)
     _lib.check(_lib.lib().capt_stage_times(st_ms, ctypes.byref(st_calls)))

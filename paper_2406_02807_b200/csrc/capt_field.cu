@@ -619,6 +619,7 @@ __global__ void __launch_bounds__(256, CAPT_K0_MINB) k_resolve(FieldArgs a) {
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t pol = l2_keep_policy();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   int ch = w0;
 #ifndef CAPT_K0_PREFETCH  // one chunk in registers: 166 us at 4 CTAs/SM vs 175 (ping-pong, 3 CTAs)
   for (; ch < nfull; ch += nwarps) {
@@ -862,6 +863,9 @@ constexpr int kLE = 8;  // list entries per warp
 template <bool kOct>
 __global__ void __launch_bounds__(256) k_resolve_list(FieldArgs a) {
   const DevTree& t = a.t;
+  // launched with programmatic stream serialisation: scheduled while K0
+  // drains, reads K0's list only after K0 has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t n_list = *a.list_n;
   const int lane = threadIdx.x & 31;
   const int slot = lane >> 2, sl = lane & 3;
@@ -1285,7 +1289,16 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
                        a2.list, a2.list_n);
   } else {
     // grid for the worst case (every sphere listed): 8 entries per warp
-    k_resolve_list<true><<<grid_for(int64_t(n) * 4 + 32, 256, 8), 256, 0, s>>>(a);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid_for(int64_t(n) * 4 + 32, 256, 8));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CAPT_CUDA(cudaLaunchKernelEx(&cfg, k_resolve_list<true>, a));
     CAPT_CUDA(cudaGetLastError());
     note_launches(1);
   }
