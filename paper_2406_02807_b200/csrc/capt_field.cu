@@ -619,6 +619,8 @@ __global__ void __launch_bounds__(256, CAPT_K0_MINB) k_resolve(FieldArgs a) {
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t pol = l2_keep_policy();
+  // (launched after k_field_zero with programmatic serialisation)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   int ch = w0;
 #ifndef CAPT_K0_PREFETCH  // one chunk in registers: 166 us at 4 CTAs/SM vs 175 (ping-pong, 3 CTAs)
@@ -1183,6 +1185,31 @@ bool field_eligible(const DevTree& t, int64_t n, uint32_t flags) {
   return !(flags & (CAPT_MODE_DIRECT | CAPT_MODE_BINNED | CAPT_MODE_THREAD | CAPT_MODE_WARP));
 }
 
+// The pipeline's zeroing (list counter; the verdict words when lane groups
+// OR into them) as a kernel, so K0 can follow it with programmatic launch.
+__global__ void k_field_zero(uint32_t* __restrict__ ctr, uint32_t* __restrict__ bits,
+                             int64_t n_words) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int64_t i0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i0 < 8) ctr[i0] = 0u;
+  for (int64_t i = i0; i < n_words; i += int64_t(gridDim.x) * blockDim.x) bits[i] = 0u;
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl_f(void (*kernel)(KArgs...), int grid, int block, cudaStream_t s,
+                                Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // Stage timing (capt_stage_timing / capt_stage_times): CUDA events on the
 // launching stream around K0 and the list stage of every field-pipeline call,
 // read back and summed on request (no synchronisation inside the calls).
@@ -1216,10 +1243,14 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   if (double(hi) > t.r_max) hi = nextafterf(hi, -INFINITY);
   a.rlo_f = lo;
   a.rhi_f = hi;
-  CAPT_CUDA(dmalloc(&a.list_n, 1, s));
+  CAPT_CUDA(dmalloc(&a.list_n, 8, s));
   CAPT_CUDA(dmalloc(&a.list, n, s));
-  CAPT_CUDA(cudaMemsetAsync(a.list_n, 0, 4, s));
-  if (L >= 8) CAPT_CUDA(cudaMemsetAsync(bits, 0, 4 * (n_words ? n_words : 1), s));
+  {
+    const int64_t zw = L >= 8 ? n_words : 0;
+    k_field_zero<<<grid_for(zw + 8, 256, 4), 256, 0, s>>>(a.list_n, bits, zw);
+    CAPT_CUDA(cudaGetLastError());
+    note_launches(1);
+  }
   const int tcall = (g_stage.on && g_stage.n < StageEvents::kMax) ? g_stage.n++ : -1;
   if (tcall >= 0) g_stage.record(tcall, 0, s);
   const bool vec = (reinterpret_cast<uintptr_t>(centers) & 15) == 0 &&
@@ -1255,10 +1286,10 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
     else k_resolve_wtma<8><<<gw, 256, kWtmaSmem, s>>>(a);
   } else if (vec && !mask && use_pipe && L == 1) k_resolve_pipe<1><<<grid, 256, 0, s>>>(a);
   else if (vec && !mask && use_pipe && L == 8) k_resolve_pipe<8><<<grid, 256, 0, s>>>(a);
-  else if (vec && !mask && L == 1) k_resolve<true, false, 1><<<grid, 256, 0, s>>>(a);
-  else if (vec && !mask && L == 8) k_resolve<true, false, 8><<<grid, 256, 0, s>>>(a);
-  else if (mask) k_resolve<false, true, 0><<<grid, 256, 0, s>>>(a);
-  else k_resolve<false, false, 0><<<grid, 256, 0, s>>>(a);
+  else if (vec && !mask && L == 1) CAPT_CUDA(launch_pdl_f(k_resolve<true, false, 1>, grid, 256, s, a));
+  else if (vec && !mask && L == 8) CAPT_CUDA(launch_pdl_f(k_resolve<true, false, 8>, grid, 256, s, a));
+  else if (mask) CAPT_CUDA(launch_pdl_f(k_resolve<false, true, 0>, grid, 256, s, a));
+  else CAPT_CUDA(launch_pdl_f(k_resolve<false, false, 0>, grid, 256, s, a));
   CAPT_CUDA(cudaGetLastError());
   note_launches(1);
   if (tcall >= 0) g_stage.record(tcall, 1, s);
