@@ -524,7 +524,7 @@ def main_sweep(args):
             e1.record(stream)
             torch.cuda.synchronize()
             ms_graph = e0.elapsed_time(e1) / steps
-            mode = args.mode if args.mode != "auto" else "field"
+            mode = args.mode if args.mode != "auto" else ("field" if n >= 8192 else "direct")
             rows.append({"rate": rate, "n": n, "ms": ms, "queries_per_s": n / (ms * 1e-3),
                          "ms_graph": ms_graph, "queries_per_s_graph": n / (ms_graph * 1e-3),
                          "mode": mode, "labels_match": label_ok})

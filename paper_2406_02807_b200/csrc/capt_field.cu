@@ -484,121 +484,6 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
   emit_chunk<LT>(a, ch, lane, check, hitb, undb, badb);
 }
 
-#ifndef CAPT_K0P_MINB
-#define CAPT_K0P_MINB 2
-#endif
-// Pipelined K0 pieces: the records of chunk i+1 are requested before chunk
-// i is decided, so each record load has a whole chunk of work to arrive.
-struct Pend {
-  float4 rec[4];
-  unsigned look;  // bit v: record v was requested
-};
-
-template <bool kMask, bool kFull>
-__device__ __forceinline__ void issue_records(const FieldArgs& a, const FieldGeom& g,
-                                              const Chunk& k, int ch, int lane, uint64_t pol,
-                                              Pend& P) {
-  const float x[4] = {k.p0.x, k.p0.w, k.p1.z, k.p2.y};
-  const float y[4] = {k.p0.y, k.p1.x, k.p1.w, k.p2.z};
-  const float z[4] = {k.p0.z, k.p1.y, k.p2.x, k.p2.w};
-  const float r[4] = {k.pr.x, k.pr.y, k.pr.z, k.pr.w};
-  const int q0 = (ch << 7) + 4 * lane;
-  const unsigned nxu = unsigned(g.nx), nyu = unsigned(g.ny), nzu = unsigned(g.nz);
-  P.look = 0;
-#pragma unroll
-  for (int v = 0; v < 4; ++v) {
-    bool valid = kFull || q0 + v < a.n;
-    if (kMask) valid = valid && a.mask[valid ? q0 + v : 0] != 0;
-    const bool inband = r[v] >= a.rlo_f && r[v] <= a.rhi_f;
-    const int ix = __float2int_rd(__fmul_rn(__fsub_rn(x[v], g.lo[0]), g.inv_h));
-    const int iy = __float2int_rd(__fmul_rn(__fsub_rn(y[v], g.lo[1]), g.inv_h));
-    const int iz = __float2int_rd(__fmul_rn(__fsub_rn(z[v], g.lo[2]), g.inv_h));
-    const bool in = unsigned(ix) < nxu && unsigned(iy) < nyu && unsigned(iz) < nzu;
-    const bool look = valid && inband && in;
-    P.rec[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (look)
-      P.rec[v] = ldg_keep(a.t.field + ((unsigned(iz) * nyu + unsigned(iy)) * nxu + unsigned(ix)), pol);
-    P.look |= unsigned(look) << v;
-  }
-}
-
-template <bool kMask, int LT, bool kFull>
-__device__ __forceinline__ void finish_chunk(const FieldArgs& a, const FieldGeom& g,
-                                             const Chunk& k, int ch, int lane, bool check,
-                                             const Pend& P) {
-  const float x[4] = {k.p0.x, k.p0.w, k.p1.z, k.p2.y};
-  const float y[4] = {k.p0.y, k.p1.x, k.p1.w, k.p2.z};
-  const float z[4] = {k.p0.z, k.p1.y, k.p2.x, k.p2.w};
-  const float r[4] = {k.pr.x, k.pr.y, k.pr.z, k.pr.w};
-  const int q0 = (ch << 7) + 4 * lane;
-  const float band_lo = 1.0f - kTau;
-  unsigned hitb = 0, undb = 0, badb = 0;
-#pragma unroll
-  for (int v = 0; v < 4; ++v) {
-    bool valid = kFull || q0 + v < a.n;
-    if (kMask) valid = valid && a.mask[valid ? q0 + v : 0] != 0;
-    const bool inband = r[v] >= a.rlo_f && r[v] <= a.rhi_f;
-    const bool look = (P.look >> v) & 1u;
-    // (recomputed: cheaper than keeping the indices live across a chunk)
-    const int ix = __float2int_rd(__fmul_rn(__fsub_rn(x[v], g.lo[0]), g.inv_h));
-    const int iy = __float2int_rd(__fmul_rn(__fsub_rn(y[v], g.lo[1]), g.inv_h));
-    const int iz = __float2int_rd(__fmul_rn(__fsub_rn(z[v], g.lo[2]), g.inv_h));
-    const float e2 = d2_fma(x[v] - centre_of(ix, g.h, g.c0[0]), y[v] - centre_of(iy, g.h, g.c0[1]),
-                            z[v] - centre_of(iz, g.h, g.c0[2]));
-    const float4 rc = P.rec[v];
-    const float r2 = r[v] * r[v];
-    const bool hit = d2_fma(x[v] - rc.x, y[v] - rc.y, z[v] - rc.z) <= r2 * band_lo;
-    const float A = rc.w - r[v] * kK1;
-    const bool free = A > 0.f && A * A > e2 * kK1;
-    hitb |= unsigned(look && hit) << v;
-    const bool bad = check && valid && (r[v] < a.rlo_f || r[v] > a.rhi_f);
-    badb |= unsigned(bad) << v;
-    const bool decided = inband && (!look || hit || free);
-    undb |= unsigned(valid && !decided && !bad) << v;
-  }
-  emit_chunk<LT>(a, ch, lane, check, hitb, undb, badb);
-}
-
-template <int LT>
-__global__ void __launch_bounds__(256, CAPT_K0P_MINB) k_resolve_pipe(FieldArgs a) {
-  const FieldGeom g = a.t.fg;
-  const bool check = a.flags & CAPT_CHECK_RADII;
-  const int n = a.n;
-  const int lane = threadIdx.x & 31;
-  const int nfull = n >> 7;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t pol = l2_keep_policy();
-  int c0 = w0;
-  if (c0 < nfull) {
-    // A: chunk c0 (records requested), B: chunk c1 (inputs in flight)
-    Chunk A = load_chunk<true, true>(a.c, a.r, c0, lane, n), B;
-    Pend PA, PB;
-    issue_records<false, true>(a, g, A, c0, lane, pol, PA);
-    int c1 = c0 + nw;
-    if (c1 < nfull) B = load_chunk<true, true>(a.c, a.r, c1, lane, n);
-    while (true) {
-      if (c1 < nfull) issue_records<false, true>(a, g, B, c1, lane, pol, PB);
-      finish_chunk<false, LT, true>(a, g, A, c0, lane, check, PA);
-      if (c1 >= nfull) break;
-      int c2 = c1 + nw;
-      if (c2 < nfull) {
-        A = load_chunk<true, true>(a.c, a.r, c2, lane, n);
-        issue_records<false, true>(a, g, A, c2, lane, pol, PA);
-      }
-      finish_chunk<false, LT, true>(a, g, B, c1, lane, check, PB);
-      if (c2 >= nfull) break;
-      c0 = c2;
-      c1 = c2 + nw;
-      if (c1 < nfull) B = load_chunk<true, true>(a.c, a.r, c1, lane, n);
-    }
-  }
-  if ((n & 127) && w0 == nfull % nw) {
-    const Chunk T = load_chunk<false>(a.c, a.r, nfull, lane, n);
-    resolve_chunk<false, LT, false>(a, g, T, nfull, lane, check, pol);
-  }
-}
-
 // K0 CTAs per SM the register allocation must allow: one chunk per warp in
 // registers, 4 (54 registers; 5: 48 registers, slower on config 3); with the
 // ping-pong prefetch (CAPT_K0_PREFETCH) 3 was best (78 registers)
@@ -736,70 +621,6 @@ __global__ void __launch_bounds__(256, 4) k_resolve_tma(FieldArgs a) {
     const Chunk k = load_chunk<true>(a.c, a.r, ch, lane, n);
     if ((ch << 7) + 128 <= n) resolve_chunk<false, LT, true>(a, g, k, ch, lane, check, keep);
     else resolve_chunk<false, LT, false>(a, g, k, ch, lane, check, keep);
-  }
-}
-
-// K0 fed by warp-private TMA rings: each warp streams its own chunks (1.5 KB
-// of centres + 0.5 KB of radii) into kWS shared-memory slots with
-// cp.async.bulk (lane 0 issues, completion on the slot's mbarrier), so the
-// sphere stream runs kWS - 1 chunks ahead of the warp without registers and
-// without any CTA-wide barrier.
-#ifndef CAPT_K0W_SLOTS
-#define CAPT_K0W_SLOTS 3
-#endif
-constexpr int kWS = CAPT_K0W_SLOTS;
-constexpr size_t kWtmaSmem = size_t(8) * kWS * 2048 + 8 * kWS * 8;
-
-template <int LT>
-__global__ void __launch_bounds__(256, 4) k_resolve_wtma(FieldArgs a) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float* const slots = reinterpret_cast<float*>(smem + size_t(warp) * kWS * 2048);
-  uint64_t* const bar = reinterpret_cast<uint64_t*>(smem + size_t(8) * kWS * 2048) + warp * kWS;
-  const FieldGeom g = a.t.fg;
-  const bool check = a.flags & CAPT_CHECK_RADII;
-  const int n = a.n;
-  const int nfull = n >> 7;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t keep = l2_keep_policy();
-  const uint64_t stream = l2_stream_policy();
-  if (lane == 0) {
-    for (int st = 0; st < kWS; ++st) tc::mbar_init(&bar[st], 1);
-    tc::fence_async_smem();
-  }
-  __syncwarp();
-  auto issue = [&](int ch, int st) {
-    mbar_expect_tx(&bar[st], 2048);
-    bulk_g2s(slots + st * 512, a.c + size_t(ch) * 384, 1536, &bar[st], stream);
-    bulk_g2s(slots + st * 512 + 384, a.r + size_t(ch) * 128, 512, &bar[st], stream);
-  };
-  if (lane == 0)
-    for (int st = 0; st < kWS; ++st)
-      if (w0 + st * nw < nfull) issue(w0 + st * nw, st);
-  int it = 0;
-  for (int ch = w0; ch < nfull; ch += nw, ++it) {
-    const int st = it % kWS;
-    tc::mbar_wait(&bar[st], uint32_t((it / kWS) & 1));
-    const float4* c4 = reinterpret_cast<const float4*>(slots + st * 512) + 3 * lane;
-    Chunk k;
-    k.p0 = c4[0];
-    k.p1 = c4[1];
-    k.p2 = c4[2];
-    k.pr = reinterpret_cast<const float4*>(slots + st * 512 + 384)[lane];
-    resolve_chunk<false, LT, true>(a, g, k, ch, lane, check, keep);
-    __syncwarp();  // every lane has consumed the slot
-    if (lane == 0) {
-      const int next = ch + kWS * nw;
-      if (next < nfull) {
-        tc::fence_async_smem();
-        issue(next, st);
-      }
-    }
-  }
-  if ((n & 127) && w0 == nfull % nw) {
-    const Chunk T = load_chunk<false>(a.c, a.r, nfull, lane, n);
-    resolve_chunk<false, LT, false>(a, g, T, nfull, lane, check, keep);
   }
 }
 
@@ -1259,8 +1080,6 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   // unmasked 16-B aligned batches: the TMA-fed kernel (specialised for single
   // spheres and 8-sphere groups, configs 0-4); everything else the register path
   static const bool use_tma = getenv("CAPT_K0_TMA") != nullptr;
-  static const bool use_pipe = getenv("CAPT_K0_PIPE") != nullptr;
-  static const bool use_wtma = getenv("CAPT_K0_WTMA") != nullptr;
   if (vec && !mask && use_tma && n >= kTileSpheres) {
     static bool attr = false;
     if (!attr) {
@@ -1272,20 +1091,7 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
     if (L == 1) k_resolve_tma<1><<<gt, 256, kTmaSmem, s>>>(a);
     else if (L == 8) k_resolve_tma<8><<<gt, 256, kTmaSmem, s>>>(a);
     else k_resolve_tma<0><<<gt, 256, kTmaSmem, s>>>(a);
-  } else if (vec && !mask && use_wtma && (L == 1 || L == 8) && n >= 128) {
-    static bool wattr = false;
-    if (!wattr) {
-      CAPT_CUDA(cudaFuncSetAttribute(k_resolve_wtma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(kWtmaSmem)));
-      CAPT_CUDA(cudaFuncSetAttribute(k_resolve_wtma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(kWtmaSmem)));
-      wattr = true;
-    }
-    const int gw = grid_for(((n + 127) / 128) * 32, 256, 4);
-    if (L == 1) k_resolve_wtma<1><<<gw, 256, kWtmaSmem, s>>>(a);
-    else k_resolve_wtma<8><<<gw, 256, kWtmaSmem, s>>>(a);
-  } else if (vec && !mask && use_pipe && L == 1) k_resolve_pipe<1><<<grid, 256, 0, s>>>(a);
-  else if (vec && !mask && use_pipe && L == 8) k_resolve_pipe<8><<<grid, 256, 0, s>>>(a);
+  }
   else if (vec && !mask && L == 1) CAPT_CUDA(launch_pdl_f(k_resolve<true, false, 1>, grid, 256, s, a));
   else if (vec && !mask && L == 8) CAPT_CUDA(launch_pdl_f(k_resolve<true, false, 8>, grid, 256, s, a));
   else if (mask) CAPT_CUDA(launch_pdl_f(k_resolve<false, true, 0>, grid, 256, s, a));
