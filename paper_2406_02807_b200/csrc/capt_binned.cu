@@ -1093,8 +1093,13 @@ __global__ void __launch_bounds__(kTcThreads) k_binned_scan_tc(BinArgs a) {
     const TileMeta tm = a.tiles[tile];
     const int cnt = tm.cnt;
     const float4 org = tm.org;
-    const uint32_t m = tm.m, m4 = (m + 3u) & ~3u;
-    const float* xs = reinterpret_cast<const float*>(t.data + tm.setx);
+    const uint32_t m4 = (tm.m + 3u) & ~3u;
+    // with the distance-sorted copy (capt_field.cu) the rows are ordered by
+    // |p - org| and the tile stops at the first row beyond every sphere's
+    // r + |c - org| (m shrinks below; rows before it are all real points)
+    uint32_t m = tm.m;
+    const float* xs = t.sdata ? t.sdata + int64_t(tm.setx) * 4
+                              : reinterpret_cast<const float*>(t.data + tm.setx);
     const int nb = (cnt + 127) >> 7;  // sphere blocks in this tile
     // thread i < kTcNc stages row i of every chunk; the next chunk's point is
     // loaded while the current chunk's product runs (one chunk ahead), the
@@ -1136,6 +1141,20 @@ __global__ void __launch_bounds__(kTcThreads) k_binned_scan_tc(BinArgs a) {
 #pragma unroll
       for (int k = 11; k < 16; ++k) row[k] = 0.f;
       put_row(S.A, e, row);
+    }
+    if (t.sdata) {
+      __shared__ uint32_t s_cut;
+      if (tid == 0) s_cut = 0u;
+      __syncthreads();
+      if (tb < nb && e < cnt) {
+        const float4 rc = a.lrec[a.perm[tm.s0 + e]];
+        const float dx = rc.x - org.x, dy = rc.y - org.y, dz = rc.z - org.z;
+        const float ex = sqrtf(fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
+        atomicMax(&s_cut, __float_as_uint(__fmul_ru(__fadd_ru(rc.w, ex), 1.0f + 0x1p-18f)));
+      }
+      __syncthreads();
+      m = min(m, sorted_limit(t.sdist + int64_t(tm.setx) * 4 / 3, m4, __uint_as_float(s_cut)));
+      __syncthreads();
     }
     bool done = false;
     for (uint32_t c0 = 0; c0 < m && !done; c0 += kTcNc) {

@@ -261,6 +261,62 @@ __global__ void __launch_bounds__(256, 1) k_field_nn(FieldGeom g, BucketGrid b,
   }
 }
 
+// Distance-sorted set copy.  Keys: fp32 |p - o| (o = the set's origin) of
+// every stored row (padding rows +inf), sorted within each set; the scan of a
+// sphere (c, r) can stop at the first row with |p - o| > r + |c - o| (a row
+// beyond it is farther than r from c).  Stored distances are rounded down.
+__global__ void k_sort_keys(DevTree t, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                            int* __restrict__ seg_begin, int* __restrict__ seg_end) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t j = warp; j < t.n; j += nwarps) {
+    const uint2 st = t.set[j];
+    const uint32_t m4 = (st.y + 3u) & ~3u;
+    const float* base = reinterpret_cast<const float*>(t.data + st.x);
+    const int64_t b = int64_t(st.x) * 4 / 3;
+    const float4 o = t.org[j];
+    if (lane == 0) {
+      seg_begin[j] = int(b);
+      seg_end[j] = int(b + m4);
+    }
+    for (uint32_t i = lane; i < m4; i += 32) {
+      float d = __int_as_float(0x7f800000);
+      if (i < st.y) {
+        const float dx = base[i] - o.x, dy = base[m4 + i] - o.y, dz = base[2 * m4 + i] - o.z;
+        d = sqrtf(d2_fma(dx, dy, dz));
+        if (!(d <= 3.0e38f)) d = __int_as_float(0x7f800000);  // (+inf rows of padding leaves)
+      }
+      keys[b + i] = __float_as_uint(d);
+      vals[b + i] = i;
+    }
+  }
+}
+
+__global__ void k_sort_gather(DevTree t, const uint32_t* __restrict__ keys,
+                              const uint32_t* __restrict__ vals, float* __restrict__ sdata,
+                              float* __restrict__ sdist) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t j = warp; j < t.n; j += nwarps) {
+    const uint2 st = t.set[j];
+    const uint32_t m4 = (st.y + 3u) & ~3u;
+    const float* src = reinterpret_cast<const float*>(t.data + st.x);
+    float* dst = sdata + int64_t(st.x) * 4;
+    const int64_t b = int64_t(st.x) * 4 / 3;
+    for (uint32_t i = lane; i < m4; i += 32) {
+      const uint32_t k = vals[b + i];
+      dst[i] = src[k];
+      dst[m4 + i] = src[m4 + k];
+      dst[2 * m4 + i] = src[2 * m4 + k];
+      // fp32 |p - o| has relative error < 4u: (1 - 2^-19) rounds it below the real distance
+      sdist[b + i] = __fmul_rn(__uint_as_float(keys[b + i]), 1.0f - 0x1p-19f);
+    }
+  }
+}
+
+
 // ---------------------------------------------------------------- query
 
 struct FieldArgs {
@@ -750,7 +806,16 @@ __global__ void __launch_bounds__(256) k_resolve_list(FieldArgs a) {
     // warp takes ceil(sum items / 8) steps instead of the longest set's
     const bool scan32 = scan && st == 2;
     const uint32_t m4e = scan32 ? ((set.y + 3u) & ~3u) : 0u;   // lanes 0-7: entry lane
-    const uint32_t items = (m4e + 63u) >> 6;
+    // rows to scan: with the distance-sorted copy, only those within
+    // r + |c - o| of the set's origin (fl, rounded up: see sorted_limit)
+    uint32_t lime = m4e;
+    if (scan32 && t.sdata) {
+      const float4 o = __ldg(t.org + leaf);
+      const float e = sqrtf(d2_fma(cx - o.x, cy - o.y, cz - o.z));
+      const float cut = __fmul_ru(__fadd_ru(r, e), 1.0f + 0x1p-18f);
+      lime = sorted_limit(t.sdist + int64_t(set.x) * 4 / 3, m4e, cut);
+    }
+    const uint32_t items = (lime + 63u) >> 6;
     uint32_t incl = items;  // inclusive prefix over lanes 0-7
 #pragma unroll
     for (int o = 1; o < 8; o <<= 1) {
@@ -776,10 +841,12 @@ __global__ void __launch_bounds__(256) k_resolve_list(FieldArgs a) {
       const float loB = __shfl_sync(0xffffffffu, loB0, e);
       const float hiB = __shfl_sync(0xffffffffu, hiB0, e);
       const uint32_t sset = __shfl_sync(0xffffffffu, set.x, e);
-      const uint32_t m4 = __shfl_sync(0xffffffffu, m4e, e);
+      const uint32_t m4 = __shfl_sync(0xffffffffu, m4e, e);    // SoA stride
+      const uint32_t lim = __shfl_sync(0xffffffffu, lime, e);  // rows to scan
       const bool done = __shfl_sync(0xffffffffu, hit_e, e);  // entry already hit: skip
       const bool live = item < total && !done;
-      const float* base = reinterpret_cast<const float*>(t.data + sset);
+      const float* base = t.sdata ? t.sdata + int64_t(sset) * 4
+                                  : reinterpret_cast<const float*>(t.data + sset);
       const uint32_t p0 = (item - first) * 64u;
       bool hit = false, amb = false;
       if (live) {
@@ -789,14 +856,14 @@ __global__ void __launch_bounds__(256) k_resolve_list(FieldArgs a) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const uint32_t p = p0 + 16 * u + 4 * sl;
-          const uint32_t pc = p < m4 ? p : 0u;
+          const uint32_t pc = p < lim ? p : 0u;
           px[u] = __ldg(reinterpret_cast<const float4*>(base + pc));
           py[u] = __ldg(reinterpret_cast<const float4*>(base + m4 + pc));
           pz[u] = __ldg(reinterpret_cast<const float4*>(base + 2 * m4 + pc));
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const bool in = p0 + 16 * u + 4 * sl < m4;
+          const bool in = p0 + 16 * u + 4 * sl < lim;
           const float xs[4] = {px[u].x, px[u].y, px[u].z, px[u].w},
                       ys[4] = {py[u].x, py[u].y, py[u].z, py[u].w},
                       zs[4] = {pz[u].x, pz[u].y, pz[u].z, pz[u].w};
@@ -852,6 +919,63 @@ __global__ void __launch_bounds__(256) k_resolve_list(FieldArgs a) {
 }  // namespace
 
 // ---------------------------------------------------------------- host
+
+static int build_sorted(capt_tree* tree, cudaStream_t s) {
+  if (tree->sdata) cudaFree(tree->sdata);
+  if (tree->sdist) cudaFree(tree->sdist);
+  tree->sdata = tree->sdist = nullptr;
+  const DevTree t = view(tree);
+  const int64_t nf = tree->h.data_f4 * 4;  // floats of the data section
+  const int64_t items = nf / 3;
+  if (items <= 0 || items >= (int64_t(1) << 31)) return CAPT_OK;  // (no sorted copy)
+  uint32_t *keys = nullptr, *keys_o = nullptr, *vals = nullptr, *vals_o = nullptr;
+  int *sb = nullptr, *se = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  CAPT_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, keys, keys_o, vals, vals_o, int(items),
+                                                int(t.n), sb, se, s));
+  cudaError_t e = cudaSuccess;
+  float *sdata = nullptr, *sdist = nullptr;
+  e = cudaMalloc(&sdata, sizeof(float) * size_t(nf));
+  if (e == cudaSuccess) e = cudaMalloc(&sdist, sizeof(float) * size_t(items));
+  if (e == cudaSuccess) e = dmalloc(&keys, items, s);
+  if (e == cudaSuccess) e = dmalloc(&keys_o, items, s);
+  if (e == cudaSuccess) e = dmalloc(&vals, items, s);
+  if (e == cudaSuccess) e = dmalloc(&vals_o, items, s);
+  if (e == cudaSuccess) e = dmalloc(&sb, t.n, s);
+  if (e == cudaSuccess) e = dmalloc(&se, t.n, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&tmp, tb + 16, s);
+  if (e == cudaSuccess) {
+    k_sort_keys<<<grid_for(t.n * 32, 256, 8), 256, 0, s>>>(t, keys, vals, sb, se);
+    e = cub::DeviceSegmentedSort::SortPairs(tmp, tb, keys, keys_o, vals, vals_o, int(items),
+                                            int(t.n), sb, se, s);
+  }
+  if (e == cudaSuccess) {
+    k_sort_gather<<<grid_for(t.n * 32, 256, 8), 256, 0, s>>>(t, keys_o, vals_o, sdata, sdist);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFreeAsync(keys, s);
+  cudaFreeAsync(keys_o, s);
+  cudaFreeAsync(vals, s);
+  cudaFreeAsync(vals_o, s);
+  cudaFreeAsync(sb, s);
+  cudaFreeAsync(se, s);
+  cudaFreeAsync(tmp, s);
+  if (e != cudaSuccess) {
+    cudaFree(sdata);
+    cudaFree(sdist);
+    if (e == cudaErrorMemoryAllocation) {  // optional acceleration: run without it
+      cudaGetLastError();
+      return CAPT_OK;
+    }
+    return cuda_fail(e, "sorted set copy");
+  }
+  note_launches(3);
+  tree->sdata = sdata;
+  tree->sdist = sdist;
+  return CAPT_OK;
+}
 
 int build_field(capt_tree* tree, cudaStream_t s) {
   if (tree->field) {
@@ -989,7 +1113,7 @@ int build_field(capt_tree* tree, cudaStream_t s) {
   note_launches(6);
   tree->field = field;
   tree->fg = g;
-  return CAPT_OK;
+  return build_sorted(tree, s);
 }
 
 constexpr int64_t kFieldMinBatch = 8192;

@@ -88,6 +88,11 @@ struct DevTree {
   const float* probe; // 8 floats per leaf: rep xyz, fp16 box (conservative), 2 spare
   const float4* field;  // clearance field: per cell witness xyz + lower bound (or nullptr)
   FieldGeom fg;
+  // distance-sorted copy of the sets (capt_field.cu; nullptr if absent): the
+  // data section's layout with each set's rows ordered by |p - o| (o = org),
+  // and per set the sorted distances, rounded down: m4 floats at 4 set.x / 3
+  const float* sdata;
+  const float* sdist;
 };
 
 }  // namespace capt
@@ -98,6 +103,8 @@ struct capt_tree {
   char* slab;  // device pointer
   float4* field = nullptr;  // derived per device from the slab (capt_field.cu)
   capt::FieldGeom fg{};
+  float* sdata = nullptr;   // distance-sorted set copy (capt_field.cu)
+  float* sdist = nullptr;
 };
 
 namespace capt {
@@ -139,6 +146,8 @@ inline DevTree view(const capt_tree* t) {
   d.probe = reinterpret_cast<const float*>(t->slab + t->h.off_probe);
   d.field = t->field;
   d.fg = t->fg;
+  d.sdata = t->sdata;
+  d.sdist = t->sdist;
   return d;
 }
 

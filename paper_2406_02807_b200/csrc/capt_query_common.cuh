@@ -237,4 +237,16 @@ __device__ __forceinline__ bool warp_scan_f64(const DevTree& t, uint2 set, const
   return false;
 }
 
+// first row of a distance-sorted set beyond `cut` (binary search over 64-row items)
+__device__ __forceinline__ uint32_t sorted_limit(const float* __restrict__ sd, uint32_t m4,
+                                                 float cut) {
+  uint32_t lo = 0, hi = (m4 + 63u) >> 6;  // items [0, hi): the answer is in items
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(sd + 64u * mid) > cut) hi = mid;
+    else lo = mid + 1;
+  }
+  return min(m4, lo * 64u);  // every row at or after it is beyond cut
+}
+
 }  // namespace capt

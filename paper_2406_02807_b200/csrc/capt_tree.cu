@@ -379,6 +379,8 @@ void capt_tree_destroy(capt_tree* t) {
   cudaSetDevice(t->device);
   cudaFree(t->slab);
   if (t->field) cudaFree(t->field);
+  if (t->sdata) cudaFree(t->sdata);
+  if (t->sdist) cudaFree(t->sdist);
   cudaSetDevice(cur);
   delete t;
 }
