@@ -794,7 +794,7 @@ struct Spheres8 {
 // slot's owner (phase 0) writes their decision limits.
 __device__ __forceinline__ void load_spheres(Spheres8& sp, SmemBinned& S, const BinArgs& a,
                                              int64_t s0, const float4 org, int count, int slot,
-                                             bool active, bool owner) {
+                                             bool active, bool owner, uint32_t* cut = nullptr) {
   const float INF = __int_as_float(0x7f800000);
   sp.real = 0;
   sp.base = slot * kS;
@@ -819,6 +819,8 @@ __device__ __forceinline__ void load_spheres(Spheres8& sp, SmemBinned& S, const 
           const float thr = r2 - aa, band = kBand * (aa + org.w + r2);
           S.lim_lo[e] = thr - band;
           S.lim_hi[e] = thr + band;
+          if (cut)  // sorted copy: the tile's row cutoff (see k_binned_scan_tc)
+            atomicMax(cut, __float_as_uint(__fmul_ru(__fadd_ru(rc.w, sqrtf(aa)), 1.0f + 0x1p-18f)));
         }
       }
     }
@@ -956,7 +958,11 @@ __global__ void __launch_bounds__(kBT, CAPT_K5_MINB) k_binned_scan(BinArgs a) {
   const DevTree& t = a.t;
   const int tid = threadIdx.x;
   const int n_tiles = int(*a.n_tiles);
-  if (tid == 0) S.tile = int(atomicAdd(a.tile_ctr, 1u));
+  __shared__ uint32_t s_cut;  // the tile's row cutoff (distance-sorted copy)
+  if (tid == 0) {
+    S.tile = int(atomicAdd(a.tile_ctr, 1u));
+    s_cut = 0u;
+  }
   __syncthreads();
   while (true) {
     const int tile = S.tile;
@@ -971,9 +977,10 @@ __global__ void __launch_bounds__(kBT, CAPT_K5_MINB) k_binned_scan(BinArgs a) {
     const int cnt = tm.cnt;
     const uint2 st = make_uint2(tm.setx, tm.m);
     const float4 org = tm.org;
-    const uint32_t m = st.y;
+    uint32_t m = st.y;  // (shrinks to the sorted copy's cutoff after the first barrier)
     const uint32_t m4 = (m + 3u) & ~3u;
-    const float* xs = reinterpret_cast<const float*>(t.data + st.x);
+    const float* xs = t.sdata ? t.sdata + int64_t(st.x) * 4
+                              : reinterpret_cast<const float*>(t.data + st.x);
 
     // thread -> (sphere slot of kS spheres, phase over the point pairs)
     const int nslot = (cnt + kS - 1) / kS;
@@ -986,7 +993,8 @@ __global__ void __launch_bounds__(kBT, CAPT_K5_MINB) k_binned_scan(BinArgs a) {
     StagedRows rows;
     stage_load(rows, xs, m4, 0, min(uint32_t(kChunk), m));
     Spheres8 sp;
-    load_spheres(sp, S, a, s0, org, cnt, slot, active, active && ph == 0);
+    load_spheres(sp, S, a, s0, org, cnt, slot, active, active && ph == 0,
+                 t.sdata ? &s_cut : nullptr);
     for (int e = tid; e < nslot * kS; e += kBT) S.minkey[e] = 0xffffffffu;
     for (int e = tid; e < nslot; e += kBT) S.hitmask[e] = 0;
     stage_store(rows, sA, sB, (min(uint32_t(kChunk), m) + 7u) & ~7u, org);
@@ -1002,6 +1010,8 @@ __global__ void __launch_bounds__(kBT, CAPT_K5_MINB) k_binned_scan(BinArgs a) {
         stage_store(rows, sA, sB, len8, org);
       }
       __syncthreads();  // chunk staged; inits and limits visible
+      if (c0 == 0 && t.sdata)
+        m = min(m, sorted_limit(t.sdist + int64_t(st.x) * 4 / 3, m4, __uint_as_float(s_cut)));
       if (!done) {
         scan_pairs(sp, sA, sB, int(len8 / 2), ph, P, &S.hitmask[slot], S.lim_lo);
         uint32_t h = definite_hits(sp, S.lim_lo);
@@ -1018,6 +1028,7 @@ __global__ void __launch_bounds__(kBT, CAPT_K5_MINB) k_binned_scan(BinArgs a) {
     __syncthreads();
     if (tid == 32) S.tile = next;  // every thread has read S.tile by now
     if (active && ph == 0) decide(sp, S, a, s0, leaf, S.hitmask[slot], P > 1);
+    if (tid == 0) s_cut = 0u;
     __syncthreads();  // tile state (minkey, hitmask, smem points) free for the next tile
   }
 }
