@@ -244,3 +244,33 @@ def test_field_forced_mode_rejects_f64():
     c, r = W.cfg0_queries(1024)
     with pytest.raises(ValueError, match="clearance-field"):
         q(tree, c.astype(np.float64) + 1e-12, r.astype(np.float64))
+
+
+def test_stage_timing_abi():
+    # capt_stage_timing / capt_stage_times: events around K0 and the list
+    # stage of field-pipeline calls (bench.py's roofline split)
+    import ctypes
+    torch = pytest.importorskip("torch")
+    z = load_golden("cfg0.npz")
+    tree = upload(golden_tree(z, ""))
+    c, r = W.cfg0_queries(1 << 18)
+    cd, rd = torch.from_numpy(c).cuda(), torch.from_numpy(r).cuda()
+    L = _lib.lib()
+    ms = (ctypes.c_double * 3)()
+    calls = ctypes.c_int64(0)
+    assert L.capt_stage_timing(1) == 0
+    for _ in range(3):
+        P.query_bits(tree, cd, rd, 1)
+    torch.cuda.synchronize()
+    assert L.capt_stage_times(ms, ctypes.byref(calls)) == 0
+    assert calls.value == 3
+    assert ms[0] > 0 and ms[1] > 0 and abs(ms[2] - ms[0] - ms[1]) < 1e-6
+    # the record is cleared by the read; disabled timing records nothing
+    assert L.capt_stage_times(ms, ctypes.byref(calls)) == 0 and calls.value == 0
+    assert L.capt_stage_timing(0) == 0
+    P.query_bits(tree, cd, rd, 1)
+    torch.cuda.synchronize()
+    assert L.capt_stage_times(ms, ctypes.byref(calls)) == 0 and calls.value == 0
+    exp = O.collides_many(golden_tree(z, ""), c, r)
+    got = P.collides_many(tree, c, r)
+    assert np.array_equal(got, exp)
