@@ -809,7 +809,7 @@ __global__ void __launch_bounds__(256) k_resolve_list(FieldArgs a) {
     // rows to scan: with the distance-sorted copy, only those within
     // r + |c - o| of the set's origin (fl, rounded up: see sorted_limit)
     uint32_t lime = m4e;
-    if (scan32 && t.sdata) {
+    if (scan32 && t.sdata && m4e > 256u) {  // (short sets: scanning beats the search)
       const float4 o = __ldg(t.org + leaf);
       const float e = sqrtf(d2_fma(cx - o.x, cy - o.y, cz - o.z));
       const float cut = __fmul_ru(__fadd_ru(r, e), 1.0f + 0x1p-18f);
@@ -904,7 +904,16 @@ __global__ void __launch_bounds__(256) k_resolve_list(FieldArgs a) {
       const double r64 = __shfl_sync(0xffffffffu, double(r), src);
       const uint2 sset = make_uint2(__shfl_sync(0xffffffffu, set.x, src),
                                     __shfl_sync(0xffffffffu, set.y, src));
-      const bool h64 = warp_scan_f64(t, sset, c64, r64, lane);
+      const uint32_t slim = __shfl_sync(0xffffffffu, lime, src);
+      const bool sfast = __shfl_sync(0xffffffffu, st == 2, src);
+      const uint32_t sm4 = (sset.y + 3u) & ~3u;
+      // a fast sphere's rows beyond its cutoff are float64 misses: the sorted
+      // copy's first slim rows hold every possible hit
+      const bool h64 =
+          (sfast && t.sdata)
+              ? warp_scan_f64_rows(t.sdata + int64_t(sset.x) * 4, sm4, min(slim, sset.y),
+                                   t.k, c64, __dmul_rn(r64, r64), lane)
+              : warp_scan_f64(t, sset, c64, r64, lane);
       if (lane == src) verdict = h64;
     }
     // one OR per hit sphere (L = 1) or per group (first hitting lane)

@@ -213,28 +213,43 @@ __device__ __forceinline__ int warp_scan_f32(const DevTree& t, uint2 set, float 
 }
 
 // Exact reference scan (query.py:96-99), one point per lane per step.
-__device__ __forceinline__ bool warp_scan_f64(const DevTree& t, uint2 set, const double c[3],
-                                              double r64, int lane) {
-  const float* base = reinterpret_cast<const float*>(t.data + set.x);
-  const uint32_t m4 = (set.y + 3u) & ~3u;
-  const double R = __dmul_rn(r64, r64);
-  for (uint32_t p0 = 0; p0 < set.y; p0 += 32) {
-    const uint32_t p = p0 + lane;
+// Exact scan of rows [0, rows) of a set stored SoA with stride m4 from base:
+// 128 rows per step (4 per lane, all loads in flight), warp vote per step.
+__device__ __forceinline__ bool warp_scan_f64_rows(const float* base, uint32_t m4, uint32_t rows,
+                                                   int k, const double c[3], double R, int lane) {
+  for (uint32_t p0 = 0; p0 < rows; p0 += 128) {
+    float v[4][kMaxK];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t p = p0 + 32 * u + lane;
+      const uint32_t pc = p < rows ? p : 0u;
+#pragma unroll
+      for (int d = 0; d < kMaxK; ++d) v[u][d] = d < k ? __ldg(base + d * m4 + pc) : 0.f;
+    }
     bool hit = false;
-    if (p < set.y) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (p0 + 32 * u + lane >= rows) continue;
       double s = 0.0;
 #pragma unroll
       for (int d = 0; d < kMaxK; ++d) {
-        if (d >= t.k) break;
-        const double x = __dsub_rn(c[d], double(__ldg(base + d * m4 + p)));
+        if (d >= k) break;
+        const double x = __dsub_rn(c[d], double(v[u][d]));
         const double sq = __dmul_rn(x, x);
         s = (d == 0) ? sq : __dadd_rn(s, sq);
       }
-      hit = s <= R;
+      hit |= s <= R;
     }
     if (__any_sync(0xffffffffu, hit)) return true;
   }
   return false;
+}
+
+__device__ __forceinline__ bool warp_scan_f64(const DevTree& t, uint2 set, const double c[3],
+                                              double r64, int lane) {
+  const float* base = reinterpret_cast<const float*>(t.data + set.x);
+  const uint32_t m4 = (set.y + 3u) & ~3u;
+  return warp_scan_f64_rows(base, m4, set.y, t.k, c, __dmul_rn(r64, r64), lane);
 }
 
 // first row of a distance-sorted set beyond `cut` (binary search over 64-row items)
