@@ -392,9 +392,24 @@ __device__ __forceinline__ Chunk load_chunk(const float* __restrict__ cf,
 
 // The common tail of a decided chunk: first_bad, lane-group resolution, the
 // verdict bits, the list of undecided spheres (in sphere order).
+// A CTA's list entries collect in shared memory (one shared atomic per warp
+// and chunk instead of a returning global atomic on every chunk's critical
+// path) and are copied out once at the end of the kernel; a full buffer
+// falls back to direct appends.
+#ifndef CAPT_K0_LISTBUF
+#define CAPT_K0_LISTBUF 4096
+#endif
+constexpr int kListBuf = CAPT_K0_LISTBUF;
+struct ListBuf {
+  uint32_t* buf;  // shared memory (nullptr: append to the global list directly)
+  uint32_t* n;    // entries reserved in buf (may run past kListBuf)
+  uint32_t* end;  // the first reservation that did not fit (its range is a hole)
+};
+
 template <int LT>
 __device__ __forceinline__ void emit_chunk(const FieldArgs& a, int ch, int lane, bool check,
-                                           unsigned hitb, unsigned undb, unsigned badb) {
+                                           unsigned hitb, unsigned undb, unsigned badb,
+                                           ListBuf lb = {nullptr, nullptr, nullptr}) {
   const int n = a.n;
   const int q0 = (ch << 7) + 4 * lane;
   if (check && __any_sync(0xffffffffu, badb != 0)) {
@@ -458,11 +473,21 @@ __device__ __forceinline__ void emit_chunk(const FieldArgs& a, int ch, int lane,
     }
     const int tot = __shfl_sync(0xffffffffu, incl, 31);
     unsigned base = 0;
-    if (lane == 0) base = atomicAdd(a.list_n, unsigned(tot));
+    bool local = false;
+    if (lane == 0) {
+      if (lb.buf) {
+        base = atomicAdd(lb.n, unsigned(tot));
+        local = base + unsigned(tot) <= unsigned(kListBuf);
+        if (!local && base < unsigned(kListBuf)) atomicMin(lb.end, base);
+      }
+      if (!local) base = atomicAdd(a.list_n, unsigned(tot));
+    }
     base = __shfl_sync(0xffffffffu, base, 0) + unsigned(incl - cnt);
+    local = __shfl_sync(0xffffffffu, local, 0);
+    uint32_t* dst = local ? lb.buf : a.list;
 #pragma unroll
     for (int v = 0; v < 4; ++v)
-      if ((lst >> v) & 1u) a.list[base + __popc(lst & ((1u << v) - 1u))] = uint32_t(q0 + v);
+      if ((lst >> v) & 1u) dst[base + __popc(lst & ((1u << v) - 1u))] = uint32_t(q0 + v);
   }
 }
 
@@ -472,7 +497,7 @@ __device__ __forceinline__ void emit_chunk(const FieldArgs& a, int ch, int lane,
 template <bool kMask, int LT, bool kFull>
 __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeom& g,
                                               const Chunk& k, int ch, int lane, bool check,
-                                              uint64_t pol) {
+                                              uint64_t pol, ListBuf lb = {nullptr, nullptr, nullptr}) {
   const float x[4] = {k.p0.x, k.p0.w, k.p1.z, k.p2.y};
   const float y[4] = {k.p0.y, k.p1.x, k.p1.w, k.p2.z};
   const float z[4] = {k.p0.z, k.p1.y, k.p2.x, k.p2.w};
@@ -537,7 +562,7 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
 #pragma unroll
     for (int v = 0; v < 4; ++v) cert(v);
   }
-  emit_chunk<LT>(a, ch, lane, check, hitb, undb, badb);
+  emit_chunk<LT>(a, ch, lane, check, hitb, undb, badb, lb);
 }
 
 // K0 CTAs per SM the register allocation must allow: one chunk per warp in
@@ -560,6 +585,14 @@ __global__ void __launch_bounds__(256, CAPT_K0_MINB) k_resolve(FieldArgs a) {
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t pol = l2_keep_policy();
+  __shared__ uint32_t s_list[kListBuf];
+  __shared__ uint32_t s_ln, s_end, s_gbase;
+  if (threadIdx.x == 0) {
+    s_ln = 0u;
+    s_end = uint32_t(kListBuf);
+  }
+  __syncthreads();
+  const ListBuf lb = {s_list, &s_ln, &s_end};
   // (launched after k_field_zero with programmatic serialisation)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -567,7 +600,7 @@ __global__ void __launch_bounds__(256, CAPT_K0_MINB) k_resolve(FieldArgs a) {
 #ifndef CAPT_K0_PREFETCH  // one chunk in registers: 166 us at 4 CTAs/SM vs 175 (ping-pong, 3 CTAs)
   for (; ch < nfull; ch += nwarps) {
     const Chunk A = load_chunk<kVec, true>(a.c, a.r, ch, lane, n);
-    resolve_chunk<kMask, LT, !kMask>(a, g, A, ch, lane, check, pol);
+    resolve_chunk<kMask, LT, !kMask>(a, g, A, ch, lane, check, pol, lb);
   }
   if (false) {
 #else
@@ -588,8 +621,14 @@ __global__ void __launch_bounds__(256, CAPT_K0_MINB) k_resolve(FieldArgs a) {
   }
   if ((n & 127) && w0 == nfull % nwarps) {
     const Chunk T = load_chunk<false>(a.c, a.r, nfull, lane, n);
-    resolve_chunk<kMask, LT, false>(a, g, T, nfull, lane, check, pol);
+    resolve_chunk<kMask, LT, false>(a, g, T, nfull, lane, check, pol, lb);
   }
+  // the CTA's buffered list entries, in one reservation
+  __syncthreads();
+  const uint32_t cnt = min(s_ln, s_end);  // (entries past a non-fitting reservation went global)
+  if (threadIdx.x == 0 && cnt) s_gbase = atomicAdd(a.list_n, cnt);
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) a.list[s_gbase + i] = s_list[i];
 }
 
 // K0 with TMA bulk copies (the default for unmasked, 16-B aligned batches).
