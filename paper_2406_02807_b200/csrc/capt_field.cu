@@ -585,14 +585,17 @@ __global__ void __launch_bounds__(256, CAPT_K0_MINB) k_resolve(FieldArgs a) {
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t pol = l2_keep_policy();
-  __shared__ uint32_t s_list[kListBuf];
+  __shared__ uint32_t s_list[LT == 8 ? 1 : kListBuf];
   __shared__ uint32_t s_ln, s_end, s_gbase;
   if (threadIdx.x == 0) {
     s_ln = 0u;
     s_end = uint32_t(kListBuf);
   }
   __syncthreads();
-  const ListBuf lb = {s_list, &s_ln, &s_end};
+  // (8-sphere groups: most groups resolve on a hit, lists are short -- the
+  // buffer's shared memory would cost the record loads L1 capacity instead:
+  // config 1 K0 170 vs 166 us)
+  const ListBuf lb = LT == 8 ? ListBuf{nullptr, nullptr, nullptr} : ListBuf{s_list, &s_ln, &s_end};
   // (launched after k_field_zero with programmatic serialisation)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
