@@ -432,6 +432,9 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
       // non-finite centre with a finite radius never collides (float64 r^2 is finite)
       int st = fast ? 2 : ((!cfin && isfinite(r[v])) ? 0 : 3);
       st = valid[v] ? st : 0;
+      // list mode: the clearance field's octant certificate first
+      if (kList && st == 2 && octant_free_t(t, a.rlo_f, a.rhi_f, cx[v], cy[v], cz[v], r[v]))
+        st = 0;
       // one 32-B load: representative + outward-rounded fp16 box
       float pr[8];
       ld_v8(t.probe + 8 * leaf[v], pr);

@@ -1290,13 +1290,16 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   int rc = CAPT_OK;
   FieldArgs a2 = a;  // the filtered list (binned path)
   if (binned) {
-    // octant filter first: the binned pipeline's cost follows its list
-    CAPT_CUDA(dmalloc(&a2.list_n, 1, s));
-    CAPT_CUDA(dmalloc(&a2.list, n, s));
-    CAPT_CUDA(cudaMemsetAsync(a2.list_n, 0, 4, s));
-    k_list_octant<<<grid_for(int64_t(n) / 64 + 1, 256, 2), 256, 0, s>>>(a, a2.list, a2.list_n);
-    CAPT_CUDA(cudaGetLastError());
-    note_launches(1);
+    // (K1 in list mode applies the octant certificate itself)
+    static const bool filt = getenv("CAPT_OCT_FILTER") != nullptr;
+    if (filt) {
+      CAPT_CUDA(dmalloc(&a2.list_n, 1, s));
+      CAPT_CUDA(dmalloc(&a2.list, n, s));
+      CAPT_CUDA(cudaMemsetAsync(a2.list_n, 0, 4, s));
+      k_list_octant<<<grid_for(int64_t(n) / 64 + 1, 256, 2), 256, 0, s>>>(a, a2.list, a2.list_n);
+      CAPT_CUDA(cudaGetLastError());
+      note_launches(1);
+    }
     rc = launch_binned(t, centers, radii, n, L, nullptr, flags, bits, n_words, first_bad, s,
                        a2.list, a2.list_n);
   } else {
@@ -1319,7 +1322,7 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   if (debug) {
     uint32_t nl = 0, nl2 = 0;
     CAPT_CUDA(cudaMemcpyAsync(&nl, a.list_n, 4, cudaMemcpyDeviceToHost, s));
-    if (binned) CAPT_CUDA(cudaMemcpyAsync(&nl2, a2.list_n, 4, cudaMemcpyDeviceToHost, s));
+    if (a2.list != a.list) CAPT_CUDA(cudaMemcpyAsync(&nl2, a2.list_n, 4, cudaMemcpyDeviceToHost, s));
     CAPT_CUDA(cudaStreamSynchronize(s));
     fprintf(stderr, "[capt field] n=%lld L=%d undecided=%u (%.3f%%) after octants=%u (%.3f%%) list=%s\n",
             (long long)n, L, nl, 100.0 * nl / double(n ? n : 1), nl2, 100.0 * nl2 / double(n ? n : 1),
@@ -1327,7 +1330,7 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   }
   cudaFreeAsync(a.list, s);
   cudaFreeAsync(a.list_n, s);
-  if (binned) {
+  if (a2.list != a.list) {
     cudaFreeAsync(a2.list, s);
     cudaFreeAsync(a2.list_n, s);
   }

@@ -264,4 +264,27 @@ __device__ __forceinline__ uint32_t sorted_limit(const float* __restrict__ sd, u
   return min(m4, lo * 64u);  // every row at or after it is beyond cut
 }
 
+// The clearance field's octant certificate (capt_field.cu): true when the
+// octant of c's cell holds an fp16 distance bound above fl(r (1 + 2^-20)) --
+// then no cloud point lies within r of c (in-band radius, c inside the grid).
+__device__ __forceinline__ bool octant_free_t(const DevTree& t, float rlo, float rhi, float x,
+                                              float y, float z, float r) {
+  const FieldGeom& g = t.fg;
+  const int ix = __float2int_rd(__fmul_rn(__fsub_rn(x, g.lo[0]), g.inv_h));
+  const int iy = __float2int_rd(__fmul_rn(__fsub_rn(y, g.lo[1]), g.inv_h));
+  const int iz = __float2int_rd(__fmul_rn(__fsub_rn(z, g.lo[2]), g.inv_h));
+  const bool in = unsigned(ix) < unsigned(g.nx) && unsigned(iy) < unsigned(g.ny) &&
+                  unsigned(iz) < unsigned(g.nz);
+  if (!t.field || !in || !(r >= rlo && r <= rhi)) return false;
+  auto centre = [&](int i, float c0) { return __fmaf_rn(__int2float_rn(i), g.h, c0); };
+  const unsigned o = (x - centre(ix, g.c0[0]) >= 0.f ? 1u : 0u) |
+                     (y - centre(iy, g.c0[1]) >= 0.f ? 2u : 0u) |
+                     (z - centre(iz, g.c0[2]) >= 0.f ? 4u : 0u);
+  const size_t cell =
+      (size_t(iz) * unsigned(g.ny) + unsigned(iy)) * unsigned(g.nx) + unsigned(ix);
+  const unsigned short hb =
+      __ldg(reinterpret_cast<const unsigned short*>(t.field + g.cells) + 8 * cell + o);
+  return __half2float(__ushort_as_half(hb)) > r * (1.0f + 0x1p-20f);
+}
+
 }  // namespace capt
