@@ -663,7 +663,10 @@ extern "C" int capt_query(const capt_tree* tree, const void* centers, const void
   const size_t in_elem = (flags & CAPT_INPUT_F64) ? sizeof(double) : sizeof(float);
 
   // group-sequential counters (STATS with lane groups) are additive per chunk
-  const int64_t chunk = int64_t(1) << 22;  // spheres per pipeline chunk (multiple of 32 * L)
+#ifndef CAPT_PIPE_CHUNK_LOG2
+#define CAPT_PIPE_CHUNK_LOG2 22
+#endif
+  const int64_t chunk = int64_t(1) << CAPT_PIPE_CHUNK_LOG2;  // spheres per pipeline chunk (multiple of 32 * L)
   if (host && n > chunk) {
     return query_host_pipelined(tree, t, centers, radii, n, L, lane_mask, flags, out_bits,
                                 counters, first_bad, s, chunk);
