@@ -274,3 +274,17 @@ def test_stage_timing_abi():
     exp = O.collides_many(golden_tree(z, ""), c, r)
     got = P.collides_many(tree, c, r)
     assert np.array_equal(got, exp)
+
+
+def test_field_unaligned_inputs_and_f64_exact():
+    # views 12 / 4 bytes into their buffers (no 128-bit loads: the scalar K0
+    # path), and float64 arrays holding fp32 values (converted, fp32 path)
+    z = load_golden("cfg0.npz")
+    t = golden_tree(z, "")
+    tree = upload(t)
+    c, r = W.cfg0_queries((1 << 17) + 1)
+    cu, ru = c[1:], r[1:]
+    assert cu.ctypes.data % 16 and ru.ctypes.data % 16
+    exp = O.collides_many(t, cu, ru)
+    assert np.array_equal(q(tree, cu, ru), exp)
+    assert np.array_equal(P.collides_many(tree, cu.astype(np.float64), ru.astype(np.float64)), exp)
