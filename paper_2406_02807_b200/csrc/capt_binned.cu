@@ -823,7 +823,7 @@ __device__ __forceinline__ void load_spheres(Spheres8& sp, SmemBinned& S, const 
           S.lim_lo[e] = thr - band;
           S.lim_hi[e] = thr + band;
           if (cut)  // sorted copy: the tile's row cutoff (see k_binned_scan_tc)
-            atomicMax(cut, __float_as_uint(__fmul_ru(__fadd_ru(rc.w, sqrtf(aa)), 1.0f + 0x1p-18f)));
+            atomicMax(cut, __float_as_uint(__fmul_ru(__fadd_ru(fabsf(rc.w), sqrtf(aa)), 1.0f + 0x1p-18f)));
         }
       }
     }
@@ -1164,7 +1164,7 @@ __global__ void __launch_bounds__(kTcThreads) k_binned_scan_tc(BinArgs a) {
         const float4 rc = a.lrec[a.perm[tm.s0 + e]];
         const float dx = rc.x - org.x, dy = rc.y - org.y, dz = rc.z - org.z;
         const float ex = sqrtf(fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
-        atomicMax(&s_cut, __float_as_uint(__fmul_ru(__fadd_ru(rc.w, ex), 1.0f + 0x1p-18f)));
+        atomicMax(&s_cut, __float_as_uint(__fmul_ru(__fadd_ru(fabsf(rc.w), ex), 1.0f + 0x1p-18f)));
       }
       __syncthreads();
       m = min(m, sorted_limit(t.sdist + int64_t(tm.setx) * 4 / 3, m4, __uint_as_float(s_cut)));
@@ -1298,9 +1298,25 @@ __global__ void k_slow(BinArgs a) {
     const int2 e = a.slow[i];
     double c64[3], r64;
     load_sphere<InT>(a.centers, a.radii, e.x, t.k, c64, r64);
-    const uint2 st = t.set[e.y];
+    uint2 st = t.set[e.y];
     const float* base = reinterpret_cast<const float*>(t.data + st.x);
     const uint32_t m4 = (st.y + 3u) & ~3u;
+    // distance-sorted copy: an fp32 sphere's possible hits are the rows up to
+    // its cutoff r + |c - org| (rows beyond are float64 misses with a margin)
+    if (t.sdata && t.k == 3) {
+      const float cf[3] = {float(c64[0]), float(c64[1]), float(c64[2])};
+      const float rf = float(r64);
+      if (double(cf[0]) == c64[0] && double(cf[1]) == c64[1] && double(cf[2]) == c64[2] &&
+          double(rf) == r64 && isfinite(cf[0]) && isfinite(cf[1]) && isfinite(cf[2]) &&
+          fabsf(rf) <= 1e30f) {
+        const float4 o = __ldg(t.org + e.y);
+        const float dx = cf[0] - o.x, dy = cf[1] - o.y, dz = cf[2] - o.z;
+        const float cut = __fmul_ru(__fadd_ru(fabsf(rf), sqrtf(fmaf(dz, dz, fmaf(dy, dy, dx * dx)))),
+                                    1.0f + 0x1p-18f);
+        st.y = min(st.y, sorted_limit(t.sdist + int64_t(st.x) * 4 / 3, m4, cut));
+        base = t.sdata + int64_t(st.x) * 4;
+      }
+    }
     // fp32 first pass in the direct form (relative error < 5u, band TAU as in
     // the direct kernels): most spheres the binned scan left ambiguous (its
     // band is wider) are decided here; the rest take the float64 pass

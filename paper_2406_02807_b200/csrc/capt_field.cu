@@ -854,7 +854,8 @@ __global__ void __launch_bounds__(256) k_resolve_list(FieldArgs a) {
     if (scan32 && t.sdata && m4e > 256u) {  // (short sets: scanning beats the search)
       const float4 o = __ldg(t.org + leaf);
       const float e = sqrtf(d2_fma(cx - o.x, cy - o.y, cz - o.z));
-      const float cut = __fmul_ru(__fadd_ru(r, e), 1.0f + 0x1p-18f);
+      // (|r|: a negative radius collides like its magnitude, d^2 <= r*r)
+      const float cut = __fmul_ru(__fadd_ru(fabsf(r), e), 1.0f + 0x1p-18f);
       lime = sorted_limit(t.sdist + int64_t(set.x) * 4 / 3, m4e, cut);
     }
     const uint32_t items = (lime + 63u) >> 6;

@@ -199,6 +199,7 @@ def test_field_edge_inputs(lp):
     c[7::983] = np.float32(1e30)
     r[11::977] = np.nan
     r[13::971] = np.inf
+    r[17::89] *= -1  # negative radii collide like their magnitude (d^2 <= r*r)
     exp = O.collides_many(t, c, r)
     assert np.array_equal(q(tree, c, r, mode=LIST[lp]), exp)
     assert np.array_equal(q(tree, c, r, prefilter=False, mode=LIST[lp]), O.collides_many(t, c, r, False))
