@@ -576,7 +576,10 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
 // registers: the next chunk's loads are in flight while one is decided); the
 // last, partial chunk (scalar loads, per-sphere validity) after the loop
 template <bool kVec, bool kMask, int LT>
-__global__ void __launch_bounds__(256, CAPT_K0_MINB) k_resolve(FieldArgs a) {
+#ifndef CAPT_K0_BLOCK
+#define CAPT_K0_BLOCK 256
+#endif
+__global__ void __launch_bounds__(CAPT_K0_BLOCK, CAPT_K0_MINB) k_resolve(FieldArgs a) {
   const FieldGeom g = a.t.fg;
   const bool check = a.flags & CAPT_CHECK_RADII;
   const int n = a.n;
@@ -1252,7 +1255,7 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   if (tcall >= 0) g_stage.record(tcall, 0, s);
   const bool vec = (reinterpret_cast<uintptr_t>(centers) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(radii) & 15) == 0;
-  const int grid = grid_for(((n + 127) / 128) * 32, 256, 8);
+  const int grid = grid_for(((n + 127) / 128) * 32, CAPT_K0_BLOCK, 8 * 256 / CAPT_K0_BLOCK);
   // unmasked 16-B aligned batches: the TMA-fed kernel (specialised for single
   // spheres and 8-sphere groups, configs 0-4); everything else the register path
   static const bool use_tma = getenv("CAPT_K0_TMA") != nullptr;
@@ -1268,10 +1271,10 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
     else if (L == 8) k_resolve_tma<8><<<gt, 256, kTmaSmem, s>>>(a);
     else k_resolve_tma<0><<<gt, 256, kTmaSmem, s>>>(a);
   }
-  else if (vec && !mask && L == 1) CAPT_CUDA(launch_pdl_f(k_resolve<true, false, 1>, grid, 256, s, a));
-  else if (vec && !mask && L == 8) CAPT_CUDA(launch_pdl_f(k_resolve<true, false, 8>, grid, 256, s, a));
-  else if (mask) CAPT_CUDA(launch_pdl_f(k_resolve<false, true, 0>, grid, 256, s, a));
-  else CAPT_CUDA(launch_pdl_f(k_resolve<false, false, 0>, grid, 256, s, a));
+  else if (vec && !mask && L == 1) CAPT_CUDA(launch_pdl_f(k_resolve<true, false, 1>, grid, CAPT_K0_BLOCK, s, a));
+  else if (vec && !mask && L == 8) CAPT_CUDA(launch_pdl_f(k_resolve<true, false, 8>, grid, CAPT_K0_BLOCK, s, a));
+  else if (mask) CAPT_CUDA(launch_pdl_f(k_resolve<false, true, 0>, grid, CAPT_K0_BLOCK, s, a));
+  else CAPT_CUDA(launch_pdl_f(k_resolve<false, false, 0>, grid, CAPT_K0_BLOCK, s, a));
   CAPT_CUDA(cudaGetLastError());
   note_launches(1);
   if (tcall >= 0) g_stage.record(tcall, 1, s);
