@@ -545,17 +545,22 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
     const bool decided = inband[v] && (!look[v] || hit || free);
     undb |= unsigned(valid[v] && !decided && !bad) << v;
   };
-  if (LT == 8) {
-    // 8-sphere groups span lanes (2j, 2j+1): the first sphere of each lane
-    // goes first; a group with a hit fetches no more records (query.py:152-160
-    // early exit, applied to the L2 traffic -- K0 is bound by it)
-    cell(0, false);
-    cert(0);
-    const bool any0 = __shfl_xor_sync(0xffffffffu, hitb, 1) | hitb;
+  const int L = LT ? LT : a.L;
+  if (L >= 4) {
+    // groups of L >= 4 spheres span L/4 whole lanes; a group with a hit
+    // fetches no more records (query.py:152-160 early exit, applied to the
+    // L2 traffic -- K0 is bound by it): one sphere per lane per round, each
+    // round's records fetched only for the groups still without a hit
+    // (config 1 K0: 158 us vs 167 with the lane's last three spheres in one
+    // round, 206 with all four at once)
+    bool any = false;
 #pragma unroll
-    for (int v = 1; v < 4; ++v) cell(v, any0);
-#pragma unroll
-    for (int v = 1; v < 4; ++v) cert(v);
+    for (int v = 0; v < 4; ++v) {
+      cell(v, any);
+      cert(v);
+      any = hitb != 0u;
+      for (int o = 1; o < L / 4; o <<= 1) any |= __shfl_xor_sync(0xffffffffu, any, o);
+    }
   } else {
 #pragma unroll
     for (int v = 0; v < 4; ++v) cell(v, false);
