@@ -561,6 +561,17 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
       any = hitb != 0u;
       for (int o = 1; o < L / 4; o <<= 1) any |= __shfl_xor_sync(0xffffffffu, any, o);
     }
+  } else if (L == 2) {
+    // pairs (0, 1) and (2, 3) of the lane: the second sphere of a pair is
+    // fetched only if the first did not hit
+    cell(0, false);
+    cell(2, false);
+    cert(0);
+    cert(2);
+    cell(1, (hitb & 1u) != 0u);
+    cell(3, (hitb & 4u) != 0u);
+    cert(1);
+    cert(3);
   } else {
 #pragma unroll
     for (int v = 0; v < 4; ++v) cell(v, false);
