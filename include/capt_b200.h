@@ -105,9 +105,12 @@ int capt_tree_export(const capt_tree* tree, float* tests, float* aff_lo,
 void capt_tree_destroy(capt_tree* tree);
 
 /* Position-independent device slab (for replication across GPUs: NCCL
- * broadcast the slab bytes, then capt_tree_from_slab on each rank). */
+ * broadcast the slab bytes, then capt_tree_from_slab on each rank).  With
+ * CAPT_SLAB_BORROW the new tree adopts dev_slab instead of copying it (the
+ * caller keeps the buffer alive and unchanged until capt_tree_destroy). */
+#define CAPT_SLAB_BORROW 0x1u
 int capt_tree_slab(const capt_tree* tree, const void** dev_ptr, int64_t* bytes);
-int capt_tree_from_slab(int device, const void* dev_slab, int64_t bytes,
+int capt_tree_from_slab(int device, const void* dev_slab, int64_t bytes, uint32_t flags,
                         void* stream, capt_tree** out);
 
 /* collides_many (query.py:184-219) when lane_width == 1; otherwise
@@ -155,24 +158,30 @@ int capt_nn_distances(int device, int k, const float* points, int64_t n,
 
 /* Clearance field of a k = 3 tree (derived data, built on the device with
  * the tree): a uniform grid of nx*ny*nz cells of edge h from lo; cell
- * (ix,iy,iz) is the 32-byte record (iz*ny + iy)*nx + ix = {witness x, y, z,
- * nn, 8 x fp16 octant bounds} with centre x0 = fmaf((float)ix, h, c0[0])
- * (likewise y, z).  witness = the cloud point nearest x0 (+inf if none within
- * rcap); nn <= the distance from x0 to every cloud point (nn <= rcap); the
- * fp16 bound o (bits 0/1/2 = x/y/z at or above x0) is <= the distance from
- * every point of the octant box [x0, x0 + oct_half] / [x0 - oct_half, x0]
- * (per axis) to every cloud point.  box_lo/box_hi: the cloud's box.
- * cells: NULL, or a host buffer of 8 * n_cells floats.  Returns CAPT_EINVAL
- * for trees without a field. */
+ * (ix,iy,iz) is number (iz*ny + iy)*nx + ix, with centre x0 =
+ * fmaf((float)ix, h, c0[0]) (likewise y, z).  Per cell:
+ *   witness = the cloud point nearest x0 (+inf if none within rcap);
+ *   nn <= the distance from x0 to every cloud point (nn <= rcap);
+ *   n_cand candidate points: the cloud points nearest x0 (fewer when fewer
+ *     lie within rcap), stored as int16 offsets q = rint((p - x0) / q_step)
+ *     per axis; a decoded difference fl(fl(c - x0) - q q_step) is within
+ *     q_err of c - p (Euclidean) for a centre c of the cell;
+ *   kd <= the distance from x0 to every cloud point that is not a candidate
+ *     (kd <= rcap, a multiple of q_step).
+ * box_lo/box_hi: the cloud's box.  cells: NULL, or a host buffer of
+ * 8 * n_cells floats {witness x, y, z, nn, kd, candidate count, 0, 0}.
+ * cand: NULL, or a host buffer of 3 * n_cand * n_cells floats (each
+ * candidate's offsets q, +inf for unused slots).  Returns CAPT_EINVAL for
+ * trees without a field. */
 typedef struct {
-  int32_t nx, ny, nz, reserved;
+  int32_t nx, ny, nz, n_cand;
   int64_t n_cells;
   float lo[3], h;
   float box_lo[3], box_hi[3];
-  float rcap, oct_half;
-  float c0[3], pad2;
+  float rcap, q_step;
+  float c0[3], q_err;
 } capt_field_info;
-int capt_tree_field(const capt_tree* tree, capt_field_info* info, float* cells);
+int capt_tree_field(const capt_tree* tree, capt_field_info* info, float* cells, float* cand);
 
 /* Stage timing of the clearance-field pipeline (measurement helper for
  * bench.py's roofline): while enabled, every field-pipeline capt_query

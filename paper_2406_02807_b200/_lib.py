@@ -28,6 +28,7 @@ MODE_THREAD = 0x400
 K5_FFMA = 0x800
 MODE_WARP = 0x1000
 MODE_FIELD = 0x2000
+SLAB_BORROW = 0x1  # capt_tree_from_slab flag
 
 
 class CaptTreeInfo(C.Structure):
@@ -40,10 +41,10 @@ class CaptTreeInfo(C.Structure):
 
 class CaptFieldInfo(C.Structure):
     _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32),
-                ("reserved", C.c_int32), ("n_cells", C.c_int64), ("lo", C.c_float * 3),
+                ("n_cand", C.c_int32), ("n_cells", C.c_int64), ("lo", C.c_float * 3),
                 ("h", C.c_float), ("box_lo", C.c_float * 3), ("box_hi", C.c_float * 3),
-                ("rcap", C.c_float), ("oct_half", C.c_float), ("c0", C.c_float * 3),
-                ("pad2", C.c_float)]
+                ("rcap", C.c_float), ("q_step", C.c_float), ("c0", C.c_float * 3),
+                ("q_err", C.c_float)]
 
 
 _lib = None
@@ -74,14 +75,14 @@ def lib():
     L.capt_tree_destroy.argtypes = [vp]
     L.capt_tree_destroy.restype = None
     L.capt_tree_slab.argtypes = [vp, C.POINTER(vp), C.POINTER(i64)]
-    L.capt_tree_from_slab.argtypes = [i32, vp, i64, vp, C.POINTER(vp)]
+    L.capt_tree_from_slab.argtypes = [i32, vp, i64, u32, vp, C.POINTER(vp)]
     L.capt_query.argtypes = [vp, vp, vp, i64, i32, vp, u32, vp, vp, vp, vp]
     L.capt_leaf_indices.argtypes = [vp, vp, i64, u32, vp, vp]
     L.capt_filter_cloud.argtypes = [i32, i32, vp, i64, dbl, i32, vp, dbl, u32, vp, vp, vp]
     L.capt_measure_fp32_peak.argtypes = [i32, C.POINTER(dbl)]
     L.capt_tc_selftest.argtypes = [i32, C.POINTER(dbl)]
     L.capt_nn_distances.argtypes = [i32, i32, vp, i64, u32, vp, vp]
-    L.capt_tree_field.argtypes = [vp, C.POINTER(CaptFieldInfo), vp]
+    L.capt_tree_field.argtypes = [vp, C.POINTER(CaptFieldInfo), vp, vp]
     L.capt_stage_timing.argtypes = [i32]
     L.capt_stage_times.argtypes = [C.POINTER(dbl), C.POINTER(i64)]
     L.capt_kernel_launches.restype = C.c_int64

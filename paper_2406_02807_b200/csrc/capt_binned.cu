@@ -293,10 +293,9 @@ constexpr int kSmemNodes3 = (1 << CAPT_K1_SMEM_LEVELS) - 1;
 #ifndef CAPT_K1_MINB
 #define CAPT_K1_MINB 4
 #endif
-// kList: the spheres are the clearance field's list (capt_field.cu) --
-// sphere ids a.qlist[0 .. *a.qlist_n), already masked and band-checked,
-// resolved one by one (a.L == 1; the caller ORs lane groups).
-template <int V, bool kList>
+// spheres in flight per K1 thread: 4 (339 us) beats 2 (442) and 6 (482)
+constexpr int kK1V = 4;
+template <int V>
 __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
   extern __shared__ __align__(16) float sT[];  // kSmemNodes3 floats (dynamic: may exceed 48 KB)
   const DevTree& t = a.t;
@@ -311,7 +310,7 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
   const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(sT));
   const int dsm = t.depth < CAPT_K1_SMEM_LEVELS ? t.depth : CAPT_K1_SMEM_LEVELS;
   const int nl1 = int(t.n - 1);
-  const int n = kList ? int(*a.qlist_n) : int(a.n);
+  const int n = int(a.n);
   const int n_pad = (n + 31) & ~31;
   const int lane = threadIdx.x & 31;
   const unsigned seg = a.L >= 32 ? 0xffffffffu : ((1u << a.L) - 1u) << ((lane / a.L) * a.L);
@@ -324,7 +323,7 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     const int q = blockIdx.x * blockDim.x * V + v * blockDim.x + threadIdx.x;
-    const int qq = q < n ? (kList ? int(__ldcs(a.qlist + q)) : q) : 0;
+    const int qq = q < n ? q : 0;
     nsid[v] = qq;
     nx[v] = __ldcs(cf + 3 * qq);
     ny[v] = __ldcs(cf + 3 * qq + 1);
@@ -344,7 +343,7 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
       r[v] = nr[v];
       sid[v] = nsid[v];
       const int qn = base + stride + v * blockDim.x + threadIdx.x;
-      const int qq = qn < n ? (kList ? int(__ldcs(a.qlist + qn)) : qn) : 0;
+      const int qq = qn < n ? qn : 0;
       nsid[v] = qq;
       nx[v] = __ldcs(cf + 3 * qq);
       ny[v] = __ldcs(cf + 3 * qq + 1);
@@ -355,10 +354,10 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
     for (int v = 0; v < V; ++v) {
       const int q = base + v * blockDim.x + threadIdx.x;
       valid[v] = q < n;
-      if (!kList && a.mask && valid[v]) valid[v] = a.mask[q] != 0;
+      if (a.mask && valid[v]) valid[v] = a.mask[q] != 0;
       off[v] = 0;
     }
-    if (!kList && check) {  // out-of-band radii are rare: one warp vote, then the atomics
+    if (check) {  // out-of-band radii are rare: one warp vote, then the atomics
       bool bad = false;
 #pragma unroll
       for (int v = 0; v < V; ++v) bad |= valid[v] && (r[v] < a.rlo_f || r[v] > a.rhi_f);
@@ -432,9 +431,6 @@ __global__ void __launch_bounds__(256, CAPT_K1_MINB) k_bin_count3(BinArgs a) {
       // non-finite centre with a finite radius never collides (float64 r^2 is finite)
       int st = fast ? 2 : ((!cfin && isfinite(r[v])) ? 0 : 3);
       st = valid[v] ? st : 0;
-      // list mode: the clearance field's octant certificate first
-      if (kList && st == 2 && octant_free_t(t, a.rlo_f, a.rhi_f, cx[v], cy[v], cz[v], r[v]))
-        st = 0;
       // one 32-B load: representative + outward-rounded fp16 box
       float pr[8];
       ld_v8(t.probe + 8 * leaf[v], pr);
@@ -797,7 +793,7 @@ struct Spheres8 {
 // slot's owner (phase 0) writes their decision limits.
 __device__ __forceinline__ void load_spheres(Spheres8& sp, SmemBinned& S, const BinArgs& a,
                                              int64_t s0, const float4 org, int count, int slot,
-                                             bool active, bool owner, uint32_t* cut = nullptr) {
+                                             bool active, bool owner) {
   const float INF = __int_as_float(0x7f800000);
   sp.real = 0;
   sp.base = slot * kS;
@@ -822,8 +818,6 @@ __device__ __forceinline__ void load_spheres(Spheres8& sp, SmemBinned& S, const 
           const float thr = r2 - aa, band = kBand * (aa + org.w + r2);
           S.lim_lo[e] = thr - band;
           S.lim_hi[e] = thr + band;
-          if (cut)  // sorted copy: the tile's row cutoff (see k_binned_scan_tc)
-            atomicMax(cut, __float_as_uint(__fmul_ru(__fadd_ru(fabsf(rc.w), sqrtf(aa)), 1.0f + 0x1p-18f)));
         }
       }
     }
@@ -961,11 +955,7 @@ __global__ void __launch_bounds__(kBT, CAPT_K5_MINB) k_binned_scan(BinArgs a) {
   const DevTree& t = a.t;
   const int tid = threadIdx.x;
   const int n_tiles = int(*a.n_tiles);
-  __shared__ uint32_t s_cut;  // the tile's row cutoff (distance-sorted copy)
-  if (tid == 0) {
-    S.tile = int(atomicAdd(a.tile_ctr, 1u));
-    s_cut = 0u;
-  }
+  if (tid == 0) S.tile = int(atomicAdd(a.tile_ctr, 1u));
   __syncthreads();
   while (true) {
     const int tile = S.tile;
@@ -980,10 +970,9 @@ __global__ void __launch_bounds__(kBT, CAPT_K5_MINB) k_binned_scan(BinArgs a) {
     const int cnt = tm.cnt;
     const uint2 st = make_uint2(tm.setx, tm.m);
     const float4 org = tm.org;
-    uint32_t m = st.y;  // (shrinks to the sorted copy's cutoff after the first barrier)
+    const uint32_t m = st.y;
     const uint32_t m4 = (m + 3u) & ~3u;
-    const float* xs = t.sdata ? t.sdata + int64_t(st.x) * 4
-                              : reinterpret_cast<const float*>(t.data + st.x);
+    const float* xs = reinterpret_cast<const float*>(t.data + st.x);
 
     // thread -> (sphere slot of kS spheres, phase over the point pairs)
     const int nslot = (cnt + kS - 1) / kS;
@@ -996,8 +985,7 @@ __global__ void __launch_bounds__(kBT, CAPT_K5_MINB) k_binned_scan(BinArgs a) {
     StagedRows rows;
     stage_load(rows, xs, m4, 0, min(uint32_t(kChunk), m));
     Spheres8 sp;
-    load_spheres(sp, S, a, s0, org, cnt, slot, active, active && ph == 0,
-                 t.sdata ? &s_cut : nullptr);
+    load_spheres(sp, S, a, s0, org, cnt, slot, active, active && ph == 0);
     for (int e = tid; e < nslot * kS; e += kBT) S.minkey[e] = 0xffffffffu;
     for (int e = tid; e < nslot; e += kBT) S.hitmask[e] = 0;
     stage_store(rows, sA, sB, (min(uint32_t(kChunk), m) + 7u) & ~7u, org);
@@ -1013,8 +1001,6 @@ __global__ void __launch_bounds__(kBT, CAPT_K5_MINB) k_binned_scan(BinArgs a) {
         stage_store(rows, sA, sB, len8, org);
       }
       __syncthreads();  // chunk staged; inits and limits visible
-      if (c0 == 0 && t.sdata)
-        m = min(m, sorted_limit(t.sdist + int64_t(st.x) * 4 / 3, m4, __uint_as_float(s_cut)));
       if (!done) {
         scan_pairs(sp, sA, sB, int(len8 / 2), ph, P, &S.hitmask[slot], S.lim_lo);
         uint32_t h = definite_hits(sp, S.lim_lo);
@@ -1031,7 +1017,6 @@ __global__ void __launch_bounds__(kBT, CAPT_K5_MINB) k_binned_scan(BinArgs a) {
     __syncthreads();
     if (tid == 32) S.tile = next;  // every thread has read S.tile by now
     if (active && ph == 0) decide(sp, S, a, s0, leaf, S.hitmask[slot], P > 1);
-    if (tid == 0) s_cut = 0u;
     __syncthreads();  // tile state (minkey, hitmask, smem points) free for the next tile
   }
 }
@@ -1108,12 +1093,8 @@ __global__ void __launch_bounds__(kTcThreads) k_binned_scan_tc(BinArgs a) {
     const int cnt = tm.cnt;
     const float4 org = tm.org;
     const uint32_t m4 = (tm.m + 3u) & ~3u;
-    // with the distance-sorted copy (capt_field.cu) the rows are ordered by
-    // |p - org| and the tile stops at the first row beyond every sphere's
-    // r + |c - org| (m shrinks below; rows before it are all real points)
-    uint32_t m = tm.m;
-    const float* xs = t.sdata ? t.sdata + int64_t(tm.setx) * 4
-                              : reinterpret_cast<const float*>(t.data + tm.setx);
+    const uint32_t m = tm.m;
+    const float* xs = reinterpret_cast<const float*>(t.data + tm.setx);
     const int nb = (cnt + 127) >> 7;  // sphere blocks in this tile
     // thread i < kTcNc stages row i of every chunk; the next chunk's point is
     // loaded while the current chunk's product runs (one chunk ahead), the
@@ -1155,20 +1136,6 @@ __global__ void __launch_bounds__(kTcThreads) k_binned_scan_tc(BinArgs a) {
 #pragma unroll
       for (int k = 11; k < 16; ++k) row[k] = 0.f;
       put_row(S.A, e, row);
-    }
-    if (t.sdata) {
-      __shared__ uint32_t s_cut;
-      if (tid == 0) s_cut = 0u;
-      __syncthreads();
-      if (tb < nb && e < cnt) {
-        const float4 rc = a.lrec[a.perm[tm.s0 + e]];
-        const float dx = rc.x - org.x, dy = rc.y - org.y, dz = rc.z - org.z;
-        const float ex = sqrtf(fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
-        atomicMax(&s_cut, __float_as_uint(__fmul_ru(__fadd_ru(fabsf(rc.w), ex), 1.0f + 0x1p-18f)));
-      }
-      __syncthreads();
-      m = min(m, sorted_limit(t.sdist + int64_t(tm.setx) * 4 / 3, m4, __uint_as_float(s_cut)));
-      __syncthreads();
     }
     bool done = false;
     for (uint32_t c0 = 0; c0 < m && !done; c0 += kTcNc) {
@@ -1298,25 +1265,9 @@ __global__ void k_slow(BinArgs a) {
     const int2 e = a.slow[i];
     double c64[3], r64;
     load_sphere<InT>(a.centers, a.radii, e.x, t.k, c64, r64);
-    uint2 st = t.set[e.y];
+    const uint2 st = t.set[e.y];
     const float* base = reinterpret_cast<const float*>(t.data + st.x);
     const uint32_t m4 = (st.y + 3u) & ~3u;
-    // distance-sorted copy: an fp32 sphere's possible hits are the rows up to
-    // its cutoff r + |c - org| (rows beyond are float64 misses with a margin)
-    if (t.sdata && t.k == 3) {
-      const float cf[3] = {float(c64[0]), float(c64[1]), float(c64[2])};
-      const float rf = float(r64);
-      if (double(cf[0]) == c64[0] && double(cf[1]) == c64[1] && double(cf[2]) == c64[2] &&
-          double(rf) == r64 && isfinite(cf[0]) && isfinite(cf[1]) && isfinite(cf[2]) &&
-          fabsf(rf) <= 1e30f) {
-        const float4 o = __ldg(t.org + e.y);
-        const float dx = cf[0] - o.x, dy = cf[1] - o.y, dz = cf[2] - o.z;
-        const float cut = __fmul_ru(__fadd_ru(fabsf(rf), sqrtf(fmaf(dz, dz, fmaf(dy, dy, dx * dx)))),
-                                    1.0f + 0x1p-18f);
-        st.y = min(st.y, sorted_limit(t.sdist + int64_t(st.x) * 4 / 3, m4, cut));
-        base = t.sdata + int64_t(st.x) * 4;
-      }
-    }
     // fp32 first pass in the direct form (relative error < 5u, band TAU as in
     // the direct kernels): most spheres the binned scan left ambiguous (its
     // band is wider) are decided here; the rest take the float64 pass
@@ -1416,21 +1367,6 @@ __global__ void k_pack(int64_t n_groups, int L, const uint8_t* __restrict__ v,
   }
 }
 
-// list mode: the listed spheres' verdict bytes -> OR into the verdict words
-// (bit q, or bit q / L for lane groups)
-__global__ void k_list_bits(const uint32_t* __restrict__ qlist, const uint32_t* __restrict__ qlist_n,
-                            const uint8_t* __restrict__ v, int L, uint32_t* __restrict__ bits) {
-  pdl_wait();
-  const uint32_t nq = *qlist_n;
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nq; j += gridDim.x * blockDim.x) {
-    const uint32_t q = qlist[j];
-    if (v[q]) {
-      const uint32_t b = L == 1 ? q : q / uint32_t(L);
-      atomicOr(bits + (b >> 5), 1u << (b & 31));
-    }
-  }
-}
-
 struct Arena {
   cudaStream_t s;
   void* ptrs[24];
@@ -1473,45 +1409,6 @@ static cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, siz
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
-// CAPT_STAGE_TIMING=1: CUDA events between the pipeline stages (in-loop
-// times, unlike a serialised profiler pass), summed over calls and printed at
-// exit.  Diagnostics only; adds a synchronisation per call.
-struct StageTimer {
-  static constexpr int kStages = 7;
-  bool on = getenv("CAPT_STAGE_TIMING") != nullptr;
-  cudaEvent_t ev[kStages + 1] = {};
-  double sum[kStages] = {};
-  long calls = 0;
-  StageTimer() {
-    if (on)
-      for (auto& e : ev) cudaEventCreate(&e);
-  }
-  ~StageTimer() {
-    if (!on || !calls) return;
-    static const char* names[kStages] = {"memsets", "K1 count", "K2 scans+tiles", "K3a bucket", "K3b leaf",
-                                         "K5 scan", "K6+K7 slow+pack"};
-    double tot = 0;
-    for (double v : sum) tot += v;
-    fprintf(stderr, "[capt stages] %ld calls, mean us per call:", calls);
-    for (int i = 0; i < kStages; ++i) fprintf(stderr, " %s=%.1f", names[i], 1e3 * sum[i] / calls);
-    fprintf(stderr, " total=%.1f\n", 1e3 * tot / calls);
-  }
-  void mark(int i, cudaStream_t s) {
-    if (on) cudaEventRecord(ev[i], s);
-  }
-  void finish(cudaStream_t s) {
-    if (!on) return;
-    cudaEventSynchronize(ev[kStages]);
-    for (int i = 0; i < kStages; ++i) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
-      sum[i] += ms;
-    }
-    ++calls;
-  }
-};
-static StageTimer g_stage_timer;
-
 bool binned_preferred(const DevTree& t, int64_t n, uint32_t flags) {
   if (flags & CAPT_STATS) return false;
   if (flags & (CAPT_MODE_DIRECT | CAPT_MODE_THREAD)) return false;
@@ -1526,21 +1423,35 @@ bool binned_preferred(const DevTree& t, int64_t n, uint32_t flags) {
 
 int launch_binned(const DevTree& t, const void* centers, const void* radii, int64_t n, int L,
                   const uint8_t* mask, uint32_t flags, uint32_t* bits, int64_t n_words,
-                  unsigned long long* first_bad, cudaStream_t s, const uint32_t* qlist,
-                  const uint32_t* qlist_n) {
-  const bool list_mode = qlist != nullptr;
-  const int L_out = L;
-  if (list_mode) {
-    L = 1;
-    mask = nullptr;
-    flags &= ~uint32_t(CAPT_CHECK_RADII);
+                  unsigned long long* first_bad, cudaStream_t s) {
+  constexpr int V = kK1V;
+  struct Setup {
+    int sms = 0, occ = 0, occ_tc = 0;
+  };
+  static DeviceOnce once;
+  static Setup setup[kMaxDevices];
+  {
+    const int rc = per_device_once(once, [&](int dev) {
+      Setup& u = setup[dev];
+      CAPT_CUDA(cudaFuncSetAttribute(k_binned_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(SmemBinned))));
+      CAPT_CUDA(cudaFuncSetAttribute(k_bin_count3<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(float) * kSmemNodes3)));
+      CAPT_CUDA(cudaFuncSetAttribute(k_binned_scan_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(SmemTc))));
+      CAPT_CUDA(cudaDeviceGetAttribute(&u.sms, cudaDevAttrMultiProcessorCount, dev));
+      CAPT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&u.occ, k_binned_scan, kBT,
+                                                              sizeof(SmemBinned)));
+      if (u.occ < 1) u.occ = 1;
+      u.occ_tc = 512 / kTcCols;  // TMEM columns per SM
+      if (u.occ_tc > 8) u.occ_tc = 8;
+      return CAPT_OK;
+    });
+    if (rc) return rc;
   }
-  static bool smem_set = false;
-  if (!smem_set) {
-    CAPT_CUDA(cudaFuncSetAttribute(k_binned_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(sizeof(SmemBinned))));
-    smem_set = true;
-  }
+  int dev = 0;
+  CAPT_CUDA(cudaGetDevice(&dev));
+  const Setup& u = setup[dev];
   Arena A;
   A.s = s;
   BinArgs a;
@@ -1553,8 +1464,6 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.mask = mask;
   a.flags = flags;
   a.first_bad = first_bad;
-  a.qlist = qlist;
-  a.qlist_n = qlist_n;
   const int64_t nl = t.n;
   // everything that must start at zero, in one block (one memset):
   // counters (slow_n, n_tiles, tile_ctr, n_refined, list_n) | counts | cursor | bcursor
@@ -1565,13 +1474,8 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.bcursor = ctr ? ctr + 8 + 2 * nl : nullptr;
   a.start = A.get<uint32_t>(nl);
   a.tstart = A.get<uint32_t>(nl);
-  // K5 on the tensor cores unless CAPT_K5_FFMA (or CAPT_K5_TC=0 in the
-  // environment) selects the CUDA-core kernel
-  static const bool env_ffma = [] {
-    const char* e = getenv("CAPT_K5_TC");
-    return e && e[0] == '0';
-  }();
-  const bool use_tc = !(env_ffma || (flags & CAPT_K5_FFMA));
+  // K5 on the tensor cores unless CAPT_K5_FFMA selects the CUDA-core kernel
+  const bool use_tc = !(flags & CAPT_K5_FFMA);
   a.ts = use_tc ? uint32_t(kTsTc) : uint32_t(kTS);
   a.tiles = A.get<TileMeta>(nl + n / a.ts + 1);
   a.perm = A.get<uint32_t>(n);
@@ -1598,35 +1502,16 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
   a.tile_ctr = ctr + 2;
   a.n_refined = ctr + 3;
   a.list_n = ctr + 4;
-  StageTimer& tm = g_stage_timer;
-  tm.mark(0, s);
   // (verdict bytes need no clearing: K1 writes one for every sphere)
   k_zero<<<grid_for(zero_words, 256, 4), 256, 0, s>>>(ctr, zero_words);
   const bool f64 = flags & CAPT_INPUT_F64;
   const int G = grid_for(n, 256, 8);
-#ifndef CAPT_K1_V  // spheres in flight per K1 thread: 4 (339 us) beats 2 (442) and 6 (482)
-#define CAPT_K1_V 4
-#endif
-  constexpr int V = CAPT_K1_V;
   const int G4 = grid_for((n + V - 1) / V, 256, 8);
-  tm.mark(1, s);
   if (f64) k_bin_count<double><<<G, 256, 0, s>>>(a);
   else if (t.k == 3) {
-    static bool k1_attr = false;
-    if (!k1_attr) {
-      CAPT_CUDA(cudaFuncSetAttribute(k_bin_count3<V, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(sizeof(float) * kSmemNodes3)));
-      CAPT_CUDA(cudaFuncSetAttribute(k_bin_count3<V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(sizeof(float) * kSmemNodes3)));
-      k1_attr = true;
-    }
-    if (list_mode)
-      CAPT_CUDA(launch_pdl(k_bin_count3<V, true>, G4, 256, sizeof(float) * kSmemNodes3, s, a));
-    else
-      CAPT_CUDA(launch_pdl(k_bin_count3<V, false>, G4, 256, sizeof(float) * kSmemNodes3, s, a));
+    CAPT_CUDA(launch_pdl(k_bin_count3<V>, G4, 256, sizeof(float) * kSmemNodes3, s, a));
   }
   else k_bin_count<float><<<G, 256, 0, s>>>(a);
-  tm.mark(2, s);
   // per-leaf starts and tiles
   if (nl <= kScanSingleMax) {
     CAPT_CUDA(launch_pdl(k_scan_tiles, 1, kScanT, 0, s, a));
@@ -1642,59 +1527,22 @@ int launch_binned(const DevTree& t, const void* centers, const void* radii, int6
     k_tile_total<<<1, 1, 0, s>>>(a, tc);
     note_launches(6);
   }
-  tm.mark(3, s);
   {
     const int Gp = grid_for((n + kPartItems - 1) / kPartItems * 256, 256, 4);
     CAPT_CUDA(launch_pdl(k_part_bucket, Gp, 256, 0, s, a));
-    tm.mark(4, s);
     CAPT_CUDA(launch_pdl(k_part_leaf, Gp, 256, 0, s, a));
   }
-  static int sms = 0, occ = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_binned_scan, kBT, sizeof(SmemBinned));
-    if (occ < 1) occ = 1;
-  }
-  tm.mark(5, s);
   if (use_tc) {
-    static int occ_tc = 0;
-    if (!occ_tc) {
-      CAPT_CUDA(cudaFuncSetAttribute(k_binned_scan_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(sizeof(SmemTc))));
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tc, k_binned_scan_tc, kTcThreads, sizeof(SmemTc));
-      if (getenv("CAPT_DEBUG")) fprintf(stderr, "[capt tc] occupancy %d smem %d\n", occ_tc, int(sizeof(SmemTc)));
-      occ_tc = 512 / kTcCols;  // TMEM columns per SM
-      if (occ_tc > 8) occ_tc = 8;
-    }
-    CAPT_CUDA(launch_pdl(k_binned_scan_tc, sms * occ_tc, kTcThreads, sizeof(SmemTc), s, a));
+    CAPT_CUDA(launch_pdl(k_binned_scan_tc, u.sms * u.occ_tc, kTcThreads, sizeof(SmemTc), s, a));
   } else {
-    k_binned_scan<<<sms * occ, kBT, sizeof(SmemBinned), s>>>(a);
+    k_binned_scan<<<u.sms * u.occ, kBT, sizeof(SmemBinned), s>>>(a);
   }
-  tm.mark(6, s);
-  if (f64) CAPT_CUDA(launch_pdl(k_slow<double>, sms * 8, 128, 0, s, a));
-  else CAPT_CUDA(launch_pdl(k_slow<float>, sms * 8, 128, 0, s, a));
-  if (list_mode)
-    CAPT_CUDA(launch_pdl(k_list_bits, grid_for(n, 256, 4), 256, 0, s, qlist, qlist_n,
-                         static_cast<const uint8_t*>(a.verdict), L_out, bits));
-  else
-    CAPT_CUDA(launch_pdl(k_pack, grid_for(n_words * 32, 256, 8), 256, 0, s, n / L, L,
+  if (f64) CAPT_CUDA(launch_pdl(k_slow<double>, u.sms * 8, 128, 0, s, a));
+  else CAPT_CUDA(launch_pdl(k_slow<float>, u.sms * 8, 128, 0, s, a));
+  CAPT_CUDA(launch_pdl(k_pack, grid_for(n_words * 32, 256, 8), 256, 0, s, n / L, L,
                          static_cast<const uint8_t*>(a.verdict), bits, n_words));
-  tm.mark(7, s);
-  tm.finish(s);
   CAPT_CUDA(cudaGetLastError());
   note_launches(8);  // zero, count, scan+tiles, 2 partition passes, scan, slow, pack
-  static const bool debug = getenv("CAPT_DEBUG") != nullptr;
-  if (debug) {
-    uint32_t h[4], last[2];
-    CAPT_CUDA(cudaMemcpyAsync(h, ctr, 16, cudaMemcpyDeviceToHost, s));
-    CAPT_CUDA(cudaMemcpyAsync(last, a.start + nl - 1, 4, cudaMemcpyDeviceToHost, s));
-    CAPT_CUDA(cudaMemcpyAsync(last + 1, a.counts + nl - 1, 4, cudaMemcpyDeviceToHost, s));
-    CAPT_CUDA(cudaStreamSynchronize(s));
-    fprintf(stderr, "[capt binned] n=%lld binned=%u exact_queue=%u tiles=%u refined=%u\n",
-            (long long)n, last[0] + last[1], h[0], h[1], h[3]);
-  }
   return CAPT_OK;
 }
 

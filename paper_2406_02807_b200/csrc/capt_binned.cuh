@@ -47,18 +47,12 @@ struct BinArgs {
   int bshift;         // leaf bucket = leaf >> bshift (<= kBuckets buckets)
   float rlo_f, rhi_f; // fp32 images of the double band edges
   uint32_t ts;        // spheres per K5 tile (kernel dependent)
-  const uint32_t* qlist;    // list mode: sphere ids to resolve (else nullptr)
-  const uint32_t* qlist_n;  //   ... and their count (device)
 };
 
 bool binned_preferred(const DevTree& t, int64_t n, uint32_t flags);
 
-// qlist/qlist_n (list mode): resolve only the listed spheres (the clearance
-// field's undecided ones; masked and band-checked already) and OR their hits
-// into bits, which already hold every other verdict.
 int launch_binned(const DevTree& t, const void* centers, const void* radii, int64_t n, int L,
                   const uint8_t* mask, uint32_t flags, uint32_t* bits, int64_t n_words,
-                  unsigned long long* first_bad, cudaStream_t s,
-                  const uint32_t* qlist = nullptr, const uint32_t* qlist_n = nullptr);
+                  unsigned long long* first_bad, cudaStream_t s);
 
 }  // namespace capt

@@ -4,62 +4,65 @@
 // leaf's affordance set (query.py:184-219).  Because the affordance sets are
 // complete for radii inside [r_min, r_max] (Alg. 1; pinned
 // by the reference's brute-force equality tests, test_acceptance.py:54-91),
-// the verdict of an in-band sphere is exactly "some cloud point lies within
-// r of the centre" -- the brute-force verdict (oracle.py:34-49).  Two
-// certificates decide that verdict for most spheres without the tree:
+// the verdict of an in-band sphere is exactly "some cloud point p has float64
+// ((dx^2 + dy^2) + dz^2) <= r*r" -- the brute-force verdict (oracle.py:34-49;
+// DESIGN.md section 3b).  A uniform grid over the cloud decides that verdict
+// for almost every sphere without the tree, in two stages:
 //
-//   * hit:  some cloud point w has fp32 |c - w|^2 <= r^2 (1 - TAU)  (the
-//           same definite-hit band as the representative probe);
-//   * free: a lower bound of the distance from c to every cloud point
-//           exceeds r with a relative margin.  The bound comes from a
-//           uniform grid whose cells store nn <= dist(x0, cloud) for the
-//           cell centre x0: dist(c, cloud) >= nn - |c - x0| (the distance
-//           function is 1-Lipschitz), or from the cloud's box.
+//   K0 (every sphere): one 16-B record per cell {witness w, nn}, w = the
+//     cloud point nearest the cell centre x0 and nn <= dist(x0, cloud):
+//       hit:  fp32 |c - w|^2 <= r^2 (1 - TAU);
+//       free: nn - |c - x0| > r with a relative margin (dist is 1-Lipschitz);
+//     decides ~96% (config 3) to ~99.7% (config 1) of the spheres.
+//   list (the rest): the cell's candidate record -- its kCand nearest cloud
+//     points (int16 offsets from x0) and kd <= the distance from x0 to every
+//     other cloud point: a candidate hit decides; no candidate hit and
+//     kd - |c - x0| > r (with a margin) decides free.  Simulated on configs
+//     1 and 3, this leaves ~1e-6 / 1e-4 of the spheres (within a hair of
+//     tangency to their (kCand+1)-th point).
 //
-// Each cell is one 16-B record {witness xyz, nn}, witness = the cloud point
-// nearest x0: one L2-resident 128-bit load per sphere.  Spheres that neither
-// certificate decides (a few percent; near |dist - r| ~ cell size), spheres
-// outside the band (check_radii=False), non-finite centres and extreme radii
-// go to a compact list that the tree path (descent, AABB, representative
-// probe, cooperative affordance-set scans with the float64 fix-up) resolves
-// with the reference's own semantics.
+// Spheres no certificate decides, spheres outside the band (check_radii =
+// False), non-finite centres and extreme radii take the tree path (descent,
+// AABB, representative probe, cooperative affordance-set scans with the
+// float64 fix-up) with the reference's own semantics.
 //
 // Kernels:
 //   build:  k_rep_box (cloud box), k_bucket_keys + radix sort (points into
-//           buckets of >= rcap), k_field_nn (one CTA per bucket: exact
-//           nearest point of every cell centre among the 27 neighbouring
-//           buckets, staged through shared memory)
-//   query:  k_resolve  (per sphere: band check, box / field certificates,
-//                       lane-group resolution, bit words, compact list)
-//           k_resolve_list (the tree path over the list)
+//           buckets of >= rcap), k_field_cand (one CTA per bucket: the
+//           kCand + 1 nearest points of every cell centre among the 27
+//           neighbouring buckets, staged through shared memory)
+//   query:  k_resolve      (K0: band check, grid certificates, lane groups,
+//                           bit words, the list with its spheres)
+//           k_list_knn     (candidate certificates; the open entries -> list 2)
+//           k_tree_list    (the tree path over list 2)
 #include <cub/cub.cuh>
-#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <climits>
+#include <limits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <vector>
 
-#include "capt_binned.cuh"
-#include "capt_tc.cuh"
 #include "capt_internal.cuh"
 #include "capt_query_common.cuh"
 
 namespace capt {
 
 #ifndef CAPT_FIELD_CELLS
-#define CAPT_FIELD_CELLS (1 << 21)  // 32 MB of records: L2-resident
+#define CAPT_FIELD_CELLS (1 << 21)  // 32 MB of K0 records: L2-resident
 #endif
 
 namespace {
 
-constexpr float kFreeMargin = 1.0f + 0x1p-20f;  // (r + e)(1 + 16u): see k_resolve
 constexpr float kNNShrink = 1.0f - 0x1p-19f;    // fp32 sqrt(d^2) -> certified lower bound
-constexpr int kFieldChunk = 1024;               // staged points per k_field_nn round
-constexpr int kCellsPerThread = 4;
+constexpr int kFieldChunk = 1024;               // staged points per k_field_knn round
+constexpr int kKP = kCand + 1;                  // nearest points kept per cell (+ the bound)
 
 __device__ __forceinline__ int f2o(float f) {
   const int i = __float_as_int(f);
@@ -89,14 +92,15 @@ __device__ __forceinline__ float4 ldg_keep(const float4* p, uint64_t pol) {
       : "l"(p), "l"(pol));
   return v;
 }
-// fp16 octant bound o of a cell (octant array: 8 halves per cell)
-__device__ __forceinline__ float oct_bound(const float4* oct, unsigned cell, unsigned o) {
-  const unsigned short hb =
-      __ldg(reinterpret_cast<const unsigned short*>(oct) + 8 * size_t(cell) + o);
-  return __half2float(__ushort_as_half(hb));
-}
 __device__ __forceinline__ float d2_fma(float dx, float dy, float dz) {
   return fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+}
+// the reference's float64 point test (query.py:96-99): ((dx^2 + dy^2) + dz^2) <= r*r
+__device__ __forceinline__ bool hit_f64(float cx, float cy, float cz, float r, float4 p) {
+  const double dx = __dsub_rn(double(cx), double(p.x)), dy = __dsub_rn(double(cy), double(p.y)),
+               dz = __dsub_rn(double(cz), double(p.z));
+  const double s = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  return s <= __dmul_rn(double(r), double(r));
 }
 
 // ---------------------------------------------------------------- build
@@ -158,18 +162,46 @@ __global__ void k_bucket_keys(const float4* __restrict__ rep, int64_t n, FieldGe
 __global__ void k_bucket_points(const float4* __restrict__ rep, const int* __restrict__ ids,
                                 int64_t n_fin, float4* __restrict__ pts) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_fin;
-       i += int64_t(gridDim.x) * blockDim.x)
-    pts[i] = rep[ids[i]];
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const float4 p = rep[ids[i]];
+    pts[i] = make_float4(p.x, p.y, p.z, 0.f);
+  }
+}
+
+// Insert (d2, id) into the ascending list bd[0..kKP) (the caller knows
+// d2 < bd[kKP-1]); equal distances keep the earlier candidate first.
+__device__ __forceinline__ void knn_insert(float (&bd)[kKP], int (&bi)[kKP], float d2, int id) {
+#pragma unroll
+  for (int j = kKP - 1; j > 0; --j) {
+    const bool shift = d2 < bd[j - 1];
+    const bool place = !shift && d2 < bd[j];
+    bd[j] = shift ? bd[j - 1] : (place ? d2 : bd[j]);
+    bi[j] = shift ? bi[j - 1] : (place ? id : bi[j]);
+  }
+  if (d2 < bd[0]) {
+    bd[0] = d2;
+    bi[0] = id;
+  }
+}
+
+// Set int16 slot j of the axis block at w[0..15] (two slots per word).
+__device__ __forceinline__ void put_slot(uint32_t* w, int j, int v) {
+  const uint32_t u = uint32_t(v) & 0xffffu;
+  w[j >> 1] = (j & 1) ? ((w[j >> 1] & 0xffffu) | (u << 16)) : ((w[j >> 1] & 0xffff0000u) | u);
 }
 
 // One CTA per bucket: every cell of the bucket against every point of the
 // 27 neighbouring buckets (points farther than rcap from a cell centre lie
 // outside them: bucket edge m*h >= rcap + 2h, see build_field), the
-// candidates staged through shared memory in chunks.
-__global__ void __launch_bounds__(256, 1) k_field_nn(FieldGeom g, BucketGrid b,
-                                                  const uint32_t* __restrict__ bstart,
-                                                  const float4* __restrict__ pts,
-                                                  float4* __restrict__ field) {
+// candidates staged through shared memory in chunks.  Per cell: the kCand + 1
+// nearest points by fp32 distance (candidates in bucket order: deterministic
+// on every replica) -> the K0 record {nearest point, nn} and the candidate
+// record (the kCand nearest as int16 offsets from x0, the bound kd_q).
+__global__ void __launch_bounds__(256, 1) k_field_cand(FieldGeom g, BucketGrid b,
+                                                    const uint32_t* __restrict__ bstart,
+                                                    const float4* __restrict__ pts,
+                                                    float4* __restrict__ field,
+                                                    uint32_t* __restrict__ cand) {
   __shared__ float4 sp[kFieldChunk];
   const int bid = blockIdx.x;
   const int bx = bid % b.nbx, by = (bid / b.nbx) % b.nby, bz = bid / (b.nbx * b.nby);
@@ -177,22 +209,18 @@ __global__ void __launch_bounds__(256, 1) k_field_nn(FieldGeom g, BucketGrid b,
   const int cx = min(g.m, g.nx - x0), cy = min(g.m, g.ny - y0), cz = min(g.m, g.nz - z0);
   const int ncells = cx * cy * cz;
   const float INF = __int_as_float(0x7f800000);
-  const float hh = g.oct_half;
-  for (int pass = 0; pass < ncells; pass += 256 * kCellsPerThread) {
-    float px[kCellsPerThread], py[kCellsPerThread], pz[kCellsPerThread], best[kCellsPerThread];
-    float ob[kCellsPerThread][8];  // squared distance from each octant box
-    int bi[kCellsPerThread];
+  for (int pass = 0; pass < ncells; pass += 256) {
+    const int j = pass + threadIdx.x;
+    const int lx = j % cx, ly = (j / cx) % cy, lz = j / (cx * cy);
+    const float px = centre_of(x0 + lx, g.h, g.c0[0]);
+    const float py = centre_of(y0 + ly, g.h, g.c0[1]);
+    const float pz = centre_of(z0 + lz, g.h, g.c0[2]);
+    float bd[kKP];
+    int bi[kKP];
 #pragma unroll
-    for (int k = 0; k < kCellsPerThread; ++k) {
-      const int j = pass + k * 256 + threadIdx.x;
-      const int lx = j % cx, ly = (j / cx) % cy, lz = j / (cx * cy);
-      px[k] = centre_of(x0 + lx, g.h, g.c0[0]);
-      py[k] = centre_of(y0 + ly, g.h, g.c0[1]);
-      pz[k] = centre_of(z0 + lz, g.h, g.c0[2]);
-      best[k] = INF;
-      bi[k] = -1;
-#pragma unroll
-      for (int o = 0; o < 8; ++o) ob[k][o] = INF;
+    for (int i = 0; i < kKP; ++i) {
+      bd[i] = INF;
+      bi[i] = -1;
     }
     for (int nz = max(bz - 1, 0); nz <= min(bz + 1, b.nbz - 1); ++nz)
       for (int ny = max(by - 1, 0); ny <= min(by + 1, b.nby - 1); ++ny)
@@ -206,116 +234,59 @@ __global__ void __launch_bounds__(256, 1) k_field_nn(FieldGeom g, BucketGrid b,
             __syncthreads();
             for (int i = 0; i < cnt; ++i) {
               const float4 p = sp[i];
-#pragma unroll
-              for (int k = 0; k < kCellsPerThread; ++k) {
-                const float ax = p.x - px[k], ay = p.y - py[k], az = p.z - pz[k];
-                const float d2 = d2_fma(ax, ay, az);
-                if (d2 < best[k]) {
-                  best[k] = d2;
-                  bi[k] = int(c0) + i;
-                }
-                // gap from the octant box [x0, x0 + hh] (bit 1) / [x0 - hh, x0] (bit 0)
-                const float gx1 = fmaxf(fmaxf(-ax, ax - hh), 0.f), gx0 = fmaxf(fmaxf(ax, -ax - hh), 0.f);
-                const float gy1 = fmaxf(fmaxf(-ay, ay - hh), 0.f), gy0 = fmaxf(fmaxf(ay, -ay - hh), 0.f);
-                const float gz1 = fmaxf(fmaxf(-az, az - hh), 0.f), gz0 = fmaxf(fmaxf(az, -az - hh), 0.f);
-                const float xy[4] = {fmaf(gy0, gy0, gx0 * gx0), fmaf(gy0, gy0, gx1 * gx1),
-                                     fmaf(gy1, gy1, gx0 * gx0), fmaf(gy1, gy1, gx1 * gx1)};
-                const float zz0 = gz0 * gz0, zz1 = gz1 * gz1;
-#pragma unroll
-                for (int o = 0; o < 4; ++o) {
-                  ob[k][o] = fminf(ob[k][o], xy[o] + zz0);
-                  ob[k][o + 4] = fminf(ob[k][o + 4], xy[o] + zz1);
-                }
-              }
+              const float d2 = d2_fma(p.x - px, p.y - py, p.z - pz);
+              if (d2 < bd[kKP - 1]) knn_insert(bd, bi, d2, int(c0) + i);
             }
           }
         }
+    if (j >= ncells) continue;
+    const int64_t cell = (int64_t(z0 + lz) * g.ny + (y0 + ly)) * g.nx + (x0 + lx);
+    // fp32 |x0 - p|^2 has relative error < 5u, sqrtf one more u:
+    // sqrtf(d2) (1 - 2^-19) (rounded) < the real distance.  Points outside
+    // the 27 buckets are farther than rcap: the bounds are capped there.
+    const float nn = fminf(g.rcap, __fmul_rn(sqrtf(bd[0]), kNNShrink));
+    const float4 w = bi[0] >= 0 ? pts[bi[0]] : make_float4(INF, INF, INF, 0.f);
+    field[cell] = make_float4(w.x, w.y, w.z, nn);
+    // candidates: offsets (p - x0) / q_step rounded (exact in double: the
+    // difference of two floats, a power-of-two scale), |offset| <= 32767;
+    // the first point that does not fit (or lies beyond rcap) ends the list
+    // and bounds kd
+    uint32_t wd[kCandWords];
 #pragma unroll
-    for (int k = 0; k < kCellsPerThread; ++k) {
-      const int j = pass + k * 256 + threadIdx.x;
-      // fp32 |x0 - p|^2 has relative error < 5u, sqrtf one more u:
-      // sqrtf(d2) (1 - 2^-19) (rounded) < the real distance
-      const int bsel = bi[k] >= 0 ? bi[k] : 0;
-      const float nn = fminf(g.rcap, __fmul_rn(sqrtf(best[k]), kNNShrink));
-      // octant bounds: the same relative margin and an absolute one for the
-      // rounded gaps, capped where the candidate search ends, fp16 rounded down
-      unsigned short hb[8];
+    for (int i = 0; i < kCandWords; ++i) wd[i] = 0x80008000u;  // kCandNone pairs
+    float kd = fminf(g.rcap, __fmul_rn(sqrtf(bd[kKP - 1]), kNNShrink));
+    int count = 0;
+    bool open = true;
+    const double inv = 1.0 / double(g.q_step);
 #pragma unroll
-      for (int o = 0; o < 8; ++o) {
-        float lb = fmaf(sqrtf(ob[k][o]), kNNShrink, -g.oct_abs);
-        lb = fminf(fmaxf(lb, 0.f), g.oct_cap);
-        hb[o] = __half_as_ushort(__float2half_rd(lb));
+    for (int k = 0; k < kCand; ++k) {
+      if (!open || bi[k] < 0) {
+        open = false;
+        continue;
       }
-      if (j < ncells) {
-        const int lx = j % cx, ly = (j / cx) % cy, lz = j / (cx * cy);
-        const int64_t cell = (int64_t(z0 + lz) * g.ny + (y0 + ly)) * g.nx + (x0 + lx);
-        const float4 w = bi[k] >= 0 ? pts[bsel] : make_float4(INF, INF, INF, 0.f);
-        field[cell] = make_float4(w.x, w.y, w.z, nn);
-        field[g.cells + cell] = make_float4(
-            __uint_as_float(unsigned(hb[0]) | (unsigned(hb[1]) << 16)),
-            __uint_as_float(unsigned(hb[2]) | (unsigned(hb[3]) << 16)),
-            __uint_as_float(unsigned(hb[4]) | (unsigned(hb[5]) << 16)),
-            __uint_as_float(unsigned(hb[6]) | (unsigned(hb[7]) << 16)));
+      const float4 p = pts[bi[k]];
+      const double qx = rint((double(p.x) - double(px)) * inv);
+      const double qy = rint((double(p.y) - double(py)) * inv);
+      const double qz = rint((double(p.z) - double(pz)) * inv);
+      const float lb = __fmul_rn(sqrtf(bd[k]), kNNShrink);
+      if (fabs(qx) > 32767.0 || fabs(qy) > 32767.0 || fabs(qz) > 32767.0 || !(lb < g.rcap)) {
+        kd = fminf(kd, lb);  // (every later candidate is at least as far)
+        open = false;
+        continue;
       }
+      put_slot(wd, k, int(qx));
+      put_slot(wd + 16, k, int(qy));
+      put_slot(wd + 32, k, int(qz));
+      ++count;
     }
+    put_slot(wd, 31, int(floor(double(kd) * inv)));  // kd_q q_step <= kd
+    put_slot(wd + 16, 31, count);
+    uint4* dst = reinterpret_cast<uint4*>(cand + cell * kCandWords);
+#pragma unroll
+    for (int i = 0; i < kCandWords / 4; ++i)
+      dst[i] = make_uint4(wd[4 * i], wd[4 * i + 1], wd[4 * i + 2], wd[4 * i + 3]);
   }
 }
-
-// Distance-sorted set copy.  Keys: fp32 |p - o| (o = the set's origin) of
-// every stored row (padding rows +inf), sorted within each set; the scan of a
-// sphere (c, r) can stop at the first row with |p - o| > r + |c - o| (a row
-// beyond it is farther than r from c).  Stored distances are rounded down.
-__global__ void k_sort_keys(DevTree t, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                            int* __restrict__ seg_begin, int* __restrict__ seg_end) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t j = warp; j < t.n; j += nwarps) {
-    const uint2 st = t.set[j];
-    const uint32_t m4 = (st.y + 3u) & ~3u;
-    const float* base = reinterpret_cast<const float*>(t.data + st.x);
-    const int64_t b = int64_t(st.x) * 4 / 3;
-    const float4 o = t.org[j];
-    if (lane == 0) {
-      seg_begin[j] = int(b);
-      seg_end[j] = int(b + m4);
-    }
-    for (uint32_t i = lane; i < m4; i += 32) {
-      float d = __int_as_float(0x7f800000);
-      if (i < st.y) {
-        const float dx = base[i] - o.x, dy = base[m4 + i] - o.y, dz = base[2 * m4 + i] - o.z;
-        d = sqrtf(d2_fma(dx, dy, dz));
-        if (!(d <= 3.0e38f)) d = __int_as_float(0x7f800000);  // (+inf rows of padding leaves)
-      }
-      keys[b + i] = __float_as_uint(d);
-      vals[b + i] = i;
-    }
-  }
-}
-
-__global__ void k_sort_gather(DevTree t, const uint32_t* __restrict__ keys,
-                              const uint32_t* __restrict__ vals, float* __restrict__ sdata,
-                              float* __restrict__ sdist) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t j = warp; j < t.n; j += nwarps) {
-    const uint2 st = t.set[j];
-    const uint32_t m4 = (st.y + 3u) & ~3u;
-    const float* src = reinterpret_cast<const float*>(t.data + st.x);
-    float* dst = sdata + int64_t(st.x) * 4;
-    const int64_t b = int64_t(st.x) * 4 / 3;
-    for (uint32_t i = lane; i < m4; i += 32) {
-      const uint32_t k = vals[b + i];
-      dst[i] = src[k];
-      dst[m4 + i] = src[m4 + k];
-      dst[2 * m4 + i] = src[2 * m4 + k];
-      // fp32 |p - o| has relative error < 4u: (1 - 2^-19) rounds it below the real distance
-      sdist[b + i] = __fmul_rn(__uint_as_float(keys[b + i]), 1.0f - 0x1p-19f);
-    }
-  }
-}
-
 
 // ---------------------------------------------------------------- query
 
@@ -329,15 +300,15 @@ struct FieldArgs {
   uint32_t flags;
   uint32_t* bits;
   unsigned long long* first_bad;
-  uint32_t* list;    // sphere ids the tree path resolves
+  uint32_t* list;    // undecided sphere ids
+  float4* list_s;    //   ... and their spheres {x, y, z, r} (K0's list; nullptr for the tree path's)
   uint32_t* list_n;
   float rlo_f, rhi_f;  // fp32 images of the double band edges
 };
 
 // K0.  A warp takes chunks of 128 consecutive spheres; lane l owns spheres
 // 4l .. 4l+3 of the chunk, so a chunk is three 128-bit centre loads and one
-// 128-bit radius load per lane (the next chunk is loaded while this one is
-// decided).  For an in-band sphere (r in [r_min, r_max] in double; NaN is
+// 128-bit radius load per lane.  For an in-band sphere (r in [r_min, r_max] in double; NaN is
 // not) the verdict is certified without the tree (see the file comment):
 //   * outside the grid: the raw cell index leaves [0, n) on some axis, so the
 //     centre is more than r_max + h from the cloud's box -> free (this also
@@ -352,8 +323,8 @@ struct FieldArgs {
 // spheres near |dist - r| ~ h) is undecided.  Lane groups (L | 32) resolve on
 // any definite hit (query.py:152-160); verdict bits are written directly
 // (L <= 4: whole words; L >= 8: OR into cleared words); the undecided
-// spheres of unresolved groups are appended to the list in sphere order (a
-// group's spheres stay contiguous) with one atomic per warp and chunk.
+// spheres of unresolved groups are appended to the list (single spheres via
+// a per-CTA shared-memory buffer: list order is not sphere order).
 constexpr float kK1 = 1.0f + 0x1p-20f;
 
 struct Chunk {
@@ -391,25 +362,41 @@ __device__ __forceinline__ Chunk load_chunk(const float* __restrict__ cf,
 }
 
 // The common tail of a decided chunk: first_bad, lane-group resolution, the
-// verdict bits, the list of undecided spheres (in sphere order).
-// A CTA's list entries collect in shared memory (one shared atomic per warp
-// and chunk instead of a returning global atomic on every chunk's critical
-// path) and are copied out once at the end of the kernel; a full buffer
-// falls back to direct appends.
-#ifndef CAPT_K0_LISTBUF
-#define CAPT_K0_LISTBUF 4096
-#endif
-constexpr int kListBuf = CAPT_K0_LISTBUF;
-struct ListBuf {
-  uint32_t* buf;  // shared memory (nullptr: append to the global list directly)
-  uint32_t* n;    // entries reserved in buf (may run past kListBuf)
-  uint32_t* end;  // the first reservation that did not fit (its range is a hole)
+// verdict bits, the list of undecided spheres.
+// List entries carry the sphere ({x, y, z, r} and its index), so the list
+// stage reads them coalesced instead of gathering four words per entry.  A
+// warp collects its entries in a private 64-entry ring in shared memory and
+// writes them out 32 at a time (one returning global atomic per 32 entries,
+// coalesced stores), the rest at the end of the kernel; a chunk with more
+// than 32 entries appends directly.
+constexpr int kRing = 64;
+struct Ring {
+  float4* s;      // this warp's ring: spheres
+  uint32_t* q;    //   ... and their indices
+  unsigned head;  // (warp-uniform) oldest entry
+  unsigned cnt;   // (warp-uniform) entries held
 };
+
+__device__ __forceinline__ void ring_flush(const FieldArgs& a, Ring& rg, unsigned k, int lane) {
+  __syncwarp();
+  unsigned base = 0;
+  if (lane == 0) base = atomicAdd(a.list_n, k);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (unsigned(lane) < k) {
+    const unsigned slot = (rg.head + lane) & (kRing - 1);
+    a.list[base + lane] = rg.q[slot];
+    a.list_s[base + lane] = rg.s[slot];
+  }
+  __syncwarp();
+  rg.head = (rg.head + k) & (kRing - 1);
+  rg.cnt -= k;
+}
 
 template <int LT>
 __device__ __forceinline__ void emit_chunk(const FieldArgs& a, int ch, int lane, bool check,
                                            unsigned hitb, unsigned undb, unsigned badb,
-                                           ListBuf lb = {nullptr, nullptr, nullptr}) {
+                                           const float (&x)[4], const float (&y)[4],
+                                           const float (&z)[4], const float (&r)[4], Ring& rg) {
   const int n = a.n;
   const int q0 = (ch << 7) + 4 * lane;
   if (check && __any_sync(0xffffffffu, badb != 0)) {
@@ -460,7 +447,7 @@ __device__ __forceinline__ void emit_chunk(const FieldArgs& a, int ch, int lane,
     const int g0 = (ch << 7) / L;  // first group of the chunk
     if (lane == 0 && outw) atomicOr(a.bits + (g0 >> 5), outw << (g0 & 31));
   }
-  // the list, in sphere order
+  // the list
   const unsigned lst = undb & ~resb;
   const unsigned has = __ballot_sync(0xffffffffu, lst != 0);
   if (has) {
@@ -471,23 +458,30 @@ __device__ __forceinline__ void emit_chunk(const FieldArgs& a, int ch, int lane,
       const int t = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += t;
     }
-    const int tot = __shfl_sync(0xffffffffu, incl, 31);
-    unsigned base = 0;
-    bool local = false;
-    if (lane == 0) {
-      if (lb.buf) {
-        base = atomicAdd(lb.n, unsigned(tot));
-        local = base + unsigned(tot) <= unsigned(kListBuf);
-        if (!local && base < unsigned(kListBuf)) atomicMin(lb.end, base);
-      }
-      if (!local) base = atomicAdd(a.list_n, unsigned(tot));
-    }
-    base = __shfl_sync(0xffffffffu, base, 0) + unsigned(incl - cnt);
-    local = __shfl_sync(0xffffffffu, local, 0);
-    uint32_t* dst = local ? lb.buf : a.list;
+    const unsigned tot = unsigned(__shfl_sync(0xffffffffu, incl, 31));
+    if (tot > 32u) {  // (rare: NaN or out-of-band batches) straight to the list
+      unsigned base = 0;
+      if (lane == 0) base = atomicAdd(a.list_n, tot);
+      base = __shfl_sync(0xffffffffu, base, 0) + unsigned(incl - cnt);
 #pragma unroll
-    for (int v = 0; v < 4; ++v)
-      if ((lst >> v) & 1u) dst[base + __popc(lst & ((1u << v) - 1u))] = uint32_t(q0 + v);
+      for (int v = 0; v < 4; ++v)
+        if ((lst >> v) & 1u) {
+          const unsigned at = base + __popc(lst & ((1u << v) - 1u));
+          a.list[at] = uint32_t(q0 + v);
+          a.list_s[at] = make_float4(x[v], y[v], z[v], r[v]);
+        }
+    } else {
+      const unsigned pos = rg.head + rg.cnt + unsigned(incl - cnt);
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if ((lst >> v) & 1u) {
+          const unsigned slot = (pos + __popc(lst & ((1u << v) - 1u))) & (kRing - 1);
+          rg.q[slot] = uint32_t(q0 + v);
+          rg.s[slot] = make_float4(x[v], y[v], z[v], r[v]);
+        }
+      rg.cnt += tot;
+      if (rg.cnt >= 32u) ring_flush(a, rg, 32u, lane);
+    }
   }
 }
 
@@ -497,7 +491,7 @@ __device__ __forceinline__ void emit_chunk(const FieldArgs& a, int ch, int lane,
 template <bool kMask, int LT, bool kFull>
 __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeom& g,
                                               const Chunk& k, int ch, int lane, bool check,
-                                              uint64_t pol, ListBuf lb = {nullptr, nullptr, nullptr}) {
+                                              uint64_t pol, Ring& rg) {
   const float x[4] = {k.p0.x, k.p0.w, k.p1.z, k.p2.y};
   const float y[4] = {k.p0.y, k.p1.x, k.p1.w, k.p2.z};
   const float z[4] = {k.p0.z, k.p1.y, k.p2.x, k.p2.w};
@@ -578,19 +572,18 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
 #pragma unroll
     for (int v = 0; v < 4; ++v) cert(v);
   }
-  emit_chunk<LT>(a, ch, lane, check, hitb, undb, badb, lb);
+  emit_chunk<LT>(a, ch, lane, check, hitb, undb, badb, x, y, z, r, rg);
 }
 
 // K0 CTAs per SM the register allocation must allow: one chunk per warp in
-// registers, 4 (54 registers; 5: 48 registers, slower on config 3); with the
-// ping-pong prefetch (CAPT_K0_PREFETCH) 3 was best (78 registers)
+// registers, 4 (54 registers; 5: 48 registers, slower on config 3; a
+// ping-pong prefetch of the next chunk was best at 3 and slower overall)
 #ifndef CAPT_K0_MINB
 #define CAPT_K0_MINB 4
 #endif
 
-// persistent warps over the whole 128-sphere chunks, two per round (ping-pong
-// registers: the next chunk's loads are in flight while one is decided); the
-// last, partial chunk (scalar loads, per-sphere validity) after the loop
+// persistent warps over the whole 128-sphere chunks; the last, partial chunk
+// (scalar loads, per-sphere validity) after the loop
 template <bool kVec, bool kMask, int LT>
 #ifndef CAPT_K0_BLOCK
 #define CAPT_K0_BLOCK 256
@@ -604,386 +597,221 @@ __global__ void __launch_bounds__(CAPT_K0_BLOCK, CAPT_K0_MINB) k_resolve(FieldAr
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t pol = l2_keep_policy();
-  __shared__ uint32_t s_list[LT == 8 ? 1 : kListBuf];
-  __shared__ uint32_t s_ln, s_end, s_gbase;
-  if (threadIdx.x == 0) {
-    s_ln = 0u;
-    s_end = uint32_t(kListBuf);
-  }
-  __syncthreads();
-  // (8-sphere groups: most groups resolve on a hit, lists are short -- the
-  // buffer's shared memory would cost the record loads L1 capacity instead:
-  // config 1 K0 170 vs 166 us)
-  const ListBuf lb = LT == 8 ? ListBuf{nullptr, nullptr, nullptr} : ListBuf{s_list, &s_ln, &s_end};
+  __shared__ float4 s_ring[CAPT_K0_BLOCK / 32][kRing];
+  __shared__ uint32_t s_ringq[CAPT_K0_BLOCK / 32][kRing];
+  Ring rg{s_ring[threadIdx.x >> 5], s_ringq[threadIdx.x >> 5], 0u, 0u};
   // (launched after k_field_zero with programmatic serialisation)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  int ch = w0;
-#ifndef CAPT_K0_PREFETCH  // one chunk in registers: 166 us at 4 CTAs/SM vs 175 (ping-pong, 3 CTAs)
-  for (; ch < nfull; ch += nwarps) {
+  for (int ch = w0; ch < nfull; ch += nwarps) {
     const Chunk A = load_chunk<kVec, true>(a.c, a.r, ch, lane, n);
-    resolve_chunk<kMask, LT, !kMask>(a, g, A, ch, lane, check, pol, lb);
-  }
-  if (false) {
-#else
-  if (ch < nfull) {
-#endif
-    Chunk A = load_chunk<kVec, true>(a.c, a.r, ch, lane, n), B;
-    while (true) {
-      const int c1 = ch + nwarps;
-      if (c1 < nfull) B = load_chunk<kVec, true>(a.c, a.r, c1, lane, n);
-      resolve_chunk<kMask, LT, !kMask>(a, g, A, ch, lane, check, pol);
-      if (c1 >= nfull) break;
-      const int c2 = c1 + nwarps;
-      if (c2 < nfull) A = load_chunk<kVec, true>(a.c, a.r, c2, lane, n);
-      resolve_chunk<kMask, LT, !kMask>(a, g, B, c1, lane, check, pol);
-      if (c2 >= nfull) break;
-      ch = c2;
-    }
+    resolve_chunk<kMask, LT, !kMask>(a, g, A, ch, lane, check, pol, rg);
   }
   if ((n & 127) && w0 == nfull % nwarps) {
     const Chunk T = load_chunk<false>(a.c, a.r, nfull, lane, n);
-    resolve_chunk<kMask, LT, false>(a, g, T, nfull, lane, check, pol, lb);
+    resolve_chunk<kMask, LT, false>(a, g, T, nfull, lane, check, pol, rg);
   }
-  // the CTA's buffered list entries, in one reservation
-  __syncthreads();
-  const uint32_t cnt = min(s_ln, s_end);  // (entries past a non-fitting reservation went global)
-  if (threadIdx.x == 0 && cnt) s_gbase = atomicAdd(a.list_n, cnt);
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) a.list[s_gbase + i] = s_list[i];
+  if (rg.cnt) ring_flush(a, rg, rg.cnt, lane);
 }
 
-// K0 with TMA bulk copies (the default for unmasked, 16-B aligned batches).
-// Persistent CTAs of 8 warps take tiles of 1024 spheres; one thread streams
-// each tile's centres (12 KB) and radii (4 KB) into a ring of kStages
-// shared-memory stages with cp.async.bulk (completion on the stage's
-// mbarrier, L2 evict-first), so the sphere stream stays in flight without
-// holding registers; warp w decides chunk w of the tile from shared memory
-// (resolve_chunk), the stage is refilled once every warp is past it.  The
-// spheres after the last whole tile take the register path.
-constexpr int kTileSpheres = 1024;
-constexpr int kStages = 3;
-constexpr uint32_t kTileC = kTileSpheres * 12, kTileR = kTileSpheres * 4;
-constexpr size_t kTmaSmem = size_t(kStages) * (kTileC + kTileR) + 64;
 
-__device__ __forceinline__ uint64_t l2_stream_policy() {
-  uint64_t pol;
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(mbar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar,
-                                         uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-      "[%0], [%1], %2, [%3], %4;" ::"r"(tc::smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(tc::smem_u32(mbar)), "l"(pol)
-      : "memory");
-}
+// The list stage, part 1 (k_list_knn): every listed sphere meets its cell's
+// candidate record -- the kCand cloud points nearest x0, stored as int16
+// offsets (p - x0) / q_step, and kd_q q_step <= the distance from x0 to every
+// other cloud point.  A decoded difference v = fl(fl(c - x0) - q q_step) is
+// within q_err (Euclidean; q_step / 2 per axis from the offset rounding plus
+// the fp32 roundings) of c - p, so with S = fp32 |v|^2 (relative error < 5u):
+//   * hit:  RH = fl(r (1 - 2^-18)) - q_err (1 + 2^-17) > 0 and
+//           S <= fl(RH^2)(1 - 2^-20): then |c - p| <= |v| + q_err < r(1 - 2^-19)
+//           and the reference's float64 d^2 is <= r*r;
+//   * miss: S >= fl(RM^2)(1 + 2^-20), RM = fl(r (1 + 2^-18)) + q_err (1 + 2^-17):
+//           |c - p| >= |v| - q_err > r(1 + 2^-19): float64 d^2 > r*r;
+//   * free: every candidate a miss and A = fl(kd - fl(r (1 + 2^-20))) > 0 with
+//           A*A > fl(|c - x0|^2)(1 + 2^-20): every other cloud point p has
+//           |p - c| >= kd - |c - x0| > r (1 + 16u) (the K0 free argument
+//           with kd in place of nn).
+// A candidate hit is a brute-force hit; "free" proves no point within r
+// (DESIGN 3b; both need an in-band radius and a centre inside the grid).
+// Candidates within about q_err of the sphere's surface are neither: the
+// entry goes to the tree path.  One thread per entry: the entry itself
+// (coalesced), then the record's six 32-byte loads; the list stage is bound
+// by the L1 wavefronts of its gathers, so the record is one contiguous line
+// and a half instead of a gather per candidate.  Hits set their bit; the
+// open entries (about 1e-5 of a batch, plus every sphere the grid cannot
+// take) go to a second list for part 2.
+__device__ __forceinline__ int slot_lo(uint32_t w) { return int(w << 16) >> 16; }
+__device__ __forceinline__ int slot_hi(uint32_t w) { return int(w) >> 16; }
 
-template <int LT>
-__global__ void __launch_bounds__(256, 4) k_resolve_tma(FieldArgs a) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  float* const sc = reinterpret_cast<float*>(smem);
-  float* const sr = reinterpret_cast<float*>(smem + kStages * kTileC);
-  uint64_t* const full = reinterpret_cast<uint64_t*>(smem + kStages * (kTileC + kTileR));
-  const FieldGeom g = a.t.fg;
-  const bool check = a.flags & CAPT_CHECK_RADII;
-  const int n = a.n;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int ntiles = n / kTileSpheres;
-  const uint64_t keep = l2_keep_policy();
-  if (threadIdx.x == 0) {
-    for (int st = 0; st < kStages; ++st) tc::mbar_init(&full[st], 1);
-    tc::fence_async_smem();
-  }
-  __syncthreads();
-  auto issue = [&](int tile, int st) {
-    const uint64_t pol = l2_stream_policy();
-    mbar_expect_tx(&full[st], kTileC + kTileR);
-    bulk_g2s(sc + st * (kTileC / 4), a.c + size_t(tile) * kTileSpheres * 3, kTileC, &full[st], pol);
-    bulk_g2s(sr + st * (kTileR / 4), a.r + size_t(tile) * kTileSpheres, kTileR, &full[st], pol);
-  };
-  if (threadIdx.x == 0)
-    for (int st = 0; st < kStages; ++st) {
-      const int tile = blockIdx.x + st * gridDim.x;
-      if (tile < ntiles) issue(tile, st);
-    }
-  int it = 0;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const int st = it % kStages;
-    tc::mbar_wait(&full[st], uint32_t((it / kStages) & 1));
-    const float4* c4 = reinterpret_cast<const float4*>(sc + st * (kTileC / 4) + warp * 384) + 3 * lane;
-    Chunk k;
-    k.p0 = c4[0];
-    k.p1 = c4[1];
-    k.p2 = c4[2];
-    k.pr = reinterpret_cast<const float4*>(sr + st * (kTileR / 4) + warp * 128)[lane];
-    resolve_chunk<false, LT, true>(a, g, k, tile * (kTileSpheres / 128) + warp, lane, check, keep);
-    __syncthreads();  // every warp is past stage st
-    if (threadIdx.x == 0) {
-      const int next = tile + kStages * gridDim.x;
-      if (next < ntiles) issue(next, st);
-    }
-  }
-  // the spheres after the last whole tile: register path, one chunk per warp
-  const int nchunks = (n + 127) >> 7;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int ch = ntiles * (kTileSpheres / 128) + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-       ch < nchunks; ch += nwarps) {
-    const Chunk k = load_chunk<true>(a.c, a.r, ch, lane, n);
-    if ((ch << 7) + 128 <= n) resolve_chunk<false, LT, true>(a, g, k, ch, lane, check, keep);
-    else resolve_chunk<false, LT, false>(a, g, k, ch, lane, check, keep);
-  }
+__device__ __forceinline__ void ld_v8u(const uint32_t* p, uint32_t (&v)[8]) {
+  asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7])
+      : "l"(p));
 }
 
-// List filter: the octant certificate.  Each cell also stores, per octant
-// (bit d set: the centre is at or above x0 on axis d -- an exact sign test),
-// an fp16 lower bound of the distance from the octant's box to the cloud
-// (rounded down at build, the box grown by the cell-index rounding); an
-// undecided in-band sphere whose bound exceeds fl(r (1 + 2^-20)) is free.
-// Survivors are compacted in order within each warp (one atomic per warp).
-// One 2-byte load per listed sphere instead of an octant record for every
-// sphere in K0 (32-byte records there cost more than the shorter list saves).
-__device__ __forceinline__ bool octant_free(const FieldArgs& a, const FieldGeom& g, float x,
-                                            float y, float z, float r) {
-  const int ix = __float2int_rd(__fmul_rn(__fsub_rn(x, g.lo[0]), g.inv_h));
-  const int iy = __float2int_rd(__fmul_rn(__fsub_rn(y, g.lo[1]), g.inv_h));
-  const int iz = __float2int_rd(__fmul_rn(__fsub_rn(z, g.lo[2]), g.inv_h));
-  const bool in = unsigned(ix) < unsigned(g.nx) && unsigned(iy) < unsigned(g.ny) &&
-                  unsigned(iz) < unsigned(g.nz);
-  if (!in || !(r >= a.rlo_f && r <= a.rhi_f)) return false;
-  const unsigned o = (x - centre_of(ix, g.h, g.c0[0]) >= 0.f ? 1u : 0u) |
-                     (y - centre_of(iy, g.h, g.c0[1]) >= 0.f ? 2u : 0u) |
-                     (z - centre_of(iz, g.h, g.c0[2]) >= 0.f ? 4u : 0u);
-  const unsigned cell =
-      (unsigned(iz) * unsigned(g.ny) + unsigned(iy)) * unsigned(g.nx) + unsigned(ix);
-  return oct_bound(a.t.field + g.cells, cell, o) > r * kK1;
-}
-
-__global__ void __launch_bounds__(256) k_list_octant(FieldArgs a, uint32_t* __restrict__ out,
-                                                     uint32_t* __restrict__ out_n) {
-  const FieldGeom g = a.t.fg;
+__global__ void __launch_bounds__(256) k_list_knn(FieldArgs a, uint32_t* __restrict__ list2,
+                                                  uint32_t* __restrict__ list2_n) {
+  const DevTree& t = a.t;
+  const FieldGeom& g = a.t.fg;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // K0's list is complete
   const uint32_t n_list = *a.list_n;
   const int lane = threadIdx.x & 31;
   const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t j0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; j0 < n_list; j0 += stride) {
-    const uint32_t j = j0 + lane;
+  const int L = a.L;
+  const float qs = g.q_step, qe = g.q_err * (1.0f + 0x1p-17f);
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j - lane < n_list; j += stride) {
     const bool act = j < n_list;
-    const uint32_t q = act ? a.list[j] : 0u;
-    bool keep = act;
+    uint32_t q = 0u;
+    float4 sph = make_float4(0.f, 0.f, 0.f, 0.f);
     if (act) {
-      const float x = __ldg(a.c + 3 * size_t(q)), y = __ldg(a.c + 3 * size_t(q) + 1),
-                  z = __ldg(a.c + 3 * size_t(q) + 2), r = __ldg(a.r + q);
-      keep = !octant_free(a, g, x, y, z, r);
+      q = __ldcs(a.list + j);
+      sph = __ldcs(a.list_s + j);
     }
-    const unsigned km = __ballot_sync(0xffffffffu, keep);
-    unsigned base = 0;
-    if (lane == 0 && km) base = atomicAdd(out_n, unsigned(__popc(km)));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (keep) out[base + __popc(km & ((1u << lane) - 1u))] = q;
+    const float x = sph.x, y = sph.y, z = sph.z, r = sph.w;
+    const int ix = __float2int_rd(__fmul_rn(__fsub_rn(x, g.lo[0]), g.inv_h));
+    const int iy = __float2int_rd(__fmul_rn(__fsub_rn(y, g.lo[1]), g.inv_h));
+    const int iz = __float2int_rd(__fmul_rn(__fsub_rn(z, g.lo[2]), g.inv_h));
+    const bool cert = act && r >= a.rlo_f && r <= a.rhi_f && unsigned(ix) < unsigned(g.nx) &&
+                      unsigned(iy) < unsigned(g.ny) && unsigned(iz) < unsigned(g.nz);
+    bool hit = false, open = act;
+    if (cert) {
+      const unsigned cell =
+          (unsigned(iz) * unsigned(g.ny) + unsigned(iy)) * unsigned(g.nx) + unsigned(ix);
+      const uint32_t* rec = t.cand + size_t(cell) * kCandWords;
+      uint32_t w[kCandWords];
+#pragma unroll
+      for (int i = 0; i < kCandWords / 8; ++i) {
+        uint32_t v[8];
+        ld_v8u(rec + 8 * i, v);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) w[8 * i + k] = v[k];
+      }
+      const float ex = x - centre_of(ix, g.h, g.c0[0]);
+      const float ey = y - centre_of(iy, g.h, g.c0[1]);
+      const float ez = z - centre_of(iz, g.h, g.c0[2]);
+      const float RH = r * (1.0f - 0x1p-18f) - qe;
+      const float RM = r * (1.0f + 0x1p-18f) + qe;
+      const float lo = RH > 0.f ? RH * RH * (1.0f - 0x1p-20f) : -1.f;
+      const float hi = RM * RM * (1.0f + 0x1p-20f);
+      bool amb = false;
+#pragma unroll
+      for (int k = 0; k < kCand; ++k) {
+        const uint32_t wx = w[k >> 1], wy = w[16 + (k >> 1)], wz = w[32 + (k >> 1)];
+        const int ox = (k & 1) ? slot_hi(wx) : slot_lo(wx);
+        const int oy = (k & 1) ? slot_hi(wy) : slot_lo(wy);
+        const int oz = (k & 1) ? slot_hi(wz) : slot_lo(wz);
+        const float vx = fmaf(-float(ox), qs, ex), vy = fmaf(-float(oy), qs, ey),
+                    vz = fmaf(-float(oz), qs, ez);
+        const float S = d2_fma(vx, vy, vz);
+        const bool used = ox != kCandNone;
+        hit |= used && S <= lo;
+        amb |= used && S < hi;
+      }
+      const float kd = float(slot_hi(w[15])) * qs;  // (x slot 31: kd_q, exact)
+      const float A = kd - r * kK1;
+      const bool free = !amb && A > 0.f && A * A > d2_fma(ex, ey, ez) * kK1;
+      open = !hit && !free;
+    }
+    if (hit) {
+      const uint32_t b = L == 1 ? q : q / uint32_t(L);
+      atomicOr(a.bits + (b >> 5), 1u << (b & 31));
+    }
+    const unsigned om = __ballot_sync(0xffffffffu, open);
+    if (om) {
+      unsigned base = 0;
+      if (lane == 0) base = atomicAdd(list2_n, unsigned(__popc(om)));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (open) list2[base + __popc(om & ((1u << lane) - 1u))] = q;
+    }
   }
 }
 
-// The tree path over the list (the reference's semantics for every sphere it
-// holds).  The list is short but its spheres are the hard ones, so the kernel
-// is built for short dependent-load chains: a warp takes 8 entries; lanes 0-7
-// descend (T through L1), load the leaf's probe record
-// (conservative AABB reject, representative probe); then 4 lanes per entry
-// scan its set, 64 points per step (12 128-bit loads in flight per lane),
-// fp32 with the float64 re-scan of the band.  (One entry per lane with a
-// serial warp scan, or a per-thread scan, measured ~73 us for config 1's 85 K
-// entries: the warp waits on its longest chain.)
-constexpr int kLE = 8;  // list entries per warp
-
-template <bool kOct>
-__global__ void __launch_bounds__(256) k_resolve_list(FieldArgs a) {
+// The list stage, part 2 (k_tree_list): the tree path over the entries part
+// 1 left open, with the reference's semantics (query.py:184-219): descent,
+// AABB prefilter, set scan.  The entries are few (about 1e-5 of a batch) and
+// their sets long (config 3: up to 6,851 rows), so the kernel is built for
+// short dependent chains: one warp per entry, the descent 5 levels per round
+// trip (warp_descend), the leaf's probe record (conservative fp16 AABB
+// reject, representative probe), then the set in steps of 512 rows (twelve
+// 128-bit loads in flight per lane), fp32 with the float64 re-scan of the
+// band; spheres outside the fast path (non-finite, extreme radii) take the
+// exact float64 scan.
+__global__ void __launch_bounds__(256) k_tree_list(FieldArgs a) {
   const DevTree& t = a.t;
-  // launched with programmatic stream serialisation: scheduled while K0
-  // drains, reads K0's list only after K0 has completed
+  // launched with programmatic stream serialisation: scheduled while part 1
+  // drains, reads its list only after it has completed
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t n_list = *a.list_n;
   const int lane = threadIdx.x & 31;
-  const int slot = lane >> 2, sl = lane & 3;
   const int L = a.L;
   const bool prefilter = a.flags & CAPT_PREFILTER;
   const float band_lo = 1.0f - kTau, band_hi = 1.0f + kTau;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t j0 = warp * kLE; j0 < n_list; j0 += nwarps * kLE) {
-    const uint32_t j = j0 + lane;
-    const bool active = lane < kLE && j < n_list;
-    const uint32_t q = active ? a.list[j] : 0u;
-    float cx = 0.f, cy = 0.f, cz = 0.f, r = 0.f;
-    if (active) {
-      cx = __ldg(a.c + 3 * size_t(q));
-      cy = __ldg(a.c + 3 * size_t(q) + 1);
-      cz = __ldg(a.c + 3 * size_t(q) + 2);
-      r = __ldg(a.r + q);
+  for (uint32_t e = warp; e < n_list; e += nwarps) {
+    const uint32_t q = a.list[e];
+    const uint32_t b = L == 1 ? q : q / uint32_t(L);
+    // (a lane group already resolved by another entry: nothing to add)
+    if (L > 1 && (__ldcg(a.bits + (b >> 5)) >> (b & 31)) & 1u) continue;
+    const float c[3] = {__ldg(a.c + 3 * size_t(q)), __ldg(a.c + 3 * size_t(q) + 1),
+                        __ldg(a.c + 3 * size_t(q) + 2)};
+    const float r = __ldg(a.r + q);
+    const int leaf = int(warp_descend<float>(t, c, lane));
+    const float r2 = r * r;
+    const bool cfin = isfinite(c[0]) && isfinite(c[1]) && isfinite(c[2]);
+    const bool fast = cfin && r2 >= kR2Min && r2 <= kR2Max;
+    // non-finite centre with a finite radius never collides (float64 r^2 is finite)
+    int st = fast ? 2 : ((!cfin && isfinite(r)) ? 0 : 3);
+    float pr[8];
+    ld_v8(t.probe + 8 * leaf, pr);
+    if (prefilter && fast) {
+      const float2 l01 = h2f2(pr[3]), l2h0 = h2f2(pr[4]), h12 = h2f2(pr[5]);
+      const float rx = fmaxf(fmaxf(l01.x - c[0], 0.f), c[0] - l2h0.y);
+      const float ry = fmaxf(fmaxf(l01.y - c[1], 0.f), c[1] - h12.x);
+      const float rz = fmaxf(fmaxf(l2h0.x - c[2], 0.f), c[2] - h12.y);
+      if (d2_fma(rx, ry, rz) > r2 * band_hi) st = 0;
     }
-    const uint32_t gid = active ? q / uint32_t(L) : 0xffffffffu - lane;
-    const unsigned gm = L > 1 ? __match_any_sync(0xffffffffu, gid) : (1u << lane);
-    int st = 0, leaf = 0;
-    bool verdict = false;
-    float r2 = 0.f;
-    // the octant certificate first (k_list_octant when the list is filtered)
-    const bool sure_free = kOct && active && octant_free(a, a.t.fg, cx, cy, cz, r);
-    if (active && !sure_free) {
-      // descent (tree.py:266-273)
-      int i = 0;
-      for (int s = 0; s < t.depth; ++s) {  // (the top levels stay in L1)
-        const int ax = s % 3;
-        const float cv = ax == 0 ? cx : (ax == 1 ? cy : cz);
-        i = 2 * i + 1 + (cv > __ldg(t.T + i) ? 1 : 0);
-      }
-      leaf = i - int(t.n - 1);
-      // classification (as k_bin_count3 / k_query_hybrid)
-      r2 = r * r;
-      const bool cfin = isfinite(cx) && isfinite(cy) && isfinite(cz);
-      const bool fast = cfin && r2 >= kR2Min && r2 <= kR2Max;
-      st = fast ? 2 : ((!cfin && isfinite(r)) ? 0 : 3);
-      float pr[8];
-      ld_v8(t.probe + 8 * leaf, pr);
-      if (prefilter) {
-        const float2 l01 = h2f2(pr[3]), l2h0 = h2f2(pr[4]), h12 = h2f2(pr[5]);
-        const float rx = fmaxf(fmaxf(l01.x - cx, 0.f), cx - l2h0.y);
-        const float ry = fmaxf(fmaxf(l01.y - cy, 0.f), cy - h12.x);
-        const float rz = fmaxf(fmaxf(l2h0.x - cz, 0.f), cz - h12.y);
-        st = (fast && d2_fma(rx, ry, rz) > r2 * band_hi) ? 0 : st;
-      }
-      verdict = st == 2 && d2_fma(cx - pr[0], cy - pr[1], cz - pr[2]) <= r2 * band_lo;
-    }
-    const unsigned hitm = __ballot_sync(0xffffffffu, verdict);
-    const bool scan = (st == 2 || st == 3) && !verdict && (hitm & gm) == 0;
-    uint2 set = make_uint2(0u, 0u);
-    if (scan) set = __ldg(t.set + leaf);
-    // the scan, load-balanced over the warp: entry e's set is split into
-    // items of 64 points; in each step slot k (lanes 4k .. 4k+3, 16 points
-    // per lane) takes item 8 step + k of the concatenated item list, so the
-    // warp takes ceil(sum items / 8) steps instead of the longest set's
-    const bool scan32 = scan && st == 2;
-    const uint32_t m4e = scan32 ? ((set.y + 3u) & ~3u) : 0u;   // lanes 0-7: entry lane
-    // rows to scan: with the distance-sorted copy, only those within
-    // r + |c - o| of the set's origin (fl, rounded up: see sorted_limit)
-    uint32_t lime = m4e;
-    if (scan32 && t.sdata && m4e > 256u) {  // (short sets: scanning beats the search)
-      const float4 o = __ldg(t.org + leaf);
-      const float e = sqrtf(d2_fma(cx - o.x, cy - o.y, cz - o.z));
-      // (|r|: a negative radius collides like its magnitude, d^2 <= r*r)
-      const float cut = __fmul_ru(__fadd_ru(fabsf(r), e), 1.0f + 0x1p-18f);
-      lime = sorted_limit(t.sdist + int64_t(set.x) * 4 / 3, m4e, cut);
-    }
-    const uint32_t items = (lime + 63u) >> 6;
-    uint32_t incl = items;  // inclusive prefix over lanes 0-7
-#pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
-      const uint32_t tv = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += tv;
-    }
-    uint32_t pre[kLE];  // inclusive prefix of every entry (uniform)
-#pragma unroll
-    for (int e = 0; e < kLE; ++e) pre[e] = __shfl_sync(0xffffffffu, incl, e);
-    const uint32_t total = pre[kLE - 1];
-    const float loB0 = r2 * band_lo, hiB0 = r2 * band_hi;
-    bool hit_e = false, amb_e = false;  // lanes 0-7: their entry's result
-    for (uint32_t s0 = 0; s0 < total; s0 += kLE) {
-      const uint32_t item = s0 + slot;
-      int e = 0;
-#pragma unroll
-      for (int k = 0; k < kLE - 1; ++k) e += item >= pre[k] ? 1 : 0;
-      const uint32_t first = e ? pre[e - 1] : 0u;
-      // entry e's data (shuffles are warp-wide; lanes past the end read entry 7)
-      const float sx = __shfl_sync(0xffffffffu, cx, e);
-      const float sy = __shfl_sync(0xffffffffu, cy, e);
-      const float sz = __shfl_sync(0xffffffffu, cz, e);
-      const float loB = __shfl_sync(0xffffffffu, loB0, e);
-      const float hiB = __shfl_sync(0xffffffffu, hiB0, e);
-      const uint32_t sset = __shfl_sync(0xffffffffu, set.x, e);
-      const uint32_t m4 = __shfl_sync(0xffffffffu, m4e, e);    // SoA stride
-      const uint32_t lim = __shfl_sync(0xffffffffu, lime, e);  // rows to scan
-      const bool done = __shfl_sync(0xffffffffu, hit_e, e);  // entry already hit: skip
-      const bool live = item < total && !done;
-      const float* base = t.sdata ? t.sdata + int64_t(sset) * 4
-                                  : reinterpret_cast<const float*>(t.data + sset);
-      const uint32_t p0 = (item - first) * 64u;
-      bool hit = false, amb = false;
-      if (live) {
-        // all 12 loads in flight: rows past the set are clamped to row 0 and
-        // masked out of the result
+    if (st == 0) continue;
+    const float loB = r2 * band_lo, hiB = r2 * band_hi;
+    bool verdict = st == 2 && d2_fma(c[0] - pr[0], c[1] - pr[1], c[2] - pr[2]) <= loB;
+    const uint2 set = __ldg(t.set + leaf);
+    if (!verdict && st == 2) {
+      const float* xs = reinterpret_cast<const float*>(t.data + set.x);
+      const uint32_t m4 = (set.y + 3u) & ~3u;
+      bool amb = false;
+      for (uint32_t p0 = 0; p0 < m4 && !verdict; p0 += 512) {
         float4 px[4], py[4], pz[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const uint32_t p = p0 + 16 * u + 4 * sl;
-          const uint32_t pc = p < lim ? p : 0u;
-          px[u] = __ldg(reinterpret_cast<const float4*>(base + pc));
-          py[u] = __ldg(reinterpret_cast<const float4*>(base + m4 + pc));
-          pz[u] = __ldg(reinterpret_cast<const float4*>(base + 2 * m4 + pc));
+          const uint32_t p = p0 + 128 * u + 4 * lane;
+          const uint32_t pc = p < m4 ? p : 0u;
+          px[u] = __ldg(reinterpret_cast<const float4*>(xs + pc));
+          py[u] = __ldg(reinterpret_cast<const float4*>(xs + m4 + pc));
+          pz[u] = __ldg(reinterpret_cast<const float4*>(xs + 2 * m4 + pc));
         }
+        bool hit = false;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const bool in = p0 + 16 * u + 4 * sl < lim;
-          const float xs[4] = {px[u].x, px[u].y, px[u].z, px[u].w},
-                      ys[4] = {py[u].x, py[u].y, py[u].z, py[u].w},
-                      zs[4] = {pz[u].x, pz[u].y, pz[u].z, pz[u].w};
+          if (p0 + 128 * u + 4 * lane >= m4) continue;  // (padding rows are +inf: misses)
+          const float X[4] = {px[u].x, px[u].y, px[u].z, px[u].w},
+                      Y[4] = {py[u].x, py[u].y, py[u].z, py[u].w},
+                      Z[4] = {pz[u].x, pz[u].y, pz[u].z, pz[u].w};
 #pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            const float d2 = d2_fma(sx - xs[w], sy - ys[w], sz - zs[w]);
-            hit |= in && d2 <= loB;
-            amb |= in && d2 < hiB;
+          for (int k = 0; k < 4; ++k) {
+            const float d2 = d2_fma(c[0] - X[k], c[1] - Y[k], c[2] - Z[k]);
+            hit |= d2 <= loB;
+            amb |= d2 < hiB;
           }
         }
+        verdict = __any_sync(0xffffffffu, hit);
       }
-      // fold the step's results into the owning entries (lanes 0-7)
-      const unsigned hb = __ballot_sync(0xffffffffu, hit);
-      const unsigned ab = __ballot_sync(0xffffffffu, amb);
-#pragma unroll
-      for (int k = 0; k < kLE; ++k) {
-        const uint32_t ik = s0 + k;
-        int ek = 0;
-#pragma unroll
-        for (int j = 0; j < kLE - 1; ++j) ek += ik >= pre[j] ? 1 : 0;
-        if (ek == lane && ik < total) {
-          hit_e |= ((hb >> (4 * k)) & 15u) != 0;
-          amb_e |= ((ab >> (4 * k)) & 15u) != 0;
-        }
-      }
+      if (!verdict && __any_sync(0xffffffffu, amb)) st = 3;  // band: decide exactly
     }
-    if (scan && st == 2) verdict = hit_e;
-    // float64 re-scans (fp32 band hits; st == 3: the exact path only), one
-    // entry at a time by the whole warp (a per-thread scan of a 600-point set
-    // is a chain of dependent loads that outlasts the rest of the kernel)
-    unsigned exact = __ballot_sync(0xffffffffu, scan && !verdict && (st == 3 || amb_e));
-    while (exact) {
-      const int src = __ffs(exact) - 1;
-      exact &= exact - 1;
-      const double c64[3] = {__shfl_sync(0xffffffffu, double(cx), src),
-                             __shfl_sync(0xffffffffu, double(cy), src),
-                             __shfl_sync(0xffffffffu, double(cz), src)};
-      const double r64 = __shfl_sync(0xffffffffu, double(r), src);
-      const uint2 sset = make_uint2(__shfl_sync(0xffffffffu, set.x, src),
-                                    __shfl_sync(0xffffffffu, set.y, src));
-      const uint32_t slim = __shfl_sync(0xffffffffu, lime, src);
-      const bool sfast = __shfl_sync(0xffffffffu, st == 2, src);
-      const uint32_t sm4 = (sset.y + 3u) & ~3u;
-      // a fast sphere's rows beyond its cutoff are float64 misses: the sorted
-      // copy's first slim rows hold every possible hit
-      const bool h64 =
-          (sfast && t.sdata)
-              ? warp_scan_f64_rows(t.sdata + int64_t(sset.x) * 4, sm4, min(slim, sset.y),
-                                   t.k, c64, __dmul_rn(r64, r64), lane)
-              : warp_scan_f64(t, sset, c64, r64, lane);
-      if (lane == src) verdict = h64;
+    if (st == 3 && !verdict) {
+      const double c64[3] = {double(c[0]), double(c[1]), double(c[2])};
+      verdict = warp_scan_f64(t, set, c64, double(r), lane);
     }
-    // one OR per hit sphere (L = 1) or per group (first hitting lane)
-    const unsigned vm = __ballot_sync(0xffffffffu, verdict);
-    if (verdict && lane == __ffs(vm & gm) - 1) {
-      const uint32_t b = L == 1 ? q : q / uint32_t(L);
-      atomicOr(a.bits + (b >> 5), 1u << (b & 31));
-    }
+    if (verdict && lane == 0) atomicOr(a.bits + (b >> 5), 1u << (b & 31));
   }
 }
 
@@ -991,67 +819,12 @@ __global__ void __launch_bounds__(256) k_resolve_list(FieldArgs a) {
 
 // ---------------------------------------------------------------- host
 
-static int build_sorted(capt_tree* tree, cudaStream_t s) {
-  if (tree->sdata) cudaFree(tree->sdata);
-  if (tree->sdist) cudaFree(tree->sdist);
-  tree->sdata = tree->sdist = nullptr;
-  const DevTree t = view(tree);
-  const int64_t nf = tree->h.data_f4 * 4;  // floats of the data section
-  const int64_t items = nf / 3;
-  if (items <= 0 || items >= (int64_t(1) << 31)) return CAPT_OK;  // (no sorted copy)
-  uint32_t *keys = nullptr, *keys_o = nullptr, *vals = nullptr, *vals_o = nullptr;
-  int *sb = nullptr, *se = nullptr;
-  void* tmp = nullptr;
-  size_t tb = 0;
-  CAPT_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, keys, keys_o, vals, vals_o, int(items),
-                                                int(t.n), sb, se, s));
-  cudaError_t e = cudaSuccess;
-  float *sdata = nullptr, *sdist = nullptr;
-  e = cudaMalloc(&sdata, sizeof(float) * size_t(nf));
-  if (e == cudaSuccess) e = cudaMalloc(&sdist, sizeof(float) * size_t(items));
-  if (e == cudaSuccess) e = dmalloc(&keys, items, s);
-  if (e == cudaSuccess) e = dmalloc(&keys_o, items, s);
-  if (e == cudaSuccess) e = dmalloc(&vals, items, s);
-  if (e == cudaSuccess) e = dmalloc(&vals_o, items, s);
-  if (e == cudaSuccess) e = dmalloc(&sb, t.n, s);
-  if (e == cudaSuccess) e = dmalloc(&se, t.n, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&tmp, tb + 16, s);
-  if (e == cudaSuccess) {
-    k_sort_keys<<<grid_for(t.n * 32, 256, 8), 256, 0, s>>>(t, keys, vals, sb, se);
-    e = cub::DeviceSegmentedSort::SortPairs(tmp, tb, keys, keys_o, vals, vals_o, int(items),
-                                            int(t.n), sb, se, s);
-  }
-  if (e == cudaSuccess) {
-    k_sort_gather<<<grid_for(t.n * 32, 256, 8), 256, 0, s>>>(t, keys_o, vals_o, sdata, sdist);
-    e = cudaGetLastError();
-  }
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  cudaFreeAsync(keys, s);
-  cudaFreeAsync(keys_o, s);
-  cudaFreeAsync(vals, s);
-  cudaFreeAsync(vals_o, s);
-  cudaFreeAsync(sb, s);
-  cudaFreeAsync(se, s);
-  cudaFreeAsync(tmp, s);
-  if (e != cudaSuccess) {
-    cudaFree(sdata);
-    cudaFree(sdist);
-    if (e == cudaErrorMemoryAllocation) {  // optional acceleration: run without it
-      cudaGetLastError();
-      return CAPT_OK;
-    }
-    return cuda_fail(e, "sorted set copy");
-  }
-  note_launches(3);
-  tree->sdata = sdata;
-  tree->sdist = sdist;
-  return CAPT_OK;
-}
-
 int build_field(capt_tree* tree, cudaStream_t s) {
-  if (tree->field) {
-    cudaFree(tree->field);
+  if (tree->field_mem) {
+    cudaFree(tree->field_mem);
+    tree->field_mem = nullptr;
     tree->field = nullptr;
+    tree->cand = nullptr;
   }
   if (tree->h.k != 3) return CAPT_OK;
   const DevTree t = view(tree);
@@ -1115,23 +888,17 @@ int build_field(capt_tree* tree, cudaStream_t s) {
   // even when its computed cell index is off by one
   g.rcap = float(rmax + h);
   g.m = int(std::ceil(double(g.rcap) / h)) + 2;
-  // octant boxes: a centre assigned to a cell lies within h/2 + delta of its
-  // x0 per axis (delta covers the rounding of the cell index and of x0);
-  // half-edge hh = h/2 + delta rounded up; absolute slack for the rounded
-  // gaps; bounds capped at rcap - sqrt(3) hh (points beyond the candidate
-  // search are farther than that from every octant point)
+  // candidate offsets: int16 multiples of a power-of-two step covering rcap;
+  // the decoded difference fl(fl(c - x0) - q step) is within, per axis,
+  // step / 2 (offset rounding) + u |c - x0| + u |fl(c - x0) - q step| of
+  // c - p (u = 2^-24, |c - x0| <= h, |q step| <= 2 rcap): q_err bounds the
+  // Euclidean sum, rounded up
   {
-    double maxabs = 0.0;
-    int64_t maxdim = std::max<int64_t>(dims[0], std::max<int64_t>(dims[1], dims[2]));
-    for (int d = 0; d < 3; ++d)
-      maxabs = std::max(maxabs, std::max(std::fabs(double(g.lo[d])),
-                                         std::fabs(double(g.lo[d]) + dims[d] * h)));
     const double u = std::ldexp(1.0, -24);
-    const double delta = h * std::ldexp(1.0, -12) + 8 * u * (double(maxdim) * h + maxabs);
-    g.oct_half = std::nextafter(float(0.5 * h + delta), INFINITY);
-    g.oct_abs = float(16 * u * (maxabs + double(g.rcap) + h));
-    g.oct_cap = std::max(0.0f, float(double(g.rcap) - std::sqrt(3.0) * double(g.oct_half)) *
-                                   (1.0f - 0x1p-20f));
+    const double step = std::ldexp(1.0, int(std::ceil(std::log2(double(g.rcap) / 32767.0))));
+    g.q_step = float(step);
+    const double ax = 0.5 * step + 4.0 * u * (h + 2.0 * double(g.rcap) + step);
+    g.q_err = std::nextafter(float(std::sqrt(3.0) * ax * (1.0 + 1e-6)), INFINITY);
   }
   BucketGrid b;
   b.nbx = (g.nx + g.m - 1) / g.m;
@@ -1141,19 +908,29 @@ int build_field(capt_tree* tree, cudaStream_t s) {
 
   uint32_t *keys = nullptr, *keys_out = nullptr, *counts = nullptr, *bstart = nullptr;
   int *ids = nullptr, *ids_out = nullptr;
-  float4* pts = nullptr;
   void* tmp = nullptr;
   size_t tb_sort = 0, tb_scan = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tb_sort, keys, keys_out, ids, ids_out, int(n), 0, 32, s);
   cub::DeviceScan::ExclusiveSum(nullptr, tb_scan, counts, bstart, int(b.nb + 2), s);
-  CAPT_CUDA(dmalloc(&keys, n, s));
-  CAPT_CUDA(dmalloc(&keys_out, n, s));
-  CAPT_CUDA(dmalloc(&ids, n, s));
-  CAPT_CUDA(dmalloc(&ids_out, n, s));
-  CAPT_CUDA(dmalloc(&counts, b.nb + 2, s));
-  CAPT_CUDA(dmalloc(&bstart, b.nb + 2, s));
-  CAPT_CUDA(dmalloc(&pts, n, s));
-  CAPT_CUDA(cudaMallocAsync(&tmp, std::max(tb_sort, tb_scan) + 16, s));
+  struct Scratch {
+    cudaStream_t s;
+    std::vector<void*> p;
+    ~Scratch() {
+      for (void* q : p) cudaFreeAsync(q, s);
+    }
+  } scratch{s, {}};
+  auto get = [&](auto** ptr, size_t count) {
+    const cudaError_t e = dmalloc(ptr, count, s);
+    if (e == cudaSuccess) scratch.p.push_back(*ptr);
+    return e;
+  };
+  CAPT_CUDA(get(&keys, n));
+  CAPT_CUDA(get(&keys_out, n));
+  CAPT_CUDA(get(&ids, n));
+  CAPT_CUDA(get(&ids_out, n));
+  CAPT_CUDA(get(&counts, b.nb + 2));
+  CAPT_CUDA(get(&bstart, b.nb + 2));
+  CAPT_CUDA(get(reinterpret_cast<char**>(&tmp), std::max(tb_sort, tb_scan) + 16));
   CAPT_CUDA(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * (b.nb + 2), s));
   k_bucket_keys<<<grid_for(n, 256, 8), 256, 0, s>>>(t.rep, n, g, b, keys, ids, counts);
   CAPT_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb_sort, keys, keys_out, ids, ids_out, int(n), 0,
@@ -1162,29 +939,30 @@ int build_field(capt_tree* tree, cudaStream_t s) {
   uint32_t n_fin = 0;
   CAPT_CUDA(cudaMemcpyAsync(&n_fin, bstart + b.nb, 4, cudaMemcpyDeviceToHost, s));
   CAPT_CUDA(cudaStreamSynchronize(s));
-  k_bucket_points<<<grid_for(n_fin, 256, 8), 256, 0, s>>>(t.rep, ids_out, n_fin, pts);
-  float4* field = nullptr;
-  cudaError_t e = cudaMalloc(&field, 2 * sizeof(float4) * size_t(g.cells));
+  float4* pts = nullptr;
+  CAPT_CUDA(get(&pts, std::max<uint32_t>(n_fin, 1)));
+  // one allocation: K0 records | candidate records
+  const size_t off_cand = (sizeof(float4) * size_t(g.cells) + 255) & ~size_t(255);  // (32-B loads)
+  const size_t bytes = off_cand + sizeof(uint32_t) * kCandWords * size_t(g.cells);
+  char* mem = nullptr;
+  cudaError_t e = cudaMalloc(&mem, bytes);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(clearance field)");
-  k_field_nn<<<int(b.nb), 256, 0, s>>>(g, b, bstart, pts, field);
+  float4* field = reinterpret_cast<float4*>(mem);
+  uint32_t* cand = reinterpret_cast<uint32_t*>(mem + off_cand);
+  k_bucket_points<<<grid_for(n_fin, 256, 8), 256, 0, s>>>(t.rep, ids_out, n_fin, pts);
+  k_field_cand<<<int(b.nb), 256, 0, s>>>(g, b, bstart, pts, field, cand);
   e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  cudaFreeAsync(keys, s);
-  cudaFreeAsync(keys_out, s);
-  cudaFreeAsync(ids, s);
-  cudaFreeAsync(ids_out, s);
-  cudaFreeAsync(counts, s);
-  cudaFreeAsync(bstart, s);
-  cudaFreeAsync(pts, s);
-  cudaFreeAsync(tmp, s);
   if (e != cudaSuccess) {
-    cudaFree(field);
+    cudaFree(mem);
     return cuda_fail(e, "clearance field build");
   }
   note_launches(6);
+  tree->field_mem = mem;
   tree->field = field;
+  tree->cand = cand;
   tree->fg = g;
-  return build_sorted(tree, s);
+  return CAPT_OK;
 }
 
 constexpr int64_t kFieldMinBatch = 8192;
@@ -1194,9 +972,8 @@ bool field_eligible(const DevTree& t, int64_t n, uint32_t flags) {
   if (n >= (int64_t(1) << 31) - (int64_t(1) << 24)) return false;
   // fp32 r^2 of every in-band radius must stay normal and finite
   if (!(t.r_min >= 0x1p-50) || !(t.r_max <= 0x1p50)) return false;
-  if (flags & CAPT_MODE_FIELD) return true;  // (+ MODE_BINNED / MODE_DIRECT: the list path)
+  if (flags & CAPT_MODE_FIELD) return true;
   // below a few thousand spheres the one-kernel warp path has less fixed cost
-  // (two kernels, two memsets here: ~13 us at 1 K spheres vs ~8)
   if (n < kFieldMinBatch) return false;
   return !(flags & (CAPT_MODE_DIRECT | CAPT_MODE_BINNED | CAPT_MODE_THREAD | CAPT_MODE_WARP));
 }
@@ -1226,20 +1003,46 @@ static cudaError_t launch_pdl_f(void (*kernel)(KArgs...), int grid, int block, c
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
+// Per-(device, stream) scratch for the list: reused across calls instead of
+// a cudaMallocAsync / cudaFreeAsync pair per call.  A call holds the entry's
+// lock while it enqueues its kernels, so two host threads issuing queries on
+// the same stream cannot interleave their uses of the buffer (the stream
+// orders the kernels of each call after the previous call's).
+struct ListScratch {
+  std::mutex mu;
+  uint32_t* buf = nullptr;  // counters (8 words: list_n, list2_n) | list | list2 | list_s
+  int64_t cap = 0;          // capacity of each list (entries, a multiple of 4)
+};
+static std::mutex g_scratch_mu;
+static std::map<std::pair<int, cudaStream_t>, ListScratch*>* g_scratch = nullptr;
+
+static ListScratch* scratch_for(int dev, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_scratch_mu);
+  if (!g_scratch) g_scratch = new std::map<std::pair<int, cudaStream_t>, ListScratch*>();
+  ListScratch*& e = (*g_scratch)[{dev, s}];
+  if (!e) e = new ListScratch();  // (kept for the process: streams are reused)
+  return e;
+}
+
 // Stage timing (capt_stage_timing / capt_stage_times): CUDA events on the
 // launching stream around K0 and the list stage of every field-pipeline call,
 // read back and summed on request (no synchronisation inside the calls).
 struct StageEvents {
   static constexpr int kMax = 2048;
+  std::mutex mu;
   bool on = false;
   int n = 0;
   cudaEvent_t ev[kMax][3] = {};
-  void record(int call, int k, cudaStream_t s) {
-    if (!ev[call][k]) cudaEventCreate(&ev[call][k]);
-    cudaEventRecord(ev[call][k], s);
-  }
 };
-static StageEvents g_stage;
+static StageEvents g_stage[kMaxDevices];
+
+static int stage_record(int dev, int call, int k, cudaStream_t s) {
+  StageEvents& st = g_stage[dev];
+  std::lock_guard<std::mutex> lk(st.mu);
+  if (!st.ev[call][k]) CAPT_CUDA(cudaEventCreate(&st.ev[call][k]));
+  CAPT_CUDA(cudaEventRecord(st.ev[call][k], s));
+  return CAPT_OK;
+}
 
 int launch_field(const DevTree& t, const void* centers, const void* radii, int64_t n, int L,
                  const uint8_t* mask, uint32_t flags, uint32_t* bits, int64_t n_words,
@@ -1251,7 +1054,7 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   a.n = int(n);
   a.L = L;
   a.mask = mask;
-  a.flags = flags;
+  a.flags = flags & ~uint32_t(CAPT_MODE_BINNED | CAPT_MODE_DIRECT | CAPT_MODE_FIELD);
   a.bits = bits;
   a.first_bad = first_bad;
   float lo = float(t.r_min), hi = float(t.r_max);
@@ -1259,109 +1062,82 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   if (double(hi) > t.r_max) hi = nextafterf(hi, -INFINITY);
   a.rlo_f = lo;
   a.rhi_f = hi;
-  CAPT_CUDA(dmalloc(&a.list_n, 8, s));
-  CAPT_CUDA(dmalloc(&a.list, n, s));
+  int dev = 0;
+  CAPT_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return fail(CAPT_ECUDA, "device index out of range");
+  ListScratch* sc = scratch_for(dev, s);
+  std::lock_guard<std::mutex> lk(sc->mu);
+  if (sc->cap < n) {
+    if (sc->buf) CAPT_CUDA(cudaFreeAsync(sc->buf, s));
+    sc->buf = nullptr;
+    sc->cap = 0;
+    const int64_t cap = (n + 3) & ~int64_t(3);
+    CAPT_CUDA(dmalloc(&sc->buf, 6 * size_t(cap) + 8, s));
+    sc->cap = cap;
+  }
+  a.list_n = sc->buf;
+  a.list = sc->buf + 8;
+  uint32_t* const list2_n = sc->buf + 1;
+  uint32_t* const list2 = sc->buf + 8 + sc->cap;
+  a.list_s = reinterpret_cast<float4*>(sc->buf + 8 + 2 * sc->cap);
   {
     const int64_t zw = L >= 8 ? n_words : 0;
     k_field_zero<<<grid_for(zw + 8, 256, 4), 256, 0, s>>>(a.list_n, bits, zw);
     CAPT_CUDA(cudaGetLastError());
     note_launches(1);
   }
-  const int tcall = (g_stage.on && g_stage.n < StageEvents::kMax) ? g_stage.n++ : -1;
-  if (tcall >= 0) g_stage.record(tcall, 0, s);
+  int tcall = -1;
+  {
+    StageEvents& st = g_stage[dev];
+    std::lock_guard<std::mutex> lk2(st.mu);
+    if (st.on && st.n < StageEvents::kMax) tcall = st.n++;
+  }
+  if (tcall >= 0) {
+    const int rc = stage_record(dev, tcall, 0, s);
+    if (rc) return rc;
+  }
   const bool vec = (reinterpret_cast<uintptr_t>(centers) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(radii) & 15) == 0;
   const int grid = grid_for(((n + 127) / 128) * 32, CAPT_K0_BLOCK, 8 * 256 / CAPT_K0_BLOCK);
-  // unmasked 16-B aligned batches: the TMA-fed kernel (specialised for single
-  // spheres and 8-sphere groups, configs 0-4); everything else the register path
-  static const bool use_tma = getenv("CAPT_K0_TMA") != nullptr;
-  if (vec && !mask && use_tma && n >= kTileSpheres) {
-    static bool attr = false;
-    if (!attr) {
-      for (auto f : {k_resolve_tma<1>, k_resolve_tma<8>, k_resolve_tma<0>})
-        CAPT_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTmaSmem)));
-      attr = true;
-    }
-    const int gt = grid_for(((n + kTileSpheres - 1) / kTileSpheres) * 256, 256, 4);
-    if (L == 1) k_resolve_tma<1><<<gt, 256, kTmaSmem, s>>>(a);
-    else if (L == 8) k_resolve_tma<8><<<gt, 256, kTmaSmem, s>>>(a);
-    else k_resolve_tma<0><<<gt, 256, kTmaSmem, s>>>(a);
-  }
-  else if (vec && !mask && L == 1) CAPT_CUDA(launch_pdl_f(k_resolve<true, false, 1>, grid, CAPT_K0_BLOCK, s, a));
+  if (vec && !mask && L == 1) CAPT_CUDA(launch_pdl_f(k_resolve<true, false, 1>, grid, CAPT_K0_BLOCK, s, a));
   else if (vec && !mask && L == 8) CAPT_CUDA(launch_pdl_f(k_resolve<true, false, 8>, grid, CAPT_K0_BLOCK, s, a));
   else if (mask) CAPT_CUDA(launch_pdl_f(k_resolve<false, true, 0>, grid, CAPT_K0_BLOCK, s, a));
   else CAPT_CUDA(launch_pdl_f(k_resolve<false, false, 0>, grid, CAPT_K0_BLOCK, s, a));
   CAPT_CUDA(cudaGetLastError());
   note_launches(1);
-  if (tcall >= 0) g_stage.record(tcall, 1, s);
-  // the list: one warp-cooperative kernel, or -- for large batches over large
-  // affordance sets, where the tensor-core binned scan amortises each set
-  // over up to 128 spheres -- the leaf-binned pipeline in list mode
-  static const int force = [] {
-    const char* e = getenv("CAPT_FIELD_LIST");
-    return !e ? 0 : (e[0] == 'b' ? 2 : 1);
-  }();
-  bool binned = force ? force == 2 : (n >= (int64_t(1) << 22) && t.total >= 512 * t.n);
-  if (flags & CAPT_MODE_FIELD) {
-    if (flags & CAPT_MODE_BINNED) binned = true;
-    if (flags & CAPT_MODE_DIRECT) binned = false;
+  if (tcall >= 0) {
+    const int rc = stage_record(dev, tcall, 1, s);
+    if (rc) return rc;
   }
-  flags &= ~uint32_t(CAPT_MODE_BINNED | CAPT_MODE_DIRECT | CAPT_MODE_FIELD);
-  int rc = CAPT_OK;
-  FieldArgs a2 = a;  // the filtered list (binned path)
-  if (binned) {
-    // (K1 in list mode applies the octant certificate itself)
-    static const bool filt = getenv("CAPT_OCT_FILTER") != nullptr;
-    if (filt) {
-      CAPT_CUDA(dmalloc(&a2.list_n, 1, s));
-      CAPT_CUDA(dmalloc(&a2.list, n, s));
-      CAPT_CUDA(cudaMemsetAsync(a2.list_n, 0, 4, s));
-      k_list_octant<<<grid_for(int64_t(n) / 64 + 1, 256, 2), 256, 0, s>>>(a, a2.list, a2.list_n);
-      CAPT_CUDA(cudaGetLastError());
-      note_launches(1);
-    }
-    rc = launch_binned(t, centers, radii, n, L, nullptr, flags, bits, n_words, first_bad, s,
-                       a2.list, a2.list_n);
-  } else {
-    // grid for the worst case (every sphere listed): 8 entries per warp
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid_for(int64_t(n) * 4 + 32, 256, 8));
-    cfg.blockDim = dim3(256);
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    CAPT_CUDA(cudaLaunchKernelEx(&cfg, k_resolve_list<true>, a));
-    CAPT_CUDA(cudaGetLastError());
-    note_launches(1);
+  // the list stage: persistent grids (the list lengths are known on the device only)
+  CAPT_CUDA(launch_pdl_f(k_list_knn, grid_for(n, 256, 8), 256, s, a, list2, list2_n));
+  FieldArgs a2 = a;
+  a2.list = list2;
+  a2.list_s = nullptr;
+  a2.list_n = list2_n;
+  CAPT_CUDA(launch_pdl_f(k_tree_list, grid_for(int64_t(n) * 32, 256, 8), 256, s, a2));
+  CAPT_CUDA(cudaGetLastError());
+  note_launches(2);
+  if (tcall >= 0) {
+    const int rc = stage_record(dev, tcall, 2, s);
+    if (rc) return rc;
   }
-  if (tcall >= 0) g_stage.record(tcall, 2, s);
-  static const bool debug = getenv("CAPT_DEBUG") != nullptr;
-  if (debug) {
-    uint32_t nl = 0, nl2 = 0;
-    CAPT_CUDA(cudaMemcpyAsync(&nl, a.list_n, 4, cudaMemcpyDeviceToHost, s));
-    if (a2.list != a.list) CAPT_CUDA(cudaMemcpyAsync(&nl2, a2.list_n, 4, cudaMemcpyDeviceToHost, s));
-    CAPT_CUDA(cudaStreamSynchronize(s));
-    fprintf(stderr, "[capt field] n=%lld L=%d undecided=%u (%.3f%%) after octants=%u (%.3f%%) list=%s\n",
-            (long long)n, L, nl, 100.0 * nl / double(n ? n : 1), nl2, 100.0 * nl2 / double(n ? n : 1),
-            binned ? "binned" : "thread");
-  }
-  cudaFreeAsync(a.list, s);
-  cudaFreeAsync(a.list_n, s);
-  if (a2.list != a.list) {
-    cudaFreeAsync(a2.list, s);
-    cudaFreeAsync(a2.list_n, s);
-  }
-  return rc;
+#ifdef CAPT_FIELD_STATS  // diagnostics build (build_ext -D CAPT_FIELD_STATS --out ...)
+  uint32_t nl[2] = {0, 0};
+  CAPT_CUDA(cudaMemcpyAsync(nl, a.list_n, 8, cudaMemcpyDeviceToHost, s));
+  CAPT_CUDA(cudaStreamSynchronize(s));
+  fprintf(stderr, "[capt field] n=%lld L=%d list=%u (%.4f%%) tree path=%u (%.5f%%)\n",
+          (long long)n, L, nl[0], 100.0 * nl[0] / double(n), nl[1], 100.0 * nl[1] / double(n));
+#endif
+  return CAPT_OK;
 }
 
 }  // namespace capt
 
 using namespace capt;
 
-extern "C" int capt_tree_field(const capt_tree* tree, capt_field_info* info, float* cells) {
+extern "C" int capt_tree_field(const capt_tree* tree, capt_field_info* info, float* cells,
+                               float* cand) {
   if (!tree || !info) return fail(CAPT_EINVAL, "NULL argument");
   if (!tree->field) return fail(CAPT_EINVAL, "tree has no clearance field (k < 3)");
   const FieldGeom& g = tree->fg;
@@ -1369,49 +1145,81 @@ extern "C" int capt_tree_field(const capt_tree* tree, capt_field_info* info, flo
   info->nx = g.nx;
   info->ny = g.ny;
   info->nz = g.nz;
+  info->n_cand = kCand;
   info->n_cells = g.cells;
   info->h = g.h;
   info->rcap = g.rcap;
-  info->oct_half = g.oct_half;
+  info->q_step = g.q_step;
+  info->q_err = g.q_err;
   for (int d = 0; d < 3; ++d) {
     info->lo[d] = g.lo[d];
     info->c0[d] = g.c0[d];
     info->box_lo[d] = g.blo[d];
     info->box_hi[d] = g.bhi[d];
   }
-  if (cells) {  // device: all witness records, then all octant records; out: interleaved
-    CAPT_CUDA(cudaSetDevice(tree->device));
-    std::vector<float4> tmp(2 * size_t(g.cells));
-    CAPT_CUDA(cudaMemcpy(tmp.data(), tree->field, 2 * sizeof(float4) * size_t(g.cells),
-                         cudaMemcpyDeviceToHost));
-    float4* out = reinterpret_cast<float4*>(cells);
-    for (int64_t i = 0; i < g.cells; ++i) {
-      out[2 * i] = tmp[i];
-      out[2 * i + 1] = tmp[g.cells + i];
+  if (!cells && !cand) return CAPT_OK;
+  CAPT_CUDA(cudaSetDevice(tree->device));
+  const size_t nc = size_t(g.cells);
+  std::vector<float4> rec(nc);
+  std::vector<uint32_t> w(nc * kCandWords);
+  CAPT_CUDA(cudaMemcpy(rec.data(), tree->field, sizeof(float4) * nc, cudaMemcpyDeviceToHost));
+  CAPT_CUDA(cudaMemcpy(w.data(), tree->cand, sizeof(uint32_t) * w.size(), cudaMemcpyDeviceToHost));
+  auto slot = [&](size_t cell, int axis, int j) {
+    const uint32_t v = w[cell * kCandWords + 16 * axis + (j >> 1)];
+    return int(int16_t(uint16_t((j & 1) ? (v >> 16) : (v & 0xffffu))));
+  };
+  const float INF = std::numeric_limits<float>::infinity();
+  for (size_t i = 0; i < nc; ++i) {
+    if (cells) {
+      float* o = cells + 8 * i;
+      o[0] = rec[i].x;
+      o[1] = rec[i].y;
+      o[2] = rec[i].z;
+      o[3] = rec[i].w;
+      o[4] = float(slot(i, 0, 31)) * g.q_step;  // kd
+      o[5] = float(slot(i, 1, 31));            // candidates
+      o[6] = o[7] = 0.f;
+    }
+    if (cand) {  // offsets (p - x0) / q_step, kCandNone for unused slots
+      for (int k = 0; k < kCand; ++k)
+        for (int d = 0; d < 3; ++d) {
+          const int q = slot(i, d, k);
+          cand[(i * kCand + k) * 3 + d] = q == kCandNone ? INF : float(q);
+        }
     }
   }
   return CAPT_OK;
 }
 
 extern "C" int capt_stage_timing(int enable) {
-  g_stage.on = enable != 0;
-  g_stage.n = 0;
+  int dev = 0;
+  CAPT_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return fail(CAPT_ECUDA, "device index out of range");
+  StageEvents& st = g_stage[dev];
+  std::lock_guard<std::mutex> lk(st.mu);
+  st.on = enable != 0;
+  st.n = 0;
   return CAPT_OK;
 }
 
 extern "C" int capt_stage_times(double* ms, int64_t* calls) {
   if (!ms || !calls) return fail(CAPT_EINVAL, "NULL argument");
+  int dev = 0;
+  CAPT_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return fail(CAPT_ECUDA, "device index out of range");
+  StageEvents& st = g_stage[dev];
+  std::lock_guard<std::mutex> lk(st.mu);
   ms[0] = ms[1] = ms[2] = 0.0;
-  for (int i = 0; i < g_stage.n; ++i) {
-    CAPT_CUDA(cudaEventSynchronize(g_stage.ev[i][2]));
+  for (int i = 0; i < st.n; ++i) {
+    CAPT_CUDA(cudaEventSynchronize(st.ev[i][2]));
     float a = 0.f, b = 0.f;
-    CAPT_CUDA(cudaEventElapsedTime(&a, g_stage.ev[i][0], g_stage.ev[i][1]));
-    CAPT_CUDA(cudaEventElapsedTime(&b, g_stage.ev[i][1], g_stage.ev[i][2]));
+    CAPT_CUDA(cudaEventElapsedTime(&a, st.ev[i][0], st.ev[i][1]));
+    CAPT_CUDA(cudaEventElapsedTime(&b, st.ev[i][1], st.ev[i][2]));
     ms[0] += a;
     ms[1] += b;
     ms[2] += a + b;
   }
-  *calls = g_stage.n;
-  g_stage.n = 0;
+  *calls = st.n;
+  st.n = 0;
   return CAPT_OK;
 }

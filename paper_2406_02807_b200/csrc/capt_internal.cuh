@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 
 #include "../../include/capt_b200.h"
@@ -68,9 +69,21 @@ struct FieldGeom {
   float h, inv_h;
   float blo[3], bhi[3];
   float rcap;
-  float oct_half, oct_abs, oct_cap;  // octant boxes (half-edge), bound slack and cap
+  float q_step;        // candidate offsets from x0: int16 multiples of q_step (a power of two)
+  float q_err;         // bound on the Euclidean error of a decoded candidate difference
   int64_t cells;
 };
+
+// Candidate record of a cell: the kCand cloud points nearest its centre x0,
+// as int16 offsets (p - x0) / q_step per axis, and kd_q: kd_q * q_step <= the
+// distance from x0 to every other cloud point.  48 words (192 B, six 32-B
+// loads): words 0-15 hold the x offsets of slots 0..31 (two per word, slot 2w
+// in the low half), words 16-31 the y offsets, words 32-47 the z offsets;
+// x slot 31 is kd_q, y slot 31 the candidate count; unused slots hold
+// kCandNone.
+constexpr int kCand = 31;
+constexpr int kCandWords = 48;
+constexpr int kCandNone = -32768;
 
 struct DevTree {
   int k, depth;
@@ -86,13 +99,10 @@ struct DevTree {
   const float4* rep;  // row 0 of every set (the point owning the cell), +inf for padding
   const int* order;   // leaves by descending set size
   const float* probe; // 8 floats per leaf: rep xyz, fp16 box (conservative), 2 spare
-  const float4* field;  // clearance field: per cell witness xyz + lower bound (or nullptr)
+  // clearance field (capt_field.cu; field == nullptr if absent)
+  const float4* field;    // per cell: witness xyz + lower bound nn
+  const uint32_t* cand;   // per cell: kCandWords words (candidate record, see kCand)
   FieldGeom fg;
-  // distance-sorted copy of the sets (capt_field.cu; nullptr if absent): the
-  // data section's layout with each set's rows ordered by |p - o| (o = org),
-  // and per set the sorted distances, rounded down: m4 floats at 4 set.x / 3
-  const float* sdata;
-  const float* sdist;
 };
 
 }  // namespace capt
@@ -101,10 +111,13 @@ struct capt_tree {
   capt::SlabHeader h;
   int device;
   char* slab;  // device pointer
-  float4* field = nullptr;  // derived per device from the slab (capt_field.cu)
+  bool owns_slab = true;  // false: borrowed from the caller (capt_tree_from_slab, CAPT_SLAB_BORROW)
+  // clearance field: derived per device from the slab (capt_field.cu), one
+  // allocation holding the K0 records and the candidate records
+  void* field_mem = nullptr;
+  float4* field = nullptr;
+  uint32_t* cand = nullptr;
   capt::FieldGeom fg{};
-  float* sdata = nullptr;   // distance-sorted set copy (capt_field.cu)
-  float* sdist = nullptr;
 };
 
 namespace capt {
@@ -145,9 +158,8 @@ inline DevTree view(const capt_tree* t) {
   d.order = reinterpret_cast<const int*>(t->slab + t->h.off_order);
   d.probe = reinterpret_cast<const float*>(t->slab + t->h.off_probe);
   d.field = t->field;
+  d.cand = t->cand;
   d.fg = t->fg;
-  d.sdata = t->sdata;
-  d.sdist = t->sdist;
   return d;
 }
 
@@ -207,14 +219,29 @@ inline cudaError_t dmalloc(T** p, size_t count, cudaStream_t s) {
   return cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(T) * (count ? count : 1), s);
 }
 
+// One-time per-device set-up (function attributes apply to the current
+// device only): f(device) runs once per device, its status is kept.
+constexpr int kMaxDevices = 64;
+struct DeviceOnce {
+  std::once_flag flag[kMaxDevices];
+  int rc[kMaxDevices] = {};
+};
+template <class F>
+inline int per_device_once(DeviceOnce& o, F&& f) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
+    return fail(CAPT_ECUDA, "no current CUDA device");
+  std::call_once(o.flag[dev], [&] { o.rc[dev] = f(dev); });
+  return o.rc[dev];
+}
+
 inline int grid_for(int64_t work, int block, int max_blocks_per_sm = 8) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
+  static const int sms = [] {  // (every device of the box is the same part)
+    int dev = 0, v = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
   int64_t need = (work + block - 1) / block;
   int64_t cap = int64_t(sms) * max_blocks_per_sm;
   if (need < 1) need = 1;

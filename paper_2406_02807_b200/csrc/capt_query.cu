@@ -23,7 +23,9 @@
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <mutex>
 #include <type_traits>
+#include <vector>
 
 #include "capt_binned.cuh"
 #include "capt_internal.cuh"
@@ -217,31 +219,6 @@ __global__ void __launch_bounds__(kBlock)
 //     (coalesced SoA loads), with a warp vote after every iteration;
 //   * re-run the exact float64 scan cooperatively for band/slow spheres.
 // ---------------------------------------------------------------------------
-template <typename C>
-__device__ __forceinline__ int64_t warp_descend(const DevTree& t, const C c[3], int lane) {
-  int64_t i = 0;
-  int ax = 0;
-  for (int s = 0; s < t.depth;) {
-    const int lv = min(5, t.depth - s);
-    const int nodes = (1 << lv) - 1;
-    float tv = 0.f;
-    if (lane < nodes) {
-      const int lvl = 31 - __clz(lane + 1);
-      const int64_t g = ((i + 1) << lvl) - 1 + (lane + 1 - (1 << lvl));
-      tv = __ldg(t.T + g);
-    }
-    int j = 0;
-    for (int r = 0; r < lv; ++r) {
-      const float v = __shfl_sync(0xffffffffu, tv, j);
-      j = 2 * j + 1 + (pick3(c, ax) > C(v) ? 1 : 0);
-      ax = (ax + 1 == t.k) ? 0 : ax + 1;
-    }
-    i = ((i + 1) << lv) - 1 + (j + 1 - (1 << lv));
-    s += lv;
-  }
-  return i - (t.n - 1);
-}
-
 template <typename InT>
 __global__ void __launch_bounds__(kBlock)
     k_query_warp(DevTree t, const void* __restrict__ centers, const void* __restrict__ radii,
@@ -541,88 +518,132 @@ int query_device(const DevTree& t, const void* d_c, const void* d_r, int64_t n, 
 // are written into one device array copied back once at the end (a
 // per-chunk copy into pageable user memory would block the host thread and
 // serialise the pipeline).
+//
+// Each call takes a PipeState (two worker streams, events, a pinned buffer
+// for the per-chunk first_bad and counters) from a per-device free list, so
+// concurrent calls on one tree never share them (a Capt is safe for any
+// number of concurrent readers, tree.py:67-71).
 struct PipeState {
+  static constexpr int kMaxChunks = 1024;
   cudaStream_t w[2] = {nullptr, nullptr};
   cudaEvent_t start = nullptr, done[2] = {nullptr, nullptr};
   unsigned long long* pinned = nullptr;  // per chunk: first_bad + 6 counters
-  static constexpr int kMaxChunks = 1024;
 };
 
-static PipeState* pipe_state(int device) {
-  static PipeState states[64];
-  static bool init[64] = {false};
-  if (device < 0 || device >= 64) return nullptr;
-  PipeState& p = states[device];
-  if (!init[device]) {
-    for (int i = 0; i < 2; ++i) {
-      cudaStreamCreateWithFlags(&p.w[i], cudaStreamNonBlocking);
-      cudaEventCreateWithFlags(&p.done[i], cudaEventDisableTiming);
+struct PipePool {
+  std::mutex mu;
+  std::vector<PipeState*> free_list;
+};
+static PipePool g_pipes[kMaxDevices];
+
+static PipeState* pipe_acquire(int device) {
+  if (device < 0 || device >= kMaxDevices) return nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_pipes[device].mu);
+    auto& fl = g_pipes[device].free_list;
+    if (!fl.empty()) {
+      PipeState* p = fl.back();
+      fl.pop_back();
+      return p;
     }
-    cudaEventCreateWithFlags(&p.start, cudaEventDisableTiming);
-    cudaHostAlloc(reinterpret_cast<void**>(&p.pinned),
-                  sizeof(unsigned long long) * 7 * PipeState::kMaxChunks, cudaHostAllocDefault);
-    init[device] = true;
   }
-  return p.pinned ? &p : nullptr;
+  PipeState* p = new PipeState();
+  bool ok = true;
+  for (int i = 0; i < 2; ++i) {
+    ok = ok && cudaStreamCreateWithFlags(&p->w[i], cudaStreamNonBlocking) == cudaSuccess;
+    ok = ok && cudaEventCreateWithFlags(&p->done[i], cudaEventDisableTiming) == cudaSuccess;
+  }
+  ok = ok && cudaEventCreateWithFlags(&p->start, cudaEventDisableTiming) == cudaSuccess;
+  ok = ok && cudaHostAlloc(reinterpret_cast<void**>(&p->pinned),
+                           sizeof(unsigned long long) * 7 * PipeState::kMaxChunks,
+                           cudaHostAllocDefault) == cudaSuccess;
+  if (!ok) {
+    for (int i = 0; i < 2; ++i) {
+      if (p->w[i]) cudaStreamDestroy(p->w[i]);
+      if (p->done[i]) cudaEventDestroy(p->done[i]);
+    }
+    if (p->start) cudaEventDestroy(p->start);
+    if (p->pinned) cudaFreeHost(p->pinned);
+    delete p;
+    return nullptr;
+  }
+  return p;
+}
+
+static void pipe_release(int device, PipeState* p) {
+  std::lock_guard<std::mutex> lk(g_pipes[device].mu);
+  g_pipes[device].free_list.push_back(p);
 }
 
 int query_host_pipelined(const capt_tree* tree, const DevTree& t, const void* centers,
                          const void* radii, int64_t n, int L, const uint8_t* lane_mask,
                          uint32_t flags, uint32_t* out_bits, uint64_t* counters,
                          int64_t* first_bad, cudaStream_t s, int64_t chunk) {
-  PipeState* p = pipe_state(tree->device);
-  if (!p) return fail(CAPT_ECUDA, "pipeline streams unavailable");
   const size_t in_elem = (flags & CAPT_INPUT_F64) ? sizeof(double) : sizeof(float);
   const int64_t n_chunks = (n + chunk - 1) / chunk;
   if (n_chunks > PipeState::kMaxChunks) return fail(CAPT_EINVAL, "batch too large for the pipeline");
-  struct Buf {
-    void* c = nullptr;
-    void* r = nullptr;
-    uint8_t* m = nullptr;
-    unsigned long long* aux = nullptr;  // first_bad + 6 counters
-  } buf[2];
+  PipeState* p = pipe_acquire(tree->device);
+  if (!p) return fail(CAPT_ECUDA, "pipeline streams unavailable");
+  // every exit path: device buffers freed in stream order, the worker
+  // streams joined into s, s drained, the state returned to the pool
+  struct Call {
+    PipeState* p;
+    int device;
+    cudaStream_t s;
+    void* c[2] = {nullptr, nullptr};
+    void* r[2] = {nullptr, nullptr};
+    uint8_t* m[2] = {nullptr, nullptr};
+    unsigned long long* aux[2] = {nullptr, nullptr};  // first_bad + 6 counters
+    uint32_t* d_bits = nullptr;
+    ~Call() {
+      for (int i = 0; i < 2; ++i) {
+        if (c[i]) cudaFreeAsync(c[i], p->w[i]);
+        if (r[i]) cudaFreeAsync(r[i], p->w[i]);
+        if (m[i]) cudaFreeAsync(m[i], p->w[i]);
+        if (aux[i]) cudaFreeAsync(aux[i], p->w[i]);
+        cudaEventRecord(p->done[i], p->w[i]);
+        cudaStreamWaitEvent(s, p->done[i], 0);
+      }
+      if (d_bits) cudaFreeAsync(d_bits, s);
+      cudaStreamSynchronize(s);
+      cudaStreamSynchronize(p->w[0]);
+      cudaStreamSynchronize(p->w[1]);
+      pipe_release(device, p);
+    }
+  } call{p, tree->device, s};
   const int64_t words_total = (n / L + 31) / 32;
-  uint32_t* d_bits = nullptr;
-  CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_bits), 4 * words_total, s));
+  CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&call.d_bits), 4 * words_total, s));
   CAPT_CUDA(cudaEventRecord(p->start, s));
   for (int i = 0; i < 2; ++i) {
     cudaStream_t w = p->w[i];
     CAPT_CUDA(cudaStreamWaitEvent(w, p->start, 0));
-    CAPT_CUDA(cudaMallocAsync(&buf[i].c, in_elem * t.k * chunk, w));
-    CAPT_CUDA(cudaMallocAsync(&buf[i].r, in_elem * chunk, w));
-    if (lane_mask) CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf[i].m), chunk, w));
-    CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf[i].aux), 8 * 7, w));
+    CAPT_CUDA(cudaMallocAsync(&call.c[i], in_elem * t.k * chunk, w));
+    CAPT_CUDA(cudaMallocAsync(&call.r[i], in_elem * chunk, w));
+    if (lane_mask) CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&call.m[i]), chunk, w));
+    CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&call.aux[i]), 8 * 7, w));
   }
-  int rc = CAPT_OK;
-  for (int64_t ci = 0; ci < n_chunks && rc == CAPT_OK; ++ci) {
+  for (int64_t ci = 0; ci < n_chunks; ++ci) {
     const int b = int(ci & 1);
     cudaStream_t w = p->w[b];
     const int64_t base = ci * chunk;
     const int64_t len = n - base < chunk ? n - base : chunk;
     const char* hc = static_cast<const char*>(centers) + in_elem * t.k * base;
     const char* hr = static_cast<const char*>(radii) + in_elem * base;
-    CAPT_CUDA(cudaMemcpyAsync(buf[b].c, hc, in_elem * t.k * len, cudaMemcpyHostToDevice, w));
-    CAPT_CUDA(cudaMemcpyAsync(buf[b].r, hr, in_elem * len, cudaMemcpyHostToDevice, w));
+    CAPT_CUDA(cudaMemcpyAsync(call.c[b], hc, in_elem * t.k * len, cudaMemcpyHostToDevice, w));
+    CAPT_CUDA(cudaMemcpyAsync(call.r[b], hr, in_elem * len, cudaMemcpyHostToDevice, w));
     if (lane_mask)
-      CAPT_CUDA(cudaMemcpyAsync(buf[b].m, lane_mask + base, len, cudaMemcpyHostToDevice, w));
-    rc = query_device(t, buf[b].c, buf[b].r, len, L, lane_mask ? buf[b].m : nullptr, flags,
-                      d_bits + base / L / 32, buf[b].aux + 1, buf[b].aux, w);
-    if (rc) break;
-    CAPT_CUDA(cudaMemcpyAsync(p->pinned + 7 * ci, buf[b].aux, 8 * 7, cudaMemcpyDeviceToHost, w));
+      CAPT_CUDA(cudaMemcpyAsync(call.m[b], lane_mask + base, len, cudaMemcpyHostToDevice, w));
+    const int rc = query_device(t, call.c[b], call.r[b], len, L, lane_mask ? call.m[b] : nullptr,
+                               flags, call.d_bits + base / L / 32, call.aux[b] + 1, call.aux[b], w);
+    if (rc) return rc;
+    CAPT_CUDA(cudaMemcpyAsync(p->pinned + 7 * ci, call.aux[b], 8 * 7, cudaMemcpyDeviceToHost, w));
   }
   for (int i = 0; i < 2; ++i) {
-    cudaFreeAsync(buf[i].c, p->w[i]);
-    cudaFreeAsync(buf[i].r, p->w[i]);
-    if (buf[i].m) cudaFreeAsync(buf[i].m, p->w[i]);
-    cudaFreeAsync(buf[i].aux, p->w[i]);
     CAPT_CUDA(cudaEventRecord(p->done[i], p->w[i]));
     CAPT_CUDA(cudaStreamWaitEvent(s, p->done[i], 0));
   }
-  if (rc == CAPT_OK)
-    CAPT_CUDA(cudaMemcpyAsync(out_bits, d_bits, 4 * words_total, cudaMemcpyDeviceToHost, s));
-  cudaFreeAsync(d_bits, s);
+  CAPT_CUDA(cudaMemcpyAsync(out_bits, call.d_bits, 4 * words_total, cudaMemcpyDeviceToHost, s));
   CAPT_CUDA(cudaStreamSynchronize(s));
-  if (rc) return rc;
   int64_t fb = -1;
   uint64_t cnt[6] = {0, 0, 0, 0, 0, 0};
   for (int64_t ci = 0; ci < n_chunks; ++ci) {

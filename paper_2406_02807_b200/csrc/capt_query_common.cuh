@@ -252,39 +252,32 @@ __device__ __forceinline__ bool warp_scan_f64(const DevTree& t, uint2 set, const
   return warp_scan_f64_rows(base, m4, set.y, t.k, c, __dmul_rn(r64, r64), lane);
 }
 
-// first row of a distance-sorted set beyond `cut` (binary search over 64-row items)
-__device__ __forceinline__ uint32_t sorted_limit(const float* __restrict__ sd, uint32_t m4,
-                                                 float cut) {
-  uint32_t lo = 0, hi = (m4 + 63u) >> 6;  // items [0, hi): the answer is in items
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (__ldg(sd + 64u * mid) > cut) hi = mid;
-    else lo = mid + 1;
+// Warp-cooperative descent (tree.py:266-273): 5 Eytzinger levels per L1/L2
+// round trip -- lane j loads node j of the 31-node subtree under the current
+// node, the path is then walked with shuffles.
+template <typename C>
+__device__ __forceinline__ int64_t warp_descend(const DevTree& t, const C c[3], int lane) {
+  int64_t i = 0;
+  int ax = 0;
+  for (int s = 0; s < t.depth;) {
+    const int lv = min(5, t.depth - s);
+    const int nodes = (1 << lv) - 1;
+    float tv = 0.f;
+    if (lane < nodes) {
+      const int lvl = 31 - __clz(lane + 1);
+      const int64_t g = ((i + 1) << lvl) - 1 + (lane + 1 - (1 << lvl));
+      tv = __ldg(t.T + g);
+    }
+    int j = 0;
+    for (int r = 0; r < lv; ++r) {
+      const float v = __shfl_sync(0xffffffffu, tv, j);
+      j = 2 * j + 1 + (pick3(c, ax) > C(v) ? 1 : 0);
+      ax = (ax + 1 == t.k) ? 0 : ax + 1;
+    }
+    i = ((i + 1) << lv) - 1 + (j + 1 - (1 << lv));
+    s += lv;
   }
-  return min(m4, lo * 64u);  // every row at or after it is beyond cut
-}
-
-// The clearance field's octant certificate (capt_field.cu): true when the
-// octant of c's cell holds an fp16 distance bound above fl(r (1 + 2^-20)) --
-// then no cloud point lies within r of c (in-band radius, c inside the grid).
-__device__ __forceinline__ bool octant_free_t(const DevTree& t, float rlo, float rhi, float x,
-                                              float y, float z, float r) {
-  const FieldGeom& g = t.fg;
-  const int ix = __float2int_rd(__fmul_rn(__fsub_rn(x, g.lo[0]), g.inv_h));
-  const int iy = __float2int_rd(__fmul_rn(__fsub_rn(y, g.lo[1]), g.inv_h));
-  const int iz = __float2int_rd(__fmul_rn(__fsub_rn(z, g.lo[2]), g.inv_h));
-  const bool in = unsigned(ix) < unsigned(g.nx) && unsigned(iy) < unsigned(g.ny) &&
-                  unsigned(iz) < unsigned(g.nz);
-  if (!t.field || !in || !(r >= rlo && r <= rhi)) return false;
-  auto centre = [&](int i, float c0) { return __fmaf_rn(__int2float_rn(i), g.h, c0); };
-  const unsigned o = (x - centre(ix, g.c0[0]) >= 0.f ? 1u : 0u) |
-                     (y - centre(iy, g.c0[1]) >= 0.f ? 2u : 0u) |
-                     (z - centre(iz, g.c0[2]) >= 0.f ? 4u : 0u);
-  const size_t cell =
-      (size_t(iz) * unsigned(g.ny) + unsigned(iy)) * unsigned(g.nx) + unsigned(ix);
-  const unsigned short hb =
-      __ldg(reinterpret_cast<const unsigned short*>(t.field + g.cells) + 8 * cell + o);
-  return __half2float(__ushort_as_half(hb)) > r * (1.0f + 0x1p-20f);
+  return i - (t.n - 1);
 }
 
 }  // namespace capt

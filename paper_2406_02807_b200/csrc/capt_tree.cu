@@ -377,10 +377,9 @@ void capt_tree_destroy(capt_tree* t) {
   int cur = 0;
   cudaGetDevice(&cur);
   cudaSetDevice(t->device);
-  cudaFree(t->slab);
-  if (t->field) cudaFree(t->field);
-  if (t->sdata) cudaFree(t->sdata);
-  if (t->sdist) cudaFree(t->sdist);
+  if (t->owns_slab) cudaFree(t->slab);
+  else cudaDeviceSynchronize();  // (cudaFree's implicit sync: no query still reads the borrowed slab)
+  if (t->field_mem) cudaFree(t->field_mem);
   cudaSetDevice(cur);
   delete t;
 }
@@ -392,8 +391,8 @@ int capt_tree_slab(const capt_tree* t, const void** dev_ptr, int64_t* bytes) {
   return CAPT_OK;
 }
 
-int capt_tree_from_slab(int device, const void* dev_slab, int64_t bytes, void* stream,
-                        capt_tree** out) {
+int capt_tree_from_slab(int device, const void* dev_slab, int64_t bytes, uint32_t flags,
+                        void* stream, capt_tree** out) {
   if (!out || !dev_slab) return fail(CAPT_EINVAL, "NULL argument");
   *out = nullptr;
   CAPT_CUDA(cudaSetDevice(device));
@@ -403,10 +402,21 @@ int capt_tree_from_slab(int device, const void* dev_slab, int64_t bytes, void* s
   CAPT_CUDA(cudaStreamSynchronize(s));
   if (h.magic != kSlabMagic || h.version != kSlabVersion || h.bytes != bytes)
     return fail(CAPT_EINVAL, "not a capt_b200 tree slab");
-  int rc = alloc_slab(out, device, h);
-  if (rc) return rc;
-  cudaError_t e = cudaMemcpyAsync((*out)->slab, dev_slab, size_t(bytes), cudaMemcpyDeviceToDevice, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  int rc = CAPT_OK;
+  cudaError_t e = cudaSuccess;
+  if (flags & CAPT_SLAB_BORROW) {
+    // adopt the caller's buffer (a replica received by broadcast): no copy
+    *out = new capt_tree();
+    (*out)->h = h;
+    (*out)->device = device;
+    (*out)->slab = static_cast<char*>(const_cast<void*>(dev_slab));
+    (*out)->owns_slab = false;
+  } else {
+    rc = alloc_slab(out, device, h);
+    if (rc) return rc;
+    e = cudaMemcpyAsync((*out)->slab, dev_slab, size_t(bytes), cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  }
   if (e != cudaSuccess) {
     capt_tree_destroy(*out);
     *out = nullptr;

@@ -61,7 +61,7 @@ def replicate_tree(tree, src: int = 0, group=None, device=None):
     if rank == src:
         return tree
     torch.cuda.synchronize(dev)
-    return Capt.from_slab(slab, device=device)
+    return Capt.from_slab(slab, device=device, adopt=True)
 
 
 def reduce_counters(counters, group=None):

@@ -116,6 +116,7 @@ class Capt:
             except Exception:  # noqa: BLE001 - interpreter shutdown
                 pass
             self._h = None
+        self._slab_owner = None  # an adopted slab outlives the handle
 
     @property
     def handle(self) -> C.c_void_p:
@@ -189,26 +190,36 @@ class Capt:
     def device_bytes(self) -> int:
         return int(self._info.device_bytes)
 
-    def clearance_field(self, cells: bool = False):
+    def clearance_field(self, cells: bool = False, candidates: bool = False):
         """The tree's clearance field (include/capt_b200.h capt_tree_field):
-        a dict of its geometry, plus the (nz, ny, nx, 8) float32 records
-        {witness xyz, nn, 8 fp16 octant bounds in 4 words} when ``cells``;
-        None for trees without one (k < 3)."""
+        a dict of its geometry, plus with ``cells`` the (nz, ny, nx, 8)
+        float32 records {witness xyz, nn, kd, candidate count, 0, 0} and with
+        ``candidates`` the (nz, ny, nx, n_cand, 3) candidate offsets
+        (p - x0) / q_step (+inf for unused slots); None for trees without
+        one (k < 3)."""
         info = _lib.CaptFieldInfo()
         L = _lib.lib()
-        if L.capt_tree_field(self._h, C.byref(info), None) != _lib.CAPT_OK:
+        if L.capt_tree_field(self._h, C.byref(info), None, None) != _lib.CAPT_OK:
             return None
         out = dict(shape=(info.nz, info.ny, info.nx), n_cells=int(info.n_cells),
                    lo=np.array(info.lo[:], np.float32), h=np.float32(info.h),
                    c0=np.array(info.c0[:], np.float32),
                    box_lo=np.array(info.box_lo[:], np.float32),
                    box_hi=np.array(info.box_hi[:], np.float32), rcap=np.float32(info.rcap),
-                   oct_half=np.float32(info.oct_half))
-        if cells:
-            buf = np.empty((info.nz, info.ny, info.nx, 8), np.float32)
-            _lib.check(L.capt_tree_field(self._h, C.byref(info), buf.ctypes.data),
+                   n_cand=int(info.n_cand), q_step=np.float32(info.q_step),
+                   q_err=np.float32(info.q_err))
+        if cells or candidates:
+            buf = np.empty((info.nz, info.ny, info.nx, 8), np.float32) if cells else None
+            cb = (np.empty((info.nz, info.ny, info.nx, info.n_cand, 3), np.float32)
+                  if candidates else None)
+            _lib.check(L.capt_tree_field(self._h, C.byref(info),
+                                         None if buf is None else buf.ctypes.data,
+                                         None if cb is None else cb.ctypes.data),
                        "capt_tree_field")
-            out["cells"] = buf
+            if cells:
+                out["cells"] = buf
+            if candidates:
+                out["candidates"] = cb
         return out
 
     # -- replication (multi-GPU) ---------------------------------------------
@@ -228,16 +239,25 @@ class Capt:
         return t
 
     @classmethod
-    def from_slab(cls, slab, device: int | None = None, stream=None) -> "Capt":
-        """Copy a slab (CUDA uint8 tensor) into a new tree on ``device``."""
+    def from_slab(cls, slab, device: int | None = None, stream=None,
+                  adopt: bool = False) -> "Capt":
+        """A tree over a slab (CUDA uint8 tensor) on ``device``: a copy, or with
+        ``adopt`` the tensor itself (kept alive by the tree; no second copy of
+        a broadcast replica)."""
         dev = slab.device.index if device is None else int(device)
+        if adopt and slab.device.index != dev:
+            raise ValueError("an adopted slab must live on the tree's device")
         h = C.c_void_p()
-        _lib.check(_lib.lib().capt_tree_from_slab(dev, slab.data_ptr(), int(slab.numel()),
+        flags = _lib.SLAB_BORROW if adopt else 0
+        _lib.check(_lib.lib().capt_tree_from_slab(dev, slab.data_ptr(), int(slab.numel()), flags,
                                                   None if stream is None else int(stream),
                                                   C.byref(h)), "capt_tree_from_slab")
         info = _lib.CaptTreeInfo()
         _lib.check(_lib.lib().capt_tree_info_get(h, C.byref(info)))
-        return cls._from_handle(h, info.r_min, info.r_max)
+        obj = cls._from_handle(h, info.r_min, info.r_max)
+        if adopt:
+            obj._slab_owner = slab  # released after the tree (see __del__)
+        return obj
 
     def __repr__(self) -> str:
         return (f"Capt(k={self.k}, n={self.n}, points={self.n_points}, "

@@ -1,10 +1,12 @@
 """The clearance-field query pipeline (csrc/capt_field.cu) against the oracle.
 
 The field resolves most in-band spheres from a per-cell witness point and a
-certified nearest-point lower bound; everything else goes through the tree
-path.  Every case forces CAPT_MODE_FIELD and must equal the oracle's
-collides_many / group bits (query.py:184-219, 126-167) bit for bit; the field
-records themselves are checked against float64 nearest-neighbour distances."""
+certified nearest-point lower bound (K0), then from the cell's candidate list
+(its nearest cloud points and a bound on every other point); everything else
+goes through the tree path.  Every case forces CAPT_MODE_FIELD and must equal
+the oracle's collides_many / group bits (query.py:184-219, 126-167) bit for
+bit; the field records themselves are checked against float64
+nearest-neighbour distances."""
 
 import numpy as np
 import pytest
@@ -20,8 +22,6 @@ from paper_2406_02807_b200 import workloads as W  # noqa: E402
 from paper_2406_02807_b200.query import _host_inputs, _host_query  # noqa: E402
 
 FIELD = _lib.MODE_FIELD
-# the undecided spheres go through the warp list kernel or the binned pipeline
-LIST = {"warp": FIELD | _lib.MODE_DIRECT, "binned": FIELD | _lib.MODE_BINNED}
 
 
 def upload(t):
@@ -46,9 +46,11 @@ def centres(f):
 
 def check_field(tree, cloud, sample=200000, seed=0):
     from scipy.spatial import cKDTree
-    f = tree.clearance_field(cells=True)
+    f = tree.clearance_field(cells=True, candidates=True)
     assert f is not None
     cells = f["cells"].reshape(-1, 8)
+    K = f["n_cand"]
+    cand = f["candidates"].reshape(-1, K, 3)
     nz, ny, nx = f["shape"]
     assert f["n_cells"] == nx * ny * nz <= int((1 << 21) * 1.05)
     pts = np.unique(cloud.astype(np.float32), axis=0).astype(np.float64)
@@ -59,7 +61,9 @@ def check_field(tree, cloud, sample=200000, seed=0):
     iz, rem = np.divmod(idx, ny * nx)
     iy, ix = np.divmod(rem, nx)
     x0 = np.stack([ax[0][ix], ax[1][iy], ax[2][iz]], 1).astype(np.float64)
-    nn, _ = cKDTree(pts).query(x0)
+    kt = cKDTree(cloud.astype(np.float64))  # (duplicates kept: they are distinct candidates)
+    dk, _ = kt.query(x0, k=K + 1)
+    nn = dk[:, 0]
     rec = cells[idx].astype(np.float64)
     rcap = np.float64(f["rcap"])
     # certified lower bound (one fp32 ulp of slack for the centre's double rounding here)
@@ -78,18 +82,33 @@ def check_field(tree, cloud, sample=200000, seed=0):
     assert np.allclose(rec[near, 3], nn[near], rtol=1e-5, atol=1e-7)
     wset = {tuple(p) for p in cloud.astype(np.float32)[:, :3].tolist()}
     assert all(tuple(w) in wset for w in rec[has][:2000, :3].astype(np.float32).tolist())
-    # octant bounds: below the distance from random points of the octant box
-    # (and from its corners) to the cloud, and not vacuous where nn is small
-    octs = cells[idx, 4:].copy().view(np.float16).astype(np.float64)  # (m, 8)
-    hh = np.float64(f["oct_half"])
-    o = rng.integers(0, 8, len(idx))
-    bits = np.stack([(o >> d) & 1 for d in range(3)], 1).astype(np.float64)
-    for u in (rng.uniform(0, 1, (len(idx), 3)), np.ones((len(idx), 3)), np.zeros((len(idx), 3))):
-        qpt = x0 + np.where(bits == 1, u, -u) * hh
-        dq, _ = cKDTree(pts).query(qpt)
-        assert np.all(octs[np.arange(len(idx)), o] <= dq + 1e-9)
-    lb = octs[np.arange(len(idx)), o]
-    assert np.mean(lb[near] > 0) > 0.5
+    # candidate records: the K nearest cloud points of x0 as int16 offsets
+    # (distances equal to the float64 K-nearest distances within the offset
+    # rounding where those lie inside rcap), and kd a lower bound of the
+    # (K+1)-th nearest distance, tight (to one step) inside rcap
+    step = np.float64(f["q_step"])
+    assert step == 2.0 ** np.round(np.log2(step)) and 32767 * step >= rcap
+    assert f["q_err"] >= np.sqrt(3) * step / 2
+    kd = rec[:, 4]
+    assert np.all(kd <= dk[:, K] + slack) and np.all(kd <= rcap)
+    cnt = rec[:, 5].astype(int)
+    off = cand[idx].astype(np.float64)
+    fin = np.isfinite(off[:, :, 0])
+    assert np.array_equal(fin.sum(1), cnt)
+    assert np.all(np.abs(off[fin]) <= 32767)
+    dc = np.where(fin, np.linalg.norm(off * step, axis=2), np.inf)
+    inside = dk[:, K - 1] < rcap * (1 - 1e-3)
+    assert np.all(cnt[inside] == K)
+    tol = np.sqrt(3) * step / 2 + 1e-6 * rcap
+    assert np.all(np.abs(np.sort(dc[inside], axis=1) - dk[inside, :K]) <= tol)
+    # the decoded candidates are cloud points (up to the offset rounding)
+    m = np.nonzero(inside)[0][:2000]
+    for i in m[:200]:
+        got = x0[i] + off[i, :cnt[i]] * step
+        dd, _ = kt.query(got)
+        assert np.all(dd <= tol)
+    tight = dk[:, K] < rcap * (1 - 1e-3)
+    assert np.all(kd[tight] >= dk[tight, K] - 2 * step - 1e-6 * rcap)
     return f
 
 
@@ -105,12 +124,13 @@ def test_field_records_uploaded_and_built_trees():
     # replicated trees rebuild the same field from the slab
     pytest.importorskip("torch")
     t2 = P.Capt.from_slab(tree1.slab_tensor())
-    f2 = t2.clearance_field(cells=True)
-    assert np.array_equal(f2["cells"], tree1.clearance_field(cells=True)["cells"])
+    f2 = t2.clearance_field(cells=True, candidates=True)
+    f1 = tree1.clearance_field(cells=True, candidates=True)
+    assert np.array_equal(f2["cells"], f1["cells"])
+    assert np.array_equal(f2["candidates"], f1["candidates"])
 
 
-@pytest.mark.parametrize("lp", ["warp", "binned"])
-def test_field_golden_masks_and_groups(lp):
+def test_field_golden_masks_and_groups():
     z = load_golden("queries.npz")
     for name in z["names"]:
         pts = z[f"{name}/points"]
@@ -122,12 +142,12 @@ def test_field_golden_masks_and_groups(lp):
         c, r = z[f"{name}/centers"], z[f"{name}/radii"]
         n = len(r)
         exp = np.unpackbits(z[f"{name}/mask"])[:n].astype(bool)
-        assert np.array_equal(q(tree, c, r, mode=LIST[lp]), exp), name
+        assert np.array_equal(q(tree, c, r), exp), name
         nopre = np.unpackbits(z[f"{name}/mask_nopre"])[:n].astype(bool)
-        assert np.array_equal(q(tree, c, r, prefilter=False, mode=LIST[lp]), nopre), name
+        assert np.array_equal(q(tree, c, r, prefilter=False), nopre), name
         lane = np.unpackbits(z[f"{name}/lane_mask"])[:n].astype(bool)
         gb = np.unpackbits(z[f"{name}/group8"])[: n // 8].astype(bool)
-        assert np.array_equal(q(tree, c, r, 8, lane.astype(np.uint8), mode=LIST[lp]), gb), name
+        assert np.array_equal(q(tree, c, r, 8, lane.astype(np.uint8)), gb), name
 
 
 def test_field_cfg0_golden_and_full_batch():
@@ -142,9 +162,8 @@ def test_field_cfg0_golden_and_full_batch():
     assert np.array_equal(P.collides_many(tree, c, r), O.collides_many(t, c, r))
 
 
-@pytest.mark.parametrize("lp", ["warp", "binned"])
-@pytest.mark.parametrize("L", [1, 2, 8, 32])
-def test_field_tabletop_groups_and_lane_masks(L, lp):
+@pytest.mark.parametrize("L", [1, 2, 4, 8, 16, 32])
+def test_field_tabletop_groups_and_lane_masks(L):
     cloud = W.cfg1_cloud()
     tree = P.construct(P.PointCloud(cloud), P.BuildParams(0.02, 0.08))
     t = O.tree_from(tree)
@@ -152,13 +171,14 @@ def test_field_tabletop_groups_and_lane_masks(L, lp):
     rng = np.random.default_rng(L)
     mask = (rng.uniform(size=len(r)) > 0.2).astype(np.uint8)
     exp = O.collides_groups(t, c, r, L, mask.astype(bool))
-    assert np.array_equal(q(tree, c, r, L, mask, mode=LIST[lp]), exp)
+    assert np.array_equal(q(tree, c, r, L, mask), exp)
+    # unmasked: the specialised K0 paths (L = 1, 8) and the generic one
+    assert np.array_equal(q(tree, c, r, L), O.collides_groups(t, c, r, L))
     if L == 1:
-        assert np.array_equal(q(tree, c, r, mode=LIST[lp]), O.brute_collides_many(cloud, c, r))
+        assert np.array_equal(q(tree, c, r), O.brute_collides_many(cloud, c, r))
 
 
-@pytest.mark.parametrize("lp", ["warp", "binned"])
-def test_field_tangent_spheres(lp):
+def test_field_tangent_spheres():
     # radius = the float32 image of the exact nearest-point distance, and one
     # ulp either side: every sphere sits on the certificates' decision edge
     from scipy.spatial import cKDTree
@@ -177,13 +197,12 @@ def test_field_tangent_spheres(lp):
     for rr in (r, np.nextafter(r, np.float32(0)), np.nextafter(r, np.float32(1))):
         rr = W.clamp_radii(rr.astype(np.float32), 0.01, 0.08)
         exp = O.collides_many(t, c, rr)
-        got = q(tree, c, rr, mode=LIST[lp])
+        got = q(tree, c, rr)
         assert np.array_equal(got, exp)
         assert np.array_equal(got, O.brute_collides_many(pts, c, rr))
 
 
-@pytest.mark.parametrize("lp", ["warp", "binned"])
-def test_field_edge_inputs(lp):
+def test_field_edge_inputs():
     # out-of-band radii with check_radii=False (the reference's own semantics,
     # not the brute-force ones), NaN radii, non-finite centres, centres far
     # outside the cloud's box, a batch that is not a multiple of 32
@@ -201,32 +220,34 @@ def test_field_edge_inputs(lp):
     r[13::971] = np.inf
     r[17::89] *= -1  # negative radii collide like their magnitude (d^2 <= r*r)
     exp = O.collides_many(t, c, r)
-    assert np.array_equal(q(tree, c, r, mode=LIST[lp]), exp)
-    assert np.array_equal(q(tree, c, r, prefilter=False, mode=LIST[lp]), O.collides_many(t, c, r, False))
+    assert np.array_equal(q(tree, c, r), exp)
+    assert np.array_equal(q(tree, c, r, prefilter=False), O.collides_many(t, c, r, False))
     # check_radii: the first out-of-band index is reported (NaN is not flagged)
-    bits, bad = q(tree, c, r, check=True, mode=LIST[lp])
+    bits, bad = q(tree, c, r, check=True)
     inb = (r.astype(np.float64) >= 0.02) & (r.astype(np.float64) <= 0.08)
     flagged = ~inb & ~np.isnan(r)
     assert bad == int(np.argmax(flagged))
 
 
-@pytest.mark.parametrize("lp", ["warp", "binned"])
-def test_field_dense_gaussians(lp):
+def test_field_dense_gaussians():
     cloud = W.cfg3_cloud(n=32768, n_comp=8, seed=5)
     t = O.construct(cloud, 0.01, 0.1)
     tree = upload(t)
     check_field(tree, cloud, sample=50000)
     c, r = W.cfg3_queries(1 << 19, seed=7)
-    assert np.array_equal(q(tree, c, r, mode=LIST[lp]), O.collides_many(t, c, r))
+    assert np.array_equal(q(tree, c, r), O.collides_many(t, c, r))
 
 
-@pytest.mark.parametrize("lp", ["warp", "binned"])
-def test_field_degenerate_clouds(lp):
+def test_field_degenerate_clouds():
     # one point; a flat plane (zero z extent); duplicates; a line
     rng = np.random.default_rng(3)
     clouds = [np.array([[0.25, -0.5, 1.0]], np.float32),
               np.c_[rng.uniform(-1, 1, (3000, 2)), np.zeros(3000)].astype(np.float32),
               np.repeat(rng.uniform(0, 1, (500, 3)), 3, axis=0).astype(np.float32),
+              # 40 copies of every point: the candidate lists fill with copies
+              # of one point, so their bound certifies little and many
+              # spheres take the tree path
+              np.repeat(rng.uniform(0, 1, (100, 3)), 40, axis=0).astype(np.float32),
               np.c_[np.linspace(0, 1, 2000), np.zeros(2000), np.zeros(2000)].astype(np.float32)]
     for i, cloud in enumerate(clouds):
         t = O.construct(cloud, 0.01, 0.05)
@@ -235,8 +256,8 @@ def test_field_degenerate_clouds(lp):
         lo, hi = cloud.min(0) - 0.1, cloud.max(0) + 0.1
         c = rng.uniform(lo, hi, (100000, 3)).astype(np.float32)
         r = W.clamp_radii(rng.uniform(0.01, 0.05, 100000).astype(np.float32), 0.01, 0.05)
-        assert np.array_equal(q(tree, c, r, mode=LIST[lp]), O.collides_many(t, c, r)), i
-        assert np.array_equal(q(tree, c, r, 8, mode=LIST[lp]), O.collides_groups(t, c, r, 8)), i
+        assert np.array_equal(q(tree, c, r), O.collides_many(t, c, r)), i
+        assert np.array_equal(q(tree, c, r, 8), O.collides_groups(t, c, r, 8)), i
 
 
 def test_field_forced_mode_rejects_f64():
