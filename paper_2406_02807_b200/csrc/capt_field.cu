@@ -95,6 +95,9 @@ __device__ __forceinline__ float4 ldg_keep(const float4* p, uint64_t pol) {
 __device__ __forceinline__ float d2_fma(float dx, float dy, float dz) {
   return fmaf(dz, dz, fmaf(dy, dy, dx * dx));
 }
+// signed int16 slots of a word (candidate offsets)
+__device__ __forceinline__ int slot_lo(uint32_t w) { return int(w << 16) >> 16; }
+__device__ __forceinline__ int slot_hi(uint32_t w) { return int(w) >> 16; }
 // the reference's float64 point test (query.py:96-99): ((dx^2 + dy^2) + dz^2) <= r*r
 __device__ __forceinline__ bool hit_f64(float cx, float cy, float cz, float r, float4 p) {
   const double dx = __dsub_rn(double(cx), double(p.x)), dy = __dsub_rn(double(cy), double(p.y)),
@@ -184,6 +187,10 @@ __device__ __forceinline__ void knn_insert(float (&bd)[kKP], int (&bi)[kKP], flo
   }
 }
 
+// int16 slot j of the axis block at w[0..15] (two slots per word), as raw bits
+__device__ __forceinline__ uint32_t get_slot(const uint32_t* w, int j) {
+  return (j & 1) ? (w[j >> 1] >> 16) : (w[j >> 1] & 0xffffu);
+}
 // Set int16 slot j of the axis block at w[0..15] (two slots per word).
 __device__ __forceinline__ void put_slot(uint32_t* w, int j, int v) {
   const uint32_t u = uint32_t(v) & 0xffffu;
@@ -244,9 +251,7 @@ __global__ void __launch_bounds__(256, 1) k_field_cand(FieldGeom g, BucketGrid b
     // fp32 |x0 - p|^2 has relative error < 5u, sqrtf one more u:
     // sqrtf(d2) (1 - 2^-19) (rounded) < the real distance.  Points outside
     // the 27 buckets are farther than rcap: the bounds are capped there.
-    const float nn = fminf(g.rcap, __fmul_rn(sqrtf(bd[0]), kNNShrink));
-    const float4 w = bi[0] >= 0 ? pts[bi[0]] : make_float4(INF, INF, INF, 0.f);
-    field[cell] = make_float4(w.x, w.y, w.z, nn);
+    auto lb = [&](int k) { return fminf(g.rcap, __fmul_rn(sqrtf(bd[k]), kNNShrink)); };
     // candidates: offsets (p - x0) / q_step rounded (exact in double: the
     // difference of two floats, a power-of-two scale), |offset| <= 32767;
     // the first point that does not fit (or lies beyond rcap) ends the list
@@ -254,8 +259,7 @@ __global__ void __launch_bounds__(256, 1) k_field_cand(FieldGeom g, BucketGrid b
     uint32_t wd[kCandWords];
 #pragma unroll
     for (int i = 0; i < kCandWords; ++i) wd[i] = 0x80008000u;  // kCandNone pairs
-    float kd = fminf(g.rcap, __fmul_rn(sqrtf(bd[kKP - 1]), kNNShrink));
-    int count = 0;
+    int count = 0, drop = kKP - 1;  // (the first candidate not stored)
     bool open = true;
     const double inv = 1.0 / double(g.q_step);
 #pragma unroll
@@ -268,9 +272,8 @@ __global__ void __launch_bounds__(256, 1) k_field_cand(FieldGeom g, BucketGrid b
       const double qx = rint((double(p.x) - double(px)) * inv);
       const double qy = rint((double(p.y) - double(py)) * inv);
       const double qz = rint((double(p.z) - double(pz)) * inv);
-      const float lb = __fmul_rn(sqrtf(bd[k]), kNNShrink);
-      if (fabs(qx) > 32767.0 || fabs(qy) > 32767.0 || fabs(qz) > 32767.0 || !(lb < g.rcap)) {
-        kd = fminf(kd, lb);  // (every later candidate is at least as far)
+      if (fabs(qx) > 32767.0 || fabs(qy) > 32767.0 || fabs(qz) > 32767.0 || !(lb(k) < g.rcap)) {
+        drop = k;  // (every later candidate is at least as far)
         open = false;
         continue;
       }
@@ -279,8 +282,20 @@ __global__ void __launch_bounds__(256, 1) k_field_cand(FieldGeom g, BucketGrid b
       put_slot(wd + 32, k, int(qz));
       ++count;
     }
-    put_slot(wd, 31, int(floor(double(kd) * inv)));  // kd_q q_step <= kd
+    // kd: below the distance of the first point not stored (capped at rcap)
+    put_slot(wd, 31, int(floor(double(lb(drop)) * inv)));  // kd_q q_step <= kd
     put_slot(wd + 16, 31, count);
+    // K0's records: {nearest point w (exact), lb of the 2nd nearest} (read
+    // for every sphere) and {the 2nd and 3rd nearest as offsets, kd3_q: lb
+    // of the 4th nearest} (read for the spheres the first leaves open)
+    const float4 w = bi[0] >= 0 ? pts[bi[0]] : make_float4(INF, INF, INF, 0.f);
+    field[cell] = make_float4(w.x, w.y, w.z, lb(1));
+    const int kd3 = int(floor(double(lb(min(drop, 3))) * inv));
+    field[g.cells + cell] = make_float4(
+        __uint_as_float((get_slot(wd, 1) & 0xffffu) | (get_slot(wd + 16, 1) << 16)),
+        __uint_as_float((get_slot(wd + 32, 1) & 0xffffu) | (get_slot(wd, 2) << 16)),
+        __uint_as_float((get_slot(wd + 16, 2) & 0xffffu) | (get_slot(wd + 32, 2) << 16)),
+        __uint_as_float(uint32_t(kd3) & 0xffffu));
     uint4* dst = reinterpret_cast<uint4*>(cand + cell * kCandWords);
 #pragma unroll
     for (int i = 0; i < kCandWords / 4; ++i)
@@ -377,17 +392,73 @@ struct Ring {
   unsigned cnt;   // (warp-uniform) entries held
 };
 
-__device__ __forceinline__ void ring_flush(const FieldArgs& a, Ring& rg, unsigned k, int lane) {
+// Drain the k (<= 32) oldest ring entries, one per lane.  An entry flagged
+// (bit 31 of its index: the witness was a definite miss) first meets the
+// cell's second record -- the 2nd and 3rd nearest points of x0 as int16
+// offsets and kd3 <= the distance to every other point, read only here so
+// the hot records stay 16 B per cell -- the candidate certificate of
+// k_list_knn with three candidates: a hit sets its bit (the same warp wrote
+// the chunk's words; __syncwarp orders the two), free drops it.  The rest
+// are written to the list (coalesced, one atomic).
+__device__ __forceinline__ void ring_drain(const FieldArgs& a, Ring& rg, unsigned k, int lane) {
   __syncwarp();
-  unsigned base = 0;
-  if (lane == 0) base = atomicAdd(a.list_n, k);
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (unsigned(lane) < k) {
-    const unsigned slot = (rg.head + lane) & (kRing - 1);
-    a.list[base + lane] = rg.q[slot];
-    a.list_s[base + lane] = rg.s[slot];
+  const FieldGeom& g = a.t.fg;
+  const unsigned slot = (rg.head + lane) & (kRing - 1);
+  const bool mine = unsigned(lane) < k;
+  uint32_t q = 0u;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (mine) {
+    q = rg.q[slot];
+    s = rg.s[slot];
   }
   __syncwarp();
+  bool open = mine;
+  if (q >> 31) {
+    q &= 0x7fffffffu;
+    const int ix = __float2int_rd(__fmul_rn(__fsub_rn(s.x, g.lo[0]), g.inv_h));
+    const int iy = __float2int_rd(__fmul_rn(__fsub_rn(s.y, g.lo[1]), g.inv_h));
+    const int iz = __float2int_rd(__fmul_rn(__fsub_rn(s.z, g.lo[2]), g.inv_h));
+    const unsigned cell =
+        (unsigned(iz) * unsigned(g.ny) + unsigned(iy)) * unsigned(g.nx) + unsigned(ix);
+    const uint4 h2 = __ldg(reinterpret_cast<const uint4*>(a.t.field + g.cells + cell));
+    const float qs = g.q_step, qe = g.q_err * (1.0f + 0x1p-17f);
+    const float ex = s.x - centre_of(ix, g.h, g.c0[0]);
+    const float ey = s.y - centre_of(iy, g.h, g.c0[1]);
+    const float ez = s.z - centre_of(iz, g.h, g.c0[2]);
+    const float RH = s.w * (1.0f - 0x1p-18f) - qe;
+    const float RM = s.w * (1.0f + 0x1p-18f) + qe;
+    const float lo = RH > 0.f ? RH * RH * (1.0f - 0x1p-20f) : -1.f;
+    const float hi = RM * RM * (1.0f + 0x1p-20f);
+    const int o[6] = {slot_lo(h2.x), slot_hi(h2.x), slot_lo(h2.y),
+                      slot_hi(h2.y), slot_lo(h2.z), slot_hi(h2.z)};
+    bool hit = false, amb = false;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const float vx = fmaf(-float(o[3 * c]), qs, ex), vy = fmaf(-float(o[3 * c + 1]), qs, ey),
+                  vz = fmaf(-float(o[3 * c + 2]), qs, ez);
+      const float S = d2_fma(vx, vy, vz);
+      const bool used = o[3 * c] != kCandNone;
+      hit |= used && S <= lo;
+      amb |= used && S < hi;
+    }
+    const float A = float(slot_lo(h2.w)) * qs - s.w * kK1;
+    const bool free = !hit && !amb && A > 0.f && A * A > d2_fma(ex, ey, ez) * kK1;
+    if (hit) {
+      const uint32_t b = a.L == 1 ? q : q / uint32_t(a.L);
+      atomicOr(a.bits + (b >> 5), 1u << (b & 31));
+    }
+    open = !hit && !free;
+  }
+  const unsigned om = __ballot_sync(0xffffffffu, open);
+  if (om) {
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(a.list_n, unsigned(__popc(om)));
+    base = __shfl_sync(0xffffffffu, base, 0) + __popc(om & ((1u << lane) - 1u));
+    if (open) {
+      a.list[base] = q;
+      a.list_s[base] = s;
+    }
+  }
   rg.head = (rg.head + k) & (kRing - 1);
   rg.cnt -= k;
 }
@@ -395,7 +466,7 @@ __device__ __forceinline__ void ring_flush(const FieldArgs& a, Ring& rg, unsigne
 template <int LT>
 __device__ __forceinline__ void emit_chunk(const FieldArgs& a, int ch, int lane, bool check,
                                            unsigned hitb, unsigned undb, unsigned badb,
-                                           const float (&x)[4], const float (&y)[4],
+                                           unsigned elig, const float (&x)[4], const float (&y)[4],
                                            const float (&z)[4], const float (&r)[4], Ring& rg) {
   const int n = a.n;
   const int q0 = (ch << 7) + 4 * lane;
@@ -476,11 +547,11 @@ __device__ __forceinline__ void emit_chunk(const FieldArgs& a, int ch, int lane,
       for (int v = 0; v < 4; ++v)
         if ((lst >> v) & 1u) {
           const unsigned slot = (pos + __popc(lst & ((1u << v) - 1u))) & (kRing - 1);
-          rg.q[slot] = uint32_t(q0 + v);
+          rg.q[slot] = uint32_t(q0 + v) | (((elig >> v) & 1u) << 31);
           rg.s[slot] = make_float4(x[v], y[v], z[v], r[v]);
         }
       rg.cnt += tot;
-      if (rg.cnt >= 32u) ring_flush(a, rg, 32u, lane);
+      if (rg.cnt >= 32u) ring_drain(a, rg, 32u, lane);
     }
   }
 }
@@ -520,17 +591,23 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
                         pol);
   };
   // phase 2: the certificates of sphere v
-  unsigned hitb = 0, undb = 0, badb = 0;
-  const float band_lo = 1.0f - kTau;
+  unsigned hitb = 0, undb = 0, badb = 0, elig = 0;
+  const float band_lo = 1.0f - kTau, band_hi = 1.0f + kTau;
   auto cert = [&](int v) {
     const float ex = x[v] - centre_of(ix[v], g.h, g.c0[0]);
     const float ey = y[v] - centre_of(iy[v], g.h, g.c0[1]);
     const float ez = z[v] - centre_of(iz[v], g.h, g.c0[2]);
     const float e2 = d2_fma(ex, ey, ez);
     const float r2 = r[v] * r[v];
-    const bool hit = d2_fma(x[v] - rec[v].x, y[v] - rec[v].y, z[v] - rec[v].z) <= r2 * band_lo;
+    const float dw = d2_fma(x[v] - rec[v].x, y[v] - rec[v].y, z[v] - rec[v].z);
+    const bool hit = dw <= r2 * band_lo;
+    // free: the witness a definite miss and every other point beyond
+    // rec.w - |c - x0| > r (rec.w: lower bound of the 2nd-nearest distance)
     const float A = rec[v].w - r[v] * kK1;  // (fl(r k) >= r (1 + 15u))
-    const bool free = A > 0.f && A * A > e2 * kK1;
+    bool free = dw > r2 * band_hi && A > 0.f && A * A > e2 * kK1;
+    // the spheres the first record leaves open with the witness a definite
+    // miss meet the cell's second record when their ring is drained
+    elig |= unsigned(look[v] && !hit && !free && dw > r2 * band_hi) << v;
     hitb |= unsigned(look[v] && hit) << v;
     // decided: in-band and (outside the grid / skipped, or certified); with
     // check_radii an out-of-band (non-NaN) radius only reports first_bad
@@ -572,7 +649,7 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
 #pragma unroll
     for (int v = 0; v < 4; ++v) cert(v);
   }
-  emit_chunk<LT>(a, ch, lane, check, hitb, undb, badb, x, y, z, r, rg);
+  emit_chunk<LT>(a, ch, lane, check, hitb, undb, badb, elig, x, y, z, r, rg);
 }
 
 // K0 CTAs per SM the register allocation must allow: one chunk per warp in
@@ -611,7 +688,7 @@ __global__ void __launch_bounds__(CAPT_K0_BLOCK, CAPT_K0_MINB) k_resolve(FieldAr
     const Chunk T = load_chunk<false>(a.c, a.r, nfull, lane, n);
     resolve_chunk<kMask, LT, false>(a, g, T, nfull, lane, check, pol, rg);
   }
-  if (rg.cnt) ring_flush(a, rg, rg.cnt, lane);
+  if (rg.cnt) ring_drain(a, rg, rg.cnt, lane);
 }
 
 
@@ -639,8 +716,6 @@ __global__ void __launch_bounds__(CAPT_K0_BLOCK, CAPT_K0_MINB) k_resolve(FieldAr
 // and a half instead of a gather per candidate.  Hits set their bit; the
 // open entries (about 1e-5 of a batch, plus every sphere the grid cannot
 // take) go to a second list for part 2.
-__device__ __forceinline__ int slot_lo(uint32_t w) { return int(w << 16) >> 16; }
-__device__ __forceinline__ int slot_hi(uint32_t w) { return int(w) >> 16; }
 
 __device__ __forceinline__ void ld_v8u(const uint32_t* p, uint32_t (&v)[8]) {
   asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
@@ -942,7 +1017,7 @@ int build_field(capt_tree* tree, cudaStream_t s) {
   float4* pts = nullptr;
   CAPT_CUDA(get(&pts, std::max<uint32_t>(n_fin, 1)));
   // one allocation: K0 records | candidate records
-  const size_t off_cand = (sizeof(float4) * size_t(g.cells) + 255) & ~size_t(255);  // (32-B loads)
+  const size_t off_cand = (2 * sizeof(float4) * size_t(g.cells) + 255) & ~size_t(255);  // (32-B loads)
   const size_t bytes = off_cand + sizeof(uint32_t) * kCandWords * size_t(g.cells);
   char* mem = nullptr;
   cudaError_t e = cudaMalloc(&mem, bytes);
@@ -1160,9 +1235,9 @@ extern "C" int capt_tree_field(const capt_tree* tree, capt_field_info* info, flo
   if (!cells && !cand) return CAPT_OK;
   CAPT_CUDA(cudaSetDevice(tree->device));
   const size_t nc = size_t(g.cells);
-  std::vector<float4> rec(nc);
+  std::vector<float4> rec(2 * nc);
   std::vector<uint32_t> w(nc * kCandWords);
-  CAPT_CUDA(cudaMemcpy(rec.data(), tree->field, sizeof(float4) * nc, cudaMemcpyDeviceToHost));
+  CAPT_CUDA(cudaMemcpy(rec.data(), tree->field, 2 * sizeof(float4) * nc, cudaMemcpyDeviceToHost));
   CAPT_CUDA(cudaMemcpy(w.data(), tree->cand, sizeof(uint32_t) * w.size(), cudaMemcpyDeviceToHost));
   auto slot = [&](size_t cell, int axis, int j) {
     const uint32_t v = w[cell * kCandWords + 16 * axis + (j >> 1)];
@@ -1178,7 +1253,10 @@ extern "C" int capt_tree_field(const capt_tree* tree, capt_field_info* info, flo
       o[3] = rec[i].w;
       o[4] = float(slot(i, 0, 31)) * g.q_step;  // kd
       o[5] = float(slot(i, 1, 31));            // candidates
-      o[6] = o[7] = 0.f;
+      uint32_t kd3;
+      memcpy(&kd3, &rec[nc + i].w, 4);
+      o[6] = float(int16_t(uint16_t(kd3 & 0xffffu))) * g.q_step;  // K0's kd3
+      o[7] = 0.f;
     }
     if (cand) {  // offsets (p - x0) / q_step, kCandNone for unused slots
       for (int k = 0; k < kCand; ++k)

@@ -66,22 +66,25 @@ def check_field(tree, cloud, sample=200000, seed=0):
     nn = dk[:, 0]
     rec = cells[idx].astype(np.float64)
     rcap = np.float64(f["rcap"])
-    # certified lower bound (one fp32 ulp of slack for the centre's double rounding here)
+    # rec[3]: a certified lower bound of the 2nd-nearest distance (one fp32
+    # ulp of slack for the centre's double rounding here), tight inside rcap
     slack = 2.0 * np.spacing(np.abs(x0).max(1).astype(np.float32)).astype(np.float64)
-    assert np.all(rec[:, 3] <= nn + slack)
+    assert np.all(rec[:, 3] <= dk[:, 1] + slack)
     assert np.all(rec[:, 3] <= rcap)
-    # and tight where a witness exists: the witness is a cloud point at distance nn
+    in2 = dk[:, 1] < rcap * (1 - 1e-6)
+    assert np.allclose(rec[in2, 3], dk[in2, 1], rtol=1e-5, atol=1e-7)
+    # the witness: the nearest cloud point (+inf when none lies within rcap)
     has = np.isfinite(rec[:, 0])
-    assert np.all(rec[~has, 3] == np.float32(rcap))
     assert np.all(nn[~has] > rcap * (1 - 1e-6))
     near = nn < rcap * (1 - 1e-6)
     assert np.all(has[near])
     # (beyond rcap the witness is only the nearest point of the 27 buckets)
     dw = np.linalg.norm(x0[near] - rec[near, :3], axis=1)
     assert np.allclose(dw, nn[near], rtol=1e-5, atol=1e-7)
-    assert np.allclose(rec[near, 3], nn[near], rtol=1e-5, atol=1e-7)
     wset = {tuple(p) for p in cloud.astype(np.float32)[:, :3].tolist()}
     assert all(tuple(w) in wset for w in rec[has][:2000, :3].astype(np.float32).tolist())
+    # rec[6]: K0's bound of the 4th-nearest distance (a multiple of q_step)
+    assert np.all(rec[:, 6] <= dk[:, 3] + slack) and np.all(rec[:, 6] <= rcap)
     # candidate records: the K nearest cloud points of x0 as int16 offsets
     # (distances equal to the float64 K-nearest distances within the offset
     # rounding where those lie inside rcap), and kd a lower bound of the
