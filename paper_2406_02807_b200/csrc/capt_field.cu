@@ -79,6 +79,19 @@ __device__ __forceinline__ int cell_of(float c, float lo, float inv, int n) {
 __device__ __forceinline__ float centre_of(int i, float h, float c0) {
   return __fmaf_rn(__int2float_rn(i), h, c0);
 }
+// A query's cell along one axis: round(fma(c, inv_h, -c0 / h)), by the
+// 1.5 * 2^23 magic-number rounding (two full-rate adds instead of two
+// conversions); fi = the index as a float, for the centre fma(fi, h, c0).
+// Any cell serves the certificates (they hold for every x0 with e = c - x0
+// computed from it); the index lies in [0, n) iff c is in [lo, lo + n h) up
+// to the rounding of t -- NaN and infinite coordinates give indices outside
+// (the float bits of a non-finite or huge m are never magic + [0, n)).  K0,
+// the ring drain and the list kernels all use this one function.
+__device__ __forceinline__ int qcell(float c, float inv_h, float nc0, float& fi) {
+  const float m = fmaf(c, inv_h, nc0) + 12582912.0f;
+  fi = m - 12582912.0f;
+  return __float_as_int(m) - 0x4B400000;
+}
 // field records stay in L2 while the sphere stream passes through it
 __device__ __forceinline__ uint64_t l2_keep_policy() {
   uint64_t pol;
@@ -415,16 +428,17 @@ __device__ __forceinline__ void ring_drain(const FieldArgs& a, Ring& rg, unsigne
   bool open = mine;
   if (q >> 31) {
     q &= 0x7fffffffu;
-    const int ix = __float2int_rd(__fmul_rn(__fsub_rn(s.x, g.lo[0]), g.inv_h));
-    const int iy = __float2int_rd(__fmul_rn(__fsub_rn(s.y, g.lo[1]), g.inv_h));
-    const int iz = __float2int_rd(__fmul_rn(__fsub_rn(s.z, g.lo[2]), g.inv_h));
+    float fx, fy, fz;
+    const int ix = qcell(s.x, g.inv_h, g.nc0[0], fx);
+    const int iy = qcell(s.y, g.inv_h, g.nc0[1], fy);
+    const int iz = qcell(s.z, g.inv_h, g.nc0[2], fz);
     const unsigned cell =
         (unsigned(iz) * unsigned(g.ny) + unsigned(iy)) * unsigned(g.nx) + unsigned(ix);
     const uint4 h2 = __ldg(reinterpret_cast<const uint4*>(a.t.field + g.cells + cell));
     const float qs = g.q_step, qe = g.q_err * (1.0f + 0x1p-17f);
-    const float ex = s.x - centre_of(ix, g.h, g.c0[0]);
-    const float ey = s.y - centre_of(iy, g.h, g.c0[1]);
-    const float ez = s.z - centre_of(iz, g.h, g.c0[2]);
+    const float ex = s.x - __fmaf_rn(fx, g.h, g.c0[0]);
+    const float ey = s.y - __fmaf_rn(fy, g.h, g.c0[1]);
+    const float ez = s.z - __fmaf_rn(fz, g.h, g.c0[2]);
     const float RH = s.w * (1.0f - 0x1p-18f) - qe;
     const float RM = s.w * (1.0f + 0x1p-18f) + qe;
     const float lo = RH > 0.f ? RH * RH * (1.0f - 0x1p-20f) : -1.f;
@@ -574,14 +588,15 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
   // group already has a hit -- no record is fetched)
   bool valid[4], inband[4], look[4];
   int ix[4], iy[4], iz[4];
+  float fx[4], fy[4], fz[4];
   float4 rec[4];
   auto cell = [&](int v, bool skip) {
     valid[v] = kFull || q0 + v < n;
     if (kMask) valid[v] = valid[v] && a.mask[valid[v] ? q0 + v : 0] != 0;
     inband[v] = r[v] >= a.rlo_f && r[v] <= a.rhi_f;
-    ix[v] = __float2int_rd(__fmul_rn(__fsub_rn(x[v], g.lo[0]), g.inv_h));
-    iy[v] = __float2int_rd(__fmul_rn(__fsub_rn(y[v], g.lo[1]), g.inv_h));
-    iz[v] = __float2int_rd(__fmul_rn(__fsub_rn(z[v], g.lo[2]), g.inv_h));
+    ix[v] = qcell(x[v], g.inv_h, g.nc0[0], fx[v]);
+    iy[v] = qcell(y[v], g.inv_h, g.nc0[1], fy[v]);
+    iz[v] = qcell(z[v], g.inv_h, g.nc0[2], fz[v]);
     // (the index is used only inside the grid: no clamp)
     const bool in = unsigned(ix[v]) < nxu && unsigned(iy[v]) < nyu && unsigned(iz[v]) < nzu;
     look[v] = valid[v] && inband[v] && in && !skip;
@@ -594,9 +609,9 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
   unsigned hitb = 0, undb = 0, badb = 0, elig = 0;
   const float band_lo = 1.0f - kTau, band_hi = 1.0f + kTau;
   auto cert = [&](int v) {
-    const float ex = x[v] - centre_of(ix[v], g.h, g.c0[0]);
-    const float ey = y[v] - centre_of(iy[v], g.h, g.c0[1]);
-    const float ez = z[v] - centre_of(iz[v], g.h, g.c0[2]);
+    const float ex = x[v] - __fmaf_rn(fx[v], g.h, g.c0[0]);
+    const float ey = y[v] - __fmaf_rn(fy[v], g.h, g.c0[1]);
+    const float ez = z[v] - __fmaf_rn(fz[v], g.h, g.c0[2]);
     const float e2 = d2_fma(ex, ey, ez);
     const float r2 = r[v] * r[v];
     const float dw = d2_fma(x[v] - rec[v].x, y[v] - rec[v].y, z[v] - rec[v].z);
@@ -692,6 +707,133 @@ __global__ void __launch_bounds__(CAPT_K0_BLOCK, CAPT_K0_MINB) k_resolve(FieldAr
 }
 
 
+// K0 for single spheres (L = 1, unmasked: collides_many), the same
+// certificates with a strided lane map: lane l of a warp owns spheres
+// l, 32 + l, 64 + l, 96 + l of its 128-sphere chunk, so the verdict word of
+// spheres 32 v .. 32 v + 31 is one ballot and the list positions are ballot
+// prefix counts (the 4-consecutive-spheres map needs shuffles for both).
+// The centres are scalar loads (x, y, z of a sphere: each instruction spans
+// 3 lines of 128 B for 32 spheres; y and z hit L1 after x).
+template <bool kFull>
+__device__ __forceinline__ void resolve1(const FieldArgs& a, const FieldGeom& g, int ch, int lane,
+                                         bool check, uint64_t pol, Ring& rg) {
+  const int n = a.n;
+  const int q0 = (ch << 7) + lane;
+  float x[4], y[4], z[4], r[4];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const int q = kFull || q0 + 32 * v < n ? q0 + 32 * v : 0;
+    x[v] = __ldcs(a.c + 3 * size_t(q));
+    y[v] = __ldcs(a.c + 3 * size_t(q) + 1);
+    z[v] = __ldcs(a.c + 3 * size_t(q) + 2);
+    r[v] = __ldcs(a.r + q);
+  }
+  const unsigned nxu = unsigned(g.nx), nyu = unsigned(g.ny), nzu = unsigned(g.nz);
+  float4 rec[4];
+  float fx[4], fy[4], fz[4];
+  bool look[4], inb[4];
+  unsigned cell[4];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    inb[v] = (kFull || q0 + 32 * v < n) && r[v] >= a.rlo_f && r[v] <= a.rhi_f;
+    const int ix = qcell(x[v], g.inv_h, g.nc0[0], fx[v]);
+    const int iy = qcell(y[v], g.inv_h, g.nc0[1], fy[v]);
+    const int iz = qcell(z[v], g.inv_h, g.nc0[2], fz[v]);
+    look[v] = inb[v] && unsigned(ix) < nxu && unsigned(iy) < nyu && unsigned(iz) < nzu;
+    cell[v] = (unsigned(iz) * nyu + unsigned(iy)) * nxu + unsigned(ix);
+    rec[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (look[v]) rec[v] = ldg_keep(a.t.field + cell[v], pol);
+  }
+  const float band_lo = 1.0f - kTau, band_hi = 1.0f + kTau;
+  bool hit[4], und[4], elg[4], bad[4];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const float ex = x[v] - __fmaf_rn(fx[v], g.h, g.c0[0]);
+    const float ey = y[v] - __fmaf_rn(fy[v], g.h, g.c0[1]);
+    const float ez = z[v] - __fmaf_rn(fz[v], g.h, g.c0[2]);
+    const float r2 = r[v] * r[v];
+    const float dw = d2_fma(x[v] - rec[v].x, y[v] - rec[v].y, z[v] - rec[v].z);
+    const float A = rec[v].w - r[v] * kK1;  // (fl(r k) >= r (1 + 15u))
+    const bool h = look[v] && dw <= r2 * band_lo;
+    const bool wmiss = dw > r2 * band_hi;
+    const bool free = wmiss && A > 0.f && A * A > d2_fma(ex, ey, ez) * kK1;
+    const bool valid = kFull || q0 + 32 * v < n;
+    hit[v] = h;
+    bad[v] = check && valid && (r[v] < a.rlo_f || r[v] > a.rhi_f);
+    // undecided: in-band in-grid uncertified, or out of band (NaN, or
+    // check_radii off); out-of-band with check_radii only reports first_bad
+    und[v] = valid && !bad[v] && !(inb[v] && (!look[v] || h || free));
+    elg[v] = look[v] && !h && !free && wmiss;
+  }
+  // verdict words: word 4 ch + v = the ballot of sphere v
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const unsigned w = __ballot_sync(0xffffffffu, hit[v]);
+    if (lane == v && (kFull || (ch << 7) + 32 * v < n)) a.bits[(ch << 2) + v] = w;
+  }
+  if (check && __any_sync(0xffffffffu, bad[0] || bad[1] || bad[2] || bad[3])) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+      if (bad[v]) atomicMin(a.first_bad, static_cast<unsigned long long>(q0 + 32 * v));
+  }
+  // the list: ballot prefix counts
+  unsigned ub[4], tot = 0;
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    ub[v] = __ballot_sync(0xffffffffu, und[v]);
+    tot += __popc(ub[v]);
+  }
+  if (tot == 0) return;
+  const unsigned lt = (1u << lane) - 1u;
+  if (tot > 32u) {  // (rare: NaN or out-of-band batches) straight to the list
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(a.list_n, tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      if (und[v]) {
+        const unsigned at = base + __popc(ub[v] & lt);
+        a.list[at] = uint32_t(q0 + 32 * v);
+        a.list_s[at] = make_float4(x[v], y[v], z[v], r[v]);
+      }
+      base += __popc(ub[v]);
+    }
+    return;
+  }
+  unsigned pos = rg.head + rg.cnt;
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    if (und[v]) {
+      const unsigned slot = (pos + __popc(ub[v] & lt)) & (kRing - 1);
+      rg.q[slot] = uint32_t(q0 + 32 * v) | (unsigned(elg[v]) << 31);
+      rg.s[slot] = make_float4(x[v], y[v], z[v], r[v]);
+    }
+    pos += __popc(ub[v]);
+  }
+  rg.cnt += tot;
+  if (rg.cnt >= 32u) ring_drain(a, rg, 32u, lane);
+}
+
+__global__ void __launch_bounds__(CAPT_K0_BLOCK, CAPT_K0_MINB) k_resolve1(FieldArgs a) {
+  const FieldGeom g = a.t.fg;
+  const bool check = a.flags & CAPT_CHECK_RADII;
+  const int n = a.n;
+  const int lane = threadIdx.x & 31;
+  const int nfull = n >> 7;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t pol = l2_keep_policy();
+  __shared__ float4 s_ring[CAPT_K0_BLOCK / 32][kRing];
+  __shared__ uint32_t s_ringq[CAPT_K0_BLOCK / 32][kRing];
+  Ring rg{s_ring[threadIdx.x >> 5], s_ringq[threadIdx.x >> 5], 0u, 0u};
+  // (launched after k_field_zero with programmatic serialisation)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  for (int ch = w0; ch < nfull; ch += nwarps) resolve1<true>(a, g, ch, lane, check, pol, rg);
+  if ((n & 127) && w0 == nfull % nwarps) resolve1<false>(a, g, nfull, lane, check, pol, rg);
+  if (rg.cnt) ring_drain(a, rg, rg.cnt, lane);
+}
+
 // The list stage, part 1 (k_list_knn): every listed sphere meets its cell's
 // candidate record -- the kCand cloud points nearest x0, stored as int16
 // offsets (p - x0) / q_step, and kd_q q_step <= the distance from x0 to every
@@ -743,9 +885,10 @@ __global__ void __launch_bounds__(256) k_list_knn(FieldArgs a, uint32_t* __restr
       sph = __ldcs(a.list_s + j);
     }
     const float x = sph.x, y = sph.y, z = sph.z, r = sph.w;
-    const int ix = __float2int_rd(__fmul_rn(__fsub_rn(x, g.lo[0]), g.inv_h));
-    const int iy = __float2int_rd(__fmul_rn(__fsub_rn(y, g.lo[1]), g.inv_h));
-    const int iz = __float2int_rd(__fmul_rn(__fsub_rn(z, g.lo[2]), g.inv_h));
+    float fx, fy, fz;
+    const int ix = qcell(x, g.inv_h, g.nc0[0], fx);
+    const int iy = qcell(y, g.inv_h, g.nc0[1], fy);
+    const int iz = qcell(z, g.inv_h, g.nc0[2], fz);
     const bool cert = act && r >= a.rlo_f && r <= a.rhi_f && unsigned(ix) < unsigned(g.nx) &&
                       unsigned(iy) < unsigned(g.ny) && unsigned(iz) < unsigned(g.nz);
     bool hit = false, open = act;
@@ -761,9 +904,9 @@ __global__ void __launch_bounds__(256) k_list_knn(FieldArgs a, uint32_t* __restr
 #pragma unroll
         for (int k = 0; k < 8; ++k) w[8 * i + k] = v[k];
       }
-      const float ex = x - centre_of(ix, g.h, g.c0[0]);
-      const float ey = y - centre_of(iy, g.h, g.c0[1]);
-      const float ez = z - centre_of(iz, g.h, g.c0[2]);
+      const float ex = x - __fmaf_rn(fx, g.h, g.c0[0]);
+      const float ey = y - __fmaf_rn(fy, g.h, g.c0[1]);
+      const float ez = z - __fmaf_rn(fz, g.h, g.c0[2]);
       const float RH = r * (1.0f - 0x1p-18f) - qe;
       const float RM = r * (1.0f + 0x1p-18f) + qe;
       const float lo = RH > 0.f ? RH * RH * (1.0f - 0x1p-20f) : -1.f;
@@ -808,9 +951,9 @@ __global__ void __launch_bounds__(256) k_list_knn(FieldArgs a, uint32_t* __restr
 // short dependent chains: one warp per entry, the descent 5 levels per round
 // trip (warp_descend), the leaf's probe record (conservative fp16 AABB
 // reject, representative probe), then the set in steps of 512 rows (twelve
-// 128-bit loads in flight per lane), fp32 with the float64 re-scan of the
-// band; spheres outside the fast path (non-finite, extreme radii) take the
-// exact float64 scan.
+// 128-bit loads in flight per lane), fp32 with the rows in the error band
+// re-tested in float64 on the spot; spheres outside the fast path
+// (non-finite, extreme radii) take the exact float64 scan.
 __global__ void __launch_bounds__(256) k_tree_list(FieldArgs a) {
   const DevTree& t = a.t;
   // launched with programmatic stream serialisation: scheduled while part 1
@@ -853,7 +996,6 @@ __global__ void __launch_bounds__(256) k_tree_list(FieldArgs a) {
     if (!verdict && st == 2) {
       const float* xs = reinterpret_cast<const float*>(t.data + set.x);
       const uint32_t m4 = (set.y + 3u) & ~3u;
-      bool amb = false;
       for (uint32_t p0 = 0; p0 < m4 && !verdict; p0 += 512) {
         float4 px[4], py[4], pz[4];
 #pragma unroll
@@ -874,13 +1016,13 @@ __global__ void __launch_bounds__(256) k_tree_list(FieldArgs a) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const float d2 = d2_fma(c[0] - X[k], c[1] - Y[k], c[2] - Z[k]);
-            hit |= d2 <= loB;
-            amb |= d2 < hiB;
+            // (a row in the error band: the reference's float64 test, inline)
+            hit |= d2 <= loB ||
+                   (d2 < hiB && hit_f64(c[0], c[1], c[2], r, make_float4(X[k], Y[k], Z[k], 0.f)));
           }
         }
         verdict = __any_sync(0xffffffffu, hit);
       }
-      if (!verdict && __any_sync(0xffffffffu, amb)) st = 3;  // band: decide exactly
     }
     if (st == 3 && !verdict) {
       const double c64[3] = {double(c[0]), double(c[1]), double(c[2])};
@@ -952,6 +1094,7 @@ int build_field(capt_tree* tree, cudaStream_t s) {
   for (int d = 0; d < 3; ++d) {
     g.lo[d] = float(double(g.blo[d]) - (rmax + h));
     g.c0[d] = float(double(g.lo[d]) + 0.5 * h);
+    g.nc0[d] = float(-double(g.c0[d]) / h);
   }
   g.nx = int(dims[0]);
   g.ny = int(dims[1]);
@@ -1174,7 +1317,7 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   const bool vec = (reinterpret_cast<uintptr_t>(centers) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(radii) & 15) == 0;
   const int grid = grid_for(((n + 127) / 128) * 32, CAPT_K0_BLOCK, 8 * 256 / CAPT_K0_BLOCK);
-  if (vec && !mask && L == 1) CAPT_CUDA(launch_pdl_f(k_resolve<true, false, 1>, grid, CAPT_K0_BLOCK, s, a));
+  if (!mask && L == 1) CAPT_CUDA(launch_pdl_f(k_resolve1, grid, CAPT_K0_BLOCK, s, a));
   else if (vec && !mask && L == 8) CAPT_CUDA(launch_pdl_f(k_resolve<true, false, 8>, grid, CAPT_K0_BLOCK, s, a));
   else if (mask) CAPT_CUDA(launch_pdl_f(k_resolve<false, true, 0>, grid, CAPT_K0_BLOCK, s, a));
   else CAPT_CUDA(launch_pdl_f(k_resolve<false, false, 0>, grid, CAPT_K0_BLOCK, s, a));

@@ -67,6 +67,7 @@ struct FieldGeom {
   float lo[3];         // grid origin: cell i spans lo + [i, i+1) h (cell_of)
   float c0[3];         // centre of cell 0: x0(i) = fma(i, h, c0) exactly, build and query
   float h, inv_h;
+  float nc0[3];        // -c0 / h: a query's cell is round(fma(c, inv_h, nc0)) (qcell)
   float blo[3], bhi[3];
   float rcap;
   float q_step;        // candidate offsets from x0: int16 multiples of q_step (a power of two)
