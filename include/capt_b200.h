@@ -192,6 +192,13 @@ int capt_tree_field(const capt_tree* tree, capt_field_info* info, float* cells, 
 int capt_stage_timing(int enable);
 int capt_stage_times(double* ms, int64_t* calls);
 
+/* List lengths of the last field-pipeline capt_query issued on `stream` on
+ * the current device (measurement helper for the list stage's roofline):
+ * out[0] = spheres K0 left undecided (the candidate-record list), out[1] =
+ * entries the candidate records left open (the tree path).  Waits for the
+ * stream.  CAPT_EINVAL if no field query ran on that stream. */
+int capt_field_list_counts(void* stream, uint32_t* out);
+
 /* Number of kernels this library has launched in the process so far
  * (all devices/threads); used by bench.py to report gpu_launches. */
 int64_t capt_kernel_launches(void);

@@ -4,6 +4,7 @@
  * morton,oracle}.py in C; each function cites the lines it follows.
  * Build: oracle/Makefile (gcc -O2 -fopenmp -ffp-contract=off).
  */
+#define _GNU_SOURCE /* qsort_r */
 #include "capt_oracle.h"
 
 #include <math.h>
@@ -68,17 +69,21 @@ typedef struct {
   double* leaf_lo;  /* n*k */
   double* leaf_hi;
   int64_t ties;
-  /* sort scratch */
-  int sort_axis;
 } build_ctx;
 
-static build_ctx* g_sort_ctx; /* qsort comparator context (single-threaded) */
+typedef struct {
+  const build_ctx* c;
+  int axis;
+} sort_arg;
 
-static int cmp_coord_idx(const void* a, const void* b) {
+/* (coordinate, original index) order; qsort_r keeps it reentrant so the
+ * subtrees can be built by parallel OpenMP tasks */
+static int cmp_coord_idx(const void* a, const void* b, void* arg) {
   int32_t i = *(const int32_t*)a, j = *(const int32_t*)b;
-  const build_ctx* c = g_sort_ctx;
-  double x = c->work[(int64_t)i * c->k + c->sort_axis];
-  double y = c->work[(int64_t)j * c->k + c->sort_axis];
+  const build_ctx* c = ((const sort_arg*)arg)->c;
+  const int ax = ((const sort_arg*)arg)->axis;
+  double x = c->work[(int64_t)i * c->k + ax];
+  double y = c->work[(int64_t)j * c->k + ax];
   if (x < y) return -1;
   if (x > y) return 1;
   return (i > j) - (i < j);
@@ -155,12 +160,16 @@ static void build_rec(build_ctx* c, int32_t* idx, int64_t m, const double* clo,
   int d = depth % k;
   int64_t half = m / 2;
   /* np.argpartition(coords, half-1); ties broken by original index here */
-  c->sort_axis = d;
-  g_sort_ctx = c;
-  qsort(idx, (size_t)m, sizeof(int32_t), cmp_coord_idx);
+  sort_arg sa = {c, d};
+  qsort_r(idx, (size_t)m, sizeof(int32_t), cmp_coord_idx, &sa);
   double t = c->work[(int64_t)idx[half - 1] * k + d];
   double t_next = c->work[(int64_t)idx[half] * k + d];
-  if (t == t_next && isfinite(t)) c->ties++;
+  if (t == t_next && isfinite(t)) {
+#ifdef _OPENMP
+#pragma omp atomic
+#endif
+    c->ties++;
+  }
   c->tests[node] = (float)t;
   double lo1[KMAX], hi1[KMAX], lo2[KMAX], hi2[KMAX];
   memcpy(lo1, clo, sizeof(double) * k);
@@ -189,10 +198,26 @@ static void build_rec(build_ctx* c, int32_t* idx, int64_t m, const double* clo,
     if (c->finite[left[i]]) fin[nfl++] = left[i];
   int64_t nz2 = afforded(c, z, nz, fin, nfl, lo2, hi2, zc);
   free(fin);
-  build_rec(c, left, half, lo1, hi1, z1, nz1, 2 * node + 1, depth + 1);
-  free(z1);
+  /* the two subtrees touch disjoint idx ranges, leaves and nodes: the top
+   * levels run as parallel tasks (the result does not depend on the order) */
+#ifdef _OPENMP
+#pragma omp task if (depth < 12) firstprivate(left, half, z1, nz1, node, depth) \
+    shared(lo1, hi1)
+#endif
+  {
+    build_rec(c, left, half, lo1, hi1, z1, nz1, 2 * node + 1, depth + 1);
+    free(z1);
+  }
   build_rec(c, right, mr, lo2, hi2, zc, nz2, 2 * node + 2, depth + 1);
   free(zc);
+#ifdef _OPENMP
+#pragma omp taskwait
+#endif
+}
+
+static int cmp_i32(const void* a, const void* b) {
+  int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
+  return (x > y) - (x < y);
 }
 
 static int64_t next_pow2(int64_t n) {
@@ -236,6 +261,10 @@ oracle_tree* oracle_construct(int k, int64_t n0, const float* pts, double r_min,
   } else {
     int32_t* idx = (int32_t*)malloc(sizeof(int32_t) * n);
     for (int64_t i = 0; i < n; ++i) idx[i] = (int32_t)i;
+#ifdef _OPENMP
+#pragma omp parallel
+#pragma omp single
+#endif
     build_rec(&c, idx, n, rlo, rhi, NULL, 0, 0, 0);
     free(idx);
   }
@@ -250,23 +279,14 @@ oracle_tree* oracle_construct(int k, int64_t n0, const float* pts, double r_min,
   t->values = (float*)malloc(sizeof(float) * (size_t)(t->total * k + 1));
   t->lo = (float*)malloc(sizeof(float) * n * k);
   t->hi = (float*)malloc(sizeof(float) * n * k);
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 256)
+#endif
   for (int64_t j = 0; j < n; ++j) {
     int64_t a = t->offsets[j], m = c.set_len[j];
     int32_t* set = c.sets[j];
     /* rows 1.. in ascending original index (deterministic) */
-    if (m > 2) {
-      /* insertion-free: simple sort of ints */
-      int32_t* rest = set + 1;
-      for (int64_t i = 1; i < m - 1; ++i) {
-        int32_t v = rest[i];
-        int64_t q = i - 1;
-        while (q >= 0 && rest[q] > v) {
-          rest[q + 1] = rest[q];
-          --q;
-        }
-        rest[q + 1] = v;
-      }
-    }
+    if (m > 2) qsort(set + 1, (size_t)(m - 1), sizeof(int32_t), cmp_i32);
     for (int d = 0; d < k; ++d)
       for (int64_t i = 0; i < m; ++i)
         t->values[a * k + d * m + i] =
@@ -324,11 +344,11 @@ static inline uint32_t f32_order(float f) {
 typedef struct {
   uint32_t key[KMAX];
 } row_key;
-static int g_canon_k;
-static int cmp_row(const void* a, const void* b) {
+static int cmp_row(const void* a, const void* b, void* arg) {
   const row_key* x = (const row_key*)a;
   const row_key* y = (const row_key*)b;
-  for (int d = 0; d < g_canon_k; ++d) {
+  const int k = *(const int*)arg;
+  for (int d = 0; d < k; ++d) {
     if (x->key[d] < y->key[d]) return -1;
     if (x->key[d] > y->key[d]) return 1;
   }
@@ -337,9 +357,15 @@ static int cmp_row(const void* a, const void* b) {
 
 void oracle_canonicalize(int k, int64_t n_leaves, const int64_t* offsets,
                          float* values) {
-  g_canon_k = k;
+#ifdef _OPENMP
+#pragma omp parallel
+#endif
+  {
   row_key* rows = NULL;
   int64_t cap = 0;
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 256)
+#endif
   for (int64_t j = 0; j < n_leaves; ++j) {
     int64_t a = offsets[j], m = offsets[j + 1] - a;
     if (m <= 2) continue;
@@ -350,7 +376,7 @@ void oracle_canonicalize(int k, int64_t n_leaves, const int64_t* offsets,
     float* base = values + a * k;
     for (int64_t i = 1; i < m; ++i)
       for (int d = 0; d < k; ++d) rows[i - 1].key[d] = f32_order(base[d * m + i]);
-    qsort(rows, (size_t)(m - 1), sizeof(row_key), cmp_row);
+    qsort_r(rows, (size_t)(m - 1), sizeof(row_key), cmp_row, &k);
     for (int64_t i = 1; i < m; ++i)
       for (int d = 0; d < k; ++d) {
         uint32_t u = rows[i - 1].key[d];
@@ -361,6 +387,7 @@ void oracle_canonicalize(int k, int64_t n_leaves, const int64_t* offsets,
       }
   }
   free(rows);
+  }
 }
 
 /* ------------------------------------------------------------------ */

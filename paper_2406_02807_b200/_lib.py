@@ -85,13 +85,14 @@ def lib():
     L.capt_tree_field.argtypes = [vp, C.POINTER(CaptFieldInfo), vp, vp]
     L.capt_stage_timing.argtypes = [i32]
     L.capt_stage_times.argtypes = [C.POINTER(dbl), C.POINTER(i64)]
+    L.capt_field_list_counts.argtypes = [vp, C.POINTER(u32)]
     L.capt_kernel_launches.restype = C.c_int64
     L.capt_kernel_launches.argtypes = []
     for name in ("capt_tree_create", "capt_tree_build", "capt_tree_info_get",
                  "capt_tree_export", "capt_tree_slab", "capt_tree_from_slab", "capt_query",
                  "capt_leaf_indices", "capt_filter_cloud", "capt_measure_fp32_peak",
                  "capt_tc_selftest", "capt_nn_distances", "capt_tree_field",
-                 "capt_stage_timing", "capt_stage_times"):
+                 "capt_stage_timing", "capt_stage_times", "capt_field_list_counts"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -141,5 +142,5 @@ EXPORTED_SYMBOLS = (
     "capt_tree_info_get", "capt_tree_export", "capt_tree_destroy", "capt_tree_slab",
     "capt_tree_from_slab", "capt_query", "capt_leaf_indices", "capt_filter_cloud",
     "capt_measure_fp32_peak", "capt_kernel_launches", "capt_tc_selftest", "capt_nn_distances",
-    "capt_tree_field", "capt_stage_timing", "capt_stage_times",
+    "capt_tree_field", "capt_stage_timing", "capt_stage_times", "capt_field_list_counts",
 )

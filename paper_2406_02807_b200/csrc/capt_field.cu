@@ -1412,6 +1412,30 @@ extern "C" int capt_tree_field(const capt_tree* tree, capt_field_info* info, flo
   return CAPT_OK;
 }
 
+extern "C" int capt_field_list_counts(void* stream, uint32_t* out) {
+  if (!out) return fail(CAPT_EINVAL, "NULL argument");
+  int dev = 0;
+  CAPT_CUDA(cudaGetDevice(&dev));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ListScratch* sc = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    if (g_scratch) {
+      auto it = g_scratch->find({dev, s});
+      if (it != g_scratch->end()) sc = it->second;
+    }
+  }
+  if (!sc) return fail(CAPT_EINVAL, "no field query on this stream");
+  std::lock_guard<std::mutex> lk(sc->mu);
+  if (!sc->buf) return fail(CAPT_EINVAL, "no field query on this stream");
+  uint32_t h[2] = {0, 0};
+  CAPT_CUDA(cudaMemcpyAsync(h, sc->buf, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CAPT_CUDA(cudaStreamSynchronize(s));
+  out[0] = h[0];
+  out[1] = h[1];
+  return CAPT_OK;
+}
+
 extern "C" int capt_stage_timing(int enable) {
   int dev = 0;
   CAPT_CUDA(cudaGetDevice(&dev));

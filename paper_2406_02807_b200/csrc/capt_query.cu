@@ -492,6 +492,122 @@ int launch_direct(const DevTree& t, const void* centers, const void* radii, int6
   return CAPT_OK;
 }
 
+// ---------------------------------------------------------------------------
+// float64 inputs on the clearance-field pipeline.  Reference callers pass
+// float64 arrays (query.py:192-193); when a sphere's four values are fp32
+// values, the fp32 kernels see exactly the reference's inputs.  k_split_f64
+// converts every sphere, marks the exact ones valid for the field pipeline
+// (which then skips the others as masked lanes) and lists the inexact ones;
+// k_list_f64 answers the listed spheres with the reference's float64
+// arithmetic (band check, descent, AABB prefilter, set scan) and ORs their
+// verdicts into the words the field pipeline wrote.  A group's bit is the OR
+// of its valid lanes' verdicts either way (query.py:126-167).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock) k_split_f64(const double* __restrict__ c,
+                                                      const double* __restrict__ r, int64_t n,
+                                                      const uint8_t* __restrict__ umask,
+                                                      float* __restrict__ c32,
+                                                      float* __restrict__ r32,
+                                                      uint8_t* __restrict__ m32,
+                                                      uint32_t* __restrict__ list,
+                                                      uint32_t* __restrict__ list_n) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t q0 = int64_t(blockIdx.x) * blockDim.x; q0 < n; q0 += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t q = q0 + threadIdx.x;
+    bool inexact = false;
+    if (q < n) {
+      const double v[4] = {__ldcs(c + 3 * q), __ldcs(c + 3 * q + 1), __ldcs(c + 3 * q + 2),
+                           __ldcs(r + q)};
+      bool exact = true;
+#pragma unroll
+      for (int d = 0; d < 4; ++d) {
+        const float f = __double2float_rn(v[d]);
+        exact &= double(f) == v[d] || (isnan(v[d]) && isnan(f));
+        if (d < 3) c32[3 * q + d] = f; else r32[q] = f;
+      }
+      const bool valid = !umask || umask[q];
+      m32[q] = uint8_t(valid && exact);
+      inexact = valid && !exact;
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, inexact);
+    if (b) {
+      unsigned base = 0;
+      if (lane == 0) base = atomicAdd(list_n, unsigned(__popc(b)));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (inexact) list[base + __popc(b & ((1u << lane) - 1u))] = uint32_t(q);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_list_f64(DevTree t, const double* __restrict__ c,
+                                                     const double* __restrict__ r, int L,
+                                                     uint32_t flags,
+                                                     const uint32_t* __restrict__ list,
+                                                     const uint32_t* __restrict__ list_n,
+                                                     uint32_t* __restrict__ bits,
+                                                     unsigned long long* __restrict__ first_bad) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const bool prefilter = flags & CAPT_PREFILTER;
+  const bool check = flags & CAPT_CHECK_RADII;
+  const uint32_t m = *list_n;
+  for (uint32_t e = warp; e < m; e += nwarps) {
+    const uint32_t q = list[e];
+    const uint32_t g = q / uint32_t(L);
+    double c64[3], r64;
+    SphereIn<double>::load(c, r, q, 3, c64, r64);
+    // (query.py:194-197: a NaN radius is not flagged)
+    if (check && lane == 0 && (r64 < t.r_min || r64 > t.r_max))
+      atomicMin(first_bad, static_cast<unsigned long long>(q));
+    if (L > 1 && ((__ldcg(bits + (g >> 5)) >> (g & 31)) & 1u)) continue;
+    const int64_t leaf = warp_descend<double>(t, c64, lane);
+    const uint2 set = __ldg(t.set + leaf);
+    float cx, cy, cz, r2, loB, hiB;
+    const int status = classify(t, leaf, c64, r64, prefilter, cx, cy, cz, r2, loB, hiB);
+    if (status == ST_FALSE) continue;
+    int v = 2;
+    if (status == ST_SCAN) v = warp_scan_f32(t, set, cx, cy, cz, loB, hiB, lane);
+    const bool verdict = (v == 1) || (v == 2 && warp_scan_f64(t, set, c64, r64, lane));
+    if (verdict && lane == 0) atomicOr(bits + (g >> 5), 1u << (g & 31));
+  }
+}
+
+static int launch_field_f64(const DevTree& t, const void* d_c, const void* d_r, int64_t n, int L,
+                            const uint8_t* d_m, uint32_t fl, uint32_t* d_bits, int64_t n_words,
+                            unsigned long long* d_bad, cudaStream_t s) {
+  struct Scratch {
+    cudaStream_t s;
+    char* p = nullptr;
+    ~Scratch() {
+      if (p) cudaFreeAsync(p, s);
+    }
+  } sc{s};
+  const size_t nn = size_t(n);
+  const size_t off_r = 12 * nn, off_m = 16 * nn, off_l = (17 * nn + 15) & ~size_t(15);
+  CAPT_CUDA(dmalloc(&sc.p, off_l + 4 * nn + 16, s));
+  float* c32 = reinterpret_cast<float*>(sc.p);
+  float* r32 = reinterpret_cast<float*>(sc.p + off_r);
+  uint8_t* m32 = reinterpret_cast<uint8_t*>(sc.p + off_m);
+  uint32_t* list_n = reinterpret_cast<uint32_t*>(sc.p + off_l);
+  uint32_t* list = list_n + 4;
+  CAPT_CUDA(cudaMemsetAsync(list_n, 0, 4, s));
+  k_split_f64<<<grid_for(n, kBlock, 8), kBlock, 0, s>>>(static_cast<const double*>(d_c),
+                                                        static_cast<const double*>(d_r), n, d_m,
+                                                        c32, r32, m32, list, list_n);
+  CAPT_CUDA(cudaGetLastError());
+  note_launches(1);
+  const int rc = launch_field(t, c32, r32, n, L, m32, fl & ~uint32_t(CAPT_INPUT_F64), d_bits,
+                              n_words, d_bad, s);
+  if (rc) return rc;
+  k_list_f64<<<grid_for(int64_t(n) * 32, kBlock, 4), kBlock, 0, s>>>(
+      t, static_cast<const double*>(d_c), static_cast<const double*>(d_r), L, fl, list, list_n,
+      d_bits, d_bad);
+  CAPT_CUDA(cudaGetLastError());
+  note_launches(1);
+  return CAPT_OK;
+}
+
 // One query over device buffers on stream s (direct or binned pipeline).
 int query_device(const DevTree& t, const void* d_c, const void* d_r, int64_t n, int L,
                  const uint8_t* d_m, uint32_t flags, uint32_t* d_bits,
@@ -505,6 +621,8 @@ int query_device(const DevTree& t, const void* d_c, const void* d_r, int64_t n, 
   if (!d_bad) fl &= ~CAPT_CHECK_RADII;
   if (field_eligible(t, n, fl))
     return launch_field(t, d_c, d_r, n, L, d_m, fl, d_bits, n_words, d_bad, s);
+  if ((fl & CAPT_INPUT_F64) && field_eligible(t, n, fl & ~uint32_t(CAPT_INPUT_F64)))
+    return launch_field_f64(t, d_c, d_r, n, L, d_m, fl, d_bits, n_words, d_bad, s);
   if (fl & CAPT_MODE_FIELD)
     return fail(CAPT_EINVAL, "clearance-field pipeline unavailable for this tree/input");
   return binned_preferred(t, n, fl)

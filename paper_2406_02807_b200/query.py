@@ -87,23 +87,15 @@ class QueryOutcome:
 # low-level calls
 # ---------------------------------------------------------------------------
 
-def _fp32_exact(a: np.ndarray) -> bool:
-    """True when every value of a float64 array is an fp32 value (NaN kept):
-    the fp32 kernels then see exactly the reference's float64 inputs."""
-    with np.errstate(over="ignore", invalid="ignore"):
-        return bool(np.array_equal(a.astype(np.float32).astype(np.float64), a, equal_nan=True))
-
-
 def _host_inputs(tree: Capt, centers, radii):
+    """Contiguous host arrays for a CAPT_HOST_IO call: fp32 pairs as they
+    are; anything else as float64 (the reference converts with
+    np.asarray(float64), query.py:192-193).  Float64 batches go to the
+    device unchanged: capt_query sends every sphere whose values are fp32
+    values through the fp32 kernels (bit-identical) and the rest through
+    the float64 path, on the device."""
     c = np.asarray(centers)
     r = np.asarray(radii)
-    if c.dtype != np.float32 or r.dtype != np.float32:
-        # reference callers pass float64 (query.py:192-193); fp32-exact values
-        # take the fp32 kernels (the clearance-field pipeline), bit-identically
-        c64 = np.asarray(c, dtype=np.float64)
-        r64 = np.asarray(r, dtype=np.float64)
-        if c64.size + r64.size and _fp32_exact(c64) and _fp32_exact(r64):
-            c, r = c64.astype(np.float32), r64.astype(np.float32)
     if c.dtype == np.float32 and r.dtype == np.float32:
         c = np.ascontiguousarray(c)
         r = np.ascontiguousarray(r)

@@ -280,8 +280,38 @@ def make_dispersion():
         out[f"{name}/nn"] = nn
     np.savez_compressed(os.path.join(HERE, "dispersion.npz"), **out)
 
+
+def make_capt_files():
+    """.capt dumps written by the reference's own save_capt (tree.py:276-288):
+    a 3-D tree with padding leaves, the r_min shortcut and duplicates, and a
+    k = 2 tree, plus queries and the reference's masks on the loaded trees."""
+    from captree.tree import load_capt, save_capt
+    rng = np.random.default_rng(4321)
+    pts3 = np.concatenate([rng.uniform(-1, 1, (700, 3)),
+                           np.repeat(rng.uniform(0, 0.2, (20, 3)), 3, axis=0)]).astype(np.float32)
+    pts2 = rng.normal(0, 0.3, (300, 2)).astype(np.float32)
+    out = {}
+    for name, pts, band in (("ref3d", pts3, (0.02, 0.15)), ("ref2d", pts2, (0.01, 0.1))):
+        tree = construct(PointCloud(pts), BuildParams(*band))
+        path = os.path.join(HERE, f"{name}.capt")
+        save_capt(tree, path)
+        back = load_capt(path)  # (r_min / r_max come back as fp32 values)
+        k = pts.shape[1]
+        c = rng.uniform(pts.min(0) - 0.2, pts.max(0) + 0.2, (4096, k))
+        r = rng.uniform(back.r_min, back.r_max, 4096)
+        r = np.clip(r, np.nextafter(np.float32(back.r_min), np.float32(1)), back.r_max)
+        out[f"{name}/centers"] = c
+        out[f"{name}/radii"] = r
+        out[f"{name}/mask"] = np.packbits(collides_many(back, c, r))
+    np.savez_compressed(os.path.join(HERE, "capt_files.npz"), **out)
+
+
 if __name__ == "__main__":
     print("reference", captree.__version__, "numpy", np.__version__)
+    if len(sys.argv) > 1:  # regenerate only the named fixtures, e.g. capt_files
+        for name in sys.argv[1:]:
+            globals()[f"make_{name}"]()
+        sys.exit(0)
     make_hand_cases()
     make_trees()
     make_queries()
@@ -289,3 +319,4 @@ if __name__ == "__main__":
     make_cfg0_slice()
     make_trace()
     make_dispersion()
+    make_capt_files()

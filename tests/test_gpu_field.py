@@ -263,12 +263,35 @@ def test_field_degenerate_clouds():
         assert np.array_equal(q(tree, c, r, 8), O.collides_groups(t, c, r, 8)), i
 
 
-def test_field_forced_mode_rejects_f64():
-    z = load_golden("cfg0.npz")
-    tree = upload(golden_tree(z, ""))
-    c, r = W.cfg0_queries(1024)
-    with pytest.raises(ValueError, match="clearance-field"):
-        q(tree, c.astype(np.float64) + 1e-12, r.astype(np.float64))
+@pytest.mark.parametrize("L", [1, 8])
+def test_field_f64_inputs_split_on_device(L):
+    # float64 batches: the spheres whose values are fp32 values take the
+    # field pipeline, the others (perturbed centres or radii, huge values)
+    # the float64 path, on the device; masks and the first out-of-band
+    # index (an inexact radius) come out as the reference's
+    cloud = W.cfg1_cloud()
+    t = O.construct(cloud, 0.02, 0.08)
+    tree = upload(t)
+    c, r = W.cfg1_queries(cloud, n_groups=1 << 15, seed=41)
+    c64, r64 = c.astype(np.float64), r.astype(np.float64)
+    rng = np.random.default_rng(42)
+    n = len(r)
+    pick = rng.choice(n, n // 10, replace=False)
+    c64[pick[: len(pick) // 2], 1] += 1e-9
+    r64[pick[len(pick) // 2:]] *= 1 + 1e-12
+    c64[pick[:50], 0] = 1e300
+    mask = (rng.uniform(size=n) > 0.1).astype(np.uint8)
+    for m in (None, mask):
+        exp = (O.collides_many(t, c64, r64) if L == 1 and m is None else
+               O.collides_groups(t, c64, r64, L, None if m is None else m.astype(bool)))
+        assert np.array_equal(q(tree, c64, r64, L, m), exp)
+        assert np.array_equal(q(tree, c64, r64, L, m, mode=0), exp)
+    # check_radii: an inexact out-of-band radius is the first bad index
+    r_bad = r64.copy()
+    r_bad[777] = 0.08 + 1e-12
+    r_bad[5000] = 0.5
+    bits, bad = q(tree, c64, r_bad, L, check=True, mode=0)
+    assert bad == 777
 
 
 def test_stage_timing_abi():
