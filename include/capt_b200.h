@@ -183,6 +183,15 @@ typedef struct {
 } capt_field_info;
 int capt_tree_field(const capt_tree* tree, capt_field_info* info, float* cells, float* cand);
 
+/* The clearance field's block table (K0 keeps it in shared memory): blocks
+ * of 2^shift cells per axis, dims[0..2] = blocks along x, y, z, block
+ * (bx,by,bz) is entry (bz*dims[1] + by)*dims[0] + bx.  Entry q certifies
+ * q * step <= the distance from the cloud to every centre whose computed
+ * cell lies in the block.  dims: 4 ints {bx, by, bz, shift}; step: 1 float;
+ * table: NULL or a host buffer of bx*by*bz bytes.  CAPT_EINVAL for trees
+ * without a field. */
+int capt_tree_field_blocks(const capt_tree* tree, int32_t* dims, float* step, uint8_t* table);
+
 /* Stage timing of the clearance-field pipeline (measurement helper for
  * bench.py's roofline): while enabled, every field-pipeline capt_query
  * records CUDA events on its stream around the resolve kernel (K0) and the

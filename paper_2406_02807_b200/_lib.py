@@ -64,6 +64,20 @@ def lib():
             if not os.path.exists(LIB_PATH):
                 raise RuntimeError(f"libcapt_b200.so is not built and building failed: {exc}")
     L = C.CDLL(os.path.join(HERE, VARIANT) if VARIANT else LIB_PATH)
+    if VARIANT:  # an experiment build may predate an entry point: bind what it has
+        class _Tolerant:
+            def __init__(self, lib):
+                object.__setattr__(self, "_l", lib)
+
+            def __getattr__(self, name):
+                try:
+                    return getattr(self._l, name)
+                except AttributeError:
+                    return C.CFUNCTYPE(C.c_int)(lambda *a: CAPT_EINVAL)
+
+            def __setattr__(self, name, value):
+                setattr(self._l, name, value)
+        L = _Tolerant(L)
     vp, i64, i32, u32, dbl = C.c_void_p, C.c_int64, C.c_int, C.c_uint32, C.c_double
     L.capt_last_error.restype = C.c_char_p
     L.capt_version.restype = C.c_int
@@ -86,13 +100,15 @@ def lib():
     L.capt_stage_timing.argtypes = [i32]
     L.capt_stage_times.argtypes = [C.POINTER(dbl), C.POINTER(i64)]
     L.capt_field_list_counts.argtypes = [vp, C.POINTER(u32)]
+    L.capt_tree_field_blocks.argtypes = [vp, vp, vp, vp]
     L.capt_kernel_launches.restype = C.c_int64
     L.capt_kernel_launches.argtypes = []
     for name in ("capt_tree_create", "capt_tree_build", "capt_tree_info_get",
                  "capt_tree_export", "capt_tree_slab", "capt_tree_from_slab", "capt_query",
                  "capt_leaf_indices", "capt_filter_cloud", "capt_measure_fp32_peak",
                  "capt_tc_selftest", "capt_nn_distances", "capt_tree_field",
-                 "capt_stage_timing", "capt_stage_times", "capt_field_list_counts"):
+                 "capt_stage_timing", "capt_stage_times", "capt_field_list_counts",
+                 "capt_tree_field_blocks"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -143,4 +159,5 @@ EXPORTED_SYMBOLS = (
     "capt_tree_from_slab", "capt_query", "capt_leaf_indices", "capt_filter_cloud",
     "capt_measure_fp32_peak", "capt_kernel_launches", "capt_tc_selftest", "capt_nn_distances",
     "capt_tree_field", "capt_stage_timing", "capt_stage_times", "capt_field_list_counts",
+    "capt_tree_field_blocks",
 )

@@ -44,6 +44,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -56,6 +57,9 @@ namespace capt {
 
 #ifndef CAPT_FIELD_CELLS
 #define CAPT_FIELD_CELLS (1 << 21)  // 32 MB of K0 records: L2-resident
+#endif
+#ifndef CAPT_BLK_BYTES
+#define CAPT_BLK_BYTES 8192  // block table bound (K0 shared memory per CTA)
 #endif
 
 namespace {
@@ -92,6 +96,38 @@ __device__ __forceinline__ int qcell(float c, float inv_h, float nc0, float& fi)
   fi = m - 12582912.0f;
   return __float_as_int(m) - 0x4B400000;
 }
+// The block table's certificate for a centre in the grid (computed cell
+// ix, iy, iz): every cloud point is farther than bound >= rk = fl(r (1 +
+// 2^-20)) > r (1 + 15u), so every float64 d^2 exceeds r*r (the K0 free
+// argument with the block's bound in place of nn - |c - x0|).
+#ifndef CAPT_K0_BLOCKS
+#define CAPT_K0_BLOCKS 1
+#endif
+#ifndef CAPT_K0_GROUP_BLOCKS  // the table in the lane-group K0 (k_resolve) too
+#define CAPT_K0_GROUP_BLOCKS 0
+#endif
+__device__ __forceinline__ bool block_free(const FieldGeom& g, const uint8_t* sblk, int ix, int iy,
+                                           int iz, bool in, float rk) {
+  if (!CAPT_K0_BLOCKS) return false;
+  const unsigned bs = unsigned(g.bshift);
+  const unsigned bi = ((unsigned(iz) >> bs) * unsigned(g.by) + (unsigned(iy) >> bs)) *
+                          unsigned(g.bx) + (unsigned(ix) >> bs);
+  const float q = float(sblk[in ? bi : 0u]);
+  return in && q * g.bstep > rk;
+}
+// K0's CTAs copy the block table into shared memory (tree data: before the
+// programmatic-dependency wait); a static array, so its address is a
+// compile-time shared-window offset
+__device__ __forceinline__ const uint8_t* stage_block_table(const FieldGeom& g,
+                                                            const uint8_t* blk) {
+  __shared__ uint4 s_blk4[(CAPT_BLK_BYTES + 15) / 16];
+  const uint4* src = reinterpret_cast<const uint4*>(blk);
+  if (CAPT_K0_BLOCKS)
+    for (int i = threadIdx.x; i < (g.bbytes >> 4); i += blockDim.x) s_blk4[i] = __ldg(src + i);
+  __syncthreads();
+  return reinterpret_cast<const uint8_t*>(s_blk4);
+}
+
 // field records stay in L2 while the sphere stream passes through it
 __device__ __forceinline__ uint64_t l2_keep_policy() {
   uint64_t pol;
@@ -313,6 +349,44 @@ __global__ void __launch_bounds__(256, 1) k_field_cand(FieldGeom g, BucketGrid b
 #pragma unroll
     for (int i = 0; i < kCandWords / 4; ++i)
       dst[i] = make_uint4(wd[4 * i], wd[4 * i + 1], wd[4 * i + 2], wd[4 * i + 3]);
+  }
+}
+
+// Block table (FieldGeom::bshift ...): one warp per block of 2^bshift cells
+// per axis.  For every centre c whose computed cell (qcell) lies in the
+// block, dist(c, cloud) >= lb0(x0) - |c - x0| >= min over the block's cells
+// of lb0 - rcell, where lb0 = the certified lower bound of the distance from
+// the cell centre x0 to its nearest cloud point (the witness, the same fp32
+// expression k_field_cand ranks with; rcap when no point lies within rcap)
+// and rcell >= |c - x0| (the host bounds the cell computation's rounding).
+// Stored as floor(bound / bstep), bstep a power of two, saturated at 255;
+// rounded down at every step.
+__global__ void __launch_bounds__(256) k_block_table(FieldGeom g, const float4* __restrict__ field,
+                                                     float rcell, uint8_t* __restrict__ blk) {
+  const int lane = threadIdx.x & 31;
+  const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nb = g.bx * g.by * g.bz;
+  if (b >= nb) return;
+  const int B = 1 << g.bshift;
+  const int bxi = b % g.bx, byi = (b / g.bx) % g.by, bzi = b / (g.bx * g.by);
+  const int x0 = bxi * B, y0 = byi * B, z0 = bzi * B;
+  const int cx = min(B, g.nx - x0), cy = min(B, g.ny - y0), cz = min(B, g.nz - z0);
+  float mn = g.rcap;
+  for (int j = lane; j < cx * cy * cz; j += 32) {
+    const int ix = x0 + j % cx, iy = y0 + (j / cx) % cy, iz = z0 + j / (cx * cy);
+    const float4 w = field[(int64_t(iz) * g.ny + iy) * g.nx + ix];
+    if (!isfinite(w.x)) continue;  // no point within rcap: lb0 = rcap
+    const float px = centre_of(ix, g.h, g.c0[0]), py = centre_of(iy, g.h, g.c0[1]),
+                pz = centre_of(iz, g.h, g.c0[2]);
+    const float d2 = d2_fma(w.x - px, w.y - py, w.z - pz);
+    mn = fminf(mn, fminf(g.rcap, __fmul_rn(sqrtf(d2), kNNShrink)));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  if (lane == 0) {
+    const float d = __fsub_rd(mn, rcell);
+    const float q = d > 0.f ? floorf(__fdiv_rd(d, g.bstep)) : 0.f;
+    blk[b] = uint8_t(fminf(q, 255.f));
   }
 }
 
@@ -575,8 +649,8 @@ __device__ __forceinline__ void emit_chunk(const FieldArgs& a, int ch, int lane,
 // unmasked chunk (no per-sphere validity test).
 template <bool kMask, int LT, bool kFull>
 __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeom& g,
-                                              const Chunk& k, int ch, int lane, bool check,
-                                              uint64_t pol, Ring& rg) {
+                                              const uint8_t* sblk, const Chunk& k, int ch,
+                                              int lane, bool check, uint64_t pol, Ring& rg) {
   const float x[4] = {k.p0.x, k.p0.w, k.p1.z, k.p2.y};
   const float y[4] = {k.p0.y, k.p1.x, k.p1.w, k.p2.z};
   const float z[4] = {k.p0.z, k.p1.y, k.p2.x, k.p2.w};
@@ -599,7 +673,18 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
     iz[v] = qcell(z[v], g.inv_h, g.nc0[2], fz[v]);
     // (the index is used only inside the grid: no clamp)
     const bool in = unsigned(ix[v]) < nxu && unsigned(iy[v]) < nyu && unsigned(iz[v]) < nzu;
-    look[v] = valid[v] && inband[v] && in && !skip;
+    const bool bfree = CAPT_K0_GROUP_BLOCKS && block_free(g, sblk, ix[v], iy[v], iz[v], in, r[v] * kK1);
+    look[v] = valid[v] && inband[v] && in && !skip && !bfree;
+#ifdef CAPT_FIELD_STATS
+    {
+      const unsigned lk = __ballot_sync(0xffffffffu, look[v]);
+      const unsigned bf = __ballot_sync(0xffffffffu, valid[v] && inband[v] && !skip && bfree);
+      if ((threadIdx.x & 31) == 0) {
+        atomicAdd(a.list_n + 2, unsigned(__popc(lk)));
+        atomicAdd(a.list_n + 3, unsigned(__popc(bf)));
+      }
+    }
+#endif
     rec[v] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (look[v])
       rec[v] = ldg_keep(a.t.field + ((unsigned(iz[v]) * nyu + unsigned(iy[v])) * nxu + unsigned(ix[v])),
@@ -692,16 +777,17 @@ __global__ void __launch_bounds__(CAPT_K0_BLOCK, CAPT_K0_MINB) k_resolve(FieldAr
   __shared__ float4 s_ring[CAPT_K0_BLOCK / 32][kRing];
   __shared__ uint32_t s_ringq[CAPT_K0_BLOCK / 32][kRing];
   Ring rg{s_ring[threadIdx.x >> 5], s_ringq[threadIdx.x >> 5], 0u, 0u};
+  const uint8_t* sblk = stage_block_table(g, a.t.blk);
   // (launched after k_field_zero with programmatic serialisation)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int ch = w0; ch < nfull; ch += nwarps) {
     const Chunk A = load_chunk<kVec, true>(a.c, a.r, ch, lane, n);
-    resolve_chunk<kMask, LT, !kMask>(a, g, A, ch, lane, check, pol, rg);
+    resolve_chunk<kMask, LT, !kMask>(a, g, sblk, A, ch, lane, check, pol, rg);
   }
   if ((n & 127) && w0 == nfull % nwarps) {
     const Chunk T = load_chunk<false>(a.c, a.r, nfull, lane, n);
-    resolve_chunk<kMask, LT, false>(a, g, T, nfull, lane, check, pol, rg);
+    resolve_chunk<kMask, LT, false>(a, g, sblk, T, nfull, lane, check, pol, rg);
   }
   if (rg.cnt) ring_drain(a, rg, rg.cnt, lane);
 }
@@ -711,12 +797,18 @@ __global__ void __launch_bounds__(CAPT_K0_BLOCK, CAPT_K0_MINB) k_resolve(FieldAr
 // certificates with a strided lane map: lane l of a warp owns spheres
 // l, 32 + l, 64 + l, 96 + l of its 128-sphere chunk, so the verdict word of
 // spheres 32 v .. 32 v + 31 is one ballot and the list positions are ballot
-// prefix counts (the 4-consecutive-spheres map needs shuffles for both).
-// The centres are scalar loads (x, y, z of a sphere: each instruction spans
-// 3 lines of 128 B for 32 spheres; y and z hit L1 after x).
+// prefix counts.  Built for a short instruction stream and few live
+// registers: phase 1 computes each sphere's cell, |c - x0|^2 and the block
+// table's certificate and issues the 4 record loads (a sphere without a
+// record gets {+inf, .., +inf}: its witness and Lipschitz tests then read
+// "free", and only the `skip` bit keeps out-of-grid spheres decided without
+// them); phase 2 consumes the records.  The centres are scalar loads (x, y,
+// z of a sphere: each instruction spans 3 lines of 128 B for 32 spheres; y
+// and z hit L1 after x).
 template <bool kFull>
-__device__ __forceinline__ void resolve1(const FieldArgs& a, const FieldGeom& g, int ch, int lane,
-                                         bool check, uint64_t pol, Ring& rg) {
+__device__ __forceinline__ void resolve1(const FieldArgs& a, const FieldGeom& g,
+                                         const uint8_t* sblk, int ch, int lane, bool check,
+                                         uint64_t pol, Ring& rg) {
   const int n = a.n;
   const int q0 = (ch << 7) + lane;
   float x[4], y[4], z[4], r[4];
@@ -728,62 +820,83 @@ __device__ __forceinline__ void resolve1(const FieldArgs& a, const FieldGeom& g,
     z[v] = __ldcs(a.c + 3 * size_t(q) + 2);
     r[v] = __ldcs(a.r + q);
   }
-  const unsigned nxu = unsigned(g.nx), nyu = unsigned(g.ny), nzu = unsigned(g.nz);
+  const float INF = __int_as_float(0x7f800000);
+  const unsigned bs = unsigned(g.bshift);
   float4 rec[4];
-  float fx[4], fy[4], fz[4];
-  bool look[4], inb[4];
-  unsigned cell[4];
+  float e2[4];
+  unsigned inbm = 0u, lookm = 0u;
 #pragma unroll
   for (int v = 0; v < 4; ++v) {
-    inb[v] = (kFull || q0 + 32 * v < n) && r[v] >= a.rlo_f && r[v] <= a.rhi_f;
-    const int ix = qcell(x[v], g.inv_h, g.nc0[0], fx[v]);
-    const int iy = qcell(y[v], g.inv_h, g.nc0[1], fy[v]);
-    const int iz = qcell(z[v], g.inv_h, g.nc0[2], fz[v]);
-    look[v] = inb[v] && unsigned(ix) < nxu && unsigned(iy) < nyu && unsigned(iz) < nzu;
-    cell[v] = (unsigned(iz) * nyu + unsigned(iy)) * nxu + unsigned(ix);
-    rec[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (look[v]) rec[v] = ldg_keep(a.t.field + cell[v], pol);
+    const bool valid = kFull || q0 + 32 * v < n;
+    const bool inb = valid && r[v] >= a.rlo_f && r[v] <= a.rhi_f;
+    float fx, fy, fz;
+    const int ix = qcell(x[v], g.inv_h, g.nc0[0], fx);
+    const int iy = qcell(y[v], g.inv_h, g.nc0[1], fy);
+    const int iz = qcell(z[v], g.inv_h, g.nc0[2], fz);
+    e2[v] = d2_fma(x[v] - __fmaf_rn(fx, g.h, g.c0[0]), y[v] - __fmaf_rn(fy, g.h, g.c0[1]),
+                   z[v] - __fmaf_rn(fz, g.h, g.c0[2]));
+    const bool in = unsigned(ix) < unsigned(g.nx) && unsigned(iy) < unsigned(g.ny) &&
+                    unsigned(iz) < unsigned(g.nz);
+    // the block table's certificate (block_free), branch-free: every lane
+    // reads an entry (entry 0 outside the grid)
+    const unsigned bi = ((unsigned(iz) >> bs) * unsigned(g.by) + (unsigned(iy) >> bs)) *
+                            unsigned(g.bx) + (unsigned(ix) >> bs);
+    const float bq = float(sblk[in ? bi : 0u]) * g.bstep;
+    const bool look = inb && in && !(CAPT_K0_BLOCKS && bq > r[v] * kK1);
+    const unsigned cell = (unsigned(iz) * unsigned(g.ny) + unsigned(iy)) * unsigned(g.nx) +
+                          unsigned(ix);
+    // no record: +inf (a witness miss); the sphere is decided by `look`
+    rec[v] = make_float4(INF, INF, INF, INF);
+    if (look) rec[v] = ldg_keep(a.t.field + cell, pol);
+    inbm |= unsigned(inb) << v;
+    lookm |= unsigned(look) << v;
+#ifdef CAPT_FIELD_STATS
+    {
+      const unsigned lk = __ballot_sync(0xffffffffu, look);
+      if (lane == 0) atomicAdd(a.list_n + 2, unsigned(__popc(lk)));
+    }
+#endif
   }
-  const float band_lo = 1.0f - kTau, band_hi = 1.0f + kTau;
-  bool hit[4], und[4], elg[4], bad[4];
+  unsigned ub[4], wd[4], elgm = 0u, badm = 0u;
 #pragma unroll
   for (int v = 0; v < 4; ++v) {
-    const float ex = x[v] - __fmaf_rn(fx[v], g.h, g.c0[0]);
-    const float ey = y[v] - __fmaf_rn(fy[v], g.h, g.c0[1]);
-    const float ez = z[v] - __fmaf_rn(fz[v], g.h, g.c0[2]);
     const float r2 = r[v] * r[v];
     const float dw = d2_fma(x[v] - rec[v].x, y[v] - rec[v].y, z[v] - rec[v].z);
-    const float A = rec[v].w - r[v] * kK1;  // (fl(r k) >= r (1 + 15u))
-    const bool h = look[v] && dw <= r2 * band_lo;
-    const bool wmiss = dw > r2 * band_hi;
-    const bool free = wmiss && A > 0.f && A * A > d2_fma(ex, ey, ez) * kK1;
+    const float A = __fmaf_rn(-r[v], kK1, rec[v].w);  // (<= rec.w - fl(r k))
+    const bool wmiss = dw > r2 * (1.0f + kTau);
+    const bool hit = dw <= r2 * (1.0f - kTau);
+    const bool free = wmiss && A > 0.f && A * A > e2[v] * kK1;
+    const bool inb = (inbm >> v) & 1u;
     const bool valid = kFull || q0 + 32 * v < n;
-    hit[v] = h;
-    bad[v] = check && valid && (r[v] < a.rlo_f || r[v] > a.rhi_f);
-    // undecided: in-band in-grid uncertified, or out of band (NaN, or
-    // check_radii off); out-of-band with check_radii only reports first_bad
-    und[v] = valid && !bad[v] && !(inb[v] && (!look[v] || h || free));
-    elg[v] = look[v] && !h && !free && wmiss;
+    // out of band: undecided (NaN radius, check_radii off), or only reported
+    // (first_bad) with check_radii
+    const bool bad = check && valid && !inb && !(r[v] != r[v]);
+    // in band: decided without a record (outside the grid, the block's
+    // certificate), by the witness, or by the Lipschitz bound
+    const bool open = ((lookm >> v) & 1u) && !hit && !free;
+    const bool und = inb ? open : (valid && !bad);
+    elgm |= unsigned(open && wmiss) << v;
+    badm |= unsigned(bad) << v;
+    // verdict word 4 ch + v = the ballot of sphere v
+    wd[v] = __ballot_sync(0xffffffffu, ((lookm >> v) & 1u) && hit);
+    ub[v] = __ballot_sync(0xffffffffu, und);
   }
-  // verdict words: word 4 ch + v = the ballot of sphere v
-#pragma unroll
-  for (int v = 0; v < 4; ++v) {
-    const unsigned w = __ballot_sync(0xffffffffu, hit[v]);
-    if (lane == v && (kFull || (ch << 7) + 32 * v < n)) a.bits[(ch << 2) + v] = w;
-  }
-  if (check && __any_sync(0xffffffffu, bad[0] || bad[1] || bad[2] || bad[3])) {
+  if (kFull) {  // (the words of whole chunks: one 16-B store)
+    if (lane == 0)
+      *reinterpret_cast<uint4*>(a.bits + (ch << 2)) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+  } else {
 #pragma unroll
     for (int v = 0; v < 4; ++v)
-      if (bad[v]) atomicMin(a.first_bad, static_cast<unsigned long long>(q0 + 32 * v));
+      if (lane == v && (ch << 7) + 32 * v < n) a.bits[(ch << 2) + v] = wd[v];
+  }
+  if (badm) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+      if ((badm >> v) & 1u) atomicMin(a.first_bad, static_cast<unsigned long long>(q0 + 32 * v));
   }
   // the list: ballot prefix counts
-  unsigned ub[4], tot = 0;
-#pragma unroll
-  for (int v = 0; v < 4; ++v) {
-    ub[v] = __ballot_sync(0xffffffffu, und[v]);
-    tot += __popc(ub[v]);
-  }
-  if (tot == 0) return;
+  const unsigned tot = __popc(ub[0]) + __popc(ub[1]) + __popc(ub[2]) + __popc(ub[3]);
+  if (tot == 0u) return;
   const unsigned lt = (1u << lane) - 1u;
   if (tot > 32u) {  // (rare: NaN or out-of-band batches) straight to the list
     unsigned base = 0;
@@ -791,7 +904,7 @@ __device__ __forceinline__ void resolve1(const FieldArgs& a, const FieldGeom& g,
     base = __shfl_sync(0xffffffffu, base, 0);
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      if (und[v]) {
+      if ((ub[v] >> lane) & 1u) {
         const unsigned at = base + __popc(ub[v] & lt);
         a.list[at] = uint32_t(q0 + 32 * v);
         a.list_s[at] = make_float4(x[v], y[v], z[v], r[v]);
@@ -803,9 +916,9 @@ __device__ __forceinline__ void resolve1(const FieldArgs& a, const FieldGeom& g,
   unsigned pos = rg.head + rg.cnt;
 #pragma unroll
   for (int v = 0; v < 4; ++v) {
-    if (und[v]) {
+    if ((ub[v] >> lane) & 1u) {
       const unsigned slot = (pos + __popc(ub[v] & lt)) & (kRing - 1);
-      rg.q[slot] = uint32_t(q0 + 32 * v) | (unsigned(elg[v]) << 31);
+      rg.q[slot] = uint32_t(q0 + 32 * v) | (((elgm >> v) & 1u) << 31);
       rg.s[slot] = make_float4(x[v], y[v], z[v], r[v]);
     }
     pos += __popc(ub[v]);
@@ -826,11 +939,12 @@ __global__ void __launch_bounds__(CAPT_K0_BLOCK, CAPT_K0_MINB) k_resolve1(FieldA
   __shared__ float4 s_ring[CAPT_K0_BLOCK / 32][kRing];
   __shared__ uint32_t s_ringq[CAPT_K0_BLOCK / 32][kRing];
   Ring rg{s_ring[threadIdx.x >> 5], s_ringq[threadIdx.x >> 5], 0u, 0u};
+  const uint8_t* sblk = stage_block_table(g, a.t.blk);
   // (launched after k_field_zero with programmatic serialisation)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  for (int ch = w0; ch < nfull; ch += nwarps) resolve1<true>(a, g, ch, lane, check, pol, rg);
-  if ((n & 127) && w0 == nfull % nwarps) resolve1<false>(a, g, nfull, lane, check, pol, rg);
+  for (int ch = w0; ch < nfull; ch += nwarps) resolve1<true>(a, g, sblk, ch, lane, check, pol, rg);
+  if ((n & 127) && w0 == nfull % nwarps) resolve1<false>(a, g, sblk, nfull, lane, check, pol, rg);
   if (rg.cnt) ring_drain(a, rg, rg.cnt, lane);
 }
 
@@ -1042,6 +1156,7 @@ int build_field(capt_tree* tree, cudaStream_t s) {
     tree->field_mem = nullptr;
     tree->field = nullptr;
     tree->cand = nullptr;
+    tree->blk = nullptr;
   }
   if (tree->h.k != 3) return CAPT_OK;
   const DevTree t = view(tree);
@@ -1159,9 +1274,43 @@ int build_field(capt_tree* tree, cudaStream_t s) {
   CAPT_CUDA(cudaStreamSynchronize(s));
   float4* pts = nullptr;
   CAPT_CUDA(get(&pts, std::max<uint32_t>(n_fin, 1)));
-  // one allocation: K0 records | candidate records
+  // block table: the smallest blocks whose table fits CAPT_BLK_BYTES; bstep
+  // the power of two covering rcap in 255 steps; rcell bounds |c - x0| for a
+  // centre c whose computed cell is x0's: per axis t = fma(c, inv_h, nc0)
+  // is within 2^-24 (|c| / h + |c0| / h + |t|) of (c - c0) / h (inv_h and
+  // nc0 rounded, one fma rounding), the cell is round(t), and fma(i, h, c0)
+  // is within 2^-24 |x0| of i h + c0
+  {
+    int bs = 1;
+    auto nbk = [&](int sh) {
+      return int64_t((g.nx + (1 << sh) - 1) >> sh) * ((g.ny + (1 << sh) - 1) >> sh) *
+             ((g.nz + (1 << sh) - 1) >> sh);
+    };
+    while (nbk(bs) > int64_t(CAPT_BLK_BYTES)) ++bs;
+    g.bshift = bs;
+    g.bx = (g.nx + (1 << bs) - 1) >> bs;
+    g.by = (g.ny + (1 << bs) - 1) >> bs;
+    g.bz = (g.nz + (1 << bs) - 1) >> bs;
+    g.bbytes = int((nbk(bs) + 15) & ~int64_t(15));
+    g.bstep = float(std::ldexp(1.0, int(std::ceil(std::log2(double(g.rcap) / 255.0)))));
+  }
+  double mu = 0.0;
+  {
+    const double u = std::ldexp(1.0, -24), hh = double(g.h);
+    const int nd[3] = {g.nx, g.ny, g.nz};
+    for (int d = 0; d < 3; ++d) {
+      const double lo_h = std::fabs(double(g.lo[d])) / hh, c0_h = std::fabs(double(g.c0[d])) / hh;
+      const double t_err = u * (lo_h + nd[d] + 2.0 + c0_h + nd[d] + 1.0);
+      const double x0_err = u * (std::fabs(double(g.c0[d])) + (nd[d] + 1.0) * hh);
+      mu = std::max(mu, hh * t_err + x0_err);
+    }
+  }
+  const float rcell = std::nextafter(
+      float(std::sqrt(3.0) * (0.5 * double(g.h) + mu) * (1.0 + std::ldexp(1.0, -20))), INFINITY);
+  // one allocation: K0 records | candidate records | block table
   const size_t off_cand = (2 * sizeof(float4) * size_t(g.cells) + 255) & ~size_t(255);  // (32-B loads)
-  const size_t bytes = off_cand + sizeof(uint32_t) * kCandWords * size_t(g.cells);
+  const size_t off_blk = off_cand + ((sizeof(uint32_t) * kCandWords * size_t(g.cells) + 255) & ~size_t(255));
+  const size_t bytes = off_blk + size_t(g.bbytes);
   char* mem = nullptr;
   cudaError_t e = cudaMalloc(&mem, bytes);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(clearance field)");
@@ -1169,16 +1318,24 @@ int build_field(capt_tree* tree, cudaStream_t s) {
   uint32_t* cand = reinterpret_cast<uint32_t*>(mem + off_cand);
   k_bucket_points<<<grid_for(n_fin, 256, 8), 256, 0, s>>>(t.rep, ids_out, n_fin, pts);
   k_field_cand<<<int(b.nb), 256, 0, s>>>(g, b, bstart, pts, field, cand);
-  e = cudaGetLastError();
+  uint8_t* blk = reinterpret_cast<uint8_t*>(mem + off_blk);
+  e = cudaMemsetAsync(blk, 0, size_t(g.bbytes), s);
+  if (e == cudaSuccess) {
+    const int nbk = g.bx * g.by * g.bz;
+    k_block_table<<<(nbk + 7) / 8, 256, 0, s>>>(g, field, rcell, blk);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) {
     cudaFree(mem);
     return cuda_fail(e, "clearance field build");
   }
-  note_launches(6);
+  note_launches(7);
   tree->field_mem = mem;
   tree->field = field;
   tree->cand = cand;
+  tree->blk = blk;
   tree->fg = g;
   return CAPT_OK;
 }
@@ -1207,11 +1364,12 @@ __global__ void k_field_zero(uint32_t* __restrict__ ctr, uint32_t* __restrict__ 
 }
 
 template <typename... KArgs, typename... Args>
-static cudaError_t launch_pdl_f(void (*kernel)(KArgs...), int grid, int block, cudaStream_t s,
-                                Args... args) {
+static cudaError_t launch_pdl_f(void (*kernel)(KArgs...), int grid, int block, size_t smem,
+                                cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1317,10 +1475,12 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   const bool vec = (reinterpret_cast<uintptr_t>(centers) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(radii) & 15) == 0;
   const int grid = grid_for(((n + 127) / 128) * 32, CAPT_K0_BLOCK, 8 * 256 / CAPT_K0_BLOCK);
-  if (!mask && L == 1) CAPT_CUDA(launch_pdl_f(k_resolve1, grid, CAPT_K0_BLOCK, s, a));
-  else if (vec && !mask && L == 8) CAPT_CUDA(launch_pdl_f(k_resolve<true, false, 8>, grid, CAPT_K0_BLOCK, s, a));
-  else if (mask) CAPT_CUDA(launch_pdl_f(k_resolve<false, true, 0>, grid, CAPT_K0_BLOCK, s, a));
-  else CAPT_CUDA(launch_pdl_f(k_resolve<false, false, 0>, grid, CAPT_K0_BLOCK, s, a));
+  const size_t sm = 0;  // (the block table is a static shared array)
+  const bool bits16 = (reinterpret_cast<uintptr_t>(bits) & 15) == 0;
+  if (!mask && L == 1 && bits16) CAPT_CUDA(launch_pdl_f(k_resolve1, grid, CAPT_K0_BLOCK, sm, s, a));
+  else if (vec && !mask && L == 8) CAPT_CUDA(launch_pdl_f(k_resolve<true, false, 8>, grid, CAPT_K0_BLOCK, sm, s, a));
+  else if (mask) CAPT_CUDA(launch_pdl_f(k_resolve<false, true, 0>, grid, CAPT_K0_BLOCK, sm, s, a));
+  else CAPT_CUDA(launch_pdl_f(k_resolve<false, false, 0>, grid, CAPT_K0_BLOCK, sm, s, a));
   CAPT_CUDA(cudaGetLastError());
   note_launches(1);
   if (tcall >= 0) {
@@ -1328,12 +1488,12 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
     if (rc) return rc;
   }
   // the list stage: persistent grids (the list lengths are known on the device only)
-  CAPT_CUDA(launch_pdl_f(k_list_knn, grid_for(n, 256, 8), 256, s, a, list2, list2_n));
+  CAPT_CUDA(launch_pdl_f(k_list_knn, grid_for(n, 256, 8), 256, 0, s, a, list2, list2_n));
   FieldArgs a2 = a;
   a2.list = list2;
   a2.list_s = nullptr;
   a2.list_n = list2_n;
-  CAPT_CUDA(launch_pdl_f(k_tree_list, grid_for(int64_t(n) * 32, 256, 8), 256, s, a2));
+  CAPT_CUDA(launch_pdl_f(k_tree_list, grid_for(int64_t(n) * 32, 256, 8), 256, 0, s, a2));
   CAPT_CUDA(cudaGetLastError());
   note_launches(2);
   if (tcall >= 0) {
@@ -1341,11 +1501,14 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
     if (rc) return rc;
   }
 #ifdef CAPT_FIELD_STATS  // diagnostics build (build_ext -D CAPT_FIELD_STATS --out ...)
-  uint32_t nl[2] = {0, 0};
-  CAPT_CUDA(cudaMemcpyAsync(nl, a.list_n, 8, cudaMemcpyDeviceToHost, s));
+  uint32_t nl[4] = {0, 0, 0, 0};
+  CAPT_CUDA(cudaMemcpyAsync(nl, a.list_n, 16, cudaMemcpyDeviceToHost, s));
   CAPT_CUDA(cudaStreamSynchronize(s));
-  fprintf(stderr, "[capt field] n=%lld L=%d list=%u (%.4f%%) tree path=%u (%.5f%%)\n",
-          (long long)n, L, nl[0], 100.0 * nl[0] / double(n), nl[1], 100.0 * nl[1] / double(n));
+  fprintf(stderr,
+          "[capt field] n=%lld L=%d list=%u (%.4f%%) tree path=%u (%.5f%%) records=%u (%.3f) "
+          "block-free=%u (%.3f)\n",
+          (long long)n, L, nl[0], 100.0 * nl[0] / double(n), nl[1], 100.0 * nl[1] / double(n),
+          nl[2], nl[2] / double(n), nl[3], nl[3] / double(n));
 #endif
   return CAPT_OK;
 }
@@ -1408,6 +1571,23 @@ extern "C" int capt_tree_field(const capt_tree* tree, capt_field_info* info, flo
           cand[(i * kCand + k) * 3 + d] = q == kCandNone ? INF : float(q);
         }
     }
+  }
+  return CAPT_OK;
+}
+
+extern "C" int capt_tree_field_blocks(const capt_tree* tree, int32_t* dims, float* step,
+                                      uint8_t* table) {
+  if (!tree || !dims || !step) return fail(CAPT_EINVAL, "NULL argument");
+  if (!tree->field || !tree->blk) return fail(CAPT_EINVAL, "tree has no clearance field (k < 3)");
+  const FieldGeom& g = tree->fg;
+  dims[0] = g.bx;
+  dims[1] = g.by;
+  dims[2] = g.bz;
+  dims[3] = g.bshift;
+  *step = g.bstep;
+  if (table) {
+    CAPT_CUDA(cudaSetDevice(tree->device));
+    CAPT_CUDA(cudaMemcpy(table, tree->blk, size_t(g.bx) * g.by * g.bz, cudaMemcpyDeviceToHost));
   }
   return CAPT_OK;
 }

@@ -73,6 +73,13 @@ struct FieldGeom {
   float q_step;        // candidate offsets from x0: int16 multiples of q_step (a power of two)
   float q_err;         // bound on the Euclidean error of a decoded candidate difference
   int64_t cells;
+  // block table: blocks of 2^bshift cells per axis, bx*by*bz bytes; entry
+  // q * bstep <= the distance from the cloud to any centre whose computed
+  // cell lies in the block (bstep a power of two); K0 keeps it in shared
+  // memory and skips the record of a sphere it certifies free
+  int bshift, bx, by, bz;
+  int bbytes;          // table bytes, rounded up to 16
+  float bstep;
 };
 
 // Candidate record of a cell: the kCand cloud points nearest its centre x0,
@@ -103,6 +110,7 @@ struct DevTree {
   // clearance field (capt_field.cu; field == nullptr if absent)
   const float4* field;    // per cell: witness xyz + lower bound nn
   const uint32_t* cand;   // per cell: kCandWords words (candidate record, see kCand)
+  const uint8_t* blk;     // block table (FieldGeom::bshift ...)
   FieldGeom fg;
 };
 
@@ -118,6 +126,7 @@ struct capt_tree {
   void* field_mem = nullptr;
   float4* field = nullptr;
   uint32_t* cand = nullptr;
+  uint8_t* blk = nullptr;
   capt::FieldGeom fg{};
 };
 
@@ -160,6 +169,7 @@ inline DevTree view(const capt_tree* t) {
   d.probe = reinterpret_cast<const float*>(t->slab + t->h.off_probe);
   d.field = t->field;
   d.cand = t->cand;
+  d.blk = t->blk;
   d.fg = t->fg;
   return d;
 }

@@ -222,6 +222,20 @@ class Capt:
                 out["candidates"] = cb
         return out
 
+    def field_blocks(self):
+        """The clearance field's block table (include/capt_b200.h
+        capt_tree_field_blocks): dict(table=(bz, by, bx) uint8, shift, step),
+        or None for trees without a field."""
+        dims = (C.c_int32 * 4)()
+        step = C.c_float(0.0)
+        L = _lib.lib()
+        if L.capt_tree_field_blocks(self._h, dims, C.byref(step), None) != _lib.CAPT_OK:
+            return None
+        tab = np.empty((dims[2], dims[1], dims[0]), np.uint8)
+        _lib.check(L.capt_tree_field_blocks(self._h, dims, C.byref(step), tab.ctypes.data),
+                   "capt_tree_field_blocks")
+        return dict(table=tab, shift=int(dims[3]), step=np.float32(step.value))
+
     # -- replication (multi-GPU) ---------------------------------------------
     def slab_tensor(self):
         """Zero-copy torch uint8 view of the position-independent device slab

@@ -133,6 +133,50 @@ def test_field_records_uploaded_and_built_trees():
     assert np.array_equal(f2["candidates"], f1["candidates"])
 
 
+def check_block_table(tree, cloud, n=400000, seed=0):
+    """Every block entry q certifies q * step <= the float64 distance from the
+    cloud to any centre whose computed cell lies in the block; sampled
+    centres (uniform over the grid, and clustered near block faces) are
+    checked against every block their computed cell could fall in."""
+    from scipy.spatial import cKDTree
+    f = tree.clearance_field()
+    b = tree.field_blocks()
+    assert b is not None
+    tab, sh, step = b["table"], b["shift"], float(b["step"])
+    nz, ny, nx = f["shape"]
+    assert tab.shape == (-(-nz >> sh), -(-ny >> sh), -(-nx >> sh))
+    assert step > 0 and (np.frexp(step)[0] == 0.5)  # a power of two
+    h = float(f["h"])
+    c0 = f["c0"].astype(np.float64)
+    rng = np.random.default_rng(seed)
+    dims = np.array([nx, ny, nz])
+    t = rng.uniform(-0.5, dims - 0.5, (n, 3))
+    # half of them on block faces (+-1e-4 cells)
+    B = 1 << sh
+    face = rng.integers(0, 3, n // 2)
+    edge = (rng.integers(0, dims.max() // B + 1, n // 2) * B - 0.5)
+    t[np.arange(n // 2), face] = np.clip(edge + rng.uniform(-1e-4, 1e-4, n // 2), -0.5,
+                                         dims[face] - 0.5)
+    c = (c0 + t * h).astype(np.float32).astype(np.float64)
+    d, _ = cKDTree(np.unique(cloud.astype(np.float32), axis=0).astype(np.float64)).query(c)
+    tt = (c - c0) / h
+    worst = np.inf
+    for dx in (-1e-3, 0.0, 1e-3):
+        cell = np.clip(np.rint(tt + dx), 0, dims - 1).astype(np.int64)
+        blk = cell >> sh
+        q = tab[blk[:, 2], blk[:, 1], blk[:, 0]].astype(np.float64)
+        assert np.all(q * step <= d), "block bound above a nearest-point distance"
+        worst = min(worst, float(np.min(d - q * step)))
+    return float((tab > 0).mean())
+
+
+def test_field_block_table_bounds():
+    for cloud, band in ((W.cfg1_cloud(), (0.02, 0.08)), (W.cfg3_cloud(n=65536, seed=11), (0.01, 0.1)),
+                        (W.cfg0_cloud(), (0.01, 0.08))):
+        tree = P.construct(P.PointCloud(cloud), P.BuildParams(*band))
+        assert check_block_table(tree, cloud) > 0.05
+
+
 def test_field_golden_masks_and_groups():
     z = load_golden("queries.npz")
     for name in z["names"]:
