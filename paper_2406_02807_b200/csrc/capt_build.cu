@@ -15,12 +15,14 @@
 //      tree.py:164-188).  This equals the recursive definition because the
 //      float64 point-box distance is monotone under cell inclusion, so a point
 //      afforded by the leaf cell survives every ancestor's filter
-//      (tree.py:209-218).  Candidates come from a stackless traversal of the
-//      implicit tree pruned by a conservative fp32 box-box distance, then
-//      the exact float64 test of tree.py:209-213 decides membership;
+//      (tree.py:209-218).  Candidates come from a uniform grid of point
+//      buckets (edge >= r_max): one warp per leaf scans the buckets its cell
+//      grown by r_max overlaps, then the exact float64 test of
+//      tree.py:209-213 decides membership;
 //   5. count pass -> exclusive scan -> fill pass into the padded slab layout.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -123,22 +125,6 @@ __device__ __forceinline__ double dist_cell64(int k, const double* p, const Cell
   return s;
 }
 
-// Conservative lower bound test: may the node cell hold a point within r of
-// the leaf cell?  (fp32 with a relative margin; exact test happens per point)
-__device__ __forceinline__ bool cells_near(int k, const float* nlo, const float* nhi,
-                                           const Cell& c, float r2_hi) {
-  float s = 0.f;
-  for (int d = 0; d < k; ++d) {
-    if (nlo[d] == INFINITY) return false;  // all-padding subtree
-    float g = 0.f;
-    if (nlo[d] > c.hi[d]) g = nlo[d] - c.hi[d];
-    else if (c.lo[d] > nhi[d]) g = c.lo[d] - nhi[d];
-    g *= (1.0f - 0x1p-20f);
-    s = fmaf(g, g, s);
-  }
-  return s <= r2_hi;
-}
-
 struct BuildView {
   int k, depth;
   int64_t n, n0;
@@ -146,67 +132,9 @@ struct BuildView {
   const int32_t* rep;  // n (leaf -> point index)
   const float* T;
   double r_min_sq, r_max_sq;
-  float r2_hi;         // fp32 r_max^2 upper margin for pruning
+  float r2_hi;         // fp32 r_max^2 with an upward margin (clear-miss prefilter)
   int shortcut;
 };
-
-// Stackless DFS over the implicit tree; visit(point index) for every finite
-// leaf representative (other than `self`) whose cell may be within r_max of
-// cell `c`, applying the exact membership test.
-template <class F>
-__device__ __forceinline__ void for_each_afforded(const BuildView& v, const Cell& c, int64_t self,
-                                                  F&& visit) {
-  float lo[3] = {-INFINITY, -INFINITY, -INFINITY}, hi[3] = {INFINITY, INFINITY, INFINITY};
-  float savedHi[48], savedLo[48];
-  int64_t i = 0;
-  int level = 0;
-  const int64_t inner = v.n - 1;
-  while (true) {
-    bool descend = false;
-    if (cells_near(v.k, lo, hi, c, v.r2_hi)) {
-      if (i >= inner) {
-        const int64_t leaf = i - inner;
-        const int32_t p = v.rep[leaf];
-        if (leaf != self && p < v.n0) {
-          double q[3];
-          for (int d = 0; d < v.k; ++d) q[d] = double(v.X[d * v.n + p]);
-          if (dist_cell64(v.k, q, c) <= v.r_max_sq) visit(p);
-        }
-      } else {
-        descend = true;
-      }
-    }
-    if (descend) {
-      const int a = level % v.k;
-      savedHi[level] = hi[a];
-      hi[a] = v.T[i];
-      i = 2 * i + 1;
-      ++level;
-      continue;
-    }
-    // advance to the next node in DFS order
-    bool done = false;
-    while (true) {
-      if (i == 0) {
-        done = true;
-        break;
-      }
-      const int64_t parent = (i - 1) / 2;
-      const int a = (level - 1) % v.k;
-      if (i & 1) {  // left child -> right sibling
-        hi[a] = savedHi[level - 1];
-        savedLo[level - 1] = lo[a];
-        lo[a] = v.T[parent];
-        i = i + 1;
-        break;
-      }
-      lo[a] = savedLo[level - 1];  // right child -> up
-      i = parent;
-      --level;
-    }
-    if (done) break;
-  }
-}
 
 // shortcut test (tree.py:176-181): sum max(|rep-lo|, |rep-hi|)^2 <= r_min^2
 __device__ __forceinline__ bool shortcut_fires(const BuildView& v, const Cell& c, int32_t p) {
@@ -222,52 +150,163 @@ __device__ __forceinline__ bool shortcut_fires(const BuildView& v, const Cell& c
   return s <= v.r_min_sq;
 }
 
-__global__ void k_count(BuildView v, uint32_t* __restrict__ sizes) {
-  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < v.n;
-       j += int64_t(gridDim.x) * blockDim.x) {
-    const Cell c = leaf_cell(v.T, v.n, v.depth, v.k, j);
-    const int32_t p = v.rep[j];
-    uint32_t m = 1;
-    if (!(p < v.n0 && v.shortcut && shortcut_fires(v, c, p)))
-      for_each_afforded(v, c, j, [&](int32_t) { ++m; });
-    sizes[j] = m;
+// ---------------------------------------------------------------------------
+// Bucketed affordance sets.  The finite points are sorted into a uniform grid
+// of buckets of edge b (x fastest); a leaf's candidates are the points of the
+// buckets its cell grown by r' = r_max (1 + 2^-20) overlaps, clamped to the
+// grid.  bucket(x) = floor((x - lo) / b) is monotone in x, and a point with
+// float64 dist^2(p, cell) <= r_max^2 lies within r' of the cell on every
+// axis, so it is among the candidates; the exact test (tree.py:209-213)
+// decides.  One warp per leaf: the x-buckets of one (y, z) row are one
+// contiguous range of the sorted points, scanned 32 points at a time (an fp32
+// box distance with a relative margin rejects the clear misses first).
+// ---------------------------------------------------------------------------
+struct Buckets {
+  double lo[3], inv_b;
+  int dims[3];
+  const uint32_t* start;  // nb + 1
+  const float4* pts;      // sorted points {x, y, z, index bits}
+};
+
+__device__ __forceinline__ int bucket_of(const Buckets& B, int d, double x) {
+  double t = floor(__dmul_rn(__dsub_rn(x, B.lo[d]), B.inv_b));
+  if (!(t >= 0.0)) t = 0.0;  // (also -inf)
+  return t >= double(B.dims[d] - 1) ? B.dims[d] - 1 : int(t);
+}
+
+__global__ void k_bucket_key(int k, int64_t n0, Buckets B, const float* __restrict__ X, int64_t n,
+                             uint32_t* __restrict__ key, int32_t* __restrict__ id,
+                             uint32_t* __restrict__ count) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n0;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    int c[3] = {0, 0, 0};
+    for (int d = 0; d < k; ++d) c[d] = bucket_of(B, d, double(X[d * n + i]));
+    const uint32_t kk = (uint32_t(c[2]) * uint32_t(B.dims[1]) + uint32_t(c[1])) * uint32_t(B.dims[0]) +
+                        uint32_t(c[0]);
+    key[i] = kk;
+    id[i] = int32_t(i);
+    atomicAdd(count + kk, 1u);
   }
 }
 
-__global__ void k_fill(BuildView v, const uint2* __restrict__ set, float4* __restrict__ data,
-                       float4* __restrict__ box) {
-  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < v.n;
-       j += int64_t(gridDim.x) * blockDim.x) {
+__global__ void k_bucket_gather(int k, int64_t n0, const float* __restrict__ X, int64_t n,
+                                const int32_t* __restrict__ id, float4* __restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n0;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t p = id[i];
+    float v[3] = {0.f, 0.f, 0.f};
+    for (int d = 0; d < k; ++d) v[d] = X[d * n + p];
+    out[i] = make_float4(v[0], v[1], v[2], __int_as_float(p));
+  }
+}
+
+// fp32 lower bound of the box distance (clear misses only: a relative
+// margin of 2^-20 on every gap covers the roundings)
+__device__ __forceinline__ bool cell_near32(int k, const float4 q, const Cell& c, float r2_hi) {
+  const float v[3] = {q.x, q.y, q.z};
+  float s = 0.f;
+  for (int d = 0; d < k; ++d) {
+    float g = fmaxf(fmaxf(c.lo[d] - v[d], 0.f), v[d] - c.hi[d]);
+    g *= (1.0f - 0x1p-20f);
+    s = fmaf(g, g, s);
+  }
+  return s <= r2_hi;
+}
+
+// Candidates of leaf j's set (excluding its representative), in a fixed
+// order (bucket rows, then sorted point order): visit(lane_hit, point).
+template <class F>
+__device__ __forceinline__ void warp_afforded(const BuildView& v, const Buckets& B, const Cell& c,
+                                              int32_t self, int lane, F&& visit) {
+  const double rp = v.r_max_sq > 0.0 ? sqrt(v.r_max_sq) * (1.0 + 0x1p-20) : 0.0;
+  int b0[3] = {0, 0, 0}, b1[3] = {0, 0, 0};
+  for (int d = 0; d < v.k; ++d) {
+    b0[d] = bucket_of(B, d, __dsub_rn(double(c.lo[d]), rp));
+    b1[d] = bucket_of(B, d, __dadd_rn(double(c.hi[d]), rp));
+  }
+  for (int bz = b0[2]; bz <= b1[2]; ++bz)
+    for (int by = b0[1]; by <= b1[1]; ++by) {
+      const uint32_t row = (uint32_t(bz) * uint32_t(B.dims[1]) + uint32_t(by)) * uint32_t(B.dims[0]);
+      const uint32_t i0 = __ldg(B.start + row + b0[0]), i1 = __ldg(B.start + row + b1[0] + 1);
+      for (uint32_t i = i0; i < i1; i += 32) {
+        const uint32_t ii = i + lane;
+        bool hit = false;
+        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ii < i1) {
+          q = __ldg(B.pts + ii);
+          if (__float_as_int(q.w) != self && cell_near32(v.k, q, c, v.r2_hi)) {
+            const double pq[3] = {double(q.x), double(q.y), double(q.z)};
+            hit = dist_cell64(v.k, pq, c) <= v.r_max_sq;
+          }
+        }
+        visit(hit, q);
+      }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_count_b(BuildView v, Buckets B,
+                                                 uint32_t* __restrict__ sizes) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t j = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; j < v.n; j += nw) {
+    const Cell c = leaf_cell(v.T, v.n, v.depth, v.k, j);
+    const int32_t p = v.rep[j];
+    uint32_t m = 0;
+    if (!(p < v.n0 && v.shortcut && shortcut_fires(v, c, p)))
+      warp_afforded(v, B, c, p, lane, [&](bool hit, float4) {
+        m += __popc(__ballot_sync(0xffffffffu, hit));
+      });
+    if (lane == 0) sizes[j] = 1 + m;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_fill_b(BuildView v, Buckets B,
+                                                const uint2* __restrict__ set,
+                                                float4* __restrict__ data,
+                                                float4* __restrict__ box) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const float INF = __int_as_float(0x7f800000);
+  for (int64_t j = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; j < v.n; j += nw) {
     const Cell c = leaf_cell(v.T, v.n, v.depth, v.k, j);
     const int32_t p = v.rep[j];
     const uint2 st = set[j];
     const uint32_t m4 = (st.y + 3u) & ~3u;
     float* dst = reinterpret_cast<float*>(data + st.x);
-    float blo[3], bhi[3];
-    for (int d = 0; d < 3; ++d) {
-      const float x = d < v.k ? (p < v.n0 ? v.X[d * v.n + p] : INFINITY) : 0.f;
-      dst[d * m4] = x;
-      blo[d] = x;
-      bhi[d] = x;
-    }
+    // row 0: the representative (+inf for a padding leaf)
+    float rx[3] = {0.f, 0.f, 0.f};
+    for (int d = 0; d < v.k; ++d) rx[d] = p < v.n0 ? v.X[d * v.n + p] : INF;
+    float blo[3] = {rx[0], rx[1], rx[2]}, bhi[3] = {rx[0], rx[1], rx[2]};
+    if (lane < 3) dst[lane * m4] = rx[lane];
     uint32_t w = 1;
-    if (st.y > 1) {
-      for_each_afforded(v, c, j, [&](int32_t q) {
-        for (int d = 0; d < v.k; ++d) {
-          const float x = v.X[d * v.n + q];
-          dst[d * m4 + w] = x;
-          blo[d] = fminf(blo[d], x);
-          bhi[d] = fmaxf(bhi[d], x);
+    if (st.y > 1)
+      warp_afforded(v, B, c, p, lane, [&](bool hit, float4 q) {
+        const unsigned b = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          const uint32_t at = w + __popc(b & ((1u << lane) - 1u));
+          const float qv[3] = {q.x, q.y, q.z};
+          for (int d = 0; d < 3; ++d) {
+            dst[d * m4 + at] = d < v.k ? qv[d] : 0.f;
+            blo[d] = fminf(blo[d], qv[d]);
+            bhi[d] = fmaxf(bhi[d], qv[d]);
+          }
         }
-        ++w;
+        w += __popc(b);
       });
+    // padding rows (+inf), unused axes 0
+    for (uint32_t i = st.y + lane; i < m4; i += 32)
+      for (int d = 0; d < 3; ++d) dst[d * m4 + i] = d < v.k ? INF : 0.f;
+    for (int d = 0; d < 3; ++d) {
+      for (int o = 16; o; o >>= 1) {
+        blo[d] = fminf(blo[d], __shfl_xor_sync(0xffffffffu, blo[d], o));
+        bhi[d] = fmaxf(bhi[d], __shfl_xor_sync(0xffffffffu, bhi[d], o));
+      }
+      if (d >= v.k) blo[d] = bhi[d] = 0.f;
     }
-    for (uint32_t i = st.y; i < m4; ++i)
-      for (int d = 0; d < 3; ++d) dst[d * m4 + i] = d < v.k ? INFINITY : 0.f;
-    for (int d = v.k; d < 3; ++d)
-      for (uint32_t i = 1; i < st.y; ++i) dst[d * m4 + i] = 0.f;
-    box[2 * j] = make_float4(blo[0], blo[1], blo[2], 0.f);
-    box[2 * j + 1] = make_float4(bhi[0], bhi[1], bhi[2], 0.f);
+    if (lane == 0) {
+      box[2 * j] = make_float4(blo[0], blo[1], blo[2], 0.f);
+      box[2 * j + 1] = make_float4(bhi[0], bhi[1], bhi[2], 0.f);
+    }
   }
 }
 
@@ -296,11 +335,12 @@ __global__ void k_widen(int64_t n, const uint32_t* __restrict__ sizes, int64_t* 
 // Scratch arena for one build (freed at the end).
 struct Scratch {
   cudaStream_t s;
-  void* ptrs[48];
+  void* ptrs[64];
   int np = 0;
   template <class T>
   T* get(size_t count) {
     void* p = nullptr;
+    if (np == 64) return nullptr;
     if (cudaMallocAsync(&p, (count ? count : 1) * sizeof(T), s) != cudaSuccess) return nullptr;
     ptrs[np++] = p;
     return static_cast<T*>(p);
@@ -377,6 +417,15 @@ extern "C" int capt_tree_build(int device, int k, const float* points, int64_t n
                                               int(n), 0, 32, s));
   }
 
+  // the cloud's extremes per axis (bucket grid): first / last finite entry
+  // of each presorted list, kept before the partitions reorder them
+  int32_t* P0sorted[3] = {nullptr, nullptr, nullptr};
+  for (int d = 0; d < k; ++d) {
+    P0sorted[d] = S.get<int32_t>(size_t(n0));
+    if (!P0sorted[d]) return fail(CAPT_ENOMEM, "scratch allocation");
+    CAPT_CUDA(cudaMemcpyAsync(P0sorted[d], P[d], sizeof(int32_t) * n0, cudaMemcpyDeviceToDevice, s));
+  }
+
   // 2. level-by-level median split with stable partitions
   for (int L = 0; L < depth; ++L) {
     const int64_t n_seg = int64_t(1) << L;
@@ -410,7 +459,74 @@ extern "C" int capt_tree_build(int device, int k, const float* points, int64_t n
   v.r_max_sq = r_max * r_max;
   v.r2_hi = float(r_max * r_max) * (1.0f + 0x1p-16f);
   v.shortcut = use_rmin_shortcut;
-  k_count<<<grid_for(n, 128, 16), 128, 0, s>>>(v, sizes);
+  // the point buckets (edge >= r_max, at most ~2^21 buckets)
+  Buckets B;
+  {
+    float hb[6];
+    {
+      // the cloud's box: the first / last entries of the presorted axis lists
+      // hold the extremes (finite points sort before the +inf padding)
+      for (int d = 0; d < 3; ++d) {
+        hb[d] = 0.f;
+        hb[3 + d] = 0.f;
+      }
+      int32_t ends[6] = {0, 0, 0, 0, 0, 0};
+      for (int d = 0; d < k; ++d) {
+        CAPT_CUDA(cudaMemcpyAsync(ends + d, P0sorted[d], 4, cudaMemcpyDeviceToHost, s));
+        CAPT_CUDA(cudaMemcpyAsync(ends + 3 + d, P0sorted[d] + (n0 - 1), 4, cudaMemcpyDeviceToHost, s));
+      }
+      CAPT_CUDA(cudaStreamSynchronize(s));
+      for (int d = 0; d < k; ++d) {
+        CAPT_CUDA(cudaMemcpyAsync(hb + d, X + size_t(d) * n + ends[d], 4, cudaMemcpyDeviceToHost, s));
+        CAPT_CUDA(cudaMemcpyAsync(hb + 3 + d, X + size_t(d) * n + ends[3 + d], 4, cudaMemcpyDeviceToHost, s));
+      }
+      CAPT_CUDA(cudaStreamSynchronize(s));
+    }
+    double ext[3] = {0.0, 0.0, 0.0}, vol = 1.0;
+    for (int d = 0; d < 3; ++d) {
+      B.lo[d] = 0.0;
+      B.dims[d] = 1;
+    }
+    for (int d = 0; d < k; ++d) {
+      B.lo[d] = double(hb[d]);
+      ext[d] = double(hb[3 + d]) - double(hb[d]);
+    }
+    double b = r_max;
+    for (int it = 0; it < 400; ++it) {
+      vol = 1.0;
+      for (int d = 0; d < k; ++d) vol *= std::floor(ext[d] / b) + 1.0;
+      if (vol <= double(1 << 21)) break;
+      b *= 1.1;
+    }
+    B.inv_b = 1.0 / b;
+    int64_t nb = 1;
+    for (int d = 0; d < k; ++d) {
+      B.dims[d] = int(std::floor(ext[d] / b) + 1.0);
+      nb *= B.dims[d];
+    }
+    uint32_t* bkey = S.get<uint32_t>(size_t(n0));
+    uint32_t* bkeyS = S.get<uint32_t>(size_t(n0));
+    int32_t* bid = S.get<int32_t>(size_t(n0));
+    int32_t* bidS = S.get<int32_t>(size_t(n0));
+    uint32_t* cnt = S.get<uint32_t>(size_t(nb + 1));
+    uint32_t* start = S.get<uint32_t>(size_t(nb + 1));
+    float4* bp = S.get<float4>(size_t(n0));
+    if (!bkey || !bkeyS || !bid || !bidS || !cnt || !start || !bp)
+      return fail(CAPT_ENOMEM, "scratch allocation");
+    CAPT_CUDA(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (nb + 1), s));
+    k_bucket_key<<<grid_for(n0, 256, 8), 256, 0, s>>>(k, n0, B, X, n, bkey, bid, cnt);
+    size_t t1 = 0, t2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, t1, bkey, bkeyS, bid, bidS, int(n0), 0, 32, s);
+    cub::DeviceScan::ExclusiveSum(nullptr, t2, cnt, start, int(nb + 1), s);
+    void* tmpb = S.get<char>(std::max(t1, t2));
+    if (!tmpb) return fail(CAPT_ENOMEM, "scratch allocation");
+    CAPT_CUDA(cub::DeviceRadixSort::SortPairs(tmpb, t1, bkey, bkeyS, bid, bidS, int(n0), 0, 32, s));
+    CAPT_CUDA(cub::DeviceScan::ExclusiveSum(tmpb, t2, cnt, start, int(nb + 1), s));
+    k_bucket_gather<<<grid_for(n0, 256, 8), 256, 0, s>>>(k, n0, X, n, bidS, bp);
+    B.start = start;
+    B.pts = bp;
+  }
+  k_count_b<<<grid_for(n * 32, 256, 8), 256, 0, s>>>(v, B, sizes);
   CAPT_CUDA(cudaGetLastError());
 
   // 5. layout: exclusive scans of padded float4 counts and of set sizes
@@ -471,8 +587,8 @@ extern "C" int capt_tree_build(int device, int k, const float* points, int64_t n
   if (e == cudaSuccess) {
     k_set_layout<<<G, 256, 0, s>>>(n, sizes, f4x, offx, const_cast<uint2*>(dv.set),
                                    const_cast<int64_t*>(dv.offs));
-    k_fill<<<grid_for(n, 128, 16), 128, 0, s>>>(v, dv.set, const_cast<float4*>(dv.data),
-                                                const_cast<float4*>(dv.box));
+    k_fill_b<<<grid_for(n * 32, 256, 8), 256, 0, s>>>(v, B, dv.set, const_cast<float4*>(dv.data),
+                                                      const_cast<float4*>(dv.box));
     e = cudaGetLastError();
     if (e == cudaSuccess && compute_origins(dv, s)) e = cudaErrorLaunchFailure;
   }

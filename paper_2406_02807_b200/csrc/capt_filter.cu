@@ -17,9 +17,11 @@
 //              are a max-scan of kept positions.
 // Orphan repair (morton.py:212-235): every dropped point whose anchor was
 // dropped later is re-added, in ascending original index, iff no final
-// survivor lies within r_filter (tiled float64 brute-force check).
+// survivor lies within r_filter (float64 test against the survivors of the
+// neighbouring cells of a uniform grid, k_orphans).
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -200,35 +202,75 @@ __global__ void k_candidates(int64_t n0, const uint8_t* __restrict__ surv,
     cand[i] = !surv[i] && !surv[anchor_of[i]];
 }
 
-// orphan check: candidate c is an orphan iff no survivor within r (fp64)
-constexpr int kTile = 256;
-__global__ void __launch_bounds__(kTile)
-    k_orphans(int k, int64_t nc, const int32_t* __restrict__ cidx, int64_t ns,
-              const int32_t* __restrict__ sidx, const float* __restrict__ p, double r2,
-              uint8_t* __restrict__ orphan) {
-  __shared__ float sp[kTile * 3];
-  for (int64_t base = int64_t(blockIdx.x) * kTile; base < nc; base += int64_t(gridDim.x) * kTile) {
-    const int64_t c = base + threadIdx.x;
+// Orphan check (morton.py:212-235): candidate c is an orphan iff no final
+// survivor lies within r (the float64 test of the brute-force reference).
+// Survivors are bucketed on a uniform grid of edge cs >= r (1 + 2^-20):
+// bucket(x) = floor((x - lo) / cs) per axis in float64, clamped to the grid
+// (monotone in x), so a survivor within r of c differs from c by at most one
+// bucket per axis; keys are x-fastest, so the three x-buckets of one (y, z)
+// row are one key range of the sorted survivors, found by binary search.
+struct OrphanGrid {
+  double lo[3], inv_cs;
+  int dims[3];
+};
+
+__device__ __forceinline__ int og_cell(const OrphanGrid& G, int d, float x) {
+  const double t = floor(__dmul_rn(__dsub_rn(double(x), G.lo[d]), G.inv_cs));
+  return t < 0.0 ? 0 : (t >= double(G.dims[d] - 1) ? G.dims[d] - 1 : int(t));
+}
+
+__global__ void k_orphan_keys(int k, OrphanGrid G, int64_t m, const int32_t* __restrict__ sidx,
+                              const float* __restrict__ p, uint32_t* __restrict__ key,
+                              int32_t* __restrict__ val) {
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
+       j += int64_t(gridDim.x) * blockDim.x) {
+    const float* q = p + int64_t(sidx[j]) * k;
+    int c[3] = {0, 0, 0};
+    for (int d = 0; d < k; ++d) c[d] = og_cell(G, d, q[d]);
+    key[j] = (uint32_t(c[2]) * uint32_t(G.dims[1]) + uint32_t(c[1])) * uint32_t(G.dims[0]) +
+             uint32_t(c[0]);
+    val[j] = sidx[j];
+  }
+}
+
+__device__ __forceinline__ int64_t lower_bound_u32(const uint32_t* a, int64_t n, uint32_t v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (__ldg(a + mid) < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_orphans(int k, OrphanGrid G, int64_t nc, const int32_t* __restrict__ cidx,
+                          int64_t ns, const uint32_t* __restrict__ skey,
+                          const int32_t* __restrict__ sval, const float* __restrict__ p,
+                          double r2, uint8_t* __restrict__ orphan) {
+  for (int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < nc;
+       c += int64_t(gridDim.x) * blockDim.x) {
     float pc[3] = {0.f, 0.f, 0.f};
-    bool found = c >= nc;
-    if (c < nc)
-      for (int d = 0; d < k; ++d) pc[d] = p[int64_t(cidx[c]) * k + d];
-    for (int64_t s0 = 0; s0 < ns; s0 += kTile) {
-      if (__syncthreads_and(found)) break;
-      const int64_t s = s0 + threadIdx.x;
-      if (s < ns)
-        for (int d = 0; d < k; ++d) sp[threadIdx.x * 3 + d] = p[int64_t(sidx[s]) * k + d];
-      __syncthreads();
-      const int cnt = int(ns - s0 < kTile ? ns - s0 : kTile);
-      if (!found)
-        for (int t = 0; t < cnt; ++t)
-          if (dist64(k, pc, sp + t * 3) <= r2) {
+    int cc[3] = {0, 0, 0};
+    for (int d = 0; d < k; ++d) {
+      pc[d] = p[int64_t(cidx[c]) * k + d];
+      cc[d] = og_cell(G, d, pc[d]);
+    }
+    bool found = false;
+    const int z0 = k > 2 ? max(cc[2] - 1, 0) : 0, z1 = k > 2 ? min(cc[2] + 1, G.dims[2] - 1) : 0;
+    const int y0 = k > 1 ? max(cc[1] - 1, 0) : 0, y1 = k > 1 ? min(cc[1] + 1, G.dims[1] - 1) : 0;
+    const int x0 = max(cc[0] - 1, 0), x1 = min(cc[0] + 1, G.dims[0] - 1);
+    for (int z = z0; z <= z1 && !found; ++z)
+      for (int y = y0; y <= y1 && !found; ++y) {
+        const uint32_t row = (uint32_t(z) * uint32_t(G.dims[1]) + uint32_t(y)) * uint32_t(G.dims[0]);
+        const int64_t b = lower_bound_u32(skey, ns, row + uint32_t(x0));
+        const int64_t e = lower_bound_u32(skey, ns, row + uint32_t(x1) + 1u);
+        for (int64_t i = b; i < e; ++i)
+          if (dist64(k, pc, p + int64_t(sval[i]) * k) <= r2) {
             found = true;
             break;
           }
-      __syncthreads();
-    }
-    if (c < nc) orphan[c] = !found;
+      }
+    orphan[c] = !found;
   }
 }
 
@@ -453,7 +495,48 @@ extern "C" int capt_filter_cloud(int device, int k, const float* points, int64_t
     k_candidates<<<grid_for(n0, 256, 8), 256, 0, s>>>(n0, surv, anchor_of, cand);
     TRY(select_flagged(A, cand, n0, cidx, &nc));
     if (nc) {
-      k_orphans<<<grid_for(nc, kTile, 4), kTile, 0, s>>>(k, nc, cidx, m, fin, pts0, r2, orph);
+      // the grid over the survivors' box (the last pass's bounds cover them)
+      uint32_t hb[6];
+      CAPT_CUDA(cudaMemcpyAsync(hb, mnmx, sizeof(hb), cudaMemcpyDeviceToHost, s));
+      CAPT_CUDA(cudaStreamSynchronize(s));
+      OrphanGrid G;
+      double ext = 0.0;
+      for (int d = 0; d < 3; ++d) {
+        G.lo[d] = 0.0;
+        G.dims[d] = 1;
+      }
+      auto inv = [](uint32_t u) {
+        u = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+        float f;
+        std::memcpy(&f, &u, 4);
+        return double(f);
+      };
+      for (int d = 0; d < k; ++d) {
+        G.lo[d] = inv(hb[d]);
+        ext = std::max(ext, inv(hb[3 + d]) - G.lo[d]);
+      }
+      // cells of edge >= r (1 + 2^-20), at most ~2^8 per axis (keys fit in 32 bits)
+      const double cs = std::max(r_filter * (1.0 + std::ldexp(1.0, -20)), ext / 256.0);
+      G.inv_cs = cs > 0.0 ? 1.0 / cs : 0.0;
+      if (!(cs > 0.0) || !std::isfinite(G.inv_cs)) G.inv_cs = 0.0;  // (one bucket)
+      else
+        for (int d = 0; d < k; ++d)
+          G.dims[d] = int(std::min(258.0, std::floor((inv(hb[3 + d]) - G.lo[d]) / cs) + 2.0));
+      // 1/cs rounded: the bucket map stays monotone; cs' = 1/inv_cs >= r still
+      // holds up to a relative 2^-52, far inside the 2^-20 margin
+      uint32_t* skey = A.get<uint32_t>(m);
+      uint32_t* skeyS = A.get<uint32_t>(m);
+      int32_t* sval = A.get<int32_t>(m);
+      int32_t* svalS = A.get<int32_t>(m);
+      if (!skey || !skeyS || !sval || !svalS) return fail(CAPT_ENOMEM, "scratch allocation");
+      k_orphan_keys<<<grid_for(m, 256, 8), 256, 0, s>>>(k, G, m, fin, pts0, skey, sval);
+      size_t t = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, t, skey, skeyS, sval, svalS, m, 0, 32, s);
+      void* tmp2 = t <= tb_sort ? tmp : A.get<char>(t);
+      if (!tmp2) return fail(CAPT_ENOMEM, "scratch allocation");
+      CAPT_CUDA(cub::DeviceRadixSort::SortPairs(tmp2, t, skey, skeyS, sval, svalS, m, 0, 32, s));
+      k_orphans<<<grid_for(nc, 128, 8), 128, 0, s>>>(k, G, nc, cidx, m, skeyS, svalS, pts0, r2,
+                                                     orph);
       TRY(select_values(A, cidx, orph, nc, oidx, &no));
     }
   }
