@@ -246,60 +246,66 @@ __device__ __forceinline__ void put_slot(uint32_t* w, int j, int v) {
   w[j >> 1] = (j & 1) ? ((w[j >> 1] & 0xffffu) | (u << 16)) : ((w[j >> 1] & 0xffff0000u) | u);
 }
 
-// One CTA per bucket: every cell of the bucket against every point of the
-// 27 neighbouring buckets (points farther than rcap from a cell centre lie
-// outside them: bucket edge m*h >= rcap + 2h, see build_field), the
-// candidates staged through shared memory in chunks.  Per cell: the kCand + 1
-// nearest points by fp32 distance (candidates in bucket order: deterministic
-// on every replica) -> the K0 record {nearest point, nn} and the candidate
+// One CTA per tile of 8 x 8 x 4 cells (one cell per thread).  A point within
+// rcap of a cell centre lies within R = ceil(rcap / h) + 1 cells of the cell
+// on every axis (cell_of is monotone; the +1 covers its rounding), so the
+// tile's candidates are the points of the buckets (edge m cells) overlapping
+// the tile grown by R cells: for every (y, z) bucket row one contiguous range
+// of the bucket-sorted points, staged through shared memory in chunks.  Tiles
+// far from the cloud have no candidates.  Per cell: the kCand + 1 nearest
+// points by fp32 distance (candidates in a fixed order: deterministic on
+// every replica) -> the K0 record {nearest point, nn} and the candidate
 // record (the kCand nearest as int16 offsets from x0, the bound kd_q).
+constexpr int kTileX = 8, kTileY = 8, kTileZ = 4;
 __global__ void __launch_bounds__(256, 1) k_field_cand(FieldGeom g, BucketGrid b,
                                                     const uint32_t* __restrict__ bstart,
                                                     const float4* __restrict__ pts,
                                                     float4* __restrict__ field,
                                                     uint32_t* __restrict__ cand) {
   __shared__ float4 sp[kFieldChunk];
+  const int tx = (g.nx + kTileX - 1) / kTileX, ty = (g.ny + kTileY - 1) / kTileY;
   const int bid = blockIdx.x;
-  const int bx = bid % b.nbx, by = (bid / b.nbx) % b.nby, bz = bid / (b.nbx * b.nby);
-  const int x0 = bx * g.m, y0 = by * g.m, z0 = bz * g.m;
-  const int cx = min(g.m, g.nx - x0), cy = min(g.m, g.ny - y0), cz = min(g.m, g.nz - z0);
-  const int ncells = cx * cy * cz;
+  const int x0 = (bid % tx) * kTileX, y0 = ((bid / tx) % ty) * kTileY, z0 = (bid / (tx * ty)) * kTileZ;
+  const int lx = threadIdx.x % kTileX, ly = (threadIdx.x / kTileX) % kTileY,
+            lz = threadIdx.x / (kTileX * kTileY);
+  const bool live = x0 + lx < g.nx && y0 + ly < g.ny && z0 + lz < g.nz;
   const float INF = __int_as_float(0x7f800000);
-  for (int pass = 0; pass < ncells; pass += 256) {
-    const int j = pass + threadIdx.x;
-    const int lx = j % cx, ly = (j / cx) % cy, lz = j / (cx * cy);
-    const float px = centre_of(x0 + lx, g.h, g.c0[0]);
-    const float py = centre_of(y0 + ly, g.h, g.c0[1]);
-    const float pz = centre_of(z0 + lz, g.h, g.c0[2]);
-    float bd[kKP];
-    int bi[kKP];
+  const float px = centre_of(x0 + lx, g.h, g.c0[0]);
+  const float py = centre_of(y0 + ly, g.h, g.c0[1]);
+  const float pz = centre_of(z0 + lz, g.h, g.c0[2]);
+  float bd[kKP];
+  int bi[kKP];
 #pragma unroll
-    for (int i = 0; i < kKP; ++i) {
-      bd[i] = INF;
-      bi[i] = -1;
-    }
-    for (int nz = max(bz - 1, 0); nz <= min(bz + 1, b.nbz - 1); ++nz)
-      for (int ny = max(by - 1, 0); ny <= min(by + 1, b.nby - 1); ++ny)
-        for (int nx = max(bx - 1, 0); nx <= min(bx + 1, b.nbx - 1); ++nx) {
-          const int nbid = (nz * b.nby + ny) * b.nbx + nx;
-          const uint32_t s0 = bstart[nbid], s1 = bstart[nbid + 1];
-          for (uint32_t c0 = s0; c0 < s1; c0 += kFieldChunk) {
-            const int cnt = int(min(uint32_t(kFieldChunk), s1 - c0));
-            __syncthreads();
-            for (int i = threadIdx.x; i < cnt; i += 256) sp[i] = pts[c0 + i];
-            __syncthreads();
-            for (int i = 0; i < cnt; ++i) {
-              const float4 p = sp[i];
-              const float d2 = d2_fma(p.x - px, p.y - py, p.z - pz);
-              if (d2 < bd[kKP - 1]) knn_insert(bd, bi, d2, int(c0) + i);
-            }
-          }
+  for (int i = 0; i < kKP; ++i) {
+    bd[i] = INF;
+    bi[i] = -1;
+  }
+  const int R = g.rr;
+  const int bx0 = max(x0 - R, 0) / g.m, bx1 = min(x0 + kTileX - 1 + R, g.nx - 1) / g.m;
+  const int by0 = max(y0 - R, 0) / g.m, by1 = min(y0 + kTileY - 1 + R, g.ny - 1) / g.m;
+  const int bz0 = max(z0 - R, 0) / g.m, bz1 = min(z0 + kTileZ - 1 + R, g.nz - 1) / g.m;
+  for (int bz = bz0; bz <= bz1; ++bz)
+    for (int by = by0; by <= by1; ++by) {
+      const int row = (bz * b.nby + by) * b.nbx;
+      const uint32_t s0 = bstart[row + bx0], s1 = bstart[row + bx1 + 1];
+      for (uint32_t c0 = s0; c0 < s1; c0 += kFieldChunk) {
+        const int cnt = int(min(uint32_t(kFieldChunk), s1 - c0));
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt; i += 256) sp[i] = pts[c0 + i];
+        __syncthreads();
+        for (int i = 0; i < cnt; ++i) {
+          const float4 p = sp[i];
+          const float d2 = d2_fma(p.x - px, p.y - py, p.z - pz);
+          if (d2 < bd[kKP - 1]) knn_insert(bd, bi, d2, int(c0) + i);
         }
-    if (j >= ncells) continue;
+      }
+    }
+  {
+    if (!live) return;
     const int64_t cell = (int64_t(z0 + lz) * g.ny + (y0 + ly)) * g.nx + (x0 + lx);
     // fp32 |x0 - p|^2 has relative error < 5u, sqrtf one more u:
     // sqrtf(d2) (1 - 2^-19) (rounded) < the real distance.  Points outside
-    // the 27 buckets are farther than rcap: the bounds are capped there.
+    // the candidate buckets are farther than rcap: the bounds are capped there.
     auto lb = [&](int k) { return fminf(g.rcap, __fmul_rn(sqrtf(bd[k]), kNNShrink)); };
     // candidates: offsets (p - x0) / q_step rounded (exact in double: the
     // difference of two floats, a power-of-two scale), |offset| <= 32767;
@@ -1216,11 +1222,12 @@ int build_field(capt_tree* tree, cudaStream_t s) {
   g.nz = int(dims[2]);
   g.cells = dims[0] * dims[1] * dims[2];
   // stored bounds are capped at rcap >= r_max + h (> r_max + |c - x0| for a
-  // centre inside its cell); buckets of m cells with m h >= rcap + 2h: a
-  // point outside a centre's 27 neighbouring buckets is more than rcap away
-  // even when its computed cell index is off by one
+  // centre inside its cell); a point within rcap of a cell centre has its
+  // computed cell within ceil(rcap / h) + 1 cells of it per axis, + 1 more
+  // for the rounding of cell_of: rr; point buckets of m = 2 cells
   g.rcap = float(rmax + h);
-  g.m = int(std::ceil(double(g.rcap) / h)) + 2;
+  g.m = 2;
+  g.rr = int(std::ceil(double(g.rcap) / h)) + 2;
   // candidate offsets: int16 multiples of a power-of-two step covering rcap;
   // the decoded difference fl(fl(c - x0) - q step) is within, per axis,
   // step / 2 (offset rounding) + u |c - x0| + u |fl(c - x0) - q step| of
@@ -1317,7 +1324,11 @@ int build_field(capt_tree* tree, cudaStream_t s) {
   float4* field = reinterpret_cast<float4*>(mem);
   uint32_t* cand = reinterpret_cast<uint32_t*>(mem + off_cand);
   k_bucket_points<<<grid_for(n_fin, 256, 8), 256, 0, s>>>(t.rep, ids_out, n_fin, pts);
-  k_field_cand<<<int(b.nb), 256, 0, s>>>(g, b, bstart, pts, field, cand);
+  {
+    const int64_t tiles = int64_t((g.nx + kTileX - 1) / kTileX) * ((g.ny + kTileY - 1) / kTileY) *
+                          ((g.nz + kTileZ - 1) / kTileZ);
+    k_field_cand<<<int(tiles), 256, 0, s>>>(g, b, bstart, pts, field, cand);
+  }
   uint8_t* blk = reinterpret_cast<uint8_t*>(mem + off_blk);
   e = cudaMemsetAsync(blk, 0, size_t(g.bbytes), s);
   if (e == cudaSuccess) {

@@ -64,6 +64,7 @@ static_assert(sizeof(SlabHeader) <= 256, "header must fit its 256-B section");
 // lower bounds.  field == nullptr: no field (k < 3, or not built).
 struct FieldGeom {
   int nx, ny, nz, m;   // cells per axis; bucket edge in cells (build only)
+  int rr;              // candidate reach in cells (build only)
   float lo[3];         // grid origin: cell i spans lo + [i, i+1) h (cell_of)
   float c0[3];         // centre of cell 0: x0(i) = fma(i, h, c0) exactly, build and query
   float h, inv_h;
