@@ -488,7 +488,7 @@ def main():
     st_calls = ctypes.c_int64(0)
     _lib.check(lib.capt_stage_times(st_ms, ctypes.byref(st_calls)))
     lib.capt_stage_timing(0)
-    lc = (ctypes.c_uint32 * 2)()
+    lc = (ctypes.c_uint32 * 3)()
     have_lists = lib.capt_field_list_counts(ctypes.c_void_p(stream.cuda_stream), lc) == 0
 
     # ---- reference counters of the same batch from the device counter
@@ -527,17 +527,19 @@ def main():
                    "bound": "hbm", "algorithmic_bytes": bytes_step,
                    "achieved_gbs": roof["achieved"], "frac": roof["frac"]}]
         if have_lists:
-            n1, n2 = int(lc[0]), int(lc[1])
+            n1, n2, n3 = int(lc[0]), int(lc[1]), int(lc[2])
             mean_set = float(tree.stats().mean_affordance)
-            lbytes = n1 * (20 + 20 + CAND_RECORD_BYTES) + n2 * (20 + 12 * mean_set)
+            lbytes = n1 * (20 + 20 + CAND_RECORD_BYTES) + (n2 + n3) * 20 + \
+                n3 * 12 * mean_set
             stages.append({
-                "kernel": "k_list_knn + k_tree_list (list stage)", "ms": list_ms,
+                "kernel": "k_list_knn + k_bucket_list + k_tree_list (list stage)", "ms": list_ms,
                 "share_of_step": list_ms / ms_per_step, "bound": "hbm",
-                "entries": n1, "entries_tree_path": n2,
+                "entries": n1, "entries_bucket_scan": n2, "entries_tree_path": n3,
                 "algorithmic_bytes": lbytes,
                 "algorithmic_bytes_definition": "per entry: 20 B written by K0 + read back, "
-                                                "a 192-B candidate record; per tree-path entry "
-                                                "its sphere + the mean affordance set (12 B/pt)",
+                                                "a 192-B candidate record; per bucket-scan or "
+                                                "tree-path entry its sphere; per tree-path entry "
+                                                "the mean affordance set (12 B/pt)",
                 "achieved_gbs": lbytes / (list_ms * 1e-3) / 1e9,
                 "frac": lbytes / (list_ms * 1e-3) / 1e9 / hbm_peak,
                 "note": "latency-bound: a few thousand dependent record gathers per step"})

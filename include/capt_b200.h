@@ -204,8 +204,10 @@ int capt_stage_times(double* ms, int64_t* calls);
 /* List lengths of the last field-pipeline capt_query issued on `stream` on
  * the current device (measurement helper for the list stage's roofline):
  * out[0] = spheres K0 left undecided (the candidate-record list), out[1] =
- * entries the candidate records left open (the tree path).  Waits for the
- * stream.  CAPT_EINVAL if no field query ran on that stream. */
+ * open in-band entries resolved by the exact bucket scan, out[2] = entries
+ * taking the tree path (out-of-band radii with check_radii off, non-finite
+ * or out-of-grid centres).  out holds 3 values.  Waits for the stream.
+ * CAPT_EINVAL if no field query ran on that stream. */
 int capt_field_list_counts(void* stream, uint32_t* out);
 
 /* Number of kernels this library has launched in the process so far

@@ -28,13 +28,19 @@
 //
 // Kernels:
 //   build:  k_rep_box (cloud box), k_bucket_keys + radix sort (points into
-//           buckets of >= rcap), k_field_cand (one CTA per bucket: the
-//           kCand + 1 nearest points of every cell centre among the 27
-//           neighbouring buckets, staged through shared memory)
-//   query:  k_resolve      (K0: band check, grid certificates, lane groups,
-//                           bit words, the list with its spheres)
-//           k_list_knn     (candidate certificates; the open entries -> list 2)
-//           k_tree_list    (the tree path over list 2)
+//           buckets of 2 cells), k_field_cand (one CTA per 8x8x4-cell tile:
+//           the kCand + 1 nearest points of every cell centre among the
+//           points of the buckets the tile grown by rcap overlaps, staged
+//           through shared memory), k_block_table (per 8^3-cell block, a
+//           lower bound on the distance to the cloud)
+//   query:  k_resolve1 / k_resolve (K0: band check, block table, grid
+//                           certificates, lane groups, bit words, the list
+//                           with its spheres)
+//           k_list_knn     (candidate certificates; open in-band entries ->
+//                           list 2, the others -> list 3)
+//           k_bucket_list  (list 2: exact brute force over the points of the
+//                           buckets the sphere's box overlaps)
+//           k_tree_list    (list 3: the tree path, the reference's semantics)
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -686,8 +692,8 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
       const unsigned lk = __ballot_sync(0xffffffffu, look[v]);
       const unsigned bf = __ballot_sync(0xffffffffu, valid[v] && inband[v] && !skip && bfree);
       if ((threadIdx.x & 31) == 0) {
-        atomicAdd(a.list_n + 2, unsigned(__popc(lk)));
-        atomicAdd(a.list_n + 3, unsigned(__popc(bf)));
+        atomicAdd(a.list_n + 4, unsigned(__popc(lk)));
+        atomicAdd(a.list_n + 5, unsigned(__popc(bf)));
       }
     }
 #endif
@@ -859,7 +865,7 @@ __device__ __forceinline__ void resolve1(const FieldArgs& a, const FieldGeom& g,
 #ifdef CAPT_FIELD_STATS
     {
       const unsigned lk = __ballot_sync(0xffffffffu, look);
-      if (lane == 0) atomicAdd(a.list_n + 2, unsigned(__popc(lk)));
+      if (lane == 0) atomicAdd(a.list_n + 4, unsigned(__popc(lk)));
     }
 #endif
   }
@@ -987,7 +993,9 @@ __device__ __forceinline__ void ld_v8u(const uint32_t* p, uint32_t (&v)[8]) {
 }
 
 __global__ void __launch_bounds__(256) k_list_knn(FieldArgs a, uint32_t* __restrict__ list2,
-                                                  uint32_t* __restrict__ list2_n) {
+                                                  uint32_t* __restrict__ list2_n,
+                                                  uint32_t* __restrict__ list3,
+                                                  uint32_t* __restrict__ list3_n) {
   const DevTree& t = a.t;
   const FieldGeom& g = a.t.fg;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // K0's list is complete
@@ -1031,7 +1039,7 @@ __global__ void __launch_bounds__(256) k_list_knn(FieldArgs a, uint32_t* __restr
       const float RM = r * (1.0f + 0x1p-18f) + qe;
       const float lo = RH > 0.f ? RH * RH * (1.0f - 0x1p-20f) : -1.f;
       const float hi = RM * RM * (1.0f + 0x1p-20f);
-      bool amb = false;
+      bool amb = false;  // a candidate neither a definite hit nor a definite miss
 #pragma unroll
       for (int k = 0; k < kCand; ++k) {
         const uint32_t wx = w[k >> 1], wy = w[16 + (k >> 1)], wz = w[32 + (k >> 1)];
@@ -1054,13 +1062,103 @@ __global__ void __launch_bounds__(256) k_list_knn(FieldArgs a, uint32_t* __restr
       const uint32_t b = L == 1 ? q : q / uint32_t(L);
       atomicOr(a.bits + (b >> 5), 1u << (b & 31));
     }
-    const unsigned om = __ballot_sync(0xffffffffu, open);
-    if (om) {
+    // open entries: in band inside the grid -> the exact bucket scan
+    // (list 2); the rest (out-of-band radii with check_radii off, NaN,
+    // centres outside the grid) -> the tree path (list 3)
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned om2 = __ballot_sync(0xffffffffu, open && cert);
+    if (om2) {
       unsigned base = 0;
-      if (lane == 0) base = atomicAdd(list2_n, unsigned(__popc(om)));
+      if (lane == 0) base = atomicAdd(list2_n, unsigned(__popc(om2)));
       base = __shfl_sync(0xffffffffu, base, 0);
-      if (open) list2[base + __popc(om & ((1u << lane) - 1u))] = q;
+      if (open && cert) list2[base + __popc(om2 & lt)] = q;
     }
+    const unsigned om3 = __ballot_sync(0xffffffffu, open && !cert);
+    if (om3) {
+      unsigned base = 0;
+      if (lane == 0) base = atomicAdd(list3_n, unsigned(__popc(om3)));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (open && !cert) list3[base + __popc(om3 & lt)] = q;
+    }
+  }
+}
+
+// The list stage, part 2a (k_bucket_list): an open entry of list 2 has an
+// in-band radius and a centre inside the grid, so its verdict is the
+// brute-force one (DESIGN 3b): some cloud point with the reference's float64
+// ((dx^2 + dy^2) + dz^2) <= r*r.  Such a point lies within r (1 + 2^-20) of
+// c on every axis, so in the point buckets (edge m cells; cell_of monotone,
+// clamped) the box [c - r', c + r'] overlaps; one warp per entry scans those
+// buckets row by row (one contiguous range of the bucket-sorted points per
+// (y, z) bucket row), 32 points at a time, fp32 with the rows in the error
+// band re-tested in float64, and stops at the first hit.
+__global__ void __launch_bounds__(256) k_bucket_list(FieldArgs a, const uint32_t* __restrict__ list2,
+                                                     const uint32_t* __restrict__ list2_n) {
+  const DevTree& t = a.t;
+  const FieldGeom& g = a.t.fg;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const uint32_t n_list = *list2_n;
+  const int lane = threadIdx.x & 31;
+  const int L = a.L;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t e = warp; e < n_list; e += nwarps) {
+    const uint32_t q = list2[e];
+    const uint32_t b = L == 1 ? q : q / uint32_t(L);
+    if (L > 1 && (__ldcg(a.bits + (b >> 5)) >> (b & 31)) & 1u) continue;
+    const float4 s = make_float4(__ldg(a.c + 3 * size_t(q)), __ldg(a.c + 3 * size_t(q) + 1),
+                                 __ldg(a.c + 3 * size_t(q) + 2), __ldg(a.r + q));
+    const float r2 = s.w * s.w;
+    const float loB = r2 * (1.0f - kTau), hiB = r2 * (1.0f + kTau);
+    const float rp = s.w * (1.0f + 0x1p-20f);
+    const int bx0 = cell_of(s.x - rp, g.lo[0], g.inv_h, g.nx) / g.m;
+    const int bx1 = cell_of(s.x + rp, g.lo[0], g.inv_h, g.nx) / g.m;
+    const int by0 = cell_of(s.y - rp, g.lo[1], g.inv_h, g.ny) / g.m;
+    const int by1 = cell_of(s.y + rp, g.lo[1], g.inv_h, g.ny) / g.m;
+    const int bz0 = cell_of(s.z - rp, g.lo[2], g.inv_h, g.nz) / g.m;
+    const int bz1 = cell_of(s.z + rp, g.lo[2], g.inv_h, g.nz) / g.m;
+    // the (y, z) bucket rows, 32 at a time: lane l reads row l's point
+    // range, a warp scan flattens the ranges, and the warp then tests 32
+    // points per step wherever they lie (a point's row by a binary search
+    // over the lanes' inclusive offsets)
+    const int ny_rows = by1 - by0 + 1, rows = ny_rows * (bz1 - bz0 + 1);
+    bool verdict = false;
+    for (int r0 = 0; r0 < rows && !verdict; r0 += 32) {
+      uint32_t i0 = 0, len = 0;
+      if (r0 + lane < rows) {
+        const int by = by0 + (r0 + lane) % ny_rows, bz = bz0 + (r0 + lane) / ny_rows;
+        const int row = (bz * g.nby + by) * g.nbx;
+        i0 = __ldg(t.bstart + row + bx0);
+        len = __ldg(t.bstart + row + bx1 + 1) - i0;
+      }
+      uint32_t incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      for (uint32_t k0 = 0; k0 < total && !verdict; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        // the first lane whose inclusive offset exceeds k holds k's row
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step; step >>= 1) {
+          const uint32_t v = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+          if (v <= k) lo += step;
+        }
+        const uint32_t base = __shfl_sync(0xffffffffu, i0, lo);
+        const uint32_t excl = __shfl_sync(0xffffffffu, incl - len, lo);
+        bool hit = false;
+        if (k < total) {
+          const float4 p = __ldg(t.cpts + base + (k - excl));
+          const float d2 = d2_fma(s.x - p.x, s.y - p.y, s.z - p.z);
+          hit = d2 <= loB || (d2 < hiB && hit_f64(s.x, s.y, s.z, s.w, p));
+        }
+        verdict = __any_sync(0xffffffffu, hit);
+      }
+    }
+    if (verdict && lane == 0) atomicOr(a.bits + (b >> 5), 1u << (b & 31));
   }
 }
 
@@ -1074,12 +1172,13 @@ __global__ void __launch_bounds__(256) k_list_knn(FieldArgs a, uint32_t* __restr
 // 128-bit loads in flight per lane), fp32 with the rows in the error band
 // re-tested in float64 on the spot; spheres outside the fast path
 // (non-finite, extreme radii) take the exact float64 scan.
-__global__ void __launch_bounds__(256) k_tree_list(FieldArgs a) {
+__global__ void __launch_bounds__(256) k_tree_list(FieldArgs a, const uint32_t* __restrict__ list3,
+                                                   const uint32_t* __restrict__ list3_n) {
   const DevTree& t = a.t;
   // launched with programmatic stream serialisation: scheduled while part 1
   // drains, reads its list only after it has completed
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const uint32_t n_list = *a.list_n;
+  const uint32_t n_list = *list3_n;
   const int lane = threadIdx.x & 31;
   const int L = a.L;
   const bool prefilter = a.flags & CAPT_PREFILTER;
@@ -1087,7 +1186,7 @@ __global__ void __launch_bounds__(256) k_tree_list(FieldArgs a) {
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t e = warp; e < n_list; e += nwarps) {
-    const uint32_t q = a.list[e];
+    const uint32_t q = list3[e];
     const uint32_t b = L == 1 ? q : q / uint32_t(L);
     // (a lane group already resolved by another entry: nothing to add)
     if (L > 1 && (__ldcg(a.bits + (b >> 5)) >> (b & 31)) & 1u) continue;
@@ -1163,6 +1262,8 @@ int build_field(capt_tree* tree, cudaStream_t s) {
     tree->field = nullptr;
     tree->cand = nullptr;
     tree->blk = nullptr;
+    tree->cpts = nullptr;
+    tree->bstart = nullptr;
   }
   if (tree->h.k != 3) return CAPT_OK;
   const DevTree t = view(tree);
@@ -1279,8 +1380,6 @@ int build_field(capt_tree* tree, cudaStream_t s) {
   uint32_t n_fin = 0;
   CAPT_CUDA(cudaMemcpyAsync(&n_fin, bstart + b.nb, 4, cudaMemcpyDeviceToHost, s));
   CAPT_CUDA(cudaStreamSynchronize(s));
-  float4* pts = nullptr;
-  CAPT_CUDA(get(&pts, std::max<uint32_t>(n_fin, 1)));
   // block table: the smallest blocks whose table fits CAPT_BLK_BYTES; bstep
   // the power of two covering rcap in 255 steps; rcell bounds |c - x0| for a
   // centre c whose computed cell is x0's: per axis t = fma(c, inv_h, nc0)
@@ -1314,20 +1413,34 @@ int build_field(capt_tree* tree, cudaStream_t s) {
   }
   const float rcell = std::nextafter(
       float(std::sqrt(3.0) * (0.5 * double(g.h) + mu) * (1.0 + std::ldexp(1.0, -20))), INFINITY);
-  // one allocation: K0 records | candidate records | block table
-  const size_t off_cand = (2 * sizeof(float4) * size_t(g.cells) + 255) & ~size_t(255);  // (32-B loads)
-  const size_t off_blk = off_cand + ((sizeof(uint32_t) * kCandWords * size_t(g.cells) + 255) & ~size_t(255));
-  const size_t bytes = off_blk + size_t(g.bbytes);
+  // one allocation: K0 records | candidate records | block table | the
+  // points in bucket order | the bucket starts (the list stage's exact scan)
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t off_cand = al(2 * sizeof(float4) * size_t(g.cells));  // (32-B loads)
+  const size_t off_blk = off_cand + al(sizeof(uint32_t) * kCandWords * size_t(g.cells));
+  const size_t off_cpts = off_blk + al(size_t(g.bbytes));
+  const size_t off_bst = off_cpts + al(sizeof(float4) * std::max<size_t>(n_fin, 1));
+  const size_t bytes = off_bst + sizeof(uint32_t) * size_t(b.nb + 2);
   char* mem = nullptr;
   cudaError_t e = cudaMalloc(&mem, bytes);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(clearance field)");
   float4* field = reinterpret_cast<float4*>(mem);
   uint32_t* cand = reinterpret_cast<uint32_t*>(mem + off_cand);
-  k_bucket_points<<<grid_for(n_fin, 256, 8), 256, 0, s>>>(t.rep, ids_out, n_fin, pts);
+  float4* cpts = reinterpret_cast<float4*>(mem + off_cpts);
+  uint32_t* bst = reinterpret_cast<uint32_t*>(mem + off_bst);
+  g.nbx = b.nbx;
+  g.nby = b.nby;
+  g.nbz = b.nbz;
+  e = cudaMemcpyAsync(bst, bstart, sizeof(uint32_t) * size_t(b.nb + 2), cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) {
+    cudaFree(mem);
+    return cuda_fail(e, "clearance field build");
+  }
+  k_bucket_points<<<grid_for(n_fin, 256, 8), 256, 0, s>>>(t.rep, ids_out, n_fin, cpts);
   {
     const int64_t tiles = int64_t((g.nx + kTileX - 1) / kTileX) * ((g.ny + kTileY - 1) / kTileY) *
                           ((g.nz + kTileZ - 1) / kTileZ);
-    k_field_cand<<<int(tiles), 256, 0, s>>>(g, b, bstart, pts, field, cand);
+    k_field_cand<<<int(tiles), 256, 0, s>>>(g, b, bstart, cpts, field, cand);
   }
   uint8_t* blk = reinterpret_cast<uint8_t*>(mem + off_blk);
   e = cudaMemsetAsync(blk, 0, size_t(g.bbytes), s);
@@ -1347,6 +1460,8 @@ int build_field(capt_tree* tree, cudaStream_t s) {
   tree->field = field;
   tree->cand = cand;
   tree->blk = blk;
+  tree->cpts = cpts;
+  tree->bstart = bst;
   tree->fg = g;
   return CAPT_OK;
 }
@@ -1459,14 +1574,18 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
     sc->buf = nullptr;
     sc->cap = 0;
     const int64_t cap = (n + 3) & ~int64_t(3);
-    CAPT_CUDA(dmalloc(&sc->buf, 6 * size_t(cap) + 8, s));
+    CAPT_CUDA(dmalloc(&sc->buf, 7 * size_t(cap) + 8, s));
     sc->cap = cap;
   }
+  // counters: list_n (K0's list), list2_n (the bucket scan), list3_n (the
+  // tree path); lists: list | list2 | list_s (4 words) | list3
   a.list_n = sc->buf;
   a.list = sc->buf + 8;
   uint32_t* const list2_n = sc->buf + 1;
+  uint32_t* const list3_n = sc->buf + 2;
   uint32_t* const list2 = sc->buf + 8 + sc->cap;
   a.list_s = reinterpret_cast<float4*>(sc->buf + 8 + 2 * sc->cap);
+  uint32_t* const list3 = sc->buf + 8 + 6 * sc->cap;
   {
     const int64_t zw = L >= 8 ? n_words : 0;
     k_field_zero<<<grid_for(zw + 8, 256, 4), 256, 0, s>>>(a.list_n, bits, zw);
@@ -1499,27 +1618,27 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
     if (rc) return rc;
   }
   // the list stage: persistent grids (the list lengths are known on the device only)
-  CAPT_CUDA(launch_pdl_f(k_list_knn, grid_for(n, 256, 8), 256, 0, s, a, list2, list2_n));
-  FieldArgs a2 = a;
-  a2.list = list2;
-  a2.list_s = nullptr;
-  a2.list_n = list2_n;
-  CAPT_CUDA(launch_pdl_f(k_tree_list, grid_for(int64_t(n) * 32, 256, 8), 256, 0, s, a2));
+  CAPT_CUDA(launch_pdl_f(k_list_knn, grid_for(n, 256, 8), 256, 0, s, a, list2, list2_n, list3,
+                         list3_n));
+  CAPT_CUDA(launch_pdl_f(k_bucket_list, grid_for(int64_t(n) * 32, 256, 8), 256, 0, s, a,
+                         static_cast<const uint32_t*>(list2), static_cast<const uint32_t*>(list2_n)));
+  CAPT_CUDA(launch_pdl_f(k_tree_list, grid_for(int64_t(n) * 32, 256, 8), 256, 0, s, a,
+                         static_cast<const uint32_t*>(list3), static_cast<const uint32_t*>(list3_n)));
   CAPT_CUDA(cudaGetLastError());
-  note_launches(2);
+  note_launches(3);
   if (tcall >= 0) {
     const int rc = stage_record(dev, tcall, 2, s);
     if (rc) return rc;
   }
 #ifdef CAPT_FIELD_STATS  // diagnostics build (build_ext -D CAPT_FIELD_STATS --out ...)
-  uint32_t nl[4] = {0, 0, 0, 0};
-  CAPT_CUDA(cudaMemcpyAsync(nl, a.list_n, 16, cudaMemcpyDeviceToHost, s));
+  uint32_t nl[6] = {0, 0, 0, 0, 0, 0};
+  CAPT_CUDA(cudaMemcpyAsync(nl, a.list_n, 24, cudaMemcpyDeviceToHost, s));
   CAPT_CUDA(cudaStreamSynchronize(s));
   fprintf(stderr,
-          "[capt field] n=%lld L=%d list=%u (%.4f%%) tree path=%u (%.5f%%) records=%u (%.3f) "
-          "block-free=%u (%.3f)\n",
-          (long long)n, L, nl[0], 100.0 * nl[0] / double(n), nl[1], 100.0 * nl[1] / double(n),
-          nl[2], nl[2] / double(n), nl[3], nl[3] / double(n));
+          "[capt field] n=%lld L=%d list=%u (%.4f%%) bucket scan=%u tree path=%u records=%u "
+          "(%.3f) block-free=%u (%.3f)\n",
+          (long long)n, L, nl[0], 100.0 * nl[0] / double(n), nl[1], nl[2], nl[4],
+          nl[4] / double(n), nl[5], nl[5] / double(n));
 #endif
   return CAPT_OK;
 }
@@ -1619,11 +1738,12 @@ extern "C" int capt_field_list_counts(void* stream, uint32_t* out) {
   if (!sc) return fail(CAPT_EINVAL, "no field query on this stream");
   std::lock_guard<std::mutex> lk(sc->mu);
   if (!sc->buf) return fail(CAPT_EINVAL, "no field query on this stream");
-  uint32_t h[2] = {0, 0};
+  uint32_t h[3] = {0, 0, 0};
   CAPT_CUDA(cudaMemcpyAsync(h, sc->buf, sizeof(h), cudaMemcpyDeviceToHost, s));
   CAPT_CUDA(cudaStreamSynchronize(s));
   out[0] = h[0];
   out[1] = h[1];
+  out[2] = h[2];
   return CAPT_OK;
 }
 

@@ -63,8 +63,9 @@ static_assert(sizeof(SlabHeader) <= 256, "header must fit its 256-B section");
 // blo/bhi = the cloud's box (finite representatives); rcap caps the stored
 // lower bounds.  field == nullptr: no field (k < 3, or not built).
 struct FieldGeom {
-  int nx, ny, nz, m;   // cells per axis; bucket edge in cells (build only)
+  int nx, ny, nz, m;   // cells per axis; point-bucket edge in cells
   int rr;              // candidate reach in cells (build only)
+  int nbx, nby, nbz;   // point buckets per axis (the list stage's exact scan)
   float lo[3];         // grid origin: cell i spans lo + [i, i+1) h (cell_of)
   float c0[3];         // centre of cell 0: x0(i) = fma(i, h, c0) exactly, build and query
   float h, inv_h;
@@ -112,6 +113,8 @@ struct DevTree {
   const float4* field;    // per cell: witness xyz + lower bound nn
   const uint32_t* cand;   // per cell: kCandWords words (candidate record, see kCand)
   const uint8_t* blk;     // block table (FieldGeom::bshift ...)
+  const float4* cpts;     // the cloud's finite points (the field's bucket order)
+  const uint32_t* bstart; // per point bucket (x fastest): first index into cpts; nb + 1
   FieldGeom fg;
 };
 
@@ -128,6 +131,8 @@ struct capt_tree {
   float4* field = nullptr;
   uint32_t* cand = nullptr;
   uint8_t* blk = nullptr;
+  float4* cpts = nullptr;
+  uint32_t* bstart = nullptr;
   capt::FieldGeom fg{};
 };
 
@@ -171,6 +176,8 @@ inline DevTree view(const capt_tree* t) {
   d.field = t->field;
   d.cand = t->cand;
   d.blk = t->blk;
+  d.cpts = t->cpts;
+  d.bstart = t->bstart;
   d.fg = t->fg;
   return d;
 }
