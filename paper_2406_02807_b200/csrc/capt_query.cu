@@ -22,8 +22,10 @@
 // __dadd_rn/__dmul_rn), so verdicts are bit-identical to the reference.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <type_traits>
 #include <vector>
 
@@ -646,7 +648,40 @@ struct PipeState {
   cudaStream_t w[2] = {nullptr, nullptr};
   cudaEvent_t start = nullptr, done[2] = {nullptr, nullptr};
   unsigned long long* pinned = nullptr;  // per chunk: first_bad + 6 counters
+  // pageable inputs: two pinned staging buffers (centres + radii + mask of
+  // one chunk each), filled by host threads while the other one's copy and
+  // kernels run; staged[b] is recorded after the copy out of buffer b
+  char* stage[2] = {nullptr, nullptr};
+  size_t stage_bytes = 0;
+  cudaEvent_t staged[2] = {nullptr, nullptr};
 };
+
+// memcpy with up to `threads` host threads (pageable -> pinned staging)
+static void parallel_copy(char* dst, const char* src, size_t bytes, int threads) {
+  constexpr size_t kMinPerThread = size_t(8) << 20;
+  const int t = int(std::min<size_t>(threads, std::max<size_t>(1, bytes / kMinPerThread)));
+  if (t <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  const size_t per = (bytes + t - 1) / t;
+  for (int i = 1; i < t; ++i) {
+    const size_t a = per * i, b = std::min(bytes, a + per);
+    if (a < b) th.emplace_back([=] { std::memcpy(dst + a, src + a, b - a); });
+  }
+  std::memcpy(dst, src, std::min(per, bytes));
+  for (auto& x : th) x.join();
+}
+
+static bool is_pageable(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();  // (clear the sticky-free error of a plain host pointer)
+    return true;
+  }
+  return at.type == cudaMemoryTypeUnregistered;
+}
 
 struct PipePool {
   std::mutex mu;
@@ -740,6 +775,26 @@ int query_host_pipelined(const capt_tree* tree, const DevTree& t, const void* ce
     if (lane_mask) CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&call.m[i]), chunk, w));
     CAPT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&call.aux[i]), 8 * 7, w));
   }
+  // pageable (plain malloc'd / numpy) inputs go through pinned staging
+  // buffers filled by host threads: a pageable cudaMemcpyAsync is staged by
+  // the driver one thread at a time and blocks the calling thread
+  const bool pageable = is_pageable(centers) || is_pageable(radii) ||
+                        (lane_mask && is_pageable(lane_mask));
+  const size_t cb = in_elem * t.k * size_t(chunk), rb = in_elem * size_t(chunk);
+  const size_t need = cb + rb + (lane_mask ? size_t(chunk) : 0);
+  const int nthreads = int(std::min(8u, std::max(1u, std::thread::hardware_concurrency() / 2)));
+  if (pageable && p->stage_bytes < need) {
+    for (int i = 0; i < 2; ++i) {
+      if (p->stage[i]) cudaFreeHost(p->stage[i]);
+      p->stage[i] = nullptr;
+    }
+    p->stage_bytes = 0;
+    for (int i = 0; i < 2; ++i) {
+      CAPT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p->stage[i]), need, cudaHostAllocDefault));
+      if (!p->staged[i]) CAPT_CUDA(cudaEventCreateWithFlags(&p->staged[i], cudaEventDisableTiming));
+    }
+    p->stage_bytes = need;
+  }
   for (int64_t ci = 0; ci < n_chunks; ++ci) {
     const int b = int(ci & 1);
     cudaStream_t w = p->w[b];
@@ -747,10 +802,23 @@ int query_host_pipelined(const capt_tree* tree, const DevTree& t, const void* ce
     const int64_t len = n - base < chunk ? n - base : chunk;
     const char* hc = static_cast<const char*>(centers) + in_elem * t.k * base;
     const char* hr = static_cast<const char*>(radii) + in_elem * base;
+    const uint8_t* hm = lane_mask ? lane_mask + base : nullptr;
+    if (pageable) {
+      // (buffer b's previous copy to the device has completed)
+      CAPT_CUDA(cudaEventSynchronize(p->staged[b]));
+      char* st = p->stage[b];
+      parallel_copy(st, hc, in_elem * t.k * len, nthreads);
+      parallel_copy(st + cb, hr, in_elem * len, nthreads);
+      if (hm) std::memcpy(st + cb + rb, hm, size_t(len));
+      hc = st;
+      hr = st + cb;
+      if (hm) hm = reinterpret_cast<const uint8_t*>(st + cb + rb);
+    }
     CAPT_CUDA(cudaMemcpyAsync(call.c[b], hc, in_elem * t.k * len, cudaMemcpyHostToDevice, w));
     CAPT_CUDA(cudaMemcpyAsync(call.r[b], hr, in_elem * len, cudaMemcpyHostToDevice, w));
     if (lane_mask)
-      CAPT_CUDA(cudaMemcpyAsync(call.m[b], lane_mask + base, len, cudaMemcpyHostToDevice, w));
+      CAPT_CUDA(cudaMemcpyAsync(call.m[b], hm, len, cudaMemcpyHostToDevice, w));
+    if (pageable) CAPT_CUDA(cudaEventRecord(p->staged[b], w));
     const int rc = query_device(t, call.c[b], call.r[b], len, L, lane_mask ? call.m[b] : nullptr,
                                flags, call.d_bits + base / L / 32, call.aux[b] + 1, call.aux[b], w);
     if (rc) return rc;
