@@ -1092,20 +1092,33 @@ __global__ void __launch_bounds__(256) k_list_knn(FieldArgs a, uint32_t* __restr
 // buckets row by row (one contiguous range of the bucket-sorted points per
 // (y, z) bucket row), 32 points at a time, fp32 with the rows in the error
 // band re-tested in float64, and stops at the first hit.
-__global__ void __launch_bounds__(256) k_bucket_list(FieldArgs a, const uint32_t* __restrict__ list2,
-                                                     const uint32_t* __restrict__ list2_n) {
+#ifndef CAPT_BUCKET_WARPS
+#define CAPT_BUCKET_WARPS 4
+#endif
+constexpr int kBucketWarps = CAPT_BUCKET_WARPS;  // warps per entry (one CTA)
+__global__ void __launch_bounds__(32 * kBucketWarps) k_bucket_list(
+    FieldArgs a, const uint32_t* __restrict__ list2, const uint32_t* __restrict__ list2_n) {
   const DevTree& t = a.t;
   const FieldGeom& g = a.t.fg;
+  __shared__ volatile int s_hit;
+  __shared__ int s_skip;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t n_list = *list2_n;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int L = a.L;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t e = warp; e < n_list; e += nwarps) {
+  for (uint32_t e = blockIdx.x; e < n_list; e += gridDim.x) {
     const uint32_t q = list2[e];
     const uint32_t b = L == 1 ? q : q / uint32_t(L);
-    if (L > 1 && (__ldcg(a.bits + (b >> 5)) >> (b & 31)) & 1u) continue;
+    if (threadIdx.x == 0) {
+      s_hit = 0;
+      // (a lane group already resolved by another entry: nothing to add)
+      s_skip = L > 1 && ((__ldcg(a.bits + (b >> 5)) >> (b & 31)) & 1u);
+    }
+    __syncthreads();
+    if (s_skip) {
+      __syncthreads();
+      continue;
+    }
     const float4 s = make_float4(__ldg(a.c + 3 * size_t(q)), __ldg(a.c + 3 * size_t(q) + 1),
                                  __ldg(a.c + 3 * size_t(q) + 2), __ldg(a.r + q));
     const float r2 = s.w * s.w;
@@ -1118,12 +1131,14 @@ __global__ void __launch_bounds__(256) k_bucket_list(FieldArgs a, const uint32_t
     const int bz0 = cell_of(s.z - rp, g.lo[2], g.inv_h, g.nz) / g.m;
     const int bz1 = cell_of(s.z + rp, g.lo[2], g.inv_h, g.nz) / g.m;
     // the (y, z) bucket rows, 32 at a time: lane l reads row l's point
-    // range, a warp scan flattens the ranges, and the warp then tests 32
-    // points per step wherever they lie (a point's row by a binary search
-    // over the lanes' inclusive offsets)
+    // range, a warp scan flattens the ranges, and the CTA's warps then test
+    // 32 points per step each, interleaved, wherever they lie (a point's row
+    // by a binary search over the lanes' inclusive offsets), until one warp
+    // finds a hit
     const int ny_rows = by1 - by0 + 1, rows = ny_rows * (bz1 - bz0 + 1);
-    bool verdict = false;
-    for (int r0 = 0; r0 < rows && !verdict; r0 += 32) {
+    // (every exit test is warp-uniform: lane 0's read of the flag)
+    auto stop = [&]() { return __shfl_sync(0xffffffffu, int(s_hit), 0) != 0; };
+    for (int r0 = 0; r0 < rows && !stop(); r0 += 32) {
       uint32_t i0 = 0, len = 0;
       if (r0 + lane < rows) {
         const int by = by0 + (r0 + lane) % ny_rows, bz = bz0 + (r0 + lane) / ny_rows;
@@ -1138,9 +1153,8 @@ __global__ void __launch_bounds__(256) k_bucket_list(FieldArgs a, const uint32_t
         if (lane >= o) incl += u;
       }
       const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      for (uint32_t k0 = 0; k0 < total && !verdict; k0 += 32) {
+      for (uint32_t k0 = 32u * wid; k0 < total && !stop(); k0 += 32u * kBucketWarps) {
         const uint32_t k = k0 + lane;
-        // the first lane whose inclusive offset exceeds k holds k's row
         int lo = 0;
 #pragma unroll
         for (int step = 16; step; step >>= 1) {
@@ -1155,10 +1169,12 @@ __global__ void __launch_bounds__(256) k_bucket_list(FieldArgs a, const uint32_t
           const float d2 = d2_fma(s.x - p.x, s.y - p.y, s.z - p.z);
           hit = d2 <= loB || (d2 < hiB && hit_f64(s.x, s.y, s.z, s.w, p));
         }
-        verdict = __any_sync(0xffffffffu, hit);
+        if (__any_sync(0xffffffffu, hit) && lane == 0) s_hit = 1;
+        __syncwarp();
       }
     }
-    if (verdict && lane == 0) atomicOr(a.bits + (b >> 5), 1u << (b & 31));
+    __syncthreads();
+    if (threadIdx.x == 0 && s_hit) atomicOr(a.bits + (b >> 5), 1u << (b & 31));
   }
 }
 
@@ -1620,8 +1636,9 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   // the list stage: persistent grids (the list lengths are known on the device only)
   CAPT_CUDA(launch_pdl_f(k_list_knn, grid_for(n, 256, 8), 256, 0, s, a, list2, list2_n, list3,
                          list3_n));
-  CAPT_CUDA(launch_pdl_f(k_bucket_list, grid_for(int64_t(n) * 32, 256, 8), 256, 0, s, a,
-                         static_cast<const uint32_t*>(list2), static_cast<const uint32_t*>(list2_n)));
+  CAPT_CUDA(launch_pdl_f(k_bucket_list, grid_for(int64_t(n) * 32 * kBucketWarps, 32 * kBucketWarps, 16),
+                         32 * kBucketWarps, 0, s, a, static_cast<const uint32_t*>(list2),
+                         static_cast<const uint32_t*>(list2_n)));
   CAPT_CUDA(launch_pdl_f(k_tree_list, grid_for(int64_t(n) * 32, 256, 8), 256, 0, s, a,
                          static_cast<const uint32_t*>(list3), static_cast<const uint32_t*>(list3_n)));
   CAPT_CUDA(cudaGetLastError());
