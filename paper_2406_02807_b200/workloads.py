@@ -23,7 +23,7 @@ import numpy as np
 __all__ = ["CONFIGS", "f32_band", "clamp_radii", "cfg0_cloud", "cfg0_queries",
            "tabletop_scene", "cfg1_cloud", "cfg1_queries", "cfg2_raw_cloud",
            "cfg2_queries", "cfg3_cloud", "cfg3_queries", "cfg4_queries",
-           "uniform_queries"]
+           "uniform_queries", "room_cloud", "room_queries"]
 
 
 @dataclass(frozen=True)
@@ -274,3 +274,42 @@ def cfg4_queries(cloud: np.ndarray, n: int, rate: float, seed: int = 104,
             c[todo[good]] = cand[good]
             todo = todo[~good]
     return c, r, label
+
+
+# --------------------------------------------------------------------------
+# room-scale stress case (not a BASELINE config): the clearance field's cell
+# edge grows with the scene, so this covers the regime where a fixed cell
+# budget would leave cells wider than r_min
+# --------------------------------------------------------------------------
+
+def room_cloud(n: int = 200000, seed: int = 7, size=(8.0, 8.0, 3.0), n_boxes: int = 40,
+               noise: float = 0.002) -> np.ndarray:
+    """Points on the floor, walls and ceiling of a size[0] x size[1] x size[2]
+    room plus n_boxes furniture boxes on the floor, area-weighted, N(0, noise)."""
+    rng = np.random.default_rng(seed)
+    X, Y, Z = size
+    rects = [(np.array([0.0, 0, 0]), np.array([X, 0, 0.0]), np.array([0, Y, 0.0])),
+             (np.array([0.0, 0, Z]), np.array([X, 0, 0.0]), np.array([0, Y, 0.0])),
+             (np.array([0.0, 0, 0]), np.array([X, 0, 0.0]), np.array([0, 0, Z])),
+             (np.array([0.0, Y, 0]), np.array([X, 0, 0.0]), np.array([0, 0, Z])),
+             (np.array([0.0, 0, 0]), np.array([0, Y, 0.0]), np.array([0, 0, Z])),
+             (np.array([X, 0, 0.0]), np.array([0, Y, 0.0]), np.array([0, 0, Z]))]
+    sides = rng.uniform(0.3, 1.5, size=(n_boxes, 3))
+    lo = np.stack([rng.uniform(0, X - sides[:, 0]), rng.uniform(0, Y - sides[:, 1]),
+                   np.zeros(n_boxes)], 1)
+    for l, d in zip(lo, sides):
+        ex, ey, ez = np.diag(d)
+        rects += [(l + ez, ex, ey), (l, ex, ez), (l + ey, ex, ez), (l, ey, ez), (l + ex, ey, ez)]
+    areas = np.array([np.linalg.norm(np.cross(u, v)) for _, u, v in rects])
+    counts = rng.multinomial(n, areas / areas.sum())
+    chunks = [o + rng.uniform(size=(m, 1)) * u + rng.uniform(size=(m, 1)) * v
+              for (o, u, v), m in zip(rects, counts) if m]
+    pts = np.concatenate(chunks, 0) + rng.normal(0.0, noise, size=(n, 3))
+    return pts.astype(np.float32)
+
+
+def room_queries(cloud: np.ndarray, n: int = 16 << 20, seed: int = 8, r_min: float = 0.01,
+                 r_max: float = 0.08):
+    rng = np.random.default_rng(seed)
+    return uniform_queries(rng, n, cloud.min(0).astype(np.float64),
+                           cloud.max(0).astype(np.float64), r_min, r_max)

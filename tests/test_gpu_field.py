@@ -380,3 +380,18 @@ def test_field_unaligned_inputs_and_f64_exact():
     exp = O.collides_many(t, cu, ru)
     assert np.array_equal(q(tree, cu, ru), exp)
     assert np.array_equal(P.collides_many(tree, cu.astype(np.float64), ru.astype(np.float64)), exp)
+
+
+def test_field_room_scale_cells_wider_than_r_min():
+    # an 8 x 8 x 3 m room: the ~2 M-cell field has cells of 4.8 cm, wider
+    # than r_min = 1 cm, so the certificates decide less and more spheres
+    # take the list stage (candidate records, bucket scan); verdicts stay
+    # the reference's
+    cloud = W.room_cloud(n=100000, seed=9)
+    tree = P.construct(P.PointCloud(cloud), P.BuildParams(0.01, 0.08))
+    f = tree.clearance_field()
+    assert f["h"] > 0.01
+    t = O.construct(cloud, 0.01, 0.08)
+    c, r = W.room_queries(cloud, n=1 << 20, seed=10)
+    assert np.array_equal(q(tree, c, r, mode=0), O.collides_many(t, c, r))
+    assert np.array_equal(q(tree, c, r, 8, mode=0), O.collides_groups(t, c, r, 8))
