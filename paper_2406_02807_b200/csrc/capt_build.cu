@@ -16,8 +16,8 @@
 //      float64 point-box distance is monotone under cell inclusion, so a point
 //      afforded by the leaf cell survives every ancestor's filter
 //      (tree.py:209-218).  Candidates come from a uniform grid of point
-//      buckets (edge >= r_max): one warp per leaf scans the buckets its cell
-//      grown by r_max overlaps, then the exact float64 test of
+//      buckets (edge >= r_max / 2): one warp per leaf scans the buckets its
+//      cell grown by r_max overlaps, then the exact float64 test of
 //      tree.py:209-213 decides membership;
 //   5. count pass -> exclusive scan -> fill pass into the padded slab layout.
 #include <cub/cub.cuh>

@@ -1188,27 +1188,16 @@ __global__ void __launch_bounds__(32 * kBucketWarps) k_bucket_list(
 // 128-bit loads in flight per lane), fp32 with the rows in the error band
 // re-tested in float64 on the spot; spheres outside the fast path
 // (non-finite, extreme radii) take the exact float64 scan.
-__global__ void __launch_bounds__(256) k_tree_list(FieldArgs a, const uint32_t* __restrict__ list3,
-                                                   const uint32_t* __restrict__ list3_n) {
+// The tree path for one sphere (warp-cooperative; the reference's semantics,
+// query.py:184-219): descent, probe record (conservative fp16 AABB,
+// representative), set scan 512 rows per step with band rows re-tested in
+// float64 inline; spheres outside the fast path (non-finite, extreme radii)
+// take the exact float64 scan.
+__device__ __forceinline__ bool tree_verdict(const FieldArgs& a, const float (&c)[3], float r,
+                                          int lane) {
   const DevTree& t = a.t;
-  // launched with programmatic stream serialisation: scheduled while part 1
-  // drains, reads its list only after it has completed
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  const uint32_t n_list = *list3_n;
-  const int lane = threadIdx.x & 31;
-  const int L = a.L;
   const bool prefilter = a.flags & CAPT_PREFILTER;
   const float band_lo = 1.0f - kTau, band_hi = 1.0f + kTau;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t e = warp; e < n_list; e += nwarps) {
-    const uint32_t q = list3[e];
-    const uint32_t b = L == 1 ? q : q / uint32_t(L);
-    // (a lane group already resolved by another entry: nothing to add)
-    if (L > 1 && (__ldcg(a.bits + (b >> 5)) >> (b & 31)) & 1u) continue;
-    const float c[3] = {__ldg(a.c + 3 * size_t(q)), __ldg(a.c + 3 * size_t(q) + 1),
-                        __ldg(a.c + 3 * size_t(q) + 2)};
-    const float r = __ldg(a.r + q);
     const int leaf = int(warp_descend<float>(t, c, lane));
     const float r2 = r * r;
     const bool cfin = isfinite(c[0]) && isfinite(c[1]) && isfinite(c[2]);
@@ -1224,7 +1213,7 @@ __global__ void __launch_bounds__(256) k_tree_list(FieldArgs a, const uint32_t* 
       const float rz = fmaxf(fmaxf(l2h0.x - c[2], 0.f), c[2] - h12.y);
       if (d2_fma(rx, ry, rz) > r2 * band_hi) st = 0;
     }
-    if (st == 0) continue;
+    if (st == 0) return false;
     const float loB = r2 * band_lo, hiB = r2 * band_hi;
     bool verdict = st == 2 && d2_fma(c[0] - pr[0], c[1] - pr[1], c[2] - pr[2]) <= loB;
     const uint2 set = __ldg(t.set + leaf);
@@ -1263,7 +1252,216 @@ __global__ void __launch_bounds__(256) k_tree_list(FieldArgs a, const uint32_t* 
       const double c64[3] = {double(c[0]), double(c[1]), double(c[2])};
       verdict = warp_scan_f64(t, set, c64, double(r), lane);
     }
+  return verdict;
+}
+
+__global__ void __launch_bounds__(256) k_tree_list(FieldArgs a, const uint32_t* __restrict__ list3,
+                                                   const uint32_t* __restrict__ list3_n) {
+  // launched with programmatic stream serialisation: scheduled while part 1
+  // drains, reads its list only after it has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const uint32_t n_list = *list3_n;
+  const int lane = threadIdx.x & 31;
+  const int L = a.L;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t e = warp; e < n_list; e += nwarps) {
+    const uint32_t q = list3[e];
+    const uint32_t b = L == 1 ? q : q / uint32_t(L);
+    // (a lane group already resolved by another entry: nothing to add)
+    if (L > 1 && (__ldcg(a.bits + (b >> 5)) >> (b & 31)) & 1u) continue;
+    const float c[3] = {__ldg(a.c + 3 * size_t(q)), __ldg(a.c + 3 * size_t(q) + 1),
+                        __ldg(a.c + 3 * size_t(q) + 2)};
+    const bool verdict = tree_verdict(a, c, __ldg(a.r + q), lane);
     if (verdict && lane == 0) atomicOr(a.bits + (b >> 5), 1u << (b & 31));
+  }
+}
+
+// ---------------------------------------------------------------- small batches
+//
+// One kernel for batches below kSmallBatch spheres: the fixed cost of the
+// pipeline above (zero kernel, K0, three list kernels) is most of a small
+// call.  A warp takes 32 lane groups (32 L spheres, one verdict word) at a
+// time, 32 spheres per sub-step, one per lane: K0's certificates (band,
+// block table, witness, Lipschitz); each sphere they leave open -- in a
+// group without a hit -- is then resolved by the whole warp, one at a time:
+// its cell's candidate record (lane k decodes candidate k), then the exact
+// bucket scan (in band, inside the grid) or the tree path (the rest).  The
+// verdict word is written whole (no zeroing, no atomics).
+
+// Candidate record of the sphere's cell, one candidate per lane: 1 = a
+// certified hit, 0 = certified free, 2 = open (the k_list_knn tests).
+__device__ __forceinline__ int cand_verdict_warp(const DevTree& t, float x, float y, float z,
+                                                 float r, int lane) {
+  const FieldGeom& g = t.fg;
+  float fx, fy, fz;
+  const int ix = qcell(x, g.inv_h, g.nc0[0], fx);
+  const int iy = qcell(y, g.inv_h, g.nc0[1], fy);
+  const int iz = qcell(z, g.inv_h, g.nc0[2], fz);
+  const unsigned cell =
+      (unsigned(iz) * unsigned(g.ny) + unsigned(iy)) * unsigned(g.nx) + unsigned(ix);
+  const uint32_t* rec = t.cand + size_t(cell) * kCandWords;
+  const float qs = g.q_step, qe = g.q_err * (1.0f + 0x1p-17f);
+  const float ex = x - __fmaf_rn(fx, g.h, g.c0[0]);
+  const float ey = y - __fmaf_rn(fy, g.h, g.c0[1]);
+  const float ez = z - __fmaf_rn(fz, g.h, g.c0[2]);
+  const float RH = r * (1.0f - 0x1p-18f) - qe;
+  const float RM = r * (1.0f + 0x1p-18f) + qe;
+  const float lo = RH > 0.f ? RH * RH * (1.0f - 0x1p-20f) : -1.f;
+  const float hi = RM * RM * (1.0f + 0x1p-20f);
+  bool hit = false, amb = false;
+  if (lane < kCand) {
+    const int k = lane;
+    const uint32_t wx = __ldg(rec + (k >> 1)), wy = __ldg(rec + 16 + (k >> 1)),
+                   wz = __ldg(rec + 32 + (k >> 1));
+    const int ox = (k & 1) ? slot_hi(wx) : slot_lo(wx);
+    const int oy = (k & 1) ? slot_hi(wy) : slot_lo(wy);
+    const int oz = (k & 1) ? slot_hi(wz) : slot_lo(wz);
+    const float vx = fmaf(-float(ox), qs, ex), vy = fmaf(-float(oy), qs, ey),
+                vz = fmaf(-float(oz), qs, ez);
+    const float S = d2_fma(vx, vy, vz);
+    const bool used = ox != kCandNone;
+    hit = used && S <= lo;
+    amb = used && S < hi;
+  }
+  if (__any_sync(0xffffffffu, hit)) return 1;
+  const float kd = float(slot_hi(__ldg(rec + 15))) * qs;  // (x slot 31: kd_q, exact)
+  const float A = kd - r * kK1;
+  const bool free = !__any_sync(0xffffffffu, amb) && A > 0.f && A * A > d2_fma(ex, ey, ez) * kK1;
+  return free ? 0 : 2;
+}
+
+// The exact bucket scan of k_bucket_list with one warp.
+__device__ __forceinline__ bool bucket_verdict_warp(const DevTree& t, float4 s, int lane) {
+  const FieldGeom& g = t.fg;
+  const float r2 = s.w * s.w;
+  const float loB = r2 * (1.0f - kTau), hiB = r2 * (1.0f + kTau);
+  const float rp = s.w * (1.0f + 0x1p-20f);
+  const int bx0 = cell_of(s.x - rp, g.lo[0], g.inv_h, g.nx) / g.m;
+  const int bx1 = cell_of(s.x + rp, g.lo[0], g.inv_h, g.nx) / g.m;
+  const int by0 = cell_of(s.y - rp, g.lo[1], g.inv_h, g.ny) / g.m;
+  const int by1 = cell_of(s.y + rp, g.lo[1], g.inv_h, g.ny) / g.m;
+  const int bz0 = cell_of(s.z - rp, g.lo[2], g.inv_h, g.nz) / g.m;
+  const int bz1 = cell_of(s.z + rp, g.lo[2], g.inv_h, g.nz) / g.m;
+  const int ny_rows = by1 - by0 + 1, rows = ny_rows * (bz1 - bz0 + 1);
+  bool verdict = false;
+  for (int r0 = 0; r0 < rows && !verdict; r0 += 32) {
+    uint32_t i0 = 0, len = 0;
+    if (r0 + lane < rows) {
+      const int by = by0 + (r0 + lane) % ny_rows, bz = bz0 + (r0 + lane) / ny_rows;
+      const int row = (bz * g.nby + by) * g.nbx;
+      i0 = __ldg(t.bstart + row + bx0);
+      len = __ldg(t.bstart + row + bx1 + 1) - i0;
+    }
+    uint32_t incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    for (uint32_t k0 = 0; k0 < total && !verdict; k0 += 32) {
+      const uint32_t k = k0 + lane;
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const uint32_t v = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+        if (v <= k) lo += step;
+      }
+      const uint32_t base = __shfl_sync(0xffffffffu, i0, lo);
+      const uint32_t excl = __shfl_sync(0xffffffffu, incl - len, lo);
+      bool hit = false;
+      if (k < total) {
+        const float4 p = __ldg(t.cpts + base + (k - excl));
+        const float d2 = d2_fma(s.x - p.x, s.y - p.y, s.z - p.z);
+        hit = d2 <= loB || (d2 < hiB && hit_f64(s.x, s.y, s.z, s.w, p));
+      }
+      verdict = __any_sync(0xffffffffu, hit);
+    }
+  }
+  return verdict;
+}
+
+__global__ void __launch_bounds__(256) k_resolve_small(FieldArgs a) {
+  const DevTree& t = a.t;
+  const FieldGeom g = t.fg;
+  const uint8_t* sblk = stage_block_table(g, t.blk);
+  const bool check = a.flags & CAPT_CHECK_RADII;
+  const int lane = threadIdx.x & 31;
+  const int L = a.L;
+  const int64_t n = a.n, n_groups = n / L, n_words = (n_groups + 31) / 32;
+  const uint64_t pol = l2_keep_policy();
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t wi = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; wi < n_words;
+       wi += nw) {
+    unsigned word = 0u;
+    for (int sub = 0; sub < L; ++sub) {
+      const int64_t q = wi * 32 * L + sub * 32 + lane;
+      const int gb = (sub * 32 + lane) / L;  // this lane's group bit in the word
+      const bool valid = q < n && (!a.mask || a.mask[q]);
+      float x = 0.f, y = 0.f, z = 0.f, r = 0.f;
+      if (q < n) {
+        x = __ldg(a.c + 3 * q);
+        y = __ldg(a.c + 3 * q + 1);
+        z = __ldg(a.c + 3 * q + 2);
+        r = __ldg(a.r + q);
+      }
+      const bool inb = valid && r >= a.rlo_f && r <= a.rhi_f;
+      const bool bad = check && valid && !inb && r == r;
+      if (bad) atomicMin(a.first_bad, static_cast<unsigned long long>(q));
+      float fx, fy, fz;
+      const int ix = qcell(x, g.inv_h, g.nc0[0], fx);
+      const int iy = qcell(y, g.inv_h, g.nc0[1], fy);
+      const int iz = qcell(z, g.inv_h, g.nc0[2], fz);
+      const bool in = unsigned(ix) < unsigned(g.nx) && unsigned(iy) < unsigned(g.ny) &&
+                      unsigned(iz) < unsigned(g.nz);
+      const bool look = inb && in && !block_free(g, sblk, ix, iy, iz, in, r * kK1);
+      float4 rec = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (look)
+        rec = ldg_keep(t.field + ((unsigned(iz) * unsigned(g.ny) + unsigned(iy)) *
+                                      unsigned(g.nx) + unsigned(ix)), pol);
+      const float r2 = r * r;
+      const float dw = d2_fma(x - rec.x, y - rec.y, z - rec.z);
+      const bool hit = look && dw <= r2 * (1.0f - kTau);
+      const float A = rec.w - r * kK1;
+      const float e2 = d2_fma(x - __fmaf_rn(fx, g.h, g.c0[0]), y - __fmaf_rn(fy, g.h, g.c0[1]),
+                              z - __fmaf_rn(fz, g.h, g.c0[2]));
+      const bool free = dw > r2 * (1.0f + kTau) && A > 0.f && A * A > e2 * kK1;
+      // decided: in band and (no record needed, witness hit, Lipschitz free);
+      // an out-of-band radius with check_radii only reports first_bad
+      const bool open = valid && !bad && !(inb && (!look || hit || free));
+      // this sub-step's group bits with a hit
+      const unsigned hb = __ballot_sync(0xffffffffu, hit);
+      if (L == 1) {
+        word |= hb;
+      } else {
+        const int per = 32 / L;  // (L <= 32) groups of this sub-step
+        const unsigned lm = L == 32 ? 0xffffffffu : ((1u << L) - 1u);
+        for (int j = 0; j < per; ++j)
+          if ((hb >> (j * L)) & lm) word |= 1u << (sub * per + j);
+      }
+      // the open spheres of groups without a hit, one at a time by the warp
+      unsigned um = __ballot_sync(0xffffffffu, open && !((word >> gb) & 1u));
+      while (um) {
+        const int u = __ffs(int(um)) - 1;
+        um &= um - 1u;
+        const int ub = __shfl_sync(0xffffffffu, gb, u);
+        if ((word >> ub) & 1u) continue;  // (its group got a hit meanwhile)
+        const float ux = __shfl_sync(0xffffffffu, x, u), uy = __shfl_sync(0xffffffffu, y, u),
+                    uz = __shfl_sync(0xffffffffu, z, u), ur = __shfl_sync(0xffffffffu, r, u);
+        const bool ucert = __shfl_sync(0xffffffffu, int(inb && in), u) != 0;
+        bool v;
+        if (ucert) {
+          const int cv = cand_verdict_warp(t, ux, uy, uz, ur, lane);
+          v = cv == 1 || (cv == 2 && bucket_verdict_warp(t, make_float4(ux, uy, uz, ur), lane));
+        } else {
+          const float cu[3] = {ux, uy, uz};
+          v = tree_verdict(a, cu, ur, lane);
+        }
+        if (v) word |= 1u << ub;
+      }
+    }
+    if (lane == 0) a.bits[wi] = word;
   }
 }
 
@@ -1482,7 +1680,11 @@ int build_field(capt_tree* tree, cudaStream_t s) {
   return CAPT_OK;
 }
 
-constexpr int64_t kFieldMinBatch = 8192;
+// below this many spheres (auto mode) one fused kernel (k_resolve_small)
+// beats the pipeline's fixed cost
+#ifndef CAPT_SMALL_BATCH
+#define CAPT_SMALL_BATCH (int64_t(1) << 20)
+#endif
 
 bool field_eligible(const DevTree& t, int64_t n, uint32_t flags) {
   if (!t.field || t.k != 3 || (flags & (CAPT_INPUT_F64 | CAPT_STATS))) return false;
@@ -1490,8 +1692,6 @@ bool field_eligible(const DevTree& t, int64_t n, uint32_t flags) {
   // fp32 r^2 of every in-band radius must stay normal and finite
   if (!(t.r_min >= 0x1p-50) || !(t.r_max <= 0x1p50)) return false;
   if (flags & CAPT_MODE_FIELD) return true;
-  // below a few thousand spheres the one-kernel warp path has less fixed cost
-  if (n < kFieldMinBatch) return false;
   return !(flags & (CAPT_MODE_DIRECT | CAPT_MODE_BINNED | CAPT_MODE_THREAD | CAPT_MODE_WARP));
 }
 
@@ -1580,6 +1780,13 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   if (double(hi) > t.r_max) hi = nextafterf(hi, -INFINITY);
   a.rlo_f = lo;
   a.rhi_f = hi;
+  if (n < CAPT_SMALL_BATCH && !(flags & CAPT_MODE_FIELD)) {
+    const int64_t nwd = (n / L + 31) / 32;
+    k_resolve_small<<<grid_for(nwd * 32, 256, 8), 256, 0, s>>>(a);
+    CAPT_CUDA(cudaGetLastError());
+    note_launches(1);
+    return CAPT_OK;
+  }
   int dev = 0;
   CAPT_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= kMaxDevices) return fail(CAPT_ECUDA, "device index out of range");

@@ -351,8 +351,8 @@ def test_stage_timing_abi():
     ms = (ctypes.c_double * 3)()
     calls = ctypes.c_int64(0)
     assert L.capt_stage_timing(1) == 0
-    for _ in range(3):
-        P.query_bits(tree, cd, rd, 1)
+    for _ in range(3):  # (forced: below 1 M spheres auto mode takes the fused small kernel)
+        P.query_bits(tree, cd, rd, 1, mode=FIELD)
     torch.cuda.synchronize()
     assert L.capt_stage_times(ms, ctypes.byref(calls)) == 0
     assert calls.value == 3
@@ -360,7 +360,7 @@ def test_stage_timing_abi():
     # the record is cleared by the read; disabled timing records nothing
     assert L.capt_stage_times(ms, ctypes.byref(calls)) == 0 and calls.value == 0
     assert L.capt_stage_timing(0) == 0
-    P.query_bits(tree, cd, rd, 1)
+    P.query_bits(tree, cd, rd, 1, mode=FIELD)
     torch.cuda.synchronize()
     assert L.capt_stage_times(ms, ctypes.byref(calls)) == 0 and calls.value == 0
     exp = O.collides_many(golden_tree(z, ""), c, r)
@@ -395,3 +395,34 @@ def test_field_room_scale_cells_wider_than_r_min():
     c, r = W.room_queries(cloud, n=1 << 20, seed=10)
     assert np.array_equal(q(tree, c, r, mode=0), O.collides_many(t, c, r))
     assert np.array_equal(q(tree, c, r, 8, mode=0), O.collides_groups(t, c, r, 8))
+
+
+@pytest.mark.parametrize("L", [1, 2, 8, 32])
+def test_small_batch_fused_kernel(L):
+    # batches below CAPT_SMALL_BATCH take one fused kernel (k_resolve_small):
+    # K0's certificates, then per open sphere the candidate record, the
+    # bucket scan or the tree path, whole verdict words; sizes with partial
+    # last words, lane masks, out-of-band and non-finite spheres (check_radii
+    # off: the reference's semantics), the first bad radius (check_radii on)
+    cloud = W.cfg1_cloud()
+    t = O.construct(cloud, 0.02, 0.08)
+    tree = upload(t)
+    rng = np.random.default_rng(100 + L)
+    for groups in (1, 3, 37, 1000, 8191):
+        c, r = W.cfg1_queries(cloud, n_groups=groups, lane_width=L, seed=groups)
+        c = c.copy()
+        r = r.copy()
+        k = len(r)
+        if k > 16:
+            c[3, 0] = np.nan
+            c[5, 1] = np.inf
+            r[7] = 0.5        # out of band
+            r[11] = np.nan
+        exp = O.collides_groups(t, c, r, L)
+        assert np.array_equal(q(tree, c, r, L, mode=0), exp), groups
+        m = (rng.uniform(size=k) > 0.3).astype(np.uint8)
+        assert np.array_equal(q(tree, c, r, L, m, mode=0),
+                              O.collides_groups(t, c, r, L, m.astype(bool))), groups
+        if k > 16:
+            bits, bad = q(tree, c, r, L, check=True, mode=0)
+            assert bad == 7
