@@ -26,6 +26,8 @@
 #include <cmath>
 #include <cstring>
 
+#include <cuda_fp16.h>
+
 #include "capt_internal.cuh"
 
 #ifndef CAPT_BUCKET_SCALE
@@ -228,24 +230,49 @@ __device__ __forceinline__ void warp_afforded(const BuildView& v, const Buckets&
     b0[d] = bucket_of(B, d, __dsub_rn(double(c.lo[d]), rp));
     b1[d] = bucket_of(B, d, __dadd_rn(double(c.hi[d]), rp));
   }
-  for (int bz = b0[2]; bz <= b1[2]; ++bz)
-    for (int by = b0[1]; by <= b1[1]; ++by) {
+  // the (y, z) bucket rows, 32 at a time: lane l reads row l's point range,
+  // a warp scan flattens the ranges, and the warp tests 32 candidates per
+  // step wherever they lie (a candidate's row by a binary search over the
+  // lanes' inclusive offsets) -- rows of a few points keep the lanes busy;
+  // the order (rows, then sorted points) is fixed
+  const int ny_rows = b1[1] - b0[1] + 1, rows = ny_rows * (b1[2] - b0[2] + 1);
+  for (int r0 = 0; r0 < rows; r0 += 32) {
+    uint32_t i0 = 0, len = 0;
+    if (r0 + lane < rows) {
+      const int by = b0[1] + (r0 + lane) % ny_rows, bz = b0[2] + (r0 + lane) / ny_rows;
       const uint32_t row = (uint32_t(bz) * uint32_t(B.dims[1]) + uint32_t(by)) * uint32_t(B.dims[0]);
-      const uint32_t i0 = __ldg(B.start + row + b0[0]), i1 = __ldg(B.start + row + b1[0] + 1);
-      for (uint32_t i = i0; i < i1; i += 32) {
-        const uint32_t ii = i + lane;
-        bool hit = false;
-        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (ii < i1) {
-          q = __ldg(B.pts + ii);
-          if (__float_as_int(q.w) != self && cell_near32(v.k, q, c, v.r2_hi)) {
-            const double pq[3] = {double(q.x), double(q.y), double(q.z)};
-            hit = dist_cell64(v.k, pq, c) <= v.r_max_sq;
-          }
-        }
-        visit(hit, q);
-      }
+      i0 = __ldg(B.start + row + b0[0]);
+      len = __ldg(B.start + row + b1[0] + 1) - i0;
     }
+    uint32_t incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    for (uint32_t k0 = 0; k0 < total; k0 += 32) {
+      const uint32_t k = k0 + lane;
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const uint32_t w = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+        if (w <= k) lo += step;
+      }
+      const uint32_t base = __shfl_sync(0xffffffffu, i0, lo);
+      const uint32_t excl = __shfl_sync(0xffffffffu, incl - len, lo);
+      bool hit = false;
+      float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (k < total) {
+        q = __ldg(B.pts + base + (k - excl));
+        if (__float_as_int(q.w) != self && cell_near32(v.k, q, c, v.r2_hi)) {
+          const double pq[3] = {double(q.x), double(q.y), double(q.z)};
+          hit = dist_cell64(v.k, pq, c) <= v.r_max_sq;
+        }
+      }
+      visit(hit, q);
+    }
+  }
 }
 
 __global__ void __launch_bounds__(256) k_count_b(BuildView v, Buckets B,
@@ -267,7 +294,10 @@ __global__ void __launch_bounds__(256) k_count_b(BuildView v, Buckets B,
 __global__ void __launch_bounds__(256) k_fill_b(BuildView v, Buckets B,
                                                 const uint2* __restrict__ set,
                                                 float4* __restrict__ data,
-                                                float4* __restrict__ box) {
+                                                float4* __restrict__ box,
+                                                float4* __restrict__ org,
+                                                float4* __restrict__ rep,
+                                                float* __restrict__ probe) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const float INF = __int_as_float(0x7f800000);
@@ -281,6 +311,14 @@ __global__ void __launch_bounds__(256) k_fill_b(BuildView v, Buckets B,
     float rx[3] = {0.f, 0.f, 0.f};
     for (int d = 0; d < v.k; ++d) rx[d] = p < v.n0 ? v.X[d * v.n + p] : INF;
     float blo[3] = {rx[0], rx[1], rx[2]}, bhi[3] = {rx[0], rx[1], rx[2]};
+    // the finite rows' box (the origin of the binned scan; a padding leaf's
+    // +inf row is left out, as in k_origins)
+    const bool rfin = p < v.n0;
+    float flo[3], fhi[3];
+    for (int d = 0; d < 3; ++d) {
+      flo[d] = rfin ? rx[d] : INF;
+      fhi[d] = rfin ? rx[d] : -INF;
+    }
     if (lane < 3) dst[lane * m4] = rx[lane];
     uint32_t w = 1;
     if (st.y > 1)
@@ -293,6 +331,8 @@ __global__ void __launch_bounds__(256) k_fill_b(BuildView v, Buckets B,
             dst[d * m4 + at] = d < v.k ? qv[d] : 0.f;
             blo[d] = fminf(blo[d], qv[d]);
             bhi[d] = fmaxf(bhi[d], qv[d]);
+            flo[d] = fminf(flo[d], qv[d]);
+            fhi[d] = fmaxf(fhi[d], qv[d]);
           }
         }
         w += __popc(b);
@@ -300,16 +340,36 @@ __global__ void __launch_bounds__(256) k_fill_b(BuildView v, Buckets B,
     // padding rows (+inf), unused axes 0
     for (uint32_t i = st.y + lane; i < m4; i += 32)
       for (int d = 0; d < 3; ++d) dst[d * m4 + i] = d < v.k ? INF : 0.f;
+    float o[3], bb = 0.f;
     for (int d = 0; d < 3; ++d) {
-      for (int o = 16; o; o >>= 1) {
-        blo[d] = fminf(blo[d], __shfl_xor_sync(0xffffffffu, blo[d], o));
-        bhi[d] = fmaxf(bhi[d], __shfl_xor_sync(0xffffffffu, bhi[d], o));
+      for (int s = 16; s; s >>= 1) {
+        blo[d] = fminf(blo[d], __shfl_xor_sync(0xffffffffu, blo[d], s));
+        bhi[d] = fmaxf(bhi[d], __shfl_xor_sync(0xffffffffu, bhi[d], s));
+        flo[d] = fminf(flo[d], __shfl_xor_sync(0xffffffffu, flo[d], s));
+        fhi[d] = fmaxf(fhi[d], __shfl_xor_sync(0xffffffffu, fhi[d], s));
       }
       if (d >= v.k) blo[d] = bhi[d] = 0.f;
+      // origin = the finite box's centre; org.w >= max |p - o|^2 (the
+      // farthest corner of the finite box, rounded up): the binned scan's
+      // error band only needs an upper bound
+      o[d] = flo[d] <= fhi[d] ? 0.5f * flo[d] + 0.5f * fhi[d] : 0.f;
+      const float e =
+          flo[d] <= fhi[d] ? fmaxf(__fsub_ru(fhi[d], o[d]), __fsub_ru(o[d], flo[d])) : 0.f;
+      bb = __fmaf_ru(e, e, bb);
     }
     if (lane == 0) {
       box[2 * j] = make_float4(blo[0], blo[1], blo[2], 0.f);
       box[2 * j + 1] = make_float4(bhi[0], bhi[1], bhi[2], 0.f);
+      org[j] = make_float4(o[0], o[1], o[2], __fmul_ru(bb, 1.0f + 0x1p-20f));
+      const float4 rp = make_float4(rx[0], rx[1], rx[2], 0.f);
+      rep[j] = rp;
+      const __half2 h0 = __halves2half2(__float2half_rd(blo[0]), __float2half_rd(blo[1]));
+      const __half2 h1 = __halves2half2(__float2half_rd(blo[2]), __float2half_ru(bhi[0]));
+      const __half2 h2 = __halves2half2(__float2half_ru(bhi[1]), __float2half_ru(bhi[2]));
+      float4* pr = reinterpret_cast<float4*>(probe + 8 * j);
+      pr[0] = make_float4(rp.x, rp.y, rp.z, __uint_as_float(*reinterpret_cast<const unsigned*>(&h0)));
+      pr[1] = make_float4(__uint_as_float(*reinterpret_cast<const unsigned*>(&h1)),
+                          __uint_as_float(*reinterpret_cast<const unsigned*>(&h2)), 0.f, 0.f);
     }
   }
 }
@@ -591,10 +651,11 @@ extern "C" int capt_tree_build(int device, int k, const float* points, int64_t n
   if (e == cudaSuccess) {
     k_set_layout<<<G, 256, 0, s>>>(n, sizes, f4x, offx, const_cast<uint2*>(dv.set),
                                    const_cast<int64_t*>(dv.offs));
-    k_fill_b<<<grid_for(n * 32, 256, 8), 256, 0, s>>>(v, B, dv.set, const_cast<float4*>(dv.data),
-                                                      const_cast<float4*>(dv.box));
+    k_fill_b<<<grid_for(n * 32, 256, 8), 256, 0, s>>>(
+        v, B, dv.set, const_cast<float4*>(dv.data), const_cast<float4*>(dv.box),
+        const_cast<float4*>(dv.org), const_cast<float4*>(dv.rep), const_cast<float*>(dv.probe));
     e = cudaGetLastError();
-    if (e == cudaSuccess && compute_origins(dv, s)) e = cudaErrorLaunchFailure;
+    if (e == cudaSuccess && compute_origins(dv, s, false)) e = cudaErrorLaunchFailure;
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) {

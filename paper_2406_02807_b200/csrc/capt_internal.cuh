@@ -218,7 +218,10 @@ inline int depth_of(int64_t n) {
 }
 
 // Fill the org, rep, order and probe sections of a slab whose data is final.
-int compute_origins(const DevTree& t, cudaStream_t s);
+// Per-leaf derived sections (org, rep, probe, order) of a slab whose sets
+// and boxes are final; with_origins = false when the build already wrote
+// org, rep and probe (k_fill_b) and only the order remains.
+int compute_origins(const DevTree& t, cudaStream_t s, bool with_origins = true);
 
 int alloc_slab(capt_tree** out, int device, SlabHeader h);
 

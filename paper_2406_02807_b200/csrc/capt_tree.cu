@@ -190,9 +190,11 @@ __global__ void k_order_keys(DevTree t, uint32_t* keys, int* ids) {
   }
 }
 
-int compute_origins(const DevTree& t, cudaStream_t s) {
-  k_origins<<<grid_for(t.n * 32, 256), 256, 0, s>>>(t);
-  CAPT_CUDA(cudaGetLastError());
+int compute_origins(const DevTree& t, cudaStream_t s, bool with_origins) {
+  if (with_origins) {
+    k_origins<<<grid_for(t.n * 32, 256), 256, 0, s>>>(t);
+    CAPT_CUDA(cudaGetLastError());
+  }
   // leaves by descending set size (stable: equal sizes keep leaf order)
   uint32_t *keys = nullptr, *keys_out = nullptr;
   int* ids = nullptr;

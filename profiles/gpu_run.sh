@@ -32,7 +32,7 @@ if [[ " $what " == *" ncu "* ]]; then
         --log-file $out/${tag}_cfg${c}_launches.csv $cmd > $out/${tag}_ncu_launch_cfg$c.log 2>&1
     $cmd > $out/${tag}_plain2_cfg$c.log 2>&1 && \
     ncu --set full --clock-control none --import-source on \
-        -k regex:"k_resolve|k_list_knn|k_bucket_list|k_tree_list" -s 6 -c 3 \
+        -k regex:"k_resolve|k_list_knn|k_bucket_list|k_tree_list" -s 8 -c 4 \
         -o $out/${tag}_cfg${c}_full $cmd > $out/${tag}_ncu_full_cfg$c.log 2>&1
   done
   cmd="python bench.py --config 2 --no-parity --no-cpu-baseline --e2e-steps 0 --steps 3 --warmup 3"
