@@ -1269,7 +1269,8 @@ __global__ void __launch_bounds__(256) k_tree_list(FieldArgs a, const uint32_t* 
     const uint32_t q = list3[e];
     const uint32_t b = L == 1 ? q : q / uint32_t(L);
     // (a lane group already resolved by another entry: nothing to add)
-    if (L > 1 && (__ldcg(a.bits + (b >> 5)) >> (b & 31)) & 1u) continue;
+    // (warp-uniform: lane 0's read decides for the warp)
+    if (L > 1 && __shfl_sync(0xffffffffu, (__ldcg(a.bits + (b >> 5)) >> (b & 31)) & 1u, 0)) continue;
     const float c[3] = {__ldg(a.c + 3 * size_t(q)), __ldg(a.c + 3 * size_t(q) + 1),
                         __ldg(a.c + 3 * size_t(q) + 2)};
     const bool verdict = tree_verdict(a, c, __ldg(a.r + q), lane);

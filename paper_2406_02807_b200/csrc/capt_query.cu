@@ -562,7 +562,8 @@ __global__ void __launch_bounds__(kBlock) k_list_f64(DevTree t, const double* __
     // (query.py:194-197: a NaN radius is not flagged)
     if (check && lane == 0 && (r64 < t.r_min || r64 > t.r_max))
       atomicMin(first_bad, static_cast<unsigned long long>(q));
-    if (L > 1 && ((__ldcg(bits + (g >> 5)) >> (g & 31)) & 1u)) continue;
+    // (warp-uniform: lane 0's read decides for the warp)
+    if (L > 1 && __shfl_sync(0xffffffffu, (__ldcg(bits + (g >> 5)) >> (g & 31)) & 1u, 0)) continue;
     const int64_t leaf = warp_descend<double>(t, c64, lane);
     const uint2 set = __ldg(t.set + leaf);
     float cx, cy, cz, r2, loB, hiB;
