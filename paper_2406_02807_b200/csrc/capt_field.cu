@@ -659,7 +659,7 @@ __device__ __forceinline__ void emit_chunk(const FieldArgs& a, int ch, int lane,
 // Decide one chunk (see above): writes its bits and list entries.  LT: the
 // lane width when known at compile time (0: a.L at run time); kFull: a whole
 // unmasked chunk (no per-sphere validity test).
-template <bool kMask, int LT, bool kFull>
+template <bool kMask, int LT, bool kFull, bool kBand = false>
 __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeom& g,
                                               const uint8_t* sblk, const Chunk& k, int ch,
                                               int lane, bool check, uint64_t pol, Ring& rg) {
@@ -679,7 +679,7 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
   auto cell = [&](int v, bool skip) {
     valid[v] = kFull || q0 + v < n;
     if (kMask) valid[v] = valid[v] && a.mask[valid[v] ? q0 + v : 0] != 0;
-    inband[v] = r[v] >= a.rlo_f && r[v] <= a.rhi_f;
+    inband[v] = kBand || (r[v] >= a.rlo_f && r[v] <= a.rhi_f);
     ix[v] = qcell(x[v], g.inv_h, g.nc0[0], fx[v]);
     iy[v] = qcell(y[v], g.inv_h, g.nc0[1], fy[v]);
     iz[v] = qcell(z[v], g.inv_h, g.nc0[2], fz[v]);
@@ -723,7 +723,7 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
     hitb |= unsigned(look[v] && hit) << v;
     // decided: in-band and (outside the grid / skipped, or certified); with
     // check_radii an out-of-band (non-NaN) radius only reports first_bad
-    const bool bad = check && valid[v] && (r[v] < a.rlo_f || r[v] > a.rhi_f);
+    const bool bad = !kBand && check && valid[v] && (r[v] < a.rlo_f || r[v] > a.rhi_f);
     badb |= unsigned(bad) << v;
     const bool decided = inband[v] && (!look[v] || hit || free);
     undb |= unsigned(valid[v] && !decided && !bad) << v;
@@ -761,7 +761,18 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
 #pragma unroll
     for (int v = 0; v < 4; ++v) cert(v);
   }
-  emit_chunk<LT>(a, ch, lane, check, hitb, undb, badb, elig, x, y, z, r, rg);
+  emit_chunk<LT>(a, ch, lane, check && !kBand, hitb, undb, badb, elig, x, y, z, r, rg);
+}
+
+// every radius of the chunk inside the band (warp-uniform; NaN is not)
+__device__ __forceinline__ bool chunk_in_band(const FieldArgs& a, float r0, float r1, float r2,
+                                              float r3) {
+  const float rmn = fminf(fminf(r0, r1), fminf(r2, r3));
+  const float rmx = fmaxf(fmaxf(r0, r1), fmaxf(r2, r3));
+  // (fminf / fmaxf drop a NaN beside a number: test each radius for it)
+  const bool ok = rmn >= a.rlo_f && rmx <= a.rhi_f && r0 == r0 && r1 == r1 && r2 == r2 &&
+                  r3 == r3;
+  return __all_sync(0xffffffffu, ok);
 }
 
 // K0 CTAs per SM the register allocation must allow: one chunk per warp in
@@ -769,6 +780,12 @@ __device__ __forceinline__ void resolve_chunk(const FieldArgs& a, const FieldGeo
 // ping-pong prefetch of the next chunk was best at 3 and slower overall)
 #ifndef CAPT_K0_MINB
 #define CAPT_K0_MINB 4
+#endif
+#ifndef CAPT_K0_FASTBAND  // whole in-band chunks without the out-of-band bookkeeping
+#define CAPT_K0_FASTBAND 1
+#endif
+#ifndef CAPT_K0_WAVES  // K0 grid: CTAs per SM (resident: CAPT_K0_MINB)
+#define CAPT_K0_WAVES (8 * 256 / CAPT_K0_BLOCK)
 #endif
 
 // persistent warps over the whole 128-sphere chunks; the last, partial chunk
@@ -795,7 +812,12 @@ __global__ void __launch_bounds__(CAPT_K0_BLOCK, CAPT_K0_MINB) k_resolve(FieldAr
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int ch = w0; ch < nfull; ch += nwarps) {
     const Chunk A = load_chunk<kVec, true>(a.c, a.r, ch, lane, n);
-    resolve_chunk<kMask, LT, !kMask>(a, g, sblk, A, ch, lane, check, pol, rg);
+    // whole unmasked chunks with every radius in band (the common case) shed
+    // the out-of-band bookkeeping
+    if (CAPT_K0_FASTBAND && !kMask && chunk_in_band(a, A.pr.x, A.pr.y, A.pr.z, A.pr.w))
+      resolve_chunk<kMask, LT, !kMask, true>(a, g, sblk, A, ch, lane, check, pol, rg);
+    else
+      resolve_chunk<kMask, LT, !kMask>(a, g, sblk, A, ch, lane, check, pol, rg);
   }
   if ((n & 127) && w0 == nfull % nwarps) {
     const Chunk T = load_chunk<false>(a.c, a.r, nfull, lane, n);
@@ -817,21 +839,17 @@ __global__ void __launch_bounds__(CAPT_K0_BLOCK, CAPT_K0_MINB) k_resolve(FieldAr
 // them); phase 2 consumes the records.  The centres are scalar loads (x, y,
 // z of a sphere: each instruction spans 3 lines of 128 B for 32 spheres; y
 // and z hit L1 after x).
-template <bool kFull>
-__device__ __forceinline__ void resolve1(const FieldArgs& a, const FieldGeom& g,
-                                         const uint8_t* sblk, int ch, int lane, bool check,
-                                         uint64_t pol, Ring& rg) {
+// kBand (whole chunks only): every radius of the chunk is inside the band
+// (warp-uniform, voted by the caller), so no sphere is out of band, bad or
+// listed for its radius -- the common case sheds that bookkeeping.
+template <bool kFull, bool kBand>
+__device__ __forceinline__ void resolve1_body(const FieldArgs& a, const FieldGeom& g,
+                                              const uint8_t* sblk, int ch, int lane, bool check,
+                                              uint64_t pol, Ring& rg, const float (&x)[4],
+                                              const float (&y)[4], const float (&z)[4],
+                                              const float (&r)[4]) {
   const int n = a.n;
   const int q0 = (ch << 7) + lane;
-  float x[4], y[4], z[4], r[4];
-#pragma unroll
-  for (int v = 0; v < 4; ++v) {
-    const int q = kFull || q0 + 32 * v < n ? q0 + 32 * v : 0;
-    x[v] = __ldcs(a.c + 3 * size_t(q));
-    y[v] = __ldcs(a.c + 3 * size_t(q) + 1);
-    z[v] = __ldcs(a.c + 3 * size_t(q) + 2);
-    r[v] = __ldcs(a.r + q);
-  }
   const float INF = __int_as_float(0x7f800000);
   const unsigned bs = unsigned(g.bshift);
   float4 rec[4];
@@ -840,7 +858,7 @@ __device__ __forceinline__ void resolve1(const FieldArgs& a, const FieldGeom& g,
 #pragma unroll
   for (int v = 0; v < 4; ++v) {
     const bool valid = kFull || q0 + 32 * v < n;
-    const bool inb = valid && r[v] >= a.rlo_f && r[v] <= a.rhi_f;
+    const bool inb = kBand || (valid && r[v] >= a.rlo_f && r[v] <= a.rhi_f);
     float fx, fy, fz;
     const int ix = qcell(x[v], g.inv_h, g.nc0[0], fx);
     const int iy = qcell(y[v], g.inv_h, g.nc0[1], fy);
@@ -878,11 +896,11 @@ __device__ __forceinline__ void resolve1(const FieldArgs& a, const FieldGeom& g,
     const bool wmiss = dw > r2 * (1.0f + kTau);
     const bool hit = dw <= r2 * (1.0f - kTau);
     const bool free = wmiss && A > 0.f && A * A > e2[v] * kK1;
-    const bool inb = (inbm >> v) & 1u;
+    const bool inb = kBand || ((inbm >> v) & 1u);
     const bool valid = kFull || q0 + 32 * v < n;
     // out of band: undecided (NaN radius, check_radii off), or only reported
     // (first_bad) with check_radii
-    const bool bad = check && valid && !inb && !(r[v] != r[v]);
+    const bool bad = !kBand && check && valid && !inb && !(r[v] != r[v]);
     // in band: decided without a record (outside the grid, the block's
     // certificate), by the witness, or by the Lipschitz bound
     const bool open = ((lookm >> v) & 1u) && !hit && !free;
@@ -937,6 +955,28 @@ __device__ __forceinline__ void resolve1(const FieldArgs& a, const FieldGeom& g,
   }
   rg.cnt += tot;
   if (rg.cnt >= 32u) ring_drain(a, rg, 32u, lane);
+}
+
+template <bool kFull>
+__device__ __forceinline__ void resolve1(const FieldArgs& a, const FieldGeom& g,
+                                         const uint8_t* sblk, int ch, int lane, bool check,
+                                         uint64_t pol, Ring& rg) {
+  const int n = a.n;
+  const int q0 = (ch << 7) + lane;
+  float x[4], y[4], z[4], r[4];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const int q = kFull || q0 + 32 * v < n ? q0 + 32 * v : 0;
+    x[v] = __ldcs(a.c + 3 * size_t(q));
+    y[v] = __ldcs(a.c + 3 * size_t(q) + 1);
+    z[v] = __ldcs(a.c + 3 * size_t(q) + 2);
+    r[v] = __ldcs(a.r + q);
+  }
+  if (CAPT_K0_FASTBAND && kFull && chunk_in_band(a, r[0], r[1], r[2], r[3])) {
+    resolve1_body<true, true>(a, g, sblk, ch, lane, check, pol, rg, x, y, z, r);
+    return;
+  }
+  resolve1_body<kFull, false>(a, g, sblk, ch, lane, check, pol, rg, x, y, z, r);
 }
 
 __global__ void __launch_bounds__(CAPT_K0_BLOCK, CAPT_K0_MINB) k_resolve1(FieldArgs a) {
@@ -1828,7 +1868,7 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   }
   const bool vec = (reinterpret_cast<uintptr_t>(centers) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(radii) & 15) == 0;
-  const int grid = grid_for(((n + 127) / 128) * 32, CAPT_K0_BLOCK, 8 * 256 / CAPT_K0_BLOCK);
+  const int grid = grid_for(((n + 127) / 128) * 32, CAPT_K0_BLOCK, CAPT_K0_WAVES);
   const size_t sm = 0;  // (the block table is a static shared array)
   const bool bits16 = (reinterpret_cast<uintptr_t>(bits) & 15) == 0;
   if (!mask && L == 1 && bits16) CAPT_CUDA(launch_pdl_f(k_resolve1, grid, CAPT_K0_BLOCK, sm, s, a));
