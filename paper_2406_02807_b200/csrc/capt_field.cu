@@ -65,7 +65,7 @@ namespace capt {
 #define CAPT_FIELD_CELLS (1 << 21)  // 32 MB of K0 records: L2-resident
 #endif
 #ifndef CAPT_BLK_BYTES
-#define CAPT_BLK_BYTES 8192  // block table bound (K0 shared memory per CTA)
+#define CAPT_BLK_BYTES 49152  // block table bound (K0's dynamic shared memory, one CTA per SM)
 #endif
 
 namespace {
@@ -121,15 +121,13 @@ __device__ __forceinline__ bool block_free(const FieldGeom& g, const uint8_t* sb
   const float q = float(sblk[in ? bi : 0u]);
   return in && q * g.bstep > rk;
 }
-// K0's CTAs copy the block table into shared memory (tree data: before the
-// programmatic-dependency wait); a static array, so its address is a
-// compile-time shared-window offset
+// The single-sphere K0's one CTA per SM copies the block table into (dynamic)
+// shared memory: tree data, so before the programmatic-dependency wait.
 __device__ __forceinline__ const uint8_t* stage_block_table(const FieldGeom& g,
                                                             const uint8_t* blk) {
-  __shared__ uint4 s_blk4[(CAPT_BLK_BYTES + 15) / 16];
+  extern __shared__ uint4 s_blk4[];
   const uint4* src = reinterpret_cast<const uint4*>(blk);
-  if (CAPT_K0_BLOCKS)
-    for (int i = threadIdx.x; i < (g.bbytes >> 4); i += blockDim.x) s_blk4[i] = __ldg(src + i);
+  for (int i = threadIdx.x; i < (g.bbytes >> 4); i += blockDim.x) s_blk4[i] = __ldg(src + i);
   __syncthreads();
   return reinterpret_cast<const uint8_t*>(s_blk4);
 }
@@ -775,24 +773,29 @@ __device__ __forceinline__ bool chunk_in_band(const FieldArgs& a, float r0, floa
   return __all_sync(0xffffffffu, ok);
 }
 
-// K0 CTAs per SM the register allocation must allow: one chunk per warp in
-// registers, 4 (54 registers; 5: 48 registers, slower on config 3; a
-// ping-pong prefetch of the next chunk was best at 3 and slower overall)
+// K0's CTA shapes.  Both kernels keep one chunk per warp in registers at 64
+// registers per thread (32 warps per SM; 40 warps at 48 registers were slower
+// on config 3, a ping-pong prefetch of the next chunk was best at 24 warps and
+// slower overall).  Lane groups: 2 CTAs of 512 threads per SM, two waves;
+// single spheres (CAPT_K1_*): one persistent CTA of 1024 threads per SM, so
+// one copy of the block table (up to 48 KB: blocks of 4^3 cells on a 2 M-cell
+// grid) serves the SM (config 3 K0: 0.266 -> 0.248 ms against 4 CTAs of 256
+// threads with 8 KB tables of 8^3-cell blocks).
 #ifndef CAPT_K0_MINB
-#define CAPT_K0_MINB 4
+#define CAPT_K0_MINB 2
 #endif
 #ifndef CAPT_K0_FASTBAND  // whole in-band chunks without the out-of-band bookkeeping
 #define CAPT_K0_FASTBAND 1
 #endif
 #ifndef CAPT_K0_WAVES  // K0 grid: CTAs per SM (resident: CAPT_K0_MINB)
-#define CAPT_K0_WAVES (8 * 256 / CAPT_K0_BLOCK)
+#define CAPT_K0_WAVES 4
 #endif
 
 // persistent warps over the whole 128-sphere chunks; the last, partial chunk
 // (scalar loads, per-sphere validity) after the loop
 template <bool kVec, bool kMask, int LT>
 #ifndef CAPT_K0_BLOCK
-#define CAPT_K0_BLOCK 256
+#define CAPT_K0_BLOCK 512
 #endif
 __global__ void __launch_bounds__(CAPT_K0_BLOCK, CAPT_K0_MINB) k_resolve(FieldArgs a) {
   const FieldGeom g = a.t.fg;
@@ -806,7 +809,8 @@ __global__ void __launch_bounds__(CAPT_K0_BLOCK, CAPT_K0_MINB) k_resolve(FieldAr
   __shared__ float4 s_ring[CAPT_K0_BLOCK / 32][kRing];
   __shared__ uint32_t s_ringq[CAPT_K0_BLOCK / 32][kRing];
   Ring rg{s_ring[threadIdx.x >> 5], s_ringq[threadIdx.x >> 5], 0u, 0u};
-  const uint8_t* sblk = stage_block_table(g, a.t.blk);
+  // (the lane-group K0 does not use the block table: DESIGN section 9)
+  const uint8_t* sblk = CAPT_K0_GROUP_BLOCKS ? stage_block_table(g, a.t.blk) : nullptr;
   // (launched after k_field_zero with programmatic serialisation)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -979,7 +983,17 @@ __device__ __forceinline__ void resolve1(const FieldArgs& a, const FieldGeom& g,
   resolve1_body<kFull, false>(a, g, sblk, ch, lane, check, pol, rg, x, y, z, r);
 }
 
-__global__ void __launch_bounds__(CAPT_K0_BLOCK, CAPT_K0_MINB) k_resolve1(FieldArgs a) {
+// (the single-sphere K0 has its own CTA shape: CAPT_K1_*)
+#ifndef CAPT_K1_BLOCK
+#define CAPT_K1_BLOCK 1024
+#endif
+#ifndef CAPT_K1_MINB
+#define CAPT_K1_MINB 1
+#endif
+#ifndef CAPT_K1_WAVES
+#define CAPT_K1_WAVES 1
+#endif
+__global__ void __launch_bounds__(CAPT_K1_BLOCK, CAPT_K1_MINB) k_resolve1(FieldArgs a) {
   const FieldGeom g = a.t.fg;
   const bool check = a.flags & CAPT_CHECK_RADII;
   const int n = a.n;
@@ -988,8 +1002,8 @@ __global__ void __launch_bounds__(CAPT_K0_BLOCK, CAPT_K0_MINB) k_resolve1(FieldA
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t pol = l2_keep_policy();
-  __shared__ float4 s_ring[CAPT_K0_BLOCK / 32][kRing];
-  __shared__ uint32_t s_ringq[CAPT_K0_BLOCK / 32][kRing];
+  __shared__ float4 s_ring[CAPT_K1_BLOCK / 32][kRing];
+  __shared__ uint32_t s_ringq[CAPT_K1_BLOCK / 32][kRing];
   Ring rg{s_ring[threadIdx.x >> 5], s_ringq[threadIdx.x >> 5], 0u, 0u};
   const uint8_t* sblk = stage_block_table(g, a.t.blk);
   // (launched after k_field_zero with programmatic serialisation)
@@ -1136,6 +1150,13 @@ __global__ void __launch_bounds__(256) k_list_knn(FieldArgs a, uint32_t* __restr
 #define CAPT_BUCKET_WARPS 4
 #endif
 constexpr int kBucketWarps = CAPT_BUCKET_WARPS;  // warps per entry (one CTA)
+#ifndef CAPT_KNN_WAVES  // k_list_knn grid: CTAs per SM
+#define CAPT_KNN_WAVES 8
+#endif
+#ifndef CAPT_BUCKET_UNROLL
+#define CAPT_BUCKET_UNROLL 4
+#endif
+constexpr int kBucketUnroll = CAPT_BUCKET_UNROLL;
 __global__ void __launch_bounds__(32 * kBucketWarps) k_bucket_list(
     FieldArgs a, const uint32_t* __restrict__ list2, const uint32_t* __restrict__ list2_n) {
   const DevTree& t = a.t;
@@ -1193,21 +1214,31 @@ __global__ void __launch_bounds__(32 * kBucketWarps) k_bucket_list(
         if (lane >= o) incl += u;
       }
       const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      for (uint32_t k0 = 32u * wid; k0 < total && !stop(); k0 += 32u * kBucketWarps) {
-        const uint32_t k = k0 + lane;
-        int lo = 0;
+      // (kBucketUnroll point loads of a lane in flight per step)
+      for (uint32_t k0 = 32u * wid; k0 < total && !stop();
+           k0 += 32u * kBucketWarps * kBucketUnroll) {
+        float4 p[kBucketUnroll];
+        bool in[kBucketUnroll];
 #pragma unroll
-        for (int step = 16; step; step >>= 1) {
-          const uint32_t v = __shfl_sync(0xffffffffu, incl, lo + step - 1);
-          if (v <= k) lo += step;
+        for (int u = 0; u < kBucketUnroll; ++u) {
+          const uint32_t k = k0 + 32u * kBucketWarps * u + lane;
+          int lo = 0;
+#pragma unroll
+          for (int step = 16; step; step >>= 1) {
+            const uint32_t v = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+            if (v <= k) lo += step;
+          }
+          const uint32_t base = __shfl_sync(0xffffffffu, i0, lo);
+          const uint32_t excl = __shfl_sync(0xffffffffu, incl - len, lo);
+          in[u] = k < total;
+          p[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (in[u]) p[u] = __ldg(t.cpts + base + (k - excl));
         }
-        const uint32_t base = __shfl_sync(0xffffffffu, i0, lo);
-        const uint32_t excl = __shfl_sync(0xffffffffu, incl - len, lo);
         bool hit = false;
-        if (k < total) {
-          const float4 p = __ldg(t.cpts + base + (k - excl));
-          const float d2 = d2_fma(s.x - p.x, s.y - p.y, s.z - p.z);
-          hit = d2 <= loB || (d2 < hiB && hit_f64(s.x, s.y, s.z, s.w, p));
+#pragma unroll
+        for (int u = 0; u < kBucketUnroll; ++u) {
+          const float d2 = d2_fma(s.x - p[u].x, s.y - p[u].y, s.z - p[u].z);
+          hit |= in[u] && (d2 <= loB || (d2 < hiB && hit_f64(s.x, s.y, s.z, s.w, p[u])));
         }
         if (__any_sync(0xffffffffu, hit) && lane == 0) s_hit = 1;
         __syncwarp();
@@ -1426,7 +1457,8 @@ __device__ __forceinline__ bool bucket_verdict_warp(const DevTree& t, float4 s, 
 __global__ void __launch_bounds__(256) k_resolve_small(FieldArgs a) {
   const DevTree& t = a.t;
   const FieldGeom g = t.fg;
-  const uint8_t* sblk = stage_block_table(g, t.blk);
+  // (small batches read the block table through L1 instead of staging it)
+  const uint8_t* sblk = t.blk;
   const bool check = a.flags & CAPT_CHECK_RADII;
   const int lane = threadIdx.x & 31;
   const int L = a.L;
@@ -1869,9 +1901,23 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   const bool vec = (reinterpret_cast<uintptr_t>(centers) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(radii) & 15) == 0;
   const int grid = grid_for(((n + 127) / 128) * 32, CAPT_K0_BLOCK, CAPT_K0_WAVES);
-  const size_t sm = 0;  // (the block table is a static shared array)
+  // the single-sphere K0 stages the block table in dynamic shared memory
+  // (above the 48 KB default with its rings: opted in once per device)
+  const size_t sm1 = size_t(t.fg.bbytes);
+  {
+    static std::mutex mu;
+    static bool opted[kMaxDevices] = {};
+    std::lock_guard<std::mutex> lk1(mu);
+    if (!opted[dev]) {
+      CAPT_CUDA(cudaFuncSetAttribute(k_resolve1, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     CAPT_BLK_BYTES));
+      opted[dev] = true;
+    }
+  }
+  const size_t sm = CAPT_K0_GROUP_BLOCKS ? sm1 : 0;
   const bool bits16 = (reinterpret_cast<uintptr_t>(bits) & 15) == 0;
-  if (!mask && L == 1 && bits16) CAPT_CUDA(launch_pdl_f(k_resolve1, grid, CAPT_K0_BLOCK, sm, s, a));
+  const int grid1 = grid_for(((n + 127) / 128) * 32, CAPT_K1_BLOCK, CAPT_K1_WAVES);
+  if (!mask && L == 1 && bits16) CAPT_CUDA(launch_pdl_f(k_resolve1, grid1, CAPT_K1_BLOCK, sm1, s, a));
   else if (vec && !mask && L == 8) CAPT_CUDA(launch_pdl_f(k_resolve<true, false, 8>, grid, CAPT_K0_BLOCK, sm, s, a));
   else if (mask) CAPT_CUDA(launch_pdl_f(k_resolve<false, true, 0>, grid, CAPT_K0_BLOCK, sm, s, a));
   else CAPT_CUDA(launch_pdl_f(k_resolve<false, false, 0>, grid, CAPT_K0_BLOCK, sm, s, a));
@@ -1882,7 +1928,7 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
     if (rc) return rc;
   }
   // the list stage: persistent grids (the list lengths are known on the device only)
-  CAPT_CUDA(launch_pdl_f(k_list_knn, grid_for(n, 256, 8), 256, 0, s, a, list2, list2_n, list3,
+  CAPT_CUDA(launch_pdl_f(k_list_knn, grid_for(n, 256, CAPT_KNN_WAVES), 256, 0, s, a, list2, list2_n, list3,
                          list3_n));
   CAPT_CUDA(launch_pdl_f(k_bucket_list, grid_for(int64_t(n) * 32 * kBucketWarps, 32 * kBucketWarps, 16),
                          32 * kBucketWarps, 0, s, a, static_cast<const uint32_t*>(list2),
