@@ -517,7 +517,7 @@ def main():
     roof = None
     if calls == args.steps:
         k0_ms, list_ms = st_ms[0] / calls, st_ms[1] / calls
-        k0_name = "k_resolve1" if L == 1 else "k_resolve<"
+        k0_name = "k_resolve1" if L in (1, 4, 8, 16) else "k_resolve<"
         roof = {"bound": "hbm", "kernel": f"{k0_name.rstrip('<')} (K0: clearance-field resolve)",
                 "achieved": bytes_step / (k0_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s"}
         roof["frac"] = roof["achieved"] / roof["peak"]

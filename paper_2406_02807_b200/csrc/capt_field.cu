@@ -796,20 +796,9 @@ __device__ __forceinline__ bool chunk_in_band(const FieldArgs& a, float r0, floa
 #ifndef CAPT_K0_BLOCK
 #define CAPT_K0_BLOCK 512
 #endif
-#ifndef CAPT_K8_BLOCK  // groups of 8 on aligned inputs: 48 registers, 40 warps per SM
-#define CAPT_K8_BLOCK 640
-#endif
-// (the specialised groups-of-8 kernel fits 48 registers without spills and
-// gains from the 8 more warps per SM: config 1 K0 0.149 -> 0.141 ms; the
-// run-time-L and masked instantiations would spill there)
 template <bool kVec, bool kMask, int LT>
-constexpr int k0_block() {
-  return kVec && !kMask && LT == 8 ? CAPT_K8_BLOCK : CAPT_K0_BLOCK;
-}
-template <bool kVec, bool kMask, int LT>
-__global__ void __launch_bounds__((k0_block<kVec, kMask, LT>()), CAPT_K0_MINB)
-    k_resolve(FieldArgs a) {
-  constexpr int kBlock = k0_block<kVec, kMask, LT>();
+__global__ void __launch_bounds__(CAPT_K0_BLOCK, CAPT_K0_MINB) k_resolve(FieldArgs a) {
+  constexpr int kBlock = CAPT_K0_BLOCK;
   const FieldGeom g = a.t.fg;
   const bool check = a.flags & CAPT_CHECK_RADII;
   const int n = a.n;
@@ -858,12 +847,21 @@ __global__ void __launch_bounds__((k0_block<kVec, kMask, LT>()), CAPT_K0_MINB)
 // kBand (whole chunks only): every radius of the chunk is inside the band
 // (warp-uniform, voted by the caller), so no sphere is out of band, bad or
 // listed for its radius -- the common case sheds that bookkeeping.
-template <bool kFull, bool kBand>
+// LG = 4, 8, 16 (groups of LG consecutive spheres, query.py:152-160): under
+// the strided map a group is LG adjacent lanes of one slot, so its
+// any-collision bit is a field of the slot's hit ballot -- the four records
+// of a lane are in flight together (no dependent rounds; config 1 K0 0.141
+// -> 0.123 ms against four rounds that stop at a group's first hit) and a
+// chunk's 128 / LG group bits are one 4-, 2- or 1-byte store; the spheres of
+// a group with a hit are not listed.
+template <bool kFull, bool kBand, int LG>
 __device__ __forceinline__ void resolve1_body(const FieldArgs& a, const FieldGeom& g,
                                               const uint8_t* sblk, int ch, int lane, bool check,
                                               uint64_t pol, Ring& rg, const float (&x)[4],
                                               const float (&y)[4], const float (&z)[4],
                                               const float (&r)[4]) {
+  static_assert(LG == 1 || LG == 4 || LG == 8 || LG == 16, "lane-group width");
+  constexpr unsigned kGroupMask = (1u << LG) - 1u;
   const int n = a.n;
   const int q0 = (ch << 7) + lane;
   const float INF = __int_as_float(0x7f800000);
@@ -925,9 +923,27 @@ __device__ __forceinline__ void resolve1_body(const FieldArgs& a, const FieldGeo
     badm |= unsigned(bad) << v;
     // verdict word 4 ch + v = the ballot of sphere v
     wd[v] = __ballot_sync(0xffffffffu, ((lookm >> v) & 1u) && hit);
-    ub[v] = __ballot_sync(0xffffffffu, und);
+    if (LG > 1) {  // (this lane's group already has its hit: nothing to list)
+      const bool res = (wd[v] & (kGroupMask << (lane & ~(LG - 1)))) != 0u;
+      ub[v] = __ballot_sync(0xffffffffu, und && !res);
+    } else {
+      ub[v] = __ballot_sync(0xffffffffu, und);
+    }
   }
-  if (kFull) {  // (the words of whole chunks: one 16-B store)
+  if (LG > 1) {
+    // lane i < 128 / LG holds group (128 / LG) ch + i: field i % (32 / LG) of
+    // slot i / (32 / LG)
+    constexpr int kPerSlot = 32 / LG, kBits = 128 / LG;
+    const int gv = (lane / kPerSlot) & 3;
+    const unsigned h = gv == 0 ? wd[0] : gv == 1 ? wd[1] : gv == 2 ? wd[2] : wd[3];
+    const unsigned gb =
+        __ballot_sync(0xffffffffu, (h & (kGroupMask << (LG * (lane % kPerSlot)))) != 0u);
+    if (lane == 0 && (kFull || (ch << 7) < n)) {
+      if (kBits == 32) a.bits[ch] = gb;
+      else if (kBits == 16) reinterpret_cast<uint16_t*>(a.bits)[ch] = uint16_t(gb & 0xffffu);
+      else reinterpret_cast<uint8_t*>(a.bits)[ch] = uint8_t(gb & 0xffu);
+    }
+  } else if (kFull) {  // (the words of whole chunks: one 16-B store)
     if (lane == 0)
       *reinterpret_cast<uint4*>(a.bits + (ch << 2)) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
   } else {
@@ -973,7 +989,7 @@ __device__ __forceinline__ void resolve1_body(const FieldArgs& a, const FieldGeo
   if (rg.cnt >= 32u) ring_drain(a, rg, 32u, lane);
 }
 
-template <bool kFull>
+template <bool kFull, int LG>
 __device__ __forceinline__ void resolve1(const FieldArgs& a, const FieldGeom& g,
                                          const uint8_t* sblk, int ch, int lane, bool check,
                                          uint64_t pol, Ring& rg) {
@@ -989,10 +1005,10 @@ __device__ __forceinline__ void resolve1(const FieldArgs& a, const FieldGeom& g,
     r[v] = __ldcs(a.r + q);
   }
   if (CAPT_K0_FASTBAND && kFull && chunk_in_band(a, r[0], r[1], r[2], r[3])) {
-    resolve1_body<true, true>(a, g, sblk, ch, lane, check, pol, rg, x, y, z, r);
+    resolve1_body<true, true, LG>(a, g, sblk, ch, lane, check, pol, rg, x, y, z, r);
     return;
   }
-  resolve1_body<kFull, false>(a, g, sblk, ch, lane, check, pol, rg, x, y, z, r);
+  resolve1_body<kFull, false, LG>(a, g, sblk, ch, lane, check, pol, rg, x, y, z, r);
 }
 
 // (the single-sphere K0 has its own CTA shape: CAPT_K1_*)
@@ -1005,6 +1021,7 @@ __device__ __forceinline__ void resolve1(const FieldArgs& a, const FieldGeom& g,
 #ifndef CAPT_K1_WAVES
 #define CAPT_K1_WAVES 1
 #endif
+template <int LG>
 __global__ void __launch_bounds__(CAPT_K1_BLOCK, CAPT_K1_MINB) k_resolve1(FieldArgs a) {
   const FieldGeom g = a.t.fg;
   const bool check = a.flags & CAPT_CHECK_RADII;
@@ -1021,8 +1038,10 @@ __global__ void __launch_bounds__(CAPT_K1_BLOCK, CAPT_K1_MINB) k_resolve1(FieldA
   // (launched after k_field_zero with programmatic serialisation)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  for (int ch = w0; ch < nfull; ch += nwarps) resolve1<true>(a, g, sblk, ch, lane, check, pol, rg);
-  if ((n & 127) && w0 == nfull % nwarps) resolve1<false>(a, g, sblk, nfull, lane, check, pol, rg);
+  for (int ch = w0; ch < nfull; ch += nwarps)
+    resolve1<true, LG>(a, g, sblk, ch, lane, check, pol, rg);
+  if ((n & 127) && w0 == nfull % nwarps)
+    resolve1<false, LG>(a, g, sblk, nfull, lane, check, pol, rg);
   if (rg.cnt) ring_drain(a, rg, rg.cnt, lane);
 }
 
@@ -1910,8 +1929,6 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
     const int rc = stage_record(dev, tcall, 0, s);
     if (rc) return rc;
   }
-  const bool vec = (reinterpret_cast<uintptr_t>(centers) & 15) == 0 &&
-                   (reinterpret_cast<uintptr_t>(radii) & 15) == 0;
   const int grid = grid_for(((n + 127) / 128) * 32, CAPT_K0_BLOCK, CAPT_K0_WAVES);
   // the single-sphere K0 stages the block table in dynamic shared memory
   // (above the 48 KB default with its rings: opted in once per device)
@@ -1921,7 +1938,13 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
     static bool opted[kMaxDevices] = {};
     std::lock_guard<std::mutex> lk1(mu);
     if (!opted[dev]) {
-      CAPT_CUDA(cudaFuncSetAttribute(k_resolve1, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CAPT_CUDA(cudaFuncSetAttribute(k_resolve1<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     CAPT_BLK_BYTES));
+      CAPT_CUDA(cudaFuncSetAttribute(k_resolve1<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     CAPT_BLK_BYTES));
+      CAPT_CUDA(cudaFuncSetAttribute(k_resolve1<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     CAPT_BLK_BYTES));
+      CAPT_CUDA(cudaFuncSetAttribute(k_resolve1<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      CAPT_BLK_BYTES));
       opted[dev] = true;
     }
@@ -1929,11 +1952,14 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   const size_t sm = CAPT_K0_GROUP_BLOCKS ? sm1 : 0;
   const bool bits16 = (reinterpret_cast<uintptr_t>(bits) & 15) == 0;
   const int grid1 = grid_for(((n + 127) / 128) * 32, CAPT_K1_BLOCK, CAPT_K1_WAVES);
-  if (!mask && L == 1 && bits16) CAPT_CUDA(launch_pdl_f(k_resolve1, grid1, CAPT_K1_BLOCK, sm1, s, a));
-  else if (vec && !mask && L == 8)
-    CAPT_CUDA(launch_pdl_f(k_resolve<true, false, 8>,
-                           grid_for(((n + 127) / 128) * 32, CAPT_K8_BLOCK, CAPT_K0_WAVES),
-                           CAPT_K8_BLOCK, sm, s, a));
+  if (!mask && L == 1 && bits16)
+    CAPT_CUDA(launch_pdl_f(k_resolve1<1>, grid1, CAPT_K1_BLOCK, sm1, s, a));
+  else if (!mask && L == 4)
+    CAPT_CUDA(launch_pdl_f(k_resolve1<4>, grid1, CAPT_K1_BLOCK, sm1, s, a));
+  else if (!mask && L == 8)
+    CAPT_CUDA(launch_pdl_f(k_resolve1<8>, grid1, CAPT_K1_BLOCK, sm1, s, a));
+  else if (!mask && L == 16)
+    CAPT_CUDA(launch_pdl_f(k_resolve1<16>, grid1, CAPT_K1_BLOCK, sm1, s, a));
   else if (mask) CAPT_CUDA(launch_pdl_f(k_resolve<false, true, 0>, grid, CAPT_K0_BLOCK, sm, s, a));
   else CAPT_CUDA(launch_pdl_f(k_resolve<false, false, 0>, grid, CAPT_K0_BLOCK, sm, s, a));
   CAPT_CUDA(cudaGetLastError());
