@@ -225,6 +225,28 @@ def test_field_tabletop_groups_and_lane_masks(L):
         assert np.array_equal(q(tree, c, r), O.brute_collides_many(cloud, c, r))
 
 
+@pytest.mark.parametrize("L", [4, 8, 16])
+def test_field_group_kernel_tails_and_edge_radii(L):
+    # the strided K0 with lane groups (k_resolve1<L>): a ragged last chunk
+    # (its group bits are a 4-, 2- or 1-byte store), chunks with out-of-band
+    # and NaN radii (the body with the band bookkeeping; check_radii off: the
+    # reference's own semantics for those lanes), first_bad with check_radii
+    cloud = W.cfg1_cloud()
+    tree = P.construct(P.PointCloud(cloud), P.BuildParams(0.02, 0.08))
+    t = O.tree_from(tree)
+    for n_groups in (65536 + 37, 16385, 8192 + 1):
+        c, r = W.cfg1_queries(cloud, n_groups=n_groups, lane_width=L, seed=5 + L)
+        assert np.array_equal(q(tree, c, r, L), O.collides_groups(t, c, r, L))
+        r2 = r.copy()
+        r2[3::1013] = np.float32(0.5)  # out of band
+        r2[7::2029] = np.nan
+        r2[11::4051] = np.float32(0.001)
+        assert np.array_equal(q(tree, c, r2, L), O.collides_groups(t, c, r2, L))
+        bits, bad = q(tree, c, r2, L, check=True)
+        flagged = ((r2.astype(np.float64) < 0.02) | (r2.astype(np.float64) > 0.08)) & ~np.isnan(r2)
+        assert bad == int(np.argmax(flagged))
+
+
 def test_field_tangent_spheres():
     # radius = the float32 image of the exact nearest-point distance, and one
     # ulp either side: every sphere sits on the certificates' decision edge
