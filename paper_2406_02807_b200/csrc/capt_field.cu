@@ -73,6 +73,20 @@ namespace {
 constexpr float kNNShrink = 1.0f - 0x1p-19f;    // fp32 sqrt(d^2) -> certified lower bound
 constexpr int kFieldChunk = 1024;               // staged points per k_field_knn round
 constexpr int kKP = kCand + 1;                  // nearest points kept per cell (+ the bound)
+// The second record (ring drain): the kSecond nearest points after the
+// witness as int16 offsets and the bound of the next one -- 2 candidates in
+// 16 B or 5 in 32 B (config 3 lists 346 K spheres with 2, 121 K with 5: list
+// stage 53 -> 39 us for 1% more K0).
+#ifndef CAPT_SECOND
+#define CAPT_SECOND 5
+#endif
+constexpr int kSecond = CAPT_SECOND;
+constexpr int kSecondWords = kSecond == 2 ? 4 : 8;  // (3 kSecond + 1 slots of 16 bits)
+static_assert(kSecond == 2 || kSecond == 5, "second record: 16 or 32 bytes");
+// the second records follow the K0 records at an even cell count (32-B loads)
+__host__ __device__ __forceinline__ size_t second_base(int64_t cells) {
+  return size_t((cells + 1) & ~int64_t(1));
+}
 
 __device__ __forceinline__ int f2o(float f) {
   const int i = __float_as_int(f);
@@ -147,6 +161,13 @@ __device__ __forceinline__ float4 ldg_keep(const float4* p, uint64_t pol) {
 }
 __device__ __forceinline__ float d2_fma(float dx, float dy, float dz) {
   return fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+}
+// one 256-bit load (candidate and second records)
+__device__ __forceinline__ void ld_v8u(const uint32_t* p, uint32_t (&v)[8]) {
+  asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7])
+      : "l"(p));
 }
 // signed int16 slots of a word (candidate offsets)
 __device__ __forceinline__ int slot_lo(uint32_t w) { return int(w << 16) >> 16; }
@@ -345,16 +366,29 @@ __global__ void __launch_bounds__(256, 1) k_field_cand(FieldGeom g, BucketGrid b
     put_slot(wd, 31, int(floor(double(lb(drop)) * inv)));  // kd_q q_step <= kd
     put_slot(wd + 16, 31, count);
     // K0's records: {nearest point w (exact), lb of the 2nd nearest} (read
-    // for every sphere) and {the 2nd and 3rd nearest as offsets, kd3_q: lb
-    // of the 4th nearest} (read for the spheres the first leaves open)
+    // for every sphere) and {the next kSecond nearest as offsets, kd_q: lb
+    // of the point after them} (read for the spheres the first leaves open)
     const float4 w = bi[0] >= 0 ? pts[bi[0]] : make_float4(INF, INF, INF, 0.f);
     field[cell] = make_float4(w.x, w.y, w.z, lb(1));
-    const int kd3 = int(floor(double(lb(min(drop, 3))) * inv));
-    field[g.cells + cell] = make_float4(
-        __uint_as_float((get_slot(wd, 1) & 0xffffu) | (get_slot(wd + 16, 1) << 16)),
-        __uint_as_float((get_slot(wd + 32, 1) & 0xffffu) | (get_slot(wd, 2) << 16)),
-        __uint_as_float((get_slot(wd + 16, 2) & 0xffffu) | (get_slot(wd + 32, 2) << 16)),
-        __uint_as_float(uint32_t(kd3) & 0xffffu));
+    // second record: candidates 1 .. kSecond (the 2nd .. nearest) as int16
+    // slots 3 (c - 1) + axis, then kd: lb of the first point after them
+    {
+      uint32_t w2[kSecondWords];
+#pragma unroll
+      for (int i = 0; i < kSecondWords; ++i) w2[i] = 0x80008000u;
+#pragma unroll
+      for (int c = 1; c <= kSecond; ++c) {
+        put_slot(w2, 3 * (c - 1), get_slot(wd, c));
+        put_slot(w2, 3 * (c - 1) + 1, get_slot(wd + 16, c));
+        put_slot(w2, 3 * (c - 1) + 2, get_slot(wd + 32, c));
+      }
+      put_slot(w2, 2 * kSecondWords - 1, int(floor(double(lb(min(drop, kSecond + 1))) * inv)));
+      uint4* d2 = reinterpret_cast<uint4*>(field + second_base(g.cells)) +
+                  size_t(cell) * (kSecondWords / 4);
+#pragma unroll
+      for (int i = 0; i < kSecondWords / 4; ++i)
+        d2[i] = make_uint4(w2[4 * i], w2[4 * i + 1], w2[4 * i + 2], w2[4 * i + 3]);
+    }
     uint4* dst = reinterpret_cast<uint4*>(cand + cell * kCandWords);
 #pragma unroll
     for (int i = 0; i < kCandWords / 4; ++i)
@@ -491,10 +525,10 @@ struct Ring {
 
 // Drain the k (<= 32) oldest ring entries, one per lane.  An entry flagged
 // (bit 31 of its index: the witness was a definite miss) first meets the
-// cell's second record -- the 2nd and 3rd nearest points of x0 as int16
-// offsets and kd3 <= the distance to every other point, read only here so
+// cell's second record -- the 2nd .. 6th nearest points of x0 as int16
+// offsets and kd <= the distance to every other point, read only here so
 // the hot records stay 16 B per cell -- the candidate certificate of
-// k_list_knn with three candidates: a hit sets its bit (the same warp wrote
+// k_list_knn with kSecond candidates: a hit sets its bit (the same warp wrote
 // the chunk's words; __syncwarp orders the two), free drops it.  The rest
 // are written to the list (coalesced, one atomic).
 __device__ __forceinline__ void ring_drain(const FieldArgs& a, Ring& rg, unsigned k, int lane) {
@@ -518,7 +552,17 @@ __device__ __forceinline__ void ring_drain(const FieldArgs& a, Ring& rg, unsigne
     const int iz = qcell(s.z, g.inv_h, g.nc0[2], fz);
     const unsigned cell =
         (unsigned(iz) * unsigned(g.ny) + unsigned(iy)) * unsigned(g.nx) + unsigned(ix);
-    const uint4 h2 = __ldg(reinterpret_cast<const uint4*>(a.t.field + g.cells + cell));
+    uint32_t w2[8];
+    {
+      const uint32_t* rec2 = reinterpret_cast<const uint32_t*>(a.t.field + second_base(g.cells)) +
+                             size_t(cell) * kSecondWords;
+      if (kSecondWords == 8) {
+        ld_v8u(rec2, w2);
+      } else {
+        const uint4 h2 = __ldg(reinterpret_cast<const uint4*>(rec2));
+        w2[0] = h2.x, w2[1] = h2.y, w2[2] = h2.z, w2[3] = h2.w;
+      }
+    }
     const float qs = g.q_step, qe = g.q_err * (1.0f + 0x1p-17f);
     const float ex = s.x - __fmaf_rn(fx, g.h, g.c0[0]);
     const float ey = s.y - __fmaf_rn(fy, g.h, g.c0[1]);
@@ -527,19 +571,19 @@ __device__ __forceinline__ void ring_drain(const FieldArgs& a, Ring& rg, unsigne
     const float RM = s.w * (1.0f + 0x1p-18f) + qe;
     const float lo = RH > 0.f ? RH * RH * (1.0f - 0x1p-20f) : -1.f;
     const float hi = RM * RM * (1.0f + 0x1p-20f);
-    const int o[6] = {slot_lo(h2.x), slot_hi(h2.x), slot_lo(h2.y),
-                      slot_hi(h2.y), slot_lo(h2.z), slot_hi(h2.z)};
+    auto sl = [&](int i) { return (i & 1) ? slot_hi(w2[i >> 1]) : slot_lo(w2[i >> 1]); };
     bool hit = false, amb = false;
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const float vx = fmaf(-float(o[3 * c]), qs, ex), vy = fmaf(-float(o[3 * c + 1]), qs, ey),
-                  vz = fmaf(-float(o[3 * c + 2]), qs, ez);
+    for (int c = 0; c < kSecond; ++c) {
+      const int ox = sl(3 * c), oy = sl(3 * c + 1), oz = sl(3 * c + 2);
+      const float vx = fmaf(-float(ox), qs, ex), vy = fmaf(-float(oy), qs, ey),
+                  vz = fmaf(-float(oz), qs, ez);
       const float S = d2_fma(vx, vy, vz);
-      const bool used = o[3 * c] != kCandNone;
+      const bool used = ox != kCandNone;
       hit |= used && S <= lo;
       amb |= used && S < hi;
     }
-    const float A = float(slot_lo(h2.w)) * qs - s.w * kK1;
+    const float A = float(sl(2 * kSecondWords - 1)) * qs - s.w * kK1;
     const bool free = !hit && !amb && A > 0.f && A * A > d2_fma(ex, ey, ez) * kK1;
     if (hit) {
       const uint32_t b = a.L == 1 ? q : q / uint32_t(a.L);
@@ -1070,12 +1114,6 @@ __global__ void __launch_bounds__(CAPT_K1_BLOCK, CAPT_K1_MINB) k_resolve1(FieldA
 // open entries (about 1e-5 of a batch, plus every sphere the grid cannot
 // take) go to a second list for part 2.
 
-__device__ __forceinline__ void ld_v8u(const uint32_t* p, uint32_t (&v)[8]) {
-  asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7])
-      : "l"(p));
-}
 
 __global__ void __launch_bounds__(256) k_list_knn(FieldArgs a, uint32_t* __restrict__ list2,
                                                   uint32_t* __restrict__ list2_n,
@@ -1734,7 +1772,8 @@ int build_field(capt_tree* tree, cudaStream_t s) {
   // one allocation: K0 records | candidate records | block table | the
   // points in bucket order | the bucket starts (the list stage's exact scan)
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  const size_t off_cand = al(2 * sizeof(float4) * size_t(g.cells));  // (32-B loads)
+  const size_t off_cand =  // (K0 records | second records; 32-B loads)
+      al(sizeof(float4) * second_base(g.cells) + 4 * size_t(kSecondWords) * size_t(g.cells));
   const size_t off_blk = off_cand + al(sizeof(uint32_t) * kCandWords * size_t(g.cells));
   const size_t off_cpts = off_blk + al(size_t(g.bbytes));
   const size_t off_bst = off_cpts + al(sizeof(float4) * std::max<size_t>(n_fin, 1));
@@ -2023,9 +2062,10 @@ extern "C" int capt_tree_field(const capt_tree* tree, capt_field_info* info, flo
   if (!cells && !cand) return CAPT_OK;
   CAPT_CUDA(cudaSetDevice(tree->device));
   const size_t nc = size_t(g.cells);
-  std::vector<float4> rec(2 * nc);
+  const size_t nrec = second_base(g.cells) + size_t(kSecondWords / 4) * nc;
+  std::vector<float4> rec(nrec);
   std::vector<uint32_t> w(nc * kCandWords);
-  CAPT_CUDA(cudaMemcpy(rec.data(), tree->field, 2 * sizeof(float4) * nc, cudaMemcpyDeviceToHost));
+  CAPT_CUDA(cudaMemcpy(rec.data(), tree->field, sizeof(float4) * nrec, cudaMemcpyDeviceToHost));
   CAPT_CUDA(cudaMemcpy(w.data(), tree->cand, sizeof(uint32_t) * w.size(), cudaMemcpyDeviceToHost));
   auto slot = [&](size_t cell, int axis, int j) {
     const uint32_t v = w[cell * kCandWords + 16 * axis + (j >> 1)];
@@ -2041,10 +2081,10 @@ extern "C" int capt_tree_field(const capt_tree* tree, capt_field_info* info, flo
       o[3] = rec[i].w;
       o[4] = float(slot(i, 0, 31)) * g.q_step;  // kd
       o[5] = float(slot(i, 1, 31));            // candidates
-      uint32_t kd3;
-      memcpy(&kd3, &rec[nc + i].w, 4);
-      o[6] = float(int16_t(uint16_t(kd3 & 0xffffu))) * g.q_step;  // K0's kd3
-      o[7] = 0.f;
+      uint32_t kd2;  // the second record's bound: its last 16-bit slot
+      memcpy(&kd2, &rec[second_base(g.cells) + size_t(kSecondWords / 4) * (i + 1) - 1].w, 4);
+      o[6] = float(int16_t(uint16_t(kd2 >> 16))) * g.q_step;
+      o[7] = float(kSecond);  // (o[6] bounds the (kSecond + 2)-th nearest)
     }
     if (cand) {  // offsets (p - x0) / q_step, kCandNone for unused slots
       for (int k = 0; k < kCand; ++k)

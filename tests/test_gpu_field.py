@@ -83,8 +83,14 @@ def check_field(tree, cloud, sample=200000, seed=0):
     assert np.allclose(dw, nn[near], rtol=1e-5, atol=1e-7)
     wset = {tuple(p) for p in cloud.astype(np.float32)[:, :3].tolist()}
     assert all(tuple(w) in wset for w in rec[has][:2000, :3].astype(np.float32).tolist())
-    # rec[6]: K0's bound of the 4th-nearest distance (a multiple of q_step)
-    assert np.all(rec[:, 6] <= dk[:, 3] + slack) and np.all(rec[:, 6] <= rcap)
+    # rec[6]: the second record's bound -- the distance of the first point
+    # after its rec[7] candidates (the 2nd .. nearest), a multiple of q_step,
+    # tight to one step inside rcap
+    k2 = int(rec[0, 7])
+    assert k2 in (2, 5) and np.all(rec[:, 7] == k2)
+    assert np.all(rec[:, 6] <= dk[:, k2 + 1] + slack) and np.all(rec[:, 6] <= rcap)
+    t2 = dk[:, k2 + 1] < rcap * (1 - 1e-3)
+    assert np.all(rec[t2, 6] >= dk[t2, k2 + 1] - 2 * np.float64(f["q_step"]) - 1e-6 * rcap)
     # candidate records: the K nearest cloud points of x0 as int16 offsets
     # (distances equal to the float64 K-nearest distances within the offset
     # rounding where those lie inside rcap), and kd a lower bound of the
