@@ -1216,14 +1216,14 @@ __global__ void __launch_bounds__(256) k_list_knn(FieldArgs a, uint32_t* __restr
 // (y, z) bucket row), 32 points at a time, fp32 with the rows in the error
 // band re-tested in float64, and stops at the first hit.
 #ifndef CAPT_BUCKET_WARPS
-#define CAPT_BUCKET_WARPS 4
+#define CAPT_BUCKET_WARPS 2
 #endif
 constexpr int kBucketWarps = CAPT_BUCKET_WARPS;  // warps per entry (one CTA)
 #ifndef CAPT_KNN_WAVES  // k_list_knn grid: CTAs per SM
 #define CAPT_KNN_WAVES 8
 #endif
 #ifndef CAPT_BUCKET_UNROLL
-#define CAPT_BUCKET_UNROLL 4
+#define CAPT_BUCKET_UNROLL 8
 #endif
 constexpr int kBucketUnroll = CAPT_BUCKET_UNROLL;
 __global__ void __launch_bounds__(32 * kBucketWarps) k_bucket_list(
@@ -2010,7 +2010,7 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
   // the list stage: persistent grids (the list lengths are known on the device only)
   CAPT_CUDA(launch_pdl_f(k_list_knn, grid_for(n, 256, CAPT_KNN_WAVES), 256, 0, s, a, list2, list2_n, list3,
                          list3_n));
-  CAPT_CUDA(launch_pdl_f(k_bucket_list, grid_for(int64_t(n) * 32 * kBucketWarps, 32 * kBucketWarps, 16),
+  CAPT_CUDA(launch_pdl_f(k_bucket_list, grid_for(int64_t(n) * 32 * kBucketWarps, 32 * kBucketWarps, 64 / kBucketWarps),
                          32 * kBucketWarps, 0, s, a, static_cast<const uint32_t*>(list2),
                          static_cast<const uint32_t*>(list2_n)));
   CAPT_CUDA(launch_pdl_f(k_tree_list, grid_for(int64_t(n) * 32, 256, 8), 256, 0, s, a,
