@@ -169,7 +169,9 @@ int capt_nn_distances(int device, int k, const float* points, int64_t n,
  *   kd <= the distance from x0 to every cloud point that is not a candidate
  *     (kd <= rcap, a multiple of q_step).
  * box_lo/box_hi: the cloud's box.  cells: NULL, or a host buffer of
- * 8 * n_cells floats {witness x, y, z, nn, kd, candidate count, 0, 0}.
+ * 8 * n_cells floats {witness x, y, z, nn, kd, candidate count, kd2, k2}:
+ * kd2 = the ring drain's second-record bound (<= the distance from x0 to
+ * every cloud point after the witness and the next k2 nearest).
  * cand: NULL, or a host buffer of 3 * n_cand * n_cells floats (each
  * candidate's offsets q, +inf for unused slots).  Returns CAPT_EINVAL for
  * trees without a field. */
