@@ -193,7 +193,8 @@ class Capt:
     def clearance_field(self, cells: bool = False, candidates: bool = False):
         """The tree's clearance field (include/capt_b200.h capt_tree_field):
         a dict of its geometry, plus with ``cells`` the (nz, ny, nx, 8)
-        float32 records {witness xyz, nn, kd, candidate count, 0, 0} and with
+        float32 records {witness xyz, nn, kd, candidate count, kd2, k2} (kd2:
+        the second record's bound after the witness and k2 more points) and with
         ``candidates`` the (nz, ny, nx, n_cand, 3) candidate offsets
         (p - x0) / q_step (+inf for unused slots); None for trees without
         one (k < 3)."""
