@@ -1968,6 +1968,10 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
     const int rc = stage_record(dev, tcall, 0, s);
     if (rc) return rc;
   }
+  // (the lane-group K0 for other widths and lane masks: 128-bit loads when
+  // the inputs are 16-byte aligned)
+  const bool vec = (reinterpret_cast<uintptr_t>(centers) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(radii) & 15) == 0;
   const int grid = grid_for(((n + 127) / 128) * 32, CAPT_K0_BLOCK, CAPT_K0_WAVES);
   // the single-sphere K0 stages the block table in dynamic shared memory
   // (above the 48 KB default with its rings: opted in once per device)
@@ -1999,8 +2003,14 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
     CAPT_CUDA(launch_pdl_f(k_resolve1<8>, grid1, CAPT_K1_BLOCK, sm1, s, a));
   else if (!mask && L == 16)
     CAPT_CUDA(launch_pdl_f(k_resolve1<16>, grid1, CAPT_K1_BLOCK, sm1, s, a));
-  else if (mask) CAPT_CUDA(launch_pdl_f(k_resolve<false, true, 0>, grid, CAPT_K0_BLOCK, sm, s, a));
-  else CAPT_CUDA(launch_pdl_f(k_resolve<false, false, 0>, grid, CAPT_K0_BLOCK, sm, s, a));
+  else if (mask && vec)
+    CAPT_CUDA(launch_pdl_f(k_resolve<true, true, 0>, grid, CAPT_K0_BLOCK, sm, s, a));
+  else if (mask)
+    CAPT_CUDA(launch_pdl_f(k_resolve<false, true, 0>, grid, CAPT_K0_BLOCK, sm, s, a));
+  else if (vec)
+    CAPT_CUDA(launch_pdl_f(k_resolve<true, false, 0>, grid, CAPT_K0_BLOCK, sm, s, a));
+  else
+    CAPT_CUDA(launch_pdl_f(k_resolve<false, false, 0>, grid, CAPT_K0_BLOCK, sm, s, a));
   CAPT_CUDA(cudaGetLastError());
   note_launches(1);
   if (tcall >= 0) {
