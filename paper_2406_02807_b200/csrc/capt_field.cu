@@ -898,12 +898,15 @@ __global__ void __launch_bounds__(CAPT_K0_BLOCK, CAPT_K0_MINB) k_resolve(FieldAr
 // -> 0.123 ms against four rounds that stop at a group's first hit) and a
 // chunk's 128 / LG group bits are one 4-, 2- or 1-byte store; the spheres of
 // a group with a hit are not listed.
-template <bool kFull, bool kBand, int LG>
+// kMask: lane masks (bit v of vm: sphere v of the lane is a valid lane; an
+// invalid lane is never tested, listed or reported) -- kBand then means
+// "every valid radius of the chunk is in band".
+template <bool kFull, bool kBand, int LG, bool kMask>
 __device__ __forceinline__ void resolve1_body(const FieldArgs& a, const FieldGeom& g,
                                               const uint8_t* sblk, int ch, int lane, bool check,
                                               uint64_t pol, Ring& rg, const float (&x)[4],
                                               const float (&y)[4], const float (&z)[4],
-                                              const float (&r)[4]) {
+                                              const float (&r)[4], unsigned vm) {
   static_assert(LG == 1 || LG == 4 || LG == 8 || LG == 16, "lane-group width");
   constexpr unsigned kGroupMask = (1u << LG) - 1u;
   const int n = a.n;
@@ -915,8 +918,8 @@ __device__ __forceinline__ void resolve1_body(const FieldArgs& a, const FieldGeo
   unsigned inbm = 0u, lookm = 0u;
 #pragma unroll
   for (int v = 0; v < 4; ++v) {
-    const bool valid = kFull || q0 + 32 * v < n;
-    const bool inb = kBand || (valid && r[v] >= a.rlo_f && r[v] <= a.rhi_f);
+    const bool valid = (kFull || q0 + 32 * v < n) && (!kMask || ((vm >> v) & 1u));
+    const bool inb = kBand ? (!kMask || valid) : (valid && r[v] >= a.rlo_f && r[v] <= a.rhi_f);
     float fx, fy, fz;
     const int ix = qcell(x[v], g.inv_h, g.nc0[0], fx);
     const int iy = qcell(y[v], g.inv_h, g.nc0[1], fy);
@@ -954,8 +957,8 @@ __device__ __forceinline__ void resolve1_body(const FieldArgs& a, const FieldGeo
     const bool wmiss = dw > r2 * (1.0f + kTau);
     const bool hit = dw <= r2 * (1.0f - kTau);
     const bool free = wmiss && A > 0.f && A * A > e2[v] * kK1;
-    const bool inb = kBand || ((inbm >> v) & 1u);
-    const bool valid = kFull || q0 + 32 * v < n;
+    const bool inb = (kBand && !kMask) || ((inbm >> v) & 1u);
+    const bool valid = (kFull || q0 + 32 * v < n) && (!kMask || ((vm >> v) & 1u));
     // out of band: undecided (NaN radius, check_radii off), or only reported
     // (first_bad) with check_radii
     const bool bad = !kBand && check && valid && !inb && !(r[v] != r[v]);
@@ -1033,13 +1036,14 @@ __device__ __forceinline__ void resolve1_body(const FieldArgs& a, const FieldGeo
   if (rg.cnt >= 32u) ring_drain(a, rg, 32u, lane);
 }
 
-template <bool kFull, int LG>
+template <bool kFull, int LG, bool kMask>
 __device__ __forceinline__ void resolve1(const FieldArgs& a, const FieldGeom& g,
                                          const uint8_t* sblk, int ch, int lane, bool check,
                                          uint64_t pol, Ring& rg) {
   const int n = a.n;
   const int q0 = (ch << 7) + lane;
   float x[4], y[4], z[4], r[4];
+  unsigned vm = 15u;
 #pragma unroll
   for (int v = 0; v < 4; ++v) {
     const int q = kFull || q0 + 32 * v < n ? q0 + 32 * v : 0;
@@ -1047,12 +1051,17 @@ __device__ __forceinline__ void resolve1(const FieldArgs& a, const FieldGeom& g,
     y[v] = __ldcs(a.c + 3 * size_t(q) + 1);
     z[v] = __ldcs(a.c + 3 * size_t(q) + 2);
     r[v] = __ldcs(a.r + q);
+    if (kMask && a.mask[q] == 0) vm &= ~(1u << v);
   }
-  if (CAPT_K0_FASTBAND && kFull && chunk_in_band(a, r[0], r[1], r[2], r[3])) {
-    resolve1_body<true, true, LG>(a, g, sblk, ch, lane, check, pol, rg, x, y, z, r);
+  // (an invalid lane's radius does not count in the vote)
+  const float rin = a.rlo_f;
+  if (CAPT_K0_FASTBAND && kFull &&
+      chunk_in_band(a, kMask && !(vm & 1u) ? rin : r[0], kMask && !(vm & 2u) ? rin : r[1],
+                    kMask && !(vm & 4u) ? rin : r[2], kMask && !(vm & 8u) ? rin : r[3])) {
+    resolve1_body<true, true, LG, kMask>(a, g, sblk, ch, lane, check, pol, rg, x, y, z, r, vm);
     return;
   }
-  resolve1_body<kFull, false, LG>(a, g, sblk, ch, lane, check, pol, rg, x, y, z, r);
+  resolve1_body<kFull, false, LG, kMask>(a, g, sblk, ch, lane, check, pol, rg, x, y, z, r, vm);
 }
 
 // (the single-sphere K0 has its own CTA shape: CAPT_K1_*)
@@ -1065,7 +1074,7 @@ __device__ __forceinline__ void resolve1(const FieldArgs& a, const FieldGeom& g,
 #ifndef CAPT_K1_WAVES
 #define CAPT_K1_WAVES 1
 #endif
-template <int LG>
+template <int LG, bool kMask>
 __global__ void __launch_bounds__(CAPT_K1_BLOCK, CAPT_K1_MINB) k_resolve1(FieldArgs a) {
   const FieldGeom g = a.t.fg;
   const bool check = a.flags & CAPT_CHECK_RADII;
@@ -1083,9 +1092,9 @@ __global__ void __launch_bounds__(CAPT_K1_BLOCK, CAPT_K1_MINB) k_resolve1(FieldA
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int ch = w0; ch < nfull; ch += nwarps)
-    resolve1<true, LG>(a, g, sblk, ch, lane, check, pol, rg);
+    resolve1<true, LG, kMask>(a, g, sblk, ch, lane, check, pol, rg);
   if ((n & 127) && w0 == nfull % nwarps)
-    resolve1<false, LG>(a, g, sblk, nfull, lane, check, pol, rg);
+    resolve1<false, LG, kMask>(a, g, sblk, nfull, lane, check, pol, rg);
   if (rg.cnt) ring_drain(a, rg, rg.cnt, lane);
 }
 
@@ -1981,28 +1990,31 @@ int launch_field(const DevTree& t, const void* centers, const void* radii, int64
     static bool opted[kMaxDevices] = {};
     std::lock_guard<std::mutex> lk1(mu);
     if (!opted[dev]) {
-      CAPT_CUDA(cudaFuncSetAttribute(k_resolve1<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     CAPT_BLK_BYTES));
-      CAPT_CUDA(cudaFuncSetAttribute(k_resolve1<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     CAPT_BLK_BYTES));
-      CAPT_CUDA(cudaFuncSetAttribute(k_resolve1<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     CAPT_BLK_BYTES));
-      CAPT_CUDA(cudaFuncSetAttribute(k_resolve1<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     CAPT_BLK_BYTES));
+      const auto opt_in = [](auto kernel) {
+        return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    CAPT_BLK_BYTES);
+      };
+      CAPT_CUDA(opt_in(k_resolve1<1, false>));
+      CAPT_CUDA(opt_in(k_resolve1<4, false>));
+      CAPT_CUDA(opt_in(k_resolve1<8, false>));
+      CAPT_CUDA(opt_in(k_resolve1<16, false>));
+      CAPT_CUDA(opt_in(k_resolve1<1, true>));
+      CAPT_CUDA(opt_in(k_resolve1<4, true>));
+      CAPT_CUDA(opt_in(k_resolve1<8, true>));
+      CAPT_CUDA(opt_in(k_resolve1<16, true>));
       opted[dev] = true;
     }
   }
   const size_t sm = CAPT_K0_GROUP_BLOCKS ? sm1 : 0;
   const bool bits16 = (reinterpret_cast<uintptr_t>(bits) & 15) == 0;
   const int grid1 = grid_for(((n + 127) / 128) * 32, CAPT_K1_BLOCK, CAPT_K1_WAVES);
-  if (!mask && L == 1 && bits16)
-    CAPT_CUDA(launch_pdl_f(k_resolve1<1>, grid1, CAPT_K1_BLOCK, sm1, s, a));
-  else if (!mask && L == 4)
-    CAPT_CUDA(launch_pdl_f(k_resolve1<4>, grid1, CAPT_K1_BLOCK, sm1, s, a));
-  else if (!mask && L == 8)
-    CAPT_CUDA(launch_pdl_f(k_resolve1<8>, grid1, CAPT_K1_BLOCK, sm1, s, a));
-  else if (!mask && L == 16)
-    CAPT_CUDA(launch_pdl_f(k_resolve1<16>, grid1, CAPT_K1_BLOCK, sm1, s, a));
+  const auto k1 = [&](auto kernel) {
+    return launch_pdl_f(kernel, grid1, CAPT_K1_BLOCK, sm1, s, a);
+  };
+  if (L == 1 && bits16) CAPT_CUDA(mask ? k1(k_resolve1<1, true>) : k1(k_resolve1<1, false>));
+  else if (L == 4) CAPT_CUDA(mask ? k1(k_resolve1<4, true>) : k1(k_resolve1<4, false>));
+  else if (L == 8) CAPT_CUDA(mask ? k1(k_resolve1<8, true>) : k1(k_resolve1<8, false>));
+  else if (L == 16) CAPT_CUDA(mask ? k1(k_resolve1<16, true>) : k1(k_resolve1<16, false>));
   else if (mask && vec)
     CAPT_CUDA(launch_pdl_f(k_resolve<true, true, 0>, grid, CAPT_K0_BLOCK, sm, s, a));
   else if (mask)
