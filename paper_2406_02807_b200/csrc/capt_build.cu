@@ -139,6 +139,7 @@ struct BuildView {
   const float* T;
   double r_min_sq, r_max_sq;
   float r2_hi;         // fp32 r_max^2 with an upward margin (clear-miss prefilter)
+  float r2_in;         // fp32 r_max^2 with a downward margin (clear members)
   int shortcut;
 };
 
@@ -206,9 +207,12 @@ __global__ void k_bucket_gather(int k, int64_t n0, const float* __restrict__ X, 
   }
 }
 
-// fp32 lower bound of the box distance (clear misses only: a relative
-// margin of 2^-20 on every gap covers the roundings)
-__device__ __forceinline__ bool cell_near32(int k, const float4 q, const Cell& c, float r2_hi) {
+// fp32 lower bound s of the squared box distance: a relative margin of 2^-20
+// on every gap covers the roundings, so s <= d^2 <= s (1 + 2^-18) for the
+// float64 d^2 of dist_cell64.  s > r2_hi: a clear miss; s <= r2_in = fl(r_max^2)
+// (1 - 2^-16): a clear member (d^2 <= s (1 + 2^-18) < r_max^2); only the
+// band between them needs the exact float64 expression.
+__device__ __forceinline__ float cell_lb32(int k, const float4 q, const Cell& c) {
   const float v[3] = {q.x, q.y, q.z};
   float s = 0.f;
   for (int d = 0; d < k; ++d) {
@@ -216,7 +220,7 @@ __device__ __forceinline__ bool cell_near32(int k, const float4 q, const Cell& c
     g *= (1.0f - 0x1p-20f);
     s = fmaf(g, g, s);
   }
-  return s <= r2_hi;
+  return s;
 }
 
 // Candidates of leaf j's set (excluding its representative), in a fixed
@@ -265,9 +269,14 @@ __device__ __forceinline__ void warp_afforded(const BuildView& v, const Buckets&
       float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
       if (k < total) {
         q = __ldg(B.pts + base + (k - excl));
-        if (__float_as_int(q.w) != self && cell_near32(v.k, q, c, v.r2_hi)) {
-          const double pq[3] = {double(q.x), double(q.y), double(q.z)};
-          hit = dist_cell64(v.k, pq, c) <= v.r_max_sq;
+        const float s32 = cell_lb32(v.k, q, c);
+        if (__float_as_int(q.w) != self && s32 <= v.r2_hi) {
+          if (s32 <= v.r2_in) {
+            hit = true;
+          } else {
+            const double pq[3] = {double(q.x), double(q.y), double(q.z)};
+            hit = dist_cell64(v.k, pq, c) <= v.r_max_sq;
+          }
         }
       }
       visit(hit, q);
@@ -522,6 +531,10 @@ extern "C" int capt_tree_build(int device, int k, const float* points, int64_t n
   v.r_min_sq = r_min * r_min;
   v.r_max_sq = r_max * r_max;
   v.r2_hi = float(r_max * r_max) * (1.0f + 0x1p-16f);
+  // (the relative-error argument needs r_max^2 well inside the normal floats)
+  v.r2_in = (r_max * r_max > 0x1p-100 && r_max * r_max < 0x1p100)
+                ? float(r_max * r_max) * (1.0f - 0x1p-16f)
+                : -1.0f;
   v.shortcut = use_rmin_shortcut;
   // the point buckets (edge >= r_max, at most ~2^21 buckets)
   Buckets B;
