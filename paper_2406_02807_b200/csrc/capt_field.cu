@@ -309,8 +309,16 @@ __global__ void __launch_bounds__(256, 1) k_field_cand(FieldGeom g, BucketGrid b
   const int bx0 = max(x0 - R, 0) / g.m, bx1 = min(x0 + kTileX - 1 + R, g.nx - 1) / g.m;
   const int by0 = max(y0 - R, 0) / g.m, by1 = min(y0 + kTileY - 1 + R, g.ny - 1) / g.m;
   const int bz0 = max(z0 - R, 0) / g.m, bz1 = min(z0 + kTileZ - 1 + R, g.nz - 1) / g.m;
-  for (int bz = bz0; bz <= bz1; ++bz)
-    for (int by = by0; by <= by1; ++by) {
+  // bucket rows nearest the tile first (rings of Chebyshev distance around
+  // the tile's own row): the 32-nearest lists are close to final after the
+  // first rings, so the later points mostly fail the one compare instead of
+  // walking the insertion (same lists up to ties)
+  const int cy = (y0 + kTileY / 2) / g.m, cz = (z0 + kTileZ / 2) / g.m;
+  const int ring_max = max(max(cy - by0, by1 - cy), max(cz - bz0, bz1 - cz));
+  for (int ring = 0; ring <= ring_max; ++ring)
+  for (int bz = max(bz0, cz - ring); bz <= min(bz1, cz + ring); ++bz)
+    for (int by = max(by0, cy - ring); by <= min(by1, cy + ring); ++by) {
+      if (max(abs(by - cy), abs(bz - cz)) != ring) continue;
       const int row = (bz * b.nby + by) * b.nbx;
       const uint32_t s0 = bstart[row + bx0], s1 = bstart[row + bx1 + 1];
       for (uint32_t c0 = s0; c0 < s1; c0 += kFieldChunk) {
