@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(256, 1) k_field_cand(FieldGeom g, BucketGrid b
   // walking the insertion (same lists up to ties)
   const int cy = (y0 + kTileY / 2) / g.m, cz = (z0 + kTileZ / 2) / g.m;
   const int ring_max = max(max(cy - by0, by1 - cy), max(cz - bz0, bz1 - cz));
-  for (int ring = 0; ring <= ring_max; ++ring)
+  for (int ring = 0; ring <= ring_max; ++ring) {
   for (int bz = max(bz0, cz - ring); bz <= min(bz1, cz + ring); ++bz)
     for (int by = max(by0, cy - ring); by <= min(by1, cy + ring); ++by) {
       if (max(abs(by - cy), abs(bz - cz)) != ring) continue;
@@ -333,6 +333,20 @@ __global__ void __launch_bounds__(256, 1) k_field_cand(FieldGeom g, BucketGrid b
         }
       }
     }
+    // every point of a later ring lies at least `gap` from every cell centre
+    // of the tile along y or z (its bucket row is ring + 1 rows from the
+    // tile's; two cells of slack for the cell rounding and the half cell):
+    // once no list of the tile reaches that far, the lists are final
+    if (ring < ring_max) {
+      const int gy = min((cy + ring + 1) * g.m - (y0 + kTileY - 1),
+                         y0 - ((cy - ring - 1) * g.m + g.m - 1)) - 2;
+      const int gz = min((cz + ring + 1) * g.m - (z0 + kTileZ - 1),
+                         z0 - ((cz - ring - 1) * g.m + g.m - 1)) - 2;
+      const float gap = float(min(gy, gz)) * g.h;
+      const float t2 = gap > 0.f ? gap * gap * (1.0f - 0x1p-10f) : 0.f;
+      if (!__syncthreads_or(bd[kKP - 1] >= t2)) break;
+    }
+  }
   {
     if (!live) return;
     const int64_t cell = (int64_t(z0 + lz) * g.ny + (y0 + ly)) * g.nx + (x0 + lx);
