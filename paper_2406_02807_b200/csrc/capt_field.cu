@@ -1855,9 +1855,11 @@ int build_field(capt_tree* tree, cudaStream_t s) {
 }
 
 // below this many spheres (auto mode) one fused kernel (k_resolve_small)
-// beats the pipeline's fixed cost
+// beats the pipeline's fixed cost: on the tabletop cloud up to ~768 K spheres,
+// on the dense config-3 cloud (more spheres left to the in-warp paths) not
+// beyond ~256 K (profiles/small_crossover.py); 512 K is the compromise
 #ifndef CAPT_SMALL_BATCH
-#define CAPT_SMALL_BATCH (int64_t(1) << 20)
+#define CAPT_SMALL_BATCH (int64_t(1) << 19)
 #endif
 
 bool field_eligible(const DevTree& t, int64_t n, uint32_t flags) {
