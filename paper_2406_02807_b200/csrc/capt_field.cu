@@ -1225,14 +1225,14 @@ __global__ void __launch_bounds__(256) k_list_knn(FieldArgs a, uint32_t* __restr
       unsigned base = 0;
       if (lane == 0) base = atomicAdd(list2_n, unsigned(__popc(om2)));
       base = __shfl_sync(0xffffffffu, base, 0);
-      if (open && cert) list2[base + __popc(om2 & lt)] = q;
+      if (open && cert) list2[base + __popc(om2 & lt)] = j;  // (its position in list 1)
     }
     const unsigned om3 = __ballot_sync(0xffffffffu, open && !cert);
     if (om3) {
       unsigned base = 0;
       if (lane == 0) base = atomicAdd(list3_n, unsigned(__popc(om3)));
       base = __shfl_sync(0xffffffffu, base, 0);
-      if (open && !cert) list3[base + __popc(om3 & lt)] = q;
+      if (open && !cert) list3[base + __popc(om3 & lt)] = j;
     }
   }
 }
@@ -1268,7 +1268,10 @@ __global__ void __launch_bounds__(32 * kBucketWarps) k_bucket_list(
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int L = a.L;
   for (uint32_t e = blockIdx.x; e < n_list; e += gridDim.x) {
-    const uint32_t q = list2[e];
+    // (list 2 holds positions in list 1: the sphere and its index come from
+    // K0's entry, one coalesced read instead of four gathers of the batch)
+    const uint32_t j = list2[e];
+    const uint32_t q = a.list[j];
     const uint32_t b = L == 1 ? q : q / uint32_t(L);
     if (threadIdx.x == 0) {
       s_hit = 0;
@@ -1280,8 +1283,7 @@ __global__ void __launch_bounds__(32 * kBucketWarps) k_bucket_list(
       __syncthreads();
       continue;
     }
-    const float4 s = make_float4(__ldg(a.c + 3 * size_t(q)), __ldg(a.c + 3 * size_t(q) + 1),
-                                 __ldg(a.c + 3 * size_t(q) + 2), __ldg(a.r + q));
+    const float4 s = a.list_s[j];
     const float r2 = s.w * s.w;
     const float loB = r2 * (1.0f - kTau), hiB = r2 * (1.0f + kTau);
     const float rp = s.w * (1.0f + 0x1p-20f);
@@ -1437,14 +1439,15 @@ __global__ void __launch_bounds__(256) k_tree_list(FieldArgs a, const uint32_t* 
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t e = warp; e < n_list; e += nwarps) {
-    const uint32_t q = list3[e];
+    const uint32_t j = list3[e];  // (a position in list 1)
+    const uint32_t q = a.list[j];
     const uint32_t b = L == 1 ? q : q / uint32_t(L);
     // (a lane group already resolved by another entry: nothing to add)
     // (warp-uniform: lane 0's read decides for the warp)
     if (L > 1 && __shfl_sync(0xffffffffu, (__ldcg(a.bits + (b >> 5)) >> (b & 31)) & 1u, 0)) continue;
-    const float c[3] = {__ldg(a.c + 3 * size_t(q)), __ldg(a.c + 3 * size_t(q) + 1),
-                        __ldg(a.c + 3 * size_t(q) + 2)};
-    const bool verdict = tree_verdict(a, c, __ldg(a.r + q), lane);
+    const float4 sph = a.list_s[j];
+    const float c[3] = {sph.x, sph.y, sph.z};
+    const bool verdict = tree_verdict(a, c, sph.w, lane);
     if (verdict && lane == 0) atomicOr(a.bits + (b >> 5), 1u << (b & 31));
   }
 }
